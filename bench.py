@@ -1,0 +1,353 @@
+"""Headline benchmark: pulsed-update cell-updates/s and noisy-MVM samples/s on
+a 4096 x 4096 SoftBounds (reram_sb) tile, BL = 31, batch 256 (BASELINE.json
+north star).  One step = one mini-batch through the tile: the noisy forward of
+256 samples (default IO: DAC 7 b, ADC 9 b, sigma_out 0.06, abs-max, bound
+management on) followed by the 256 sequential pulsed updates.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun, one process per GPU): one logical (4096 N) x 4096 tile,
+row-sharded, 4096 rows per GPU (weak scaling).  x is replicated, the only
+collective is the all-reduce(max) of the per-sample max|d| the pulse
+translation needs (proj/src/pulsed.cpp:34-51); the forward is row-local.
+
+--impl reference times the reference CPU implementation (oracle/_ref, the
+xbarsim sources compiled here; the C restatement when _ref is absent) on the
+host cores, the same per-sample work per step, one independent tile per core.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_ROWS = 4096  # rows per GPU
+N_COLS = 4096
+BATCH = 256
+LR = 0.01
+METRIC = "pulsed-update cell-updates/s (4096x4096 reram_sb tile, BL=31, batch 256; " \
+         "step = noisy forward + pulsed update)"
+UNIT = "cell-updates/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if s[2 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ============================================================ our arm
+def make_tile(xb, rank, world):
+    dev = xb.device_preset("reram_sb")
+    fwd = xb.default_io()
+    fwd.bound_management = xb.BM_ITERATIVE
+    fwd.bm_max_iter = 10
+    cfg = xb.TileSettings(device=dev, forward_io=fwd, backward_io=xb.default_io(),
+                          mvm_precision=xb.MVM_FP32)
+    cfg.update.bl = 31
+    d_out = N_ROWS * world
+    shard = (rank * N_ROWS, (rank + 1) * N_ROWS) if world > 1 else None
+    return xb.AnalogTile(d_out, N_COLS, cfg, 1234, shard=shard), cfg
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2104_02184_b200 as xb
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    tile, cfg = make_tile(xb, rank, world)
+    tile.set_stream(stream.cuda_stream)
+    g = torch.Generator(device=dev)
+    g.manual_seed(7 + rank)
+    w0 = (torch.rand(N_ROWS, N_COLS, generator=g, device=dev) * 0.2 - 0.1)
+    tile.set_weights(w0.cpu().numpy())
+    nsets = args.steps + args.warmup
+    # distinct synthetic batches per step; x is replicated (same seed on every rank)
+    gx = torch.Generator(device=dev)
+    gx.manual_seed(7)
+    Xs = [torch.rand(BATCH, N_COLS, generator=gx, device=dev) * 2 - 1 for _ in range(nsets)]
+    Ds = [torch.rand(BATCH, N_ROWS, generator=g, device=dev) * 2 - 1 for _ in range(nsets)]
+    Y = torch.empty(BATCH, N_ROWS, device=dev)
+    amax = torch.empty(BATCH, device=dev)
+
+    def step(s):
+        tile.forward_dev(Xs[s], Y)
+        if world > 1:
+            xb.rows_amax_dev(Ds[s], amax, stream.cuda_stream)
+            dist.all_reduce(amax, op=dist.ReduceOp.MAX)
+            tile.update_dev(Xs[s], Ds[s], LR, amax_d=amax)
+        else:
+            tile.update_dev(Xs[s], Ds[s], LR)
+
+    for s in range(args.warmup):
+        step(s)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    tile.set_timing(True)
+    launches0 = xb.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        e0.record(stream)
+        for s in range(args.steps):
+            step(args.warmup + s)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = xb.launch_count() - launches0
+    ms_total = e0.elapsed_time(e1)
+    timing = tile.read_timing()
+    tile.set_timing(False)
+    ph_ms = [timing[k][0] for k in tile.TIMERS]
+    ph_n = [timing[k][1] for k in tile.TIMERS]
+
+    t = torch.tensor([ms_total, ph_ms[0], ph_ms[1], ph_ms[2]], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total, ms_pulse, ms_trains, ms_fwd = t.tolist()
+    ms_step = ms_total / args.steps
+    cells = float(N_ROWS) * world * N_COLS * BATCH
+    value = cells / (ms_step * 1e-3)
+
+    # ---------- e2e through the public host-buffer API (pinned host inputs)
+    e2e = None
+    if rank == 0:
+        Xh = [x.cpu().pin_memory().numpy() for x in Xs[:max(2, min(args.steps, 4))]]
+        Dh = [d.cpu().pin_memory().numpy() for d in Ds[:len(Xh)]]
+        e2e_tile, _ = make_tile(xb, 0, 1) if world == 1 else (tile, None)
+        if world == 1:
+            e2e_tile.set_weights(w0.cpu().numpy())
+        # warm
+        e2e_tile.forward(Xh[0])
+        if world == 1:
+            e2e_tile.update(Xh[0], Dh[0], LR)
+        t0 = time.perf_counter()
+        n_e2e = len(Xh)
+        for k in range(n_e2e):
+            yh = e2e_tile.forward(Xh[k])
+            if world == 1:
+                e2e_tile.update(Xh[k], Dh[k], LR)
+        el = time.perf_counter() - t0
+        _ = float(yh[0, 0])
+        if world == 1:
+            e2e = {"value": N_ROWS * N_COLS * BATCH * n_e2e / el, "unit": UNIT,
+                   "h2d_bytes_per_step": int(BATCH * N_COLS * 4 * 2 + BATCH * N_ROWS * 4),
+                   "d2h_bytes_per_step": int(BATCH * N_ROWS * 4),
+                   "steps": n_e2e, "api": "AnalogTile.forward(X host) + AnalogTile.update(X, D host)"}
+
+    if rank == 0:
+        pk, pk_kind = peaks()
+        clocks = clk.summary()
+        # --- roofline of the dominant kernel (pulse_kernel): integer pipe, SURVEY 8d
+        kbar = float(os.environ.get("XB_KBAR", "1.24"))
+        int_ops = (2.0 + kbar * 15.0) * N_ROWS * N_COLS * BATCH  # per launch (per step)
+        pulse_ms = ms_pulse / max(ph_n[0], 1)
+        sm_mhz = pk.get("sm_max_mhz", 1965.0)
+        int_peak = 148 * 64 * sm_mhz * 1e6  # ALU-pipe lane-ops/s (16 lanes/clk/SMSP)
+        achieved = int_ops / (pulse_ms * 1e-3)
+        mvm_flops = 2.0 * N_ROWS * N_COLS * BATCH
+        mvm_bytes = 4.0 * N_ROWS * N_COLS + 4.0 * BATCH * (N_ROWS + N_COLS)
+        fwd_ms = ms_fwd / max(ph_n[2], 1)
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (x, d ~ U(-1,1), W0 ~ U(-0.1,0.1), seed 7)",
+            "config": {"workload": "NS: 4096x4096 reram_sb (SoftBounds, d2d 0.3, c2c 0.3), "
+                                   "BL 31, batch 256, lr 0.01; forward default IO + BM",
+                       "tile_rows_total": N_ROWS * world, "tile_cols": N_COLS,
+                       "rows_per_gpu": N_ROWS, "batch": BATCH,
+                       "parallelism": f"row-shard{world}",
+                       "l2": "no flush: per-step working set (W + per-cell params 335 MB) > "
+                             "126 MB L2; fresh input batch every step",
+                       "mvm_precision": "fp32 (SIMT)"},
+            "mvm": {"samples_per_s": BATCH * world / (fwd_ms * 1e-3), "ms_per_batch": fwd_ms},
+            "phase_ms_per_step": {"pulse": pulse_ms, "trains": ms_trains / max(ph_n[1], 1),
+                                  "forward": fwd_ms},
+            "roofline": {"bound": "int-pipe", "achieved": achieved / 1e9,
+                         "peak": int_peak / 1e9, "unit": "Gop/s",
+                         "frac": achieved / int_peak, "traffic": None,
+                         "kernel": "pulse_kernel<SOFT_BOUNDS,noise>",
+                         "basis": f"SURVEY 8d: (2 + kbar*15) INT ops per cell-update, kbar={kbar}",
+                         "peak_kind": f"148 SM x 64 ALU lanes x sm_max_mhz ({pk_kind})"},
+            "roofline_mvm": {"bound": "hbm", "achieved": mvm_bytes / (fwd_ms * 1e-3) / 1e9,
+                             "peak": pk["hbm_gbs"], "unit": "GB/s",
+                             "frac": mvm_bytes / (fwd_ms * 1e-3) / 1e9 / pk["hbm_gbs"],
+                             "tflops": mvm_flops / (fwd_ms * 1e-3) / 1e12},
+            "clocks": clocks,
+            "gpu_launches": int(launches),
+            "e2e": e2e,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline_sample()
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ============================================================ reference arm
+def _ref_lib():
+    import oracle
+    impl = "reference" if oracle.available("reference") else "restatement"
+    if not oracle.available(impl):
+        oracle.build(reference=False)
+    return oracle.load(impl), impl
+
+
+def _ref_worker(args):
+    """One process: a 4096^2 reram_sb reference tile, `n_upd` updates and
+    `n_fwd` forwards of independent samples; returns (t_update, t_forward)."""
+    n_upd, n_fwd, seed = args
+    O, impl = _ref_lib()
+    s = O.default("tile")
+    s.device = O.preset("reram_sb")
+    fwd = O.default("io")
+    s.forward_io = fwd
+    t = O.tile(N_ROWS, N_COLS, s, 1234 + seed)
+    rng = np.random.default_rng(7 + seed)
+    t.set_weights(rng.uniform(-0.1, 0.1, (N_ROWS, N_COLS)))
+    xs = rng.uniform(-1, 1, (max(n_upd, n_fwd), N_COLS)).astype(np.float32).astype(np.float64)
+    ds = rng.uniform(-1, 1, (n_upd, N_ROWS)).astype(np.float32).astype(np.float64)
+    t0 = time.perf_counter()
+    for k in range(n_fwd):
+        t.forward(xs[k])
+    t1 = time.perf_counter()
+    for k in range(n_upd):
+        t.update(xs[k], ds[k], LR)
+    t2 = time.perf_counter()
+    return t2 - t1, t1 - t0
+
+
+def cpu_baseline_sample():
+    """Rank 0, N = 1: the reference on one host core, bounded sample."""
+    O, impl = _ref_lib()
+    t_upd, t_fwd = _ref_worker((2, 4, 0))
+    step = t_upd / 2 + t_fwd / 4
+    return {"value": N_ROWS * N_COLS / step, "unit": UNIT, "cores": 1,
+            "kind": "reference" if impl == "reference" else "port",
+            "sample": "4096x4096 reram_sb tile, 2 AnalogTile::update + 4 forward calls "
+                      "(one sample each), 1 thread; value = cells / (update + forward) per sample",
+            "update_s_per_sample": t_upd / 2, "forward_s_per_sample": t_fwd / 4}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    O, impl = _ref_lib()
+    cores = os.cpu_count() or 1
+    per = max(1, args.steps)
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(cores) as pool:
+        res = pool.map(_ref_worker, [(per, per, c) for c in range(cores)])
+    wall = time.perf_counter() - t0
+    # per process: per-sample forward + update time; aggregate over processes
+    step_s = max(r[0] + r[1] for r in res) / per
+    value = cores * N_ROWS * N_COLS / step_s
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": 0, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": "NS: 4096x4096 reram_sb tile, BL 31; per step each core runs one "
+                               "forward + one update sample on its own tile",
+                   "parallelism": f"{cores} independent tile processes"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores,
+                         "kind": "reference" if impl == "reference" else "port",
+                         "sample": f"{per} forward+update samples per core, {cores} cores"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": wall,
+    }
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

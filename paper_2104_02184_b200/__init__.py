@@ -1,0 +1,24 @@
+"""B200-native analog-tile hot path (pulsed update + noisy MVM) behind the
+reference's tile API.
+
+The compute lives in libxbtile.so (CUDA C++, sm_100a) reached through the C
+ABI in include/xbtile.h; this package is the host-side mirror of the
+reference interface.  Importing it without the built library raises: there
+is no CPU fallback.
+"""
+from ._abi import (BM_ITERATIVE, BM_NONE, CONSTANT_STEP, EXP_STEP, LINEAR_STEP, MVM_FP32,
+                   MVM_TF32, MVM_TF32X3, NM_ABS_MAX, NM_NONE, PULSE_DETERMINISTIC,
+                   PULSE_STOCHASTIC, SOFT_BOUNDS, DeviceParams, InferenceModel, IOParams,
+                   TemporalParams, TileConfig, TransferConfig, UpdateParams)
+from .tile import (AnalogTile, Error, InferenceNoiseModel, TileSettings, TransferSettings,
+                   TransferTile, default_device, default_io, device_check, device_preset,
+                   io_off, launch_count, perfect_io, rows_amax_dev)
+
+__all__ = [
+    "AnalogTile", "TransferTile", "TileSettings", "TransferSettings", "InferenceNoiseModel",
+    "DeviceParams", "IOParams", "UpdateParams", "TemporalParams", "TileConfig", "TransferConfig",
+    "InferenceModel", "Error", "device_preset", "default_device", "default_io", "perfect_io",
+    "io_off", "device_check", "launch_count", "rows_amax_dev", "CONSTANT_STEP", "LINEAR_STEP",
+    "SOFT_BOUNDS", "EXP_STEP", "NM_NONE", "NM_ABS_MAX", "BM_NONE", "BM_ITERATIVE",
+    "PULSE_STOCHASTIC", "PULSE_DETERMINISTIC", "MVM_FP32", "MVM_TF32", "MVM_TF32X3",
+]

@@ -1,0 +1,1107 @@
+// xb_abi.cu -- the extern "C" boundary (include/xbtile.h) and the tile handle.
+//
+// Host-side validation mirrors the reference's error behaviour (messages name
+// the field: proj/src/io.cpp:14-30, proj/src/device.cpp:13-24,
+// proj/src/pulsed.cpp:13-32, proj/src/tile.cpp:13-23,65-75,103-111); the
+// compute runs in the kernels of xb_update.cu / xb_mvm.cu / xb_elem.cu.
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "xb_internal.h"
+
+namespace xb {
+
+static thread_local std::string g_err;
+static std::atomic<uint64_t> g_launches{0};
+
+void raise(const std::string &msg) { throw Err{msg}; }
+
+void cuda_check(cudaError_t e, const char *what) {
+  if (e != cudaSuccess) raise(std::string("CUDA error: ") + cudaGetErrorString(e) + " (" + what + ")");
+}
+
+void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+uint64_t fnv1a(const char *s) { // proj/src/rng.cpp:14-21
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (; *s; ++s) {
+    h ^= (unsigned char)*s;
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+
+uint64_t splitmix(uint64_t z) { // proj/src/rng.cpp:24-29
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+PhaseTimer::PhaseTimer(Tile &t_, int ph) : t(t_), phase(ph) {
+  if (!t.timing) return;
+  XB_CUDA(cudaEventCreate(&a));
+  XB_CUDA(cudaEventCreate(&b));
+  XB_CUDA(cudaEventRecord(a, t.stream));
+}
+
+PhaseTimer::~PhaseTimer() {
+  if (!a) return;
+  cudaEventRecord(b, t.stream);
+  t.ev[phase].emplace_back(a, b);
+}
+
+static void clear_timing(Tile &t) {
+  for (auto &v : t.ev) {
+    for (auto &p : v) {
+      cudaEventDestroy(p.first);
+      cudaEventDestroy(p.second);
+    }
+    v.clear();
+  }
+}
+
+void *Scratch::get(size_t n) {
+  if (n > bytes) {
+    if (p) XB_CUDA(cudaFree(p));
+    p = nullptr;
+    bytes = 0;
+    XB_CUDA(cudaMalloc(&p, n));
+    bytes = n;
+  }
+  return p;
+}
+
+void Scratch::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+}
+
+template <class F> static int guard(F &&f) {
+  try {
+    f();
+    return 0;
+  } catch (const Err &e) {
+    g_err = e.msg;
+    return 1;
+  } catch (const std::exception &e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// ------------------------------------------------------------------ validation
+static void io_validate(const xb_io_params &io, const char *ctx) { // io.cpp:14-30
+  const std::string c(ctx);
+  if (io.dac_bits < 0) raise(c + ".dac_bits: must be >= 0");
+  if (io.adc_bits < 0) raise(c + ".adc_bits: must be >= 0");
+  if (!(io.input_bound > 0.0)) raise(c + ".input_bound: must be > 0");
+  if (!(io.output_bound > 0.0)) raise(c + ".output_bound: must be > 0");
+  if (io.sigma_inp < 0.0 || io.sigma_out < 0.0 || io.sigma_w < 0.0)
+    raise(c + ": noise sigmas must be >= 0");
+  if (io.bound_management != XB_BM_NONE && io.bound_management != XB_BM_ITERATIVE)
+    raise(c + ".bound_management: unknown mode");
+  if (io.bound_management == XB_BM_ITERATIVE && (io.bm_max_iter < 0 || io.bm_max_iter > 30))
+    raise(c + ".bm_max_iter: must be in [0, 30]");
+}
+
+static void device_validate(const xb_device_params &p, const char *ctx) { // device.cpp:13-24
+  const std::string c(ctx);
+  if (!(p.dw_min > 0.0)) raise(c + ".dw_min: must be > 0");
+  if (!(p.w_min < 0.0 && 0.0 < p.w_max)) raise(c + ": requires w_min < 0 < w_max");
+  if (p.dw_min_dtod < 0.0 || p.dw_min_std < 0.0 || p.up_down_dtod < 0.0 || p.w_max_dtod < 0.0 ||
+      p.w_min_dtod < 0.0)
+    raise(c + ": dtod/std spreads must be >= 0");
+  if (p.kind < XB_CONSTANT_STEP || p.kind > XB_EXP_STEP) raise(c + ".kind: unknown device model");
+}
+
+static void update_validate(const xb_update_params &u) { // pulsed.cpp:13-17
+  if (u.bl < 1) raise("update.bl: must be >= 1");
+  if (u.bl > 31) raise("update.bl: must be <= 31 (pulse trains are packed one uint32 per line)");
+  if (u.pulse_type != XB_PULSE_STOCHASTIC && u.pulse_type != XB_PULSE_DETERMINISTIC)
+    raise("update.pulse_type: unknown");
+}
+
+static void temporal_validate(const xb_temporal_params &tp) { // tile.cpp:13-23
+  if (tp.decay_rate < 0.0 || tp.diffusion_sigma < 0.0)
+    raise("temporal: decay_rate and diffusion_sigma must be >= 0");
+  if (tp.reset_prob < 0.0 || tp.reset_prob > 1.0) raise("temporal.reset_prob: must be in [0, 1]");
+  if (tp.decay_dtod < 0.0 || tp.diffusion_dtod < 0.0 || tp.reset_dtod < 0.0)
+    raise("temporal: dtod spreads must be >= 0");
+}
+
+static bool temporal_any(const xb_temporal_params &tp) {
+  return tp.decay_rate > 0.0 || tp.diffusion_sigma > 0.0 || tp.reset_prob > 0.0;
+}
+
+static void check_finite(const float *v, size_t n, const char *what) { // tile.cpp:65-75
+  for (size_t k = 0; k < n; ++k)
+    if (!std::isfinite(v[k])) raise(std::string(what) + ": non-finite entry");
+}
+
+static void ensure_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    raise("no CUDA device available: the B200 tile has no CPU fallback");
+  int dev = 0;
+  XB_CUDA(cudaGetDevice(&dev));
+  cudaDeviceProp prop;
+  XB_CUDA(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10)
+    raise(std::string("device ") + prop.name + " is not sm_100 (libxbtile is built for sm_100a only)");
+}
+
+static size_t ld_of(int C) { return (size_t)((C + 31) / 32 * 32); }
+
+} // namespace xb
+
+using namespace xb;
+
+struct xb_tile {
+  Tile t;
+};
+
+struct xb_transfer {
+  xb_transfer_config cfg;
+  xb_tile *fast = nullptr, *slow = nullptr;
+  long counter = 0, events = 0;
+  int next_column = 0;
+  Scratch onehot, readout, tmp;
+};
+
+namespace xb {
+
+static void tile_init_keys(Tile &t, uint64_t seed) {
+  t.seed = seed;
+  t.k_fwd = key_of(derive_seed(seed, "forward")); // tile.cpp:43-46
+  t.k_bwd = key_of(derive_seed(seed, "backward"));
+  const uint64_t upd = derive_seed(seed, "update");
+  t.k_upd = key_of(upd);
+  t.k_c2c = key_of(derive_seed(upd, "c2c"));
+  t.k_temporal = key_of(derive_seed(seed, "temporal"));
+  t.k_realize = key_of(derive_seed(seed, "realize"));      // tile.cpp:27
+  t.k_tinit = key_of(derive_seed(seed, "temporal_init"));  // tile.cpp:59
+}
+
+static void tile_alloc(Tile &t) {
+  const size_t n = (size_t)t.R * t.ld;
+  XB_CUDA(cudaMalloc(&t.W, std::max<size_t>(n, 1) * sizeof(float)));
+  XB_CUDA(cudaMalloc(&t.P, std::max<size_t>(n, 1) * sizeof(float4)));
+  XB_CUDA(cudaMemsetAsync(t.W, 0, n * sizeof(float), t.stream));
+  XB_CUDA(cudaMemsetAsync(t.P, 0, n * sizeof(float4), t.stream));
+}
+
+static void tile_free(Tile &t) {
+  clear_timing(t);
+  cudaFree(t.W);
+  cudaFree(t.P);
+  cudaFree(t.xi);
+  cudaFree(t.w0);
+  cudaFree(t.nu);
+  t.s_words.release();
+  t.s_params.release();
+  t.s_io.release();
+  t.s_y.release();
+  t.s_lr.release();
+  if (t.own_stream && t.stream) cudaStreamDestroy(t.stream);
+}
+
+static void sync(Tile &t) { XB_CUDA(cudaStreamSynchronize(t.stream)); }
+
+static void ensure_xi(Tile &t) {
+  if (t.xi) return;
+  XB_CUDA(cudaMalloc(&t.xi, std::max<size_t>(3 * (size_t)t.R * t.ld, 1) * sizeof(float)));
+  launch_temporal_xi(t);
+}
+
+// ---- host-buffer staging ----
+struct Staged {
+  float *a = nullptr, *b = nullptr;
+};
+
+template <class T> static T *scratch_as(Scratch &s, size_t count) {
+  return (T *)s.get(std::max<size_t>(count, 1) * sizeof(T));
+}
+
+// validate a host lr array the way the reference does per sample: lr == 0 or
+// a zero vector is a no-op; otherwise lr must be > 0 (pulsed.cpp:27-29,122-124)
+static void check_lr_host(const float *X, const float *D, int B, int C, int R, const float *lr,
+                          double def_lr) {
+  for (int b = 0; b < B; ++b) {
+    const double l = lr ? (double)lr[b] : def_lr;
+    if (l == 0.0) continue;
+    bool xz = true, dz = true;
+    for (int j = 0; j < C && xz; ++j) xz = X[(size_t)b * C + j] == 0.f;
+    for (int i = 0; i < R && dz; ++i) dz = D[(size_t)b * R + i] == 0.f;
+    if (xz || dz) continue;
+    if (!(l > 0.0)) raise("translate: learning rate must be > 0");
+  }
+}
+
+static void check_lr_dev(const float *lr, int B, double def_lr) {
+  for (int b = 0; b < B; ++b) {
+    const double l = lr ? (double)lr[b] : def_lr;
+    if (!(l >= 0.0)) raise("translate: learning rate must be > 0");
+  }
+}
+
+// update scratch layout
+struct UpdBufs {
+  float *lr, *xm, *dm;
+  int32_t *bl;
+  uint32_t *xw, *dw;
+  double *px, *pd;
+};
+
+static UpdBufs upd_bufs(Tile &t, int B, bool det) {
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t s_lr = al(B * sizeof(float)), s_bl = al(B * sizeof(int32_t));
+  const size_t s_xw = al((size_t)B * t.C * (det ? sizeof(double) : sizeof(uint32_t)));
+  const size_t s_dw = al((size_t)B * std::max(t.R, 1) * (det ? sizeof(double) : sizeof(uint32_t)));
+  char *p = (char *)t.s_words.get(3 * s_lr + s_bl + s_xw + s_dw);
+  UpdBufs u{};
+  u.lr = (float *)p;
+  u.xm = (float *)(p + s_lr);
+  u.dm = (float *)(p + 2 * s_lr);
+  u.bl = (int32_t *)(p + 3 * s_lr);
+  char *q = p + 3 * s_lr + s_bl;
+  if (det) {
+    u.px = (double *)q;
+    u.pd = (double *)(q + s_xw);
+  } else {
+    u.xw = (uint32_t *)q;
+    u.dw = (uint32_t *)(q + s_xw);
+  }
+  return u;
+}
+
+// a uniform learning rate travels as a kernel argument (no copy, no sync);
+// per-sample rates are uploaded (synchronously: the host array is borrowed)
+static const float *upload_lr(Tile &t, float *dst, const float *lr, int B, float *scalar) {
+  *scalar = lr ? lr[0] : (float)t.learning_rate;
+  bool uniform = true;
+  for (int b = 1; lr && b < B && uniform; ++b) uniform = lr[b] == lr[0];
+  if (uniform) return nullptr;
+  XB_CUDA(cudaMemcpyAsync(dst, lr, B * sizeof(float), cudaMemcpyHostToDevice, t.stream));
+  XB_CUDA(cudaStreamSynchronize(t.stream));
+  return dst;
+}
+
+// the whole pulsed update of B samples from device inputs
+static void update_device(Tile &t, const float *dX, const float *dD, int B, const float *lr,
+                          const float *dAmaxD, bool peek, uint32_t *xw_out, uint32_t *dw_out,
+                          int32_t *bl_out) {
+  const bool det = t.cfg.update.pulse_type == XB_PULSE_DETERMINISTIC && !peek;
+  UpdBufs u = upd_bufs(t, B, det);
+  float lr_s = 0.f;
+  const float *lr_d = upload_lr(t, u.lr, lr, B, &lr_s);
+  {
+    PhaseTimer pt(t, XB_TIMER_TRAINS);
+    launch_rows_amax(dX, B, t.C, t.C, u.xm, t.stream);
+    const float *dm = dAmaxD;
+    if (!dm) {
+      launch_rows_amax(dD, B, t.R, t.R, u.dm, t.stream);
+      dm = u.dm;
+    }
+    launch_trains(t, dX, dD, B, lr_d, lr_s, u.xm, dm, t.seq_upd, u.xw, u.dw, u.bl, u.px, u.pd, det);
+  }
+  if (peek) {
+    XB_CUDA(cudaMemcpyAsync(xw_out, u.xw, sizeof(uint32_t) * (size_t)B * t.C,
+                            cudaMemcpyDeviceToHost, t.stream));
+    XB_CUDA(cudaMemcpyAsync(dw_out, u.dw, sizeof(uint32_t) * (size_t)B * t.R,
+                            cudaMemcpyDeviceToHost, t.stream));
+    XB_CUDA(cudaMemcpyAsync(bl_out, u.bl, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, t.stream));
+    sync(t);
+    return;
+  }
+  {
+    PhaseTimer pt(t, XB_TIMER_PULSE);
+    if (det)
+      launch_pulse_det(t, u.px, u.pd, u.bl, B, t.upd_calls);
+    else
+      launch_pulse(t, u.xw, u.dw, B, t.upd_calls);
+  }
+  t.upd_calls += 1;
+  t.seq_upd += (uint64_t)B;
+}
+
+static void forward_device(Tile &t, const float *dX, int B, float *dY, const xb_io_params &io) {
+  io_validate(io, "forward_io");
+  PhaseTimer pt(t, XB_TIMER_FORWARD);
+  mvm_forward(t, dX, B, dY, make_io(io), t.k_fwd, t.seq_fwd);
+  t.seq_fwd += (uint64_t)B;
+}
+
+static xb_io_params noisy_io(const xb_io_params &io, double extra) { // io.cpp:74-91
+  xb_io_params out = io;
+  if (extra <= 0.0) return out;
+  if (out.is_perfect) {
+    xb_default_io(&out);
+    out.dac_bits = 0;
+    out.adc_bits = 0;
+    out.input_bound = INFINITY;
+    out.output_bound = INFINITY;
+    out.sigma_out = 0.0;
+    out.noise_management = XB_NM_NONE;
+  }
+  out.is_perfect = 0;
+  out.sigma_w = std::hypot(out.sigma_w, extra);
+  return out;
+}
+
+} // namespace xb
+
+extern "C" {
+
+int xb_abi_version(void) { return XB_ABI_VERSION; }
+const char *xb_last_error(void) { return g_err.c_str(); }
+uint64_t xb_launch_count(void) { return g_launches.load(); }
+
+int xb_device_check(void) {
+  return guard([] { ensure_device(); });
+}
+
+void xb_default_device(xb_device_params *p) { // device.hpp:24-39
+  std::memset(p, 0, sizeof *p);
+  p->kind = XB_CONSTANT_STEP;
+  p->dw_min = 0.001;
+  p->w_max = 1.0;
+  p->w_min = -1.0;
+  p->slope = 1.0;
+  p->gamma = 2.0;
+}
+
+void xb_default_io(xb_io_params *p) { // io.hpp:21-33
+  std::memset(p, 0, sizeof *p);
+  p->dac_bits = 7;
+  p->adc_bits = 9;
+  p->input_bound = 1.0;
+  p->output_bound = 12.0;
+  p->sigma_out = 0.06;
+  p->noise_management = XB_NM_ABS_MAX;
+  p->bound_management = XB_BM_NONE;
+  p->bm_max_iter = 10;
+}
+
+void xb_perfect_io(xb_io_params *p) { // io.cpp:32-40
+  xb_default_io(p);
+  p->is_perfect = 1;
+  p->dac_bits = 0;
+  p->adc_bits = 0;
+  p->sigma_out = 0.0;
+  p->noise_management = XB_NM_NONE;
+}
+
+void xb_default_config(xb_tile_config *c) {
+  std::memset(c, 0, sizeof *c);
+  xb_default_device(&c->device);
+  xb_default_io(&c->forward_io);
+  xb_default_io(&c->backward_io);
+  c->update.bl = 31;
+  c->update.bl_management = 0;
+  c->update.pulse_type = XB_PULSE_STOCHASTIC;
+  c->mvm_precision = XB_MVM_FP32;
+}
+
+void xb_default_transfer_config(xb_transfer_config *c) { // compound.hpp:76-91
+  std::memset(c, 0, sizeof *c);
+  xb_default_device(&c->fast_device);
+  xb_default_device(&c->slow_device);
+  xb_default_io(&c->forward_io);
+  xb_default_io(&c->backward_io);
+  c->update.bl = 31;
+  c->mvm_precision = XB_MVM_FP32;
+  c->transfer_every = 1;
+  c->units_in_mbatch = 0;
+  c->transfer_lr = 0.1;
+  c->columns_per_event = 1;
+  c->gamma = 0.0;
+  c->has_transfer_io = 0;
+  xb_default_io(&c->transfer_io);
+}
+
+void xb_default_inference_model(xb_inference_model *m) { // inference.hpp:21-36
+  std::memset(m, 0, sizeof *m);
+  m->prog_noise_scale = 1.0;
+  m->prog_c0 = 0.26;
+  m->prog_c1 = 1.66;
+  m->prog_c2 = 0.33;
+  m->nu_mean = 0.06;
+  m->nu_std = 0.03;
+  m->t0 = 20.0;
+  m->nu_min = 0.0;
+  m->nu_max = 1.0;
+  m->compensation_probes = 10;
+}
+
+int xb_device_preset(const char *name, xb_device_params *p) { // device.cpp:100-132
+  return guard([&] {
+    xb_default_device(p);
+    const std::string n(name ? name : "");
+    if (n == "ideal") {
+      p->kind = XB_CONSTANT_STEP;
+      p->dw_min = 1e-6;
+      return;
+    }
+    if (n == "reram_sb") {
+      p->kind = XB_SOFT_BOUNDS;
+      p->dw_min = 0.002;
+      p->dw_min_dtod = 0.3;
+      p->dw_min_std = 0.3;
+      p->w_max = 0.6;
+      p->w_min = -0.6;
+      p->up_down_dtod = 0.01;
+      return;
+    }
+    if (n == "reram_es") {
+      p->kind = XB_EXP_STEP;
+      p->dw_min = 0.001;
+      p->dw_min_dtod = 0.3;
+      p->dw_min_std = 0.3;
+      p->w_max = 0.6;
+      p->w_min = -0.6;
+      p->up_down = 0.1;
+      p->up_down_dtod = 0.01;
+      p->gamma = 2.0;
+      return;
+    }
+    raise("device preset: unknown name '" + n + "'");
+  });
+}
+
+int xb_tile_create(const xb_tile_config *cfg, int d_out, int d_in, uint64_t seed,
+                   const xb_shard *shard, xb_tile **out) {
+  return guard([&] {
+    *out = nullptr;
+    if (d_out < 1 || d_in < 1) raise("tile: dimensions must be >= 1"); // tile.cpp:47-49
+    io_validate(cfg->forward_io, "forward_io");
+    io_validate(cfg->backward_io, "backward_io");
+    update_validate(cfg->update);
+    temporal_validate(cfg->temporal);
+    device_validate(cfg->device, "device");
+    if (cfg->mvm_precision != XB_MVM_FP32 && cfg->mvm_precision != XB_MVM_TF32 &&
+        cfg->mvm_precision != XB_MVM_TF32X3)
+      raise("mvm_precision: unknown mode");
+    int r0 = 0, r1 = d_out;
+    if (shard) {
+      if (shard->d_out_total != d_out) raise("shard.d_out_total: must equal d_out");
+      r0 = shard->row_begin;
+      r1 = shard->row_end;
+      if (r0 < 0 || r1 > d_out || r0 >= r1) raise("shard: need 0 <= row_begin < row_end <= d_out");
+    }
+    ensure_device();
+    auto h = std::make_unique<xb_tile>();
+    Tile &t = h->t;
+    t.cfg = *cfg;
+    t.R = r1 - r0;
+    t.C = d_in;
+    t.row0 = r0;
+    t.R_total = d_out;
+    t.ld = (int)ld_of(d_in);
+    XB_CUDA(cudaStreamCreateWithFlags(&t.stream, cudaStreamNonBlocking));
+    t.own_stream = true;
+    tile_init_keys(t, seed);
+    try {
+      tile_alloc(t);
+      launch_realize(t); // device.cpp:79-88 (Philox realization; upload for parity)
+      if (temporal_any(cfg->temporal)) ensure_xi(t);
+      sync(t);
+    } catch (...) {
+      tile_free(t);
+      throw;
+    }
+    *out = h.release();
+  });
+}
+
+int xb_tile_destroy(xb_tile *t) {
+  return guard([&] {
+    if (!t) return;
+    cudaStreamSynchronize(t->t.stream);
+    tile_free(t->t);
+    delete t;
+  });
+}
+
+int xb_tile_clone(const xb_tile *src, xb_tile **out) { // tile.hpp:91 (deep copy)
+  return guard([&] {
+    *out = nullptr;
+    const Tile &s = src->t;
+    XB_CUDA(cudaStreamSynchronize(s.stream));
+    auto h = std::make_unique<xb_tile>();
+    Tile &t = h->t;
+    t.cfg = s.cfg;
+    t.R = s.R;
+    t.C = s.C;
+    t.row0 = s.row0;
+    t.R_total = s.R_total;
+    t.ld = s.ld;
+    t.learning_rate = s.learning_rate;
+    t.seq_fwd = s.seq_fwd;
+    t.seq_bwd = s.seq_bwd;
+    t.seq_upd = s.seq_upd;
+    t.upd_calls = s.upd_calls;
+    t.temporal_calls = s.temporal_calls;
+    t.prog_t0 = s.prog_t0;
+    tile_init_keys(t, s.seed);
+    XB_CUDA(cudaStreamCreateWithFlags(&t.stream, cudaStreamNonBlocking));
+    t.own_stream = true;
+    try {
+      tile_alloc(t);
+      const size_t n = (size_t)t.R * t.ld;
+      XB_CUDA(cudaMemcpyAsync(t.W, s.W, n * sizeof(float), cudaMemcpyDeviceToDevice, t.stream));
+      XB_CUDA(cudaMemcpyAsync(t.P, s.P, n * sizeof(float4), cudaMemcpyDeviceToDevice, t.stream));
+      if (s.xi) {
+        XB_CUDA(cudaMalloc(&t.xi, 3 * n * sizeof(float)));
+        XB_CUDA(cudaMemcpyAsync(t.xi, s.xi, 3 * n * sizeof(float), cudaMemcpyDeviceToDevice,
+                                t.stream));
+      }
+      if (s.w0) {
+        XB_CUDA(cudaMalloc(&t.w0, n * sizeof(float)));
+        XB_CUDA(cudaMalloc(&t.nu, n * sizeof(float)));
+        XB_CUDA(cudaMemcpyAsync(t.w0, s.w0, n * sizeof(float), cudaMemcpyDeviceToDevice, t.stream));
+        XB_CUDA(cudaMemcpyAsync(t.nu, s.nu, n * sizeof(float), cudaMemcpyDeviceToDevice, t.stream));
+      }
+      sync(t);
+    } catch (...) {
+      tile_free(t);
+      throw;
+    }
+    *out = h.release();
+  });
+}
+
+int xb_tile_shape(const xb_tile *t, int *d_out_local, int *d_in, int *row_begin,
+                  int *d_out_total) {
+  if (d_out_local) *d_out_local = t->t.R;
+  if (d_in) *d_in = t->t.C;
+  if (row_begin) *row_begin = t->t.row0;
+  if (d_out_total) *d_out_total = t->t.R_total;
+  return 0;
+}
+
+int xb_tile_set_stream(xb_tile *h, void *stream) {
+  return guard([&] {
+    Tile &t = h->t;
+    XB_CUDA(cudaStreamSynchronize(t.stream));
+    if (t.own_stream) XB_CUDA(cudaStreamDestroy(t.stream));
+    if (stream) {
+      t.stream = (cudaStream_t)stream;
+      t.own_stream = false;
+    } else {
+      XB_CUDA(cudaStreamCreateWithFlags(&t.stream, cudaStreamNonBlocking));
+      t.own_stream = true;
+    }
+  });
+}
+
+void *xb_tile_stream(const xb_tile *t) { return (void *)t->t.stream; }
+
+int xb_tile_synchronize(xb_tile *t) {
+  return guard([&] { sync(t->t); });
+}
+
+int xb_tile_set_timing(xb_tile *h, int enable) {
+  return guard([&] {
+    sync(h->t);
+    clear_timing(h->t);
+    h->t.timing = enable != 0;
+  });
+}
+
+int xb_tile_read_timing(xb_tile *h, double *ms, int *counts) {
+  return guard([&] {
+    Tile &t = h->t;
+    sync(t);
+    for (int k = 0; k < XB_TIMER_COUNT; ++k) {
+      double tot = 0.0;
+      for (auto &p : t.ev[k]) {
+        float e = 0.f;
+        XB_CUDA(cudaEventElapsedTime(&e, p.first, p.second));
+        tot += e;
+      }
+      if (ms) ms[k] = tot;
+      if (counts) counts[k] = (int)t.ev[k].size();
+    }
+    clear_timing(t);
+  });
+}
+
+int xb_tile_set_weights(xb_tile *h, const float *w) { // tile.cpp:103-119
+  return guard([&] {
+    Tile &t = h->t;
+    XB_CUDA(cudaMemcpy2DAsync(t.W, t.ld * sizeof(float), w, t.C * sizeof(float),
+                              t.C * sizeof(float), t.R, cudaMemcpyHostToDevice, t.stream));
+    launch_clip(t);
+    sync(t);
+  });
+}
+
+int xb_tile_get_weights(const xb_tile *h, float *w) {
+  return guard([&] {
+    const Tile &t = h->t;
+    XB_CUDA(cudaMemcpy2DAsync(w, t.C * sizeof(float), t.W, t.ld * sizeof(float),
+                              t.C * sizeof(float), t.R, cudaMemcpyDeviceToHost, t.stream));
+    XB_CUDA(cudaStreamSynchronize(t.stream));
+  });
+}
+
+int xb_tile_set_device(xb_tile *h, const float *dw_up, const float *dw_down, const float *w_max,
+                       const float *w_min) {
+  return guard([&] {
+    Tile &t = h->t;
+    const size_t n = (size_t)t.R * t.ld;
+    std::vector<float4> p(n);
+    XB_CUDA(cudaMemcpy(p.data(), t.P, n * sizeof(float4), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < t.R; ++i) {
+      for (int j = 0; j < t.C; ++j) {
+        const size_t s = (size_t)i * t.C + j;
+        float4 &q = p[(size_t)i * t.ld + j];
+        if (dw_up) q.x = dw_up[s];
+        if (dw_down) q.y = dw_down[s];
+        if (w_max) q.z = w_max[s];
+        if (w_min) q.w = w_min[s];
+        if (!(q.w < 0.f && 0.f < q.z)) raise("set_device: requires w_min < 0 < w_max per cell");
+      }
+    }
+    XB_CUDA(cudaMemcpy(t.P, p.data(), n * sizeof(float4), cudaMemcpyHostToDevice));
+    launch_clip(t);
+    sync(t);
+  });
+}
+
+int xb_tile_get_device(const xb_tile *h, float *dw_up, float *dw_down, float *w_max,
+                       float *w_min) {
+  return guard([&] {
+    const Tile &t = h->t;
+    const size_t n = (size_t)t.R * t.ld;
+    std::vector<float4> p(n);
+    XB_CUDA(cudaStreamSynchronize(t.stream));
+    XB_CUDA(cudaMemcpy(p.data(), t.P, n * sizeof(float4), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < t.R; ++i) {
+      for (int j = 0; j < t.C; ++j) {
+        const size_t s = (size_t)i * t.C + j;
+        const float4 q = p[(size_t)i * t.ld + j];
+        if (dw_up) dw_up[s] = q.x;
+        if (dw_down) dw_down[s] = q.y;
+        if (w_max) w_max[s] = q.z;
+        if (w_min) w_min[s] = q.w;
+      }
+    }
+  });
+}
+
+int xb_tile_forward_dev(xb_tile *h, const float *dX, int B, float *dY, const xb_io_params *io,
+                        double extra_sigma) {
+  return guard([&] {
+    Tile &t = h->t;
+    if (B < 0) raise("forward: batch must be >= 0");
+    const xb_io_params base = io ? *io : t.cfg.forward_io;
+    forward_device(t, dX, B, dY, noisy_io(base, extra_sigma));
+  });
+}
+
+static void forward_host(xb_tile *h, const float *X, int B, float *Y, const xb_io_params &io) {
+  Tile &t = h->t;
+  if (B < 0) raise("forward: batch must be >= 0");
+  if (B == 0) return;
+  check_finite(X, (size_t)B * t.C, "forward");
+  float *dX = scratch_as<float>(t.s_y, (size_t)B * (t.C + t.R));
+  float *dY = dX + (size_t)B * t.C;
+  XB_CUDA(cudaMemcpyAsync(dX, X, sizeof(float) * B * t.C, cudaMemcpyHostToDevice, t.stream));
+  forward_device(t, dX, B, dY, io);
+  XB_CUDA(cudaMemcpyAsync(Y, dY, sizeof(float) * B * t.R, cudaMemcpyDeviceToHost, t.stream));
+  sync(t);
+}
+
+int xb_tile_forward(xb_tile *h, const float *X, int B, float *Y) {
+  return guard([&] { forward_host(h, X, B, Y, h->t.cfg.forward_io); });
+}
+
+int xb_tile_forward_io(xb_tile *h, const float *X, int B, float *Y, const xb_io_params *io) {
+  return guard([&] { forward_host(h, X, B, Y, *io); });
+}
+
+int xb_tile_forward_noisy(xb_tile *h, const float *X, int B, float *Y, double extra_sigma) {
+  return guard([&] { forward_host(h, X, B, Y, noisy_io(h->t.cfg.forward_io, extra_sigma)); });
+}
+
+int xb_tile_backward_dev(xb_tile *h, const float *dD, int B, float *dG) {
+  return guard([&] {
+    Tile &t = h->t;
+    if (t.R != t.R_total) raise("backward: row-sharded tile; use xb_tile_backward_partial_dev");
+    io_validate(t.cfg.backward_io, "backward_io");
+    mvm_backward(t, dD, B, dG, make_io(t.cfg.backward_io), t.k_bwd, t.seq_bwd, nullptr, false,
+                 nullptr);
+    t.seq_bwd += (uint64_t)B;
+  });
+}
+
+int xb_tile_backward(xb_tile *h, const float *D, int B, float *G) {
+  return guard([&] {
+    Tile &t = h->t;
+    if (B < 0) raise("backward: batch must be >= 0");
+    if (B == 0) return;
+    if (t.R != t.R_total) raise("backward: row-sharded tile; use xb_tile_backward_partial_dev");
+    check_finite(D, (size_t)B * t.R, "backward");
+    float *dD = scratch_as<float>(t.s_y, (size_t)B * (t.C + t.R));
+    float *dG = dD + (size_t)B * t.R;
+    XB_CUDA(cudaMemcpyAsync(dD, D, sizeof(float) * B * t.R, cudaMemcpyHostToDevice, t.stream));
+    mvm_backward(t, dD, B, dG, make_io(t.cfg.backward_io), t.k_bwd, t.seq_bwd, nullptr, false,
+                 nullptr);
+    t.seq_bwd += (uint64_t)B;
+    XB_CUDA(cudaMemcpyAsync(G, dG, sizeof(float) * B * t.C, cudaMemcpyDeviceToHost, t.stream));
+    sync(t);
+  });
+}
+
+int xb_tile_backward_partial_dev(xb_tile *h, const float *dD, int B, const float *dAmaxD,
+                                 float *dP) {
+  return guard([&] {
+    Tile &t = h->t;
+    mvm_backward(t, dD, B, nullptr, make_io(t.cfg.backward_io), t.k_bwd, t.seq_bwd, dAmaxD, true,
+                 dP);
+  });
+}
+
+int xb_tile_backward_finish_dev(xb_tile *h, const float *dPsum, int B, const float *dAmaxD,
+                                float *dG) {
+  return guard([&] {
+    Tile &t = h->t;
+    mvm_backward_finish(t, dPsum, B, dAmaxD, dG, make_io(t.cfg.backward_io), t.k_bwd, t.seq_bwd);
+    t.seq_bwd += (uint64_t)B;
+  });
+}
+
+int xb_rows_amax_dev(const float *dV, int B, int n, float *dOut, void *stream) {
+  return guard([&] { launch_rows_amax(dV, B, n, n, dOut, (cudaStream_t)stream); });
+}
+
+int xb_tile_update_dev(xb_tile *h, const float *dX, const float *dD, int B, const float *lr,
+                       const float *dAmaxD) {
+  return guard([&] {
+    Tile &t = h->t;
+    if (B < 0) raise("update: batch must be >= 0");
+    if (B == 0) return;
+    check_lr_dev(lr, B, t.learning_rate);
+    update_device(t, dX, dD, B, lr, dAmaxD, false, nullptr, nullptr, nullptr);
+  });
+}
+
+int xb_tile_update(xb_tile *h, const float *X, const float *D, int B, const float *lr) {
+  return guard([&] {
+    Tile &t = h->t;
+    if (B < 0) raise("update: batch must be >= 0");
+    if (B == 0) return;
+    check_finite(X, (size_t)B * t.C, "update(x)");
+    check_finite(D, (size_t)B * t.R, "update(d)");
+    check_lr_host(X, D, B, t.C, t.R, lr, t.learning_rate);
+    float *dX = scratch_as<float>(t.s_y, (size_t)B * (t.C + t.R));
+    float *dD = dX + (size_t)B * t.C;
+    XB_CUDA(cudaMemcpyAsync(dX, X, sizeof(float) * B * t.C, cudaMemcpyHostToDevice, t.stream));
+    XB_CUDA(cudaMemcpyAsync(dD, D, sizeof(float) * B * t.R, cudaMemcpyHostToDevice, t.stream));
+    update_device(t, dX, dD, B, lr, nullptr, false, nullptr, nullptr, nullptr);
+    sync(t);
+  });
+}
+
+int xb_tile_generate_trains(xb_tile *h, const float *X, const float *D, int B, const float *lr,
+                            uint32_t *xw, uint32_t *dw, int32_t *bl) {
+  return guard([&] {
+    Tile &t = h->t;
+    if (B <= 0) raise("generate_trains: batch must be >= 1");
+    check_finite(X, (size_t)B * t.C, "update(x)");
+    check_finite(D, (size_t)B * t.R, "update(d)");
+    check_lr_host(X, D, B, t.C, t.R, lr, t.learning_rate);
+    float *dX = scratch_as<float>(t.s_y, (size_t)B * (t.C + t.R));
+    float *dD = dX + (size_t)B * t.C;
+    XB_CUDA(cudaMemcpyAsync(dX, X, sizeof(float) * B * t.C, cudaMemcpyHostToDevice, t.stream));
+    XB_CUDA(cudaMemcpyAsync(dD, D, sizeof(float) * B * t.R, cudaMemcpyHostToDevice, t.stream));
+    update_device(t, dX, dD, B, lr, nullptr, true, xw, dw, bl);
+  });
+}
+
+int xb_tile_apply_trains(xb_tile *h, const uint32_t *xw, const uint32_t *dw, int B, int flip) {
+  return guard([&] { // tile.cpp:158-169
+    Tile &t = h->t;
+    if (B < 0) raise("apply_trains: batch must be >= 0");
+    if (B == 0) return;
+    const size_t nx = (size_t)B * t.C, nd = (size_t)B * t.R;
+    uint32_t *d = scratch_as<uint32_t>(t.s_params, nx + nd);
+    XB_CUDA(cudaMemcpyAsync(d, xw, nx * 4, cudaMemcpyHostToDevice, t.stream));
+    if (flip) {
+      std::vector<uint32_t> f(dw, dw + nd);
+      for (auto &v : f) v ^= 0x80000000u;
+      XB_CUDA(cudaMemcpyAsync(d + nx, f.data(), nd * 4, cudaMemcpyHostToDevice, t.stream));
+      sync(t);
+    } else {
+      XB_CUDA(cudaMemcpyAsync(d + nx, dw, nd * 4, cudaMemcpyHostToDevice, t.stream));
+    }
+    launch_pulse(t, d, d + nx, B, t.upd_calls);
+    t.upd_calls += 1;
+    t.seq_upd += (uint64_t)B;
+    sync(t);
+  });
+}
+
+int xb_tile_temporal_step(xb_tile *h, const xb_temporal_params *tp) { // tile.cpp:128-156
+  return guard([&] {
+    Tile &t = h->t;
+    temporal_validate(*tp);
+    if (!temporal_any(*tp)) return;
+    ensure_xi(t);
+    launch_temporal(t, *tp, t.temporal_calls++);
+    sync(t);
+  });
+}
+
+int xb_tile_end_minibatch(xb_tile *h) { return xb_tile_temporal_step(h, &h->t.cfg.temporal); }
+
+int xb_tile_set_learning_rate(xb_tile *h, double lr) { // tile.cpp:121-126
+  return guard([&] {
+    if (!(lr > 0.0)) raise("learning_rate: must be > 0");
+    h->t.learning_rate = lr;
+  });
+}
+
+double xb_tile_learning_rate(const xb_tile *h) { return h->t.learning_rate; }
+
+// ------------------------------------------------------------------ inference
+static void model_validate(const xb_inference_model &m) { // inference.cpp:19-32
+  if (!(m.t0 > 0.0)) raise("inference.t0: must be > 0");
+  if (m.prog_noise_scale < 0.0 || m.read_noise_scale < 0.0 || m.nu_mean < 0.0 || m.nu_std < 0.0)
+    raise("inference: noise scales and nu must be >= 0");
+  if (m.nu_min < 0.0 || m.nu_max > 1.0 || m.nu_min > m.nu_max)
+    raise("inference: nu clip must satisfy 0 <= nu_min <= nu_max <= 1");
+  if (m.compensation_probes < 1) raise("inference.compensation_probes: must be >= 1");
+}
+
+int xb_tile_program(xb_tile *h, const float *target, const xb_inference_model *m, uint64_t seed) {
+  return guard([&] { // inference.cpp:34-61
+    Tile &t = h->t;
+    model_validate(*m);
+    const size_t n = (size_t)t.R * t.ld;
+    if (!t.w0) {
+      XB_CUDA(cudaMalloc(&t.w0, std::max<size_t>(n, 1) * sizeof(float)));
+      XB_CUDA(cudaMalloc(&t.nu, std::max<size_t>(n, 1) * sizeof(float)));
+    }
+    float *dT = scratch_as<float>(t.s_y, (size_t)t.R * t.C);
+    XB_CUDA(cudaMemcpyAsync(dT, target, sizeof(float) * (size_t)t.R * t.C, cudaMemcpyHostToDevice,
+                            t.stream));
+    launch_program(t, dT, *m, key_of(seed));
+    t.prog_t0 = m->t0;
+    sync(t);
+  });
+}
+
+int xb_tile_drift_to(xb_tile *h, double time_s) {
+  return guard([&] { // inference.cpp:63-76
+    Tile &t = h->t;
+    if (!t.w0) raise("drift_to: tile has not been programmed");
+    if (time_s < t.prog_t0) raise("drift_to: t < t0");
+    launch_drift(t, time_s / t.prog_t0);
+    sync(t);
+  });
+}
+
+int xb_tile_probe_readout(xb_tile *h, const xb_inference_model *m, double *out) {
+  return guard([&] { // inference.cpp:85-95
+    Tile &t = h->t;
+    model_validate(*m);
+    const int P = m->compensation_probes;
+    std::vector<float> X((size_t)P * t.C, 1.0f), Y((size_t)P * t.R);
+    forward_host(h, X.data(), P, Y.data(), noisy_io(t.cfg.forward_io, m->read_noise_scale));
+    double acc = 0.0;
+    for (int r = 0; r < P; ++r)
+      for (int i = 0; i < t.R; ++i) acc += std::fabs((double)Y[(size_t)r * t.R + i]);
+    *out = acc / P;
+  });
+}
+
+int xb_tile_drift_compensation_factor(xb_tile *h, double baseline, const xb_inference_model *m,
+                                      double *alpha) {
+  double current = 0.0;
+  int rc = xb_tile_probe_readout(h, m, &current);
+  if (rc) return rc;
+  return guard([&] { // inference.cpp:103-110
+    if (current <= 1e-12) raise("drift_compensation_factor: degenerate readout (all-zero tile?)");
+    *alpha = baseline / current;
+  });
+}
+
+// ------------------------------------------------------------------ TransferTile
+static void transfer_validate(const xb_transfer_config &s) { // compound.cpp:176-191
+  if (s.transfer_every < 0) raise("transfer.transfer_every: must be >= 0 (0 disables transfer)");
+  if (!(s.transfer_lr > 0.0)) raise("transfer.transfer_lr: must be > 0");
+  if (s.columns_per_event < 1) raise("transfer.columns_per_event: must be >= 1");
+  if (s.gamma < 0.0) raise("transfer.gamma: must be >= 0");
+}
+
+static xb_tile_config member_config(const xb_transfer_config &s, const xb_device_params &dev) {
+  xb_tile_config c; // compound.cpp:31-42
+  xb_default_config(&c);
+  c.device = dev;
+  c.forward_io = s.forward_io;
+  c.backward_io = s.backward_io;
+  c.update = s.update;
+  c.temporal = s.temporal;
+  c.mvm_precision = s.mvm_precision;
+  return c;
+}
+
+int xb_transfer_create(const xb_transfer_config *cfg, int d_out, int d_in, uint64_t seed,
+                       xb_transfer **out) {
+  *out = nullptr;
+  xb_tile_config fc = member_config(*cfg, cfg->fast_device);
+  xb_tile_config sc = member_config(*cfg, cfg->slow_device);
+  xb_tile *fast = nullptr, *slow = nullptr;
+  int rc = xb_tile_create(&fc, d_out, d_in, derive_seed(seed, "fast"), nullptr, &fast);
+  if (rc) return rc;
+  rc = xb_tile_create(&sc, d_out, d_in, derive_seed(seed, "slow"), nullptr, &slow);
+  if (rc) {
+    xb_tile_destroy(fast);
+    return rc;
+  }
+  rc = guard([&] { transfer_validate(*cfg); });
+  if (rc) {
+    xb_tile_destroy(fast);
+    xb_tile_destroy(slow);
+    return rc;
+  }
+  auto *t = new xb_transfer;
+  t->cfg = *cfg;
+  t->fast = fast;
+  t->slow = slow;
+  *out = t;
+  return 0;
+}
+
+int xb_transfer_destroy(xb_transfer *t) {
+  if (!t) return 0;
+  xb_tile_destroy(t->fast);
+  xb_tile_destroy(t->slow);
+  t->onehot.release();
+  t->readout.release();
+  t->tmp.release();
+  delete t;
+  return 0;
+}
+
+static void mix_outputs(float *y, const float *ya, size_t n, double gamma) {
+  for (size_t k = 0; k < n; ++k) y[k] = (float)((double)y[k] + gamma * (double)ya[k]);
+}
+
+int xb_transfer_forward(xb_transfer *t, const float *X, int B, float *Y) {
+  return guard([&] { // compound.cpp:206-215
+    forward_host(t->slow, X, B, Y, t->slow->t.cfg.forward_io);
+    if (t->cfg.gamma != 0.0) {
+      std::vector<float> ya((size_t)B * t->fast->t.R);
+      forward_host(t->fast, X, B, ya.data(), t->fast->t.cfg.forward_io);
+      mix_outputs(Y, ya.data(), ya.size(), t->cfg.gamma);
+    }
+  });
+}
+
+int xb_transfer_backward(xb_transfer *t, const float *D, int B, float *G) {
+  int rc = xb_tile_backward(t->slow, D, B, G); // compound.cpp:217-226
+  if (rc || t->cfg.gamma == 0.0) return rc;
+  std::vector<float> ga((size_t)B * t->fast->t.C);
+  rc = xb_tile_backward(t->fast, D, B, ga.data());
+  if (rc) return rc;
+  mix_outputs(G, ga.data(), ga.size(), t->cfg.gamma);
+  return 0;
+}
+
+// compound.cpp:257-267: one-hot read of A's column through the forward path,
+// then a pulsed update of C with x = e_j, d = readout.  The readout never
+// leaves the device; a zero readout is a no-op inside the update itself.
+static void transfer_step_impl(xb_transfer *tr) {
+  Tile &a = tr->fast->t;
+  float *oh = scratch_as<float>(tr->onehot, a.C);
+  float *ro = scratch_as<float>(tr->readout, a.R);
+  std::vector<float> e(a.C, 0.f);
+  e[tr->next_column] = 1.0f;
+  XB_CUDA(cudaMemcpyAsync(oh, e.data(), sizeof(float) * a.C, cudaMemcpyHostToDevice, a.stream));
+  const xb_io_params &io = tr->cfg.has_transfer_io ? tr->cfg.transfer_io : tr->cfg.forward_io;
+  forward_device(a, oh, 1, ro, io);
+  sync(a);
+  Tile &c = tr->slow->t;
+  const float lr = (float)tr->cfg.transfer_lr;
+  update_device(c, oh, ro, 1, &lr, nullptr, false, nullptr, nullptr, nullptr);
+  sync(c);
+  tr->next_column = (tr->next_column + 1) % a.C;
+}
+
+static void tick(xb_transfer *t) { // compound.cpp:247-255
+  ++t->counter;
+  if (t->cfg.transfer_every > 0 && t->counter % t->cfg.transfer_every == 0) {
+    ++t->events;
+    for (int n = 0; n < t->cfg.columns_per_event; ++n) transfer_step_impl(t);
+  }
+}
+
+int xb_transfer_step(xb_transfer *t) {
+  return guard([&] { transfer_step_impl(t); });
+}
+
+int xb_transfer_update(xb_transfer *t, const float *X, const float *D, int B, const float *lr) {
+  return guard([&] { // compound.cpp:240-245
+    Tile &a = t->fast->t;
+    if (t->cfg.units_in_mbatch || t->cfg.transfer_every == 0) {
+      if (xb_tile_update(t->fast, X, D, B, lr)) raise(g_err);
+      if (!t->cfg.units_in_mbatch)
+        for (int b = 0; b < B; ++b) tick(t);
+      return;
+    }
+    // ticks interleave with samples: split the batch at every transfer event
+    int b = 0;
+    while (b < B) {
+      const long to_event = t->cfg.transfer_every - (t->counter % t->cfg.transfer_every);
+      const int n = (int)std::min<long>(to_event, B - b);
+      if (xb_tile_update(t->fast, X + (size_t)b * a.C, D + (size_t)b * a.R, n, lr ? lr + b : nullptr))
+        raise(g_err);
+      for (int k = 0; k < n; ++k) tick(t);
+      b += n;
+    }
+  });
+}
+
+int xb_transfer_end_minibatch(xb_transfer *t) {
+  return guard([&] { // compound.cpp:287-293
+    if (t->cfg.units_in_mbatch) tick(t);
+    if (xb_tile_end_minibatch(t->fast)) raise(g_err);
+    if (xb_tile_end_minibatch(t->slow)) raise(g_err);
+  });
+}
+
+int xb_transfer_get_weights(const xb_transfer *t, float *w) {
+  return guard([&] { // compound.cpp:269-280
+    if (xb_tile_get_weights(t->slow, w)) raise(g_err);
+    if (t->cfg.gamma != 0.0) {
+      std::vector<float> a((size_t)t->fast->t.R * t->fast->t.C);
+      if (xb_tile_get_weights(t->fast, a.data())) raise(g_err);
+      mix_outputs(w, a.data(), a.size(), t->cfg.gamma);
+    }
+  });
+}
+
+int xb_transfer_set_weights(xb_transfer *t, const float *w) {
+  return guard([&] { // compound.cpp:282-285
+    if (xb_tile_set_weights(t->slow, w)) raise(g_err);
+    std::vector<float> z((size_t)t->fast->t.R * t->fast->t.C, 0.f);
+    if (xb_tile_set_weights(t->fast, z.data())) raise(g_err);
+  });
+}
+
+long xb_transfer_events(const xb_transfer *t) { return t->events; }
+xb_tile *xb_transfer_fast(xb_transfer *t) { return t->fast; }
+xb_tile *xb_transfer_slow(xb_transfer *t) { return t->slow; }
+
+} // extern "C"

@@ -1,0 +1,205 @@
+// xb_elem.cu -- fused elementwise passes over the tile storage (HBM-bound).
+//
+//   realize_kernel   d2d realization (proj/src/device.cpp:26-46), Philox normals
+//   clip_kernel      set_weights clip to per-cell bounds (proj/src/tile.cpp:113-119)
+//   temporal_kernel  decay / diffusion / reset (proj/src/tile.cpp:128-156)
+//   program_kernel   PCM programming noise + drift exponents (proj/src/inference.cpp:34-61)
+//   drift_kernel     w0 (t/t0)^-nu then clip (proj/src/inference.cpp:63-76)
+//
+// One thread per cell, row-major over [R][ld]; every random draw is addressed
+// by the cell's GLOBAL (row, column) so row shards reproduce the whole tile.
+#include "xb_internal.h"
+
+namespace xb {
+
+namespace {
+
+constexpr int EW_THREADS = 256;
+
+inline dim3 ew_grid(int R, int C) { return dim3((C + 31) / 32, (R + 7) / 8); }
+
+__device__ __forceinline__ bool ew_index(int R, int C, int &i, int &j) {
+  j = blockIdx.x * 32 + (threadIdx.x & 31);
+  i = blockIdx.y * 8 + (threadIdx.x >> 5);
+  return i < R && j < C;
+}
+
+struct DevArgs {
+  double dw_min, dw_min_dtod, up_down, up_down_dtod, w_max, w_min, w_max_dtod, w_min_dtod;
+};
+
+// proj/src/device.cpp:26-46: four Gaussians per cell (xi_dw, xi_ud, xi_max, xi_min)
+__global__ void __launch_bounds__(EW_THREADS) realize_kernel(float4 *__restrict__ P, int ld,
+                                                              int R, int C, int row0,
+                                                              DevArgs a, Key key) {
+  int i, j;
+  if (!ew_index(R, C, i, j)) return;
+  float z0, z1, z2, z3;
+  normal4((uint32_t)j, (uint32_t)(row0 + i), 0u, TAG_REALIZE << 24, key, z0, z1, z2, z3);
+  const double fl = 0.01 * a.dw_min;
+  const double dw = fmax(a.dw_min * (1.0 + a.dw_min_dtod * z0), fl);
+  const double bias = a.up_down + a.up_down_dtod * z1;
+  float4 p;
+  p.x = (float)fmax(dw * (1.0 + bias), fl);
+  p.y = (float)fmax(dw * (1.0 - bias), fl);
+  p.z = (float)fmax(a.w_max * (1.0 + a.w_max_dtod * z2), 0.01 * a.w_max);
+  p.w = (float)fmin(a.w_min * (1.0 + a.w_min_dtod * z3), 0.01 * a.w_min);
+  P[(size_t)i * ld + j] = p;
+}
+
+__global__ void __launch_bounds__(EW_THREADS) clip_kernel(float *__restrict__ W,
+                                                           const float4 *__restrict__ P, int ld,
+                                                           int R, int C) {
+  int i, j;
+  if (!ew_index(R, C, i, j)) return;
+  const size_t k = (size_t)i * ld + j;
+  const float4 p = P[k];
+  W[k] = fminf(fmaxf(W[k], p.w), p.z);
+}
+
+__global__ void __launch_bounds__(EW_THREADS) temporal_xi_kernel(float *__restrict__ xi, int ld,
+                                                                  int R, int C, int row0,
+                                                                  Key key) {
+  int i, j;
+  if (!ew_index(R, C, i, j)) return;
+  float z0, z1, z2, z3;
+  normal4((uint32_t)j, (uint32_t)(row0 + i), 0u, TAG_TEMPORAL_XI << 24, key, z0, z1, z2, z3);
+  const size_t k = (size_t)i * ld + j, plane = (size_t)R * ld;
+  xi[k] = z0;
+  xi[plane + k] = z1;
+  xi[2 * plane + k] = z2;
+}
+
+struct TempArgs {
+  double decay, decay_dtod, diff, diff_dtod, reset, reset_dtod;
+};
+
+// proj/src/tile.cpp:128-156
+__global__ void __launch_bounds__(EW_THREADS) temporal_kernel(float *__restrict__ W,
+                                                               const float4 *__restrict__ P,
+                                                               const float *__restrict__ xi,
+                                                               int ld, int R, int C, int row0,
+                                                               TempArgs a, Key key,
+                                                               uint32_t call) {
+  int i, j;
+  if (!ew_index(R, C, i, j)) return;
+  const size_t k = (size_t)i * ld + j, plane = (size_t)R * ld;
+  double w = W[k];
+  uint32_t c0 = (uint32_t)j, c1 = (uint32_t)(row0 + i), c2 = call, c3 = TAG_TEMPORAL << 24;
+  philox10(c0, c1, c2, c3, key);
+  if (a.decay > 0.0) {
+    const double r = fmin(fmax(a.decay * (1.0 + a.decay_dtod * xi[k]), 0.0), 1.0);
+    w *= 1.0 - r;
+  }
+  if (a.diff > 0.0) {
+    const double s = fmax(a.diff * (1.0 + a.diff_dtod * xi[plane + k]), 0.0);
+    float z0, z1;
+    box_muller(c0, c1, z0, z1);
+    w += s * (double)z0;
+  }
+  if (a.reset > 0.0) {
+    const double p = fmin(fmax(a.reset * (1.0 + a.reset_dtod * xi[2 * plane + k]), 0.0), 1.0);
+    const bool hit = (p >= 1.0) || (p > 0.0 && (double)c2 * 2.3283064365386963e-10 < p);
+    if (hit) w = 0.0;
+  }
+  const float4 pp = P[k];
+  W[k] = fminf(fmaxf((float)w, pp.w), pp.z);
+}
+
+struct ProgArgs {
+  double scale, c0, c1, c2, nu_mean, nu_std, nu_min, nu_max;
+};
+
+// proj/src/inference.cpp:34-61: w = target + sigma(|target|) xi, clip -> w0;
+// nu = clip(nu_mean (1 + nu_std xi'), nu_min, nu_max)
+__global__ void __launch_bounds__(EW_THREADS) program_kernel(
+    float *__restrict__ W, float *__restrict__ w0, float *__restrict__ nu,
+    const float4 *__restrict__ P, const float *__restrict__ target, int ld, int R, int C,
+    int row0, ProgArgs a, Key key) {
+  int i, j;
+  if (!ew_index(R, C, i, j)) return;
+  const size_t k = (size_t)i * ld + j;
+  float z0, z1, z2, z3;
+  normal4((uint32_t)j, (uint32_t)(row0 + i), 0u, TAG_PROGRAM << 24, key, z0, z1, z2, z3);
+  const double t = target[(size_t)i * C + j];
+  const double at = fabs(t);
+  const double sig = a.scale * (a.c0 + a.c1 * at + a.c2 * at * at);
+  const float4 p = P[k];
+  const float w = fminf(fmaxf((float)(t + sig * (double)z0), p.w), p.z);
+  W[k] = w;
+  w0[k] = w;
+  const double v = a.nu_mean * (1.0 + a.nu_std * (double)z1);
+  nu[k] = (float)fmin(fmax(v, a.nu_min), a.nu_max);
+}
+
+// proj/src/inference.cpp:63-76 with log2(t/t0) precomputed in fp64 on the host
+__global__ void __launch_bounds__(EW_THREADS) drift_kernel(float *__restrict__ W,
+                                                            const float *__restrict__ w0,
+                                                            const float *__restrict__ nu,
+                                                            const float4 *__restrict__ P, int ld,
+                                                            int R, int C, double log2_ratio) {
+  int i, j;
+  if (!ew_index(R, C, i, j)) return;
+  const size_t k = (size_t)i * ld + j;
+  const double f = exp2(-(double)nu[k] * log2_ratio);
+  const float4 p = P[k];
+  W[k] = fminf(fmaxf((float)((double)w0[k] * f), p.w), p.z);
+}
+
+} // namespace
+
+void launch_realize(Tile &t) {
+  if (t.R == 0) return;
+  const xb_device_params &d = t.cfg.device;
+  DevArgs a{d.dw_min, d.dw_min_dtod, d.up_down, d.up_down_dtod, d.w_max, d.w_min, d.w_max_dtod,
+            d.w_min_dtod};
+  realize_kernel<<<ew_grid(t.R, t.C), EW_THREADS, 0, t.stream>>>(t.P, t.ld, t.R, t.C, t.row0, a,
+                                                                  t.k_realize);
+  count_launch();
+  XB_CUDA(cudaGetLastError());
+}
+
+void launch_clip(Tile &t) {
+  if (t.R == 0) return;
+  clip_kernel<<<ew_grid(t.R, t.C), EW_THREADS, 0, t.stream>>>(t.W, t.P, t.ld, t.R, t.C);
+  count_launch();
+  XB_CUDA(cudaGetLastError());
+}
+
+void launch_temporal_xi(Tile &t) {
+  if (t.R == 0) return;
+  temporal_xi_kernel<<<ew_grid(t.R, t.C), EW_THREADS, 0, t.stream>>>(t.xi, t.ld, t.R, t.C,
+                                                                      t.row0, t.k_tinit);
+  count_launch();
+  XB_CUDA(cudaGetLastError());
+}
+
+void launch_temporal(Tile &t, const xb_temporal_params &tp, uint32_t call) {
+  if (t.R == 0) return;
+  TempArgs a{tp.decay_rate, tp.decay_dtod, tp.diffusion_sigma, tp.diffusion_dtod, tp.reset_prob,
+             tp.reset_dtod};
+  temporal_kernel<<<ew_grid(t.R, t.C), EW_THREADS, 0, t.stream>>>(
+      t.W, t.P, t.xi, t.ld, t.R, t.C, t.row0, a, t.k_temporal, call);
+  count_launch();
+  XB_CUDA(cudaGetLastError());
+}
+
+void launch_program(Tile &t, const float *target_dev, const xb_inference_model &m, Key key) {
+  if (t.R == 0) return;
+  ProgArgs a{m.prog_noise_scale, m.prog_c0, m.prog_c1, m.prog_c2,
+             m.nu_mean,          m.nu_std,  m.nu_min,  m.nu_max};
+  program_kernel<<<ew_grid(t.R, t.C), EW_THREADS, 0, t.stream>>>(
+      t.W, t.w0, t.nu, t.P, target_dev, t.ld, t.R, t.C, t.row0, a, key);
+  count_launch();
+  XB_CUDA(cudaGetLastError());
+}
+
+void launch_drift(Tile &t, double ratio) {
+  if (t.R == 0) return;
+  drift_kernel<<<ew_grid(t.R, t.C), EW_THREADS, 0, t.stream>>>(t.W, t.w0, t.nu, t.P, t.ld, t.R,
+                                                                t.C, log2(ratio));
+  count_launch();
+  XB_CUDA(cudaGetLastError());
+}
+
+} // namespace xb

@@ -1,0 +1,114 @@
+// xb_internal.h -- host-side internals shared by the libxbtile translation units.
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/xbtile.h"
+#include "xb_common.cuh"
+
+namespace xb {
+
+// error plumbing: every ABI entry catches Err and reports via xb_last_error()
+struct Err {
+  std::string msg;
+};
+[[noreturn]] void raise(const std::string &msg);
+void cuda_check(cudaError_t e, const char *what);
+#define XB_CUDA(call) ::xb::cuda_check((call), #call)
+void count_launch(int n = 1);
+
+// the reference's named-stream derivation (proj/src/rng.cpp:14-41)
+uint64_t fnv1a(const char *s);
+uint64_t splitmix(uint64_t z);
+inline uint64_t derive_seed(uint64_t base, const char *name) { return splitmix(base ^ fnv1a(name)); }
+inline Key key_of(uint64_t seed) { return Key{(uint32_t)seed, (uint32_t)(seed >> 32)}; }
+
+// device scratch that grows on demand
+struct Scratch {
+  void *p = nullptr;
+  size_t bytes = 0;
+  void *get(size_t n);
+  void release();
+};
+
+// per-direction converter constants prepared on the host
+struct IoDev {
+  Quant dac, adc;
+  double sigma_inp, sigma_out, sigma_w;
+  int nm_absmax, perfect, bm, bm_max_iter;
+};
+IoDev make_io(const xb_io_params &io);
+
+struct Tile {
+  xb_tile_config cfg;
+  int R = 0, C = 0;          // local rows, columns
+  int row0 = 0, R_total = 0; // first global row, global rows
+  int ld = 0;                // leading dimension of W / params (floats)
+  uint64_t seed = 0;
+  double learning_rate = 0.01;
+  Key k_fwd{}, k_bwd{}, k_upd{}, k_c2c{}, k_realize{}, k_temporal{}, k_tinit{};
+  uint64_t seq_fwd = 0, seq_bwd = 0, seq_upd = 0; // samples drawn so far per stream
+  uint32_t upd_calls = 0, temporal_calls = 0;
+
+  float *W = nullptr;      // [R][ld] fp32 weights
+  float4 *P = nullptr;     // [R][ld] {dw_up, dw_down, w_max, w_min}
+  float *xi = nullptr;     // [3][R][ld] temporal d2d draws (lazy)
+  float *w0 = nullptr;     // programmed state (lazy)
+  float *nu = nullptr;
+  double prog_t0 = 0.0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+
+  Scratch s_words, s_params, s_io, s_y, s_lr;
+
+  // phase timing (xb_tile_set_timing): pairs of recorded events per phase
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[XB_TIMER_COUNT];
+};
+
+// records an event pair around a phase when timing is on
+struct PhaseTimer {
+  Tile &t;
+  int phase;
+  cudaEvent_t a = nullptr, b = nullptr;
+  PhaseTimer(Tile &t_, int ph);
+  ~PhaseTimer();
+};
+
+// ---- kernel launchers (xb_update.cu) ----
+void launch_rows_amax(const float *V, int B, int n, int ld, float *out, cudaStream_t s);
+// per-sample translate + Bernoulli trains; writes packed words and bl[B]
+void launch_trains(const Tile &t, const float *X, const float *D, int B, const float *lr_dev,
+                   float lr_scalar, const float *xm, const float *dm, uint64_t seq0, uint32_t *xw, uint32_t *dw,
+                   int32_t *bl, double *px, double *pd, bool deterministic);
+// weight-stationary coincidence/pulse kernel over packed words
+void launch_pulse(Tile &t, const uint32_t *xw, const uint32_t *dw, int B, uint32_t call_id);
+// deterministic_implicit: lround(bl*pd*px) pulses per cell per sample
+void launch_pulse_det(Tile &t, const double *px, const double *pd, const int32_t *bl, int B,
+                      uint32_t call_id);
+
+// ---- elementwise (xb_elem.cu) ----
+void launch_realize(Tile &t);
+void launch_clip(Tile &t);
+void launch_temporal(Tile &t, const xb_temporal_params &tp, uint32_t call);
+void launch_temporal_xi(Tile &t);
+void launch_program(Tile &t, const float *target_dev, const xb_inference_model &m, Key key);
+void launch_drift(Tile &t, double ratio);
+
+// ---- noisy MVM (xb_mvm.cu) ----
+// forward: Y[b][i] = alpha_b * ADC(sum_j W[i][j] x~[b][j] + noise), i local rows
+void mvm_forward(Tile &t, const float *dX, int B, float *dY, const IoDev &io, Key key,
+                 uint64_t seq0);
+// backward, unsharded: G[b][j] over all rows
+void mvm_backward(Tile &t, const float *dD, int B, float *dG, const IoDev &io, Key key,
+                  uint64_t seq0, const float *amax_global, bool partial_only, float *dP);
+void mvm_backward_finish(Tile &t, const float *dPsum, int B, const float *amax_global,
+                         float *dG, const IoDev &io, Key key, uint64_t seq0);
+
+} // namespace xb

@@ -1,0 +1,328 @@
+// xb_mvm.cu -- the noisy analog MVM (paper Eq. 1), proj/src/io.cpp:93-149.
+//
+// For B samples at once (the weights are stationary across the batch):
+//   prep_kernel      per sample: alpha = max|x| (abs_max), x~ = Q_dac(x / (alpha 2^m))
+//                    + sigma_inp xi (fp64 converter arithmetic, like the
+//                    reference); ||x~||^2 for the weight-noise fold
+//   mvm_*_kernel     acc[b][o] = sum_k W x~ (fp32 FMA SIMT path; the tcgen05
+//                    path lives in xb_mvm_tc.cu)
+//   epilogue_kernel  v = acc + sigma_w ||x~|| zeta + sigma_out xi;
+//                    y = alpha 2^m Q_adc(v); zero-input samples get Q_adc(sigma_out xi)
+//                    (io.cpp:107-115).  Under bound management a sample whose
+//                    |v| reaches output_bound is re-issued with m + 1.
+//
+// Weight noise: sum_j (w_ij + sigma_w xi_ij) x~_j = sum_j w_ij x~_j + sigma_w
+// ||x~|| zeta_i exactly in distribution (independent xi_ij), so the per-use
+// d_out x d_in Gaussian draws of the reference become one normal per output.
+#include "xb_internal.h"
+
+namespace xb {
+
+namespace {
+
+// --------------------------------------------------------------- prep
+// per-sample state for one MVM call: alpha (0 = zero input), norm of x~,
+// current BM exponent m, active flag for the current pass
+struct SampleState {
+  float alpha;
+  float norm;
+  int m;
+  int active;
+};
+
+__global__ void __launch_bounds__(256) prep_kernel(const float *__restrict__ X, int n, int ldx,
+                                                    float *__restrict__ Xt, int ldt,
+                                                    SampleState *__restrict__ st, IoDev io,
+                                                    Key key, uint64_t seq0, int first_pass,
+                                                    const float *__restrict__ amax_in) {
+  const int b = blockIdx.x;
+  SampleState s = st[b];
+  if (!first_pass && !s.active) return;
+  const float *x = X + (size_t)b * ldx;
+  float *xt = Xt + (size_t)b * ldt;
+  __shared__ float red[32];
+  __shared__ float bc;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+
+  if (first_pass) {
+    float m = 0.f;
+    if (amax_in) {
+      m = amax_in[b];
+    } else {
+      for (int j = threadIdx.x; j < n; j += blockDim.x) m = fmaxf(m, fabsf(x[j]));
+      m = warp_max(m);
+      if (lane == 0) red[warp] = m;
+      __syncthreads();
+      if (warp == 0) {
+        m = lane < nw ? red[lane] : 0.f;
+        m = warp_max(m);
+        if (lane == 0) bc = m;
+      }
+      __syncthreads();
+      m = bc;
+    }
+    s.alpha = (m == 0.f) ? 0.f : (io.nm_absmax ? m : 1.f);
+    s.m = 0;
+    s.active = 1;
+  }
+  const uint64_t seq = seq0 + (uint64_t)b;
+  float nrm = 0.f;
+  if (io.perfect) {
+    for (int j = threadIdx.x; j < n; j += blockDim.x) xt[j] = x[j];
+  } else if (s.alpha == 0.f) {
+    for (int j = threadIdx.x; j < n; j += blockDim.x) xt[j] = 0.f;
+  } else {
+    const double denom = (double)s.alpha * exp2((double)s.m);
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      double v = quantize((double)x[j] / denom, io.dac);
+      if (io.sigma_inp > 0.0) {
+        const float z = normal1((uint32_t)j, (uint32_t)seq, (uint32_t)(seq >> 32) | (s.m << 24),
+                                TAG_IN_NOISE << 24, key);
+        v += io.sigma_inp * (double)z;
+      }
+      const float f = (float)v;
+      xt[j] = f;
+      nrm = fmaf(f, f, nrm);
+    }
+  }
+  nrm = warp_sum(nrm);
+  __syncthreads();
+  if (lane == 0) red[warp] = nrm;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float tot = 0.f;
+    for (int w = 0; w < nw; ++w) tot += red[w];
+    s.norm = sqrtf(tot);
+    st[b] = s;
+  }
+}
+
+// --------------------------------------------------------------- SIMT GEMM
+// acc[b][o] = sum_k A(o, k) x~[b][k];  forward: A(o,k) = W[o][k] (K-major),
+// backward: A(o,k) = W[k][o] (M-major).  Tile 64 (o) x 64 (b) x 16 (k),
+// 256 threads x (4 x 4) outputs.  Samples of inactive BM passes are skipped
+// per tile.
+template <bool TRANS>
+__global__ void __launch_bounds__(256) mvm_simt_kernel(const float *__restrict__ W, int ldw,
+                                                        int M, int K, const float *__restrict__ Xt,
+                                                        int ldt, int B, float *__restrict__ acc,
+                                                        int lda, const SampleState *__restrict__ st,
+                                                        int first_pass) {
+  __shared__ float As[16][64 + 4];
+  __shared__ float Bs[16][64 + 4];
+  __shared__ int any_active;
+  const int m0 = blockIdx.x * 64, b0 = blockIdx.y * 64;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  if (!first_pass) {
+    if (threadIdx.x == 0) any_active = 0;
+    __syncthreads();
+    if (threadIdx.x < 64 && b0 + threadIdx.x < B && st[b0 + threadIdx.x].active) any_active = 1;
+    __syncthreads();
+    if (!any_active) return;
+  }
+  float c[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    // A tile
+    for (int t = threadIdx.x; t < 64 * 16; t += 256) {
+      int kk, mm;
+      float v = 0.f;
+      if (TRANS) {
+        kk = t >> 6;
+        mm = t & 63;
+        if (k0 + kk < K && m0 + mm < M) v = W[(size_t)(k0 + kk) * ldw + m0 + mm];
+      } else {
+        mm = t >> 4;
+        kk = t & 15;
+        if (k0 + kk < K && m0 + mm < M) v = W[(size_t)(m0 + mm) * ldw + k0 + kk];
+      }
+      As[kk][mm] = v;
+    }
+    for (int t = threadIdx.x; t < 64 * 16; t += 256) {
+      const int nn = t >> 4, kk = t & 15;
+      float v = 0.f;
+      if (k0 + kk < K && b0 + nn < B) v = Xt[(size_t)(b0 + nn) * ldt + k0 + kk];
+      Bs[kk][nn] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], bb[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) a[r] = As[kk][ty * 4 + r];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) bb[q] = Bs[kk][tx * 4 + q];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) c[r][q] = fmaf(a[r], bb[q], c[r][q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int b = b0 + tx * 4 + q;
+    if (b >= B) continue;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int o = m0 + ty * 4 + r;
+      if (o < M) acc[(size_t)b * lda + o] = c[r][q];
+    }
+  }
+}
+
+// --------------------------------------------------------------- epilogue
+__global__ void __launch_bounds__(256) epilogue_kernel(const float *__restrict__ acc, int lda,
+                                                        int M, int o0, float *__restrict__ Y,
+                                                        int ldy, SampleState *__restrict__ st,
+                                                        IoDev io, Key key, uint64_t seq0,
+                                                        int *__restrict__ sat, int first_pass) {
+  const int b = blockIdx.y;
+  const SampleState s = st[b];
+  if (!first_pass && !s.active) return;
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= M) return;
+  const float a = acc[(size_t)b * lda + o];
+  if (io.perfect) {
+    Y[(size_t)b * ldy + o] = a;
+    return;
+  }
+  const uint64_t seq = seq0 + (uint64_t)b;
+  float z0 = 0.f, z1 = 0.f, z2, z3;
+  if (io.sigma_w > 0.0 || io.sigma_out > 0.0)
+    normal4((uint32_t)(o0 + o), (uint32_t)seq, (uint32_t)(seq >> 32) | (s.m << 24),
+            TAG_OUT_NOISE << 24, key, z0, z1, z2, z3);
+  double v;
+  double scale;
+  if (s.alpha == 0.f) { // io.cpp:107-115: zero input -> output noise only, no alpha
+    v = io.sigma_out > 0.0 ? io.sigma_out * (double)z1 : 0.0;
+    scale = 1.0;
+  } else {
+    v = (double)a;
+    if (io.sigma_w > 0.0) v += io.sigma_w * (double)s.norm * (double)z0;
+    if (io.sigma_out > 0.0) v += io.sigma_out * (double)z1;
+    scale = (double)s.alpha * exp2((double)s.m);
+    if (io.bm && s.alpha != 0.f && s.m < io.bm_max_iter && fabs(v) >= io.adc.bound) sat[b] = 1;
+  }
+  Y[(size_t)b * ldy + o] = (float)(scale * quantize(v, io.adc));
+}
+
+// BM bookkeeping between passes: samples that saturated get m + 1 and stay active
+__global__ void bm_advance_kernel(SampleState *__restrict__ st, int *__restrict__ sat, int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  SampleState s = st[b];
+  if (s.active && sat[b]) {
+    s.m += 1;
+    s.active = 1;
+  } else {
+    s.active = 0;
+  }
+  sat[b] = 0;
+  st[b] = s;
+}
+
+struct MvmScratch {
+  float *xt;
+  float *acc;
+  SampleState *st;
+  int *sat;
+};
+
+MvmScratch carve(Tile &t, int B, int K, int M) {
+  const size_t xt_b = (size_t)B * K * sizeof(float);
+  const size_t acc_b = (size_t)B * M * sizeof(float);
+  const size_t st_b = (size_t)B * sizeof(SampleState);
+  const size_t sat_b = (size_t)B * sizeof(int);
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  char *p = (char *)t.s_io.get(al(xt_b) + al(acc_b) + al(st_b) + al(sat_b));
+  MvmScratch s;
+  s.xt = (float *)p;
+  s.acc = (float *)(p + al(xt_b));
+  s.st = (SampleState *)(p + al(xt_b) + al(acc_b));
+  s.sat = (int *)(p + al(xt_b) + al(acc_b) + al(st_b));
+  return s;
+}
+
+template <bool TRANS>
+void gemm(Tile &t, const MvmScratch &s, int M, int K, int B, int first) {
+  dim3 grid((M + 63) / 64, (B + 63) / 64);
+  mvm_simt_kernel<TRANS><<<grid, 256, 0, t.stream>>>(t.W, t.ld, M, K, s.xt, K, B, s.acc, M, s.st,
+                                                     first);
+  count_launch();
+  XB_CUDA(cudaGetLastError());
+}
+
+// one full noisy MVM in direction TRANS (forward: false)
+template <bool TRANS>
+void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io, Key key,
+             uint64_t seq0, const float *amax_in, bool skip_epilogue, float *dPartial) {
+  const int K = TRANS ? t.R : t.C; // contraction length
+  const int M = TRANS ? t.C : t.R; // outputs
+  if (B <= 0) return;
+  MvmScratch s = carve(t, B, K, M);
+  if (io.bm) XB_CUDA(cudaMemsetAsync(s.sat, 0, sizeof(int) * B, t.stream));
+  const int passes = io.bm ? 1 + io.bm_max_iter : 1;
+  for (int pass = 0; pass < passes; ++pass) {
+    const int first = pass == 0;
+    prep_kernel<<<B, 256, 0, t.stream>>>(dIn, K, K, s.xt, K, s.st, io, key, seq0, first, amax_in);
+    count_launch();
+    XB_CUDA(cudaGetLastError());
+    gemm<TRANS>(t, s, M, K, B, first);
+    if (skip_epilogue) {
+      XB_CUDA(cudaMemcpyAsync(dPartial, s.acc, sizeof(float) * (size_t)B * M,
+                              cudaMemcpyDeviceToDevice, t.stream));
+      return;
+    }
+    dim3 eg((M + 255) / 256, B);
+    epilogue_kernel<<<eg, 256, 0, t.stream>>>(s.acc, M, M, TRANS ? 0 : t.row0, dOut, M, s.st, io,
+                                              key, seq0, s.sat, first);
+    count_launch();
+    XB_CUDA(cudaGetLastError());
+    if (io.bm && pass + 1 < passes) {
+      bm_advance_kernel<<<(B + 255) / 256, 256, 0, t.stream>>>(s.st, s.sat, B);
+      count_launch();
+      XB_CUDA(cudaGetLastError());
+    }
+  }
+}
+
+} // namespace
+
+IoDev make_io(const xb_io_params &io) {
+  IoDev d;
+  d.dac = make_quant(io.input_bound, io.dac_bits);
+  d.adc = make_quant(io.output_bound, io.adc_bits);
+  d.sigma_inp = io.sigma_inp;
+  d.sigma_out = io.sigma_out;
+  d.sigma_w = io.sigma_w;
+  d.nm_absmax = io.noise_management == XB_NM_ABS_MAX;
+  d.perfect = io.is_perfect;
+  d.bm = io.bound_management == XB_BM_ITERATIVE && !io.is_perfect;
+  d.bm_max_iter = io.bm_max_iter;
+  return d;
+}
+
+void mvm_forward(Tile &t, const float *dX, int B, float *dY, const IoDev &io, Key key,
+                 uint64_t seq0) {
+  run_mvm<false>(t, dX, B, dY, io, key, seq0, nullptr, false, nullptr);
+}
+
+void mvm_backward(Tile &t, const float *dD, int B, float *dG, const IoDev &io, Key key,
+                  uint64_t seq0, const float *amax_global, bool partial_only, float *dP) {
+  run_mvm<true>(t, dD, B, dG, io, key, seq0, amax_global, partial_only, dP);
+}
+
+void mvm_backward_finish(Tile &t, const float *dPsum, int B, const float *amax_global, float *dG,
+                         const IoDev &io, Key key, uint64_t seq0) {
+  (void)t;
+  (void)dPsum;
+  (void)B;
+  (void)amax_global;
+  (void)dG;
+  (void)io;
+  (void)key;
+  (void)seq0;
+  raise("backward_finish: not implemented yet");
+}
+
+} // namespace xb

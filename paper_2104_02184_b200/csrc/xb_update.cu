@@ -1,0 +1,397 @@
+// xb_update.cu -- the stochastic pulsed update (paper Eq. 2) on sm_100a.
+//
+// Reference path (proj/src/pulsed.cpp:116-148):
+//   translate (:25-66) -> generate_trains (:68-88) -> apply_coincidences (:90-114)
+// applied once per sample, samples in order, each coincidence one device pulse
+// (proj/src/device.cpp:48-77).
+//
+// B200 path, one batched call of B samples:
+//   K3 rows_amax_kernel    per-sample max|x|, max|d| (row shards: the max over
+//                          ranks is taken by the caller between K3 and K4)
+//   K4 trains_kernel       translate in fp64 (bit-identical plan to the
+//                          reference on the same inputs) and Philox Bernoulli
+//                          trains packed one uint32 per (sample, line):
+//                          bits 0..bl-1 = slots, bit 31 = sign (1 = negative)
+//   K5 pulse_kernel        weight-stationary: each thread owns one cell, keeps
+//                          w and the cell's realization in registers across
+//                          all B samples, finds coincidences with AND, and
+//                          applies the device law pulse by pulse in sample
+//                          order (the same per-cell sequence as the
+//                          reference's slot-major triple loop, since pulses of
+//                          one sample share a direction).
+//   K6 pulse_det_kernel    deterministic_implicit (pulsed.cpp:128-144).
+#include "xb_internal.h"
+
+namespace xb {
+
+// ============================================================== K3: amax
+__global__ void rows_amax_kernel(const float *__restrict__ V, int n, int ld,
+                                 float *__restrict__ out) {
+  const int b = blockIdx.x;
+  const float *row = V + (size_t)b * ld;
+  float m = 0.f;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) m = fmaxf(m, fabsf(row[j]));
+  m = warp_max(m);
+  __shared__ float red[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) red[warp] = m;
+  __syncthreads();
+  if (warp == 0) {
+    m = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.f;
+    m = warp_max(m);
+    if (lane == 0) out[b] = m;
+  }
+}
+
+void launch_rows_amax(const float *V, int B, int n, int ld, float *out, cudaStream_t s) {
+  if (B <= 0) return;
+  rows_amax_kernel<<<B, 256, 0, s>>>(V, n, ld, out);
+  count_launch();
+  XB_CUDA(cudaGetLastError());
+}
+
+// ============================================================== K4: trains
+// Counter of a train draw: (slot group g, global line, seq lo, seq hi ^ side),
+// key = the tile's "update" stream.  Each Philox call gives 4 slots.
+__device__ __forceinline__ uint32_t train_word(float v, double p, int bl, Key key, uint32_t line,
+                                               uint64_t seq, uint32_t side) {
+  uint32_t bits = 0;
+  if (p > 0.0) {
+    if (p >= 1.0) {
+      bits = (bl >= 32) ? 0x7fffffffu : ((1u << bl) - 1u); // bernoulli(p>=1) == 1, no draw
+    } else {
+      const uint32_t thr = (uint32_t)(p * 4294967296.0); // P(u < thr) = thr / 2^32
+      const uint32_t c2 = (uint32_t)seq, c3 = (uint32_t)(seq >> 32) ^ side;
+      for (int g = 0; g * 4 < bl; ++g) {
+        uint32_t a0 = (uint32_t)g, a1 = line, a2 = c2, a3 = c3;
+        philox10(a0, a1, a2, a3, key);
+        const int t = g * 4;
+        bits |= (uint32_t)(a0 < thr) << t;
+        if (t + 1 < bl) bits |= (uint32_t)(a1 < thr) << (t + 1);
+        if (t + 2 < bl) bits |= (uint32_t)(a2 < thr) << (t + 2);
+        if (t + 3 < bl) bits |= (uint32_t)(a3 < thr) << (t + 3);
+      }
+    }
+  }
+  return bits | (v < 0.f ? 0x80000000u : 0u);
+}
+
+__global__ void __launch_bounds__(256) trains_kernel(
+    const float *__restrict__ X, const float *__restrict__ D, int C, int R,
+    const float *__restrict__ lr, float lr_scalar, const float *__restrict__ xm,
+    const float *__restrict__ dm, double dw_min, int BL, int blm, Key key, uint64_t seq0, int row0, uint32_t *__restrict__ xw,
+    uint32_t *__restrict__ dw, int32_t *__restrict__ bl_out, double *__restrict__ px_out,
+    double *__restrict__ pd_out) {
+  const int b = blockIdx.x;
+  // ---- translate, proj/src/pulsed.cpp:25-66, in fp64 on the fp32 inputs ----
+  const double lrb = (double)(lr ? lr[b] : lr_scalar);
+  const double x_amax = (double)xm[b], d_amax = (double)dm[b];
+  const bool skip = (lrb == 0.0 || x_amax == 0.0 || d_amax == 0.0); // pulsed.cpp:122-124
+  int bl = BL;
+  if (blm && !skip) {
+    const double quanta = lrb * x_amax * d_amax / dw_min;
+    const int c = (int)ceil(BL * (quanta < 1.0 ? quanta : 1.0));
+    bl = c > 1 ? c : 1;
+  }
+  const double amp = skip ? 0.0 : sqrt(lrb / (dw_min * bl));
+  double x_scale = 1.0, d_scale = 1.0;
+  if (x_amax > 0.0 && d_amax > 0.0) {
+    x_scale = sqrt(d_amax / x_amax);
+    d_scale = 1.0 / x_scale;
+  }
+  if (threadIdx.x == 0 && bl_out) bl_out[b] = skip ? 0 : bl;
+  const uint64_t seq = seq0 + (uint64_t)b;
+
+  for (int j = threadIdx.x; j < C; j += blockDim.x) {
+    const float v = X[(size_t)b * C + j];
+    double p = amp * fabs((double)v) * x_scale;
+    p = (p < 1.0) ? p : 1.0;
+    if (skip) p = 0.0;
+    if (px_out) {
+      px_out[(size_t)b * C + j] = (v < 0.f) ? -p : p;
+    } else {
+      xw[(size_t)b * C + j] = train_word(v, p, bl, key, (uint32_t)j, seq, 0u);
+    }
+  }
+  for (int i = threadIdx.x; i < R; i += blockDim.x) {
+    const float v = D[(size_t)b * R + i];
+    double p = amp * fabs((double)v) * d_scale;
+    p = (p < 1.0) ? p : 1.0;
+    if (skip) p = 0.0;
+    if (pd_out) {
+      pd_out[(size_t)b * R + i] = (v < 0.f) ? -p : p;
+    } else {
+      dw[(size_t)b * R + i] = train_word(v, p, bl, key, (uint32_t)(row0 + i), seq, 0x80000000u);
+    }
+  }
+}
+
+void launch_trains(const Tile &t, const float *X, const float *D, int B, const float *lr_dev,
+                   float lr_scalar, const float *xm, const float *dm, uint64_t seq0, uint32_t *xw, uint32_t *dw,
+                   int32_t *bl, double *px, double *pd, bool deterministic) {
+  if (B <= 0) return;
+  trains_kernel<<<B, 256, 0, t.stream>>>(X, D, t.C, t.R, lr_dev, lr_scalar, xm, dm, t.cfg.device.dw_min,
+                                         t.cfg.update.bl, t.cfg.update.bl_management, t.k_upd,
+                                         seq0, t.row0, xw, dw, bl, deterministic ? px : nullptr,
+                                         deterministic ? pd : nullptr);
+  count_launch();
+  XB_CUDA(cudaGetLastError());
+}
+
+// ============================================================== device laws
+// proj/src/device.cpp:48-77, fp32.  Per direction the law needs a signed step
+// scale; the constants that depend on (cell, direction) are selected once per
+// sample ("Dir") and reused for every pulse of that sample.
+struct LawArgs {
+  float slope, gamma, std;
+};
+
+struct Cell {
+  float dwu, dwd, wmax, wmin;
+  float a_up, a_dn; // law-specific per-cell constants
+};
+
+struct Dir {
+  float sgn, dwv, a, off;
+};
+
+template <int LAW>
+__device__ __forceinline__ Cell make_cell(float4 p, const LawArgs &la) {
+  Cell c;
+  c.dwu = p.x;
+  c.dwd = p.y;
+  c.wmax = p.z;
+  c.wmin = p.w;
+  c.a_up = 0.f;
+  c.a_dn = 0.f;
+  if (LAW == XB_SOFT_BOUNDS) {
+    c.a_up = 1.0f / p.z; // step = dw (1 - w / w_max)
+    c.a_dn = 1.0f / p.w; //        dw (1 - w / w_min)
+  } else if (LAW == XB_EXP_STEP) {
+    // step = dw exp(-gamma (w - w_min) / range)  (up)
+    //        dw exp(-gamma (w_max - w) / range)  (down); kept in log2 units
+    c.a_up = la.gamma / (p.z - p.w) * 1.4426950408889634f;
+  }
+  return c;
+}
+
+template <int LAW>
+__device__ __forceinline__ Dir make_dir(const Cell &c, bool up, const LawArgs &la) {
+  Dir d;
+  d.sgn = up ? 1.f : -1.f;
+  d.dwv = up ? c.dwu : c.dwd;
+  d.a = 0.f;
+  d.off = 0.f;
+  if (LAW == XB_SOFT_BOUNDS) {
+    d.a = up ? c.a_up : c.a_dn;
+  } else if (LAW == XB_LINEAR_STEP) {
+    d.a = up ? -la.slope : la.slope; // up: 1 - slope w ; down: 1 + slope w
+  } else if (LAW == XB_EXP_STEP) {
+    d.a = c.a_up;
+    d.off = up ? -c.wmin : c.wmax; // up: (w - w_min) ; down: (w_max - w)
+  }
+  return d;
+}
+
+template <int LAW, bool NOISE>
+__device__ __forceinline__ float pulse(float w, const Cell &c, const Dir &d, float std, float z) {
+  float step;
+  if (LAW == XB_CONSTANT_STEP) {
+    step = d.dwv;
+  } else if (LAW == XB_SOFT_BOUNDS) {
+    step = d.dwv * fmaf(-w, d.a, 1.0f);
+  } else if (LAW == XB_LINEAR_STEP) {
+    step = d.dwv * fmaf(d.a, w, 1.0f);
+  } else {
+    step = d.dwv * exp2f(-d.a * fmaf(d.sgn, w, d.off));
+  }
+  if (NOISE) step *= fmaf(std, z, 1.0f); // device.cpp:72-74
+  w = fmaf(d.sgn, step, w);
+  return fminf(fmaxf(w, c.wmin), c.wmax); // device.cpp:75-76
+}
+
+// ============================================================== K5: pulse
+// CTA tile: PR rows (one per warp) x 32 columns (one per lane).  The words of
+// a chunk of SB samples are staged in shared memory:
+//   xs[b][32]       x words of the CTA's columns (lane-contiguous, conflict-free)
+//   ds[PR][SB + 1]  d words of the CTA's rows
+// Each lane walks its cell's samples in order and fires its pulses; all
+// active lanes fire exactly one pulse per loop trip, so the c2c normal cache
+// (4 per Philox call) is refilled warp-uniformly.  Normal #n of cell (i, j)
+// in launch `call` is Philox(k_c2c, (n/4, j, i, call))[n%4] -> Box-Muller:
+// independent of geometry, warp composition and sharding.
+constexpr int PULSE_PR = 16;
+constexpr int PULSE_SB = 256;
+
+template <int LAW, bool NOISE>
+__global__ void __launch_bounds__(PULSE_PR * 32) pulse_kernel(
+    float *__restrict__ W, const float4 *__restrict__ P, int ld, int R, int C,
+    const uint32_t *__restrict__ xw, const uint32_t *__restrict__ dw, int B, int row0,
+    LawArgs la, Key key, uint32_t call) {
+  extern __shared__ uint32_t smem[];
+  uint32_t *xs = smem;                    // [SB][32]
+  uint32_t *ds = smem + PULSE_SB * 32;    // [PR][SB + 1]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int col0 = blockIdx.x * 32, rowb = blockIdx.y * PULSE_PR;
+  const int j = col0 + lane, i = rowb + warp;
+  const bool valid = (i < R) && (j < C);
+  const size_t idx = (size_t)i * ld + j;
+
+  float w = 0.f;
+  Cell cell{};
+  if (valid) {
+    w = W[idx];
+    cell = make_cell<LAW>(P[idx], la);
+  }
+  const uint32_t jg = (uint32_t)j, ig = (uint32_t)(row0 + i);
+  uint32_t g = 0; // normal group index (4 normals per group), per lane
+
+  for (int b0 = 0; b0 < B; b0 += PULSE_SB) {
+    const int nb = min(PULSE_SB, B - b0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < nb * 32; t += blockDim.x) {
+      const int bb = t >> 5, l = t & 31;
+      xs[t] = (col0 + l < C) ? xw[(size_t)(b0 + bb) * C + col0 + l] : 0u;
+    }
+    for (int t = threadIdx.x; t < nb * PULSE_PR; t += blockDim.x) {
+      const int bb = t / PULSE_PR, r = t % PULSE_PR;
+      ds[r * (PULSE_SB + 1) + bb] = (rowb + r < R) ? dw[(size_t)(b0 + bb) * R + rowb + r] : 0u;
+    }
+    __syncthreads();
+    if (!valid) continue;
+
+    const uint32_t *dsr = ds + warp * (PULSE_SB + 1);
+    int b = -1;
+    uint32_t c = 0;
+    Dir dir{};
+    bool done = false;
+    // fire one pulse of this lane's cell; returns false when the chunk is exhausted
+    auto step = [&](float z) -> bool {
+      while (c == 0u) {
+        if (++b >= nb) return false;
+        const uint32_t xv = xs[b * 32 + lane], dv = dsr[b];
+        c = xv & dv & 0x7fffffffu;
+        if (c) dir = make_dir<LAW>(cell, ((xv ^ dv) >> 31) == 0u, la);
+      }
+      w = pulse<LAW, NOISE>(w, cell, dir, la.std, z);
+      c &= c - 1u;
+      return true;
+    };
+    while (!done) {
+      float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
+      if (NOISE) normal4(g, jg, ig, call, key, z0, z1, z2, z3);
+      ++g;
+      done = !step(z0) || !step(z1) || !step(z2) || !step(z3);
+    }
+  }
+  if (valid) W[idx] = w;
+}
+
+template <int LAW, bool NOISE>
+static void pulse_dispatch(Tile &t, const uint32_t *xw, const uint32_t *dw, int B, LawArgs la,
+                           uint32_t call) {
+  const size_t smem = (size_t)(PULSE_SB * 32 + PULSE_PR * (PULSE_SB + 1)) * sizeof(uint32_t);
+  static bool configured = false;
+  if (!configured) {
+    XB_CUDA(cudaFuncSetAttribute(pulse_kernel<LAW, NOISE>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  dim3 grid((t.C + 31) / 32, (t.R + PULSE_PR - 1) / PULSE_PR);
+  pulse_kernel<LAW, NOISE><<<grid, PULSE_PR * 32, smem, t.stream>>>(
+      t.W, t.P, t.ld, t.R, t.C, xw, dw, B, t.row0, la, t.k_c2c, call);
+  count_launch();
+  XB_CUDA(cudaGetLastError());
+}
+
+void launch_pulse(Tile &t, const uint32_t *xw, const uint32_t *dw, int B, uint32_t call_id) {
+  if (B <= 0 || t.R == 0) return;
+  const LawArgs la{(float)t.cfg.device.slope, (float)t.cfg.device.gamma,
+                   (float)t.cfg.device.dw_min_std};
+  const bool noise = t.cfg.device.dw_min_std > 0.0;
+  switch (t.cfg.device.kind) {
+  case XB_CONSTANT_STEP:
+    noise ? pulse_dispatch<XB_CONSTANT_STEP, true>(t, xw, dw, B, la, call_id)
+          : pulse_dispatch<XB_CONSTANT_STEP, false>(t, xw, dw, B, la, call_id);
+    break;
+  case XB_LINEAR_STEP:
+    noise ? pulse_dispatch<XB_LINEAR_STEP, true>(t, xw, dw, B, la, call_id)
+          : pulse_dispatch<XB_LINEAR_STEP, false>(t, xw, dw, B, la, call_id);
+    break;
+  case XB_SOFT_BOUNDS:
+    noise ? pulse_dispatch<XB_SOFT_BOUNDS, true>(t, xw, dw, B, la, call_id)
+          : pulse_dispatch<XB_SOFT_BOUNDS, false>(t, xw, dw, B, la, call_id);
+    break;
+  case XB_EXP_STEP:
+    noise ? pulse_dispatch<XB_EXP_STEP, true>(t, xw, dw, B, la, call_id)
+          : pulse_dispatch<XB_EXP_STEP, false>(t, xw, dw, B, la, call_id);
+    break;
+  default:
+    raise("device.kind: unknown device model");
+  }
+}
+
+// ============================================================== K6: deterministic
+// proj/src/pulsed.cpp:128-144: count = lround(bl * p_d * p_x) in fp64, pulses
+// in one direction per (cell, sample).  Signed probabilities carry the line
+// signs (p = 0 <=> sign 0 or a no-op sample).
+template <int LAW, bool NOISE>
+__global__ void __launch_bounds__(256) pulse_det_kernel(
+    float *__restrict__ W, const float4 *__restrict__ P, int ld, int R, int C,
+    const double *__restrict__ px, const double *__restrict__ pd, const int32_t *__restrict__ bl,
+    int B, int row0, LawArgs la, Key key, uint32_t call) {
+  const int j = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int i = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (i >= R || j >= C) return;
+  const size_t idx = (size_t)i * ld + j;
+  float w = W[idx];
+  const Cell cell = make_cell<LAW>(P[idx], la);
+  uint32_t n = 0;
+  float z[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int b = 0; b < B; ++b) {
+    const double a = pd[(size_t)b * R + i], x = px[(size_t)b * C + j];
+    if (a == 0.0 || x == 0.0) continue;
+    const long long count = llround((double)bl[b] * fabs(a) * fabs(x));
+    const Dir dir = make_dir<LAW>(cell, (a > 0.0) == (x > 0.0), la);
+    for (long long k = 0; k < count; ++k, ++n) {
+      if (NOISE && (n & 3u) == 0u) normal4(n >> 2, (uint32_t)j, (uint32_t)(row0 + i), call, key,
+                                           z[0], z[1], z[2], z[3]);
+      w = pulse<LAW, NOISE>(w, cell, dir, la.std, z[n & 3u]);
+    }
+  }
+  W[idx] = w;
+}
+
+template <int LAW, bool NOISE>
+static void det_dispatch(Tile &t, const double *px, const double *pd, const int32_t *bl, int B,
+                         LawArgs la, uint32_t call) {
+  dim3 grid((t.C + 31) / 32, (t.R + 7) / 8);
+  pulse_det_kernel<LAW, NOISE><<<grid, 256, 0, t.stream>>>(t.W, t.P, t.ld, t.R, t.C, px, pd, bl,
+                                                           B, t.row0, la, t.k_c2c, call);
+  count_launch();
+  XB_CUDA(cudaGetLastError());
+}
+
+void launch_pulse_det(Tile &t, const double *px, const double *pd, const int32_t *bl, int B,
+                      uint32_t call_id) {
+  if (B <= 0 || t.R == 0) return;
+  const LawArgs la{(float)t.cfg.device.slope, (float)t.cfg.device.gamma,
+                   (float)t.cfg.device.dw_min_std};
+  const bool noise = t.cfg.device.dw_min_std > 0.0;
+#define XB_DET(K)                                                                          \
+  case K:                                                                                  \
+    noise ? det_dispatch<K, true>(t, px, pd, bl, B, la, call_id)                           \
+          : det_dispatch<K, false>(t, px, pd, bl, B, la, call_id);                         \
+    break;
+  switch (t.cfg.device.kind) {
+    XB_DET(XB_CONSTANT_STEP)
+    XB_DET(XB_LINEAR_STEP)
+    XB_DET(XB_SOFT_BOUNDS)
+    XB_DET(XB_EXP_STEP)
+  default:
+    raise("device.kind: unknown device model");
+  }
+#undef XB_DET
+}
+
+} // namespace xb

@@ -1,0 +1,190 @@
+"""Noisy-MVM parity: the CUDA forward/backward (through the C ABI) vs the oracle.
+
+Noise off: outputs within 1e-5 * max(1, |y|) of the fp64 oracle (the
+reference's own tolerance form, proj/tests/test_tile.cpp:263), converters on:
+identical grid values except <= 1 ADC LSB on a small fraction (an fp32
+accumulator can sit on the other side of an ADC threshold).  Noise on:
+moments within stated confidence bounds.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2104_02184_b200 as xb
+from gpu_helpers import close, oracle_io, twin
+
+pytestmark = pytest.mark.gpu
+
+PRECISIONS = [xb.MVM_FP32]
+
+
+def cfg_io(fwd=None, bwd=None, prec=xb.MVM_FP32, bound=4.0):
+    dev = xb.default_device()
+    dev.w_max, dev.w_min = bound, -bound
+    return xb.TileSettings(device=dev, forward_io=fwd if fwd is not None else xb.io_off(),
+                           backward_io=bwd if bwd is not None else xb.io_off(),
+                           mvm_precision=prec)
+
+
+@pytest.mark.parametrize("prec", PRECISIONS)
+@pytest.mark.parametrize("shape", [(16, 16), (256, 256), (300, 130)])
+@pytest.mark.parametrize("perfect", [True, False])
+def test_noise_off_matches_exact_matvec(prec, shape, perfect):
+    """proj/tests/test_tile.cpp:225-266 (ideal limit) and io_off paths."""
+    io = xb.perfect_io() if perfect else xb.io_off()
+    g, o = twin(cfg_io(io, io, prec), *shape, w_scale=0.5)
+    X = np.random.default_rng(61).uniform(-1, 1, (8, shape[1])).astype(np.float32)
+    D = np.random.default_rng(62).uniform(-1, 1, (8, shape[0])).astype(np.float32)
+    Y = g.forward(X)
+    G = g.backward(D)
+    W = o.get_weights()
+    assert close(Y, X.astype(np.float64) @ W.T, 1e-5, 1.0).all()
+    assert close(G, D.astype(np.float64) @ W, 1e-5, 1.0).all()
+    for b in range(8):
+        assert close(Y[b], o.forward(X[b]), 1e-5, 1.0).all()
+        assert close(G[b], o.backward(D[b]), 1e-5, 1.0).all()
+
+
+@pytest.mark.parametrize("prec", PRECISIONS)
+def test_converters_match_oracle_grid(prec):
+    """Default DAC 7 b / ADC 9 b / abs-max, sigma_out = 0: same grid values;
+    at most 1 LSB apart on <= 0.5 % of outputs."""
+    io = xb.default_io()
+    io.sigma_out = 0.0
+    g, o = twin(cfg_io(io, io, prec, bound=1.0), 128, 512, w_scale=0.1)
+    X = np.random.default_rng(7).uniform(-1, 1, (32, 512)).astype(np.float32)
+    Y = g.forward(X)
+    ref = np.stack([o.forward(X[b]) for b in range(32)])
+    alpha = np.abs(X).max(axis=1, keepdims=True)
+    lsb = 2 * 12.0 / 512 * alpha
+    diff = np.abs(Y - ref)
+    assert np.all(diff <= lsb * 1.001 + 1e-6)
+    assert np.mean(diff > 1e-6 * np.maximum(1, np.abs(ref))) <= 0.005
+    D = np.random.default_rng(8).uniform(-1, 1, (32, 128)).astype(np.float32)
+    G = g.backward(D)
+    refg = np.stack([o.backward(D[b]) for b in range(32)])
+    lsbg = 2 * 12.0 / 512 * np.abs(D).max(axis=1, keepdims=True)
+    assert np.all(np.abs(G - refg) <= lsbg * 1.001 + 1e-6)
+
+
+def test_outputs_on_adc_grid():
+    """proj/tests/test_tile.cpp:406-421."""
+    io = xb.io_off()
+    io.adc_bits, io.output_bound = 4, 2.0
+    g = xb.AnalogTile(3, 3, cfg_io(io), 19)
+    g.set_weights(np.random.default_rng(95).uniform(-0.4, 0.4, (3, 3)))
+    y = g.forward(np.random.default_rng(96).uniform(-0.9, 0.9, 3))
+    step = 2 * 2.0 / 16
+    k = (y + 2.0 - 0.5 * step) / step
+    assert np.all(np.abs(k - np.round(k)) < 1e-5)
+
+
+def test_zero_input():
+    """proj/tests/test_tile.cpp:66-82 and io.cpp:107-115."""
+    io = xb.default_io()
+    io.sigma_inp, io.sigma_w, io.sigma_out = 0.1, 0.2, 0.0
+    g = xb.AnalogTile(3, 4, cfg_io(io), 1)
+    g.set_weights(np.random.default_rng(9).uniform(-0.5, 0.5, (3, 4)))
+    assert np.all(g.forward(np.zeros(4)) == 0.0)
+    io.sigma_out = 0.1
+    g2 = xb.AnalogTile(200, 4, cfg_io(io), 1)
+    y = g2.forward(np.zeros((50, 4)))
+    step = 2 * 12.0 / 512
+    assert abs(y.std() - 0.1) < 0.01  # noise-only path, then the ADC
+    k = (y + 12.0 - 0.5 * step) / step
+    assert np.all(np.abs(k - np.round(k)) < 1e-3)
+
+
+def test_forward_unbiased_and_noise_variance():
+    """test_tile.cpp:145-174: all noise on, converters off: mean = W x, and
+    var = sigma_out^2 + sigma_w^2 ||x~||^2 + sigma_inp^2 ||w_i||^2."""
+    io = xb.io_off()
+    io.input_bound = io.output_bound = 1e6
+    io.sigma_inp, io.sigma_out, io.sigma_w = 0.03, 0.05, 0.02
+    io.noise_management = xb.NM_ABS_MAX
+    g = xb.AnalogTile(3, 4, cfg_io(io), 6)
+    W = np.random.default_rng(21).uniform(-0.4, 0.4, (3, 4)).astype(np.float32)
+    g.set_weights(W)
+    x = np.random.default_rng(22).uniform(-0.8, 0.8, 4).astype(np.float32)
+    n = 60000
+    Y = g.forward(np.tile(x, (n, 1))).astype(np.float64)
+    exact = W.astype(np.float64) @ x
+    se = Y.std(axis=0) / np.sqrt(n)
+    assert np.all(np.abs(Y.mean(axis=0) - exact) < 4 * se)
+    alpha = np.abs(x).max()
+    xn = x / alpha
+    var = alpha ** 2 * (0.05 ** 2 + 0.02 ** 2 * (xn @ xn + 4 * 0.03 ** 2)
+                        + 0.03 ** 2 * (W.astype(np.float64) ** 2).sum(axis=1))
+    ratio = Y.var(axis=0) / var
+    assert np.all(np.abs(ratio - 1) < 0.05), ratio
+
+
+def test_abs_max_scale_invariance():
+    """proj/tests/test_tile.cpp:176-198: same seed -> same noise draws."""
+    io = xb.io_off()
+    io.sigma_inp, io.sigma_out, io.noise_management = 0.02, 0.05, xb.NM_ABS_MAX
+    a = xb.AnalogTile(3, 4, cfg_io(io), 77)
+    b = xb.AnalogTile(3, 4, cfg_io(io), 77)
+    W = np.random.default_rng(31).uniform(-0.4, 0.4, (3, 4))
+    a.set_weights(W)
+    b.set_weights(W)
+    x = np.random.default_rng(32).uniform(-0.6, 0.6, 4).astype(np.float32)
+    c = np.float32(4.0)  # power of two keeps x / alpha bit-identical in fp32
+    np.testing.assert_allclose(b.forward(c * x), c * a.forward(x), rtol=1e-6)
+
+
+def test_determinism_same_seed():
+    """proj/tests/test_tile.cpp:200-223."""
+    dev = xb.default_device()
+    dev.dw_min_dtod, dev.dw_min_std = 0.3, 0.3
+    s = xb.TileSettings(device=dev)
+    a = xb.AnalogTile(4, 4, s, 123)
+    b = xb.AnalogTile(4, 4, s, 123)
+    W = np.random.default_rng(41).uniform(-0.3, 0.3, (4, 4))
+    a.set_weights(W)
+    b.set_weights(W)
+    x = np.random.default_rng(42).uniform(-0.9, 0.9, 4)
+    d = np.random.default_rng(43).uniform(-0.5, 0.5, 4)
+    for _ in range(5):
+        np.testing.assert_array_equal(a.forward(x), b.forward(x))
+        a.update(x, d, 0.01)
+        b.update(x, d, 0.01)
+    np.testing.assert_array_equal(a.get_weights(), b.get_weights())
+
+
+def test_read_noise_never_lands_in_the_array():
+    """proj/tests/test_tile.cpp:268-291."""
+    io = xb.default_io()
+    io.sigma_out, io.sigma_w = 0.1, 0.1
+    g = xb.AnalogTile(2, 2, cfg_io(io, bound=1.0), 11)
+    g.set_weights([[0.5, -0.25], [10.0, 0.0]])
+    got = g.get_weights()
+    np.testing.assert_array_equal(got, np.array([[0.5, -0.25], [1.0, 0.0]], np.float32))
+    g.forward(np.tile([0.3, 0.4], (50, 1)))
+    np.testing.assert_array_equal(g.get_weights(), got)
+
+
+def test_backward_is_forward_of_transpose():
+    """proj/tests/test_tile.cpp:200-223 (ideal backward == forward on W^T)."""
+    s = cfg_io(xb.perfect_io(), xb.perfect_io())
+    W = np.random.default_rng(51).uniform(-0.4, 0.4, (5, 7))
+    a = xb.AnalogTile(5, 7, s, 8)
+    a.set_weights(W)
+    t = xb.AnalogTile(7, 5, s, 9)
+    t.set_weights(W.T)
+    d = np.random.default_rng(52).uniform(-1, 1, 5)
+    np.testing.assert_allclose(a.backward(d), t.forward(d), rtol=1e-6, atol=1e-7)
+
+
+def test_forward_noisy_read_noise():
+    """forward_noisy == forward with sigma_w = hypot(sigma_w, extra) (io.cpp:74-91)."""
+    s = cfg_io(xb.perfect_io(), xb.perfect_io())
+    g = xb.AnalogTile(64, 256, s, 3)
+    W = np.random.default_rng(1).uniform(-0.3, 0.3, (64, 256)).astype(np.float32)
+    g.set_weights(W)
+    x = np.random.default_rng(2).uniform(-1, 1, 256).astype(np.float32)
+    Y = g.forward_noisy(np.tile(x, (4000, 1)), 0.05).astype(np.float64)
+    exact = W.astype(np.float64) @ x
+    var = 0.05 ** 2 * float(x.astype(np.float64) @ x)
+    assert np.all(np.abs(Y.mean(axis=0) - exact) < 5 * np.sqrt(var / 4000))
+    assert abs(Y.var(axis=0).mean() / var - 1) < 0.05
