@@ -125,7 +125,10 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl")
     dev = torch.device("cuda", local)
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream shared by torch and the tile, so CUDA
+    # events, NCCL and the tile's kernels are ordered on one queue
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
 
     tile, cfg = make_tile(xb, rank, world)
     tile.set_stream(stream.cuda_stream)

@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(256) trains_kernel(
     if (px_out) {
       px_out[(size_t)b * C + j] = (v < 0.f) ? -p : p;
     } else {
-      xw[(size_t)b * C + j] = train_word(v, p, bl, key, (uint32_t)j, seq, 0u);
+      xw[(size_t)b * C + j] = skip ? 0u : train_word(v, p, bl, key, (uint32_t)j, seq, 0u);
     }
   }
   for (int i = threadIdx.x; i < R; i += blockDim.x) {
@@ -121,7 +121,8 @@ __global__ void __launch_bounds__(256) trains_kernel(
     if (pd_out) {
       pd_out[(size_t)b * R + i] = (v < 0.f) ? -p : p;
     } else {
-      dw[(size_t)b * R + i] = train_word(v, p, bl, key, (uint32_t)(row0 + i), seq, 0x80000000u);
+      dw[(size_t)b * R + i] =
+          skip ? 0u : train_word(v, p, bl, key, (uint32_t)(row0 + i), seq, 0x80000000u);
     }
   }
 }
@@ -139,20 +140,25 @@ void launch_trains(const Tile &t, const float *X, const float *D, int B, const f
 }
 
 // ============================================================== device laws
-// proj/src/device.cpp:48-77, fp32.  Per direction the law needs a signed step
-// scale; the constants that depend on (cell, direction) are selected once per
-// sample ("Dir") and reused for every pulse of that sample.
+// proj/src/device.cpp:48-77 in fp32.  Everything that depends only on (cell,
+// direction) is folded once per sample into Dir, so one pulse is
+//   t  = law factor (1 for ConstantStep; 1 - w/b; 1 -+ slope w; exp(...))
+//   su = sgn dw (1 + std z)                        (c2c noise, :72-74)
+//   w  = clamp(w + su t, w_min, w_max)             (:75-76)
+// i.e. three FMAs and two min/max per pulse (plus one MUFU.EX2 for ExpStep).
 struct LawArgs {
   float slope, gamma, std;
 };
 
 struct Cell {
   float dwu, dwd, wmax, wmin;
-  float a_up, a_dn; // law-specific per-cell constants
+  float k_up, k_dn; // SoftBounds: 1/w_max, 1/w_min; ExpStep: gamma log2(e) / range
 };
 
 struct Dir {
-  float sgn, dwv, a, off;
+  float sdw;   // sgn * dw_min_{up,down}
+  float sdws;  // sgn * dw * dw_min_std
+  float a, b2; // law factor t = a w + 1 (SB, Linear) or exp2(a w + b2) (Exp)
 };
 
 template <int LAW>
@@ -162,15 +168,13 @@ __device__ __forceinline__ Cell make_cell(float4 p, const LawArgs &la) {
   c.dwd = p.y;
   c.wmax = p.z;
   c.wmin = p.w;
-  c.a_up = 0.f;
-  c.a_dn = 0.f;
+  c.k_up = 0.f;
+  c.k_dn = 0.f;
   if (LAW == XB_SOFT_BOUNDS) {
-    c.a_up = 1.0f / p.z; // step = dw (1 - w / w_max)
-    c.a_dn = 1.0f / p.w; //        dw (1 - w / w_min)
+    c.k_up = 1.0f / p.z;
+    c.k_dn = 1.0f / p.w;
   } else if (LAW == XB_EXP_STEP) {
-    // step = dw exp(-gamma (w - w_min) / range)  (up)
-    //        dw exp(-gamma (w_max - w) / range)  (down); kept in log2 units
-    c.a_up = la.gamma / (p.z - p.w) * 1.4426950408889634f;
+    c.k_up = la.gamma / (p.z - p.w) * 1.4426950408889634f;
   }
   return c;
 }
@@ -178,63 +182,100 @@ __device__ __forceinline__ Cell make_cell(float4 p, const LawArgs &la) {
 template <int LAW>
 __device__ __forceinline__ Dir make_dir(const Cell &c, bool up, const LawArgs &la) {
   Dir d;
-  d.sgn = up ? 1.f : -1.f;
-  d.dwv = up ? c.dwu : c.dwd;
+  const float dw = up ? c.dwu : c.dwd;
+  d.sdw = up ? dw : -dw;
+  d.sdws = d.sdw * la.std;
   d.a = 0.f;
-  d.off = 0.f;
+  d.b2 = 0.f;
   if (LAW == XB_SOFT_BOUNDS) {
-    d.a = up ? c.a_up : c.a_dn;
+    d.a = up ? -c.k_up : -c.k_dn; // 1 - w / w_max  |  1 - w / w_min
   } else if (LAW == XB_LINEAR_STEP) {
-    d.a = up ? -la.slope : la.slope; // up: 1 - slope w ; down: 1 + slope w
+    d.a = up ? -la.slope : la.slope; // 1 - slope w  |  1 + slope w
   } else if (LAW == XB_EXP_STEP) {
-    d.a = c.a_up;
-    d.off = up ? -c.wmin : c.wmax; // up: (w - w_min) ; down: (w_max - w)
+    // up: exp(-g (w - w_min)) ; down: exp(-g (w_max - w)), g = gamma / range (log2 units)
+    d.a = up ? -c.k_up : c.k_up;
+    d.b2 = up ? c.k_up * c.wmin : -c.k_up * c.wmax;
   }
   return d;
 }
 
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 template <int LAW, bool NOISE>
-__device__ __forceinline__ float pulse(float w, const Cell &c, const Dir &d, float std, float z) {
-  float step;
+__device__ __forceinline__ float pulse(float w, const Cell &c, const Dir &d, float z) {
+  const float su = NOISE ? fmaf(d.sdws, z, d.sdw) : d.sdw;
   if (LAW == XB_CONSTANT_STEP) {
-    step = d.dwv;
-  } else if (LAW == XB_SOFT_BOUNDS) {
-    step = d.dwv * fmaf(-w, d.a, 1.0f);
-  } else if (LAW == XB_LINEAR_STEP) {
-    step = d.dwv * fmaf(d.a, w, 1.0f);
+    w += su;
+  } else if (LAW == XB_EXP_STEP) {
+    w = fmaf(su, ex2_approx(fmaf(d.a, w, d.b2)), w);
   } else {
-    step = d.dwv * exp2f(-d.a * fmaf(d.sgn, w, d.off));
+    w = fmaf(su, fmaf(d.a, w, 1.0f), w);
   }
-  if (NOISE) step *= fmaf(std, z, 1.0f); // device.cpp:72-74
-  w = fmaf(d.sgn, step, w);
-  return fminf(fmaxf(w, c.wmin), c.wmax); // device.cpp:75-76
+  return fminf(fmaxf(w, c.wmin), c.wmax);
+}
+
+// ---- fast Box-Muller for the c2c noise (statistical parity only):
+// MUFU lg2 / rsqrt / sin / cos on uniforms strictly inside (0, 1)
+__device__ __forceinline__ void box_muller_fast(uint32_t a, uint32_t b, float &z0, float &z1) {
+  const float u = fmaf((float)(a >> 9), 1.1920928955078125e-07f, 5.9604644775390625e-08f);
+  float l, r, s, c;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(u));
+  const float x = l * -1.3862943611198906f; // -2 ln(u)
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  r *= x;
+  const float th = fmaf((float)(b >> 9), 7.490140565847061e-07f, -3.1415926535897931f);
+  asm("sin.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(th));
+  asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(th));
+  z0 = r * c;
+  z1 = r * s;
+}
+
+__device__ __forceinline__ void normal4_fast(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                             Key key, float &z0, float &z1, float &z2,
+                                             float &z3) {
+  philox10(c0, c1, c2, c3, key);
+  box_muller_fast(c0, c1, z0, z1);
+  box_muller_fast(c2, c3, z2, z3);
 }
 
 // ============================================================== K5: pulse
-// CTA tile: PR rows (one per warp) x 32 columns (one per lane).  The words of
-// a chunk of SB samples are staged in shared memory:
-//   xs[b][32]       x words of the CTA's columns (lane-contiguous, conflict-free)
-//   ds[PR][SB + 1]  d words of the CTA's rows
-// Each lane walks its cell's samples in order and fires its pulses; all
-// active lanes fire exactly one pulse per loop trip, so the c2c normal cache
-// (4 per Philox call) is refilled warp-uniformly.  Normal #n of cell (i, j)
-// in launch `call` is Philox(k_c2c, (n/4, j, i, call))[n%4] -> Box-Muller:
-// independent of geometry, warp composition and sharding.
+// CTA tile: PR rows (one per warp) x 32 columns (one per lane); each thread
+// owns one cell and keeps w and its realization in registers for the whole
+// batch.  Per chunk of SB samples:
+//   staging   xs[b][32] x words of the CTA's columns (lane-contiguous), ds[r][b]
+//             d words of the CTA's rows;
+//   pre-pass  (warp-uniform, branch-free) one bit per sample that has at least
+//             one coincidence for this cell: ms[r][b/32][lane];
+//   pulse loop  every active lane fires exactly one pulse per trip, walking
+//             its own non-empty samples in order (find-next-set-bit on the
+//             mask, AND of the two words, pop one slot bit per pulse).  Lanes
+//             never wait on each other inside a chunk except at its end.
+// c2c normal #n of cell (i, j) in launch `call` is element n%4 of
+// Philox(k_c2c, (n/4, j, i, call)); a trip group of 4 refills all active lanes
+// at once, so the refill is warp-uniform and the draw sequence of a cell is
+// independent of geometry, warp composition and row sharding.
 constexpr int PULSE_PR = 16;
 constexpr int PULSE_SB = 256;
+constexpr int PULSE_NW = PULSE_SB / 32;
 
 template <int LAW, bool NOISE>
-__global__ void __launch_bounds__(PULSE_PR * 32) pulse_kernel(
+__global__ void __launch_bounds__(PULSE_PR * 32, 3) pulse_kernel(
     float *__restrict__ W, const float4 *__restrict__ P, int ld, int R, int C,
     const uint32_t *__restrict__ xw, const uint32_t *__restrict__ dw, int B, int row0,
     LawArgs la, Key key, uint32_t call) {
   extern __shared__ uint32_t smem[];
-  uint32_t *xs = smem;                    // [SB][32]
-  uint32_t *ds = smem + PULSE_SB * 32;    // [PR][SB + 1]
+  uint32_t *xs = smem;                                 // [SB][32]
+  uint32_t *ds = xs + PULSE_SB * 32;                   // [PR][SB + 1]
+  uint32_t *ms = ds + PULSE_PR * (PULSE_SB + 1);       // [PR][NW][32]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int col0 = blockIdx.x * 32, rowb = blockIdx.y * PULSE_PR;
   const int j = col0 + lane, i = rowb + warp;
-  const bool valid = (i < R) && (j < C);
+  const bool row_ok = i < R; // warp-uniform
+  const bool valid = row_ok && (j < C);
   const size_t idx = (size_t)i * ld + j;
 
   float w = 0.f;
@@ -244,10 +285,13 @@ __global__ void __launch_bounds__(PULSE_PR * 32) pulse_kernel(
     cell = make_cell<LAW>(P[idx], la);
   }
   const uint32_t jg = (uint32_t)j, ig = (uint32_t)(row0 + i);
-  uint32_t g = 0; // normal group index (4 normals per group), per lane
+  uint32_t g = 0; // normal group index, per lane
+  const uint32_t *dsr = ds + warp * (PULSE_SB + 1);
+  uint32_t *msr = ms + warp * (PULSE_NW * 32) + lane;
 
   for (int b0 = 0; b0 < B; b0 += PULSE_SB) {
     const int nb = min(PULSE_SB, B - b0);
+    const int nw = (nb + 31) >> 5;
     __syncthreads();
     for (int t = threadIdx.x; t < nb * 32; t += blockDim.x) {
       const int bb = t >> 5, l = t & 31;
@@ -258,31 +302,50 @@ __global__ void __launch_bounds__(PULSE_PR * 32) pulse_kernel(
       ds[r * (PULSE_SB + 1) + bb] = (rowb + r < R) ? dw[(size_t)(b0 + bb) * R + rowb + r] : 0u;
     }
     __syncthreads();
-    if (!valid) continue;
+    if (!row_ok) continue;
 
-    const uint32_t *dsr = ds + warp * (PULSE_SB + 1);
-    int b = -1;
+    // ---- pre-pass: non-empty-sample bitmask of this cell (branch-free)
+    for (int wd = 0; wd < nw; ++wd) {
+      uint32_t m = 0;
+#pragma unroll 8
+      for (int t = 0; t < 32; ++t) {
+        const int bb = (wd << 5) + t;
+        const uint32_t c = (bb < nb) ? (xs[bb * 32 + lane] & dsr[bb] & 0x7fffffffu) : 0u;
+        m |= (uint32_t)(c != 0u) << t;
+      }
+      msr[wd * 32] = valid ? m : 0u;
+    }
+    __syncwarp();
+
+    // ---- pulse loop
+    int wi = 0;
+    uint32_t m = msr[0];
     uint32_t c = 0;
     Dir dir{};
-    bool done = false;
-    // fire one pulse of this lane's cell; returns false when the chunk is exhausted
     auto step = [&](float z) -> bool {
-      while (c == 0u) {
-        if (++b >= nb) return false;
-        const uint32_t xv = xs[b * 32 + lane], dv = dsr[b];
+      if (c == 0u) {
+        while (m == 0u) {
+          if (++wi >= nw) return false;
+          m = msr[wi * 32];
+        }
+        const int bb = (wi << 5) + (__ffs(m) - 1);
+        m &= m - 1u;
+        const uint32_t xv = xs[bb * 32 + lane], dv = dsr[bb];
         c = xv & dv & 0x7fffffffu;
-        if (c) dir = make_dir<LAW>(cell, ((xv ^ dv) >> 31) == 0u, la);
+        dir = make_dir<LAW>(cell, (int32_t)(xv ^ dv) >= 0, la);
       }
-      w = pulse<LAW, NOISE>(w, cell, dir, la.std, z);
+      w = pulse<LAW, NOISE>(w, cell, dir, z);
       c &= c - 1u;
       return true;
     };
-    while (!done) {
+    bool more = true;
+    while (more) {
       float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
-      if (NOISE) normal4(g, jg, ig, call, key, z0, z1, z2, z3);
+      if (NOISE) normal4_fast(g, jg, ig, call, key, z0, z1, z2, z3);
       ++g;
-      done = !step(z0) || !step(z1) || !step(z2) || !step(z3);
+      more = step(z0) && step(z1) && step(z2) && step(z3);
     }
+    __syncwarp();
   }
   if (valid) W[idx] = w;
 }
@@ -290,7 +353,8 @@ __global__ void __launch_bounds__(PULSE_PR * 32) pulse_kernel(
 template <int LAW, bool NOISE>
 static void pulse_dispatch(Tile &t, const uint32_t *xw, const uint32_t *dw, int B, LawArgs la,
                            uint32_t call) {
-  const size_t smem = (size_t)(PULSE_SB * 32 + PULSE_PR * (PULSE_SB + 1)) * sizeof(uint32_t);
+  const size_t smem = (size_t)(PULSE_SB * 32 + PULSE_PR * (PULSE_SB + 1) +
+                               PULSE_PR * PULSE_NW * 32) * sizeof(uint32_t);
   static bool configured = false;
   if (!configured) {
     XB_CUDA(cudaFuncSetAttribute(pulse_kernel<LAW, NOISE>,
@@ -309,26 +373,20 @@ void launch_pulse(Tile &t, const uint32_t *xw, const uint32_t *dw, int B, uint32
   const LawArgs la{(float)t.cfg.device.slope, (float)t.cfg.device.gamma,
                    (float)t.cfg.device.dw_min_std};
   const bool noise = t.cfg.device.dw_min_std > 0.0;
+#define XB_PULSE(K)                                                                        \
+  case K:                                                                                  \
+    noise ? pulse_dispatch<K, true>(t, xw, dw, B, la, call_id)                             \
+          : pulse_dispatch<K, false>(t, xw, dw, B, la, call_id);                           \
+    break;
   switch (t.cfg.device.kind) {
-  case XB_CONSTANT_STEP:
-    noise ? pulse_dispatch<XB_CONSTANT_STEP, true>(t, xw, dw, B, la, call_id)
-          : pulse_dispatch<XB_CONSTANT_STEP, false>(t, xw, dw, B, la, call_id);
-    break;
-  case XB_LINEAR_STEP:
-    noise ? pulse_dispatch<XB_LINEAR_STEP, true>(t, xw, dw, B, la, call_id)
-          : pulse_dispatch<XB_LINEAR_STEP, false>(t, xw, dw, B, la, call_id);
-    break;
-  case XB_SOFT_BOUNDS:
-    noise ? pulse_dispatch<XB_SOFT_BOUNDS, true>(t, xw, dw, B, la, call_id)
-          : pulse_dispatch<XB_SOFT_BOUNDS, false>(t, xw, dw, B, la, call_id);
-    break;
-  case XB_EXP_STEP:
-    noise ? pulse_dispatch<XB_EXP_STEP, true>(t, xw, dw, B, la, call_id)
-          : pulse_dispatch<XB_EXP_STEP, false>(t, xw, dw, B, la, call_id);
-    break;
+    XB_PULSE(XB_CONSTANT_STEP)
+    XB_PULSE(XB_LINEAR_STEP)
+    XB_PULSE(XB_SOFT_BOUNDS)
+    XB_PULSE(XB_EXP_STEP)
   default:
     raise("device.kind: unknown device model");
   }
+#undef XB_PULSE
 }
 
 // ============================================================== K6: deterministic
@@ -354,9 +412,9 @@ __global__ void __launch_bounds__(256) pulse_det_kernel(
     const long long count = llround((double)bl[b] * fabs(a) * fabs(x));
     const Dir dir = make_dir<LAW>(cell, (a > 0.0) == (x > 0.0), la);
     for (long long k = 0; k < count; ++k, ++n) {
-      if (NOISE && (n & 3u) == 0u) normal4(n >> 2, (uint32_t)j, (uint32_t)(row0 + i), call, key,
-                                           z[0], z[1], z[2], z[3]);
-      w = pulse<LAW, NOISE>(w, cell, dir, la.std, z[n & 3u]);
+      if (NOISE && (n & 3u) == 0u)
+        normal4_fast(n >> 2, (uint32_t)j, (uint32_t)(row0 + i), call, key, z[0], z[1], z[2], z[3]);
+      w = pulse<LAW, NOISE>(w, cell, dir, z[n & 3u]);
     }
   }
   W[idx] = w;
