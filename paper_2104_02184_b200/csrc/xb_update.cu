@@ -218,20 +218,52 @@ __device__ __forceinline__ float pulse(float w, const Cell &c, const Dir &d, flo
   return fminf(fmaxf(w, c.wmin), c.wmax);
 }
 
-// ---- fast Box-Muller for the c2c noise (statistical parity only):
-// MUFU lg2 / rsqrt / sin / cos on uniforms strictly inside (0, 1)
+// ---- c2c noise: Philox4x32-10 with the 10 round keys precomputed on the host
+// (kernel parameters, i.e. constant-bank operands of the LOP3s) and a
+// MUFU-based Box-Muller on 24-bit uniforms.  Statistical parity only; the
+// radius uses u in (0, 1], so the tail extends to sqrt(2 ln 2^24) = 5.8 sigma.
+struct RoundKeys {
+  uint32_t k0[10], k1[10];
+};
+
+static RoundKeys round_keys(Key k) {
+  RoundKeys r;
+  uint32_t a = k.k0, b = k.k1;
+  for (int i = 0; i < 10; ++i) {
+    r.k0[i] = a;
+    r.k1[i] = b;
+    a += 0x9E3779B9u;
+    b += 0xBB67AE85u;
+  }
+  return r;
+}
+
+__device__ __forceinline__ void philox10_rk(uint32_t &c0, uint32_t &c1, uint32_t &c2,
+                                            uint32_t &c3, const RoundKeys &rk) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) philox_round(c0, c1, c2, c3, rk.k0[r], rk.k1[r]);
+}
+
 __device__ __forceinline__ void box_muller_fast(uint32_t a, uint32_t b, float &z0, float &z1) {
-  const float u = fmaf((float)(a >> 9), 1.1920928955078125e-07f, 5.9604644775390625e-08f);
+  // u in (0, 1] and theta in [-pi, pi) straight from the mantissa bits
+  const float u = 2.0f - __int_as_float(0x3f800000u | (a >> 9));
+  const float th = fmaf(__int_as_float(0x3f800000u | (b >> 9)), 6.2831853071795865f,
+                        -9.4247779607693797f);
   float l, r, s, c;
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(u));
-  const float x = l * -1.3862943611198906f; // -2 ln(u)
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  r *= x;
-  const float th = fmaf((float)(b >> 9), 7.490140565847061e-07f, -3.1415926535897931f);
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(l * -1.3862943611198906f)); // -2 ln u
   asm("sin.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(th));
   asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(th));
   z0 = r * c;
   z1 = r * s;
+}
+
+__device__ __forceinline__ void normal4_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                           const RoundKeys &rk, float &z0, float &z1, float &z2,
+                                           float &z3) {
+  philox10_rk(c0, c1, c2, c3, rk);
+  box_muller_fast(c0, c1, z0, z1);
+  box_muller_fast(c2, c3, z2, z3);
 }
 
 __device__ __forceinline__ void normal4_fast(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
@@ -243,40 +275,40 @@ __device__ __forceinline__ void normal4_fast(uint32_t c0, uint32_t c1, uint32_t 
 }
 
 // ============================================================== K5: pulse
-// CTA tile: PR rows (one per warp) x 32 columns (one per lane); each thread
-// owns one cell and keeps w and its realization in registers for the whole
-// batch.  Per chunk of SB samples:
-//   staging   xs[b][32] x words of the CTA's columns (lane-contiguous), ds[r][b]
-//             d words of the CTA's rows;
-//   pre-pass  (warp-uniform, branch-free) one bit per sample that has at least
-//             one coincidence for this cell: ms[r][b/32][lane];
-//   pulse loop  every active lane fires exactly one pulse per trip, walking
-//             its own non-empty samples in order (find-next-set-bit on the
-//             mask, AND of the two words, pop one slot bit per pulse).  Lanes
-//             never wait on each other inside a chunk except at its end.
-// c2c normal #n of cell (i, j) in launch `call` is element n%4 of
-// Philox(k_c2c, (n/4, j, i, call)); a trip group of 4 refills all active lanes
-// at once, so the refill is warp-uniform and the draw sequence of a cell is
-// independent of geometry, warp composition and row sharding.
-constexpr int PULSE_PR = 16;
-constexpr int PULSE_SB = 256;
-constexpr int PULSE_NW = PULSE_SB / 32;
+// One warp = one row i of the tile and 32 consecutive columns (one cell per
+// lane); w and the cell's realization stay in registers for the whole batch.
+// The batch is consumed in segments:
+//   pre-pass (branch-free, sample order): per sample b, c = x_b & d_b (slot
+//     bits), k = popc(c), direction = sign(x) * sign(d); the lane appends k
+//     direction bits to its private pulse stream in shared memory
+//     (1 = up, 0 = down).  A segment ends when some lane's stream would pass
+//     CAP pulses (a warp vote), so any batch size and pulse density fit.
+//   pulse loop: iteration n applies pulse n of every lane whose stream is
+//     longer than n: the direction bit selects the law constants, the c2c
+//     normal comes from a warp-uniform Philox refill every 4 iterations.
+// Lanes therefore wait only on the longest stream of the segment, and the
+// per-cell pulse order is exactly the reference's (sample order; one
+// direction per sample; pulses of a sample are interchangeable).
+// c2c normal #(4q + r) of a cell's segment is element r of
+// Philox(k_c2c, (g0 + q, j, i, call)) with g0 the cell's running group count,
+// independent of launch geometry and of row sharding.
+constexpr int PULSE_WARPS = 16;          // rows per CTA
+constexpr int PULSE_QW = 16;             // stream words per lane
+constexpr int PULSE_CAP = PULSE_QW * 32; // pulses per lane per segment
 
 template <int LAW, bool NOISE>
-__global__ void __launch_bounds__(PULSE_PR * 32, 3) pulse_kernel(
+__global__ void __launch_bounds__(PULSE_WARPS * 32, 2) pulse_kernel(
     float *__restrict__ W, const float4 *__restrict__ P, int ld, int R, int C,
     const uint32_t *__restrict__ xw, const uint32_t *__restrict__ dw, int B, int row0,
-    LawArgs la, Key key, uint32_t call) {
-  extern __shared__ uint32_t smem[];
-  uint32_t *xs = smem;                                 // [SB][32]
-  uint32_t *ds = xs + PULSE_SB * 32;                   // [PR][SB + 1]
-  uint32_t *ms = ds + PULSE_PR * (PULSE_SB + 1);       // [PR][NW][32]
+    LawArgs la, RoundKeys rk, uint32_t call) {
+  __shared__ uint32_t qs[PULSE_WARPS][PULSE_QW][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int col0 = blockIdx.x * 32, rowb = blockIdx.y * PULSE_PR;
-  const int j = col0 + lane, i = rowb + warp;
-  const bool row_ok = i < R; // warp-uniform
-  const bool valid = row_ok && (j < C);
+  const int j = blockIdx.x * 32 + lane;
+  const int i = blockIdx.y * PULSE_WARPS + warp;
+  if (i >= R) return; // warp-uniform: no block-level barriers below
+  const bool valid = j < C;
   const size_t idx = (size_t)i * ld + j;
+  uint32_t *q = &qs[warp][0][lane];
 
   float w = 0.f;
   Cell cell{};
@@ -284,67 +316,76 @@ __global__ void __launch_bounds__(PULSE_PR * 32, 3) pulse_kernel(
     w = W[idx];
     cell = make_cell<LAW>(P[idx], la);
   }
+  const Dir up = make_dir<LAW>(cell, true, la), dn = make_dir<LAW>(cell, false, la);
   const uint32_t jg = (uint32_t)j, ig = (uint32_t)(row0 + i);
-  uint32_t g = 0; // normal group index, per lane
-  const uint32_t *dsr = ds + warp * (PULSE_SB + 1);
-  uint32_t *msr = ms + warp * (PULSE_NW * 32) + lane;
+  const uint32_t *xcol = xw + (valid ? j : 0);
+  const uint32_t *drow = dw + i;
+  uint32_t g0 = 0;
 
-  for (int b0 = 0; b0 < B; b0 += PULSE_SB) {
-    const int nb = min(PULSE_SB, B - b0);
-    const int nw = (nb + 31) >> 5;
-    __syncthreads();
-    for (int t = threadIdx.x; t < nb * 32; t += blockDim.x) {
-      const int bb = t >> 5, l = t & 31;
-      xs[t] = (col0 + l < C) ? xw[(size_t)(b0 + bb) * C + col0 + l] : 0u;
-    }
-    for (int t = threadIdx.x; t < nb * PULSE_PR; t += blockDim.x) {
-      const int bb = t / PULSE_PR, r = t % PULSE_PR;
-      ds[r * (PULSE_SB + 1) + bb] = (rowb + r < R) ? dw[(size_t)(b0 + bb) * R + rowb + r] : 0u;
-    }
-    __syncthreads();
-    if (!row_ok) continue;
-
-    // ---- pre-pass: non-empty-sample bitmask of this cell (branch-free)
-    for (int wd = 0; wd < nw; ++wd) {
-      uint32_t m = 0;
-#pragma unroll 8
-      for (int t = 0; t < 32; ++t) {
-        const int bb = (wd << 5) + t;
-        const uint32_t c = (bb < nb) ? (xs[bb * 32 + lane] & dsr[bb] & 0x7fffffffu) : 0u;
-        m |= (uint32_t)(c != 0u) << t;
+  int b = 0;
+  while (b < B) {
+    // ---------------- pre-pass: build this lane's pulse stream
+    uint32_t T = 0, acc = 0, qi = 0;
+    while (b < B) {
+      uint32_t xv[8], dv[8];
+      const int nb = min(8, B - b);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        xv[u] = (u < nb && valid) ? __ldg(xcol + (size_t)(b + u) * C) : 0u;
+        dv[u] = (u < nb) ? __ldg(drow + (size_t)(b + u) * R) : 0u;
       }
-      msr[wd * 32] = valid ? m : 0u;
+      bool full = false;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (u < nb && !full) {
+          const uint32_t c = xv[u] & dv[u] & 0x7fffffffu;
+          const uint32_t k = __popc(c);
+          if (__any_sync(0xffffffffu, T + k > PULSE_CAP)) {
+            full = true;
+          } else {
+            const uint32_t bits = ((int32_t)(xv[u] ^ dv[u]) >= 0) ? ((1u << k) - 1u) : 0u;
+            const uint32_t sh = T & 31u;
+            const uint64_t wide = (uint64_t)bits << sh;
+            acc |= (uint32_t)wide;
+            if (sh + k >= 32u) {
+              q[qi * 32] = acc;
+              ++qi;
+              acc = (uint32_t)(wide >> 32);
+            }
+            T += k;
+            ++b;
+          }
+        }
+      }
+      if (full) break;
     }
+    if (T & 31u) q[qi * 32] = acc;
+    const uint32_t maxT = __reduce_max_sync(0xffffffffu, T);
     __syncwarp();
 
-    // ---- pulse loop
-    int wi = 0;
-    uint32_t m = msr[0];
-    uint32_t c = 0;
-    Dir dir{};
-    auto step = [&](float z) -> bool {
-      if (c == 0u) {
-        while (m == 0u) {
-          if (++wi >= nw) return false;
-          m = msr[wi * 32];
+    // ---------------- pulse loop: pulse n of every lane with n < T
+    for (uint32_t n0 = 0; n0 < maxT; n0 += 32) {
+      const uint32_t word = q[(n0 >> 5) * 32];
+#pragma unroll
+      for (int u4 = 0; u4 < 32; u4 += 4) {
+        if (n0 + u4 >= maxT) break;
+        float z[4] = {0.f, 0.f, 0.f, 0.f};
+        if (NOISE) normal4_rk(g0 + ((n0 + u4) >> 2), jg, ig, call, rk, z[0], z[1], z[2], z[3]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const bool on = n0 + u4 + u < T;
+          const bool is_up = (word >> (u4 + u)) & 1u;
+          Dir d;
+          d.sdw = is_up ? up.sdw : dn.sdw;
+          d.sdws = is_up ? up.sdws : dn.sdws;
+          d.a = is_up ? up.a : dn.a;
+          d.b2 = is_up ? up.b2 : dn.b2;
+          const float wn = pulse<LAW, NOISE>(w, cell, d, z[u]);
+          w = on ? wn : w;
         }
-        const int bb = (wi << 5) + (__ffs(m) - 1);
-        m &= m - 1u;
-        const uint32_t xv = xs[bb * 32 + lane], dv = dsr[bb];
-        c = xv & dv & 0x7fffffffu;
-        dir = make_dir<LAW>(cell, (int32_t)(xv ^ dv) >= 0, la);
       }
-      w = pulse<LAW, NOISE>(w, cell, dir, z);
-      c &= c - 1u;
-      return true;
-    };
-    bool more = true;
-    while (more) {
-      float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
-      if (NOISE) normal4_fast(g, jg, ig, call, key, z0, z1, z2, z3);
-      ++g;
-      more = step(z0) && step(z1) && step(z2) && step(z3);
     }
+    g0 += (T + 3u) >> 2;
     __syncwarp();
   }
   if (valid) W[idx] = w;
@@ -353,17 +394,9 @@ __global__ void __launch_bounds__(PULSE_PR * 32, 3) pulse_kernel(
 template <int LAW, bool NOISE>
 static void pulse_dispatch(Tile &t, const uint32_t *xw, const uint32_t *dw, int B, LawArgs la,
                            uint32_t call) {
-  const size_t smem = (size_t)(PULSE_SB * 32 + PULSE_PR * (PULSE_SB + 1) +
-                               PULSE_PR * PULSE_NW * 32) * sizeof(uint32_t);
-  static bool configured = false;
-  if (!configured) {
-    XB_CUDA(cudaFuncSetAttribute(pulse_kernel<LAW, NOISE>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
-  }
-  dim3 grid((t.C + 31) / 32, (t.R + PULSE_PR - 1) / PULSE_PR);
-  pulse_kernel<LAW, NOISE><<<grid, PULSE_PR * 32, smem, t.stream>>>(
-      t.W, t.P, t.ld, t.R, t.C, xw, dw, B, t.row0, la, t.k_c2c, call);
+  dim3 grid((t.C + 31) / 32, (t.R + PULSE_WARPS - 1) / PULSE_WARPS);
+  pulse_kernel<LAW, NOISE><<<grid, PULSE_WARPS * 32, 0, t.stream>>>(
+      t.W, t.P, t.ld, t.R, t.C, xw, dw, B, t.row0, la, round_keys(t.k_c2c), call);
   count_launch();
   XB_CUDA(cudaGetLastError());
 }
