@@ -263,8 +263,9 @@ struct UpdBufs {
 static UpdBufs upd_bufs(Tile &t, int B, bool det) {
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   const size_t s_lr = al(B * sizeof(float)), s_bl = al(B * sizeof(int32_t));
-  const size_t s_xw = al((size_t)B * t.C * (det ? sizeof(double) : sizeof(uint32_t)));
-  const size_t s_dw = al((size_t)B * std::max(t.R, 1) * (det ? sizeof(double) : sizeof(uint32_t)));
+  const size_t nb = det ? (size_t)B : (size_t)train_ld(B); // trains are line-major [line][ldb]
+  const size_t s_xw = al(nb * t.C * (det ? sizeof(double) : sizeof(uint32_t)));
+  const size_t s_dw = al(nb * std::max(t.R, 1) * (det ? sizeof(double) : sizeof(uint32_t)));
   char *p = (char *)t.s_words.get(3 * s_lr + s_bl + s_xw + s_dw);
   UpdBufs u{};
   u.lr = (float *)p;
@@ -310,15 +311,22 @@ static void update_device(Tile &t, const float *dX, const float *dD, int B, cons
       launch_rows_amax(dD, B, t.R, t.R, u.dm, t.stream);
       dm = u.dm;
     }
-    launch_trains(t, dX, dD, B, lr_d, lr_s, u.xm, dm, t.seq_upd, u.xw, u.dw, u.bl, u.px, u.pd, det);
+    launch_trains(t, dX, dD, B, lr_d, lr_s, u.xm, dm, t.seq_upd, u.xw, u.dw, train_ld(B), u.bl,
+                  u.px, u.pd, det);
   }
-  if (peek) {
-    XB_CUDA(cudaMemcpyAsync(xw_out, u.xw, sizeof(uint32_t) * (size_t)B * t.C,
+  if (peek) { // back to the reference-facing sample-major layout
+    const int ldb = train_ld(B);
+    std::vector<uint32_t> hx((size_t)ldb * t.C), hd((size_t)ldb * t.R);
+    XB_CUDA(cudaMemcpyAsync(hx.data(), u.xw, sizeof(uint32_t) * hx.size(),
                             cudaMemcpyDeviceToHost, t.stream));
-    XB_CUDA(cudaMemcpyAsync(dw_out, u.dw, sizeof(uint32_t) * (size_t)B * t.R,
+    XB_CUDA(cudaMemcpyAsync(hd.data(), u.dw, sizeof(uint32_t) * hd.size(),
                             cudaMemcpyDeviceToHost, t.stream));
     XB_CUDA(cudaMemcpyAsync(bl_out, u.bl, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, t.stream));
     sync(t);
+    for (int b = 0; b < B; ++b) {
+      for (int j = 0; j < t.C; ++j) xw_out[(size_t)b * t.C + j] = hx[(size_t)j * ldb + b];
+      for (int i = 0; i < t.R; ++i) dw_out[(size_t)b * t.R + i] = hd[(size_t)i * ldb + b];
+    }
     return;
   }
   {
@@ -326,7 +334,7 @@ static void update_device(Tile &t, const float *dX, const float *dD, int B, cons
     if (det)
       launch_pulse_det(t, u.px, u.pd, u.bl, B, t.upd_calls);
     else
-      launch_pulse(t, u.xw, u.dw, B, t.upd_calls);
+      launch_pulse(t, u.xw, u.dw, train_ld(B), B, t.upd_calls);
   }
   t.upd_calls += 1;
   t.seq_upd += (uint64_t)B;
@@ -833,18 +841,18 @@ int xb_tile_apply_trains(xb_tile *h, const uint32_t *xw, const uint32_t *dw, int
     Tile &t = h->t;
     if (B < 0) raise("apply_trains: batch must be >= 0");
     if (B == 0) return;
-    const size_t nx = (size_t)B * t.C, nd = (size_t)B * t.R;
-    uint32_t *d = scratch_as<uint32_t>(t.s_params, nx + nd);
-    XB_CUDA(cudaMemcpyAsync(d, xw, nx * 4, cudaMemcpyHostToDevice, t.stream));
-    if (flip) {
-      std::vector<uint32_t> f(dw, dw + nd);
-      for (auto &v : f) v ^= 0x80000000u;
-      XB_CUDA(cudaMemcpyAsync(d + nx, f.data(), nd * 4, cudaMemcpyHostToDevice, t.stream));
-      sync(t);
-    } else {
-      XB_CUDA(cudaMemcpyAsync(d + nx, dw, nd * 4, cudaMemcpyHostToDevice, t.stream));
+    // reference-facing sample-major words -> internal line-major layout
+    const int ldb = train_ld(B);
+    const size_t nx = (size_t)ldb * t.C, nd = (size_t)ldb * t.R;
+    std::vector<uint32_t> hw(nx + nd, 0u);
+    for (int b = 0; b < B; ++b) {
+      for (int j = 0; j < t.C; ++j) hw[(size_t)j * ldb + b] = xw[(size_t)b * t.C + j];
+      for (int i = 0; i < t.R; ++i)
+        hw[nx + (size_t)i * ldb + b] = dw[(size_t)b * t.R + i] ^ (flip ? 0x80000000u : 0u);
     }
-    launch_pulse(t, d, d + nx, B, t.upd_calls);
+    uint32_t *d = scratch_as<uint32_t>(t.s_params, nx + nd);
+    XB_CUDA(cudaMemcpyAsync(d, hw.data(), (nx + nd) * 4, cudaMemcpyHostToDevice, t.stream));
+    launch_pulse(t, d, d + nx, ldb, B, t.upd_calls);
     t.upd_calls += 1;
     t.seq_upd += (uint64_t)B;
     sync(t);

@@ -85,10 +85,14 @@ struct PhaseTimer {
 void launch_rows_amax(const float *V, int B, int n, int ld, float *out, cudaStream_t s);
 // per-sample translate + Bernoulli trains; writes packed words and bl[B]
 void launch_trains(const Tile &t, const float *X, const float *D, int B, const float *lr_dev,
-                   float lr_scalar, const float *xm, const float *dm, uint64_t seq0, uint32_t *xw, uint32_t *dw,
-                   int32_t *bl, double *px, double *pd, bool deterministic);
+                   float lr_scalar, const float *xm, const float *dm, uint64_t seq0,
+                   uint32_t *xw, uint32_t *dw, int ldb, int32_t *bl, double *px, double *pd,
+                   bool deterministic);
+// trains are LINE-major: xw[j][b], dw[i][b], row stride ldb (multiple of 8)
+inline int train_ld(int B) { return (B + 7) / 8 * 8; }
 // weight-stationary coincidence/pulse kernel over packed words
-void launch_pulse(Tile &t, const uint32_t *xw, const uint32_t *dw, int B, uint32_t call_id);
+void launch_pulse(Tile &t, const uint32_t *xw, const uint32_t *dw, int ldb, int B,
+                  uint32_t call_id);
 // deterministic_implicit: lround(bl*pd*px) pulses per cell per sample
 void launch_pulse_det(Tile &t, const double *px, const double *pd, const int32_t *bl, int B,
                       uint32_t call_id);

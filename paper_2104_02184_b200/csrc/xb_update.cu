@@ -76,65 +76,129 @@ __device__ __forceinline__ uint32_t train_word(float v, double p, int bl, Key ke
   return bits | (v < 0.f ? 0x80000000u : 0u);
 }
 
-__global__ void __launch_bounds__(256) trains_kernel(
-    const float *__restrict__ X, const float *__restrict__ D, int C, int R,
-    const float *__restrict__ lr, float lr_scalar, const float *__restrict__ xm,
-    const float *__restrict__ dm, double dw_min, int BL, int blm, Key key, uint64_t seq0, int row0, uint32_t *__restrict__ xw,
-    uint32_t *__restrict__ dw, int32_t *__restrict__ bl_out, double *__restrict__ px_out,
-    double *__restrict__ pd_out) {
-  const int b = blockIdx.x;
-  // ---- translate, proj/src/pulsed.cpp:25-66, in fp64 on the fp32 inputs ----
-  const double lrb = (double)(lr ? lr[b] : lr_scalar);
-  const double x_amax = (double)xm[b], d_amax = (double)dm[b];
-  const bool skip = (lrb == 0.0 || x_amax == 0.0 || d_amax == 0.0); // pulsed.cpp:122-124
+// translate, proj/src/pulsed.cpp:25-66, in fp64 on the fp32 inputs: the
+// per-sample part (BL management, amplitude, x/d rebalancing)
+struct Plan {
+  double amp, x_scale, d_scale;
+  int bl, skip;
+};
+
+__device__ __forceinline__ Plan make_plan(double lrb, double x_amax, double d_amax, double dw_min,
+                                          int BL, int blm) {
+  Plan pl;
+  pl.skip = (lrb == 0.0 || x_amax == 0.0 || d_amax == 0.0); // pulsed.cpp:122-124
   int bl = BL;
-  if (blm && !skip) {
+  if (blm && !pl.skip) {
     const double quanta = lrb * x_amax * d_amax / dw_min;
     const int c = (int)ceil(BL * (quanta < 1.0 ? quanta : 1.0));
     bl = c > 1 ? c : 1;
   }
-  const double amp = skip ? 0.0 : sqrt(lrb / (dw_min * bl));
-  double x_scale = 1.0, d_scale = 1.0;
+  pl.bl = bl;
+  pl.amp = pl.skip ? 0.0 : sqrt(lrb / (dw_min * bl));
+  pl.x_scale = 1.0;
+  pl.d_scale = 1.0;
   if (x_amax > 0.0 && d_amax > 0.0) {
-    x_scale = sqrt(d_amax / x_amax);
-    d_scale = 1.0 / x_scale;
+    pl.x_scale = sqrt(d_amax / x_amax);
+    pl.d_scale = 1.0 / pl.x_scale;
   }
-  if (threadIdx.x == 0 && bl_out) bl_out[b] = skip ? 0 : bl;
-  const uint64_t seq = seq0 + (uint64_t)b;
+  return pl;
+}
 
+// Packed trains in LINE-major layout out[line][b] (row stride ldb): the pulse
+// kernel then reads 4-8 consecutive samples of one line with a single vector
+// load.  CTA tile: 32 lines x 32 samples; x lines first, then d lines.
+__global__ void __launch_bounds__(256) trains_kernel(
+    const float *__restrict__ X, const float *__restrict__ D, int C, int R, int B,
+    const float *__restrict__ lr, float lr_scalar, const float *__restrict__ xm,
+    const float *__restrict__ dm, double dw_min, int BL, int blm, Key key, uint64_t seq0,
+    int row0, uint32_t *__restrict__ xw, uint32_t *__restrict__ dw, int ldb,
+    int32_t *__restrict__ bl_out) {
+  __shared__ Plan plan[32];
+  __shared__ uint32_t tile[32][33];
+  const int nxb = (C + 31) / 32;
+  const bool is_x = (int)blockIdx.x < nxb;
+  const int l0 = (is_x ? (int)blockIdx.x : (int)blockIdx.x - nxb) * 32;
+  const int nl = is_x ? C : R;
+  const int b0 = blockIdx.y * 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x < 32) {
+    const int b = b0 + threadIdx.x;
+    if (b < B) {
+      const double lrb = (double)(lr ? lr[b] : lr_scalar);
+      plan[threadIdx.x] = make_plan(lrb, (double)xm[b], (double)dm[b], dw_min, BL, blm);
+      if (blockIdx.x == 0 && bl_out) bl_out[b] = plan[threadIdx.x].skip ? 0 : plan[threadIdx.x].bl;
+    }
+  }
+  __syncthreads();
+  const int line = l0 + lane;
+  const float *V = is_x ? X : D;
+  for (int s = warp; s < 32; s += 8) {
+    const int b = b0 + s;
+    uint32_t word = 0;
+    if (b < B && line < nl) {
+      const Plan pl = plan[s];
+      const float v = V[(size_t)b * nl + line];
+      if (!pl.skip) {
+        double p = pl.amp * fabs((double)v) * (is_x ? pl.x_scale : pl.d_scale);
+        p = (p < 1.0) ? p : 1.0;
+        word = is_x ? train_word(v, p, pl.bl, key, (uint32_t)line, seq0 + b, 0u)
+                    : train_word(v, p, pl.bl, key, (uint32_t)(row0 + line), seq0 + b,
+                                 0x80000000u);
+      }
+    }
+    tile[lane][s] = word;
+  }
+  __syncthreads();
+  uint32_t *out = is_x ? xw : dw;
+  for (int r = warp; r < 32; r += 8) {
+    const int ln = l0 + r, b = b0 + lane;
+    if (ln < nl && b < B) out[(size_t)ln * ldb + b] = tile[r][lane];
+  }
+}
+
+// deterministic_implicit needs the probabilities themselves: signed p
+// (sign of the line, 0 for a no-op sample), sample-major [b][line]
+__global__ void __launch_bounds__(256) probs_kernel(
+    const float *__restrict__ X, const float *__restrict__ D, int C, int R,
+    const float *__restrict__ lr, float lr_scalar, const float *__restrict__ xm,
+    const float *__restrict__ dm, double dw_min, int BL, int blm, int32_t *__restrict__ bl_out,
+    double *__restrict__ px, double *__restrict__ pd) {
+  const int b = blockIdx.x;
+  const Plan pl = make_plan((double)(lr ? lr[b] : lr_scalar), (double)xm[b], (double)dm[b],
+                            dw_min, BL, blm);
+  if (threadIdx.x == 0 && bl_out) bl_out[b] = pl.skip ? 0 : pl.bl;
   for (int j = threadIdx.x; j < C; j += blockDim.x) {
     const float v = X[(size_t)b * C + j];
-    double p = amp * fabs((double)v) * x_scale;
+    double p = pl.amp * fabs((double)v) * pl.x_scale;
     p = (p < 1.0) ? p : 1.0;
-    if (skip) p = 0.0;
-    if (px_out) {
-      px_out[(size_t)b * C + j] = (v < 0.f) ? -p : p;
-    } else {
-      xw[(size_t)b * C + j] = skip ? 0u : train_word(v, p, bl, key, (uint32_t)j, seq, 0u);
-    }
+    if (pl.skip) p = 0.0;
+    px[(size_t)b * C + j] = (v < 0.f) ? -p : p;
   }
   for (int i = threadIdx.x; i < R; i += blockDim.x) {
     const float v = D[(size_t)b * R + i];
-    double p = amp * fabs((double)v) * d_scale;
+    double p = pl.amp * fabs((double)v) * pl.d_scale;
     p = (p < 1.0) ? p : 1.0;
-    if (skip) p = 0.0;
-    if (pd_out) {
-      pd_out[(size_t)b * R + i] = (v < 0.f) ? -p : p;
-    } else {
-      dw[(size_t)b * R + i] =
-          skip ? 0u : train_word(v, p, bl, key, (uint32_t)(row0 + i), seq, 0x80000000u);
-    }
+    if (pl.skip) p = 0.0;
+    pd[(size_t)b * R + i] = (v < 0.f) ? -p : p;
   }
 }
 
 void launch_trains(const Tile &t, const float *X, const float *D, int B, const float *lr_dev,
-                   float lr_scalar, const float *xm, const float *dm, uint64_t seq0, uint32_t *xw, uint32_t *dw,
-                   int32_t *bl, double *px, double *pd, bool deterministic) {
+                   float lr_scalar, const float *xm, const float *dm, uint64_t seq0,
+                   uint32_t *xw, uint32_t *dw, int ldb, int32_t *bl, double *px, double *pd,
+                   bool deterministic) {
   if (B <= 0) return;
-  trains_kernel<<<B, 256, 0, t.stream>>>(X, D, t.C, t.R, lr_dev, lr_scalar, xm, dm, t.cfg.device.dw_min,
-                                         t.cfg.update.bl, t.cfg.update.bl_management, t.k_upd,
-                                         seq0, t.row0, xw, dw, bl, deterministic ? px : nullptr,
-                                         deterministic ? pd : nullptr);
+  if (deterministic) {
+    probs_kernel<<<B, 256, 0, t.stream>>>(X, D, t.C, t.R, lr_dev, lr_scalar, xm, dm,
+                                          t.cfg.device.dw_min, t.cfg.update.bl,
+                                          t.cfg.update.bl_management, bl, px, pd);
+  } else {
+    dim3 grid((t.C + 31) / 32 + (t.R + 31) / 32, (B + 31) / 32);
+    trains_kernel<<<grid, 256, 0, t.stream>>>(X, D, t.C, t.R, B, lr_dev, lr_scalar, xm, dm,
+                                              t.cfg.device.dw_min, t.cfg.update.bl,
+                                              t.cfg.update.bl_management, t.k_upd, seq0, t.row0,
+                                              xw, dw, ldb, bl);
+  }
   count_launch();
   XB_CUDA(cudaGetLastError());
 }
@@ -293,22 +357,22 @@ __device__ __forceinline__ void normal4_fast(uint32_t c0, uint32_t c1, uint32_t 
 // Philox(k_c2c, (g0 + q, j, i, call)) with g0 the cell's running group count,
 // independent of launch geometry and of row sharding.
 constexpr int PULSE_WARPS = 16;          // rows per CTA
-constexpr int PULSE_QW = 16;             // stream words per lane
+constexpr int PULSE_QW = 32;             // stream words per lane
 constexpr int PULSE_CAP = PULSE_QW * 32; // pulses per lane per segment
 
 template <int LAW, bool NOISE>
 __global__ void __launch_bounds__(PULSE_WARPS * 32, 2) pulse_kernel(
     float *__restrict__ W, const float4 *__restrict__ P, int ld, int R, int C,
-    const uint32_t *__restrict__ xw, const uint32_t *__restrict__ dw, int B, int row0,
+    const uint32_t *__restrict__ xw, const uint32_t *__restrict__ dw, int ldb, int B, int row0,
     LawArgs la, RoundKeys rk, uint32_t call) {
-  __shared__ uint32_t qs[PULSE_WARPS][PULSE_QW][32];
+  extern __shared__ uint32_t qsm[]; // [PULSE_WARPS][PULSE_QW][32]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int j = blockIdx.x * 32 + lane;
   const int i = blockIdx.y * PULSE_WARPS + warp;
   if (i >= R) return; // warp-uniform: no block-level barriers below
   const bool valid = j < C;
   const size_t idx = (size_t)i * ld + j;
-  uint32_t *q = &qs[warp][0][lane];
+  uint32_t *q = qsm + warp * (PULSE_QW * 32) + lane;
 
   float w = 0.f;
   Cell cell{};
@@ -318,46 +382,47 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 2) pulse_kernel(
   }
   const Dir up = make_dir<LAW>(cell, true, la), dn = make_dir<LAW>(cell, false, la);
   const uint32_t jg = (uint32_t)j, ig = (uint32_t)(row0 + i);
-  const uint32_t *xcol = xw + (valid ? j : 0);
-  const uint32_t *drow = dw + i;
+  // line-major words: this lane's x line and the warp's d line, ldb % 8 == 0
+  const uint4 *xrow = reinterpret_cast<const uint4 *>(xw + (size_t)(valid ? j : 0) * ldb);
+  const uint4 *drow = reinterpret_cast<const uint4 *>(dw + (size_t)i * ldb);
   uint32_t g0 = 0;
 
   int b = 0;
   while (b < B) {
-    // ---------------- pre-pass: build this lane's pulse stream
+    // ---------------- pre-pass: append this lane's pulses, sample order
     uint32_t T = 0, acc = 0, qi = 0;
     while (b < B) {
-      uint32_t xv[8], dv[8];
-      const int nb = min(8, B - b);
+      const int b8 = b & ~7; // b is warp-uniform; loads stay 32-byte aligned
+      const uint4 xa = xrow[b8 >> 2], xb4 = xrow[(b8 >> 2) + 1];
+      const uint4 da = drow[b8 >> 2], db4 = drow[(b8 >> 2) + 1];
+      const uint32_t xv[8] = {xa.x, xa.y, xa.z, xa.w, xb4.x, xb4.y, xb4.z, xb4.w};
+      const uint32_t dv[8] = {da.x, da.y, da.z, da.w, db4.x, db4.y, db4.z, db4.w};
+      const int u0 = b - b8, nb = min(8, B - b8);
+      // fast path: a whole aligned block of 8 cannot overflow any lane's stream
+      const bool careful =
+          (u0 != 0) || (nb < 8) || __any_sync(0xffffffffu, T + 8u * 31u > (uint32_t)PULSE_CAP);
+      bool stop = false;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        xv[u] = (u < nb && valid) ? __ldg(xcol + (size_t)(b + u) * C) : 0u;
-        dv[u] = (u < nb) ? __ldg(drow + (size_t)(b + u) * R) : 0u;
-      }
-      bool full = false;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (u < nb && !full) {
-          const uint32_t c = xv[u] & dv[u] & 0x7fffffffu;
-          const uint32_t k = __popc(c);
-          if (__any_sync(0xffffffffu, T + k > PULSE_CAP)) {
-            full = true;
-          } else {
-            const uint32_t bits = ((int32_t)(xv[u] ^ dv[u]) >= 0) ? ((1u << k) - 1u) : 0u;
-            const uint32_t sh = T & 31u;
-            const uint64_t wide = (uint64_t)bits << sh;
-            acc |= (uint32_t)wide;
-            if (sh + k >= 32u) {
-              q[qi * 32] = acc;
-              ++qi;
-              acc = (uint32_t)(wide >> 32);
-            }
-            T += k;
-            ++b;
-          }
+        if (careful && (u < u0 || u >= nb)) continue;
+        const uint32_t xu = valid ? xv[u] : 0u;
+        const uint32_t k = __popc(xu & dv[u] & 0x7fffffffu);
+        if (careful && __any_sync(0xffffffffu, T + k > (uint32_t)PULSE_CAP)) {
+          stop = true;
+          break;
         }
+        const uint32_t bits = ((int32_t)(xu ^ dv[u]) >= 0) ? ((1u << k) - 1u) : 0u;
+        const uint64_t wide = (uint64_t)bits << (T & 31u);
+        acc |= (uint32_t)wide;
+        if ((T & 31u) + k >= 32u) {
+          q[qi * 32] = acc;
+          ++qi;
+          acc = (uint32_t)(wide >> 32);
+        }
+        T += k;
+        ++b;
       }
-      if (full) break;
+      if (stop) break;
     }
     if (T & 31u) q[qi * 32] = acc;
     const uint32_t maxT = __reduce_max_sync(0xffffffffu, T);
@@ -392,24 +457,32 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 2) pulse_kernel(
 }
 
 template <int LAW, bool NOISE>
-static void pulse_dispatch(Tile &t, const uint32_t *xw, const uint32_t *dw, int B, LawArgs la,
-                           uint32_t call) {
+static void pulse_dispatch(Tile &t, const uint32_t *xw, const uint32_t *dw, int ldb, int B,
+                           LawArgs la, uint32_t call) {
+  const int smem = PULSE_WARPS * PULSE_QW * 32 * (int)sizeof(uint32_t);
+  static bool configured = false;
+  if (!configured) {
+    XB_CUDA(cudaFuncSetAttribute(pulse_kernel<LAW, NOISE>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
   dim3 grid((t.C + 31) / 32, (t.R + PULSE_WARPS - 1) / PULSE_WARPS);
-  pulse_kernel<LAW, NOISE><<<grid, PULSE_WARPS * 32, 0, t.stream>>>(
-      t.W, t.P, t.ld, t.R, t.C, xw, dw, B, t.row0, la, round_keys(t.k_c2c), call);
+  pulse_kernel<LAW, NOISE><<<grid, PULSE_WARPS * 32, smem, t.stream>>>(
+      t.W, t.P, t.ld, t.R, t.C, xw, dw, ldb, B, t.row0, la, round_keys(t.k_c2c), call);
   count_launch();
   XB_CUDA(cudaGetLastError());
 }
 
-void launch_pulse(Tile &t, const uint32_t *xw, const uint32_t *dw, int B, uint32_t call_id) {
+void launch_pulse(Tile &t, const uint32_t *xw, const uint32_t *dw, int ldb, int B,
+                  uint32_t call_id) {
   if (B <= 0 || t.R == 0) return;
   const LawArgs la{(float)t.cfg.device.slope, (float)t.cfg.device.gamma,
                    (float)t.cfg.device.dw_min_std};
   const bool noise = t.cfg.device.dw_min_std > 0.0;
 #define XB_PULSE(K)                                                                        \
   case K:                                                                                  \
-    noise ? pulse_dispatch<K, true>(t, xw, dw, B, la, call_id)                             \
-          : pulse_dispatch<K, false>(t, xw, dw, B, la, call_id);                           \
+    noise ? pulse_dispatch<K, true>(t, xw, dw, ldb, B, la, call_id)                        \
+          : pulse_dispatch<K, false>(t, xw, dw, ldb, B, la, call_id);                      \
     break;
   switch (t.cfg.device.kind) {
     XB_PULSE(XB_CONSTANT_STEP)
