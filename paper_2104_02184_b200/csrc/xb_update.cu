@@ -383,48 +383,70 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 2) pulse_kernel(
   const Dir up = make_dir<LAW>(cell, true, la), dn = make_dir<LAW>(cell, false, la);
   const uint32_t jg = (uint32_t)j, ig = (uint32_t)(row0 + i);
   // line-major words: this lane's x line and the warp's d line, ldb % 8 == 0
-  const uint4 *xrow = reinterpret_cast<const uint4 *>(xw + (size_t)(valid ? j : 0) * ldb);
-  const uint4 *drow = reinterpret_cast<const uint4 *>(dw + (size_t)i * ldb);
+  const uint32_t *xline = xw + (size_t)(valid ? j : 0) * ldb;
+  const uint32_t *dline = dw + (size_t)i * ldb;
+  const uint32_t xmask = valid ? 0x7fffffffu : 0u; // idle lanes see no coincidences
+  const uint32_t q0 = (uint32_t)__cvta_generic_to_shared(q);
   uint32_t g0 = 0;
 
   int b = 0;
   while (b < B) {
     // ---------------- pre-pass: append this lane's pulses, sample order
-    uint32_t T = 0, acc = 0, qi = 0;
-    while (b < B) {
-      const int b8 = b & ~7; // b is warp-uniform; loads stay 32-byte aligned
-      const uint4 xa = xrow[b8 >> 2], xb4 = xrow[(b8 >> 2) + 1];
-      const uint4 da = drow[b8 >> 2], db4 = drow[(b8 >> 2) + 1];
-      const uint32_t xv[8] = {xa.x, xa.y, xa.z, xa.w, xb4.x, xb4.y, xb4.z, xb4.w};
-      const uint32_t dv[8] = {da.x, da.y, da.z, da.w, db4.x, db4.y, db4.z, db4.w};
-      const int u0 = b - b8, nb = min(8, B - b8);
-      // fast path: a whole aligned block of 8 cannot overflow any lane's stream
-      const bool careful =
-          (u0 != 0) || (nb < 8) || __any_sync(0xffffffffu, T + 8u * 31u > (uint32_t)PULSE_CAP);
-      bool stop = false;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (careful && (u < u0 || u >= nb)) continue;
-        const uint32_t xu = valid ? xv[u] : 0u;
-        const uint32_t k = __popc(xu & dv[u] & 0x7fffffffu);
-        if (careful && __any_sync(0xffffffffu, T + k > (uint32_t)PULSE_CAP)) {
-          stop = true;
-          break;
-        }
-        const uint32_t bits = ((int32_t)(xu ^ dv[u]) >= 0) ? ((1u << k) - 1u) : 0u;
-        const uint64_t wide = (uint64_t)bits << (T & 31u);
-        acc |= (uint32_t)wide;
-        if ((T & 31u) + k >= 32u) {
-          q[qi * 32] = acc;
-          ++qi;
-          acc = (uint32_t)(wide >> 32);
-        }
-        T += k;
-        ++b;
+    uint32_t T = 0, acc = 0, qa = q0;
+    auto append = [&](uint32_t xv, uint32_t dv) {
+      const uint32_t k = __popc(xv & dv & xmask);
+      const uint32_t bits = ((int32_t)(xv ^ dv) >= 0) ? ~(0xffffffffu << k) : 0u;
+      const uint32_t sh = T & 31u;
+      const uint64_t wide = (uint64_t)bits << sh;
+      acc |= (uint32_t)wide;
+      if (sh + k >= 32u) {
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(qa), "r"(acc));
+        qa += 128u;
+        acc = (uint32_t)(wide >> 32);
       }
-      if (stop) break;
+      T += k;
+    };
+    // fast path: aligned blocks of 8 samples, vector loads prefetched one block
+    // ahead; a block is taken only if it cannot overflow any lane's stream
+    if ((b & 7) == 0 && b + 8 <= B) {
+      const uint4 *xv4 = reinterpret_cast<const uint4 *>(xline);
+      const uint4 *dv4 = reinterpret_cast<const uint4 *>(dline);
+      uint4 xa = __ldg(xv4 + (b >> 2)), xb = __ldg(xv4 + (b >> 2) + 1);
+      uint4 da = __ldg(dv4 + (b >> 2)), db = __ldg(dv4 + (b >> 2) + 1);
+      while (true) {
+        if (__any_sync(0xffffffffu, T + 8u * 31u > (uint32_t)PULSE_CAP)) break;
+        const int bn = b + 8;
+        uint4 nxa = xa, nxb = xb, nda = da, ndb = db;
+        if (bn + 8 <= B) {
+          nxa = __ldg(xv4 + (bn >> 2));
+          nxb = __ldg(xv4 + (bn >> 2) + 1);
+          nda = __ldg(dv4 + (bn >> 2));
+          ndb = __ldg(dv4 + (bn >> 2) + 1);
+        }
+        append(xa.x, da.x);
+        append(xa.y, da.y);
+        append(xa.z, da.z);
+        append(xa.w, da.w);
+        append(xb.x, db.x);
+        append(xb.y, db.y);
+        append(xb.z, db.z);
+        append(xb.w, db.w);
+        b = bn;
+        if (b + 8 > B) break;
+        xa = nxa;
+        xb = nxb;
+        da = nda;
+        db = ndb;
+      }
     }
-    if (T & 31u) q[qi * 32] = acc;
+    // careful path, one sample at a time: the batch tail, or a stream near CAP
+    while (b < B) {
+      const uint32_t xv = __ldg(xline + b), dv = __ldg(dline + b);
+      if (__any_sync(0xffffffffu, T + __popc(xv & dv & xmask) > (uint32_t)PULSE_CAP)) break;
+      append(xv, dv);
+      ++b;
+    }
+    if (T & 31u) asm volatile("st.shared.u32 [%0], %1;" ::"r"(qa), "r"(acc));
     const uint32_t maxT = __reduce_max_sync(0xffffffffu, T);
     __syncwarp();
 
