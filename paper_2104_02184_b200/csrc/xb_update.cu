@@ -338,6 +338,69 @@ __device__ __forceinline__ void normal4_fast(uint32_t c0, uint32_t c1, uint32_t 
   box_muller_fast(c2, c3, z2, z3);
 }
 
+// ---- device laws in normalised coordinates for the pulse kernel.
+// u = (w - w_min) / (w_max - w_min) per cell, so the per-pulse clip to the
+// cell's [w_min, w_max] (device.cpp:75-76) is the free .SAT of the last FMA:
+//   u' = sat(u + (1 + std z) h(u)),  h = step / range  (device.cpp:51-74)
+// ConstantStep  h = +dw_up/range            | -dw_down/range
+// SoftBounds    h = (dw_up/w_max)(1 - u)    | -(dw_down/|w_min|) u
+// LinearStep    h = a_up + b_up u           | a_dn + b_dn u   (affine in u)
+// ExpStep       h = (dw_up/range) 2^(-g u)  | -(dw_down/range) 2^(-g (1 - u)),
+//               g = gamma log2(e)
+// Cells that receive no pulse keep their stored fp32 weight bit for bit.
+template <int LAW> struct NormCell {
+  float wmin, wmax, range;
+  float cu, cd; // per-direction scale
+  float bu, bd; // LinearStep slopes / ExpStep exponent scale in bu
+
+  __device__ __forceinline__ void init(float4 p, const LawArgs &la) {
+    wmin = p.w;
+    wmax = p.z;
+    range = p.z - p.w;
+    const float inv = 1.0f / range;
+    bu = bd = 0.f;
+    if (LAW == XB_CONSTANT_STEP) {
+      cu = p.x * inv;
+      cd = -p.y * inv;
+    } else if (LAW == XB_SOFT_BOUNDS) {
+      cu = p.x / p.z;
+      cd = p.y / p.w; // w_min < 0: dw_down / w_min = -dw_down / |w_min|
+    } else if (LAW == XB_LINEAR_STEP) {
+      cu = p.x * inv * (1.0f - la.slope * p.w);
+      bu = -p.x * la.slope;
+      cd = -p.y * inv * (1.0f + la.slope * p.w);
+      bd = -p.y * la.slope;
+    } else {
+      cu = p.x * inv;
+      cd = -p.y * inv;
+      bu = la.gamma * 1.4426950408889634f;
+    }
+  }
+  __device__ __forceinline__ float to_u(float w) const { return (w - wmin) / range; }
+  __device__ __forceinline__ float to_w(float u) const {
+    if (u >= 1.0f) return wmax;
+    if (u <= 0.0f) return wmin;
+    return fminf(fmaxf(fmaf(u, range, wmin), wmin), wmax);
+  }
+  // one pulse; f = 1 + std z (1 without c2c noise)
+  __device__ __forceinline__ float step(float u, float f, bool up) const {
+    float h;
+    if (LAW == XB_CONSTANT_STEP) {
+      h = up ? cu : cd;
+    } else if (LAW == XB_SOFT_BOUNDS) {
+      const float hu = fmaf(-cu, u, cu), hd = cd * u;
+      h = up ? hu : hd;
+    } else if (LAW == XB_LINEAR_STEP) {
+      const float hu = fmaf(bu, u, cu), hd = fmaf(bd, u, cd);
+      h = up ? hu : hd;
+    } else {
+      const float e = up ? -bu * u : fmaf(bu, u, -bu);
+      h = (up ? cu : cd) * ex2_approx(e);
+    }
+    return __saturatef(fmaf(f, h, u));
+  }
+};
+
 // ============================================================== K5: pulse
 // One warp = one row i of the tile and 32 consecutive columns (one cell per
 // lane); w and the cell's realization stay in registers for the whole batch.
@@ -374,13 +437,12 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 2) pulse_kernel(
   const size_t idx = (size_t)i * ld + j;
   uint32_t *q = qsm + warp * (PULSE_QW * 32) + lane;
 
-  float w = 0.f;
-  Cell cell{};
-  if (valid) {
-    w = W[idx];
-    cell = make_cell<LAW>(P[idx], la);
-  }
-  const Dir up = make_dir<LAW>(cell, true, la), dn = make_dir<LAW>(cell, false, la);
+  float w0 = 0.f;
+  NormCell<LAW> cell;
+  cell.init(valid ? P[idx] : make_float4(0.f, 0.f, 1.f, -1.f), la);
+  if (valid) w0 = W[idx];
+  float u = cell.to_u(w0);
+  uint32_t touched = 0;
   const uint32_t jg = (uint32_t)j, ig = (uint32_t)(row0 + i);
   // line-major words: this lane's x line and the warp's d line, ldb % 8 == 0
   const uint32_t *xline = xw + (size_t)(valid ? j : 0) * ldb;
@@ -459,23 +521,18 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 2) pulse_kernel(
         float z[4] = {0.f, 0.f, 0.f, 0.f};
         if (NOISE) normal4_rk(g0 + ((n0 + u4) >> 2), jg, ig, call, rk, z[0], z[1], z[2], z[3]);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const bool on = n0 + u4 + u < T;
-          const bool is_up = (word >> (u4 + u)) & 1u;
-          Dir d;
-          d.sdw = is_up ? up.sdw : dn.sdw;
-          d.sdws = is_up ? up.sdws : dn.sdws;
-          d.a = is_up ? up.a : dn.a;
-          d.b2 = is_up ? up.b2 : dn.b2;
-          const float wn = pulse<LAW, NOISE>(w, cell, d, z[u]);
-          w = on ? wn : w;
+        for (int v = 0; v < 4; ++v) {
+          const float f = NOISE ? fmaf(la.std, z[v], 1.0f) : 1.0f;
+          const float un = cell.step(u, f, (word >> (u4 + v)) & 1u);
+          if (n0 + u4 + v < T) u = un;
         }
       }
     }
     g0 += (T + 3u) >> 2;
+    touched |= T;
     __syncwarp();
   }
-  if (valid) W[idx] = w;
+  if (valid && touched) W[idx] = cell.to_w(u);
 }
 
 template <int LAW, bool NOISE>
