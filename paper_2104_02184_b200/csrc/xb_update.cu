@@ -338,66 +338,52 @@ __device__ __forceinline__ void normal4_fast(uint32_t c0, uint32_t c1, uint32_t 
   box_muller_fast(c2, c3, z2, z3);
 }
 
-// ---- device laws in normalised coordinates for the pulse kernel.
-// u = (w - w_min) / (w_max - w_min) per cell, so the per-pulse clip to the
-// cell's [w_min, w_max] (device.cpp:75-76) is the free .SAT of the last FMA:
-//   u' = sat(u + (1 + std z) h(u)),  h = step / range  (device.cpp:51-74)
-// ConstantStep  h = +dw_up/range            | -dw_down/range
-// SoftBounds    h = (dw_up/w_max)(1 - u)    | -(dw_down/|w_min|) u
-// LinearStep    h = a_up + b_up u           | a_dn + b_dn u   (affine in u)
-// ExpStep       h = (dw_up/range) 2^(-g u)  | -(dw_down/range) 2^(-g (1 - u)),
-//               g = gamma log2(e)
-// Cells that receive no pulse keep their stored fp32 weight bit for bit.
-template <int LAW> struct NormCell {
-  float wmin, wmax, range;
-  float cu, cd; // per-direction scale
-  float bu, bd; // LinearStep slopes / ExpStep exponent scale in bu
+// ---- device laws for the pulse kernel, folded per (cell, direction) into
+// affine constants (proj/src/device.cpp:51-76):
+//   h  = step of this pulse, signed    ConstantStep  +dw_up | -dw_down
+//                                      SoftBounds    dw_up - (dw_up/w_max) w | -dw_down + (dw_down/w_min) w
+//                                      LinearStep    dw_up - dw_up slope w | -dw_down - dw_down slope w
+//                                      ExpStep       dw_up 2^(-g (w - w_min)) | -dw_down 2^(-g (w_max - w))
+//   w' = clamp(w + (1 + std z) h, w_min, w_max)
+// so a pulse is two FMAs, a predicated select and two min/max (plus EX2 for
+// ExpStep), all in fp32 on the stored weight.
+template <int LAW> struct WCell {
+  float wmin, wmax;
+  float cu, cd; // constant parts (signed)
+  float bu, bd; // slopes in w (ExpStep: exponent offsets)
+  float g;      // ExpStep exponent scale gamma log2(e) / range
 
   __device__ __forceinline__ void init(float4 p, const LawArgs &la) {
     wmin = p.w;
     wmax = p.z;
-    range = p.z - p.w;
-    const float inv = 1.0f / range;
-    bu = bd = 0.f;
-    if (LAW == XB_CONSTANT_STEP) {
-      cu = p.x * inv;
-      cd = -p.y * inv;
-    } else if (LAW == XB_SOFT_BOUNDS) {
-      cu = p.x / p.z;
-      cd = p.y / p.w; // w_min < 0: dw_down / w_min = -dw_down / |w_min|
+    cu = p.x;
+    cd = -p.y;
+    bu = bd = g = 0.f;
+    if (LAW == XB_SOFT_BOUNDS) {
+      bu = -p.x / p.z;
+      bd = p.y / p.w;
     } else if (LAW == XB_LINEAR_STEP) {
-      cu = p.x * inv * (1.0f - la.slope * p.w);
       bu = -p.x * la.slope;
-      cd = -p.y * inv * (1.0f + la.slope * p.w);
       bd = -p.y * la.slope;
-    } else {
-      cu = p.x * inv;
-      cd = -p.y * inv;
-      bu = la.gamma * 1.4426950408889634f;
+    } else if (LAW == XB_EXP_STEP) {
+      g = la.gamma / (p.z - p.w) * 1.4426950408889634f;
+      bu = g * p.w;  // up exponent  -g w + g w_min
+      bd = -g * p.z; // down exponent g w - g w_max
     }
   }
-  __device__ __forceinline__ float to_u(float w) const { return (w - wmin) / range; }
-  __device__ __forceinline__ float to_w(float u) const {
-    if (u >= 1.0f) return wmax;
-    if (u <= 0.0f) return wmin;
-    return fminf(fmaxf(fmaf(u, range, wmin), wmin), wmax);
-  }
   // one pulse; f = 1 + std z (1 without c2c noise)
-  __device__ __forceinline__ float step(float u, float f, bool up) const {
+  __device__ __forceinline__ float step(float w, float f, bool up) const {
     float h;
     if (LAW == XB_CONSTANT_STEP) {
       h = up ? cu : cd;
-    } else if (LAW == XB_SOFT_BOUNDS) {
-      const float hu = fmaf(-cu, u, cu), hd = cd * u;
-      h = up ? hu : hd;
-    } else if (LAW == XB_LINEAR_STEP) {
-      const float hu = fmaf(bu, u, cu), hd = fmaf(bd, u, cd);
-      h = up ? hu : hd;
-    } else {
-      const float e = up ? -bu * u : fmaf(bu, u, -bu);
+    } else if (LAW == XB_EXP_STEP) {
+      const float e = up ? fmaf(-g, w, bu) : fmaf(g, w, bd);
       h = (up ? cu : cd) * ex2_approx(e);
+    } else {
+      const float hu = fmaf(bu, w, cu), hd = fmaf(bd, w, cd);
+      h = up ? hu : hd;
     }
-    return __saturatef(fmaf(f, h, u));
+    return fminf(fmaxf(fmaf(f, h, w), wmin), wmax);
   }
 };
 
@@ -437,12 +423,10 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 2) pulse_kernel(
   const size_t idx = (size_t)i * ld + j;
   uint32_t *q = qsm + warp * (PULSE_QW * 32) + lane;
 
-  float w0 = 0.f;
-  NormCell<LAW> cell;
+  float w = 0.f;
+  WCell<LAW> cell;
   cell.init(valid ? P[idx] : make_float4(0.f, 0.f, 1.f, -1.f), la);
-  if (valid) w0 = W[idx];
-  float u = cell.to_u(w0);
-  uint32_t touched = 0;
+  if (valid) w = W[idx];
   const uint32_t jg = (uint32_t)j, ig = (uint32_t)(row0 + i);
   // line-major words: this lane's x line and the warp's d line, ldb % 8 == 0
   const uint32_t *xline = xw + (size_t)(valid ? j : 0) * ldb;
@@ -523,16 +507,15 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 2) pulse_kernel(
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
           const float f = NOISE ? fmaf(la.std, z[v], 1.0f) : 1.0f;
-          const float un = cell.step(u, f, (word >> (u4 + v)) & 1u);
-          if (n0 + u4 + v < T) u = un;
+          const float wn = cell.step(w, f, (word >> (u4 + v)) & 1u);
+          if (n0 + u4 + v < T) w = wn;
         }
       }
     }
     g0 += (T + 3u) >> 2;
-    touched |= T;
     __syncwarp();
   }
-  if (valid && touched) W[idx] = cell.to_w(u);
+  if (valid) W[idx] = w;
 }
 
 template <int LAW, bool NOISE>
