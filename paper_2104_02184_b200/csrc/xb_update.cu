@@ -322,12 +322,28 @@ __device__ __forceinline__ void box_muller_fast(uint32_t a, uint32_t b, float &z
   z1 = r * s;
 }
 
-__device__ __forceinline__ void normal4_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
-                                           const RoundKeys &rk, float &z0, float &z1, float &z2,
-                                           float &z3) {
+// eight normals per Philox call from 16-bit uniforms (half-LSB centred):
+// the radius then reaches sqrt(2 ln 2^17) = 4.9 sigma, a tail mass of 1e-6
+// that the c2c write-noise statistics cannot resolve
+__device__ __forceinline__ void box_muller16(uint32_t a, float &z0, float &z1) {
+  const float u = fmaf((float)(a & 0xffffu), 1.52587890625e-05f, 7.62939453125e-06f);
+  const float th = fmaf((float)(a >> 16), 9.587379924285257e-05f, -3.1415446284412245f);
+  float l, r, s, c;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(u));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(l * -1.3862943611198906f)); // -2 ln u
+  asm("sin.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(th));
+  asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(th));
+  z0 = r * c;
+  z1 = r * s;
+}
+
+__device__ __forceinline__ void normal8_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                           const RoundKeys &rk, float *z) {
   philox10_rk(c0, c1, c2, c3, rk);
-  box_muller_fast(c0, c1, z0, z1);
-  box_muller_fast(c2, c3, z2, z3);
+  box_muller16(c0, z[0], z[1]);
+  box_muller16(c1, z[2], z[3]);
+  box_muller16(c2, z[4], z[5]);
+  box_muller16(c3, z[6], z[7]);
 }
 
 __device__ __forceinline__ void normal4_fast(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
@@ -402,7 +418,7 @@ template <int LAW> struct WCell {
 // Lanes therefore wait only on the longest stream of the segment, and the
 // per-cell pulse order is exactly the reference's (sample order; one
 // direction per sample; pulses of a sample are interchangeable).
-// c2c normal #(4q + r) of a cell's segment is element r of
+// c2c normal #(8q + r) of a cell's segment is element r of the 8 normals of
 // Philox(k_c2c, (g0 + q, j, i, call)) with g0 the cell's running group count,
 // independent of launch geometry and of row sharding.
 constexpr int PULSE_WARPS = 16;          // rows per CTA
@@ -500,19 +516,19 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 2) pulse_kernel(
     for (uint32_t n0 = 0; n0 < maxT; n0 += 32) {
       const uint32_t word = q[(n0 >> 5) * 32];
 #pragma unroll
-      for (int u4 = 0; u4 < 32; u4 += 4) {
+      for (int u4 = 0; u4 < 32; u4 += 8) {
         if (n0 + u4 >= maxT) break;
-        float z[4] = {0.f, 0.f, 0.f, 0.f};
-        if (NOISE) normal4_rk(g0 + ((n0 + u4) >> 2), jg, ig, call, rk, z[0], z[1], z[2], z[3]);
+        float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (NOISE) normal8_rk(g0 + ((n0 + u4) >> 3), jg, ig, call, rk, z);
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
+        for (int v = 0; v < 8; ++v) {
           const float f = NOISE ? fmaf(la.std, z[v], 1.0f) : 1.0f;
           const float wn = cell.step(w, f, (word >> (u4 + v)) & 1u);
           if (n0 + u4 + v < T) w = wn;
         }
       }
     }
-    g0 += (T + 3u) >> 2;
+    g0 += (T + 7u) >> 3;
     __syncwarp();
   }
   if (valid) W[idx] = w;
