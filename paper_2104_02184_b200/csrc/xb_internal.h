@@ -105,6 +105,11 @@ void launch_temporal_xi(Tile &t);
 void launch_program(Tile &t, const float *target_dev, const xb_inference_model &m, Key key);
 void launch_drift(Tile &t, double ratio);
 
+// ---- tcgen05 contraction (xb_mvm_tc.cu) ----
+int tc_splits(int M, int K);
+int tc_used_splits(int K, int splits);
+void tc_gemm_forward(Tile &t, const float *Xt, int ldt, int B, float *part, int splits);
+
 // ---- noisy MVM (xb_mvm.cu) ----
 // forward: Y[b][i] = alpha_b * ADC(sum_j W[i][j] x~[b][j] + noise), i local rows
 void mvm_forward(Tile &t, const float *dX, int B, float *dY, const IoDev &io, Key key,

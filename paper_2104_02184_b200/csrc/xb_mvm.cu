@@ -172,16 +172,18 @@ __global__ void __launch_bounds__(256) mvm_simt_kernel(const float *__restrict__
 
 // --------------------------------------------------------------- epilogue
 __global__ void __launch_bounds__(256) epilogue_kernel(const float *__restrict__ acc, int lda,
-                                                        int M, int o0, float *__restrict__ Y,
-                                                        int ldy, SampleState *__restrict__ st,
-                                                        IoDev io, Key key, uint64_t seq0,
+                                                        int nsplit, size_t split_stride, int M,
+                                                        int o0, float *__restrict__ Y, int ldy,
+                                                        SampleState *__restrict__ st, IoDev io,
+                                                        Key key, uint64_t seq0,
                                                         int *__restrict__ sat, int first_pass) {
   const int b = blockIdx.y;
   const SampleState s = st[b];
   if (!first_pass && !s.active) return;
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= M) return;
-  const float a = acc[(size_t)b * lda + o];
+  float a = acc[(size_t)b * lda + o];
+  for (int sp = 1; sp < nsplit; ++sp) a += acc[sp * split_stride + (size_t)b * lda + o];
   if (io.perfect) {
     Y[(size_t)b * ldy + o] = a;
     return;
@@ -228,9 +230,9 @@ struct MvmScratch {
   int *sat;
 };
 
-MvmScratch carve(Tile &t, int B, int K, int M) {
+MvmScratch carve(Tile &t, int B, int K, int M, int nsplit) {
   const size_t xt_b = (size_t)B * K * sizeof(float);
-  const size_t acc_b = (size_t)B * M * sizeof(float);
+  const size_t acc_b = (size_t)nsplit * B * M * sizeof(float);
   const size_t st_b = (size_t)B * sizeof(SampleState);
   const size_t sat_b = (size_t)B * sizeof(int);
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
@@ -259,7 +261,11 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io, Key
   const int K = TRANS ? t.R : t.C; // contraction length
   const int M = TRANS ? t.C : t.R; // outputs
   if (B <= 0) return;
-  MvmScratch s = carve(t, B, K, M);
+  // tensor-core contraction for the forward direction at TF32 (B >= 16);
+  // the fp32 SIMT kernel otherwise (exact-fp32 parity mode, tiny batches)
+  const bool tc = !TRANS && t.cfg.mvm_precision == XB_MVM_TF32 && B >= 16 && !skip_epilogue;
+  const int splits = tc ? tc_used_splits(K, tc_splits(M, K)) : 1;
+  MvmScratch s = carve(t, B, K, M, splits);
   if (io.bm) XB_CUDA(cudaMemsetAsync(s.sat, 0, sizeof(int) * B, t.stream));
   const int passes = io.bm ? 1 + io.bm_max_iter : 1;
   for (int pass = 0; pass < passes; ++pass) {
@@ -267,15 +273,22 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io, Key
     prep_kernel<<<B, 256, 0, t.stream>>>(dIn, K, K, s.xt, K, s.st, io, key, seq0, first, amax_in);
     count_launch();
     XB_CUDA(cudaGetLastError());
-    gemm<TRANS>(t, s, M, K, B, first);
+    int nsplit = 1;
+    if (tc && first) {
+      tc_gemm_forward(t, s.xt, K, B, s.acc, splits);
+      nsplit = splits;
+    } else {
+      gemm<TRANS>(t, s, M, K, B, first);
+    }
     if (skip_epilogue) {
       XB_CUDA(cudaMemcpyAsync(dPartial, s.acc, sizeof(float) * (size_t)B * M,
                               cudaMemcpyDeviceToDevice, t.stream));
       return;
     }
     dim3 eg((M + 255) / 256, B);
-    epilogue_kernel<<<eg, 256, 0, t.stream>>>(s.acc, M, M, TRANS ? 0 : t.row0, dOut, M, s.st, io,
-                                              key, seq0, s.sat, first);
+    epilogue_kernel<<<eg, 256, 0, t.stream>>>(s.acc, M, nsplit, (size_t)B * M, M,
+                                              TRANS ? 0 : t.row0, dOut, M, s.st, io, key, seq0,
+                                              s.sat, first);
     count_launch();
     XB_CUDA(cudaGetLastError());
     if (io.bm && pass + 1 < passes) {

@@ -1,0 +1,285 @@
+// xb_mvm_tc.cu -- the MVM contraction on the 5th-generation tensor cores.
+//
+// acc[s][b][o] = sum_{k in split s} W[o][k] x~[b][k]  (forward, both operands K-major)
+//
+// One CTA = one 128-row tile of W (M) x all BN <= 256 samples (N) x one
+// K-split.  TMA (cp.async.bulk.tensor, 128-byte swizzle) streams 32-wide K
+// blocks of W and x~ into a 4-stage shared-memory ring; a single thread
+// issues tcgen05.mma.kind::tf32 (M=128, N=BN, K=8, four per stage) into a
+// TMEM accumulator of BN fp32 columns; mbarriers chain TMA -> MMA -> smem
+// release (tcgen05.commit) and MMA -> epilogue.  The four warps then drain
+// TMEM with tcgen05.ld (warp w owns accumulator lanes 32w..32w+31 = output
+// rows) and store the fp32 partial sums; the converter/noise epilogue
+// (xb_mvm.cu) reduces the K-splits and applies sigma_w, sigma_out, ADC, alpha.
+//
+// W is row-major [R][ld] fp32, x~ is [B][K] fp32 -- the kernel reads the same
+// bytes the SIMT path reads; the tensor core consumes them as TF32.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "xb_internal.h"
+
+namespace xb {
+
+namespace {
+
+constexpr int TC_BM = 128;
+constexpr int TC_BK = 32; // fp32 elements per 128-byte swizzle row
+constexpr int TC_STAGES = 4;
+constexpr int TC_MAX_BN = 256;
+constexpr int TC_A_BYTES = TC_BM * TC_BK * 4;     // 16 KB
+constexpr int TC_B_BYTES = TC_MAX_BN * TC_BK * 4; // 32 KB (max)
+constexpr int TC_SMEM = TC_STAGES * (TC_A_BYTES + TC_B_BYTES) + 1024 /*align*/ + 256 /*bars*/;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "XB_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra XB_WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row groups
+// 1024 bytes apart (SBO), sm_100 descriptor version 1.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);  // start address
+  d |= (uint64_t)1u << 16;                  // leading byte offset (unused for SW128 K-major)
+  d |= (uint64_t)(1024u >> 4) << 32;        // stride byte offset
+  d |= (uint64_t)1u << 46;                  // descriptor version (sm_100)
+  d |= (uint64_t)2u << 61;                  // SWIZZLE_128B
+  return d;
+}
+
+// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, M=128, N=bn
+__host__ __device__ __forceinline__ uint32_t idesc_tf32(int bn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(bn >> 3) << 17) |
+         ((uint32_t)(TC_BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+
+#define XB_TMEM_LD32(taddr, r)                                                                  \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 "                                       \
+               "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"                       \
+               "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"      \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),        \
+                 "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),      \
+                 "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]),  \
+                 "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),  \
+                 "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),  \
+                 "=r"(r[30]), "=r"(r[31])                                                      \
+               : "r"(taddr))
+
+__global__ void __launch_bounds__(128, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                   int M, int K, int B, int bn, int kblocks_per_split, float *__restrict__ part,
+                   int ldp, size_t split_stride) {
+  extern __shared__ uint8_t smem_raw[];
+  // 1024-byte alignment for the 128-byte swizzle atoms
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t *sa = smem;
+  uint8_t *sb = smem + TC_STAGES * TC_A_BYTES;
+  uint64_t *bars = (uint64_t *)(sb + TC_STAGES * TC_B_BYTES);
+  uint32_t *tmem_slot = (uint32_t *)(bars + 2 * TC_STAGES + 1);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + TC_STAGES),
+                 done = smem_u32(bars + 2 * TC_STAGES);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * TC_BM;
+  const int split = blockIdx.y;
+  const int kb0 = split * kblocks_per_split;
+  const int nkb = min(kblocks_per_split, (K + TC_BK - 1) / TC_BK - kb0);
+
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_b)) : "memory");
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) { // TMEM: 256 fp32 columns x 128 lanes (the whole accumulator)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TC_MAX_BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t b_bytes = (uint32_t)bn * TC_BK * 4;
+
+  if (warp == 0 && lane == 0 && nkb > 0) {
+    // ---------------- TMA producer
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % TC_STAGES;
+      const uint32_t ph = (uint32_t)(kb / TC_STAGES) & 1u;
+      mbar_wait(empty0 + 8 * s, ph ^ 1u);
+      mbar_expect_tx(full0 + 8 * s, TC_A_BYTES + b_bytes);
+      const int kk = (kb0 + kb) * TC_BK;
+      tma_load_2d(smem_u32(sa + s * TC_A_BYTES), &tm_a, full0 + 8 * s, kk, m0);
+      tma_load_2d(smem_u32(sb + s * TC_B_BYTES), &tm_b, full0 + 8 * s, kk, 0);
+    }
+  } else if (warp == 1 && lane == 0 && nkb > 0) {
+    // ---------------- MMA issuer (one thread)
+    const uint32_t idesc = idesc_tf32(bn);
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % TC_STAGES;
+      const uint32_t ph = (uint32_t)(kb / TC_STAGES) & 1u;
+      mbar_wait(full0 + 8 * s, ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint64_t da = umma_desc_sw128(smem_u32(sa + s * TC_A_BYTES));
+      const uint64_t db = umma_desc_sw128(smem_u32(sb + s * TC_B_BYTES));
+#pragma unroll
+      for (int k = 0; k < TC_BK / 8; ++k) // 8 tf32 = 32 bytes per MMA: +2 in the 16-byte units
+        mma_tf32(tmem, da + 2u * k, db + 2u * k, idesc, (kb | k) != 0);
+      mma_commit(empty0 + 8 * s); // smem stage free once these MMAs retire
+    }
+    mma_commit(done);
+  }
+  __syncwarp();
+
+  // ---------------- epilogue: TMEM -> registers -> partial sums
+  if (nkb > 0) {
+    mbar_wait(done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
+  const int o = m0 + warp * 32 + lane;
+  float *dst = part + (size_t)split * split_stride;
+  for (int c0 = 0; c0 < bn; c0 += 32) {
+    uint32_t r[32];
+    XB_TMEM_LD32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, r);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (o < M) {
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const int b = c0 + c;
+        if (b < B) dst[(size_t)b * ldp + o] = nkb > 0 ? __uint_as_float(r[c]) : 0.f;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TC_MAX_BN));
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  });
+  if (!fn) raise("cuTensorMapEncodeTiled unavailable (driver too old for TMA)");
+  return fn;
+}
+
+// 2-D fp32 tensor map over a row-major [rows][cols] array with row stride ld
+// floats; box = [box_rows][32 floats], 128-byte swizzle, OOB zero fill
+CUtensorMap make_map(const float *base, int rows, int cols, int ld, int box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)base, dims, strides,
+                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) raise("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+} // namespace
+
+int tc_splits(int M, int K) {
+  const int mt = (M + TC_BM - 1) / TC_BM;
+  const int kbs = (K + TC_BK - 1) / TC_BK;
+  int s = std::max(1, 148 / std::max(mt, 1));
+  s = std::min(s, std::max(1, kbs / 4)); // keep >= 4 K-blocks per split
+  return std::max(1, std::min(s, 16));
+}
+
+// forward contraction on tcgen05: part[s][b][o] (split stride B x M)
+void tc_gemm_forward(Tile &t, const float *Xt, int ldt, int B, float *part, int splits) {
+  const int M = t.R, K = t.C;
+  static bool configured = false;
+  if (!configured) {
+    XB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 TC_SMEM));
+    configured = true;
+  }
+  const int kbs = (K + TC_BK - 1) / TC_BK;
+  const int per = (kbs + splits - 1) / splits;
+  const int used = (kbs + per - 1) / per;
+  for (int n0 = 0; n0 < B; n0 += TC_MAX_BN) {
+    const int nb = std::min(TC_MAX_BN, B - n0);
+    const int bn = std::max(16, (nb + 15) / 16 * 16);
+    const CUtensorMap ma = make_map(t.W, M, K, t.ld, TC_BM);
+    const CUtensorMap mb = make_map(Xt + (size_t)n0 * ldt, nb, K, ldt, bn);
+    dim3 grid((M + TC_BM - 1) / TC_BM, used);
+    // partial sums of this N slab land at part + n0 rows, split stride B x M
+    tc_gemm_kernel<<<grid, 128, TC_SMEM, t.stream>>>(ma, mb, M, K, nb, bn, per,
+                                                     part + (size_t)n0 * M, M, (size_t)B * M);
+    count_launch();
+    XB_CUDA(cudaGetLastError());
+  }
+  (void)used;
+}
+
+int tc_used_splits(int K, int splits) {
+  const int kbs = (K + TC_BK - 1) / TC_BK;
+  const int per = (kbs + splits - 1) / splits;
+  return (kbs + per - 1) / per;
+}
+
+} // namespace xb

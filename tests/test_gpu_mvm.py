@@ -188,3 +188,49 @@ def test_forward_noisy_read_noise():
     var = 0.05 ** 2 * float(x.astype(np.float64) @ x)
     assert np.all(np.abs(Y.mean(axis=0) - exact) < 5 * np.sqrt(var / 4000))
     assert abs(Y.var(axis=0).mean() / var - 1) < 0.05
+
+
+@pytest.mark.parametrize("shape,B", [((256, 256), 16), ((300, 520), 37), ((512, 4096), 256),
+                                     ((128, 64), 300)])
+def test_tcgen05_tf32_forward(shape, B):
+    """The tcgen05 kind::tf32 contraction (TMA + TMEM, split-K) against the fp32
+    SIMT path on the same weights: TF32 keeps 10 mantissa bits, so outputs
+    agree to ~1e-3 of max(1, |y|) and must NOT be bit-identical (proof that the
+    tensor-core path ran)."""
+    d_out, d_in = shape
+    io = xb.perfect_io()
+    W = np.random.default_rng(3).uniform(-0.5, 0.5, shape).astype(np.float32)
+    X = np.random.default_rng(4).uniform(-1, 1, (B, d_in)).astype(np.float32)
+    ref = X.astype(np.float64) @ W.T.astype(np.float64)
+    out = {}
+    for prec in (xb.MVM_FP32, xb.MVM_TF32):
+        t = xb.AnalogTile(d_out, d_in, cfg_io(io, io, prec), 5)
+        t.set_weights(W)
+        out[prec] = t.forward(X).astype(np.float64)
+    err32 = np.abs(out[xb.MVM_FP32] - ref) / np.maximum(1, np.abs(ref))
+    errtf = np.abs(out[xb.MVM_TF32] - ref) / np.maximum(1, np.abs(ref))
+    assert err32.max() < 1e-5
+    assert errtf.max() < 4e-3, errtf.max()
+    assert not np.array_equal(out[xb.MVM_FP32], out[xb.MVM_TF32])
+
+
+def test_tcgen05_noisy_forward_statistics():
+    """Default IO (DAC 7 b, ADC 9 b, sigma_out 0.06, abs-max) on the tensor-core
+    path: mean over repeats matches the fp64 noisy-free reference within the
+    ADC/noise budget."""
+    io = xb.default_io()
+    W = np.random.default_rng(5).uniform(-0.1, 0.1, (256, 1024)).astype(np.float32)
+    x = np.random.default_rng(6).uniform(-1, 1, 1024).astype(np.float32)
+    t = xb.AnalogTile(256, 1024, cfg_io(io, io, xb.MVM_TF32, bound=1.0), 8)
+    t.set_weights(W)
+    Y = t.forward(np.tile(x, (512, 1))).astype(np.float64)
+    alpha = np.abs(x).max()
+    xq = np.array([O_quant(v / alpha) for v in x])
+    exact = alpha * (W.astype(np.float64) @ xq)
+    se = Y.std(axis=0) / np.sqrt(512)
+    assert np.mean(np.abs(Y.mean(axis=0) - exact) < 5 * se + 2e-3) > 0.99
+    assert abs(Y.std(axis=0).mean() / (alpha * np.sqrt(0.06 ** 2 + (24 / 512) ** 2 / 12)) - 1) < 0.1
+
+
+def O_quant(v, bound=1.0, bits=7):
+    return oracle.load("restatement").quantize(v, bound, bits)
