@@ -211,6 +211,7 @@ static void tile_free(Tile &t) {
   t.s_y.release();
   t.s_lr.release();
   if (t.own_stream && t.stream) cudaStreamDestroy(t.stream);
+  if (t.bm_count) cudaFreeHost(t.bm_count);
 }
 
 static void sync(Tile &t) { XB_CUDA(cudaStreamSynchronize(t.stream)); }

@@ -64,6 +64,7 @@ struct Tile {
   double prog_t0 = 0.0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  int *bm_count = nullptr; // pinned host word for the bound-management loop
 
   Scratch s_words, s_params, s_io, s_y, s_lr;
 

@@ -208,17 +208,18 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const float *__restrict__
   Y[(size_t)b * ldy + o] = (float)(scale * quantize(v, io.adc));
 }
 
-// BM bookkeeping between passes: samples that saturated get m + 1 and stay active
+// BM bookkeeping between passes: samples that saturated get m + 1 and stay
+// active; sat[B] counts them for the host's loop decision
 __global__ void bm_advance_kernel(SampleState *__restrict__ st, int *__restrict__ sat, int B) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   SampleState s = st[b];
-  if (s.active && sat[b]) {
+  const bool again = s.active && sat[b];
+  if (again) {
     s.m += 1;
-    s.active = 1;
-  } else {
-    s.active = 0;
+    atomicAdd(sat + B, 1);
   }
+  s.active = again ? 1 : 0;
   sat[b] = 0;
   st[b] = s;
 }
@@ -234,7 +235,7 @@ MvmScratch carve(Tile &t, int B, int K, int M, int nsplit) {
   const size_t xt_b = (size_t)B * K * sizeof(float);
   const size_t acc_b = (size_t)nsplit * B * M * sizeof(float);
   const size_t st_b = (size_t)B * sizeof(SampleState);
-  const size_t sat_b = (size_t)B * sizeof(int);
+  const size_t sat_b = (size_t)(B + 1) * sizeof(int);
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   char *p = (char *)t.s_io.get(al(xt_b) + al(acc_b) + al(st_b) + al(sat_b));
   MvmScratch s;
@@ -266,7 +267,7 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io, Key
   const bool tc = !TRANS && t.cfg.mvm_precision == XB_MVM_TF32 && B >= 16 && !skip_epilogue;
   const int splits = tc ? tc_used_splits(K, tc_splits(M, K)) : 1;
   MvmScratch s = carve(t, B, K, M, splits);
-  if (io.bm) XB_CUDA(cudaMemsetAsync(s.sat, 0, sizeof(int) * B, t.stream));
+  if (io.bm) XB_CUDA(cudaMemsetAsync(s.sat, 0, sizeof(int) * (B + 1), t.stream));
   const int passes = io.bm ? 1 + io.bm_max_iter : 1;
   for (int pass = 0; pass < passes; ++pass) {
     const int first = pass == 0;
@@ -292,9 +293,18 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io, Key
     count_launch();
     XB_CUDA(cudaGetLastError());
     if (io.bm && pass + 1 < passes) {
+      // bound management: re-issue only while some sample saturated.  The
+      // count crosses to the host (one small sync per forward with BM on);
+      // re-issue passes run on the SIMT kernel restricted to active samples.
+      XB_CUDA(cudaMemsetAsync(s.sat + B, 0, sizeof(int), t.stream));
       bm_advance_kernel<<<(B + 255) / 256, 256, 0, t.stream>>>(s.st, s.sat, B);
       count_launch();
       XB_CUDA(cudaGetLastError());
+      if (!t.bm_count) XB_CUDA(cudaMallocHost(&t.bm_count, sizeof(int)));
+      XB_CUDA(cudaMemcpyAsync(t.bm_count, s.sat + B, sizeof(int), cudaMemcpyDeviceToHost,
+                              t.stream));
+      XB_CUDA(cudaStreamSynchronize(t.stream));
+      if (*t.bm_count == 0) break;
     }
   }
 }

@@ -207,10 +207,14 @@ def test_tcgen05_tf32_forward(shape, B):
         t = xb.AnalogTile(d_out, d_in, cfg_io(io, io, prec), 5)
         t.set_weights(W)
         out[prec] = t.forward(X).astype(np.float64)
-    err32 = np.abs(out[xb.MVM_FP32] - ref) / np.maximum(1, np.abs(ref))
-    errtf = np.abs(out[xb.MVM_TF32] - ref) / np.maximum(1, np.abs(ref))
-    assert err32.max() < 1e-5
-    assert errtf.max() < 4e-3, errtf.max()
+    # error relative to the dot-product scale ||w_i|| ||x_b|| (Cauchy-Schwarz bound of |y|):
+    # fp32 accumulation over K = 4096 terms cannot meet 1e-5 of max(1, |y|) near y = 0
+    scale = np.linalg.norm(X.astype(np.float64), axis=1)[:, None] * \
+        np.linalg.norm(W.astype(np.float64), axis=1)[None, :]
+    err32 = np.abs(out[xb.MVM_FP32] - ref) / scale
+    errtf = np.abs(out[xb.MVM_TF32] - ref) / scale
+    assert err32.max() < 1e-5, err32.max()
+    assert errtf.max() < 2e-3, errtf.max()
     assert not np.array_equal(out[xb.MVM_FP32], out[xb.MVM_TF32])
 
 
@@ -234,3 +238,52 @@ def test_tcgen05_noisy_forward_statistics():
 
 def O_quant(v, bound=1.0, bits=7):
     return oracle.load("restatement").quantize(v, bound, bits)
+
+
+def bm_forward_ref(W, x, io, O):
+    """Restatement of the additive bound-management rule (no reference symbol;
+    DESIGN.md): re-issue with the input halved until no pre-ADC output reaches
+    output_bound or bm_max_iter is hit; y = alpha 2^m ADC(acc_m)."""
+    alpha = np.abs(x).max()
+    if alpha == 0:
+        return np.zeros(W.shape[0])
+    if io.noise_management != xb.NM_ABS_MAX:
+        alpha = 1.0
+    m = 0
+    while True:
+        xt = np.array([O.quantize(v / (alpha * 2.0 ** m), io.input_bound, io.dac_bits) for v in x])
+        acc = W.astype(np.float64) @ xt
+        if np.abs(acc).max() >= io.output_bound and m < io.bm_max_iter:
+            m += 1
+            continue
+        return alpha * 2.0 ** m * np.array([O.quantize(a, io.output_bound, io.adc_bits)
+                                            for a in acc])
+
+
+@pytest.mark.parametrize("prec", [xb.MVM_FP32, xb.MVM_TF32])
+def test_bound_management_reissue(prec):
+    """Saturating samples are re-issued at half input scale until the ADC no
+    longer clips; non-saturating samples are untouched."""
+    O = oracle.load("restatement")
+    io = xb.default_io()
+    io.sigma_out = 0.0
+    io.bound_management, io.bm_max_iter = xb.BM_ITERATIVE, 5
+    W = np.full((24, 64), 0.9, np.float32)
+    W[::2] *= -0.25
+    X = np.random.default_rng(3).uniform(0.2, 1.0, (20, 64)).astype(np.float32)
+    X[::3] *= 0.05  # tiny samples still saturate: abs-max rescales them to full range
+    X[1::4] = np.random.default_rng(4).uniform(-1, 1, (len(X[1::4]), 64))  # cancellations
+    t = xb.AnalogTile(24, 64, cfg_io(io, io, prec, bound=1.0), 2)
+    t.set_weights(W)
+    Y = t.forward(X)
+    for b in range(X.shape[0]):
+        ref = bm_forward_ref(W, X[b].astype(np.float64), io, O)
+        lsb = 2 * 12.0 / 512 * np.abs(X[b]).max() * 2 ** 5
+        assert np.all(np.abs(Y[b] - ref) <= lsb), (b, Y[b][:4], ref[:4])
+    # without BM the same tile clips at alpha * 12
+    io.bound_management = xb.BM_NONE
+    t2 = xb.AnalogTile(24, 64, cfg_io(io, io, prec, bound=1.0), 2)
+    t2.set_weights(W)
+    Y2 = t2.forward(X)
+    assert np.abs(Y2).max() <= 12.0 * np.abs(X).max() + 1e-5
+    assert np.abs(Y).max() > 20.0
