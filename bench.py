@@ -63,7 +63,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -104,8 +104,10 @@ def make_tile(xb, rank, world):
     fwd = xb.default_io()
     fwd.bound_management = xb.BM_ITERATIVE
     fwd.bm_max_iter = 10
+    # TF32 tensor-core contraction: its ~1e-3 relative error (of the dot-product
+    # scale) is far below sigma_out = 0.06 and the 9-bit ADC step
     cfg = xb.TileSettings(device=dev, forward_io=fwd, backward_io=xb.default_io(),
-                          mvm_precision=xb.MVM_FP32)
+                          mvm_precision=xb.MVM_TF32)
     cfg.update.bl = 31
     d_out = N_ROWS * world
     shard = (rank * N_ROWS, (rank + 1) * N_ROWS) if world > 1 else None
@@ -247,7 +249,7 @@ def run_ours(args):
                        "parallelism": f"row-shard{world}",
                        "l2": "no flush: per-step working set (W + per-cell params 335 MB) > "
                              "126 MB L2; fresh input batch every step",
-                       "mvm_precision": "fp32 (SIMT)"},
+                       "mvm_precision": "tf32 (tcgen05)"},
             "mvm": {"samples_per_s": BATCH * world / (fwd_ms * 1e-3), "ms_per_batch": fwd_ms},
             "phase_ms_per_step": {"pulse": pulse_ms, "trains": ms_trains / max(ph_n[1], 1),
                                   "forward": fwd_ms},
@@ -352,7 +354,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

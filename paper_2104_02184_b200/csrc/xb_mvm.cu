@@ -275,7 +275,7 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io, Key
     count_launch();
     XB_CUDA(cudaGetLastError());
     int nsplit = 1;
-    if (tc && first) {
+    if (tc) { // re-issue passes recompute the whole batch on the tensor cores (cheap)
       tc_gemm_forward(t, s.xt, K, B, s.acc, splits);
       nsplit = splits;
     } else {
