@@ -156,6 +156,7 @@ def run_ours(args):
         else:
             tile.update_dev(Xs[s], Ds[s], LR)
 
+    clk = Clocks(local).__enter__()  # sampling starts before the warm-up so it spans the timed region
     for s in range(args.warmup):
         step(s)
     torch.cuda.synchronize()
@@ -167,12 +168,13 @@ def run_ours(args):
     launches0 = xb.launch_count()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
+    if True:
         e0.record(stream)
         for s in range(args.steps):
             step(args.warmup + s)
         e1.record(stream)
         torch.cuda.synchronize()
+    clk.__exit__(None, None, None)
     launches = xb.launch_count() - launches0
     ms_total = e0.elapsed_time(e1)
     timing = tile.read_timing()

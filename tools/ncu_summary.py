@@ -52,7 +52,7 @@ if '--blocks' in sys.argv:
                           'sass'], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(src)))
     h = rows[1]
-    data = rows[2:]
+    data = [x for x in rows[2:] if len(x) == len(h) and x[0].startswith('0x')]
     iA, iE = h.index('Address'), h.index('Instructions Executed')
     tot = sum(int(x[iE]) for x in data)
     print('   instructions per unit:', tot / units)
