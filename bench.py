@@ -132,8 +132,10 @@ def run_ours(args):
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
 
+    from paper_2104_02184_b200.parallel import RowShardedTile
     tile, cfg = make_tile(xb, rank, world)
     tile.set_stream(stream.cuda_stream)
+    sharded = RowShardedTile(tile, N_ROWS * world, N_COLS)
     g = torch.Generator(device=dev)
     g.manual_seed(7 + rank)
     w0 = (torch.rand(N_ROWS, N_COLS, generator=g, device=dev) * 0.2 - 0.1)
@@ -145,14 +147,11 @@ def run_ours(args):
     Xs = [torch.rand(BATCH, N_COLS, generator=gx, device=dev) * 2 - 1 for _ in range(nsets)]
     Ds = [torch.rand(BATCH, N_ROWS, generator=g, device=dev) * 2 - 1 for _ in range(nsets)]
     Y = torch.empty(BATCH, N_ROWS, device=dev)
-    amax = torch.empty(BATCH, device=dev)
 
     def step(s):
-        tile.forward_dev(Xs[s], Y)
+        sharded.forward(Xs[s], Y)          # row-local, no collective
         if world > 1:
-            xb.rows_amax_dev(Ds[s], amax, stream.cuda_stream)
-            dist.all_reduce(amax, op=dist.ReduceOp.MAX)
-            tile.update_dev(Xs[s], Ds[s], LR, amax_d=amax)
+            sharded.update(Xs[s], Ds[s], LR)  # all-reduce(max) of max|d| over NCCL
         else:
             tile.update_dev(Xs[s], Ds[s], LR)
 

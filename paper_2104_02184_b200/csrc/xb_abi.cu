@@ -775,8 +775,12 @@ int xb_tile_backward_partial_dev(xb_tile *h, const float *dD, int B, const float
                                  float *dP) {
   return guard([&] {
     Tile &t = h->t;
-    mvm_backward(t, dD, B, nullptr, make_io(t.cfg.backward_io), t.k_bwd, t.seq_bwd, dAmaxD, true,
-                 dP);
+    if (B < 0) raise("backward: batch must be >= 0");
+    const xb_io_params &io = t.cfg.backward_io;
+    if (io.bound_management != XB_BM_NONE)
+      raise("backward_io.bound_management: not supported on row shards");
+    IoDev d = make_io(io);
+    mvm_backward(t, dD, B, nullptr, d, t.k_bwd, t.seq_bwd, dAmaxD, true, dP);
   });
 }
 

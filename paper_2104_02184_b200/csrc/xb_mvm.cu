@@ -208,6 +208,59 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const float *__restrict__
   Y[(size_t)b * ldy + o] = (float)(scale * quantize(v, io.adc));
 }
 
+// Row-shard backward, phase 1: the shard's column sums plus its share of the
+// weight-noise fold (independent per shard: the variances of the shards add
+// up to sigma_w^2 ||d~||^2 over all rows).  No output noise, ADC or alpha yet.
+__global__ void __launch_bounds__(256) partial_kernel(const float *__restrict__ acc, int M,
+                                                       float *__restrict__ P,
+                                                       const SampleState *__restrict__ st,
+                                                       IoDev io, Key key, uint64_t seq0,
+                                                       uint32_t shard_tag) {
+  const int b = blockIdx.y;
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= M) return;
+  const SampleState s = st[b];
+  float v = acc[(size_t)b * M + o];
+  if (!io.perfect && io.sigma_w > 0.0 && s.alpha != 0.f) {
+    const uint64_t seq = seq0 + (uint64_t)b;
+    const float z = normal1((uint32_t)o, (uint32_t)seq, (uint32_t)(seq >> 32), shard_tag, key);
+    v += (float)(io.sigma_w * (double)s.norm * (double)z);
+  }
+  P[(size_t)b * M + o] = v;
+}
+
+// Row-shard backward, phase 2 (after the sum over shards): output noise, ADC
+// and alpha act on the reduced column sums, as in proj/src/io.cpp:143-146.
+__global__ void __launch_bounds__(256) finish_kernel(const float *__restrict__ Psum, int M,
+                                                      const float *__restrict__ amax,
+                                                      float *__restrict__ Y, IoDev io, Key key,
+                                                      uint64_t seq0) {
+  const int b = blockIdx.y;
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= M) return;
+  const float a = Psum[(size_t)b * M + o];
+  if (io.perfect) {
+    Y[(size_t)b * M + o] = a;
+    return;
+  }
+  const float m = amax[b];
+  const double alpha = (m == 0.f) ? 0.0 : (io.nm_absmax ? (double)m : 1.0);
+  const uint64_t seq = seq0 + (uint64_t)b;
+  float z0 = 0.f, z1 = 0.f, z2, z3;
+  if (io.sigma_out > 0.0)
+    normal4((uint32_t)o, (uint32_t)seq, (uint32_t)(seq >> 32), TAG_OUT_NOISE << 24, key, z0, z1,
+            z2, z3);
+  double v, scale;
+  if (alpha == 0.0) {
+    v = io.sigma_out > 0.0 ? io.sigma_out * (double)z1 : 0.0;
+    scale = 1.0;
+  } else {
+    v = (double)a + (io.sigma_out > 0.0 ? io.sigma_out * (double)z1 : 0.0);
+    scale = alpha;
+  }
+  Y[(size_t)b * M + o] = (float)(scale * quantize(v, io.adc));
+}
+
 // BM bookkeeping between passes: samples that saturated get m + 1 and stay
 // active; sat[B] counts them for the host's loop decision
 __global__ void bm_advance_kernel(SampleState *__restrict__ st, int *__restrict__ sat, int B) {
@@ -281,9 +334,12 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io, Key
     } else {
       gemm<TRANS>(t, s, M, K, B, first);
     }
-    if (skip_epilogue) {
-      XB_CUDA(cudaMemcpyAsync(dPartial, s.acc, sizeof(float) * (size_t)B * M,
-                              cudaMemcpyDeviceToDevice, t.stream));
+    if (skip_epilogue) { // row shard: partial sums + this shard's weight-noise fold
+      dim3 eg((M + 255) / 256, B);
+      partial_kernel<<<eg, 256, 0, t.stream>>>(s.acc, M, dPartial, s.st, io, key, seq0,
+                                               (TAG_W_NOISE << 24) | (uint32_t)t.row0);
+      count_launch();
+      XB_CUDA(cudaGetLastError());
       return;
     }
     dim3 eg((M + 255) / 256, B);
@@ -337,15 +393,12 @@ void mvm_backward(Tile &t, const float *dD, int B, float *dG, const IoDev &io, K
 
 void mvm_backward_finish(Tile &t, const float *dPsum, int B, const float *amax_global, float *dG,
                          const IoDev &io, Key key, uint64_t seq0) {
-  (void)t;
-  (void)dPsum;
-  (void)B;
-  (void)amax_global;
-  (void)dG;
-  (void)io;
-  (void)key;
-  (void)seq0;
-  raise("backward_finish: not implemented yet");
+  if (B <= 0) return;
+  if (!amax_global) raise("backward_finish: the global max|d| per sample is required");
+  dim3 eg((t.C + 255) / 256, B);
+  finish_kernel<<<eg, 256, 0, t.stream>>>(dPsum, t.C, amax_global, dG, io, key, seq0);
+  count_launch();
+  XB_CUDA(cudaGetLastError());
 }
 
 } // namespace xb

@@ -457,14 +457,18 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 2) pulse_kernel(
     uint32_t T = 0, acc = 0, qa = q0;
     auto append = [&](uint32_t xv, uint32_t dv) {
       const uint32_t k = __popc(xv & dv & xmask);
-      const uint32_t bits = ((int32_t)(xv ^ dv) >= 0) ? ~(0xffffffffu << k) : 0u;
+      const uint32_t down = (uint32_t)((int32_t)(xv ^ dv) >> 31); // all ones: signs differ
       const uint32_t sh = T & 31u;
-      const uint64_t wide = (uint64_t)bits << sh;
-      acc |= (uint32_t)wide;
-      if (sh + k >= 32u) {
+      uint32_t lo; // k ones from bit sh, clipped at bit 31 (BMSK)
+      asm("bmsk.clamp.b32 %0, %1, %2;" : "=r"(lo) : "r"(sh), "r"(k));
+      acc |= lo & ~down;
+      const uint32_t e = sh + k;
+      if (e >= 32u) {
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(qa), "r"(acc));
         qa += 128u;
-        acc = (uint32_t)(wide >> 32);
+        uint32_t hi;
+        asm("bmsk.clamp.b32 %0, %1, %2;" : "=r"(hi) : "r"(0u), "r"(e - 32u));
+        acc = hi & ~down;
       }
       T += k;
     };

@@ -326,6 +326,27 @@ class AnalogTile:
     def backward_dev(self, D, G) -> None:
         _check(_lib.xb_tile_backward_dev(self._h, _tptr(D), int(D.shape[0]), _tptr(G)))
 
+    def rows_amax(self, V):
+        """Device tensor [B] of max_j |V[b][j]| (on the tile's stream)."""
+        import torch
+        out = torch.empty(V.shape[0], dtype=torch.float32, device=V.device)
+        _check(_lib.xb_rows_amax_dev(_tptr(V), int(V.shape[0]), int(V.shape[1]), _tptr(out),
+                                     C.c_void_p(self.stream())))
+        return out
+
+    def backward_partial_dev(self, D, amax_d):
+        """Row-shard backward phase 1: this shard's column sums [B][d_in]."""
+        import torch
+        P = torch.empty(D.shape[0], self._d_in, dtype=torch.float32, device=D.device)
+        _check(_lib.xb_tile_backward_partial_dev(self._h, _tptr(D), int(D.shape[0]),
+                                                 _tptr(amax_d), _tptr(P)))
+        return P
+
+    def backward_finish_dev(self, P, amax_d, G) -> None:
+        """Row-shard backward phase 2 on the summed partials: noise, ADC, alpha."""
+        _check(_lib.xb_tile_backward_finish_dev(self._h, _tptr(P), int(P.shape[0]),
+                                                _tptr(amax_d), _tptr(G)))
+
     def update_dev(self, X, D, lr=None, amax_d=None) -> None:
         B = int(X.shape[0])
         lra = _lr_array(lr, B)
