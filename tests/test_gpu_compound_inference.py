@@ -28,11 +28,16 @@ def ideal_transfer():
     return s
 
 
-def test_deterministic_transfer_matches_oracle():
+@pytest.mark.parametrize("transfer_lr,exact", [(0.1, False), (0.113, True)])
+def test_deterministic_transfer_matches_oracle(transfer_lr, exact):
     """test_compounds.cpp:311-358: deterministic pulses, C accumulates A's columns
-    on schedule; GPU fast/slow weights vs the oracle TransferTile."""
+    on schedule; GPU fast/slow weights vs the oracle TransferTile.  With the
+    reference's own values (transfer_lr 0.1) the C counts lround(1.5) sit
+    exactly on a rounding tie that the fp32 readout of A decides differently
+    from the fp64 one: C may differ by one dw_min per transfer event there.
+    With transfer_lr 0.113 (no ties) the GPU must match exactly."""
     s = ideal_transfer()
-    s.transfer_every, s.transfer_lr = 1, 0.1
+    s.transfer_every, s.transfer_lr = 1, transfer_lr
     s.fast_device = quiet_device(1e-4)
     s.slow_device = quiet_device(1e-4)
     s.update.pulse_type = xb.PULSE_DETERMINISTIC
@@ -43,7 +48,7 @@ def test_deterministic_transfer_matches_oracle():
         dev.dw_min, dev.w_max, dev.w_min = src.dw_min, src.w_max, src.w_min
     os_.forward_io = O.default("perfect_io")
     os_.backward_io = O.default("perfect_io")
-    os_.transfer_every, os_.transfer_lr = 1, float(np.float32(0.1))
+    os_.transfer_every, os_.transfer_lr = 1, float(np.float32(transfer_lr))
     os_.update.pulse_type = oracle.PULSE_DETERMINISTIC
     o = O.transfer(2, 2, os_, 17)
     x = np.array([0.3, -0.2], np.float32)
@@ -54,7 +59,8 @@ def test_deterministic_transfer_matches_oracle():
         o.update(x.astype(np.float64), d.astype(np.float64), lr)
     assert g.transfer_events() == o.events() == 6
     np.testing.assert_allclose(g.fast_tile().get_weights(), o.fast.get_weights(), atol=2e-6)
-    np.testing.assert_allclose(g.slow_tile().get_weights(), o.slow.get_weights(), atol=2e-6)
+    tol = 2e-6 if exact else 6 * 1e-4 + 2e-6
+    np.testing.assert_allclose(g.slow_tile().get_weights(), o.slow.get_weights(), atol=tol)
 
 
 def test_transfer_schedules():
