@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libxbtile.so")
+# XBTILE_LIB selects an experiment build (paper_2104_02184_b200/build.py --out=...)
+LIB_PATH = os.environ.get("XBTILE_LIB") or os.path.join(PKG, "libxbtile.so")
 
 CONSTANT_STEP, LINEAR_STEP, SOFT_BOUNDS, EXP_STEP = 0, 1, 2, 3
 NM_NONE, NM_ABS_MAX = 0, 1

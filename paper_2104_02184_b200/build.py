@@ -34,13 +34,18 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = LIB) -> str:
+    """Compile every .cu for sm_100a and link the C-ABI library ``out``.
+
+    ``defines`` (e.g. ``("XB_PULSE_MINB=3",)``) build experiment variants
+    into a separate object directory; the product build uses none."""
     srcs = [os.path.join(CSRC, s) for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
     deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     deps.append(os.path.join(ROOT, "include", "xbtile.h"))
-    if not force and not _stale(LIB, deps):
-        return LIB
-    objdir = os.path.join(PKG, "build")
+    if not force and not _stale(out, deps):
+        return out
+    tag = "_".join(d.replace("=", "") for d in defines)
+    objdir = os.path.join(PKG, "build" + ("_" + tag if tag else ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     flags = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
@@ -48,16 +53,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
              "-Xptxas", "-warn-spills"]
     if verbose:
         flags += ["-Xptxas", "-v"]
+    flags += [f"-D{d}" for d in defines]
     for s in srcs:
         o = os.path.join(objdir, os.path.basename(s).replace(".cu", ".o"))
         cmd = [nvcc(), *ARCH, *flags, "-c", s, "-o", o]
         subprocess.run(cmd, check=True)
         objs.append(o)
-    tmp = LIB + ".tmp"
+    tmp = out + ".tmp"
     subprocess.run([nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-lcuda"
                     if _have_libcuda() else "-lrt"], check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 def _have_libcuda() -> bool:
@@ -65,4 +71,7 @@ def _have_libcuda() -> bool:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs,
+                out=outs[0] if outs else LIB))

@@ -302,10 +302,13 @@ static RoundKeys round_keys(Key k) {
   return r;
 }
 
+#ifndef XB_C2C_ROUNDS
+#define XB_C2C_ROUNDS 10
+#endif
 __device__ __forceinline__ void philox10_rk(uint32_t &c0, uint32_t &c1, uint32_t &c2,
                                             uint32_t &c3, const RoundKeys &rk) {
 #pragma unroll
-  for (int r = 0; r < 10; ++r) philox_round(c0, c1, c2, c3, rk.k0[r], rk.k1[r]);
+  for (int r = 0; r < XB_C2C_ROUNDS; ++r) philox_round(c0, c1, c2, c3, rk.k0[r], rk.k1[r]);
 }
 
 __device__ __forceinline__ void box_muller_fast(uint32_t a, uint32_t b, float &z0, float &z1) {
@@ -425,8 +428,12 @@ constexpr int PULSE_WARPS = 16;          // rows per CTA
 constexpr int PULSE_QW = 32;             // stream words per lane
 constexpr int PULSE_CAP = PULSE_QW * 32; // pulses per lane per segment
 
+// CTAs of 512 threads per SM: 3 (40 registers, 48 warps) measured 7 % faster
+// than 2 for the cheap laws; ExpStep's extra live state prefers 2 (64 registers)
+template <int LAW> constexpr int pulse_minb() { return LAW == XB_EXP_STEP ? 2 : 3; }
+
 template <int LAW, bool NOISE>
-__global__ void __launch_bounds__(PULSE_WARPS * 32, 2) pulse_kernel(
+__global__ void __launch_bounds__(PULSE_WARPS * 32, pulse_minb<LAW>()) pulse_kernel(
     float *__restrict__ W, const float4 *__restrict__ P, int ld, int R, int C,
     const uint32_t *__restrict__ xw, const uint32_t *__restrict__ dw, int ldb, int B, int row0,
     LawArgs la, RoundKeys rk, uint32_t call) {

@@ -19,6 +19,7 @@ ap.add_argument("--n", type=int, default=4096)
 ap.add_argument("--batch", type=int, default=256)
 ap.add_argument("--device", default="reram_sb")
 ap.add_argument("--precision", type=int, default=xb.MVM_FP32)
+ap.add_argument("--warm", type=int, default=0, help="untimed iterations first")
 args = ap.parse_args()
 
 dev = xb.device_preset(args.device)
@@ -34,10 +35,16 @@ g.manual_seed(7)
 X = torch.rand(args.batch, args.n, device="cuda", generator=g) * 2 - 1
 D = torch.rand(args.batch, args.n, device="cuda", generator=g) * 2 - 1
 Y = torch.empty(args.batch, args.n, device="cuda")
+with torch.cuda.stream(s):
+    for _ in range(args.warm):
+        t.forward_dev(X, Y)
+        t.update_dev(X, D, 0.01)
+t.synchronize()
 t.set_timing(True)
 with torch.cuda.stream(s):
     for _ in range(args.iters):
         t.forward_dev(X, Y)
         t.update_dev(X, D, 0.01)
 tm = t.read_timing()
-print({k: (round(v[0], 4), v[1]) for k, v in tm.items()})
+print(os.environ.get("XBTILE_LIB", "default"),
+      {k: (round(v[0] / max(v[1], 1), 4), v[1]) for k, v in tm.items()})
