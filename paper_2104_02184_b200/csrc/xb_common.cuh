@@ -75,6 +75,13 @@ __device__ __forceinline__ void normal4(uint32_t c0, uint32_t c1, uint32_t c2, u
   box_muller(c2, c3, z2, z3);
 }
 
+// two standard normals from one Philox call (one Box-Muller pair)
+__device__ __forceinline__ void normal2(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                        Key key, float &z0, float &z1) {
+  philox10(c0, c1, c2, c3, key);
+  box_muller(c0, c1, z0, z1);
+}
+
 __device__ __forceinline__ float normal1(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
                                          Key key) {
   philox10(c0, c1, c2, c3, key);
@@ -89,7 +96,7 @@ __device__ __forceinline__ float normal1(uint32_t c0, uint32_t c1, uint32_t c2, 
 // exact zero passes through, clamp, mid-rise grid -b + (k + 1/2) step with
 // k = round-half-away((v + b - step/2) / step) clamped to [0, levels - 1].
 struct Quant {
-  double bound, step, levels_m1;
+  double bound, step, inv_step, levels_m1;
   int bits;
 };
 
@@ -100,9 +107,11 @@ __host__ __device__ __forceinline__ Quant make_quant(double bound, int bits) {
   if (bits > 0) {
     const double levels = exp2((double)bits);
     q.step = 2.0 * bound / levels;
+    q.inv_step = levels / (2.0 * bound);
     q.levels_m1 = levels - 1.0;
   } else {
     q.step = 0.0;
+    q.inv_step = 0.0;
     q.levels_m1 = 0.0;
   }
   return q;
@@ -112,7 +121,9 @@ __device__ __forceinline__ double quantize(double v, const Quant &q) {
   if (v == 0.0) return 0.0;
   v = fmin(fmax(v, -q.bound), q.bound);
   if (q.bits <= 0) return v;
-  double k = round((v + q.bound - 0.5 * q.step) / q.step);
+  // the reference divides by step; multiplying by its reciprocal differs by at
+  // most one fp64 ulp, i.e. only on exact half-way ties of the grid
+  double k = round((v + q.bound - 0.5 * q.step) * q.inv_step);
   k = fmin(fmax(k, 0.0), q.levels_m1);
   return -q.bound + (k + 0.5) * q.step;
 }

@@ -30,68 +30,115 @@ struct SampleState {
   int active;
 };
 
-__global__ void __launch_bounds__(256) prep_kernel(const float *__restrict__ X, int n, int ldx,
-                                                    float *__restrict__ Xt, int ldt,
-                                                    SampleState *__restrict__ st, IoDev io,
-                                                    Key key, uint64_t seq0, int first_pass,
-                                                    const float *__restrict__ amax_in) {
+constexpr int PREP_THREADS = 512;
+constexpr int PREP_VPT = 8; // values per thread kept in registers (n <= 4096)
+
+__device__ __forceinline__ float block_max(float m, float *red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  m = warp_max(m);
+  if (lane == 0) red[warp] = m;
+  __syncthreads();
+  if (warp == 0) {
+    m = lane < nw ? red[lane] : 0.f;
+    m = warp_max(m);
+    if (lane == 0) red[32] = m;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+__global__ void __launch_bounds__(PREP_THREADS) prep_kernel(const float *__restrict__ X, int n,
+                                                             int ldx, float *__restrict__ Xt,
+                                                             int ldt,
+                                                             SampleState *__restrict__ st,
+                                                             IoDev io, Key key, uint64_t seq0,
+                                                             int first_pass,
+                                                             const float *__restrict__ amax_in,
+                                                             int *__restrict__ sat) {
   const int b = blockIdx.x;
   SampleState s = st[b];
-  if (!first_pass && !s.active) return;
+  if (!first_pass) { // bound management: re-issue the samples that saturated
+    const int again = s.active && sat[b];
+    __syncthreads(); // every thread has read the flag before it is re-armed
+    if (threadIdx.x == 0) sat[b] = 0;
+    if (!again) {
+      if (threadIdx.x == 0 && s.active) {
+        s.active = 0;
+        st[b] = s;
+      }
+      return;
+    }
+    s.m += 1;
+  }
   const float *x = X + (size_t)b * ldx;
   float *xt = Xt + (size_t)b * ldt;
-  __shared__ float red[32];
-  __shared__ float bc;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-
+  __shared__ float red[33];
+  // the sample stays in registers between the max and the conversion when it fits
+  const bool in_regs = n <= PREP_THREADS * PREP_VPT;
+  float v[PREP_VPT];
+  if (in_regs) {
+#pragma unroll
+    for (int u = 0; u < PREP_VPT; ++u) {
+      const int j = threadIdx.x + u * PREP_THREADS;
+      v[u] = j < n ? x[j] : 0.f;
+    }
+  }
   if (first_pass) {
     float m = 0.f;
     if (amax_in) {
       m = amax_in[b];
     } else {
-      for (int j = threadIdx.x; j < n; j += blockDim.x) m = fmaxf(m, fabsf(x[j]));
-      m = warp_max(m);
-      if (lane == 0) red[warp] = m;
-      __syncthreads();
-      if (warp == 0) {
-        m = lane < nw ? red[lane] : 0.f;
-        m = warp_max(m);
-        if (lane == 0) bc = m;
+      if (in_regs) {
+#pragma unroll
+        for (int u = 0; u < PREP_VPT; ++u) m = fmaxf(m, fabsf(v[u]));
+      } else {
+        for (int j = threadIdx.x; j < n; j += blockDim.x) m = fmaxf(m, fabsf(x[j]));
       }
-      __syncthreads();
-      m = bc;
+      m = block_max(m, red);
     }
     s.alpha = (m == 0.f) ? 0.f : (io.nm_absmax ? m : 1.f);
     s.m = 0;
     s.active = 1;
   }
   const uint64_t seq = seq0 + (uint64_t)b;
+  const double inv = (s.alpha == 0.f) ? 0.0 : 1.0 / ((double)s.alpha * exp2((double)s.m));
+  auto convert = [&](float xv, int j) -> float {
+    if (io.perfect) return xv;
+    if (s.alpha == 0.f) return 0.f;
+    double q = quantize((double)xv * inv, io.dac); // x / alpha, then the DAC (io.cpp:122-130)
+    if (io.sigma_inp > 0.0) {
+      const float z = normal1((uint32_t)j, (uint32_t)seq, (uint32_t)(seq >> 32) | (s.m << 24),
+                              TAG_IN_NOISE << 24, key);
+      q += io.sigma_inp * (double)z;
+    }
+    return (float)q;
+  };
   float nrm = 0.f;
-  if (io.perfect) {
-    for (int j = threadIdx.x; j < n; j += blockDim.x) xt[j] = x[j];
-  } else if (s.alpha == 0.f) {
-    for (int j = threadIdx.x; j < n; j += blockDim.x) xt[j] = 0.f;
-  } else {
-    const double denom = (double)s.alpha * exp2((double)s.m);
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
-      double v = quantize((double)x[j] / denom, io.dac);
-      if (io.sigma_inp > 0.0) {
-        const float z = normal1((uint32_t)j, (uint32_t)seq, (uint32_t)(seq >> 32) | (s.m << 24),
-                                TAG_IN_NOISE << 24, key);
-        v += io.sigma_inp * (double)z;
+  if (in_regs) {
+#pragma unroll
+    for (int u = 0; u < PREP_VPT; ++u) {
+      const int j = threadIdx.x + u * PREP_THREADS;
+      if (j < n) {
+        const float f = convert(v[u], j);
+        xt[j] = f;
+        nrm = fmaf(f, f, nrm);
       }
-      const float f = (float)v;
+    }
+  } else {
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      const float f = convert(x[j], j);
       xt[j] = f;
       nrm = fmaf(f, f, nrm);
     }
   }
   nrm = warp_sum(nrm);
   __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) red[warp] = nrm;
   __syncthreads();
   if (threadIdx.x == 0) {
     float tot = 0.f;
-    for (int w = 0; w < nw; ++w) tot += red[w];
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
     s.norm = sqrtf(tot);
     st[b] = s;
   }
@@ -176,7 +223,8 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const float *__restrict__
                                                         int o0, float *__restrict__ Y, int ldy,
                                                         SampleState *__restrict__ st, IoDev io,
                                                         Key key, uint64_t seq0,
-                                                        int *__restrict__ sat, int first_pass) {
+                                                        int *__restrict__ sat, int first_pass,
+                                                        int B, int pass_slot) {
   const int b = blockIdx.y;
   const SampleState s = st[b];
   if (!first_pass && !s.active) return;
@@ -189,10 +237,10 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const float *__restrict__
     return;
   }
   const uint64_t seq = seq0 + (uint64_t)b;
-  float z0 = 0.f, z1 = 0.f, z2, z3;
+  float z0 = 0.f, z1 = 0.f;
   if (io.sigma_w > 0.0 || io.sigma_out > 0.0)
-    normal4((uint32_t)(o0 + o), (uint32_t)seq, (uint32_t)(seq >> 32) | (s.m << 24),
-            TAG_OUT_NOISE << 24, key, z0, z1, z2, z3);
+    normal2((uint32_t)(o0 + o), (uint32_t)seq, (uint32_t)(seq >> 32) | (s.m << 24),
+            TAG_OUT_NOISE << 24, key, z0, z1);
   double v;
   double scale;
   if (s.alpha == 0.f) { // io.cpp:107-115: zero input -> output noise only, no alpha
@@ -203,7 +251,9 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const float *__restrict__
     if (io.sigma_w > 0.0) v += io.sigma_w * (double)s.norm * (double)z0;
     if (io.sigma_out > 0.0) v += io.sigma_out * (double)z1;
     scale = (double)s.alpha * exp2((double)s.m);
-    if (io.bm && s.alpha != 0.f && s.m < io.bm_max_iter && fabs(v) >= io.adc.bound) sat[b] = 1;
+    if (io.bm && s.alpha != 0.f && s.m < io.bm_max_iter && fabs(v) >= io.adc.bound) {
+      if (atomicExch(sat + b, 1) == 0) atomicAdd(sat + B + pass_slot, 1);
+    }
   }
   Y[(size_t)b * ldy + o] = (float)(scale * quantize(v, io.adc));
 }
@@ -246,10 +296,9 @@ __global__ void __launch_bounds__(256) finish_kernel(const float *__restrict__ P
   const float m = amax[b];
   const double alpha = (m == 0.f) ? 0.0 : (io.nm_absmax ? (double)m : 1.0);
   const uint64_t seq = seq0 + (uint64_t)b;
-  float z0 = 0.f, z1 = 0.f, z2, z3;
+  float z0 = 0.f, z1 = 0.f;
   if (io.sigma_out > 0.0)
-    normal4((uint32_t)o, (uint32_t)seq, (uint32_t)(seq >> 32), TAG_OUT_NOISE << 24, key, z0, z1,
-            z2, z3);
+    normal2((uint32_t)o, (uint32_t)seq, (uint32_t)(seq >> 32), TAG_OUT_NOISE << 24, key, z0, z1);
   double v, scale;
   if (alpha == 0.0) {
     v = io.sigma_out > 0.0 ? io.sigma_out * (double)z1 : 0.0;
@@ -259,22 +308,6 @@ __global__ void __launch_bounds__(256) finish_kernel(const float *__restrict__ P
     scale = alpha;
   }
   Y[(size_t)b * M + o] = (float)(scale * quantize(v, io.adc));
-}
-
-// BM bookkeeping between passes: samples that saturated get m + 1 and stay
-// active; sat[B] counts them for the host's loop decision
-__global__ void bm_advance_kernel(SampleState *__restrict__ st, int *__restrict__ sat, int B) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  SampleState s = st[b];
-  const bool again = s.active && sat[b];
-  if (again) {
-    s.m += 1;
-    atomicAdd(sat + B, 1);
-  }
-  s.active = again ? 1 : 0;
-  sat[b] = 0;
-  st[b] = s;
 }
 
 struct MvmScratch {
@@ -288,7 +321,7 @@ MvmScratch carve(Tile &t, int B, int K, int M, int nsplit) {
   const size_t xt_b = (size_t)B * K * sizeof(float);
   const size_t acc_b = (size_t)nsplit * B * M * sizeof(float);
   const size_t st_b = (size_t)B * sizeof(SampleState);
-  const size_t sat_b = (size_t)(B + 1) * sizeof(int);
+  const size_t sat_b = (size_t)(B + 32) * sizeof(int); // flags + one counter per BM pass
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   char *p = (char *)t.s_io.get(al(xt_b) + al(acc_b) + al(st_b) + al(sat_b));
   MvmScratch s;
@@ -320,11 +353,12 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io, Key
   const bool tc = !TRANS && t.cfg.mvm_precision == XB_MVM_TF32 && B >= 16 && !skip_epilogue;
   const int splits = tc ? tc_used_splits(K, tc_splits(M, K)) : 1;
   MvmScratch s = carve(t, B, K, M, splits);
-  if (io.bm) XB_CUDA(cudaMemsetAsync(s.sat, 0, sizeof(int) * (B + 1), t.stream));
+  if (io.bm) XB_CUDA(cudaMemsetAsync(s.sat, 0, sizeof(int) * (B + 32), t.stream));
   const int passes = io.bm ? 1 + io.bm_max_iter : 1;
   for (int pass = 0; pass < passes; ++pass) {
     const int first = pass == 0;
-    prep_kernel<<<B, 256, 0, t.stream>>>(dIn, K, K, s.xt, K, s.st, io, key, seq0, first, amax_in);
+    prep_kernel<<<B, PREP_THREADS, 0, t.stream>>>(dIn, K, K, s.xt, K, s.st, io, key, seq0, first,
+                                                   amax_in, s.sat);
     count_launch();
     XB_CUDA(cudaGetLastError());
     int nsplit = 1;
@@ -345,20 +379,16 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io, Key
     dim3 eg((M + 255) / 256, B);
     epilogue_kernel<<<eg, 256, 0, t.stream>>>(s.acc, M, nsplit, (size_t)B * M, M,
                                               TRANS ? 0 : t.row0, dOut, M, s.st, io, key, seq0,
-                                              s.sat, first);
+                                              s.sat, first, B, pass);
     count_launch();
     XB_CUDA(cudaGetLastError());
     if (io.bm && pass + 1 < passes) {
-      // bound management: re-issue only while some sample saturated.  The
-      // count crosses to the host (one small sync per forward with BM on);
-      // re-issue passes run on the SIMT kernel restricted to active samples.
-      XB_CUDA(cudaMemsetAsync(s.sat + B, 0, sizeof(int), t.stream));
-      bm_advance_kernel<<<(B + 255) / 256, 256, 0, t.stream>>>(s.st, s.sat, B);
-      count_launch();
-      XB_CUDA(cudaGetLastError());
+      // bound management: re-issue while some sample saturated.  The epilogue
+      // counted them; the count crosses to the host (one 4-byte read and a
+      // stream sync per pass with BM on) and the next prep re-arms the flags.
       if (!t.bm_count) XB_CUDA(cudaMallocHost(&t.bm_count, sizeof(int)));
-      XB_CUDA(cudaMemcpyAsync(t.bm_count, s.sat + B, sizeof(int), cudaMemcpyDeviceToHost,
-                              t.stream));
+      XB_CUDA(cudaMemcpyAsync(t.bm_count, s.sat + B + pass, sizeof(int),
+                              cudaMemcpyDeviceToHost, t.stream));
       XB_CUDA(cudaStreamSynchronize(t.stream));
       if (*t.bm_count == 0) break;
     }
