@@ -109,7 +109,8 @@ void launch_drift(Tile &t, double ratio);
 // ---- tcgen05 contraction (xb_mvm_tc.cu) ----
 int tc_splits(int M, int K);
 int tc_used_splits(int K, int splits);
-void tc_gemm_forward(Tile &t, const float *Xt, int ldt, int B, float *part, int splits);
+void tc_gemm(Tile &t, bool transposed, const float *Xt, int ldt, int B, float *part,
+             int splits);
 
 // ---- noisy MVM (xb_mvm.cu) ----
 // forward: Y[b][i] = alpha_b * ADC(sum_j W[i][j] x~[b][j] + noise), i local rows

@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const float *__restrict__
 // weight-noise fold (independent per shard: the variances of the shards add
 // up to sigma_w^2 ||d~||^2 over all rows).  No output noise, ADC or alpha yet.
 __global__ void __launch_bounds__(256) partial_kernel(const float *__restrict__ acc, int M,
+                                                       int nsplit, size_t split_stride,
                                                        float *__restrict__ P,
                                                        const SampleState *__restrict__ st,
                                                        IoDev io, Key key, uint64_t seq0,
@@ -271,6 +272,7 @@ __global__ void __launch_bounds__(256) partial_kernel(const float *__restrict__ 
   if (o >= M) return;
   const SampleState s = st[b];
   float v = acc[(size_t)b * M + o];
+  for (int sp = 1; sp < nsplit; ++sp) v += acc[sp * split_stride + (size_t)b * M + o];
   if (!io.perfect && io.sigma_w > 0.0 && s.alpha != 0.f) {
     const uint64_t seq = seq0 + (uint64_t)b;
     const float z = normal1((uint32_t)o, (uint32_t)seq, (uint32_t)(seq >> 32), shard_tag, key);
@@ -333,10 +335,10 @@ MvmScratch carve(Tile &t, int B, int K, int M, int nsplit) {
 }
 
 template <bool TRANS>
-void gemm(Tile &t, const MvmScratch &s, int M, int K, int B, int first) {
+void gemm(Tile &t, const MvmScratch &s, int M, int K, int ldt, int B, int first) {
   dim3 grid((M + 63) / 64, (B + 63) / 64);
-  mvm_simt_kernel<TRANS><<<grid, 256, 0, t.stream>>>(t.W, t.ld, M, K, s.xt, K, B, s.acc, M, s.st,
-                                                     first);
+  mvm_simt_kernel<TRANS><<<grid, 256, 0, t.stream>>>(t.W, t.ld, M, K, s.xt, ldt, B, s.acc, M,
+                                                     s.st, first);
   count_launch();
   XB_CUDA(cudaGetLastError());
 }
@@ -350,27 +352,29 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io, Key
   if (B <= 0) return;
   // tensor-core contraction for the forward direction at TF32 (B >= 16);
   // the fp32 SIMT kernel otherwise (exact-fp32 parity mode, tiny batches)
-  const bool tc = !TRANS && t.cfg.mvm_precision == XB_MVM_TF32 && B >= 16 && !skip_epilogue;
+  const bool tc = t.cfg.mvm_precision == XB_MVM_TF32 && B >= 16;
   const int splits = tc ? tc_used_splits(K, tc_splits(M, K)) : 1;
-  MvmScratch s = carve(t, B, K, M, splits);
+  const int ldt = (K + 3) & ~3; // x~ rows padded to 16 bytes (TMA global stride)
+  MvmScratch s = carve(t, B, ldt, M, splits);
   if (io.bm) XB_CUDA(cudaMemsetAsync(s.sat, 0, sizeof(int) * (B + 32), t.stream));
   const int passes = io.bm ? 1 + io.bm_max_iter : 1;
   for (int pass = 0; pass < passes; ++pass) {
     const int first = pass == 0;
-    prep_kernel<<<B, PREP_THREADS, 0, t.stream>>>(dIn, K, K, s.xt, K, s.st, io, key, seq0, first,
-                                                   amax_in, s.sat);
+    prep_kernel<<<B, PREP_THREADS, 0, t.stream>>>(dIn, K, K, s.xt, ldt, s.st, io, key, seq0,
+                                                   first, amax_in, s.sat);
     count_launch();
     XB_CUDA(cudaGetLastError());
     int nsplit = 1;
     if (tc) { // re-issue passes recompute the whole batch on the tensor cores (cheap)
-      tc_gemm_forward(t, s.xt, K, B, s.acc, splits);
+      tc_gemm(t, TRANS, s.xt, ldt, B, s.acc, splits);
       nsplit = splits;
     } else {
-      gemm<TRANS>(t, s, M, K, B, first);
+      gemm<TRANS>(t, s, M, K, ldt, B, first);
     }
     if (skip_epilogue) { // row shard: partial sums + this shard's weight-noise fold
       dim3 eg((M + 255) / 256, B);
-      partial_kernel<<<eg, 256, 0, t.stream>>>(s.acc, M, dPartial, s.st, io, key, seq0,
+      partial_kernel<<<eg, 256, 0, t.stream>>>(s.acc, M, nsplit, (size_t)B * M, dPartial, s.st,
+                                               io, key, seq0,
                                                (TAG_W_NOISE << 24) | (uint32_t)t.row0);
       count_launch();
       XB_CUDA(cudaGetLastError());

@@ -65,22 +65,26 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map
       : "memory");
 }
 
-// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row groups
-// 1024 bytes apart (SBO), sm_100 descriptor version 1.
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+// UMMA shared-memory descriptor, 128-byte swizzle, sm_100 version 1.
+//  K-major  : 8-row groups of 128-byte rows, SBO = 1024 B between groups (LBO unused)
+//  MN-major : atoms of 32 MN-elements x 8 K-rows (1 KB); SBO = 1024 B between
+//             K-groups, LBO = distance between MN atoms
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t lbo = 16u,
+                                                    uint32_t sbo = 1024u) {
   uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);  // start address
-  d |= (uint64_t)1u << 16;                  // leading byte offset (unused for SW128 K-major)
-  d |= (uint64_t)(1024u >> 4) << 32;        // stride byte offset
-  d |= (uint64_t)1u << 46;                  // descriptor version (sm_100)
-  d |= (uint64_t)2u << 61;                  // SWIZZLE_128B
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);   // start address
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16; // leading byte offset
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32; // stride byte offset
+  d |= (uint64_t)1u << 46;                   // descriptor version (sm_100)
+  d |= (uint64_t)2u << 61;                   // SWIZZLE_128B
   return d;
 }
 
-// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, M=128, N=bn
-__host__ __device__ __forceinline__ uint32_t idesc_tf32(int bn) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(bn >> 3) << 17) |
-         ((uint32_t)(TC_BM >> 4) << 24);
+// kind::tf32 instruction descriptor: D f32, A/B tf32, B K-major, A K- or
+// MN-major, M=128, N=bn
+__host__ __device__ __forceinline__ uint32_t idesc_tf32(int bn, bool a_mn = false) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) |
+         ((uint32_t)(bn >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
@@ -110,6 +114,10 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
                  "=r"(r[30]), "=r"(r[31])                                                      \
                : "r"(taddr))
 
+// A_MN = false: A = W tile [128 rows][32 K] (forward, K-major)
+// A_MN = true : A = W^T tile, i.e. W[32 K-rows][128 columns] (backward, MN-major):
+//               four 32x32 TMA boxes per stage, one per 32-column MN atom
+template <bool A_MN>
 __global__ void __launch_bounds__(128, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                    int M, int K, int B, int bn, int kblocks_per_split, float *__restrict__ part,
@@ -160,22 +168,32 @@ __global__ void __launch_bounds__(128, 1)
       mbar_wait(empty0 + 8 * s, ph ^ 1u);
       mbar_expect_tx(full0 + 8 * s, TC_A_BYTES + b_bytes);
       const int kk = (kb0 + kb) * TC_BK;
-      tma_load_2d(smem_u32(sa + s * TC_A_BYTES), &tm_a, full0 + 8 * s, kk, m0);
+      if (A_MN) {
+#pragma unroll
+        for (int a = 0; a < TC_BM / 32; ++a)
+          tma_load_2d(smem_u32(sa + s * TC_A_BYTES + a * 4096), &tm_a, full0 + 8 * s,
+                      m0 + 32 * a, kk);
+      } else {
+        tma_load_2d(smem_u32(sa + s * TC_A_BYTES), &tm_a, full0 + 8 * s, kk, m0);
+      }
       tma_load_2d(smem_u32(sb + s * TC_B_BYTES), &tm_b, full0 + 8 * s, kk, 0);
     }
   } else if (warp == 1 && lane == 0 && nkb > 0) {
     // ---------------- MMA issuer (one thread)
-    const uint32_t idesc = idesc_tf32(bn);
+    const uint32_t idesc = idesc_tf32(bn, A_MN);
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % TC_STAGES;
       const uint32_t ph = (uint32_t)(kb / TC_STAGES) & 1u;
       mbar_wait(full0 + 8 * s, ph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint64_t da = umma_desc_sw128(smem_u32(sa + s * TC_A_BYTES));
+      const uint64_t da = A_MN ? umma_desc_sw128(smem_u32(sa + s * TC_A_BYTES), 4096u, 1024u)
+                               : umma_desc_sw128(smem_u32(sa + s * TC_A_BYTES));
       const uint64_t db = umma_desc_sw128(smem_u32(sb + s * TC_B_BYTES));
+      // one MMA = 8 tf32 of K: K-major advances 32 bytes (+2 in 16-byte units),
+      // MN-major advances one 8-row K-group (+1024 bytes = +64)
 #pragma unroll
-      for (int k = 0; k < TC_BK / 8; ++k) // 8 tf32 = 32 bytes per MMA: +2 in the 16-byte units
-        mma_tf32(tmem, da + 2u * k, db + 2u * k, idesc, (kb | k) != 0);
+      for (int k = 0; k < TC_BK / 8; ++k)
+        mma_tf32(tmem, da + (A_MN ? 64u : 2u) * k, db + 2u * k, idesc, (kb | k) != 0);
       mma_commit(empty0 + 8 * s); // smem stage free once these MMAs retire
     }
     mma_commit(done);
@@ -249,13 +267,18 @@ int tc_splits(int M, int K) {
   return std::max(1, std::min(s, 16));
 }
 
-// forward contraction on tcgen05: part[s][b][o] (split stride B x M)
-void tc_gemm_forward(Tile &t, const float *Xt, int ldt, int B, float *part, int splits) {
-  const int M = t.R, K = t.C;
+// contraction on tcgen05: part[s][b][o] (split stride B x M).
+//   forward : o = row of W, K = columns of W   (A = W, K-major)
+//   backward: o = column of W, K = rows of W   (A = W^T, MN-major)
+void tc_gemm(Tile &t, bool transposed, const float *Xt, int ldt, int B, float *part,
+             int splits) {
+  const int M = transposed ? t.C : t.R, K = transposed ? t.R : t.C;
   static bool configured = false;
   if (!configured) {
-    XB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 TC_SMEM));
+    XB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
+    XB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
     configured = true;
   }
   const int kbs = (K + TC_BK - 1) / TC_BK;
@@ -264,12 +287,19 @@ void tc_gemm_forward(Tile &t, const float *Xt, int ldt, int B, float *part, int 
   for (int n0 = 0; n0 < B; n0 += TC_MAX_BN) {
     const int nb = std::min(TC_MAX_BN, B - n0);
     const int bn = std::max(16, (nb + 15) / 16 * 16);
-    const CUtensorMap ma = make_map(t.W, M, K, t.ld, TC_BM);
+    // W as [R][C] with row stride ld: the forward box is 128 rows x 32 columns,
+    // the backward box 32 rows (K) x 32 columns (one MN atom)
+    const CUtensorMap ma = transposed ? make_map(t.W, t.R, t.C, t.ld, 32)
+                                      : make_map(t.W, t.R, t.C, t.ld, TC_BM);
     const CUtensorMap mb = make_map(Xt + (size_t)n0 * ldt, nb, K, ldt, bn);
     dim3 grid((M + TC_BM - 1) / TC_BM, used);
     // partial sums of this N slab land at part + n0 rows, split stride B x M
-    tc_gemm_kernel<<<grid, 128, TC_SMEM, t.stream>>>(ma, mb, M, K, nb, bn, per,
-                                                     part + (size_t)n0 * M, M, (size_t)B * M);
+    if (transposed)
+      tc_gemm_kernel<true><<<grid, 128, TC_SMEM, t.stream>>>(
+          ma, mb, M, K, nb, bn, per, part + (size_t)n0 * M, M, (size_t)B * M);
+    else
+      tc_gemm_kernel<false><<<grid, 128, TC_SMEM, t.stream>>>(
+          ma, mb, M, K, nb, bn, per, part + (size_t)n0 * M, M, (size_t)B * M);
     count_launch();
     XB_CUDA(cudaGetLastError());
   }

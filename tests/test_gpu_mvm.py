@@ -287,3 +287,40 @@ def test_bound_management_reissue(prec):
     Y2 = t2.forward(X)
     assert np.abs(Y2).max() <= 12.0 * np.abs(X).max() + 1e-5
     assert np.abs(Y).max() > 20.0
+
+
+@pytest.mark.parametrize("shape,B", [((256, 256), 16), ((520, 300), 37), ((4096, 512), 256),
+                                     ((45, 37), 20), ((130, 77), 300)])
+def test_tcgen05_tf32_backward(shape, B):
+    """Backward contraction W^T d on tcgen05 with the MN-major A operand
+    (four 32x32 TMA boxes per stage) against the fp32 SIMT path."""
+    d_out, d_in = shape
+    io = xb.perfect_io()
+    W = np.random.default_rng(13).uniform(-0.5, 0.5, shape).astype(np.float32)
+    D = np.random.default_rng(14).uniform(-1, 1, (B, d_out)).astype(np.float32)
+    ref = D.astype(np.float64) @ W.astype(np.float64)
+    out = {}
+    for prec in (xb.MVM_FP32, xb.MVM_TF32):
+        t = xb.AnalogTile(d_out, d_in, cfg_io(io, io, prec), 5)
+        t.set_weights(W)
+        out[prec] = t.backward(D).astype(np.float64)
+    scale = np.linalg.norm(D.astype(np.float64), axis=1)[:, None] * \
+        np.linalg.norm(W.astype(np.float64), axis=0)[None, :]
+    assert (np.abs(out[xb.MVM_FP32] - ref) / scale).max() < 1e-5
+    assert (np.abs(out[xb.MVM_TF32] - ref) / scale).max() < 2e-3
+    if B >= 16:
+        assert not np.array_equal(out[xb.MVM_FP32], out[xb.MVM_TF32])
+
+
+def test_tcgen05_forward_odd_widths():
+    """Columns not a multiple of 4 (padded x~ stride for TMA) and rows not a
+    multiple of 128."""
+    io = xb.perfect_io()
+    W = np.random.default_rng(15).uniform(-0.5, 0.5, (77, 45)).astype(np.float32)
+    X = np.random.default_rng(16).uniform(-1, 1, (40, 45)).astype(np.float32)
+    t = xb.AnalogTile(77, 45, cfg_io(io, io, xb.MVM_TF32), 5)
+    t.set_weights(W)
+    Y = t.forward(X).astype(np.float64)
+    ref = X.astype(np.float64) @ W.T.astype(np.float64)
+    scale = np.linalg.norm(X, axis=1)[:, None] * np.linalg.norm(W, axis=1)[None, :]
+    assert (np.abs(Y - ref) / scale).max() < 2e-3
