@@ -17,6 +17,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "xb_internal.h"
@@ -65,18 +67,21 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map
       : "memory");
 }
 
-// UMMA shared-memory descriptor, 128-byte swizzle, sm_100 version 1.
-//  K-major  : 8-row groups of 128-byte rows, SBO = 1024 B between groups (LBO unused)
-//  MN-major : atoms of 32 MN-elements x 8 K-rows (1 KB); SBO = 1024 B between
-//             K-groups, LBO = distance between MN atoms
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t lbo = 16u,
-                                                    uint32_t sbo = 1024u) {
+// UMMA shared-memory descriptor, sm_100 version 1.
+//  K-major (layout 2 = SWIZZLE_128B): 8-row groups of 128-byte rows, SBO = 1024 B
+//    between groups (LBO unused)
+//  MN-major tf32 (layout 1 = SWIZZLE_128B_BASE32B, the only MN-major layout the
+//    tensor core accepts for 32-bit operands): atoms of 32 MN-elements x 4 K-rows
+//    (512 B, 32-byte swizzle granule); SBO = 512 B between K-groups, LBO =
+//    distance between 32-wide MN atoms
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
+                                              uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);   // start address
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16; // leading byte offset
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32; // stride byte offset
   d |= (uint64_t)1u << 46;                   // descriptor version (sm_100)
-  d |= (uint64_t)2u << 61;                   // SWIZZLE_128B
+  d |= (uint64_t)layout << 61;
   return d;
 }
 
@@ -116,7 +121,8 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
 
 // A_MN = false: A = W tile [128 rows][32 K] (forward, K-major)
 // A_MN = true : A = W^T tile, i.e. W[32 K-rows][128 columns] (backward, MN-major):
-//               four 32x32 TMA boxes per stage, one per 32-column MN atom
+//               four 32x32 TMA boxes (128B/32B-atom swizzle) per stage, one per
+//               32-column MN atom, 4 KB apart
 template <bool A_MN>
 __global__ void __launch_bounds__(128, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
@@ -186,11 +192,11 @@ __global__ void __launch_bounds__(128, 1)
       const uint32_t ph = (uint32_t)(kb / TC_STAGES) & 1u;
       mbar_wait(full0 + 8 * s, ph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint64_t da = A_MN ? umma_desc_sw128(smem_u32(sa + s * TC_A_BYTES), 4096u, 1024u)
-                               : umma_desc_sw128(smem_u32(sa + s * TC_A_BYTES));
-      const uint64_t db = umma_desc_sw128(smem_u32(sb + s * TC_B_BYTES));
+      const uint64_t da = A_MN ? umma_desc(smem_u32(sa + s * TC_A_BYTES), 4096u, 512u, 1u)
+                               : umma_desc(smem_u32(sa + s * TC_A_BYTES), 16u, 1024u, 2u);
+      const uint64_t db = umma_desc(smem_u32(sb + s * TC_B_BYTES), 16u, 1024u, 2u);
       // one MMA = 8 tf32 of K: K-major advances 32 bytes (+2 in 16-byte units),
-      // MN-major advances one 8-row K-group (+1024 bytes = +64)
+      // MN-major advances 8 K-rows = two 4-row groups (+1024 bytes = +64)
 #pragma unroll
       for (int k = 0; k < TC_BK / 8; ++k)
         mma_tf32(tmem, da + (A_MN ? 64u : 2u) * k, db + 2u * k, idesc, (kb | k) != 0);
@@ -242,15 +248,17 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 2-D fp32 tensor map over a row-major [rows][cols] array with row stride ld
-// floats; box = [box_rows][32 floats], 128-byte swizzle, OOB zero fill
-CUtensorMap make_map(const float *base, int rows, int cols, int ld, int box_rows) {
+// floats; box = [box_rows][32 floats], 128-byte swizzle (16- or 32-byte
+// granule), OOB zero fill
+CUtensorMap make_map(const float *base, int rows, int cols, int ld, int box_rows,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
   const cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows};
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)base, dims, strides,
-                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) raise("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
@@ -289,17 +297,20 @@ void tc_gemm(Tile &t, bool transposed, const float *Xt, int ldt, int B, float *p
     const int bn = std::max(16, (nb + 15) / 16 * 16);
     // W as [R][C] with row stride ld: the forward box is 128 rows x 32 columns,
     // the backward box 32 rows (K) x 32 columns (one MN atom)
-    const CUtensorMap ma = transposed ? make_map(t.W, t.R, t.C, t.ld, 32)
+    const CUtensorMap ma = transposed
+                               ? make_map(t.W, t.R, t.C, t.ld, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)
                                       : make_map(t.W, t.R, t.C, t.ld, TC_BM);
     const CUtensorMap mb = make_map(Xt + (size_t)n0 * ldt, nb, K, ldt, bn);
     dim3 grid((M + TC_BM - 1) / TC_BM, used);
     // partial sums of this N slab land at part + n0 rows, split stride B x M
     if (transposed)
-      tc_gemm_kernel<true><<<grid, 128, TC_SMEM, t.stream>>>(
-          ma, mb, M, K, nb, bn, per, part + (size_t)n0 * M, M, (size_t)B * M);
+      tc_gemm_kernel<true><<<grid, 128, TC_SMEM, t.stream>>>(ma, mb, M, K, nb, bn, per,
+                                                             part + (size_t)n0 * M, M,
+                                                             (size_t)B * M);
     else
-      tc_gemm_kernel<false><<<grid, 128, TC_SMEM, t.stream>>>(
-          ma, mb, M, K, nb, bn, per, part + (size_t)n0 * M, M, (size_t)B * M);
+      tc_gemm_kernel<false><<<grid, 128, TC_SMEM, t.stream>>>(ma, mb, M, K, nb, bn, per,
+                                                              part + (size_t)n0 * M, M,
+                                                              (size_t)B * M);
     count_launch();
     XB_CUDA(cudaGetLastError());
   }
