@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <initializer_list>
+
 #include "xb_internal.h"
 
 namespace xb {
@@ -140,10 +142,6 @@ static bool temporal_any(const xb_temporal_params &tp) {
   return tp.decay_rate > 0.0 || tp.diffusion_sigma > 0.0 || tp.reset_prob > 0.0;
 }
 
-static void check_finite(const float *v, size_t n, const char *what) { // tile.cpp:65-75
-  for (size_t k = 0; k < n; ++k)
-    if (!std::isfinite(v[k])) raise(std::string(what) + ": non-finite entry");
-}
 
 static void ensure_device() {
   int n = 0;
@@ -212,9 +210,40 @@ static void tile_free(Tile &t) {
   t.s_lr.release();
   if (t.own_stream && t.stream) cudaStreamDestroy(t.stream);
   if (t.bm_count) cudaFreeHost(t.bm_count);
+  if (t.chk_host) cudaFreeHost(t.chk_host);
+  cudaFree(t.chk_dev);
 }
 
 static void sync(Tile &t) { XB_CUDA(cudaStreamSynchronize(t.stream)); }
+
+// check_input's finiteness test (tile.cpp:65-75) on the inputs after their
+// H2D copy: one streaming kernel per array on the tile's stream, then one
+// 4-byte read.  Raises with the reference's message, naming the first bad
+// array in argument order, before any state of the tile changes.
+struct Finite {
+  const float *v;
+  size_t n;
+  const char *what;
+};
+static void check_finite_dev(Tile &t, std::initializer_list<Finite> arrays) {
+  if (!t.chk_dev) {
+    XB_CUDA(cudaMalloc(&t.chk_dev, sizeof(int)));
+    XB_CUDA(cudaMallocHost(&t.chk_host, sizeof(int)));
+  }
+  XB_CUDA(cudaMemsetAsync(t.chk_dev, 0, sizeof(int), t.stream));
+  int bit = 1;
+  for (const Finite &a : arrays) {
+    launch_nonfinite(a.v, a.n, bit, t.chk_dev, t.stream);
+    bit <<= 1;
+  }
+  XB_CUDA(cudaMemcpyAsync(t.chk_host, t.chk_dev, sizeof(int), cudaMemcpyDeviceToHost, t.stream));
+  sync(t);
+  bit = 1;
+  for (const Finite &a : arrays) {
+    if (*t.chk_host & bit) raise(std::string(a.what) + ": non-finite entry");
+    bit <<= 1;
+  }
+}
 
 static void ensure_xi(Tile &t) {
   if (t.xi) return;
@@ -721,10 +750,10 @@ static void forward_host(xb_tile *h, const float *X, int B, float *Y, const xb_i
   Tile &t = h->t;
   if (B < 0) raise("forward: batch must be >= 0");
   if (B == 0) return;
-  check_finite(X, (size_t)B * t.C, "forward");
   float *dX = scratch_as<float>(t.s_y, (size_t)B * (t.C + t.R));
   float *dY = dX + (size_t)B * t.C;
   XB_CUDA(cudaMemcpyAsync(dX, X, sizeof(float) * B * t.C, cudaMemcpyHostToDevice, t.stream));
+  check_finite_dev(t, {{dX, (size_t)B * t.C, "forward"}});
   forward_device(t, dX, B, dY, io);
   XB_CUDA(cudaMemcpyAsync(Y, dY, sizeof(float) * B * t.R, cudaMemcpyDeviceToHost, t.stream));
   sync(t);
@@ -759,10 +788,10 @@ int xb_tile_backward(xb_tile *h, const float *D, int B, float *G) {
     if (B < 0) raise("backward: batch must be >= 0");
     if (B == 0) return;
     if (t.R != t.R_total) raise("backward: row-sharded tile; use xb_tile_backward_partial_dev");
-    check_finite(D, (size_t)B * t.R, "backward");
     float *dD = scratch_as<float>(t.s_y, (size_t)B * (t.C + t.R));
     float *dG = dD + (size_t)B * t.R;
     XB_CUDA(cudaMemcpyAsync(dD, D, sizeof(float) * B * t.R, cudaMemcpyHostToDevice, t.stream));
+    check_finite_dev(t, {{dD, (size_t)B * t.R, "backward"}});
     mvm_backward(t, dD, B, dG, make_io(t.cfg.backward_io), t.k_bwd, t.seq_bwd, nullptr, false,
                  nullptr);
     t.seq_bwd += (uint64_t)B;
@@ -813,13 +842,12 @@ int xb_tile_update(xb_tile *h, const float *X, const float *D, int B, const floa
     Tile &t = h->t;
     if (B < 0) raise("update: batch must be >= 0");
     if (B == 0) return;
-    check_finite(X, (size_t)B * t.C, "update(x)");
-    check_finite(D, (size_t)B * t.R, "update(d)");
-    check_lr_host(X, D, B, t.C, t.R, lr, t.learning_rate);
     float *dX = scratch_as<float>(t.s_y, (size_t)B * (t.C + t.R));
     float *dD = dX + (size_t)B * t.C;
     XB_CUDA(cudaMemcpyAsync(dX, X, sizeof(float) * B * t.C, cudaMemcpyHostToDevice, t.stream));
     XB_CUDA(cudaMemcpyAsync(dD, D, sizeof(float) * B * t.R, cudaMemcpyHostToDevice, t.stream));
+    check_finite_dev(t, {{dX, (size_t)B * t.C, "update(x)"}, {dD, (size_t)B * t.R, "update(d)"}});
+    check_lr_host(X, D, B, t.C, t.R, lr, t.learning_rate);
     update_device(t, dX, dD, B, lr, nullptr, false, nullptr, nullptr, nullptr);
     sync(t);
   });
@@ -830,13 +858,12 @@ int xb_tile_generate_trains(xb_tile *h, const float *X, const float *D, int B, c
   return guard([&] {
     Tile &t = h->t;
     if (B <= 0) raise("generate_trains: batch must be >= 1");
-    check_finite(X, (size_t)B * t.C, "update(x)");
-    check_finite(D, (size_t)B * t.R, "update(d)");
-    check_lr_host(X, D, B, t.C, t.R, lr, t.learning_rate);
     float *dX = scratch_as<float>(t.s_y, (size_t)B * (t.C + t.R));
     float *dD = dX + (size_t)B * t.C;
     XB_CUDA(cudaMemcpyAsync(dX, X, sizeof(float) * B * t.C, cudaMemcpyHostToDevice, t.stream));
     XB_CUDA(cudaMemcpyAsync(dD, D, sizeof(float) * B * t.R, cudaMemcpyHostToDevice, t.stream));
+    check_finite_dev(t, {{dX, (size_t)B * t.C, "update(x)"}, {dD, (size_t)B * t.R, "update(d)"}});
+    check_lr_host(X, D, B, t.C, t.R, lr, t.learning_rate);
     update_device(t, dX, dD, B, lr, nullptr, true, xw, dw, bl);
   });
 }

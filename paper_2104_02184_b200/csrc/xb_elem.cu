@@ -5,9 +5,13 @@
 //   temporal_kernel  decay / diffusion / reset (proj/src/tile.cpp:128-156)
 //   program_kernel   PCM programming noise + drift exponents (proj/src/inference.cpp:34-61)
 //   drift_kernel     w0 (t/t0)^-nu then clip (proj/src/inference.cpp:63-76)
+//   nonfinite_kernel check_input's finiteness test on device-resident inputs
+//                    (proj/src/tile.cpp:65-75)
 //
 // One thread per cell, row-major over [R][ld]; every random draw is addressed
 // by the cell's GLOBAL (row, column) so row shards reproduce the whole tile.
+#include <algorithm>
+
 #include "xb_internal.h"
 
 namespace xb {
@@ -146,7 +150,38 @@ __global__ void __launch_bounds__(EW_THREADS) drift_kernel(float *__restrict__ W
   W[k] = fminf(fmaxf((float)((double)w0[k] * f), p.w), p.z);
 }
 
+// ORs `bit` into *flag if any of v[0..n) is Inf or NaN (exponent all ones):
+// a streaming read, 16-B loads when the pointer allows them
+__global__ void __launch_bounds__(EW_THREADS) nonfinite_kernel(const float *__restrict__ v,
+                                                               size_t n, int bit, int *flag) {
+  const size_t tid = (size_t)blockIdx.x * EW_THREADS + threadIdx.x;
+  const size_t nth = (size_t)gridDim.x * EW_THREADS;
+  uint32_t bad = 0;
+  size_t head = 0;
+  if (((uintptr_t)v & 15) == 0) {
+    const uint4 *v4 = reinterpret_cast<const uint4 *>(v);
+    const size_t n4 = n / 4;
+    for (size_t k = tid; k < n4; k += nth) {
+      const uint4 q = __ldcs(v4 + k);
+      bad |= (~q.x & 0x7f800000u) == 0 || (~q.y & 0x7f800000u) == 0 ||
+             (~q.z & 0x7f800000u) == 0 || (~q.w & 0x7f800000u) == 0;
+    }
+    head = n4 * 4;
+  }
+  const uint32_t *u = reinterpret_cast<const uint32_t *>(v);
+  for (size_t k = head + tid; k < n; k += nth) bad |= (~__ldcs(u + k) & 0x7f800000u) == 0;
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, bit);
+}
+
 } // namespace
+
+void launch_nonfinite(const float *v, size_t n, int bit, int *flag, cudaStream_t s) {
+  if (n == 0) return;
+  const size_t blocks = std::min<size_t>((n / 4 + EW_THREADS - 1) / EW_THREADS + 1, 148 * 8);
+  nonfinite_kernel<<<(unsigned)blocks, EW_THREADS, 0, s>>>(v, n, bit, flag);
+  count_launch();
+  XB_CUDA(cudaGetLastError());
+}
 
 void launch_realize(Tile &t) {
   if (t.R == 0) return;

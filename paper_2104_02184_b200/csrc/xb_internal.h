@@ -65,6 +65,8 @@ struct Tile {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int *bm_count = nullptr; // pinned host word for the bound-management loop
+  int *chk_dev = nullptr;  // input-check flag word (device) and its pinned host copy
+  int *chk_host = nullptr;
 
   Scratch s_words, s_params, s_io, s_y, s_lr;
 
@@ -105,6 +107,8 @@ void launch_temporal(Tile &t, const xb_temporal_params &tp, uint32_t call);
 void launch_temporal_xi(Tile &t);
 void launch_program(Tile &t, const float *target_dev, const xb_inference_model &m, Key key);
 void launch_drift(Tile &t, double ratio);
+// ORs `bit` into the device word *flag if v[0..n) holds an Inf or NaN
+void launch_nonfinite(const float *v, size_t n, int bit, int *flag, cudaStream_t s);
 
 // ---- tcgen05 contraction (xb_mvm_tc.cu) ----
 int tc_splits(int M, int K);

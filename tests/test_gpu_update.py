@@ -222,6 +222,44 @@ def test_errors_match_reference():
         xb.AnalogTile(0, 2, xb.TileSettings(), 1)
 
 
+@pytest.mark.parametrize("shape", [(64, 1024, 8), (37, 101, 5)])
+def test_nonfinite_inputs_leave_tile_untouched(shape):
+    """check_input (tile.cpp:65-75) runs on the device after the H2D copy; an
+    Inf/NaN anywhere (16-B vector body or scalar tail, x or d) raises before
+    the weights or the noise streams move."""
+    R, C, B = shape
+    rng = np.random.default_rng(3)
+    X = rng.uniform(-1, 1, (B, C)).astype(np.float32)
+    D = rng.uniform(-1, 1, (B, R)).astype(np.float32)
+    w0 = rng.uniform(-0.1, 0.1, (R, C)).astype(np.float32)
+    s = xb.TileSettings(device=xb.device_preset("reram_sb"))
+    a, b = xb.AnalogTile(R, C, s, 21), xb.AnalogTile(R, C, s, 21)
+    a.set_weights(w0)
+    b.set_weights(w0)
+    for arr, pos, val, msg in ((X, (B - 1, C - 1), np.nan, "update\\(x\\)"),
+                               (D, (B // 2, 3), np.inf, "update\\(d\\)"),
+                               (D, (B - 1, R - 1), -np.inf, "update\\(d\\)")):
+        bad = arr.copy()
+        bad[pos] = val
+        args = (bad, D) if arr is X else (X, bad)
+        with pytest.raises(xb.Error, match=msg + ": non-finite entry"):
+            a.update(*args, 0.01)
+    Xb = X.copy()
+    Xb[0, C // 2] = np.nan
+    with pytest.raises(xb.Error, match="forward: non-finite entry"):
+        a.forward(Xb)
+    Db = D.copy()
+    Db[B - 1, R - 1] = np.inf
+    with pytest.raises(xb.Error, match="backward: non-finite entry"):
+        a.backward(Db)
+    assert np.array_equal(a.get_weights(), b.get_weights())
+    a.update(X, D, 0.01)
+    b.update(X, D, 0.01)
+    assert np.array_equal(a.get_weights(), b.get_weights())
+    assert np.array_equal(a.forward(X), b.forward(X))
+    assert np.array_equal(a.backward(D), b.backward(D))
+
+
 def test_mean_update_equals_lr_d_xT():
     """Acceptance criterion 2 / test_pulsed.cpp:203-231: E[dW] = lr d x^T within
     2 %.  2048 samples of the same (x, d) in one batched call on a ConstantStep
