@@ -424,27 +424,62 @@ template <int LAW> struct WCell {
 // c2c normal #(8q + r) of a cell's segment is element r of the 8 normals of
 // Philox(k_c2c, (g0 + q, j, i, call)) with g0 the cell's running group count,
 // independent of launch geometry and of row sharding.
-constexpr int PULSE_WARPS = 16;          // rows per CTA
+#ifndef XB_PULSE_WARPS
+#define XB_PULSE_WARPS 16
+#endif
+constexpr int PULSE_WARPS = XB_PULSE_WARPS; // warps per CTA
 constexpr int PULSE_QW = 32;             // stream words per lane
 constexpr int PULSE_CAP = PULSE_QW * 32; // pulses per lane per segment
 
-// CTAs of 512 threads per SM: 3 (40 registers, 48 warps) measured 7 % faster
-// than 2 for the cheap laws; ExpStep's extra live state prefers 2 (64 registers)
-template <int LAW> constexpr int pulse_minb() { return LAW == XB_EXP_STEP ? 2 : 3; }
+// CTAs of 512 threads per SM.  With per-tile CTAs 3 (40 registers, 48 warps)
+// beat 2 by 7 %; with persistent warps (below) 2 CTAs (64 registers, no
+// spills) measured best: 7.9 vs 8.1 ms for the NS update (B200, round 1)
+#ifndef XB_PULSE_MINB
+#define XB_PULSE_MINB 2
+#endif
+template <int LAW> constexpr int pulse_minb() { return LAW == XB_EXP_STEP ? 2 : XB_PULSE_MINB; }
+// samples per vector block of the pre-pass (4: one uint4 of x and of d words;
+// measured 6 % slower than 8)
+#ifndef XB_PULSE_PB
+#define XB_PULSE_PB 8
+#endif
+// persistent warps walk the (row, column block) items: warps drift out of
+// phase, so the ALU-bound pre-pass of some overlaps the FMA/MUFU-bound pulse
+// loop of others (warps of a per-tile CTA grid run the two phases in lockstep)
+#ifndef XB_PULSE_PERSIST
+#define XB_PULSE_PERSIST 1
+#endif
+// ExpStep (register-heavier, 2 CTAs either way) measured 4 % faster per-tile
+template <int LAW> constexpr bool pulse_persist() {
+  return XB_PULSE_PERSIST && LAW != XB_EXP_STEP;
+}
 
 template <int LAW, bool NOISE>
 __global__ void __launch_bounds__(PULSE_WARPS * 32, pulse_minb<LAW>()) pulse_kernel(
     float *__restrict__ W, const float4 *__restrict__ P, int ld, int R, int C,
     const uint32_t *__restrict__ xw, const uint32_t *__restrict__ dw, int ldb, int B, int row0,
-    LawArgs la, RoundKeys rk, uint32_t call) {
+    LawArgs la, RoundKeys rk, uint32_t call, uint32_t one) {
   extern __shared__ uint32_t qsm[]; // [PULSE_WARPS][PULSE_QW][32]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int j = blockIdx.x * 32 + lane;
-  const int i = blockIdx.y * PULSE_WARPS + warp;
-  if (i >= R) return; // warp-uniform: no block-level barriers below
+  uint32_t *q = qsm + warp * (PULSE_QW * 32) + lane;
+  // persistent warps (pulse_persist): each walks (row, 32-column block) items
+  // with a stride of the whole grid; otherwise one item per warp of a 2-D grid
+  constexpr bool persist = pulse_persist<LAW>();
+  const uint32_t ncb = (uint32_t)(C + 31) / 32u;
+  const uint32_t n_items = persist ? (uint32_t)R * ncb : 1u; // < 2^31 for any tile that fits
+  for (uint32_t item = persist ? blockIdx.x * PULSE_WARPS + warp : 0u; item < n_items;
+       item += gridDim.x * PULSE_WARPS) {
+    int i, j;
+    if (persist) {
+      i = (int)(item / ncb);
+      j = (int)(item - (uint32_t)i * ncb) * 32 + lane;
+    } else {
+      j = blockIdx.x * 32 + lane;
+      i = blockIdx.y * PULSE_WARPS + warp;
+      if (i >= R) return; // warp-uniform: no block-level barriers below
+    }
   const bool valid = j < C;
   const size_t idx = (size_t)i * ld + j;
-  uint32_t *q = qsm + warp * (PULSE_QW * 32) + lane;
 
   float w = 0.f;
   WCell<LAW> cell;
@@ -460,12 +495,14 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, pulse_minb<LAW>()) pulse_ker
 
   int b = 0;
   while (b < B) {
-    // ---------------- pre-pass: append this lane's pulses, sample order
-    uint32_t T = 0, acc = 0, qa = q0;
+    // ---------------- pre-pass: append this lane's pulses, sample order.
+    // sh = fill of the open stream word acc, qa = its shared address; the
+    // stream length is T = (qa - q0) / 4 + sh (32 pulses per 128-B word step).
+    uint32_t sh = 0, acc = 0, qa = q0;
     auto append = [&](uint32_t xv, uint32_t dv) {
       const uint32_t k = __popc(xv & dv & xmask);
-      const uint32_t down = (uint32_t)((int32_t)(xv ^ dv) >> 31); // all ones: signs differ
-      const uint32_t sh = T & 31u;
+      uint32_t down; // all ones iff the signs differ: mul.hi by a runtime 1 keeps it on the FMA pipe
+      asm("mul.hi.s32 %0, %1, %2;" : "=r"(down) : "r"(xv ^ dv), "r"(one));
       uint32_t lo; // k ones from bit sh, clipped at bit 31 (BMSK)
       asm("bmsk.clamp.b32 %0, %1, %2;" : "=r"(lo) : "r"(sh), "r"(k));
       acc |= lo & ~down;
@@ -474,75 +511,101 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, pulse_minb<LAW>()) pulse_ker
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(qa), "r"(acc));
         qa += 128u;
         uint32_t hi;
-        asm("bmsk.clamp.b32 %0, %1, %2;" : "=r"(hi) : "r"(0u), "r"(e - 32u));
+        asm("bmsk.clamp.b32 %0, %1, %2;" : "=r"(hi) : "r"(0u), "r"(e & 31u));
         acc = hi & ~down;
       }
-      T += k;
+      sh = e & 31u;
     };
-    // fast path: aligned blocks of 8 samples, vector loads prefetched one block
-    // ahead; a block is taken only if it cannot overflow any lane's stream
-    if ((b & 7) == 0 && b + 8 <= B) {
+    auto stream_len = [&]() { return ((qa - q0) >> 2) + sh; };
+    // fast path: aligned blocks of PB samples, vector loads prefetched one
+    // block ahead; a block is taken only if it cannot overflow any lane's stream
+    constexpr int PB = XB_PULSE_PB, NV = PB / 4;
+    if ((b % PB) == 0 && b + PB <= B) {
       const uint4 *xv4 = reinterpret_cast<const uint4 *>(xline);
       const uint4 *dv4 = reinterpret_cast<const uint4 *>(dline);
-      uint4 xa = __ldg(xv4 + (b >> 2)), xb = __ldg(xv4 + (b >> 2) + 1);
-      uint4 da = __ldg(dv4 + (b >> 2)), db = __ldg(dv4 + (b >> 2) + 1);
+      uint4 xa[NV], da[NV];
+#pragma unroll
+      for (int u = 0; u < NV; ++u) {
+        xa[u] = __ldg(xv4 + (b >> 2) + u);
+        da[u] = __ldg(dv4 + (b >> 2) + u);
+      }
       while (true) {
-        if (__any_sync(0xffffffffu, T + 8u * 31u > (uint32_t)PULSE_CAP)) break;
-        const int bn = b + 8;
-        uint4 nxa = xa, nxb = xb, nda = da, ndb = db;
-        if (bn + 8 <= B) {
-          nxa = __ldg(xv4 + (bn >> 2));
-          nxb = __ldg(xv4 + (bn >> 2) + 1);
-          nda = __ldg(dv4 + (bn >> 2));
-          ndb = __ldg(dv4 + (bn >> 2) + 1);
+        if (__any_sync(0xffffffffu, stream_len() + PB * 31u > (uint32_t)PULSE_CAP)) break;
+        const int bn = b + PB;
+        uint4 nxa[NV], nda[NV];
+#pragma unroll
+        for (int u = 0; u < NV; ++u) {
+          nxa[u] = xa[u];
+          nda[u] = da[u];
         }
-        append(xa.x, da.x);
-        append(xa.y, da.y);
-        append(xa.z, da.z);
-        append(xa.w, da.w);
-        append(xb.x, db.x);
-        append(xb.y, db.y);
-        append(xb.z, db.z);
-        append(xb.w, db.w);
+        if (bn + PB <= B) {
+#pragma unroll
+          for (int u = 0; u < NV; ++u) {
+            nxa[u] = __ldg(xv4 + (bn >> 2) + u);
+            nda[u] = __ldg(dv4 + (bn >> 2) + u);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < NV; ++u) {
+          append(xa[u].x, da[u].x);
+          append(xa[u].y, da[u].y);
+          append(xa[u].z, da[u].z);
+          append(xa[u].w, da[u].w);
+        }
         b = bn;
-        if (b + 8 > B) break;
-        xa = nxa;
-        xb = nxb;
-        da = nda;
-        db = ndb;
+        if (b + PB > B) break;
+#pragma unroll
+        for (int u = 0; u < NV; ++u) {
+          xa[u] = nxa[u];
+          da[u] = nda[u];
+        }
       }
     }
     // careful path, one sample at a time: the batch tail, or a stream near CAP
     while (b < B) {
       const uint32_t xv = __ldg(xline + b), dv = __ldg(dline + b);
-      if (__any_sync(0xffffffffu, T + __popc(xv & dv & xmask) > (uint32_t)PULSE_CAP)) break;
+      if (__any_sync(0xffffffffu, stream_len() + __popc(xv & dv & xmask) > (uint32_t)PULSE_CAP))
+        break;
       append(xv, dv);
       ++b;
     }
-    if (T & 31u) asm volatile("st.shared.u32 [%0], %1;" ::"r"(qa), "r"(acc));
+    if (sh) asm volatile("st.shared.u32 [%0], %1;" ::"r"(qa), "r"(acc));
+    const uint32_t T = stream_len();
+    const uint32_t minT = __reduce_min_sync(0xffffffffu, T);
     const uint32_t maxT = __reduce_max_sync(0xffffffffu, T);
     __syncwarp();
 
-    // ---------------- pulse loop: pulse n of every lane with n < T
-    for (uint32_t n0 = 0; n0 < maxT; n0 += 32) {
+    // ---------------- pulse loop: pulse n of every lane with n < T.  Words
+    // below the shortest stream need no per-pulse activity test.
+    auto pulses8 = [&](uint32_t word, uint32_t n, int sh8, bool check) {
+      float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (NOISE) normal8_rk(g0 + (n >> 3), jg, ig, call, rk, z);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const float f = NOISE ? fmaf(la.std, z[v], 1.0f) : 1.0f;
+        const float wn = cell.step(w, f, (word >> (sh8 + v)) & 1u);
+        if (!check || n + v < T) w = wn;
+      }
+    };
+    uint32_t n0 = 0;
+    for (; n0 + 32u <= minT; n0 += 32u) {
+      const uint32_t word = q[(n0 >> 5) * 32];
+#pragma unroll
+      for (int u4 = 0; u4 < 32; u4 += 8) pulses8(word, n0 + u4, u4, false);
+    }
+    for (; n0 < maxT; n0 += 32u) {
       const uint32_t word = q[(n0 >> 5) * 32];
 #pragma unroll
       for (int u4 = 0; u4 < 32; u4 += 8) {
         if (n0 + u4 >= maxT) break;
-        float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        if (NOISE) normal8_rk(g0 + ((n0 + u4) >> 3), jg, ig, call, rk, z);
-#pragma unroll
-        for (int v = 0; v < 8; ++v) {
-          const float f = NOISE ? fmaf(la.std, z[v], 1.0f) : 1.0f;
-          const float wn = cell.step(w, f, (word >> (u4 + v)) & 1u);
-          if (n0 + u4 + v < T) w = wn;
-        }
+        pulses8(word, n0 + u4, u4, true);
       }
     }
     g0 += (T + 7u) >> 3;
     __syncwarp();
   }
   if (valid) W[idx] = w;
+  }
 }
 
 template <int LAW, bool NOISE>
@@ -556,8 +619,21 @@ static void pulse_dispatch(Tile &t, const uint32_t *xw, const uint32_t *dw, int 
     configured = true;
   }
   dim3 grid((t.C + 31) / 32, (t.R + PULSE_WARPS - 1) / PULSE_WARPS);
+  if (pulse_persist<LAW>()) {
+    static int blocks = 0;
+    if (!blocks) {
+      int per_sm = 0, dev = 0, sms = 0;
+      XB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pulse_kernel<LAW, NOISE>,
+                                                            PULSE_WARPS * 32, smem));
+      XB_CUDA(cudaGetDevice(&dev));
+      XB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      blocks = std::max(1, per_sm) * sms;
+    }
+    const long items = (long)t.R * ((t.C + 31) / 32);
+    grid = dim3((unsigned)std::min<long>(blocks, (items + PULSE_WARPS - 1) / PULSE_WARPS));
+  }
   pulse_kernel<LAW, NOISE><<<grid, PULSE_WARPS * 32, smem, t.stream>>>(
-      t.W, t.P, t.ld, t.R, t.C, xw, dw, ldb, B, t.row0, la, round_keys(t.k_c2c), call);
+      t.W, t.P, t.ld, t.R, t.C, xw, dw, ldb, B, t.row0, la, round_keys(t.k_c2c), call, 1u);
   count_launch();
   XB_CUDA(cudaGetLastError());
 }
