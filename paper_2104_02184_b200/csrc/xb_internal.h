@@ -113,7 +113,7 @@ void launch_nonfinite(const float *v, size_t n, int bit, int *flag, cudaStream_t
 // ---- tcgen05 contraction (xb_mvm_tc.cu) ----
 int tc_splits(int M, int K);
 int tc_used_splits(int K, int splits);
-void tc_gemm(Tile &t, bool transposed, const float *Xt, int ldt, int B, float *part,
+void tc_gemm(Tile &t, bool transposed, bool x3, const float *Xt, int ldt, int B, float *part,
              int splits);
 
 // ---- noisy MVM (xb_mvm.cu) ----

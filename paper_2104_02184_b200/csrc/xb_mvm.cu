@@ -350,9 +350,10 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io, Key
   const int K = TRANS ? t.R : t.C; // contraction length
   const int M = TRANS ? t.C : t.R; // outputs
   if (B <= 0) return;
-  // tensor-core contraction for the forward direction at TF32 (B >= 16);
-  // the fp32 SIMT kernel otherwise (exact-fp32 parity mode, tiny batches)
-  const bool tc = t.cfg.mvm_precision == XB_MVM_TF32 && B >= 16;
+  // tensor-core contraction at TF32 / 3xTF32 (B >= 16); the fp32 SIMT kernel
+  // otherwise (exact-fp32 parity mode, tiny batches)
+  const bool x3 = t.cfg.mvm_precision == XB_MVM_TF32X3;
+  const bool tc = (t.cfg.mvm_precision == XB_MVM_TF32 || x3) && B >= 16;
   const int splits = tc ? tc_used_splits(K, tc_splits(M, K)) : 1;
   const int ldt = (K + 3) & ~3; // x~ rows padded to 16 bytes (TMA global stride)
   MvmScratch s = carve(t, B, ldt, M, splits);
@@ -366,7 +367,7 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io, Key
     XB_CUDA(cudaGetLastError());
     int nsplit = 1;
     if (tc) { // re-issue passes recompute the whole batch on the tensor cores (cheap)
-      tc_gemm(t, TRANS, s.xt, ldt, B, s.acc, splits);
+      tc_gemm(t, TRANS, x3, s.xt, ldt, B, s.acc, splits);
       nsplit = splits;
     } else {
       gemm<TRANS>(t, s, M, K, ldt, B, first);

@@ -29,11 +29,18 @@ namespace {
 
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 32; // fp32 elements per 128-byte swizzle row
-constexpr int TC_STAGES = 4;
 constexpr int TC_MAX_BN = 256;
 constexpr int TC_A_BYTES = TC_BM * TC_BK * 4;     // 16 KB
 constexpr int TC_B_BYTES = TC_MAX_BN * TC_BK * 4; // 32 KB (max)
-constexpr int TC_SMEM = TC_STAGES * (TC_A_BYTES + TC_B_BYTES) + 1024 /*align*/ + 256 /*bars*/;
+// TF32: 4-stage ring of (A, B).  3xTF32: 2-stage ring of (A_hi, B_hi, A_lo, B_lo)
+template <bool X3> constexpr int tc_stages() { return X3 ? 2 : 4; }
+template <bool X3> constexpr int tc_stage_bytes() {
+  return (X3 ? 2 : 1) * (TC_A_BYTES + TC_B_BYTES);
+}
+template <bool X3> constexpr int tc_smem() {
+  return tc_stages<X3>() * tc_stage_bytes<X3>() + 1024 /*align*/ + 256 /*bars*/;
+}
+template <bool X3> constexpr int tc_threads() { return X3 ? 256 : 128; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -119,37 +126,60 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
                  "=r"(r[30]), "=r"(r[31])                                                      \
                : "r"(taddr))
 
+// split x into hi = x with the low 13 mantissa bits cleared (exactly a TF32
+// value, so the tensor core reads it unchanged whether it truncates or
+// rounds) and lo = x - hi (exact in fp32; TF32-rounded by the MMA)
+__device__ __forceinline__ void split_tf32(float4 &v, float4 &lo) {
+  float *e = reinterpret_cast<float *>(&v), *l = reinterpret_cast<float *>(&lo);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const float hi = __uint_as_float(__float_as_uint(e[c]) & 0xffffe000u);
+    l[c] = e[c] - hi;
+    e[c] = hi;
+  }
+}
+
 // A_MN = false: A = W tile [128 rows][32 K] (forward, K-major)
 // A_MN = true : A = W^T tile, i.e. W[32 K-rows][128 columns] (backward, MN-major):
 //               four 32x32 TMA boxes (128B/32B-atom swizzle) per stage, one per
 //               32-column MN atom, 4 KB apart
-template <bool A_MN>
-__global__ void __launch_bounds__(128, 1)
+// X3 = true   : 3xTF32.  Warps 2-7 split every landed stage in place into hi
+//               and a lo copy (generic-proxy writes, then fence.proxy.async);
+//               the MMA thread issues hi*hi + hi*lo + lo*hi per K-step, which
+//               recovers ~fp32 accuracy of the products at 3x the tensor work.
+//               Warps 4-7 run the epilogue (TMEM lane quarter = warp % 4).
+template <bool A_MN, bool X3>
+__global__ void __launch_bounds__(tc_threads<X3>(), 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                    int M, int K, int B, int bn, int kblocks_per_split, float *__restrict__ part,
                    int ldp, size_t split_stride) {
+  constexpr int STAGES = tc_stages<X3>();
+  constexpr int SB = tc_stage_bytes<X3>();
   extern __shared__ uint8_t smem_raw[];
-  // 1024-byte alignment for the 128-byte swizzle atoms
+  // 1024-byte alignment for the 128-byte swizzle atoms; stage s holds
+  // [A | B | A_lo | B_lo] at offsets 0, 16K, 48K, 64K
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t *sa = smem;
-  uint8_t *sb = smem + TC_STAGES * TC_A_BYTES;
-  uint64_t *bars = (uint64_t *)(sb + TC_STAGES * TC_B_BYTES);
-  uint32_t *tmem_slot = (uint32_t *)(bars + 2 * TC_STAGES + 1);
-  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + TC_STAGES),
-                 done = smem_u32(bars + 2 * TC_STAGES);
+  uint64_t *bars = (uint64_t *)(smem + STAGES * SB);
+  uint32_t *tmem_slot = (uint32_t *)(bars + 3 * STAGES + 1);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES),
+                 conv0 = smem_u32(bars + 2 * STAGES), done = smem_u32(bars + 3 * STAGES);
+  auto stage_a = [&](int s) { return smem + s * SB; };
+  auto stage_b = [&](int s) { return smem + s * SB + TC_A_BYTES; };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * TC_BM;
   const int split = blockIdx.y;
   const int kb0 = split * kblocks_per_split;
   const int nkb = min(kblocks_per_split, (K + TC_BK - 1) / TC_BK - kb0);
+  constexpr int CONV_THREADS = tc_threads<X3>() - 64;
 
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_b)) : "memory");
-    for (int s = 0; s < TC_STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, 1);
+      mbar_init(conv0 + 8 * s, CONV_THREADS);
     }
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -169,59 +199,93 @@ __global__ void __launch_bounds__(128, 1)
   if (warp == 0 && lane == 0 && nkb > 0) {
     // ---------------- TMA producer
     for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % TC_STAGES;
-      const uint32_t ph = (uint32_t)(kb / TC_STAGES) & 1u;
+      const int s = kb % STAGES;
+      const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
       mbar_wait(empty0 + 8 * s, ph ^ 1u);
       mbar_expect_tx(full0 + 8 * s, TC_A_BYTES + b_bytes);
       const int kk = (kb0 + kb) * TC_BK;
       if (A_MN) {
 #pragma unroll
         for (int a = 0; a < TC_BM / 32; ++a)
-          tma_load_2d(smem_u32(sa + s * TC_A_BYTES + a * 4096), &tm_a, full0 + 8 * s,
-                      m0 + 32 * a, kk);
+          tma_load_2d(smem_u32(stage_a(s) + a * 4096), &tm_a, full0 + 8 * s, m0 + 32 * a, kk);
       } else {
-        tma_load_2d(smem_u32(sa + s * TC_A_BYTES), &tm_a, full0 + 8 * s, kk, m0);
+        tma_load_2d(smem_u32(stage_a(s)), &tm_a, full0 + 8 * s, kk, m0);
       }
-      tma_load_2d(smem_u32(sb + s * TC_B_BYTES), &tm_b, full0 + 8 * s, kk, 0);
+      tma_load_2d(smem_u32(stage_b(s)), &tm_b, full0 + 8 * s, kk, 0);
     }
   } else if (warp == 1 && lane == 0 && nkb > 0) {
     // ---------------- MMA issuer (one thread)
     const uint32_t idesc = idesc_tf32(bn, A_MN);
+    const uint32_t a_lbo = A_MN ? 4096u : 16u, a_sbo = A_MN ? 512u : 1024u;
+    const uint32_t a_layout = A_MN ? 1u : 2u;
+    // one MMA = 8 tf32 of K: K-major advances 32 bytes (+2 in 16-byte units),
+    // MN-major advances 8 K-rows = two 4-row groups (+1024 bytes = +64)
+    const uint32_t a_step = A_MN ? 64u : 2u;
     for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % TC_STAGES;
-      const uint32_t ph = (uint32_t)(kb / TC_STAGES) & 1u;
-      mbar_wait(full0 + 8 * s, ph);
+      const int s = kb % STAGES;
+      const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
+      mbar_wait((X3 ? conv0 : full0) + 8 * s, ph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint64_t da = A_MN ? umma_desc(smem_u32(sa + s * TC_A_BYTES), 4096u, 512u, 1u)
-                               : umma_desc(smem_u32(sa + s * TC_A_BYTES), 16u, 1024u, 2u);
-      const uint64_t db = umma_desc(smem_u32(sb + s * TC_B_BYTES), 16u, 1024u, 2u);
-      // one MMA = 8 tf32 of K: K-major advances 32 bytes (+2 in 16-byte units),
-      // MN-major advances 8 K-rows = two 4-row groups (+1024 bytes = +64)
+      const uint64_t da = umma_desc(smem_u32(stage_a(s)), a_lbo, a_sbo, a_layout);
+      const uint64_t db = umma_desc(smem_u32(stage_b(s)), 16u, 1024u, 2u);
 #pragma unroll
-      for (int k = 0; k < TC_BK / 8; ++k)
-        mma_tf32(tmem, da + (A_MN ? 64u : 2u) * k, db + 2u * k, idesc, (kb | k) != 0);
+      for (int k = 0; k < TC_BK / 8; ++k) {
+        mma_tf32(tmem, da + a_step * k, db + 2u * k, idesc, (kb | k) != 0);
+        if (X3) {
+          const uint64_t dal =
+              umma_desc(smem_u32(stage_a(s) + TC_A_BYTES + TC_B_BYTES), a_lbo, a_sbo, a_layout);
+          const uint64_t dbl = umma_desc(smem_u32(stage_b(s) + TC_A_BYTES + TC_B_BYTES), 16u,
+                                         1024u, 2u);
+          mma_tf32(tmem, da + a_step * k, dbl + 2u * k, idesc, 1u);
+          mma_tf32(tmem, dal + a_step * k, db + 2u * k, idesc, 1u);
+        }
+      }
       mma_commit(empty0 + 8 * s); // smem stage free once these MMAs retire
     }
     mma_commit(done);
+  } else if (X3 && warp >= 2 && nkb > 0) {
+    // ---------------- hi/lo split of each landed stage (3xTF32)
+    const int ct = threadIdx.x - 64;
+    const int na4 = TC_A_BYTES / 16, nb4 = (int)(b_bytes / 16);
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
+      mbar_wait(full0 + 8 * s, ph);
+      float4 *a4 = reinterpret_cast<float4 *>(stage_a(s));
+      float4 *al4 = reinterpret_cast<float4 *>(stage_a(s) + TC_A_BYTES + TC_B_BYTES);
+      for (int e = ct; e < na4 + nb4; e += CONV_THREADS) {
+        // B words follow A's 16 KB directly, in both the hi and the lo halves
+        float4 v = a4[e], lo;
+        split_tf32(v, lo);
+        a4[e] = v;
+        al4[e] = lo;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(conv0 + 8 * s) : "memory");
+    }
   }
   __syncwarp();
 
   // ---------------- epilogue: TMEM -> registers -> partial sums
-  if (nkb > 0) {
-    mbar_wait(done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  }
-  const int o = m0 + warp * 32 + lane;
-  float *dst = part + (size_t)split * split_stride;
-  for (int c0 = 0; c0 < bn; c0 += 32) {
-    uint32_t r[32];
-    XB_TMEM_LD32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, r);
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (o < M) {
+  constexpr int EPI_W0 = X3 ? 4 : 0;
+  if (warp >= EPI_W0 && warp < EPI_W0 + 4) {
+    if (nkb > 0) {
+      mbar_wait(done, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    const int quarter = warp & 3;
+    const int o = m0 + quarter * 32 + lane;
+    float *dst = part + (size_t)split * split_stride;
+    for (int c0 = 0; c0 < bn; c0 += 32) {
+      uint32_t r[32];
+      XB_TMEM_LD32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, r);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (o < M) {
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        const int b = c0 + c;
-        if (b < B) dst[(size_t)b * ldp + o] = nkb > 0 ? __uint_as_float(r[c]) : 0.f;
+        for (int c = 0; c < 32; ++c) {
+          const int b = c0 + c;
+          if (b < B) dst[(size_t)b * ldp + o] = nkb > 0 ? __uint_as_float(r[c]) : 0.f;
+        }
       }
     }
   }
@@ -278,17 +342,24 @@ int tc_splits(int M, int K) {
 // contraction on tcgen05: part[s][b][o] (split stride B x M).
 //   forward : o = row of W, K = columns of W   (A = W, K-major)
 //   backward: o = column of W, K = rows of W   (A = W^T, MN-major)
-void tc_gemm(Tile &t, bool transposed, const float *Xt, int ldt, int B, float *part,
-             int splits) {
-  const int M = transposed ? t.C : t.R, K = transposed ? t.R : t.C;
+template <bool A_MN, bool X3>
+static void launch_tc(dim3 grid, cudaStream_t st, const CUtensorMap &ma, const CUtensorMap &mb,
+                      int M, int K, int nb, int bn, int per, float *part, size_t split_stride) {
   static bool configured = false;
   if (!configured) {
-    XB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<false>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
-    XB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<true>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
+    XB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<A_MN, X3>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem<X3>()));
     configured = true;
   }
+  tc_gemm_kernel<A_MN, X3><<<grid, tc_threads<X3>(), tc_smem<X3>(), st>>>(
+      ma, mb, M, K, nb, bn, per, part, M, split_stride);
+  count_launch();
+  XB_CUDA(cudaGetLastError());
+}
+
+void tc_gemm(Tile &t, bool transposed, bool x3, const float *Xt, int ldt, int B, float *part,
+             int splits) {
+  const int M = transposed ? t.C : t.R, K = transposed ? t.R : t.C;
   const int kbs = (K + TC_BK - 1) / TC_BK;
   const int per = (kbs + splits - 1) / splits;
   const int used = (kbs + per - 1) / per;
@@ -299,22 +370,19 @@ void tc_gemm(Tile &t, bool transposed, const float *Xt, int ldt, int B, float *p
     // the backward box 32 rows (K) x 32 columns (one MN atom)
     const CUtensorMap ma = transposed
                                ? make_map(t.W, t.R, t.C, t.ld, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)
-                                      : make_map(t.W, t.R, t.C, t.ld, TC_BM);
+                               : make_map(t.W, t.R, t.C, t.ld, TC_BM);
     const CUtensorMap mb = make_map(Xt + (size_t)n0 * ldt, nb, K, ldt, bn);
-    dim3 grid((M + TC_BM - 1) / TC_BM, used);
+    const dim3 grid((M + TC_BM - 1) / TC_BM, used);
     // partial sums of this N slab land at part + n0 rows, split stride B x M
+    float *p = part + (size_t)n0 * M;
+    const size_t ss = (size_t)B * M;
     if (transposed)
-      tc_gemm_kernel<true><<<grid, 128, TC_SMEM, t.stream>>>(ma, mb, M, K, nb, bn, per,
-                                                             part + (size_t)n0 * M, M,
-                                                             (size_t)B * M);
+      x3 ? launch_tc<true, true>(grid, t.stream, ma, mb, M, K, nb, bn, per, p, ss)
+         : launch_tc<true, false>(grid, t.stream, ma, mb, M, K, nb, bn, per, p, ss);
     else
-      tc_gemm_kernel<false><<<grid, 128, TC_SMEM, t.stream>>>(ma, mb, M, K, nb, bn, per,
-                                                              part + (size_t)n0 * M, M,
-                                                              (size_t)B * M);
-    count_launch();
-    XB_CUDA(cudaGetLastError());
+      x3 ? launch_tc<false, true>(grid, t.stream, ma, mb, M, K, nb, bn, per, p, ss)
+         : launch_tc<false, false>(grid, t.stream, ma, mb, M, K, nb, bn, per, p, ss);
   }
-  (void)used;
 }
 
 int tc_used_splits(int K, int splits) {

@@ -203,7 +203,7 @@ def test_tcgen05_tf32_forward(shape, B):
     X = np.random.default_rng(4).uniform(-1, 1, (B, d_in)).astype(np.float32)
     ref = X.astype(np.float64) @ W.T.astype(np.float64)
     out = {}
-    for prec in (xb.MVM_FP32, xb.MVM_TF32):
+    for prec in (xb.MVM_FP32, xb.MVM_TF32, xb.MVM_TF32X3):
         t = xb.AnalogTile(d_out, d_in, cfg_io(io, io, prec), 5)
         t.set_weights(W)
         out[prec] = t.forward(X).astype(np.float64)
@@ -213,9 +213,13 @@ def test_tcgen05_tf32_forward(shape, B):
         np.linalg.norm(W.astype(np.float64), axis=1)[None, :]
     err32 = np.abs(out[xb.MVM_FP32] - ref) / scale
     errtf = np.abs(out[xb.MVM_TF32] - ref) / scale
+    errx3 = np.abs(out[xb.MVM_TF32X3] - ref) / scale
     assert err32.max() < 1e-5, err32.max()
     assert errtf.max() < 2e-3, errtf.max()
+    # 3xTF32 (hi*hi + hi*lo + lo*hi on tcgen05) recovers fp32-level products
+    assert errx3.max() < 1e-5, errx3.max()
     assert not np.array_equal(out[xb.MVM_FP32], out[xb.MVM_TF32])
+    assert not np.array_equal(out[xb.MVM_FP32], out[xb.MVM_TF32X3])
 
 
 def test_tcgen05_noisy_forward_statistics():
@@ -300,7 +304,7 @@ def test_tcgen05_tf32_backward(shape, B):
     D = np.random.default_rng(14).uniform(-1, 1, (B, d_out)).astype(np.float32)
     ref = D.astype(np.float64) @ W.astype(np.float64)
     out = {}
-    for prec in (xb.MVM_FP32, xb.MVM_TF32):
+    for prec in (xb.MVM_FP32, xb.MVM_TF32, xb.MVM_TF32X3):
         t = xb.AnalogTile(d_out, d_in, cfg_io(io, io, prec), 5)
         t.set_weights(W)
         out[prec] = t.backward(D).astype(np.float64)
@@ -308,8 +312,10 @@ def test_tcgen05_tf32_backward(shape, B):
         np.linalg.norm(W.astype(np.float64), axis=0)[None, :]
     assert (np.abs(out[xb.MVM_FP32] - ref) / scale).max() < 1e-5
     assert (np.abs(out[xb.MVM_TF32] - ref) / scale).max() < 2e-3
+    assert (np.abs(out[xb.MVM_TF32X3] - ref) / scale).max() < 1e-5
     if B >= 16:
         assert not np.array_equal(out[xb.MVM_FP32], out[xb.MVM_TF32])
+        assert not np.array_equal(out[xb.MVM_FP32], out[xb.MVM_TF32X3])
 
 
 def test_tcgen05_forward_odd_widths():
