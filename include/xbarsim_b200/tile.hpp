@@ -45,7 +45,7 @@ enum class NoiseManagement { none = XB_NM_NONE, abs_max = XB_NM_ABS_MAX };
 enum class PulseType { stochastic = XB_PULSE_STOCHASTIC,
                        deterministic_implicit = XB_PULSE_DETERMINISTIC };
 enum class BoundManagement { none = XB_BM_NONE, iterative = XB_BM_ITERATIVE };
-enum class MvmPrecision { fp32 = XB_MVM_FP32, tf32 = XB_MVM_TF32 };
+enum class MvmPrecision { fp32 = XB_MVM_FP32, tf32 = XB_MVM_TF32, tf32x3 = XB_MVM_TF32X3 };
 
 // proj/include/xbarsim/device.hpp:24-39
 struct DeviceParams {
@@ -83,6 +83,21 @@ struct UpdateParams {
   int bl = 31;
   bool bl_management = false;
   PulseType pulse_type = PulseType::stochastic;
+};
+
+// proj/include/xbarsim/pulsed.hpp:37-50: Bernoulli pulse trains, slot-major
+struct PulseTrains {
+  int bl = 0;
+  int x_lines = 0;
+  int d_lines = 0;
+  std::vector<uint8_t> x_bits, d_bits;
+
+  bool x_bit(int slot, int line) const {
+    return x_bits[static_cast<size_t>(slot) * x_lines + line] != 0;
+  }
+  bool d_bit(int slot, int line) const {
+    return d_bits[static_cast<size_t>(slot) * d_lines + line] != 0;
+  }
 };
 
 // proj/include/xbarsim/tile.hpp:24-36
@@ -164,6 +179,42 @@ public:
 private:
   int rows_ = 0, cols_ = 0;
   std::vector<double> data_;
+};
+
+// proj/include/xbarsim/device.hpp:41-49: per-crosspoint sampled parameters
+struct DeviceRealization {
+  double dw_min_up = 0.0;
+  double dw_min_down = 0.0;
+  double w_max = 0.0;
+  double w_min = 0.0;
+  double slope = 0.0;
+  double gamma = 0.0;
+};
+
+// proj/include/xbarsim/device.hpp:58-79: host snapshot of the realized device
+// array (the B200 tile keeps it in HBM as fp32 SoA; device() downloads it)
+class DeviceMatrix {
+public:
+  DeviceMatrix() = default;
+  DeviceMatrix(const DeviceParams &params, int rows, int cols)
+      : params_(params), rows_(rows), cols_(cols), cells_(static_cast<size_t>(rows) * cols) {}
+  int rows() const { return rows_; }
+  int cols() const { return cols_; }
+  const DeviceParams &params() const { return params_; }
+  const DeviceRealization &at(int i, int j) const {
+    return cells_[static_cast<size_t>(i) * cols_ + j];
+  }
+  DeviceRealization &at(int i, int j) { return cells_[static_cast<size_t>(i) * cols_ + j]; }
+  // proj/src/device.cpp:79-88: clip to the cell's own bounds
+  double clip(int i, int j, double w) const {
+    const DeviceRealization &c = at(i, j);
+    return std::fmin(std::fmax(w, c.w_min), c.w_max);
+  }
+
+private:
+  DeviceParams params_;
+  int rows_ = 0, cols_ = 0;
+  std::vector<DeviceRealization> cells_;
 };
 
 namespace detail {
@@ -398,7 +449,60 @@ public:
     const xb_temporal_params c = detail::to_c(tp);
     check(xb_tile_temporal_step(h_, &c));
   }
+  // proj/include/xbarsim/tile.hpp:103-104 / proj/src/tile.cpp:158-169: apply
+  // already-generated trains (one sample) to the devices; flip inverts every
+  // pulse.  Lines with sign 0 fire nothing (pulsed.cpp:96-112).  The GPU packs
+  // a line's slots into one word, so bl <= 31.
+  void apply_pulse_trains(const PulseTrains &trains, std::span<const int> sign_x,
+                          std::span<const int> sign_d, bool flip_direction) {
+    if (trains.x_lines != d_in_ || trains.d_lines != d_out_ ||
+        static_cast<int>(sign_x.size()) != d_in_ || static_cast<int>(sign_d.size()) != d_out_)
+      throw Error("apply_coincidences: trains do not conform to tile shape");
+    if (trains.bl < 0 || trains.bl > 31)
+      throw Error("apply_pulse_trains: bl " + std::to_string(trains.bl) +
+                  " exceeds the 31 slots of a packed B200 train word");
+    flush();
+    auto pack = [&](int lines, std::span<const int> sign, bool is_x) {
+      std::vector<uint32_t> w(static_cast<size_t>(lines), 0u);
+      for (int l = 0; l < lines; ++l) {
+        if (sign[l] == 0) continue;
+        uint32_t v = sign[l] < 0 ? 0x80000000u : 0u;
+        for (int t = 0; t < trains.bl; ++t)
+          if (is_x ? trains.x_bit(t, l) : trains.d_bit(t, l)) v |= 1u << t;
+        w[static_cast<size_t>(l)] = v;
+      }
+      return w;
+    };
+    const std::vector<uint32_t> xw = pack(d_in_, sign_x, true);
+    const std::vector<uint32_t> dw = pack(d_out_, sign_d, false);
+    check(xb_tile_apply_trains(h_, xw.data(), dw.data(), 1, flip_direction ? 1 : 0));
+  }
+
   const TileSettings &settings() const { return settings_; }
+  // proj/include/xbarsim/tile.hpp:107: the realized devices (downloaded)
+  const DeviceMatrix &device() const {
+    std::vector<float> up(static_cast<size_t>(d_out_) * d_in_), dn(up.size()), mx(up.size()),
+        mn(up.size());
+    check(xb_tile_get_device(h_, up.data(), dn.data(), mx.data(), mn.data()));
+    device_ = DeviceMatrix(settings_.device, d_out_, d_in_);
+    for (int i = 0; i < d_out_; ++i)
+      for (int j = 0; j < d_in_; ++j) {
+        const size_t k = static_cast<size_t>(i) * d_in_ + j;
+        DeviceRealization &c = device_.at(i, j);
+        c.dw_min_up = up[k];
+        c.dw_min_down = dn[k];
+        c.w_max = mx[k];
+        c.w_min = mn[k];
+        c.slope = settings_.device.slope; // nominal copies (device.cpp:43-44)
+        c.gamma = settings_.device.gamma;
+      }
+    return device_;
+  }
+  // proj/include/xbarsim/tile.hpp:108: the stored (clipped) weights
+  const Matrix &stored_weights() const {
+    weights_ = get_weights();
+    return weights_;
+  }
   double learning_rate() const { return xb_tile_learning_rate(h_); }
   void set_learning_rate(double lr) { check(xb_tile_set_learning_rate(h_, lr)); }
 
@@ -428,6 +532,8 @@ private:
   xb_tile *h_ = nullptr;
   int d_out_ = 0, d_in_ = 0;
   mutable std::vector<float> qx_, qd_, qlr_;
+  mutable DeviceMatrix device_;
+  mutable Matrix weights_;
 };
 
 // proj/include/xbarsim/compound.hpp:93-131, on the GPU (updates go straight
@@ -457,7 +563,10 @@ public:
   ~TransferTile() override {
     if (h_) xb_transfer_destroy(h_);
   }
-  TransferTile(const TransferTile &) = delete;
+  // proj/include/xbarsim/compound.hpp:109-111: deep copy
+  TransferTile(const TransferTile &o) : d_out_(o.d_out_), d_in_(o.d_in_), s_(o.s_) {
+    check(xb_transfer_clone(o.h_, &h_));
+  }
   TransferTile &operator=(const TransferTile &) = delete;
 
   int d_out() const override { return d_out_; }
@@ -484,8 +593,13 @@ public:
     const float l = static_cast<float>(lr);
     check(xb_transfer_update(h_, xf.data(), df.data(), 1, &l));
   }
-  std::vector<double> forward_noisy(std::span<const double> x, double) override {
-    return forward(x);
+  // proj/src/compound.cpp:228-238
+  std::vector<double> forward_noisy(std::span<const double> x, double extra) override {
+    detail::check_input(x, d_in_, "forward");
+    auto xf = detail::to_f(x);
+    std::vector<float> y(d_out_);
+    check(xb_transfer_forward_noisy(h_, xf.data(), 1, y.data(), extra));
+    return detail::to_d(y);
   }
   Matrix get_weights() const override {
     std::vector<float> w(static_cast<size_t>(d_out_) * d_in_);
@@ -500,7 +614,7 @@ public:
   }
   void end_minibatch() override { check(xb_transfer_end_minibatch(h_)); }
   std::unique_ptr<TileBase> clone() const override {
-    throw Error("TransferTile::clone: not supported on the B200 path");
+    return std::make_unique<TransferTile>(*this);
   }
   void transfer_step() { check(xb_transfer_step(h_)); }
   long transfer_events() const { return xb_transfer_events(h_); }

@@ -237,6 +237,12 @@ int xb_transfer_create(const xb_transfer_config *cfg, int d_out, int d_in, uint6
                        xb_transfer **out);
 int xb_transfer_destroy(xb_transfer *t);
 int xb_transfer_forward(xb_transfer *t, const float *X, int B, float *Y);
+/* forward with sigma_w <- hypot(sigma_w, extra) on both members (compound.cpp:228-238) */
+int xb_transfer_forward_noisy(xb_transfer *t, const float *X, int B, float *Y,
+                              double extra_sigma);
+/* deep copy: both members with their RNG positions, counter and column cursor
+   (compound.hpp:109-111) */
+int xb_transfer_clone(const xb_transfer *t, xb_transfer **out);
 int xb_transfer_backward(xb_transfer *t, const float *D, int B, float *G);
 int xb_transfer_update(xb_transfer *t, const float *X, const float *D, int B, const float *lr);
 int xb_transfer_end_minibatch(xb_transfer *t);

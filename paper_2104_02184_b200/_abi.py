@@ -136,6 +136,8 @@ SIGNATURES = {
     "xb_transfer_destroy": (C.c_int, [_P]),
     "xb_transfer_forward": (C.c_int, [_P, _fp, C.c_int, _fp]),
     "xb_transfer_backward": (C.c_int, [_P, _fp, C.c_int, _fp]),
+    "xb_transfer_forward_noisy": (C.c_int, [_P, _fp, C.c_int, _fp, C.c_double]),
+    "xb_transfer_clone": (C.c_int, [_P, C.POINTER(_P)]),
     "xb_transfer_update": (C.c_int, [_P, _fp, _fp, C.c_int, _fp]),
     "xb_transfer_end_minibatch": (C.c_int, [_P]),
     "xb_transfer_step": (C.c_int, [_P]),

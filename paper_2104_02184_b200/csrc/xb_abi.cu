@@ -1049,6 +1049,39 @@ int xb_transfer_forward(xb_transfer *t, const float *X, int B, float *Y) {
   });
 }
 
+int xb_transfer_forward_noisy(xb_transfer *t, const float *X, int B, float *Y,
+                              double extra_sigma) {
+  return guard([&] { // compound.cpp:228-238
+    forward_host(t->slow, X, B, Y, noisy_io(t->slow->t.cfg.forward_io, extra_sigma));
+    if (t->cfg.gamma != 0.0) {
+      std::vector<float> ya((size_t)B * t->fast->t.R);
+      forward_host(t->fast, X, B, ya.data(), noisy_io(t->fast->t.cfg.forward_io, extra_sigma));
+      mix_outputs(Y, ya.data(), ya.size(), t->cfg.gamma);
+    }
+  });
+}
+
+int xb_transfer_clone(const xb_transfer *t, xb_transfer **out) {
+  *out = nullptr;
+  xb_tile *fast = nullptr, *slow = nullptr; // compound.hpp:109-111: deep copy
+  int rc = xb_tile_clone(t->fast, &fast);
+  if (rc) return rc;
+  rc = xb_tile_clone(t->slow, &slow);
+  if (rc) {
+    xb_tile_destroy(fast);
+    return rc;
+  }
+  auto *c = new xb_transfer;
+  c->cfg = t->cfg;
+  c->fast = fast;
+  c->slow = slow;
+  c->counter = t->counter;
+  c->events = t->events;
+  c->next_column = t->next_column;
+  *out = c;
+  return 0;
+}
+
 int xb_transfer_backward(xb_transfer *t, const float *D, int B, float *G) {
   int rc = xb_tile_backward(t->slow, D, B, G); // compound.cpp:217-226
   if (rc || t->cfg.gamma == 0.0) return rc;

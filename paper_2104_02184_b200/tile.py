@@ -384,11 +384,14 @@ class TransferTile:
     """GPU Tiki-Taka compound (proj/include/xbarsim/compound.hpp:93-131)."""
 
     def __init__(self, d_out: int, d_in: int, settings: Optional[TransferConfig] = None,
-                 seed: int = 0):
-        settings = settings if settings is not None else TransferSettings()
-        h = C.c_void_p()
-        _check(_lib.xb_transfer_create(C.byref(settings), int(d_out), int(d_in),
-                                       C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), C.byref(h)))
+                 seed: int = 0, _handle=None):
+        if _handle is not None:
+            h = _handle
+        else:
+            settings = settings if settings is not None else TransferSettings()
+            h = C.c_void_p()
+            _check(_lib.xb_transfer_create(C.byref(settings), int(d_out), int(d_in),
+                                           C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), C.byref(h)))
         self._h = h
         self._d_out, self._d_in = int(d_out), int(d_in)
         self._fast = AnalogTile(0, 0, _handle=C.c_void_p(_lib.xb_transfer_fast(h)))
@@ -421,6 +424,20 @@ class TransferTile:
         Y = np.empty((X.shape[0], self._d_out), dtype=np.float32)
         _check(_lib.xb_transfer_forward(self._h, _ptr(X), X.shape[0], _ptr(Y)))
         return Y[0] if single else Y
+
+    def forward_noisy(self, x, extra_weight_sigma: float):
+        """compound.cpp:228-238: both members read with the extra weight noise."""
+        X, single = _batch(x, self._d_in, "forward")
+        Y = np.empty((X.shape[0], self._d_out), dtype=np.float32)
+        _check(_lib.xb_transfer_forward_noisy(self._h, _ptr(X), X.shape[0], _ptr(Y),
+                                              float(extra_weight_sigma)))
+        return Y[0] if single else Y
+
+    def clone(self) -> "TransferTile":
+        """compound.hpp:109-111: deep copy (members, RNG positions, schedule)."""
+        h = C.c_void_p()
+        _check(_lib.xb_transfer_clone(self._h, C.byref(h)))
+        return TransferTile(self._d_out, self._d_in, _handle=h)
 
     def backward(self, d):
         D, single = _batch(d, self._d_out, "backward")

@@ -206,6 +206,67 @@ int main() {
     for (int k = 0; k < 4; ++k) CHECK(std::fabs(w.data()[k] - target.data()[k] * f) < 1e-6);
     CHECK(throws([&] { drift_to(tile, st, 0.5); }, "drift_to: t < t0"));
   });
+  run("apply_pulse_trains: saturated, flipped and zero-sign lines (test_pulsed.cpp:66-79)", [] {
+    AnalogTile t(3, 2, quiet_settings(0.001, 1.0), 21);
+    PulseTrains tr;
+    tr.bl = 31;
+    tr.x_lines = 2;
+    tr.d_lines = 3;
+    tr.x_bits.assign(31 * 2, 1);
+    tr.d_bits.assign(31 * 3, 1);
+    const std::vector<int> sx{1, 1}, sd{-1, 1, 0};
+    t.apply_pulse_trains(tr, sx, sd, false);
+    Matrix w = t.stored_weights();
+    for (int j = 0; j < 2; ++j) {
+      CHECK(std::fabs(w(0, j) + 31 * 0.001) < 1e-6);
+      CHECK(std::fabs(w(1, j) - 31 * 0.001) < 1e-6);
+      CHECK(w(2, j) == 0.0);
+    }
+    t.apply_pulse_trains(tr, sx, sd, true); // flip undoes it (constant step)
+    w = t.get_weights();
+    for (int k = 0; k < 6; ++k) CHECK(std::fabs(w.data()[k]) < 1e-6);
+    tr.bl = 40;
+    CHECK(throws([&] { t.apply_pulse_trains(tr, sx, sd, false); }, "31 slots"));
+  });
+  run("device(): nominal realization 1.1 / 0.9 dw_min (test_devices.cpp:17-31)", [] {
+    TileSettings s = quiet_settings(0.002, 0.6);
+    s.device.up_down = 0.1;
+    AnalogTile t(4, 3, s, 22);
+    const DeviceMatrix &dm = t.device();
+    CHECK(dm.rows() == 4 && dm.cols() == 3);
+    for (int i = 0; i < 4; ++i)
+      for (int j = 0; j < 3; ++j) {
+        CHECK(std::fabs(dm.at(i, j).dw_min_up - 0.0022) < 1e-9);
+        CHECK(std::fabs(dm.at(i, j).dw_min_down - 0.0018) < 1e-9);
+        CHECK(std::fabs(dm.at(i, j).w_max - 0.6) < 1e-7);
+        CHECK(std::fabs(dm.at(i, j).w_min + 0.6) < 1e-7);
+      }
+    CHECK(dm.clip(0, 0, 5.0) == dm.at(0, 0).w_max);
+  });
+  run("TransferTile clone and forward_noisy (compound.hpp:109-111, compound.cpp:228-238)", [] {
+    TransferSettings s;
+    s.forward_io = io_off();
+    s.backward_io = io_off();
+    s.fast_device = device_preset("reram_sb");
+    s.slow_device = device_preset("reram_sb");
+    s.transfer_every = 2;
+    s.gamma = 0.5;
+    TransferTile a(4, 3, s, 31);
+    a.set_weights(random_matrix(4, 3, 0.2, 32));
+    for (int k = 0; k < 3; ++k)
+      a.update(std::vector<double>{1.0, -0.5, 0.25}, std::vector<double>{0.8, -0.6, 0.1, 0.3},
+               0.05);
+    auto c = a.clone();
+    for (int k = 0; k < 5; ++k) {
+      const std::vector<double> x{0.3, 0.7, -0.2}, d{-0.4, 0.9, 0.2, -0.1};
+      a.update(x, d, 0.05);
+      c->update(x, d, 0.05);
+    }
+    CHECK(a.get_weights() == c->get_weights());
+    const std::vector<double> x{0.5, -0.25, 1.0};
+    CHECK(a.forward_noisy(x, 0.0) == a.forward(x));
+    CHECK(!(a.forward_noisy(x, 0.1) == a.forward(x)));
+  });
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;
 }

@@ -127,6 +127,45 @@ def test_compound_forward_mixes_gamma():
         assert t.forward([1.0])[0] == pytest.approx(want, abs=1e-6)
 
 
+def test_transfer_clone_is_deep_copy():
+    """compound.hpp:109-111: the clone carries both members, their RNG
+    positions and the transfer schedule, so identical inputs keep them equal."""
+    s = xb.TransferSettings()
+    s.fast_device = xb.device_preset("reram_sb")
+    s.slow_device = xb.device_preset("reram_sb")
+    s.transfer_every, s.gamma = 3, 0.5
+    rng = np.random.default_rng(5)
+    a = xb.TransferTile(16, 12, s, 41)
+    a.set_weights(rng.uniform(-0.2, 0.2, (16, 12)))
+    X = rng.uniform(-1, 1, (10, 12)).astype(np.float32)
+    D = rng.uniform(-1, 1, (10, 16)).astype(np.float32)
+    a.update(X[:4], D[:4], 0.05)
+    c = a.clone()
+    assert c.transfer_events() == a.transfer_events()
+    a.update(X[4:], D[4:], 0.05)
+    c.update(X[4:], D[4:], 0.05)
+    assert c.transfer_events() == a.transfer_events() > 0
+    assert np.array_equal(a.get_weights(), c.get_weights())
+    assert np.array_equal(a.forward(X), c.forward(X))
+
+
+def test_transfer_forward_noisy_variance():
+    """compound.cpp:228-238: both members read with sigma_w = extra, so the
+    output variance is extra^2 |x|^2 (1 + gamma^2) on perfect IO."""
+    s = ideal_transfer()
+    s.gamma = 0.5
+    t = xb.TransferTile(8, 64, s, 17)
+    W = np.random.default_rng(3).uniform(-0.3, 0.3, (8, 64))
+    t.set_weights(W)  # C = W, A = 0
+    x = np.random.default_rng(4).uniform(-1, 1, 64).astype(np.float32)
+    assert np.array_equal(t.forward_noisy(x, 0.0), t.forward(x))
+    Y = t.forward_noisy(np.tile(x, (4000, 1)), 0.05).astype(np.float64)
+    var = 0.05 ** 2 * float(x.astype(np.float64) @ x) * (1 + 0.5 ** 2)
+    exact = W @ x.astype(np.float64)
+    assert np.all(np.abs(Y.mean(axis=0) - exact) < 5 * np.sqrt(var / 4000))
+    assert abs(Y.var(axis=0).mean() / var - 1) < 0.06
+
+
 # ------------------------------------------------------------------ inference
 def wide_tile(rows, cols, seed, perfect=True):
     s = xb.TileSettings(device=quiet_device(0.001, 100.0))
