@@ -363,8 +363,11 @@ public:
     d_in_ = d_in;
   }
   ~AnalogTile() override {
-    if (h_) xb_tile_destroy(h_);
+    if (h_ && owned_) xb_tile_destroy(h_);
   }
+  // borrowed view of a member tile owned by a compound (not destroyed here)
+  AnalogTile(xb_tile *borrowed, int d_out, int d_in, const TileSettings &settings)
+      : settings_(settings), h_(borrowed), d_out_(d_out), d_in_(d_in), owned_(false) {}
   AnalogTile(const AnalogTile &o) : settings_(o.settings_), d_out_(o.d_out_), d_in_(o.d_in_) {
     // proj/include/xbarsim/tile.hpp:91: clone = deep copy (queued updates applied first)
     o.flush();
@@ -531,6 +534,7 @@ private:
   TileSettings settings_;
   xb_tile *h_ = nullptr;
   int d_out_ = 0, d_in_ = 0;
+  bool owned_ = true;
   mutable std::vector<float> qx_, qd_, qlr_;
   mutable DeviceMatrix device_;
   mutable Matrix weights_;
@@ -623,6 +627,134 @@ private:
   int d_out_, d_in_;
   TransferSettings s_;
   xb_transfer *h_ = nullptr;
+};
+
+// proj/include/xbarsim/compound.hpp:15-28
+enum class UnitCellPolicy { round_robin = XB_UC_ROUND_ROBIN, all_together = XB_UC_ALL_TOGETHER };
+struct UnitCellSettings {
+  std::vector<DeviceParams> devices;
+  std::vector<double> gains;
+  UnitCellPolicy policy = UnitCellPolicy::all_together;
+  IOParams forward_io;
+  IOParams backward_io;
+  UpdateParams update;
+  TemporalParams temporal;
+  MvmPrecision mvm_precision = MvmPrecision::fp32;
+};
+
+// proj/include/xbarsim/compound.hpp:30-71, on the GPU: members are B200 tiles,
+// the effective weight sum_k g_k W_k lives in HBM
+class UnitCellTile : public TileBase {
+public:
+  UnitCellTile(int d_out, int d_in, const UnitCellSettings &s, uint64_t seed)
+      : d_out_(d_out), d_in_(d_in), s_(s) {
+    xb_unitcell_config c;
+    xb_default_unitcell_config(&c);
+    if (s.devices.empty()) throw Error("unit_cell.devices: need at least one device");
+    if (s.gains.size() != s.devices.size())
+      throw Error("unit_cell.gains: length must match devices");
+    if (s.devices.size() > XB_MAX_CELL_DEVICES)
+      throw Error("unit_cell.devices: at most " + std::to_string(XB_MAX_CELL_DEVICES) +
+                  " on the B200 path");
+    c.n_devices = static_cast<int32_t>(s.devices.size());
+    for (size_t k = 0; k < s.devices.size(); ++k) {
+      c.devices[k] = detail::to_c(s.devices[k]);
+      c.gains[k] = s.gains[k];
+    }
+    c.policy = static_cast<int32_t>(s.policy);
+    c.forward_io = detail::to_c(s.forward_io);
+    c.backward_io = detail::to_c(s.backward_io);
+    c.update = detail::to_c(s.update);
+    c.temporal = detail::to_c(s.temporal);
+    c.mvm_precision = static_cast<int32_t>(s.mvm_precision);
+    check(xb_unitcell_create(&c, d_out, d_in, seed, &h_));
+    bind();
+  }
+  UnitCellTile(const UnitCellTile &o) : d_out_(o.d_out_), d_in_(o.d_in_), s_(o.s_) {
+    check(xb_unitcell_clone(o.h_, &h_));
+    bind();
+  }
+  UnitCellTile &operator=(const UnitCellTile &) = delete;
+  ~UnitCellTile() override {
+    if (h_) xb_unitcell_destroy(h_);
+  }
+
+  int d_out() const override { return d_out_; }
+  int d_in() const override { return d_in_; }
+  // compound.cpp:82-107: length check only (no finiteness check, unlike AnalogTile)
+  std::vector<double> forward(std::span<const double> x) override {
+    length(x, d_in_, "forward");
+    auto xf = detail::to_f(x);
+    std::vector<float> y(d_out_);
+    check(xb_unitcell_forward(h_, xf.data(), 1, y.data()));
+    return detail::to_d(y);
+  }
+  std::vector<double> backward(std::span<const double> d) override {
+    length(d, d_out_, "backward");
+    auto df = detail::to_f(d);
+    std::vector<float> g(d_in_);
+    check(xb_unitcell_backward(h_, df.data(), 1, g.data()));
+    return detail::to_d(g);
+  }
+  std::vector<double> forward_noisy(std::span<const double> x, double extra) override {
+    length(x, d_in_, "forward");
+    auto xf = detail::to_f(x);
+    std::vector<float> y(d_out_);
+    check(xb_unitcell_forward_noisy(h_, xf.data(), 1, y.data(), extra));
+    return detail::to_d(y);
+  }
+  // compound.cpp:109-147
+  void update(std::span<const double> x, std::span<const double> d, double lr) override {
+    if (static_cast<int>(x.size()) != d_in_ || static_cast<int>(d.size()) != d_out_)
+      throw Error("update: x/d lengths do not match tile shape");
+    auto xf = detail::to_f(x);
+    auto df = detail::to_f(d);
+    const float l = static_cast<float>(lr);
+    check(xb_unitcell_update(h_, xf.data(), df.data(), 1, &l));
+  }
+  Matrix get_weights() const override {
+    std::vector<float> w(static_cast<size_t>(d_out_) * d_in_);
+    check(xb_unitcell_get_weights(h_, w.data()));
+    Matrix m(d_out_, d_in_);
+    for (size_t k = 0; k < w.size(); ++k) m.data()[k] = w[k];
+    return m;
+  }
+  void set_weights(const Matrix &w) override {
+    std::vector<float> f(w.data(), w.data() + w.size());
+    check(xb_unitcell_set_weights(h_, f.data()));
+  }
+  void end_minibatch() override { check(xb_unitcell_end_minibatch(h_)); }
+  std::unique_ptr<TileBase> clone() const override {
+    return std::make_unique<UnitCellTile>(*this);
+  }
+  int n_members() const { return static_cast<int>(members_.size()); }
+  // compound.hpp:53: read-only view of member k (weights, device realization)
+  const AnalogTile &member(int k) const { return *members_.at(static_cast<size_t>(k)); }
+
+private:
+  static void length(std::span<const double> v, int expected, const char *what) {
+    if (static_cast<int>(v.size()) != expected)
+      throw Error(std::string(what) + ": length " + std::to_string(v.size()) + ", expected " +
+                  std::to_string(expected));
+  }
+  void bind() {
+    members_.clear();
+    for (int k = 0; k < xb_unitcell_n_members(h_); ++k) {
+      TileSettings m; // compound.cpp:31-42
+      m.device = s_.devices[static_cast<size_t>(k)];
+      m.forward_io = s_.forward_io;
+      m.backward_io = s_.backward_io;
+      m.update = s_.update;
+      m.temporal = s_.temporal;
+      m.mvm_precision = s_.mvm_precision;
+      members_.push_back(
+          std::make_unique<AnalogTile>(xb_unitcell_member(h_, k), d_out_, d_in_, m));
+    }
+  }
+  int d_out_, d_in_;
+  UnitCellSettings s_;
+  xb_unitcell *h_ = nullptr;
+  std::vector<std::unique_ptr<AnalogTile>> members_;
 };
 
 // ---- PCM inference, proj/include/xbarsim/inference.hpp:49-70 ----

@@ -128,8 +128,23 @@ typedef struct xb_transfer_config {
   xb_io_params transfer_io;
 } xb_transfer_config;
 
+/* proj/include/xbarsim/compound.hpp:15-28 (vectors -> fixed arrays of
+ * n_devices <= XB_MAX_CELL_DEVICES) plus the additive precision mode */
+#define XB_MAX_CELL_DEVICES 8
+enum { XB_UC_ROUND_ROBIN = 0, XB_UC_ALL_TOGETHER = 1 }; /* UnitCellPolicy order */
+typedef struct xb_unitcell_config {
+  int32_t n_devices, policy; /* policy default XB_UC_ALL_TOGETHER */
+  xb_device_params devices[XB_MAX_CELL_DEVICES];
+  double gains[XB_MAX_CELL_DEVICES];
+  xb_io_params forward_io, backward_io;
+  xb_update_params update;
+  int32_t mvm_precision;
+  xb_temporal_params temporal;
+} xb_unitcell_config;
+
 typedef struct xb_tile xb_tile;
 typedef struct xb_transfer xb_transfer;
+typedef struct xb_unitcell xb_unitcell;
 
 /* ---- library ---- */
 int xb_abi_version(void);
@@ -252,6 +267,31 @@ int xb_transfer_set_weights(xb_transfer *t, const float *w);
 long xb_transfer_events(const xb_transfer *t);
 xb_tile *xb_transfer_fast(xb_transfer *t);
 xb_tile *xb_transfer_slow(xb_transfer *t);
+
+/* ---- UnitCellTile (proj/src/compound.cpp:12-174) ----
+ * Members are full B200 tiles (member 0 shares the compound's seed, member k
+ * gets derive(seed, "cell_member", k)); the effective weight sum_k g_k W_k is
+ * kept in HBM and refreshed after any member changes.  update() draws ONE set
+ * of trains per sample from the compound's "update" stream with grain
+ * |g| dw_min (round_robin: the member's; all_together: the sum) and fires it on
+ * the member(s), flipped for negative gains.  Member handles are borrowed and
+ * read-only through the compound. */
+void xb_default_unitcell_config(xb_unitcell_config *c);
+int xb_unitcell_create(const xb_unitcell_config *cfg, int d_out, int d_in, uint64_t seed,
+                       xb_unitcell **out);
+int xb_unitcell_destroy(xb_unitcell *u);
+int xb_unitcell_clone(const xb_unitcell *u, xb_unitcell **out);
+int xb_unitcell_forward(xb_unitcell *u, const float *X, int B, float *Y);
+int xb_unitcell_forward_noisy(xb_unitcell *u, const float *X, int B, float *Y,
+                              double extra_sigma);
+int xb_unitcell_backward(xb_unitcell *u, const float *D, int B, float *G);
+/* B sequential UnitCellTile::update calls; lr may be NULL (0.01 each) */
+int xb_unitcell_update(xb_unitcell *u, const float *X, const float *D, int B, const float *lr);
+int xb_unitcell_get_weights(xb_unitcell *u, float *w);
+int xb_unitcell_set_weights(xb_unitcell *u, const float *w);
+int xb_unitcell_end_minibatch(xb_unitcell *u);
+int xb_unitcell_n_members(const xb_unitcell *u);
+xb_tile *xb_unitcell_member(xb_unitcell *u, int k);
 
 #ifdef __cplusplus
 }

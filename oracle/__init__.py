@@ -71,6 +71,17 @@ class TransferSettings(C.Structure):
                 ("has_transfer_io", _i), ("gamma", _d), ("transfer_io", IOParams)]
 
 
+MAX_CELL_DEVICES = 8
+UC_ROUND_ROBIN, UC_ALL_TOGETHER = 0, 1
+
+
+class UnitCellSettings(C.Structure):
+    _fields_ = [("n_devices", _i), ("policy", _i), ("devices", DeviceParams * MAX_CELL_DEVICES),
+                ("gains", _d * MAX_CELL_DEVICES), ("forward_io", IOParams),
+                ("backward_io", IOParams), ("update", UpdateParams), ("_pad", _i),
+                ("temporal", TemporalParams)]
+
+
 class InferenceModel(C.Structure):
     _fields_ = [("prog_noise_scale", _d), ("prog_c0", _d), ("prog_c1", _d), ("prog_c2", _d),
                 ("read_noise_scale", _d), ("nu_mean", _d), ("nu_std", _d), ("t0", _d),
@@ -163,6 +174,18 @@ class Oracle:
             "or_transfer_get_weights": (C.c_int, [_P, _dp]),
             "or_transfer_set_weights": (C.c_int, [_P, _dp]),
             "or_transfer_events": (C.c_long, [_P]),
+            "or_unitcell_new": (_P, [C.c_int, C.c_int, C.POINTER(UnitCellSettings), C.c_uint64]),
+            "or_unitcell_clone": (_P, [_P]),
+            "or_unitcell_free": (None, [_P]),
+            "or_unitcell_forward": (C.c_int, [_P, _dp, _dp]),
+            "or_unitcell_backward": (C.c_int, [_P, _dp, _dp]),
+            "or_unitcell_forward_noisy": (C.c_int, [_P, _dp, C.c_double, _dp]),
+            "or_unitcell_update": (C.c_int, [_P, _dp, _dp, C.c_double]),
+            "or_unitcell_get_weights": (C.c_int, [_P, _dp]),
+            "or_unitcell_set_weights": (C.c_int, [_P, _dp]),
+            "or_unitcell_end_minibatch": (C.c_int, [_P]),
+            "or_unitcell_n_members": (C.c_int, [_P]),
+            "or_unitcell_member": (_P, [_P, C.c_int]),
             "or_transfer_fast": (_P, [_P]),
             "or_transfer_slow": (_P, [_P]),
             "or_program": (C.c_int, [_P, _dp, C.POINTER(InferenceModel), _P, _dp, _dp]),
@@ -177,7 +200,8 @@ class Oracle:
             fn.argtypes = args
         for name in ("or_default_device", "or_default_io", "or_perfect_io", "or_default_update",
                      "or_default_temporal", "or_default_tile_settings",
-                     "or_default_transfer_settings", "or_default_inference_model"):
+                     "or_default_transfer_settings", "or_default_inference_model",
+                     "or_default_unitcell_settings"):
             getattr(L, name).restype = None
 
     # ---------------------------------------------------------------- helpers
@@ -194,6 +218,7 @@ class Oracle:
             "temporal": (TemporalParams, "or_default_temporal"),
             "tile": (TileSettings, "or_default_tile_settings"),
             "transfer": (TransferSettings, "or_default_transfer_settings"),
+            "unitcell": (UnitCellSettings, "or_default_unitcell_settings"),
             "inference": (InferenceModel, "or_default_inference_model"),
         }[kind]
         obj = cls()
@@ -247,6 +272,12 @@ class Oracle:
         if not h:
             raise OracleError(self.lib.or_last_error().decode())
         return Tile(self, h, d_out, d_in, own=True)
+
+    def unitcell(self, d_out, d_in, settings, seed) -> "UnitCell":
+        h = self.lib.or_unitcell_new(d_out, d_in, C.byref(settings), C.c_uint64(seed))
+        if not h:
+            raise OracleError(self.lib.or_last_error().decode())
+        return UnitCell(self, h, d_out, d_in)
 
     def transfer(self, d_out, d_in, settings, seed) -> "Transfer":
         h = self.lib.or_transfer_new(d_out, d_in, C.byref(settings), C.c_uint64(seed))
@@ -440,6 +471,60 @@ class Transfer:
 
     def events(self) -> int:
         return self.o.lib.or_transfer_events(self.h)
+
+
+class UnitCell:
+    """Oracle UnitCellTile (proj/include/xbarsim/compound.hpp:30-71)."""
+
+    def __init__(self, o: Oracle, h, d_out, d_in):
+        self.o, self.h, self.d_out, self.d_in = o, h, d_out, d_in
+        self.members = [Tile(o, o.lib.or_unitcell_member(h, k), d_out, d_in, own=False)
+                        for k in range(o.lib.or_unitcell_n_members(h))]
+
+    def __del__(self):
+        try:
+            self.o.lib.or_unitcell_free(self.h)
+        except Exception:
+            pass
+
+    def clone(self) -> "UnitCell":
+        return UnitCell(self.o, self.o.lib.or_unitcell_clone(self.h), self.d_out, self.d_in)
+
+    def forward(self, x):
+        x = _f64(x)
+        y = np.zeros(self.d_out)
+        self.o._check(self.o.lib.or_unitcell_forward(self.h, _dptr(x), _dptr(y)))
+        return y
+
+    def forward_noisy(self, x, extra):
+        x = _f64(x)
+        y = np.zeros(self.d_out)
+        self.o._check(self.o.lib.or_unitcell_forward_noisy(self.h, _dptr(x), float(extra),
+                                                           _dptr(y)))
+        return y
+
+    def backward(self, d):
+        d = _f64(d)
+        g = np.zeros(self.d_in)
+        self.o._check(self.o.lib.or_unitcell_backward(self.h, _dptr(d), _dptr(g)))
+        return g
+
+    def update(self, x, d, lr):
+        x = _f64(x)
+        d = _f64(d)
+        self.o._check(self.o.lib.or_unitcell_update(self.h, _dptr(x), _dptr(d), float(lr)))
+
+    def end_minibatch(self):
+        self.o._check(self.o.lib.or_unitcell_end_minibatch(self.h))
+
+    def get_weights(self):
+        w = np.zeros((self.d_out, self.d_in))
+        self.o._check(self.o.lib.or_unitcell_get_weights(self.h, _dptr(w)))
+        return w
+
+    def set_weights(self, w):
+        w = _f64(w)
+        self.o._check(self.o.lib.or_unitcell_set_weights(self.h, _dptr(w)))
 
 
 _cache: dict[str, Oracle] = {}

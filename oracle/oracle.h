@@ -90,9 +90,23 @@ typedef struct or_inference_model {
   int32_t compensation_probes, _pad;
 } or_inference_model;
 
+/* proj/include/xbarsim/compound.hpp:15-28 (vectors -> fixed arrays) */
+#define OR_MAX_CELL_DEVICES 8
+enum { OR_UC_ROUND_ROBIN = 0, OR_UC_ALL_TOGETHER = 1 };
+typedef struct or_unitcell_settings {
+  int32_t n_devices, policy;
+  or_device_params devices[OR_MAX_CELL_DEVICES];
+  double gains[OR_MAX_CELL_DEVICES];
+  or_io_params forward_io, backward_io;
+  or_update_params update;
+  int32_t _pad;
+  or_temporal_params temporal;
+} or_unitcell_settings;
+
 typedef struct or_rng or_rng;
 typedef struct or_tile or_tile;
 typedef struct or_transfer or_transfer;
+typedef struct or_unitcell or_unitcell;
 
 const char *or_last_error(void);
 /* "restatement" or "reference" -- which implementation this library is */
@@ -174,6 +188,21 @@ long or_transfer_events(const or_transfer *t);
 or_tile *or_transfer_fast(or_transfer *t);
 or_tile *or_transfer_slow(or_transfer *t);
 
+
+/* UnitCellTile -- proj/src/compound.cpp:12-174 */
+void or_default_unitcell_settings(or_unitcell_settings *s);
+or_unitcell *or_unitcell_new(int d_out, int d_in, const or_unitcell_settings *s, uint64_t seed);
+or_unitcell *or_unitcell_clone(const or_unitcell *t);
+void or_unitcell_free(or_unitcell *t);
+int or_unitcell_forward(or_unitcell *t, const double *x, double *y);
+int or_unitcell_backward(or_unitcell *t, const double *d, double *g);
+int or_unitcell_forward_noisy(or_unitcell *t, const double *x, double extra_sigma, double *y);
+int or_unitcell_update(or_unitcell *t, const double *x, const double *d, double lr);
+int or_unitcell_get_weights(const or_unitcell *t, double *w);
+int or_unitcell_set_weights(or_unitcell *t, const double *w);
+int or_unitcell_end_minibatch(or_unitcell *t);
+int or_unitcell_n_members(const or_unitcell *t);
+or_tile *or_unitcell_member(or_unitcell *t, int k);
 /* ---- PCM inference (proj/src/inference.cpp:14-110) ---- */
 int or_program(or_tile *t, const double *target, const or_inference_model *m, or_rng *rng,
                double *w0_out, double *nu_out);

@@ -145,6 +145,21 @@ TransferSettings to_ref(const or_transfer_settings &s) {
   return t;
 }
 
+UnitCellSettings to_ref(const or_unitcell_settings &s) {
+  UnitCellSettings u;
+  for (int k = 0; k < s.n_devices && k < OR_MAX_CELL_DEVICES; ++k) {
+    u.devices.push_back(to_ref(s.devices[k]));
+    u.gains.push_back(s.gains[k]);
+  }
+  u.policy = s.policy == OR_UC_ROUND_ROBIN ? UnitCellPolicy::round_robin
+                                           : UnitCellPolicy::all_together;
+  u.forward_io = to_ref(s.forward_io);
+  u.backward_io = to_ref(s.backward_io);
+  u.update = to_ref(s.update);
+  u.temporal = to_ref(s.temporal);
+  return u;
+}
+
 InferenceNoiseModel to_ref(const or_inference_model &m) {
   InferenceNoiseModel r;
   r.prog_noise_scale = m.prog_noise_scale;
@@ -185,6 +200,14 @@ struct or_tile {
 struct or_transfer {
   std::unique_ptr<TransferTile> t;
   or_tile fast, slow;
+};
+struct or_unitcell {
+  std::unique_ptr<UnitCellTile> t;
+  or_tile members[OR_MAX_CELL_DEVICES];
+  void bind() {
+    for (int k = 0; k < t->n_members(); ++k)
+      members[k].ptr = const_cast<AnalogTile *>(&t->member(k));
+  }
 };
 
 extern "C" {
@@ -451,6 +474,65 @@ int or_transfer_set_weights(or_transfer *t, const double *w) {
 long or_transfer_events(const or_transfer *t) { return t->t->transfer_events(); }
 or_tile *or_transfer_fast(or_transfer *t) { return &t->fast; }
 or_tile *or_transfer_slow(or_transfer *t) { return &t->slow; }
+
+void or_default_unitcell_settings(or_unitcell_settings *s) {
+  std::memset(s, 0, sizeof *s);
+  UnitCellSettings r;
+  s->n_devices = 1;
+  from_ref(DeviceParams{}, &s->devices[0]);
+  s->gains[0] = 1.0;
+  s->policy = r.policy == UnitCellPolicy::round_robin ? OR_UC_ROUND_ROBIN : OR_UC_ALL_TOGETHER;
+  from_ref(r.forward_io, &s->forward_io);
+  from_ref(r.backward_io, &s->backward_io);
+  or_default_update(&s->update);
+}
+or_unitcell *or_unitcell_new(int d_out, int d_in, const or_unitcell_settings *s, uint64_t seed) {
+  or_unitcell *t = nullptr;
+  guard([&] {
+    auto u = std::make_unique<UnitCellTile>(d_out, d_in, to_ref(*s), seed);
+    t = new or_unitcell;
+    t->t = std::move(u);
+    t->bind();
+  });
+  return t;
+}
+or_unitcell *or_unitcell_clone(const or_unitcell *src) {
+  auto *t = new or_unitcell;
+  t->t = std::make_unique<UnitCellTile>(*src->t);
+  t->bind();
+  return t;
+}
+void or_unitcell_free(or_unitcell *t) { delete t; }
+int or_unitcell_forward(or_unitcell *t, const double *x, double *y) {
+  return guard([&] { copy_out(t->t->forward(std::span<const double>(x, t->t->d_in())), y); });
+}
+int or_unitcell_backward(or_unitcell *t, const double *d, double *g) {
+  return guard([&] { copy_out(t->t->backward(std::span<const double>(d, t->t->d_out())), g); });
+}
+int or_unitcell_forward_noisy(or_unitcell *t, const double *x, double extra, double *y) {
+  return guard([&] {
+    copy_out(t->t->forward_noisy(std::span<const double>(x, t->t->d_in()), extra), y);
+  });
+}
+int or_unitcell_update(or_unitcell *t, const double *x, const double *d, double lr) {
+  return guard([&] {
+    t->t->update(std::span<const double>(x, t->t->d_in()),
+                 std::span<const double>(d, t->t->d_out()), lr);
+  });
+}
+int or_unitcell_get_weights(const or_unitcell *t, double *w) {
+  Matrix m = t->t->get_weights();
+  std::memcpy(w, m.data(), sizeof(double) * m.size());
+  return 0;
+}
+int or_unitcell_set_weights(or_unitcell *t, const double *w) {
+  return guard([&] { t->t->set_weights(to_matrix(w, t->t->d_out(), t->t->d_in())); });
+}
+int or_unitcell_end_minibatch(or_unitcell *t) {
+  return guard([&] { t->t->end_minibatch(); });
+}
+int or_unitcell_n_members(const or_unitcell *t) { return t->t->n_members(); }
+or_tile *or_unitcell_member(or_unitcell *t, int k) { return &t->members[k]; }
 
 int or_program(or_tile *t, const double *target, const or_inference_model *m, or_rng *rng,
                double *w0_out, double *nu_out) {

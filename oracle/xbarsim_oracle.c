@@ -966,6 +966,205 @@ or_tile *or_transfer_fast(or_transfer *t) { return t->fast; }
 or_tile *or_transfer_slow(or_transfer *t) { return t->slow; }
 
 /* ======================================================================
+ * UnitCellTile -- proj/src/compound.cpp:12-174
+ * ====================================================================== */
+
+struct or_unitcell {
+  int d_out, d_in;
+  or_unitcell_settings s;
+  or_tile *members[OR_MAX_CELL_DEVICES];
+  int next_member; /* round-robin cursor, persists across mini-batches */
+  or_rng rng_forward, rng_backward, rng_update;
+  double *effective; /* [d_out * d_in], valid when !dirty */
+  int dirty;
+};
+
+void or_default_unitcell_settings(or_unitcell_settings *s) {
+  memset(s, 0, sizeof *s);
+  s->n_devices = 1;
+  or_default_device(&s->devices[0]);
+  s->gains[0] = 1.0;
+  s->policy = OR_UC_ALL_TOGETHER; /* compound.hpp:20 */
+  or_default_io(&s->forward_io);
+  or_default_io(&s->backward_io);
+  or_default_update(&s->update);
+  or_default_temporal(&s->temporal);
+}
+
+/* proj/src/compound.cpp:12-27 */
+static int unitcell_validate(const or_unitcell_settings *s) {
+  char buf[96];
+  if (s->n_devices < 1) return fail("unit_cell.devices: need at least one device");
+  if (s->n_devices > OR_MAX_CELL_DEVICES) return fail("unit_cell.gains: length must match devices");
+  for (int k = 0; k < s->n_devices; ++k)
+    if (!isfinite(s->gains[k])) return fail("unit_cell.gains: entries must be finite");
+  for (int k = 0; k < s->n_devices; ++k) {
+    snprintf(buf, sizeof buf, "unit_cell.devices[%d]", k);
+    if (device_validate(&s->devices[k], buf)) return -1;
+  }
+  return 0;
+}
+
+/* proj/src/compound.cpp:46-48: member 0 shares the compound's seed */
+static uint64_t member_seed(uint64_t seed, int k) {
+  return k == 0 ? seed : derive_seed_idx(seed, "cell_member", (uint64_t)k);
+}
+
+/* proj/src/compound.cpp:52-64 */
+or_unitcell *or_unitcell_new(int d_out, int d_in, const or_unitcell_settings *s, uint64_t seed) {
+  if (unitcell_validate(s)) return NULL;
+  or_unitcell *t = (or_unitcell *)calloc(1, sizeof(or_unitcell));
+  t->d_out = d_out;
+  t->d_in = d_in;
+  t->s = *s;
+  rng_init(&t->rng_forward, derive_seed(seed, "forward"));
+  rng_init(&t->rng_backward, derive_seed(seed, "backward"));
+  rng_init(&t->rng_update, derive_seed(seed, "update"));
+  for (int k = 0; k < s->n_devices; ++k) {
+    or_tile_settings m; /* compound.cpp:31-42 */
+    memset(&m, 0, sizeof m);
+    m.device = s->devices[k];
+    m.forward_io = s->forward_io;
+    m.backward_io = s->backward_io;
+    m.update = s->update;
+    m.temporal = s->temporal;
+    t->members[k] = or_tile_new(d_out, d_in, &m, member_seed(seed, k));
+    if (!t->members[k]) {
+      or_unitcell_free(t);
+      return NULL;
+    }
+  }
+  t->effective = (double *)calloc((size_t)d_out * d_in, sizeof(double));
+  t->dirty = 1;
+  return t;
+}
+
+or_unitcell *or_unitcell_clone(const or_unitcell *t) {
+  or_unitcell *c = (or_unitcell *)malloc(sizeof(or_unitcell));
+  *c = *t;
+  for (int k = 0; k < t->s.n_devices; ++k) c->members[k] = or_tile_clone(t->members[k]);
+  c->effective = dup(t->effective, (size_t)t->d_out * t->d_in);
+  return c;
+}
+
+void or_unitcell_free(or_unitcell *t) {
+  if (!t) return;
+  for (int k = 0; k < t->s.n_devices; ++k) or_tile_free(t->members[k]);
+  free(t->effective);
+  free(t);
+}
+
+/* proj/src/compound.cpp:66-80: sum_k g_k W_k, members in order */
+static const double *effective(or_unitcell *t) {
+  if (t->dirty) {
+    const size_t n = (size_t)t->d_out * t->d_in;
+    for (size_t c = 0; c < n; ++c) t->effective[c] = 0.0;
+    for (int k = 0; k < t->s.n_devices; ++k) {
+      const double g = t->s.gains[k], *w = t->members[k]->w;
+      for (size_t c = 0; c < n; ++c) t->effective[c] += g * w[c];
+    }
+    t->dirty = 0;
+  }
+  return t->effective;
+}
+
+/* proj/src/compound.cpp:82-88 (the caller passes exactly d_in values) */
+int or_unitcell_forward(or_unitcell *t, const double *x, double *y) {
+  return or_analog_matvec(effective(t), t->d_out, t->d_in, x, &t->s.forward_io, &t->rng_forward,
+                          0, y);
+}
+
+/* proj/src/compound.cpp:90-96 */
+int or_unitcell_backward(or_unitcell *t, const double *d, double *g) {
+  return or_analog_matvec(effective(t), t->d_out, t->d_in, d, &t->s.backward_io,
+                          &t->rng_backward, 1, g);
+}
+
+/* proj/src/compound.cpp:98-107 */
+int or_unitcell_forward_noisy(or_unitcell *t, const double *x, double extra_sigma, double *y) {
+  or_io_params io;
+  or_with_extra_weight_noise(&t->s.forward_io, extra_sigma, &io);
+  return or_analog_matvec(effective(t), t->d_out, t->d_in, x, &io, &t->rng_forward, 0, y);
+}
+
+/* one translate + trains on the compound's update stream, applied to the
+   members in `use` (proj/src/compound.cpp:118-146) */
+static int unitcell_fire(or_unitcell *t, const double *x, const double *d, double lr,
+                         double grain, int first, int last) {
+  const int nr = t->d_out, nc = t->d_in;
+  double *px = (double *)malloc(sizeof(double) * nc);
+  double *pd = (double *)malloc(sizeof(double) * nr);
+  int *sx = (int *)malloc(sizeof(int) * nc);
+  int *sd = (int *)malloc(sizeof(int) * nr);
+  int bl;
+  int rc = or_translate(x, nc, d, nr, lr, grain, &t->s.update, &bl, px, pd, sx, sd);
+  if (rc == 0) {
+    uint8_t *xb = (uint8_t *)malloc((size_t)bl * nc + 1);
+    uint8_t *db = (uint8_t *)malloc((size_t)bl * nr + 1);
+    or_generate_trains(bl, px, nc, pd, nr, &t->rng_update, xb, db);
+    for (int k = first; k <= last; ++k)
+      if (t->s.gains[k] != 0.0)
+        apply_coincidences(t->members[k], bl, xb, db, sx, sd, t->s.gains[k] < 0.0);
+    free(xb);
+    free(db);
+  }
+  free(px);
+  free(pd);
+  free(sx);
+  free(sd);
+  return rc;
+}
+
+/* proj/src/compound.cpp:109-147 */
+int or_unitcell_update(or_unitcell *t, const double *x, const double *d, double lr) {
+  if (lr == 0.0 || max_abs(x, t->d_in) == 0.0 || max_abs(d, t->d_out) == 0.0) return 0;
+  t->dirty = 1;
+  if (t->s.policy == OR_UC_ROUND_ROBIN) {
+    const int k = t->next_member;
+    t->next_member = (t->next_member + 1) % t->s.n_devices;
+    const double grain = fabs(t->s.gains[k]) * t->members[k]->s.device.dw_min;
+    if (grain == 0.0) return 0; /* zero-gain member: this event is a no-op */
+    return unitcell_fire(t, x, d, lr, grain, k, k);
+  }
+  double grain = 0.0; /* all_together: sum_k |g_k| dw_min_k per coincidence */
+  for (int k = 0; k < t->s.n_devices; ++k)
+    grain += fabs(t->s.gains[k]) * t->members[k]->s.device.dw_min;
+  if (grain == 0.0) return 0;
+  return unitcell_fire(t, x, d, lr, grain, 0, t->s.n_devices - 1);
+}
+
+/* proj/src/compound.cpp:149 */
+int or_unitcell_get_weights(const or_unitcell *t, double *w) {
+  memcpy(w, effective((or_unitcell *)t), sizeof(double) * (size_t)t->d_out * t->d_in);
+  return 0;
+}
+
+/* proj/src/compound.cpp:151-167 */
+int or_unitcell_set_weights(or_unitcell *t, const double *w) {
+  if (t->s.gains[0] == 0.0)
+    return fail("set_weights: unit cell with zero first gain cannot be programmed");
+  const size_t n = (size_t)t->d_out * t->d_in;
+  double *scaled = (double *)calloc(n ? n : 1, sizeof(double));
+  for (size_t c = 0; c < n; ++c) scaled[c] = w[c] / t->s.gains[0];
+  or_tile_set_weights(t->members[0], scaled);
+  for (size_t c = 0; c < n; ++c) scaled[c] = 0.0;
+  for (int k = 1; k < t->s.n_devices; ++k) or_tile_set_weights(t->members[k], scaled);
+  free(scaled);
+  t->dirty = 1;
+  return 0;
+}
+
+/* proj/src/compound.cpp:169-174 */
+int or_unitcell_end_minibatch(or_unitcell *t) {
+  for (int k = 0; k < t->s.n_devices; ++k) or_tile_end_minibatch(t->members[k]);
+  t->dirty = 1;
+  return 0;
+}
+
+int or_unitcell_n_members(const or_unitcell *t) { return t->s.n_devices; }
+or_tile *or_unitcell_member(or_unitcell *t, int k) { return t->members[k]; }
+
+/* ======================================================================
  * PCM inference -- proj/src/inference.cpp:14-110
  * ====================================================================== */
 

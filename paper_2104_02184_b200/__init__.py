@@ -8,11 +8,12 @@ is no CPU fallback.
 """
 from ._abi import (BM_ITERATIVE, BM_NONE, CONSTANT_STEP, EXP_STEP, LINEAR_STEP, MVM_FP32,
                    MVM_TF32, MVM_TF32X3, NM_ABS_MAX, NM_NONE, PULSE_DETERMINISTIC,
-                   PULSE_STOCHASTIC, SOFT_BOUNDS, DeviceParams, InferenceModel, IOParams,
-                   TemporalParams, TileConfig, TransferConfig, UpdateParams)
+                   PULSE_STOCHASTIC, SOFT_BOUNDS, UC_ALL_TOGETHER, UC_ROUND_ROBIN, DeviceParams,
+                   InferenceModel, IOParams, TemporalParams, TileConfig, TransferConfig,
+                   UnitCellConfig, UpdateParams)
 from .tile import (AnalogTile, Error, InferenceNoiseModel, TileSettings, TransferSettings,
-                   TransferTile, default_device, default_io, device_check, device_preset,
-                   io_off, launch_count, perfect_io, rows_amax_dev)
+                   TransferTile, UnitCellSettings, UnitCellTile, default_device, default_io,
+                   device_check, device_preset, io_off, launch_count, perfect_io, rows_amax_dev)
 
 __all__ = [
     "AnalogTile", "TransferTile", "TileSettings", "TransferSettings", "InferenceNoiseModel",
@@ -21,4 +22,5 @@ __all__ = [
     "io_off", "device_check", "launch_count", "rows_amax_dev", "CONSTANT_STEP", "LINEAR_STEP",
     "SOFT_BOUNDS", "EXP_STEP", "NM_NONE", "NM_ABS_MAX", "BM_NONE", "BM_ITERATIVE",
     "PULSE_STOCHASTIC", "PULSE_DETERMINISTIC", "MVM_FP32", "MVM_TF32", "MVM_TF32X3",
+    "UnitCellTile", "UnitCellSettings", "UnitCellConfig", "UC_ROUND_ROBIN", "UC_ALL_TOGETHER",
 ]

@@ -76,6 +76,18 @@ class TransferConfig(C.Structure):
                 ("has_transfer_io", _i), ("gamma", _d), ("transfer_io", IOParams)]
 
 
+MAX_CELL_DEVICES = 8
+UC_ROUND_ROBIN, UC_ALL_TOGETHER = 0, 1
+
+
+class UnitCellConfig(C.Structure):
+    """proj/include/xbarsim/compound.hpp:15-28 (fixed arrays of n_devices <= 8)."""
+    _fields_ = [("n_devices", _i), ("policy", _i), ("devices", DeviceParams * MAX_CELL_DEVICES),
+                ("gains", _d * MAX_CELL_DEVICES), ("forward_io", IOParams),
+                ("backward_io", IOParams), ("update", UpdateParams), ("mvm_precision", _i),
+                ("temporal", TemporalParams)]
+
+
 _P = C.c_void_p
 _fp = C.POINTER(C.c_float)
 _u32p = C.POINTER(C.c_uint32)
@@ -144,6 +156,20 @@ SIGNATURES = {
     "xb_transfer_get_weights": (C.c_int, [_P, _fp]),
     "xb_transfer_set_weights": (C.c_int, [_P, _fp]),
     "xb_transfer_events": (C.c_long, [_P]),
+    "xb_default_unitcell_config": (None, [C.POINTER(UnitCellConfig)]),
+    "xb_unitcell_create": (C.c_int, [C.POINTER(UnitCellConfig), C.c_int, C.c_int, C.c_uint64,
+                                     C.POINTER(_P)]),
+    "xb_unitcell_destroy": (C.c_int, [_P]),
+    "xb_unitcell_clone": (C.c_int, [_P, C.POINTER(_P)]),
+    "xb_unitcell_forward": (C.c_int, [_P, _fp, C.c_int, _fp]),
+    "xb_unitcell_forward_noisy": (C.c_int, [_P, _fp, C.c_int, _fp, C.c_double]),
+    "xb_unitcell_backward": (C.c_int, [_P, _fp, C.c_int, _fp]),
+    "xb_unitcell_update": (C.c_int, [_P, _fp, _fp, C.c_int, _fp]),
+    "xb_unitcell_get_weights": (C.c_int, [_P, _fp]),
+    "xb_unitcell_set_weights": (C.c_int, [_P, _fp]),
+    "xb_unitcell_end_minibatch": (C.c_int, [_P]),
+    "xb_unitcell_n_members": (C.c_int, [_P]),
+    "xb_unitcell_member": (_P, [_P, C.c_int]),
     "xb_transfer_fast": (_P, [_P]),
     "xb_transfer_slow": (_P, [_P]),
 }

@@ -166,6 +166,14 @@ struct xb_tile {
   Tile t;
 };
 
+struct xb_unitcell {
+  xb_unitcell_config cfg;
+  xb_tile *eff = nullptr;         // weights-only handle: W_eff and the compound's streams
+  std::vector<xb_tile *> members; // all on eff's CUDA stream
+  bool dirty = true;              // W_eff stale (compound.cpp:66-80)
+  int next_member = 0;            // round-robin cursor, persists across mini-batches
+};
+
 struct xb_transfer {
   xb_transfer_config cfg;
   xb_tile *fast = nullptr, *slow = nullptr;
@@ -746,14 +754,16 @@ int xb_tile_forward_dev(xb_tile *h, const float *dX, int B, float *dY, const xb_
   });
 }
 
-static void forward_host(xb_tile *h, const float *X, int B, float *Y, const xb_io_params &io) {
+// check = false: callers without check_input (the unit cell, compound.cpp:82-107)
+static void forward_host(xb_tile *h, const float *X, int B, float *Y, const xb_io_params &io,
+                         bool check = true) {
   Tile &t = h->t;
   if (B < 0) raise("forward: batch must be >= 0");
   if (B == 0) return;
   float *dX = scratch_as<float>(t.s_y, (size_t)B * (t.C + t.R));
   float *dY = dX + (size_t)B * t.C;
   XB_CUDA(cudaMemcpyAsync(dX, X, sizeof(float) * B * t.C, cudaMemcpyHostToDevice, t.stream));
-  check_finite_dev(t, {{dX, (size_t)B * t.C, "forward"}});
+  if (check) check_finite_dev(t, {{dX, (size_t)B * t.C, "forward"}});
   forward_device(t, dX, B, dY, io);
   XB_CUDA(cudaMemcpyAsync(Y, dY, sizeof(float) * B * t.R, cudaMemcpyDeviceToHost, t.stream));
   sync(t);
@@ -782,22 +792,24 @@ int xb_tile_backward_dev(xb_tile *h, const float *dD, int B, float *dG) {
   });
 }
 
+static void backward_host(xb_tile *h, const float *D, int B, float *G, bool check = true) {
+  Tile &t = h->t;
+  if (B < 0) raise("backward: batch must be >= 0");
+  if (B == 0) return;
+  if (t.R != t.R_total) raise("backward: row-sharded tile; use xb_tile_backward_partial_dev");
+  float *dD = scratch_as<float>(t.s_y, (size_t)B * (t.C + t.R));
+  float *dG = dD + (size_t)B * t.R;
+  XB_CUDA(cudaMemcpyAsync(dD, D, sizeof(float) * B * t.R, cudaMemcpyHostToDevice, t.stream));
+  if (check) check_finite_dev(t, {{dD, (size_t)B * t.R, "backward"}});
+  mvm_backward(t, dD, B, dG, make_io(t.cfg.backward_io), t.k_bwd, t.seq_bwd, nullptr, false,
+               nullptr);
+  t.seq_bwd += (uint64_t)B;
+  XB_CUDA(cudaMemcpyAsync(G, dG, sizeof(float) * B * t.C, cudaMemcpyDeviceToHost, t.stream));
+  sync(t);
+}
+
 int xb_tile_backward(xb_tile *h, const float *D, int B, float *G) {
-  return guard([&] {
-    Tile &t = h->t;
-    if (B < 0) raise("backward: batch must be >= 0");
-    if (B == 0) return;
-    if (t.R != t.R_total) raise("backward: row-sharded tile; use xb_tile_backward_partial_dev");
-    float *dD = scratch_as<float>(t.s_y, (size_t)B * (t.C + t.R));
-    float *dG = dD + (size_t)B * t.R;
-    XB_CUDA(cudaMemcpyAsync(dD, D, sizeof(float) * B * t.R, cudaMemcpyHostToDevice, t.stream));
-    check_finite_dev(t, {{dD, (size_t)B * t.R, "backward"}});
-    mvm_backward(t, dD, B, dG, make_io(t.cfg.backward_io), t.k_bwd, t.seq_bwd, nullptr, false,
-                 nullptr);
-    t.seq_bwd += (uint64_t)B;
-    XB_CUDA(cudaMemcpyAsync(G, dG, sizeof(float) * B * t.C, cudaMemcpyDeviceToHost, t.stream));
-    sync(t);
-  });
+  return guard([&] { backward_host(h, D, B, G); });
 }
 
 int xb_tile_backward_partial_dev(xb_tile *h, const float *dD, int B, const float *dAmaxD,
@@ -1176,5 +1188,306 @@ int xb_transfer_set_weights(xb_transfer *t, const float *w) {
 long xb_transfer_events(const xb_transfer *t) { return t->events; }
 xb_tile *xb_transfer_fast(xb_transfer *t) { return t->fast; }
 xb_tile *xb_transfer_slow(xb_transfer *t) { return t->slow; }
+
+
+} // extern "C"
+
+// ============================================================== UnitCellTile
+namespace xb {
+
+static xb_tile_config uc_member_config(const xb_unitcell_config &c, const xb_device_params &d) {
+  xb_tile_config m; // compound.cpp:31-42
+  xb_default_config(&m);
+  m.device = d;
+  m.forward_io = c.forward_io;
+  m.backward_io = c.backward_io;
+  m.update = c.update;
+  m.temporal = c.temporal;
+  m.mvm_precision = c.mvm_precision;
+  return m;
+}
+
+static void unitcell_validate(const xb_unitcell_config &c) { // compound.cpp:12-27
+  if (c.n_devices < 1) raise("unit_cell.devices: need at least one device");
+  if (c.n_devices > XB_MAX_CELL_DEVICES) raise("unit_cell.gains: length must match devices");
+  for (int k = 0; k < c.n_devices; ++k)
+    if (!std::isfinite(c.gains[k])) raise("unit_cell.gains: entries must be finite");
+  for (int k = 0; k < c.n_devices; ++k)
+    device_validate(c.devices[k], ("unit_cell.devices[" + std::to_string(k) + "]").c_str());
+}
+
+// the compound's handle: W_eff only (no device arrays), keys from the compound
+// seed, so its "forward"/"backward"/"update" streams are the compound's own
+static xb_tile *view_tile_create(const xb_tile_config &cfg, int R, int C, uint64_t seed) {
+  auto h = std::make_unique<xb_tile>();
+  Tile &t = h->t;
+  t.cfg = cfg;
+  t.R = R;
+  t.C = C;
+  t.R_total = R;
+  t.ld = (int)ld_of(C);
+  tile_init_keys(t, seed);
+  XB_CUDA(cudaStreamCreateWithFlags(&t.stream, cudaStreamNonBlocking));
+  t.own_stream = true;
+  const size_t n = (size_t)R * t.ld;
+  XB_CUDA(cudaMalloc(&t.W, std::max<size_t>(n, 1) * sizeof(float)));
+  XB_CUDA(cudaMemsetAsync(t.W, 0, n * sizeof(float), t.stream));
+  return h.release();
+}
+
+static void uc_share_stream(xb_unitcell *u) {
+  for (xb_tile *m : u->members) {
+    if (m->t.own_stream && m->t.stream) {
+      XB_CUDA(cudaStreamSynchronize(m->t.stream));
+      cudaStreamDestroy(m->t.stream);
+    }
+    m->t.own_stream = false;
+    m->t.stream = u->eff->t.stream;
+  }
+}
+
+static void uc_effective(xb_unitcell *u) {
+  if (!u->dirty) return;
+  const float *w[XB_MAX_CELL_DEVICES];
+  for (size_t k = 0; k < u->members.size(); ++k) w[k] = u->members[k]->t.W;
+  Tile &e = u->eff->t;
+  launch_effective(e.W, w, u->cfg.gains, (int)u->members.size(), e.R, e.C, e.ld, e.stream);
+  u->dirty = false;
+}
+
+static void uc_free(xb_unitcell *u) {
+  for (xb_tile *m : u->members) xb_tile_destroy(m);
+  if (u->eff) xb_tile_destroy(u->eff);
+  delete u;
+}
+
+// compound.cpp:109-147 for B samples in order: one translate + trains per
+// sample on the compound's update stream (grain per sample), then each member
+// fires the trains of its samples in one weight-stationary pulse launch
+static void uc_update(xb_unitcell *u, const float *X, const float *D, int B, const float *lr) {
+  Tile &e = u->eff->t;
+  const int K = (int)u->members.size();
+  const bool rr = u->cfg.policy == XB_UC_ROUND_ROBIN;
+  double grain_all = 0.0;
+  for (int k = 0; k < K; ++k) grain_all += std::fabs(u->cfg.gains[k]) * u->cfg.devices[k].dw_min;
+  std::vector<float> lre(B, 0.f);
+  std::vector<double> grain(B, 0.0);
+  std::vector<int> member(B, -1);
+  int cursor = u->next_member;
+  bool any = false;
+  for (int b = 0; b < B; ++b) {
+    const double l = lr ? (double)lr[b] : e.learning_rate;
+    bool xz = true, dz = true;
+    for (int j = 0; j < e.C && xz; ++j) xz = X[(size_t)b * e.C + j] == 0.f;
+    for (int i = 0; i < e.R && dz; ++i) dz = D[(size_t)b * e.R + i] == 0.f;
+    if (l == 0.0 || xz || dz) continue; // :113-115, no draw, cursor unchanged
+    double g = grain_all;
+    if (rr) {
+      member[b] = cursor;
+      g = std::fabs(u->cfg.gains[cursor]) * u->cfg.devices[cursor].dw_min;
+      cursor = (cursor + 1) % K;
+    }
+    if (g == 0.0) continue; // zero-gain member (or all gains zero): a no-op event
+    if (!(l > 0.0)) raise("translate: learning rate must be > 0"); // pulsed.cpp:27-29
+    lre[b] = (float)l;
+    grain[b] = g;
+    any = true;
+  }
+  u->next_member = cursor;
+  if (!any) return;
+  u->dirty = true;
+  const int ldb = train_ld(B);
+  UpdBufs ub = upd_bufs(e, B, false);
+  float *dX = scratch_as<float>(e.s_y, (size_t)B * (e.C + e.R));
+  float *dD = dX + (size_t)B * e.C;
+  char *aux = (char *)e.s_params.get((size_t)B * (sizeof(double) + sizeof(int)) + 256);
+  double *dG = (double *)aux;
+  int *dIdx = (int *)(aux + (size_t)B * sizeof(double));
+  XB_CUDA(cudaMemcpyAsync(dX, X, sizeof(float) * B * e.C, cudaMemcpyHostToDevice, e.stream));
+  XB_CUDA(cudaMemcpyAsync(dD, D, sizeof(float) * B * e.R, cudaMemcpyHostToDevice, e.stream));
+  XB_CUDA(cudaMemcpyAsync(ub.lr, lre.data(), sizeof(float) * B, cudaMemcpyHostToDevice, e.stream));
+  XB_CUDA(cudaMemcpyAsync(dG, grain.data(), sizeof(double) * B, cudaMemcpyHostToDevice,
+                          e.stream));
+  launch_rows_amax(dX, B, e.C, e.C, ub.xm, e.stream);
+  launch_rows_amax(dD, B, e.R, e.R, ub.dm, e.stream);
+  launch_trains(e, dX, dD, B, ub.lr, 0.f, ub.xm, ub.dm, e.seq_upd, ub.xw, ub.dw, ldb, ub.bl,
+                nullptr, nullptr, false, dG);
+  e.seq_upd += (uint64_t)B;
+  if (!rr) {
+    for (int k = 0; k < K; ++k) {
+      if (u->cfg.gains[k] == 0.0) continue;
+      Tile &m = u->members[k]->t;
+      launch_pulse(m, ub.xw, ub.dw, ldb, B, m.upd_calls++, u->cfg.gains[k] < 0.0);
+    }
+  } else {
+    std::vector<int> idx;
+    idx.reserve(B);
+    uint32_t *gx = scratch_as<uint32_t>(e.s_io, (size_t)ldb * (e.C + e.R));
+    for (int k = 0; k < K; ++k) {
+      idx.clear();
+      for (int b = 0; b < B; ++b)
+        if (member[b] == k && lre[b] != 0.f) idx.push_back(b);
+      if (idx.empty()) continue;
+      const int n = (int)idx.size(), ldn = train_ld(n);
+      XB_CUDA(cudaMemcpyAsync(dIdx, idx.data(), sizeof(int) * n, cudaMemcpyHostToDevice,
+                              e.stream));
+      launch_gather_samples(ub.xw, ldb, e.C, dIdx, n, gx, ldn, e.stream);
+      launch_gather_samples(ub.dw, ldb, e.R, dIdx, n, gx + (size_t)ldn * e.C, ldn, e.stream);
+      Tile &m = u->members[k]->t;
+      launch_pulse(m, gx, gx + (size_t)ldn * e.C, ldn, n, m.upd_calls++, u->cfg.gains[k] < 0.0);
+      sync(e); // idx / gather buffers are reused by the next member
+    }
+  }
+  sync(e);
+}
+
+} // namespace xb
+
+extern "C" {
+
+void xb_default_unitcell_config(xb_unitcell_config *c) { // compound.hpp:15-28
+  std::memset(c, 0, sizeof *c);
+  c->n_devices = 1;
+  xb_default_device(&c->devices[0]);
+  c->gains[0] = 1.0;
+  c->policy = XB_UC_ALL_TOGETHER;
+  xb_default_io(&c->forward_io);
+  xb_default_io(&c->backward_io);
+  c->update = xb_update_params{31, 0, XB_PULSE_STOCHASTIC};
+  c->mvm_precision = XB_MVM_FP32;
+}
+
+int xb_unitcell_create(const xb_unitcell_config *cfg, int d_out, int d_in, uint64_t seed,
+                       xb_unitcell **out) {
+  *out = nullptr;
+  auto *u = new xb_unitcell;
+  u->cfg = *cfg;
+  int rc = guard([&] { unitcell_validate(*cfg); });
+  for (int k = 0; rc == 0 && k < cfg->n_devices; ++k) { // compound.cpp:52-64
+    const xb_tile_config mc = uc_member_config(*cfg, cfg->devices[k]);
+    xb_tile *m = nullptr;
+    rc = xb_tile_create(&mc, d_out, d_in,
+                        k == 0 ? seed : derive_seed_idx(seed, "cell_member", (uint64_t)k), nullptr,
+                        &m);
+    if (rc == 0) u->members.push_back(m);
+  }
+  if (rc == 0)
+    rc = guard([&] {
+      u->eff = view_tile_create(uc_member_config(*cfg, cfg->devices[0]), d_out, d_in, seed);
+      uc_share_stream(u);
+    });
+  if (rc) {
+    uc_free(u);
+    return rc;
+  }
+  *out = u;
+  return 0;
+}
+
+int xb_unitcell_destroy(xb_unitcell *u) {
+  if (u) uc_free(u);
+  return 0;
+}
+
+int xb_unitcell_clone(const xb_unitcell *src, xb_unitcell **out) {
+  *out = nullptr;
+  auto *u = new xb_unitcell;
+  u->cfg = src->cfg;
+  u->dirty = src->dirty;
+  u->next_member = src->next_member;
+  int rc = 0;
+  for (xb_tile *m : src->members) {
+    xb_tile *c = nullptr;
+    if ((rc = xb_tile_clone(m, &c))) break;
+    u->members.push_back(c);
+  }
+  if (rc == 0)
+    rc = guard([&] {
+      const Tile &s = src->eff->t;
+      XB_CUDA(cudaStreamSynchronize(s.stream));
+      u->eff = view_tile_create(s.cfg, s.R, s.C, s.seed);
+      Tile &t = u->eff->t;
+      t.seq_fwd = s.seq_fwd;
+      t.seq_bwd = s.seq_bwd;
+      t.seq_upd = s.seq_upd;
+      t.learning_rate = s.learning_rate;
+      XB_CUDA(cudaMemcpyAsync(t.W, s.W, (size_t)t.R * t.ld * sizeof(float),
+                              cudaMemcpyDeviceToDevice, t.stream));
+      uc_share_stream(u);
+      sync(t);
+    });
+  if (rc) {
+    uc_free(u);
+    return rc;
+  }
+  *out = u;
+  return 0;
+}
+
+int xb_unitcell_forward(xb_unitcell *u, const float *X, int B, float *Y) {
+  return guard([&] { // compound.cpp:82-88
+    uc_effective(u);
+    forward_host(u->eff, X, B, Y, u->cfg.forward_io, false);
+  });
+}
+
+int xb_unitcell_forward_noisy(xb_unitcell *u, const float *X, int B, float *Y,
+                              double extra_sigma) {
+  return guard([&] { // compound.cpp:98-107
+    uc_effective(u);
+    forward_host(u->eff, X, B, Y, noisy_io(u->cfg.forward_io, extra_sigma), false);
+  });
+}
+
+int xb_unitcell_backward(xb_unitcell *u, const float *D, int B, float *G) {
+  return guard([&] { // compound.cpp:90-96
+    uc_effective(u);
+    backward_host(u->eff, D, B, G, false);
+  });
+}
+
+int xb_unitcell_update(xb_unitcell *u, const float *X, const float *D, int B, const float *lr) {
+  return guard([&] {
+    if (B < 0) raise("update: batch must be >= 0");
+    if (B > 0) uc_update(u, X, D, B, lr);
+  });
+}
+
+int xb_unitcell_get_weights(xb_unitcell *u, float *w) {
+  return guard([&] { // compound.cpp:149
+    uc_effective(u);
+    if (xb_tile_get_weights(u->eff, w)) raise(g_err);
+  });
+}
+
+int xb_unitcell_set_weights(xb_unitcell *u, const float *w) {
+  return guard([&] { // compound.cpp:151-167
+    const double g0 = u->cfg.gains[0];
+    if (g0 == 0.0) raise("set_weights: unit cell with zero first gain cannot be programmed");
+    const Tile &e = u->eff->t;
+    const size_t n = (size_t)e.R * e.C;
+    std::vector<float> scaled(n);
+    for (size_t c = 0; c < n; ++c) scaled[c] = (float)((double)w[c] / g0);
+    if (xb_tile_set_weights(u->members[0], scaled.data())) raise(g_err);
+    std::fill(scaled.begin(), scaled.end(), 0.f);
+    for (size_t k = 1; k < u->members.size(); ++k)
+      if (xb_tile_set_weights(u->members[k], scaled.data())) raise(g_err);
+    u->dirty = true;
+  });
+}
+
+int xb_unitcell_end_minibatch(xb_unitcell *u) {
+  return guard([&] { // compound.cpp:169-174
+    for (xb_tile *m : u->members)
+      if (xb_tile_end_minibatch(m)) raise(g_err);
+    u->dirty = true;
+  });
+}
+
+int xb_unitcell_n_members(const xb_unitcell *u) { return (int)u->members.size(); }
+
+xb_tile *xb_unitcell_member(xb_unitcell *u, int k) {
+  return (k >= 0 && k < (int)u->members.size()) ? u->members[k] : nullptr;
+}
 
 } // extern "C"

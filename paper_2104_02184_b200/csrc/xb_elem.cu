@@ -173,7 +173,38 @@ __global__ void __launch_bounds__(EW_THREADS) nonfinite_kernel(const float *__re
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, bit);
 }
 
+struct EffArgs {
+  const float *w[XB_MAX_CELL_DEVICES];
+  double g[XB_MAX_CELL_DEVICES];
+  int K;
+};
+
+// proj/src/compound.cpp:66-80: effective weight of a unit cell, members in order
+__global__ void __launch_bounds__(EW_THREADS) effective_kernel(float *__restrict__ weff,
+                                                               EffArgs a, int ld, int R, int C) {
+  int i, j;
+  if (!ew_index(R, C, i, j)) return;
+  const size_t k = (size_t)i * ld + j;
+  double acc = 0.0;
+  for (int m = 0; m < a.K; ++m) acc += a.g[m] * (double)a.w[m][k];
+  weff[k] = (float)acc;
+}
+
 } // namespace
+
+void launch_effective(float *weff, const float *const *w, const double *g, int K, int R, int C,
+                      int ld, cudaStream_t s) {
+  if (R == 0 || K < 1 || K > XB_MAX_CELL_DEVICES) return;
+  EffArgs a;
+  a.K = K;
+  for (int m = 0; m < K; ++m) {
+    a.w[m] = w[m];
+    a.g[m] = g[m];
+  }
+  effective_kernel<<<ew_grid(R, C), EW_THREADS, 0, s>>>(weff, a, ld, R, C);
+  count_launch();
+  XB_CUDA(cudaGetLastError());
+}
 
 void launch_nonfinite(const float *v, size_t n, int bit, int *flag, cudaStream_t s) {
   if (n == 0) return;

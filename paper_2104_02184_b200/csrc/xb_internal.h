@@ -27,6 +27,10 @@ void count_launch(int n = 1);
 uint64_t fnv1a(const char *s);
 uint64_t splitmix(uint64_t z);
 inline uint64_t derive_seed(uint64_t base, const char *name) { return splitmix(base ^ fnv1a(name)); }
+// proj/src/rng.cpp:39-41: derive(name, index)
+inline uint64_t derive_seed_idx(uint64_t base, const char *name, uint64_t idx) {
+  return splitmix(splitmix(base ^ fnv1a(name)) + idx);
+}
 inline Key key_of(uint64_t seed) { return Key{(uint32_t)seed, (uint32_t)(seed >> 32)}; }
 
 // device scratch that grows on demand
@@ -90,12 +94,19 @@ void launch_rows_amax(const float *V, int B, int n, int ld, float *out, cudaStre
 void launch_trains(const Tile &t, const float *X, const float *D, int B, const float *lr_dev,
                    float lr_scalar, const float *xm, const float *dm, uint64_t seq0,
                    uint32_t *xw, uint32_t *dw, int ldb, int32_t *bl, double *px, double *pd,
-                   bool deterministic);
+                   bool deterministic, const double *dwmin_b = nullptr);
 // trains are LINE-major: xw[j][b], dw[i][b], row stride ldb (multiple of 8)
 inline int train_ld(int B) { return (B + 7) / 8 * 8; }
 // weight-stationary coincidence/pulse kernel over packed words
+// flip inverts every pulse (negative unit-cell gain, tile.cpp:164-167)
 void launch_pulse(Tile &t, const uint32_t *xw, const uint32_t *dw, int ldb, int B,
-                  uint32_t call_id);
+                  uint32_t call_id, bool flip = false);
+// out[line][k] = in[line][idx[k]] (k < n), zero-padded to ldb_out
+void launch_gather_samples(const uint32_t *in, int ldb_in, int lines, const int *idx, int n,
+                           uint32_t *out, int ldb_out, cudaStream_t s);
+// W_eff = sum_k g_k W_k over [R][ld] (fp64 sum, fp32 store); K <= XB_MAX_CELL_DEVICES
+void launch_effective(float *weff, const float *const *w, const double *g, int K, int R, int C,
+                      int ld, cudaStream_t s);
 // deterministic_implicit: lround(bl*pd*px) pulses per cell per sample
 void launch_pulse_det(Tile &t, const double *px, const double *pd, const int32_t *bl, int B,
                       uint32_t call_id);

@@ -110,9 +110,9 @@ __device__ __forceinline__ Plan make_plan(double lrb, double x_amax, double d_am
 __global__ void __launch_bounds__(256) trains_kernel(
     const float *__restrict__ X, const float *__restrict__ D, int C, int R, int B,
     const float *__restrict__ lr, float lr_scalar, const float *__restrict__ xm,
-    const float *__restrict__ dm, double dw_min, int BL, int blm, Key key, uint64_t seq0,
-    int row0, uint32_t *__restrict__ xw, uint32_t *__restrict__ dw, int ldb,
-    int32_t *__restrict__ bl_out) {
+    const float *__restrict__ dm, double dw_min, const double *__restrict__ dwmin_b, int BL,
+    int blm, Key key, uint64_t seq0, int row0, uint32_t *__restrict__ xw,
+    uint32_t *__restrict__ dw, int ldb, int32_t *__restrict__ bl_out) {
   __shared__ Plan plan[32];
   __shared__ uint32_t tile[32][33];
   const int nxb = (C + 31) / 32;
@@ -125,7 +125,8 @@ __global__ void __launch_bounds__(256) trains_kernel(
     const int b = b0 + threadIdx.x;
     if (b < B) {
       const double lrb = (double)(lr ? lr[b] : lr_scalar);
-      plan[threadIdx.x] = make_plan(lrb, (double)xm[b], (double)dm[b], dw_min, BL, blm);
+      plan[threadIdx.x] =
+          make_plan(lrb, (double)xm[b], (double)dm[b], dwmin_b ? dwmin_b[b] : dw_min, BL, blm);
       if (blockIdx.x == 0 && bl_out) bl_out[b] = plan[threadIdx.x].skip ? 0 : plan[threadIdx.x].bl;
     }
   }
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(256) probs_kernel(
 void launch_trains(const Tile &t, const float *X, const float *D, int B, const float *lr_dev,
                    float lr_scalar, const float *xm, const float *dm, uint64_t seq0,
                    uint32_t *xw, uint32_t *dw, int ldb, int32_t *bl, double *px, double *pd,
-                   bool deterministic) {
+                   bool deterministic, const double *dwmin_b) {
   if (B <= 0) return;
   if (deterministic) {
     probs_kernel<<<B, 256, 0, t.stream>>>(X, D, t.C, t.R, lr_dev, lr_scalar, xm, dm,
@@ -195,7 +196,7 @@ void launch_trains(const Tile &t, const float *X, const float *D, int B, const f
   } else {
     dim3 grid((t.C + 31) / 32 + (t.R + 31) / 32, (B + 31) / 32);
     trains_kernel<<<grid, 256, 0, t.stream>>>(X, D, t.C, t.R, B, lr_dev, lr_scalar, xm, dm,
-                                              t.cfg.device.dw_min, t.cfg.update.bl,
+                                              t.cfg.device.dw_min, dwmin_b, t.cfg.update.bl,
                                               t.cfg.update.bl_management, t.k_upd, seq0, t.row0,
                                               xw, dw, ldb, bl);
   }
@@ -458,7 +459,7 @@ template <int LAW, bool NOISE>
 __global__ void __launch_bounds__(PULSE_WARPS * 32, pulse_minb<LAW>()) pulse_kernel(
     float *__restrict__ W, const float4 *__restrict__ P, int ld, int R, int C,
     const uint32_t *__restrict__ xw, const uint32_t *__restrict__ dw, int ldb, int B, int row0,
-    LawArgs la, RoundKeys rk, uint32_t call, uint32_t one) {
+    LawArgs la, RoundKeys rk, uint32_t call, uint32_t one, uint32_t flip) {
   extern __shared__ uint32_t qsm[]; // [PULSE_WARPS][PULSE_QW][32]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t *q = qsm + warp * (PULSE_QW * 32) + lane;
@@ -502,7 +503,7 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, pulse_minb<LAW>()) pulse_ker
     auto append = [&](uint32_t xv, uint32_t dv) {
       const uint32_t k = __popc(xv & dv & xmask);
       uint32_t down; // all ones iff the signs differ: mul.hi by a runtime 1 keeps it on the FMA pipe
-      asm("mul.hi.s32 %0, %1, %2;" : "=r"(down) : "r"(xv ^ dv), "r"(one));
+      asm("mul.hi.s32 %0, %1, %2;" : "=r"(down) : "r"(xv ^ dv ^ flip), "r"(one));
       uint32_t lo; // k ones from bit sh, clipped at bit 31 (BMSK)
       asm("bmsk.clamp.b32 %0, %1, %2;" : "=r"(lo) : "r"(sh), "r"(k));
       acc |= lo & ~down;
@@ -610,7 +611,7 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, pulse_minb<LAW>()) pulse_ker
 
 template <int LAW, bool NOISE>
 static void pulse_dispatch(Tile &t, const uint32_t *xw, const uint32_t *dw, int ldb, int B,
-                           LawArgs la, uint32_t call) {
+                           LawArgs la, uint32_t call, bool flip) {
   const int smem = PULSE_WARPS * PULSE_QW * 32 * (int)sizeof(uint32_t);
   static bool configured = false;
   if (!configured) {
@@ -633,21 +634,22 @@ static void pulse_dispatch(Tile &t, const uint32_t *xw, const uint32_t *dw, int 
     grid = dim3((unsigned)std::min<long>(blocks, (items + PULSE_WARPS - 1) / PULSE_WARPS));
   }
   pulse_kernel<LAW, NOISE><<<grid, PULSE_WARPS * 32, smem, t.stream>>>(
-      t.W, t.P, t.ld, t.R, t.C, xw, dw, ldb, B, t.row0, la, round_keys(t.k_c2c), call, 1u);
+      t.W, t.P, t.ld, t.R, t.C, xw, dw, ldb, B, t.row0, la, round_keys(t.k_c2c), call, 1u,
+      flip ? 0x80000000u : 0u);
   count_launch();
   XB_CUDA(cudaGetLastError());
 }
 
 void launch_pulse(Tile &t, const uint32_t *xw, const uint32_t *dw, int ldb, int B,
-                  uint32_t call_id) {
+                  uint32_t call_id, bool flip) {
   if (B <= 0 || t.R == 0) return;
   const LawArgs la{(float)t.cfg.device.slope, (float)t.cfg.device.gamma,
                    (float)t.cfg.device.dw_min_std};
   const bool noise = t.cfg.device.dw_min_std > 0.0;
 #define XB_PULSE(K)                                                                        \
   case K:                                                                                  \
-    noise ? pulse_dispatch<K, true>(t, xw, dw, ldb, B, la, call_id)                        \
-          : pulse_dispatch<K, false>(t, xw, dw, ldb, B, la, call_id);                      \
+    noise ? pulse_dispatch<K, true>(t, xw, dw, ldb, B, la, call_id, flip)                  \
+          : pulse_dispatch<K, false>(t, xw, dw, ldb, B, la, call_id, flip);                \
     break;
   switch (t.cfg.device.kind) {
     XB_PULSE(XB_CONSTANT_STEP)
@@ -658,6 +660,27 @@ void launch_pulse(Tile &t, const uint32_t *xw, const uint32_t *dw, int ldb, int 
     raise("device.kind: unknown device model");
   }
 #undef XB_PULSE
+}
+
+// ============================================================== sample gather
+// out[line][k] = in[line][idx[k]] for k < n, zero up to ldb_out: the trains of
+// the samples one unit-cell member receives (round-robin policy)
+__global__ void gather_samples_kernel(const uint32_t *__restrict__ in, int ldb_in, int lines,
+                                      const int *__restrict__ idx, int n,
+                                      uint32_t *__restrict__ out, int ldb_out) {
+  const int line = blockIdx.y;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ldb_out; k += gridDim.x * blockDim.x)
+    out[(size_t)line * ldb_out + k] = k < n ? in[(size_t)line * ldb_in + idx[k]] : 0u;
+}
+
+void launch_gather_samples(const uint32_t *in, int ldb_in, int lines, const int *idx, int n,
+                           uint32_t *out, int ldb_out, cudaStream_t s) {
+  if (lines <= 0 || ldb_out <= 0) return;
+  const int threads = std::min(256, (ldb_out + 31) / 32 * 32);
+  dim3 grid((ldb_out + threads - 1) / threads, lines);
+  gather_samples_kernel<<<grid, threads, 0, s>>>(in, ldb_in, lines, idx, n, out, ldb_out);
+  count_launch();
+  XB_CUDA(cudaGetLastError());
 }
 
 // ============================================================== K6: deterministic

@@ -19,7 +19,7 @@ import numpy as np
 
 from . import _abi
 from ._abi import (DeviceParams, InferenceModel, IOParams, Shard, TemporalParams, TileConfig,
-                   TransferConfig, UpdateParams)
+                   TransferConfig, UnitCellConfig, UpdateParams)
 
 _lib = _abi.load()
 
@@ -112,6 +112,36 @@ def TileSettings(device: Optional[DeviceParams] = None, forward_io: Optional[IOP
 def TransferSettings() -> TransferConfig:
     c = TransferConfig()
     _lib.xb_default_transfer_config(C.byref(c))
+    return c
+
+
+def UnitCellSettings(devices=None, gains=None, policy: int = _abi.UC_ALL_TOGETHER,
+                     forward_io: Optional[IOParams] = None, backward_io: Optional[IOParams] = None,
+                     update: Optional[UpdateParams] = None,
+                     temporal: Optional[TemporalParams] = None,
+                     mvm_precision: int = _abi.MVM_FP32) -> UnitCellConfig:
+    """proj/include/xbarsim/compound.hpp:15-28 with reference defaults
+    (one default device of gain 1, all_together)."""
+    c = UnitCellConfig()
+    _lib.xb_default_unitcell_config(C.byref(c))
+    if devices is not None:
+        devices = list(devices)
+        gains = [1.0] * len(devices) if gains is None else list(gains)
+        if len(devices) > _abi.MAX_CELL_DEVICES:
+            raise Error(f"unit_cell.devices: at most {_abi.MAX_CELL_DEVICES} on the B200 path")
+        c.n_devices = len(devices)
+        for k, d in enumerate(devices):
+            c.devices[k] = d
+        if len(gains) != len(devices):
+            raise Error("unit_cell.gains: length must match devices")
+        for k, g in enumerate(gains):
+            c.gains[k] = float(g)
+    c.policy = policy
+    for name, v in (("forward_io", forward_io), ("backward_io", backward_io),
+                    ("update", update), ("temporal", temporal)):
+        if v is not None:
+            setattr(c, name, v)
+    c.mvm_precision = mvm_precision
     return c
 
 
@@ -469,3 +499,90 @@ class TransferTile:
     def set_weights(self, w) -> None:
         w = _f32(w, (self._d_out, self._d_in))
         _check(_lib.xb_transfer_set_weights(self._h, _ptr(w)))
+
+
+class UnitCellTile:
+    """GPU unit cell: gain-weighted device members (proj/include/xbarsim/compound.hpp:30-71)."""
+
+    def __init__(self, d_out: int, d_in: int, settings: Optional[UnitCellConfig] = None,
+                 seed: int = 0, _handle=None):
+        if _handle is not None:
+            h = _handle
+        else:
+            settings = settings if settings is not None else UnitCellSettings()
+            h = C.c_void_p()
+            _check(_lib.xb_unitcell_create(C.byref(settings), int(d_out), int(d_in),
+                                           C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), C.byref(h)))
+        self._h = h
+        self._d_out, self._d_in = int(d_out), int(d_in)
+        self._members = []
+        for k in range(_lib.xb_unitcell_n_members(h)):
+            m = AnalogTile(0, 0, _handle=C.c_void_p(_lib.xb_unitcell_member(h, k)))
+            self._members.append(m)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            for m in getattr(self, "_members", []):
+                m._h = None  # owned by the compound
+            _lib.xb_unitcell_destroy(h)
+            self._h = None
+
+    def d_out(self) -> int:
+        return self._d_out
+
+    def d_in(self) -> int:
+        return self._d_in
+
+    def n_members(self) -> int:
+        return len(self._members)
+
+    def member(self, k: int) -> "AnalogTile":
+        """compound.hpp:53 (read-only: change members through the compound)."""
+        return self._members[k]
+
+    def clone(self) -> "UnitCellTile":
+        h = C.c_void_p()
+        _check(_lib.xb_unitcell_clone(self._h, C.byref(h)))
+        return UnitCellTile(self._d_out, self._d_in, _handle=h)
+
+    def forward(self, x):
+        X, single = _batch(x, self._d_in, "forward")
+        Y = np.empty((X.shape[0], self._d_out), dtype=np.float32)
+        _check(_lib.xb_unitcell_forward(self._h, _ptr(X), X.shape[0], _ptr(Y)))
+        return Y[0] if single else Y
+
+    def forward_noisy(self, x, extra_weight_sigma: float):
+        X, single = _batch(x, self._d_in, "forward")
+        Y = np.empty((X.shape[0], self._d_out), dtype=np.float32)
+        _check(_lib.xb_unitcell_forward_noisy(self._h, _ptr(X), X.shape[0], _ptr(Y),
+                                              float(extra_weight_sigma)))
+        return Y[0] if single else Y
+
+    def backward(self, d):
+        D, single = _batch(d, self._d_out, "backward")
+        G = np.empty((D.shape[0], self._d_in), dtype=np.float32)
+        _check(_lib.xb_unitcell_backward(self._h, _ptr(D), D.shape[0], _ptr(G)))
+        return G[0] if single else G
+
+    def update(self, x, d, lr) -> None:
+        X, _ = _batch(x, self._d_in, "update(x)")
+        D, _ = _batch(d, self._d_out, "update(d)")
+        if X.shape[0] != D.shape[0]:
+            raise Error("update: x/d lengths do not match tile shape")
+        lra = _lr_array(lr, X.shape[0])
+        if lra is None:
+            lra = np.full(X.shape[0], 0.01, dtype=np.float32)
+        _check(_lib.xb_unitcell_update(self._h, _ptr(X), _ptr(D), X.shape[0], _ptr(lra)))
+
+    def get_weights(self) -> np.ndarray:
+        w = np.empty((self._d_out, self._d_in), dtype=np.float32)
+        _check(_lib.xb_unitcell_get_weights(self._h, _ptr(w)))
+        return w
+
+    def set_weights(self, w) -> None:
+        w = _f32(w, (self._d_out, self._d_in))
+        _check(_lib.xb_unitcell_set_weights(self._h, _ptr(w)))
+
+    def end_minibatch(self) -> None:
+        _check(_lib.xb_unitcell_end_minibatch(self._h))

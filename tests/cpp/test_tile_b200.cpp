@@ -267,6 +267,37 @@ int main() {
     CHECK(a.forward_noisy(x, 0.0) == a.forward(x));
     CHECK(!(a.forward_noisy(x, 0.1) == a.forward(x)));
   });
+  run("UnitCellTile: set/get, mirror pair, round robin, clone (test_compounds.cpp:43-150)", [] {
+    DeviceParams d;
+    d.dw_min = 1.0 / 1024;
+    d.w_max = 8.0;
+    d.w_min = -8.0;
+    UnitCellSettings s;
+    s.devices = {d, d};
+    s.gains = {1.0, -1.0};
+    s.forward_io = io_off();
+    s.backward_io = io_off();
+    UnitCellTile u(3, 4, s, 41);
+    CHECK(u.n_members() == 2);
+    Matrix w = random_matrix(3, 4, 0.5, 42);
+    u.set_weights(w);
+    Matrix e = u.get_weights();
+    for (size_t k = 0; k < w.size(); ++k) CHECK(std::fabs(e.data()[k] - w.data()[k]) < 1e-6);
+    const Matrix base = u.member(0).get_weights(); // fp32-stored w
+    for (int k = 0; k < 5; ++k)
+      u.update(std::vector<double>{1.0, -0.5, 0.25, 0.8}, std::vector<double>{0.7, -0.3, 0.9},
+               0.05);
+    Matrix m0 = u.member(0).get_weights(), m1 = u.member(1).get_weights();
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 4; ++j) CHECK(std::fabs(m1(i, j) + (m0(i, j) - base(i, j))) < 1e-6);
+    auto c = u.clone();
+    CHECK(c->get_weights() == u.get_weights());
+    s.gains = {0.0, 1.0};
+    UnitCellTile z(2, 2, s, 43);
+    CHECK(throws([&] { z.set_weights(Matrix(2, 2, 1.0)); }, "zero first gain"));
+    CHECK(throws([&] { u.update(std::vector<double>{1.0}, std::vector<double>{1.0}, 0.1); },
+                 "x/d lengths"));
+  });
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;
 }

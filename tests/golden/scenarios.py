@@ -234,6 +234,48 @@ def transfer(O):
     return {"transfer": np.concatenate(res), "events": np.array([t.events()])}
 
 
+def unitcell(O):
+    """UnitCellTile (proj/src/compound.cpp:12-174): a +1/-0.5 reram_sb pair with
+    c2c noise under both policies, a zero-gain member in round-robin, and the
+    single-device reduction to a plain tile."""
+    out = {}
+    rng = np.random.default_rng(9)
+    for name, policy, gains in (("rr", 0, (1.0, -0.5, 0.0)), ("all", 1, (1.0, -0.5, 0.25))):
+        s = O.default("unitcell")
+        s.n_devices, s.policy = 3, policy
+        for k, g in enumerate(gains):
+            s.devices[k] = O.preset("reram_sb")
+            s.gains[k] = g
+        s.devices[2] = O.preset("reram_es")
+        u = O.unitcell(6, 5, s, 4321)
+        u.set_weights(rng.uniform(-0.2, 0.2, (6, 5)))
+        res = []
+        for step in range(8):
+            x = rng.uniform(-1, 1, 5)
+            d = rng.uniform(-1, 1, 6)
+            res.append(u.forward(x))
+            res.append(u.backward(d))
+            u.update(x, d, 0.05 if step != 3 else 0.0)
+        u.end_minibatch()
+        res.append(u.forward_noisy(np.ones(5), 0.05))
+        res.append(u.get_weights().ravel())
+        for m in u.members:
+            res.append(m.get_weights().ravel())
+        out[name] = np.concatenate(res)
+    s = O.default("unitcell")  # one device, gain 1 == a plain tile with the same seed
+    s.devices[0] = O.preset("reram_sb")
+    u = O.unitcell(4, 3, s, 99)
+    ts = O.default("tile")
+    ts.device = O.preset("reram_sb")
+    t = O.tile(4, 3, ts, 99)
+    for _ in range(5):
+        x, d = rng.uniform(-1, 1, 3), rng.uniform(-1, 1, 4)
+        u.update(x, d, 0.05)
+        t.update(x, d, 0.05)
+    out["single"] = np.concatenate([u.get_weights().ravel(), t.get_weights().ravel()])
+    return out
+
+
 def inference(O):
     """program / drift_to / compensation (proj/src/inference.cpp:34-110)."""
     s = O.default("tile")
@@ -251,7 +293,7 @@ def inference(O):
 
 
 ALL = [rng_streams, quantizer, matvec, devices, translate_trains, tile_updates, trains_apply,
-       temporal, transfer, inference]
+       temporal, transfer, unitcell, inference]
 
 
 def run_all(O) -> dict:
@@ -312,6 +354,30 @@ def error_cases(O):
         s.transfer_lr = 0.0
         O.transfer(2, 2, s, 1)
 
+    def unitcell_no_devices():
+        s = O.default("unitcell")
+        s.n_devices = 0
+        O.unitcell(2, 2, s, 1)
+
+    def unitcell_bad_gain():
+        s = O.default("unitcell")
+        s.gains[0] = float("inf")
+        O.unitcell(2, 2, s, 1)
+
+    def unitcell_bad_member():
+        s = O.default("unitcell")
+        s.n_devices = 2
+        s.devices[1] = O.default("device")
+        s.devices[1].dw_min = -1.0
+        O.unitcell(2, 2, s, 1)
+
+    def unitcell_zero_first_gain():
+        s = O.default("unitcell")
+        s.n_devices = 2
+        s.devices[1] = O.default("device")
+        s.gains[0], s.gains[1] = 0.0, 1.0
+        O.unitcell(2, 2, s, 1).set_weights(np.ones((2, 2)))
+
     def drift_before_t0():
         t = O.tile(2, 2, O.default("tile"), 1)
         t.drift_to(np.zeros((2, 2)), np.zeros((2, 2)), 20.0, 19.0)
@@ -325,4 +391,5 @@ def error_cases(O):
 
     return [tile_bad_dims, tile_bad_io, tile_bad_device, tile_bad_bounds, tile_bad_bl,
             tile_bad_reset, translate_bad_lr, translate_bad_dw, update_negative_lr, forward_nan,
-            preset_unknown, transfer_bad_lr, drift_before_t0, degenerate_comp]
+            preset_unknown, transfer_bad_lr, unitcell_no_devices, unitcell_bad_gain,
+            unitcell_bad_member, unitcell_zero_first_gain, drift_before_t0, degenerate_comp]
