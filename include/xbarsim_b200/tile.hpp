@@ -350,6 +350,14 @@ public:
   virtual void set_weights(const Matrix &w) = 0;
   virtual void end_minibatch() = 0;
   virtual std::unique_ptr<TileBase> clone() const = 0;
+
+  // batched extras of the B200 path: B samples per call,
+  // row-major fp32 host buffers; each equals B sequential reference calls on
+  // stationary weights.  lr[B] may be null (the tile's learning rate).
+  virtual void forward_batch(const float *X, int B, float *Y) = 0;
+  virtual void forward_noisy_batch(const float *X, int B, float *Y, double extra_sigma) = 0;
+  virtual void backward_batch(const float *D, int B, float *G) = 0;
+  virtual void update_batch(const float *X, const float *D, int B, const float *lr) = 0;
 };
 
 // proj/include/xbarsim/tile.hpp:75-131, on the GPU
@@ -510,11 +518,19 @@ public:
   void set_learning_rate(double lr) { check(xb_tile_set_learning_rate(h_, lr)); }
 
   // batched extras of the B200 path: B samples per call
-  void forward_batch(const float *X, int B, float *Y) {
+  void forward_batch(const float *X, int B, float *Y) override {
     flush();
     check(xb_tile_forward(h_, X, B, Y));
   }
-  void update_batch(const float *X, const float *D, int B, const float *lr) {
+  void forward_noisy_batch(const float *X, int B, float *Y, double extra) override {
+    flush();
+    check(xb_tile_forward_noisy(h_, X, B, Y, extra));
+  }
+  void backward_batch(const float *D, int B, float *G) override {
+    flush();
+    check(xb_tile_backward(h_, D, B, G));
+  }
+  void update_batch(const float *X, const float *D, int B, const float *lr) override {
     flush();
     check(xb_tile_update(h_, X, D, B, lr));
   }
@@ -619,6 +635,18 @@ public:
   void end_minibatch() override { check(xb_transfer_end_minibatch(h_)); }
   std::unique_ptr<TileBase> clone() const override {
     return std::make_unique<TransferTile>(*this);
+  }
+  void forward_batch(const float *X, int B, float *Y) override {
+    check(xb_transfer_forward(h_, X, B, Y));
+  }
+  void forward_noisy_batch(const float *X, int B, float *Y, double extra) override {
+    check(xb_transfer_forward_noisy(h_, X, B, Y, extra));
+  }
+  void backward_batch(const float *D, int B, float *G) override {
+    check(xb_transfer_backward(h_, D, B, G));
+  }
+  void update_batch(const float *X, const float *D, int B, const float *lr) override {
+    check(xb_transfer_update(h_, X, D, B, lr));
   }
   void transfer_step() { check(xb_transfer_step(h_)); }
   long transfer_events() const { return xb_transfer_events(h_); }
@@ -726,6 +754,18 @@ public:
   void end_minibatch() override { check(xb_unitcell_end_minibatch(h_)); }
   std::unique_ptr<TileBase> clone() const override {
     return std::make_unique<UnitCellTile>(*this);
+  }
+  void forward_batch(const float *X, int B, float *Y) override {
+    check(xb_unitcell_forward(h_, X, B, Y));
+  }
+  void forward_noisy_batch(const float *X, int B, float *Y, double extra) override {
+    check(xb_unitcell_forward_noisy(h_, X, B, Y, extra));
+  }
+  void backward_batch(const float *D, int B, float *G) override {
+    check(xb_unitcell_backward(h_, D, B, G));
+  }
+  void update_batch(const float *X, const float *D, int B, const float *lr) override {
+    check(xb_unitcell_update(h_, X, D, B, lr));
   }
   int n_members() const { return static_cast<int>(members_.size()); }
   // compound.hpp:53: read-only view of member k (weights, device realization)

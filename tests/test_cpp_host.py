@@ -12,8 +12,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 @pytest.mark.skipif(shutil.which("g++") is None, reason="no g++")
 def test_header_compiles_cleanly(tmp_path):
     src = tmp_path / "t.cpp"
-    src.write_text('#include "xbarsim_b200/tile.hpp"\n'
-                   "int main() { xbarsim_b200::TileSettings s; (void)s; return 0; }\n")
+    src.write_text('#include "xbarsim_b200/tile.hpp"\n#include "xbarsim_b200/nn.hpp"\n'
+                   "int main() { xbarsim_b200::TileSettings s; (void)s;\n"
+                   "  xbarsim_b200::Network n; (void)n; return 0; }\n")
     subprocess.run(["g++", "-std=c++20", "-Wall", "-Wextra", "-Werror", "-fsyntax-only",
                     "-I", os.path.join(ROOT, "include"), str(src)], check=True)
 
@@ -22,3 +23,4 @@ def test_header_compiles_cleanly(tmp_path):
 def test_parity_driver_links():
     subprocess.run(["sh", os.path.join(ROOT, "tests", "cpp", "build.sh")], check=True)
     assert os.path.exists(os.path.join(ROOT, "tests", "cpp", "test_tile_b200"))
+    assert os.path.exists(os.path.join(ROOT, "tests", "cpp", "test_nn_b200"))
