@@ -213,6 +213,7 @@ void launch_trains(const Tile &t, const float *X, const float *D, int B, const f
 // i.e. three FMAs and two min/max per pulse (plus one MUFU.EX2 for ExpStep).
 struct LawArgs {
   float slope, gamma, std;
+  float k2; // -2 ln2 std^2: the c2c radius factor of factor8_rk
 };
 
 struct Cell {
@@ -339,6 +340,30 @@ __device__ __forceinline__ void box_muller16(uint32_t a, float &z0, float &z1) {
   asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(th));
   z0 = r * c;
   z1 = r * s;
+}
+
+// c2c factors f = 1 + std z directly: std folds into the Box-Muller radius,
+// r = sqrt(-2 std^2 ln u) = sqrt(lg2(u) * k2) with k2 = -2 ln2 std^2, so each
+// factor is one FMA (1 + r cos) instead of a multiply and an FMA
+__device__ __forceinline__ void factor_pair16(uint32_t a, float k2, float &f0, float &f1) {
+  const float u = fmaf((float)(a & 0xffffu), 1.52587890625e-05f, 7.62939453125e-06f);
+  const float th = fmaf((float)(a >> 16), 9.587379924285257e-05f, -3.1415446284412245f);
+  float l, r, s, c;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(u));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(l * k2));
+  asm("sin.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(th));
+  asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(th));
+  f0 = fmaf(r, c, 1.0f);
+  f1 = fmaf(r, s, 1.0f);
+}
+
+__device__ __forceinline__ void factor8_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                           const RoundKeys &rk, float k2, float *f) {
+  philox10_rk(c0, c1, c2, c3, rk);
+  factor_pair16(c0, k2, f[0], f[1]);
+  factor_pair16(c1, k2, f[2], f[3]);
+  factor_pair16(c2, k2, f[4], f[5]);
+  factor_pair16(c3, k2, f[6], f[7]);
 }
 
 __device__ __forceinline__ void normal8_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
@@ -579,12 +604,11 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, pulse_minb<LAW>()) pulse_ker
     // ---------------- pulse loop: pulse n of every lane with n < T.  Words
     // below the shortest stream need no per-pulse activity test.
     auto pulses8 = [&](uint32_t word, uint32_t n, int sh8, bool check) {
-      float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      if (NOISE) normal8_rk(g0 + (n >> 3), jg, ig, call, rk, z);
+      float f[8] = {1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f};
+      if (NOISE) factor8_rk(g0 + (n >> 3), jg, ig, call, rk, la.k2, f);
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
-        const float f = NOISE ? fmaf(la.std, z[v], 1.0f) : 1.0f;
-        const float wn = cell.step(w, f, (word >> (sh8 + v)) & 1u);
+        const float wn = cell.step(w, f[v], (word >> (sh8 + v)) & 1u);
         if (!check || n + v < T) w = wn;
       }
     };
@@ -643,8 +667,9 @@ static void pulse_dispatch(Tile &t, const uint32_t *xw, const uint32_t *dw, int 
 void launch_pulse(Tile &t, const uint32_t *xw, const uint32_t *dw, int ldb, int B,
                   uint32_t call_id, bool flip) {
   if (B <= 0 || t.R == 0) return;
-  const LawArgs la{(float)t.cfg.device.slope, (float)t.cfg.device.gamma,
-                   (float)t.cfg.device.dw_min_std};
+  const double sd = t.cfg.device.dw_min_std;
+  const LawArgs la{(float)t.cfg.device.slope, (float)t.cfg.device.gamma, (float)sd,
+                   (float)(-2.0 * 0.6931471805599453 * sd * sd)};
   const bool noise = t.cfg.device.dw_min_std > 0.0;
 #define XB_PULSE(K)                                                                        \
   case K:                                                                                  \
@@ -727,8 +752,9 @@ static void det_dispatch(Tile &t, const double *px, const double *pd, const int3
 void launch_pulse_det(Tile &t, const double *px, const double *pd, const int32_t *bl, int B,
                       uint32_t call_id) {
   if (B <= 0 || t.R == 0) return;
-  const LawArgs la{(float)t.cfg.device.slope, (float)t.cfg.device.gamma,
-                   (float)t.cfg.device.dw_min_std};
+  const double sd = t.cfg.device.dw_min_std;
+  const LawArgs la{(float)t.cfg.device.slope, (float)t.cfg.device.gamma, (float)sd,
+                   (float)(-2.0 * 0.6931471805599453 * sd * sd)};
   const bool noise = t.cfg.device.dw_min_std > 0.0;
 #define XB_DET(K)                                                                          \
   case K:                                                                                  \
