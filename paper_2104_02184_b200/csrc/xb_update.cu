@@ -345,6 +345,7 @@ __device__ __forceinline__ void box_muller16(uint32_t a, float &z0, float &z1) {
 // c2c factors f = 1 + std z directly: std folds into the Box-Muller radius,
 // r = sqrt(-2 std^2 ln u) = sqrt(lg2(u) * k2) with k2 = -2 ln2 std^2, so each
 // factor is one FMA (1 + r cos) instead of a multiply and an FMA
+// (an IMAD-only int->float variant measured 12 % slower: the XU has room for I2F)
 __device__ __forceinline__ void factor_pair16(uint32_t a, float k2, float &f0, float &f1) {
   const float u = fmaf((float)(a & 0xffffu), 1.52587890625e-05f, 7.62939453125e-06f);
   const float th = fmaf((float)(a >> 16), 9.587379924285257e-05f, -3.1415446284412245f);
