@@ -20,6 +20,11 @@ namespace xb {
 
 namespace {
 
+// 2^m exactly (0 <= m < 1023) from the exponent field, not the fp64 exp2 routine
+__device__ __forceinline__ double pow2i(int m) {
+  return __longlong_as_double((long long)(1023 + m) << 52);
+}
+
 // --------------------------------------------------------------- prep
 // per-sample state for one MVM call: alpha (0 = zero input), norm of x~,
 // current BM exponent m, active flag for the current pass
@@ -101,7 +106,7 @@ __global__ void __launch_bounds__(PREP_THREADS) prep_kernel(const float *__restr
     s.active = 1;
   }
   const uint64_t seq = seq0 + (uint64_t)b;
-  const double inv = (s.alpha == 0.f) ? 0.0 : 1.0 / ((double)s.alpha * exp2((double)s.m));
+  const double inv = (s.alpha == 0.f) ? 0.0 : 1.0 / ((double)s.alpha * pow2i(s.m));
   auto convert = [&](float xv, int j) -> float {
     if (io.perfect) return xv;
     if (s.alpha == 0.f) return 0.f;
@@ -218,6 +223,26 @@ __global__ void __launch_bounds__(256) mvm_simt_kernel(const float *__restrict__
 }
 
 // --------------------------------------------------------------- epilogue
+// Output noise: one Philox call per GROUP of 4 consecutive global outputs
+// (counter = group, sample sequence number, BM exponent, tag); output 4g + k
+// takes word k, i.e. two 16-bit Box-Muller normals (z0 -> sigma_w fold,
+// z1 -> sigma_out).  Keyed on the global output index, so row shards and the
+// split-phase backward draw exactly what the whole tile draws.
+__device__ __forceinline__ void out_noise_words(uint32_t g, uint64_t seq, int m, Key key,
+                                                uint32_t w[4]) {
+  uint32_t c0 = g, c1 = (uint32_t)seq, c2 = (uint32_t)(seq >> 32) | ((uint32_t)m << 24),
+           c3 = TAG_OUT_NOISE << 24;
+  philox10(c0, c1, c2, c3, key);
+  w[0] = c0;
+  w[1] = c1;
+  w[2] = c2;
+  w[3] = c3;
+}
+
+// groups of 4 global outputs covering [o0, o0 + M)
+inline int out_groups(int o0, int M) { return ((o0 + M - 1) >> 2) - (o0 >> 2) + 1; }
+
+// one thread = one group of 4 outputs of one sample
 __global__ void __launch_bounds__(256) epilogue_kernel(const float *__restrict__ acc, int lda,
                                                         int nsplit, size_t split_stride, int M,
                                                         int o0, float *__restrict__ Y, int ldy,
@@ -228,34 +253,44 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const float *__restrict__
   const int b = blockIdx.y;
   const SampleState s = st[b];
   if (!first_pass && !s.active) return;
-  const int o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= M) return;
-  float a = acc[(size_t)b * lda + o];
-  for (int sp = 1; sp < nsplit; ++sp) a += acc[sp * split_stride + (size_t)b * lda + o];
-  if (io.perfect) {
-    Y[(size_t)b * ldy + o] = a;
-    return;
-  }
+  const int g = (o0 >> 2) + blockIdx.x * blockDim.x + threadIdx.x;
+  if (4 * g >= o0 + M) return;
   const uint64_t seq = seq0 + (uint64_t)b;
-  float z0 = 0.f, z1 = 0.f;
-  if (io.sigma_w > 0.0 || io.sigma_out > 0.0)
-    normal2((uint32_t)(o0 + o), (uint32_t)seq, (uint32_t)(seq >> 32) | (s.m << 24),
-            TAG_OUT_NOISE << 24, key, z0, z1);
-  double v;
-  double scale;
-  if (s.alpha == 0.f) { // io.cpp:107-115: zero input -> output noise only, no alpha
-    v = io.sigma_out > 0.0 ? io.sigma_out * (double)z1 : 0.0;
-    scale = 1.0;
-  } else {
-    v = (double)a;
-    if (io.sigma_w > 0.0) v += io.sigma_w * (double)s.norm * (double)z0;
-    if (io.sigma_out > 0.0) v += io.sigma_out * (double)z1;
-    scale = (double)s.alpha * exp2((double)s.m);
-    if (io.bm && s.alpha != 0.f && s.m < io.bm_max_iter && fabs(v) >= io.adc.bound) {
-      if (atomicExch(sat + b, 1) == 0) atomicAdd(sat + B + pass_slot, 1);
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
+  const bool noisy = !io.perfect && (io.sigma_w > 0.0 || io.sigma_out > 0.0);
+  if (noisy) out_noise_words((uint32_t)g, seq, s.m, key, w);
+  const double scale = s.alpha == 0.f ? 1.0 : (double)s.alpha * pow2i(s.m);
+  bool hit = false;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int o = 4 * g + k - o0;
+    if (o < 0 || o >= M) continue;
+    float a = acc[(size_t)b * lda + o];
+    for (int sp = 1; sp < nsplit; ++sp) a += acc[sp * split_stride + (size_t)b * lda + o];
+    if (io.perfect) {
+      Y[(size_t)b * ldy + o] = a;
+      continue;
     }
+    float z0 = 0.f, z1 = 0.f;
+    if (noisy) box_muller16(w[k], z0, z1);
+    double v;
+    if (s.alpha == 0.f) { // io.cpp:107-115: zero input -> output noise only, no alpha
+      v = io.sigma_out > 0.0 ? io.sigma_out * (double)z1 : 0.0;
+    } else {
+      v = (double)a;
+      if (io.sigma_w > 0.0) v += io.sigma_w * (double)s.norm * (double)z0;
+      if (io.sigma_out > 0.0) v += io.sigma_out * (double)z1;
+      hit |= fabs(v) >= io.adc.bound;
+    }
+    Y[(size_t)b * ldy + o] = (float)(scale * quantize(v, io.adc));
   }
-  Y[(size_t)b * ldy + o] = (float)(scale * quantize(v, io.adc));
+  if (io.bm && s.alpha != 0.f && s.m < io.bm_max_iter) {
+    // one flag write per warp (a saturating sample saturates many outputs:
+    // per-thread atomics on the same word serialise)
+    const unsigned any = __ballot_sync(__activemask(), hit);
+    if (hit && (threadIdx.x & 31) == __ffs(any) - 1 && atomicExch(sat + b, 1) == 0)
+      atomicAdd(sat + B + pass_slot, 1);
+  }
 }
 
 // Row-shard backward, phase 1: the shard's column sums plus its share of the
@@ -283,33 +318,42 @@ __global__ void __launch_bounds__(256) partial_kernel(const float *__restrict__ 
 
 // Row-shard backward, phase 2 (after the sum over shards): output noise, ADC
 // and alpha act on the reduced column sums, as in proj/src/io.cpp:143-146.
+// Same noise groups as epilogue_kernel (o0 = 0, m = 0), so the split-phase
+// backward reproduces the whole-tile backward bit for bit.
 __global__ void __launch_bounds__(256) finish_kernel(const float *__restrict__ Psum, int M,
                                                       const float *__restrict__ amax,
                                                       float *__restrict__ Y, IoDev io, Key key,
                                                       uint64_t seq0) {
   const int b = blockIdx.y;
-  const int o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= M) return;
-  const float a = Psum[(size_t)b * M + o];
-  if (io.perfect) {
-    Y[(size_t)b * M + o] = a;
-    return;
-  }
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (4 * g >= M) return;
   const float m = amax[b];
   const double alpha = (m == 0.f) ? 0.0 : (io.nm_absmax ? (double)m : 1.0);
   const uint64_t seq = seq0 + (uint64_t)b;
-  float z0 = 0.f, z1 = 0.f;
-  if (io.sigma_out > 0.0)
-    normal2((uint32_t)o, (uint32_t)seq, (uint32_t)(seq >> 32), TAG_OUT_NOISE << 24, key, z0, z1);
-  double v, scale;
-  if (alpha == 0.0) {
-    v = io.sigma_out > 0.0 ? io.sigma_out * (double)z1 : 0.0;
-    scale = 1.0;
-  } else {
-    v = (double)a + (io.sigma_out > 0.0 ? io.sigma_out * (double)z1 : 0.0);
-    scale = alpha;
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
+  const bool noisy = !io.perfect && (io.sigma_w > 0.0 || io.sigma_out > 0.0);
+  if (noisy) out_noise_words((uint32_t)g, seq, 0, key, w);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int o = 4 * g + k;
+    if (o >= M) continue;
+    const float a = Psum[(size_t)b * M + o];
+    if (io.perfect) {
+      Y[(size_t)b * M + o] = a;
+      continue;
+    }
+    float z0 = 0.f, z1 = 0.f;
+    if (noisy) box_muller16(w[k], z0, z1);
+    double v, scale;
+    if (alpha == 0.0) {
+      v = io.sigma_out > 0.0 ? io.sigma_out * (double)z1 : 0.0;
+      scale = 1.0;
+    } else {
+      v = (double)a + (io.sigma_out > 0.0 ? io.sigma_out * (double)z1 : 0.0);
+      scale = alpha;
+    }
+    Y[(size_t)b * M + o] = (float)(scale * quantize(v, io.adc));
   }
-  Y[(size_t)b * M + o] = (float)(scale * quantize(v, io.adc));
 }
 
 struct MvmScratch {
@@ -381,7 +425,8 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io, Key
       XB_CUDA(cudaGetLastError());
       return;
     }
-    dim3 eg((M + 255) / 256, B);
+    const int o0 = TRANS ? 0 : t.row0;
+    dim3 eg((out_groups(o0, M) + 255) / 256, B);
     epilogue_kernel<<<eg, 256, 0, t.stream>>>(s.acc, M, nsplit, (size_t)B * M, M,
                                               TRANS ? 0 : t.row0, dOut, M, s.st, io, key, seq0,
                                               s.sat, first, B, pass);
@@ -430,7 +475,7 @@ void mvm_backward_finish(Tile &t, const float *dPsum, int B, const float *amax_g
                          const IoDev &io, Key key, uint64_t seq0) {
   if (B <= 0) return;
   if (!amax_global) raise("backward_finish: the global max|d| per sample is required");
-  dim3 eg((t.C + 255) / 256, B);
+  dim3 eg((out_groups(0, t.C) + 255) / 256, B);
   finish_kernel<<<eg, 256, 0, t.stream>>>(dPsum, t.C, amax_global, dG, io, key, seq0);
   count_launch();
   XB_CUDA(cudaGetLastError());

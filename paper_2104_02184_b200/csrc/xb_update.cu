@@ -327,21 +327,6 @@ __device__ __forceinline__ void box_muller_fast(uint32_t a, uint32_t b, float &z
   z1 = r * s;
 }
 
-// eight normals per Philox call from 16-bit uniforms (half-LSB centred):
-// the radius then reaches sqrt(2 ln 2^17) = 4.9 sigma, a tail mass of 1e-6
-// that the c2c write-noise statistics cannot resolve
-__device__ __forceinline__ void box_muller16(uint32_t a, float &z0, float &z1) {
-  const float u = fmaf((float)(a & 0xffffu), 1.52587890625e-05f, 7.62939453125e-06f);
-  const float th = fmaf((float)(a >> 16), 9.587379924285257e-05f, -3.1415446284412245f);
-  float l, r, s, c;
-  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(u));
-  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(l * -1.3862943611198906f)); // -2 ln u
-  asm("sin.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(th));
-  asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(th));
-  z0 = r * c;
-  z1 = r * s;
-}
-
 // c2c factors f = 1 + std z directly: std folds into the Box-Muller radius,
 // r = sqrt(-2 std^2 ln u) = sqrt(lg2(u) * k2) with k2 = -2 ln2 std^2, so each
 // factor is one FMA (1 + r cos) instead of a multiply and an FMA
@@ -367,14 +352,6 @@ __device__ __forceinline__ void factor8_rk(uint32_t c0, uint32_t c1, uint32_t c2
   factor_pair16(c3, k2, f[6], f[7]);
 }
 
-__device__ __forceinline__ void normal8_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
-                                           const RoundKeys &rk, float *z) {
-  philox10_rk(c0, c1, c2, c3, rk);
-  box_muller16(c0, z[0], z[1]);
-  box_muller16(c1, z[2], z[3]);
-  box_muller16(c2, z[4], z[5]);
-  box_muller16(c3, z[6], z[7]);
-}
 
 __device__ __forceinline__ void normal4_fast(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
                                              Key key, float &z0, float &z1, float &z2,

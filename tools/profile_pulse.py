@@ -20,6 +20,7 @@ ap.add_argument("--batch", type=int, default=256)
 ap.add_argument("--device", default="reram_sb")
 ap.add_argument("--precision", type=int, default=xb.MVM_FP32)
 ap.add_argument("--warm", type=int, default=0, help="untimed iterations first")
+ap.add_argument("--backward", action="store_true", help="also run backward_dev each iteration")
 args = ap.parse_args()
 
 dev = xb.device_preset(args.device)
@@ -41,9 +42,12 @@ with torch.cuda.stream(s):
         t.update_dev(X, D, 0.01)
 t.synchronize()
 t.set_timing(True)
+G = torch.empty(args.batch, args.n, device="cuda")
 with torch.cuda.stream(s):
     for _ in range(args.iters):
         t.forward_dev(X, Y)
+        if args.backward:
+            t.backward_dev(D, G)
         t.update_dev(X, D, 0.01)
 tm = t.read_timing()
 print(os.environ.get("XBTILE_LIB", "default"),
