@@ -122,7 +122,7 @@ void launch_drift(Tile &t, double ratio);
 void launch_nonfinite(const float *v, size_t n, int bit, int *flag, cudaStream_t s);
 
 // ---- tcgen05 contraction (xb_mvm_tc.cu) ----
-int tc_splits(int M, int K);
+int tc_splits(int M, int K, bool x3);
 int tc_used_splits(int K, int splits);
 void tc_gemm(Tile &t, bool transposed, bool x3, const float *Xt, int ldt, int B, float *part,
              int splits);

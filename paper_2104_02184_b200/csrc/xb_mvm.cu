@@ -398,7 +398,7 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io, Key
   // otherwise (exact-fp32 parity mode, tiny batches)
   const bool x3 = t.cfg.mvm_precision == XB_MVM_TF32X3;
   const bool tc = (t.cfg.mvm_precision == XB_MVM_TF32 || x3) && B >= 16;
-  const int splits = tc ? tc_used_splits(K, tc_splits(M, K)) : 1;
+  const int splits = tc ? tc_used_splits(K, tc_splits(M, K, x3)) : 1;
   const int ldt = (K + 3) & ~3; // x~ rows padded to 16 bytes (TMA global stride)
   MvmScratch s = carve(t, B, ldt, M, splits);
   if (io.bm) XB_CUDA(cudaMemsetAsync(s.sat, 0, sizeof(int) * (B + 32), t.stream));

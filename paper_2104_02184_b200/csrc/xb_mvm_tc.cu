@@ -27,18 +27,24 @@ namespace xb {
 
 namespace {
 
-constexpr int TC_BM = 128;
-constexpr int TC_BK = 32; // fp32 elements per 128-byte swizzle row
+constexpr int TC_BM = 128; // rows of one UMMA (M) = one TMEM lane per row
+constexpr int TC_BK = 32;  // fp32 elements per 128-byte swizzle row
 constexpr int TC_MAX_BN = 256;
-constexpr int TC_A_BYTES = TC_BM * TC_BK * 4;     // 16 KB
+constexpr int TC_A_BYTES = TC_BM * TC_BK * 4;     // 16 KB per 128-row sub-tile
 constexpr int TC_B_BYTES = TC_MAX_BN * TC_BK * 4; // 32 KB (max)
-// TF32: 4-stage ring of (A, B).  3xTF32: 2-stage ring of (A_hi, B_hi, A_lo, B_lo)
-template <bool X3> constexpr int tc_stages() { return X3 ? 2 : 4; }
-template <bool X3> constexpr int tc_stage_bytes() {
-  return (X3 ? 2 : 1) * (TC_A_BYTES + TC_B_BYTES);
+// A CTA owns NSUB 128-row sub-tiles of the output (NSUB accumulators of BN
+// TMEM columns) and streams ONE x~ tile per K-block for all of them: the
+// x~ operand is re-read once per CTA row-band, so NSUB = 2 halves its L2->SM
+// traffic (x~ is the larger operand per K-block at N = 256 > M = 128).
+// TF32: ring of (A, B); 3xTF32: 2-stage ring of (A_hi, B_hi, A_lo, B_lo).
+template <bool X3, int NSUB> constexpr int tc_stage_bytes() {
+  return (X3 ? 2 : 1) * (NSUB * TC_A_BYTES + TC_B_BYTES);
 }
-template <bool X3> constexpr int tc_smem() {
-  return tc_stages<X3>() * tc_stage_bytes<X3>() + 1024 /*align*/ + 256 /*bars*/;
+template <bool X3, int NSUB> constexpr int tc_stages() {
+  return X3 ? 2 : (NSUB == 1 ? 4 : 3);
+}
+template <bool X3, int NSUB> constexpr int tc_smem() {
+  return tc_stages<X3, NSUB>() * tc_stage_bytes<X3, NSUB>() + 1024 /*align*/ + 256 /*bars*/;
 }
 template <bool X3> constexpr int tc_threads() { return X3 ? 256 : 128; }
 
@@ -139,39 +145,42 @@ __device__ __forceinline__ void split_tf32(float4 &v, float4 &lo) {
   }
 }
 
-// A_MN = false: A = W tile [128 rows][32 K] (forward, K-major)
-// A_MN = true : A = W^T tile, i.e. W[32 K-rows][128 columns] (backward, MN-major):
-//               four 32x32 TMA boxes (128B/32B-atom swizzle) per stage, one per
-//               32-column MN atom, 4 KB apart
+// A_MN = false: A = W tile [NSUB*128 rows][32 K] (forward, K-major; one TMA box)
+// A_MN = true : A = W^T tile, i.e. W[32 K-rows][NSUB*128 columns] (backward,
+//               MN-major): 4*NSUB 32x32 TMA boxes (128B/32B-atom swizzle) per
+//               stage, one per 32-column MN atom, 4 KB apart
 // X3 = true   : 3xTF32.  Warps 2-7 split every landed stage in place into hi
 //               and a lo copy (generic-proxy writes, then fence.proxy.async);
 //               the MMA thread issues hi*hi + hi*lo + lo*hi per K-step, which
 //               recovers ~fp32 accuracy of the products at 3x the tensor work.
 //               Warps 4-7 run the epilogue (TMEM lane quarter = warp % 4).
-template <bool A_MN, bool X3>
+template <bool A_MN, bool X3, int NSUB>
 __global__ void __launch_bounds__(tc_threads<X3>(), 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                    int M, int K, int B, int bn, int kblocks_per_split, float *__restrict__ part,
                    int ldp, size_t split_stride) {
-  constexpr int STAGES = tc_stages<X3>();
-  constexpr int SB = tc_stage_bytes<X3>();
+  constexpr int STAGES = tc_stages<X3, NSUB>();
+  constexpr int SB = tc_stage_bytes<X3, NSUB>();
+  constexpr int AB = NSUB * TC_A_BYTES;          // A bytes per stage
+  constexpr int LO = NSUB * TC_A_BYTES + TC_B_BYTES; // offset of the lo copies (X3)
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte alignment for the 128-byte swizzle atoms; stage s holds
-  // [A | B | A_lo | B_lo] at offsets 0, 16K, 48K, 64K
+  // [A | B | A_lo | B_lo]
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t *bars = (uint64_t *)(smem + STAGES * SB);
   uint32_t *tmem_slot = (uint32_t *)(bars + 3 * STAGES + 1);
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES),
                  conv0 = smem_u32(bars + 2 * STAGES), done = smem_u32(bars + 3 * STAGES);
   auto stage_a = [&](int s) { return smem + s * SB; };
-  auto stage_b = [&](int s) { return smem + s * SB + TC_A_BYTES; };
+  auto stage_b = [&](int s) { return smem + s * SB + AB; };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * TC_BM;
+  const int m0 = blockIdx.x * TC_BM * NSUB;
   const int split = blockIdx.y;
   const int kb0 = split * kblocks_per_split;
   const int nkb = min(kblocks_per_split, (K + TC_BK - 1) / TC_BK - kb0);
   constexpr int CONV_THREADS = tc_threads<X3>() - 64;
+  constexpr uint32_t TMEM_COLS = NSUB * TC_MAX_BN; // 256 or all 512 columns
 
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_a)) : "memory");
@@ -184,10 +193,10 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1)
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) { // TMEM: 256 fp32 columns x 128 lanes (the whole accumulator)
+  if (warp == 1) { // TMEM: NSUB accumulators of 256 fp32 columns x 128 lanes
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(TC_MAX_BN));
+                 "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -202,11 +211,11 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1)
       const int s = kb % STAGES;
       const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
       mbar_wait(empty0 + 8 * s, ph ^ 1u);
-      mbar_expect_tx(full0 + 8 * s, TC_A_BYTES + b_bytes);
+      mbar_expect_tx(full0 + 8 * s, AB + b_bytes);
       const int kk = (kb0 + kb) * TC_BK;
       if (A_MN) {
 #pragma unroll
-        for (int a = 0; a < TC_BM / 32; ++a)
+        for (int a = 0; a < NSUB * TC_BM / 32; ++a)
           tma_load_2d(smem_u32(stage_a(s) + a * 4096), &tm_a, full0 + 8 * s, m0 + 32 * a, kk);
       } else {
         tma_load_2d(smem_u32(stage_a(s)), &tm_a, full0 + 8 * s, kk, m0);
@@ -226,18 +235,23 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1)
       const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
       mbar_wait((X3 ? conv0 : full0) + 8 * s, ph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint64_t da = umma_desc(smem_u32(stage_a(s)), a_lbo, a_sbo, a_layout);
       const uint64_t db = umma_desc(smem_u32(stage_b(s)), 16u, 1024u, 2u);
+      const uint64_t dbl = umma_desc(smem_u32(stage_b(s) + LO), 16u, 1024u, 2u);
 #pragma unroll
-      for (int k = 0; k < TC_BK / 8; ++k) {
-        mma_tf32(tmem, da + a_step * k, db + 2u * k, idesc, (kb | k) != 0);
-        if (X3) {
-          const uint64_t dal =
-              umma_desc(smem_u32(stage_a(s) + TC_A_BYTES + TC_B_BYTES), a_lbo, a_sbo, a_layout);
-          const uint64_t dbl = umma_desc(smem_u32(stage_b(s) + TC_A_BYTES + TC_B_BYTES), 16u,
-                                         1024u, 2u);
-          mma_tf32(tmem, da + a_step * k, dbl + 2u * k, idesc, 1u);
-          mma_tf32(tmem, dal + a_step * k, db + 2u * k, idesc, 1u);
+      for (int sub = 0; sub < NSUB; ++sub) {
+        // sub-tile: K-major rows 128*sub.. (16 KB further); MN-major atoms 4*sub..
+        const uint64_t da =
+            umma_desc(smem_u32(stage_a(s) + sub * TC_A_BYTES), a_lbo, a_sbo, a_layout);
+        const uint64_t dal =
+            umma_desc(smem_u32(stage_a(s) + LO + sub * TC_A_BYTES), a_lbo, a_sbo, a_layout);
+        const uint32_t acc = tmem + (uint32_t)(sub * TC_MAX_BN);
+#pragma unroll
+        for (int k = 0; k < TC_BK / 8; ++k) {
+          mma_tf32(acc, da + a_step * k, db + 2u * k, idesc, (kb | k) != 0);
+          if (X3) {
+            mma_tf32(acc, da + a_step * k, dbl + 2u * k, idesc, 1u);
+            mma_tf32(acc, dal + a_step * k, db + 2u * k, idesc, 1u);
+          }
         }
       }
       mma_commit(empty0 + 8 * s); // smem stage free once these MMAs retire
@@ -246,15 +260,14 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1)
   } else if (X3 && warp >= 2 && nkb > 0) {
     // ---------------- hi/lo split of each landed stage (3xTF32)
     const int ct = threadIdx.x - 64;
-    const int na4 = TC_A_BYTES / 16, nb4 = (int)(b_bytes / 16);
+    const int n4 = (AB + (int)b_bytes) / 16; // B follows A directly in both halves
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % STAGES;
       const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
       mbar_wait(full0 + 8 * s, ph);
       float4 *a4 = reinterpret_cast<float4 *>(stage_a(s));
-      float4 *al4 = reinterpret_cast<float4 *>(stage_a(s) + TC_A_BYTES + TC_B_BYTES);
-      for (int e = ct; e < na4 + nb4; e += CONV_THREADS) {
-        // B words follow A's 16 KB directly, in both the hi and the lo halves
+      float4 *al4 = reinterpret_cast<float4 *>(stage_a(s) + LO);
+      for (int e = ct; e < n4; e += CONV_THREADS) {
         float4 v = a4[e], lo;
         split_tf32(v, lo);
         a4[e] = v;
@@ -274,17 +287,21 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
     const int quarter = warp & 3;
-    const int o = m0 + quarter * 32 + lane;
     float *dst = part + (size_t)split * split_stride;
-    for (int c0 = 0; c0 < bn; c0 += 32) {
-      uint32_t r[32];
-      XB_TMEM_LD32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, r);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (o < M) {
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const int b = c0 + c;
-          if (b < B) dst[(size_t)b * ldp + o] = nkb > 0 ? __uint_as_float(r[c]) : 0.f;
+    for (int sub = 0; sub < NSUB; ++sub) {
+      const int o = m0 + sub * TC_BM + quarter * 32 + lane;
+      for (int c0 = 0; c0 < bn; c0 += 32) {
+        uint32_t r[32];
+        XB_TMEM_LD32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(sub * TC_MAX_BN + c0),
+                     r);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (o < M) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const int b = c0 + c;
+            if (b < B) dst[(size_t)b * ldp + o] = nkb > 0 ? __uint_as_float(r[c]) : 0.f;
+          }
         }
       }
     }
@@ -293,7 +310,7 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1)
   __syncthreads();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(TC_MAX_BN));
+                 "r"(TMEM_COLS));
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -331,57 +348,70 @@ CUtensorMap make_map(const float *base, int rows, int cols, int ld, int box_rows
 
 } // namespace
 
-int tc_splits(int M, int K) {
-  const int mt = (M + TC_BM - 1) / TC_BM;
+// 128-row sub-tiles per CTA.  Two halve the x~ re-reads but need twice the
+// K-splits to fill the SMs (more partial-sum traffic): measured on B200 they
+// win for 16384^2 (forward 571 vs 607 us, backward 263 vs 278 us) and lose
+// for 4096^2 (70 vs 66 us); one for 3xTF32 (its stage would not fit twice)
+static int tc_nsub(int M, bool x3) { return (!x3 && M >= 8192) ? 2 : 1; }
+
+int tc_splits(int M, int K, bool x3) {
+  const int band = TC_BM * tc_nsub(M, x3);
+  const int mt = (M + band - 1) / band;
   const int kbs = (K + TC_BK - 1) / TC_BK;
   int s = std::max(1, 148 / std::max(mt, 1));
   s = std::min(s, std::max(1, kbs / 4)); // keep >= 4 K-blocks per split
   return std::max(1, std::min(s, 16));
 }
 
-// contraction on tcgen05: part[s][b][o] (split stride B x M).
-//   forward : o = row of W, K = columns of W   (A = W, K-major)
-//   backward: o = column of W, K = rows of W   (A = W^T, MN-major)
-template <bool A_MN, bool X3>
+template <bool A_MN, bool X3, int NSUB>
 static void launch_tc(dim3 grid, cudaStream_t st, const CUtensorMap &ma, const CUtensorMap &mb,
                       int M, int K, int nb, int bn, int per, float *part, size_t split_stride) {
   static bool configured = false;
   if (!configured) {
-    XB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<A_MN, X3>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem<X3>()));
+    XB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<A_MN, X3, NSUB>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 tc_smem<X3, NSUB>()));
     configured = true;
   }
-  tc_gemm_kernel<A_MN, X3><<<grid, tc_threads<X3>(), tc_smem<X3>(), st>>>(
+  tc_gemm_kernel<A_MN, X3, NSUB><<<grid, tc_threads<X3>(), tc_smem<X3, NSUB>(), st>>>(
       ma, mb, M, K, nb, bn, per, part, M, split_stride);
   count_launch();
   XB_CUDA(cudaGetLastError());
 }
 
+// contraction on tcgen05: part[s][b][o] (split stride B x M).
+//   forward : o = row of W, K = columns of W   (A = W, K-major)
+//   backward: o = column of W, K = rows of W   (A = W^T, MN-major)
 void tc_gemm(Tile &t, bool transposed, bool x3, const float *Xt, int ldt, int B, float *part,
              int splits) {
   const int M = transposed ? t.C : t.R, K = transposed ? t.R : t.C;
+  const int nsub = tc_nsub(M, x3);
   const int kbs = (K + TC_BK - 1) / TC_BK;
   const int per = (kbs + splits - 1) / splits;
   const int used = (kbs + per - 1) / per;
   for (int n0 = 0; n0 < B; n0 += TC_MAX_BN) {
     const int nb = std::min(TC_MAX_BN, B - n0);
     const int bn = std::max(16, (nb + 15) / 16 * 16);
-    // W as [R][C] with row stride ld: the forward box is 128 rows x 32 columns,
-    // the backward box 32 rows (K) x 32 columns (one MN atom)
-    const CUtensorMap ma = transposed
-                               ? make_map(t.W, t.R, t.C, t.ld, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)
-                               : make_map(t.W, t.R, t.C, t.ld, TC_BM);
+    // W as [R][C] with row stride ld: the forward box is 128*nsub rows x 32
+    // columns, the backward box 32 rows (K) x 32 columns (one MN atom)
+    const CUtensorMap ma =
+        transposed ? make_map(t.W, t.R, t.C, t.ld, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)
+                   : make_map(t.W, t.R, t.C, t.ld, TC_BM * nsub);
     const CUtensorMap mb = make_map(Xt + (size_t)n0 * ldt, nb, K, ldt, bn);
-    const dim3 grid((M + TC_BM - 1) / TC_BM, used);
+    const dim3 grid((M + TC_BM * nsub - 1) / (TC_BM * nsub), used);
     // partial sums of this N slab land at part + n0 rows, split stride B x M
     float *p = part + (size_t)n0 * M;
     const size_t ss = (size_t)B * M;
-    if (transposed)
-      x3 ? launch_tc<true, true>(grid, t.stream, ma, mb, M, K, nb, bn, per, p, ss)
-         : launch_tc<true, false>(grid, t.stream, ma, mb, M, K, nb, bn, per, p, ss);
-    else
-      x3 ? launch_tc<false, true>(grid, t.stream, ma, mb, M, K, nb, bn, per, p, ss)
-         : launch_tc<false, false>(grid, t.stream, ma, mb, M, K, nb, bn, per, p, ss);
+    if (x3) {
+      transposed ? launch_tc<true, true, 1>(grid, t.stream, ma, mb, M, K, nb, bn, per, p, ss)
+                 : launch_tc<false, true, 1>(grid, t.stream, ma, mb, M, K, nb, bn, per, p, ss);
+    } else if (nsub == 2) {
+      transposed ? launch_tc<true, false, 2>(grid, t.stream, ma, mb, M, K, nb, bn, per, p, ss)
+                 : launch_tc<false, false, 2>(grid, t.stream, ma, mb, M, K, nb, bn, per, p, ss);
+    } else {
+      transposed ? launch_tc<true, false, 1>(grid, t.stream, ma, mb, M, K, nb, bn, per, p, ss)
+                 : launch_tc<false, false, 1>(grid, t.stream, ma, mb, M, K, nb, bn, per, p, ss);
+    }
   }
 }
 

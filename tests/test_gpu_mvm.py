@@ -191,7 +191,7 @@ def test_forward_noisy_read_noise():
 
 
 @pytest.mark.parametrize("shape,B", [((256, 256), 16), ((300, 520), 37), ((512, 4096), 256),
-                                     ((128, 64), 300)])
+                                     ((128, 64), 300), ((8320, 200), 40)])
 def test_tcgen05_tf32_forward(shape, B):
     """The tcgen05 kind::tf32 contraction (TMA + TMEM, split-K) against the fp32
     SIMT path on the same weights: TF32 keeps 10 mantissa bits, so outputs
@@ -294,7 +294,7 @@ def test_bound_management_reissue(prec):
 
 
 @pytest.mark.parametrize("shape,B", [((256, 256), 16), ((520, 300), 37), ((4096, 512), 256),
-                                     ((45, 37), 20), ((130, 77), 300)])
+                                     ((45, 37), 20), ((130, 77), 300), ((96, 8320), 24)])
 def test_tcgen05_tf32_backward(shape, B):
     """Backward contraction W^T d on tcgen05 with the MN-major A operand
     (four 32x32 TMA boxes per stage) against the fp32 SIMT path."""
