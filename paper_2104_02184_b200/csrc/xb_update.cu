@@ -25,20 +25,41 @@
 namespace xb {
 
 // ============================================================== K3: amax
-__global__ void rows_amax_kernel(const float *__restrict__ V, int n, int ld,
-                                 float *__restrict__ out) {
+// one CTA per sample row; 16-byte loads (when the row allows them), four in
+// flight per thread, so the pass streams at HBM rate instead of waiting on
+// one dependent load per iteration
+__global__ void __launch_bounds__(256) rows_amax_kernel(const float *__restrict__ V, int n, int ld,
+                                                        float *__restrict__ out) {
   const int b = blockIdx.x;
   const float *row = V + (size_t)b * ld;
-  float m = 0.f;
-  for (int j = threadIdx.x; j < n; j += blockDim.x) m = fmaxf(m, fabsf(row[j]));
-  m = warp_max(m);
-  __shared__ float red[32];
+  float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
+  int head = 0;
+  if ((((uintptr_t)row) & 15) == 0) {
+    const float4 *r4 = reinterpret_cast<const float4 *>(row);
+    const int n4 = n >> 2;
+    int j = threadIdx.x;
+    for (; j + 3 * 256 < n4; j += 4 * 256) {
+      const float4 a = __ldg(r4 + j), c = __ldg(r4 + j + 256), e = __ldg(r4 + j + 512),
+                   g = __ldg(r4 + j + 768);
+      m0 = fmaxf(m0, fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(a.z), fabsf(a.w))));
+      m1 = fmaxf(m1, fmaxf(fmaxf(fabsf(c.x), fabsf(c.y)), fmaxf(fabsf(c.z), fabsf(c.w))));
+      m2 = fmaxf(m2, fmaxf(fmaxf(fabsf(e.x), fabsf(e.y)), fmaxf(fabsf(e.z), fabsf(e.w))));
+      m3 = fmaxf(m3, fmaxf(fmaxf(fabsf(g.x), fabsf(g.y)), fmaxf(fabsf(g.z), fabsf(g.w))));
+    }
+    for (; j < n4; j += 256) {
+      const float4 a = __ldg(r4 + j);
+      m0 = fmaxf(m0, fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(a.z), fabsf(a.w))));
+    }
+    head = n4 << 2;
+  }
+  for (int j = head + threadIdx.x; j < n; j += 256) m1 = fmaxf(m1, fabsf(row[j]));
+  float m = warp_max(fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)));
+  __shared__ float red[8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) red[warp] = m;
   __syncthreads();
   if (warp == 0) {
-    m = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.f;
-    m = warp_max(m);
+    m = warp_max(lane < 8 ? red[lane] : 0.f);
     if (lane == 0) out[b] = m;
   }
 }

@@ -16,9 +16,12 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
 python tools/profile_pulse.py --precision 1 --iters 2 --backward > /dev/null
 ncu --set full --import-source on --clock-control none -k regex:pulse_kernel -s 1 -c 1 -f \
     -o $OUT/pulse python tools/profile_pulse.py --precision 1 --iters 2 > $OUT/ncu_pulse.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:tc_gemm -s 2 -c 2 -f \
+ncu --set full --import-source on --clock-control none -k regex:tc_gemm -s 2 -c 1 -f \
     -o $OUT/tc_tf32 python tools/profile_pulse.py --precision 1 --iters 2 --backward \
     > $OUT/ncu_tc.log 2>&1
+ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
+    -k "regex:tc_gemm_kernel<1" -s 1 -c 1 -f -o $OUT/tc_tf32_bwd \
+    python tools/profile_pulse.py --precision 1 --iters 2 --backward > $OUT/ncu_tcb.log 2>&1
 python tools/profile_pulse.py --precision 2 --iters 2 > /dev/null
 ncu --set full --import-source on --clock-control none -k regex:tc_gemm -s 1 -c 1 -f \
     -o $OUT/tc_x3 python tools/profile_pulse.py --precision 2 --iters 2 > $OUT/ncu_tcx3.log 2>&1
