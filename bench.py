@@ -256,7 +256,10 @@ def run_ours(args):
                                   "forward": fwd_ms},
             "roofline": {"bound": "int-pipe", "achieved": achieved / 1e9,
                          "peak": int_peak / 1e9, "unit": "Gop/s",
-                         "frac": achieved / int_peak, "traffic": None,
+                         "frac": achieved / int_peak, "traffic": pulse_traffic(),
+                         "traffic_unit": "DRAM bytes per launch (read + write)",
+                         "algorithmic_bytes": 4.0 * 2 * N_ROWS * N_COLS + 16.0 * N_ROWS * N_COLS
+                         + 4.0 * (N_ROWS + N_COLS) * BATCH,
                          "kernel": "pulse_kernel<SOFT_BOUNDS,noise>",
                          "basis": f"SURVEY 8d: (2 + kbar*15) INT ops per cell-update, "
                                   f"kbar={kbar:.4f} measured on 32 samples",
@@ -274,6 +277,27 @@ def run_ours(args):
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
+
+
+def pulse_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum of pulse_kernel per launch,
+    from the committed `ncu --set full` capture (profiles/r*/), or None."""
+    import glob
+    import re
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_full_pulse_kernel.txt")))
+    if not files:
+        return None
+    txt = open(files[-1]).read()
+    tot = 0.0
+    for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        m = re.search(name + r"\s+(\w+)\s+([0-9.]+)", txt)
+        if not m:
+            return None
+        unit = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(m.group(1))
+        if unit is None:
+            return None
+        tot += float(m.group(2)) * unit
+    return tot
 
 
 # ============================================================ reference arm
