@@ -124,8 +124,7 @@ void launch_nonfinite(const float *v, size_t n, int bit, int *flag, cudaStream_t
 // ---- tcgen05 contraction (xb_mvm_tc.cu) ----
 int tc_splits(int M, int K, bool x3);
 int tc_used_splits(int K, int splits);
-void tc_gemm(Tile &t, bool transposed, bool x3, const float *Xt, int ldt, int B, float *part,
-             int splits);
+// tc_gemm: declared in xb_mvm_common.cuh (takes the fused output-stage arguments)
 
 // ---- noisy MVM (xb_mvm.cu) ----
 // forward: Y[b][i] = alpha_b * ADC(sum_j W[i][j] x~[b][j] + noise), i local rows

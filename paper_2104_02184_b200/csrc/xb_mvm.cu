@@ -14,26 +14,13 @@
 // Weight noise: sum_j (w_ij + sigma_w xi_ij) x~_j = sum_j w_ij x~_j + sigma_w
 // ||x~|| zeta_i exactly in distribution (independent xi_ij), so the per-use
 // d_out x d_in Gaussian draws of the reference become one normal per output.
-#include "xb_internal.h"
+#include <cstdlib>
+
+#include "xb_mvm_common.cuh"
 
 namespace xb {
 
 namespace {
-
-// 2^m exactly (0 <= m < 1023) from the exponent field, not the fp64 exp2 routine
-__device__ __forceinline__ double pow2i(int m) {
-  return __longlong_as_double((long long)(1023 + m) << 52);
-}
-
-// --------------------------------------------------------------- prep
-// per-sample state for one MVM call: alpha (0 = zero input), norm of x~,
-// current BM exponent m, active flag for the current pass
-struct SampleState {
-  float alpha;
-  float norm;
-  int m;
-  int active;
-};
 
 constexpr int PREP_THREADS = 512;
 constexpr int PREP_VPT = 8; // values per thread kept in registers (n <= 4096)
@@ -223,26 +210,7 @@ __global__ void __launch_bounds__(256) mvm_simt_kernel(const float *__restrict__
 }
 
 // --------------------------------------------------------------- epilogue
-// Output noise: one Philox call per GROUP of 4 consecutive global outputs
-// (counter = group, sample sequence number, BM exponent, tag); output 4g + k
-// takes word k, i.e. two 16-bit Box-Muller normals (z0 -> sigma_w fold,
-// z1 -> sigma_out).  Keyed on the global output index, so row shards and the
-// split-phase backward draw exactly what the whole tile draws.
-__device__ __forceinline__ void out_noise_words(uint32_t g, uint64_t seq, int m, Key key,
-                                                uint32_t w[4]) {
-  uint32_t c0 = g, c1 = (uint32_t)seq, c2 = (uint32_t)(seq >> 32) | ((uint32_t)m << 24),
-           c3 = TAG_OUT_NOISE << 24;
-  philox10(c0, c1, c2, c3, key);
-  w[0] = c0;
-  w[1] = c1;
-  w[2] = c2;
-  w[3] = c3;
-}
-
-// groups of 4 global outputs covering [o0, o0 + M)
-inline int out_groups(int o0, int M) { return ((o0 + M - 1) >> 2) - (o0 >> 2) + 1; }
-
-// one thread = one group of 4 outputs of one sample
+// one thread = one group of 4 outputs of one sample (xb_mvm_common.cuh)
 __global__ void __launch_bounds__(256) epilogue_kernel(const float *__restrict__ acc, int lda,
                                                         int nsplit, size_t split_stride, int M,
                                                         int o0, float *__restrict__ Y, int ldy,
@@ -255,42 +223,17 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const float *__restrict__
   if (!first_pass && !s.active) return;
   const int g = (o0 >> 2) + blockIdx.x * blockDim.x + threadIdx.x;
   if (4 * g >= o0 + M) return;
-  const uint64_t seq = seq0 + (uint64_t)b;
-  uint32_t w[4] = {0u, 0u, 0u, 0u};
-  const bool noisy = !io.perfect && (io.sigma_w > 0.0 || io.sigma_out > 0.0);
-  if (noisy) out_noise_words((uint32_t)g, seq, s.m, key, w);
-  const double scale = s.alpha == 0.f ? 1.0 : (double)s.alpha * pow2i(s.m);
-  bool hit = false;
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int o = 4 * g + k - o0;
     if (o < 0 || o >= M) continue;
-    float a = acc[(size_t)b * lda + o];
-    for (int sp = 1; sp < nsplit; ++sp) a += acc[sp * split_stride + (size_t)b * lda + o];
-    if (io.perfect) {
-      Y[(size_t)b * ldy + o] = a;
-      continue;
-    }
-    float z0 = 0.f, z1 = 0.f;
-    if (noisy) box_muller16(w[k], z0, z1);
-    double v;
-    if (s.alpha == 0.f) { // io.cpp:107-115: zero input -> output noise only, no alpha
-      v = io.sigma_out > 0.0 ? io.sigma_out * (double)z1 : 0.0;
-    } else {
-      v = (double)a;
-      if (io.sigma_w > 0.0) v += io.sigma_w * (double)s.norm * (double)z0;
-      if (io.sigma_out > 0.0) v += io.sigma_out * (double)z1;
-      hit |= fabs(v) >= io.adc.bound;
-    }
-    Y[(size_t)b * ldy + o] = (float)(scale * quantize(v, io.adc));
+    a[k] = acc[(size_t)b * lda + o];
+    for (int sp = 1; sp < nsplit; ++sp) a[k] += acc[sp * split_stride + (size_t)b * lda + o];
   }
-  if (io.bm && s.alpha != 0.f && s.m < io.bm_max_iter) {
-    // one flag write per warp (a saturating sample saturates many outputs:
-    // per-thread atomics on the same word serialise)
-    const unsigned any = __ballot_sync(__activemask(), hit);
-    if (hit && (threadIdx.x & 31) == __ffs(any) - 1 && atomicExch(sat + b, 1) == 0)
-      atomicAdd(sat + B + pass_slot, 1);
-  }
+  const bool hit = epilogue_group4(a, g, o0, M, s, io, key, seq0 + (uint64_t)b,
+                                   Y + (size_t)b * ldy);
+  bm_flag(hit, s, io, sat, b, B, pass_slot);
 }
 
 // Row-shard backward, phase 1: the shard's column sums plus its share of the
@@ -387,6 +330,13 @@ void gemm(Tile &t, const MvmScratch &s, int M, int K, int ldt, int B, int first)
   XB_CUDA(cudaGetLastError());
 }
 
+// XB_MVM_UNFUSED=1 forces the split-K partials + epilogue kernel path: the
+// parity tests run both and require bit-identical outputs
+static bool unfused_requested() {
+  const char *e = getenv("XB_MVM_UNFUSED");
+  return e && e[0] == '1';
+}
+
 // one full noisy MVM in direction TRANS (forward: false)
 template <bool TRANS>
 void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io, Key key,
@@ -398,9 +348,16 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io, Key
   // otherwise (exact-fp32 parity mode, tiny batches)
   const bool x3 = t.cfg.mvm_precision == XB_MVM_TF32X3;
   const bool tc = (t.cfg.mvm_precision == XB_MVM_TF32 || x3) && B >= 16;
-  const int splits = tc ? tc_used_splits(K, tc_splits(M, K, x3)) : 1;
+  const int o0 = TRANS ? 0 : t.row0; // global index of output 0 (noise counters)
+  // the output stage runs inside the tcgen05 kernel (K-splits reduced over a
+  // thread-block cluster) unless the caller wants raw partial sums, the noise
+  // groups of 4 outputs do not align with the tile, or a cluster would exceed
+  // the portable 8 CTAs
+  // (both paths use the same K-splits, so they agree bit for bit)
+  const int splits = tc ? tc_used_splits(K, std::min(8, tc_splits(M, K, x3))) : 1;
+  const bool fused = tc && !skip_epilogue && (o0 & 3) == 0 && !unfused_requested();
   const int ldt = (K + 3) & ~3; // x~ rows padded to 16 bytes (TMA global stride)
-  MvmScratch s = carve(t, B, ldt, M, splits);
+  MvmScratch s = carve(t, B, ldt, M, fused ? 0 : splits);
   if (io.bm) XB_CUDA(cudaMemsetAsync(s.sat, 0, sizeof(int) * (B + 32), t.stream));
   const int passes = io.bm ? 1 + io.bm_max_iter : 1;
   for (int pass = 0; pass < passes; ++pass) {
@@ -410,8 +367,11 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io, Key
     count_launch();
     XB_CUDA(cudaGetLastError());
     int nsplit = 1;
-    if (tc) { // re-issue passes recompute the whole batch on the tensor cores (cheap)
-      tc_gemm(t, TRANS, x3, s.xt, ldt, B, s.acc, splits);
+    if (fused) { // re-issue passes recompute the whole batch on the tensor cores (cheap)
+      FusedOut fo{dOut, M, s.st, io, key, seq0, s.sat, first, B, pass, o0, 0};
+      tc_gemm(t, TRANS, x3, s.xt, ldt, B, nullptr, splits, &fo);
+    } else if (tc) {
+      tc_gemm(t, TRANS, x3, s.xt, ldt, B, s.acc, splits, nullptr);
       nsplit = splits;
     } else {
       gemm<TRANS>(t, s, M, K, ldt, B, first);
@@ -425,13 +385,13 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io, Key
       XB_CUDA(cudaGetLastError());
       return;
     }
-    const int o0 = TRANS ? 0 : t.row0;
-    dim3 eg((out_groups(o0, M) + 255) / 256, B);
-    epilogue_kernel<<<eg, 256, 0, t.stream>>>(s.acc, M, nsplit, (size_t)B * M, M,
-                                              TRANS ? 0 : t.row0, dOut, M, s.st, io, key, seq0,
-                                              s.sat, first, B, pass);
-    count_launch();
-    XB_CUDA(cudaGetLastError());
+    if (!fused) {
+      dim3 eg((out_groups(o0, M) + 255) / 256, B);
+      epilogue_kernel<<<eg, 256, 0, t.stream>>>(s.acc, M, nsplit, (size_t)B * M, M, o0, dOut, M,
+                                                s.st, io, key, seq0, s.sat, first, B, pass);
+      count_launch();
+      XB_CUDA(cudaGetLastError());
+    }
     if (io.bm && pass + 1 < passes) {
       // bound management: re-issue while some sample saturated.  The epilogue
       // counted them; the count crosses to the host (one 4-byte read and a

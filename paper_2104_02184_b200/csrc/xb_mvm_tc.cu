@@ -9,8 +9,17 @@
 // TMEM accumulator of BN fp32 columns; mbarriers chain TMA -> MMA -> smem
 // release (tcgen05.commit) and MMA -> epilogue.  The four warps then drain
 // TMEM with tcgen05.ld (warp w owns accumulator lanes 32w..32w+31 = output
-// rows) and store the fp32 partial sums; the converter/noise epilogue
-// (xb_mvm.cu) reduces the K-splits and applies sigma_w, sigma_out, ADC, alpha.
+// rows).
+//
+// Fused epilogue (FUSED): the K-splits of one M-tile form a thread-block
+// cluster.  Each CTA parks its partial tile in its own shared memory, and
+// after a cluster barrier CTA r reduces columns (samples) [r n/S, (r+1) n/S)
+// over the S partials through distributed shared memory (mapa +
+// ld.shared::cluster) and applies the output stage -- sigma_w fold, output
+// noise, ADC, alpha 2^m, bound-management flags (xb_mvm_common.cuh) --
+// writing Y directly.  No partial sums touch HBM and no epilogue kernel runs.
+// Unfused: the partial sums go to HBM for epilogue_kernel / the row-shard
+// split-phase backward.
 //
 // W is row-major [R][ld] fp32, x~ is [B][K] fp32 -- the kernel reads the same
 // bytes the SIMT path reads; the tensor core consumes them as TF32.
@@ -21,7 +30,7 @@
 #include <cstdlib>
 #include <mutex>
 
-#include "xb_internal.h"
+#include "xb_mvm_common.cuh"
 
 namespace xb {
 
@@ -46,7 +55,14 @@ template <bool X3, int NSUB> constexpr int tc_stages() {
 template <bool X3, int NSUB> constexpr int tc_smem() {
   return tc_stages<X3, NSUB>() * tc_stage_bytes<X3, NSUB>() + 1024 /*align*/ + 256 /*bars*/;
 }
-template <bool X3> constexpr int tc_threads() { return X3 ? 256 : 128; }
+// threads: 128 = producer warp, MMA warp, two more epilogue warps; 3xTF32
+// adds converter warps; the fused output stage wants more warps in flight
+#ifndef XB_TC_FUSED_THREADS
+#define XB_TC_FUSED_THREADS 512
+#endif
+template <bool X3, bool FUSED = false> constexpr int tc_threads() {
+  return FUSED ? XB_TC_FUSED_THREADS : (X3 ? 256 : 128);
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -132,6 +148,35 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
                  "=r"(r[30]), "=r"(r[31])                                                      \
                : "r"(taddr))
 
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_size() {
+  uint32_t n;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(n));
+  return n;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+               "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// address of the same shared-memory word in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t dsmem_map(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float4 dsmem_ld4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
+
+
 // split x into hi = x with the low 13 mantissa bits cleared (exactly a TF32
 // value, so the tensor core reads it unchanged whether it truncates or
 // rounds) and lo = x - hi (exact in fp32; TF32-rounded by the MMA)
@@ -154,11 +199,11 @@ __device__ __forceinline__ void split_tf32(float4 &v, float4 &lo) {
 //               the MMA thread issues hi*hi + hi*lo + lo*hi per K-step, which
 //               recovers ~fp32 accuracy of the products at 3x the tensor work.
 //               Warps 4-7 run the epilogue (TMEM lane quarter = warp % 4).
-template <bool A_MN, bool X3, int NSUB>
-__global__ void __launch_bounds__(tc_threads<X3>(), 1)
+template <bool A_MN, bool X3, int NSUB, bool FUSED>
+__global__ void __launch_bounds__(tc_threads<X3, FUSED>(), 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                    int M, int K, int B, int bn, int kblocks_per_split, float *__restrict__ part,
-                   int ldp, size_t split_stride) {
+                   int ldp, size_t split_stride, const __grid_constant__ FusedOut fo) {
   constexpr int STAGES = tc_stages<X3, NSUB>();
   constexpr int SB = tc_stage_bytes<X3, NSUB>();
   constexpr int AB = NSUB * TC_A_BYTES;          // A bytes per stage
@@ -179,7 +224,7 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1)
   const int split = blockIdx.y;
   const int kb0 = split * kblocks_per_split;
   const int nkb = min(kblocks_per_split, (K + TC_BK - 1) / TC_BK - kb0);
-  constexpr int CONV_THREADS = tc_threads<X3>() - 64;
+  constexpr int CONV_THREADS = tc_threads<X3, FUSED>() - 64;
   constexpr uint32_t TMEM_COLS = NSUB * TC_MAX_BN; // 256 or all 512 columns
 
   if (threadIdx.x == 0) {
@@ -281,29 +326,95 @@ __global__ void __launch_bounds__(tc_threads<X3>(), 1)
 
   // ---------------- epilogue: TMEM -> registers -> partial sums
   constexpr int EPI_W0 = X3 ? 4 : 0;
-  if (warp >= EPI_W0 && warp < EPI_W0 + 4) {
-    if (nkb > 0) {
+  const bool epi_warp = warp >= EPI_W0 && warp < EPI_W0 + 4;
+  if (epi_warp && nkb > 0) {
+    mbar_wait(done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
+  const int quarter = warp & 3;
+  if (!FUSED) {
+    if (epi_warp) {
+      float *dst = part + (size_t)split * split_stride;
+#pragma unroll
+      for (int sub = 0; sub < NSUB; ++sub) {
+        const int o = m0 + sub * TC_BM + quarter * 32 + lane;
+        for (int c0 = 0; c0 < bn; c0 += 32) {
+          uint32_t r[32];
+          XB_TMEM_LD32(tmem + ((uint32_t)(quarter * 32) << 16) +
+                           (uint32_t)(sub * TC_MAX_BN + c0),
+                       r);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (o < M) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+              const int b = c0 + c;
+              if (b < B) dst[(size_t)b * ldp + o] = nkb > 0 ? __uint_as_float(r[c]) : 0.f;
+            }
+          }
+        }
+      }
+    }
+  } else {
+    // partial tile of this CTA in its (now idle) pipeline memory, sample-major
+    // [bn][128 rows], then the cluster reduces and finishes it.  Every warp
+    // of the CTA works here (NW warps; TMEM lane quarter = warp % 4).
+    constexpr int NW = tc_threads<X3, FUSED>() / 32;
+    if (!epi_warp && nkb > 0) {
       mbar_wait(done, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
-    const int quarter = warp & 3;
-    float *dst = part + (size_t)split * split_stride;
-#pragma unroll
+    float *red = reinterpret_cast<float *>(smem);
+    const uint32_t red_s = smem_u32(red);
+    const uint32_t rank = cluster_rank(), ncta = cluster_size();
+    const int cols = (bn + (int)ncta - 1) / (int)ncta;
+    const int c_lo = (int)rank * cols, c_hi = min(bn, c_lo + cols);
+#pragma unroll 1
     for (int sub = 0; sub < NSUB; ++sub) {
-      const int o = m0 + sub * TC_BM + quarter * 32 + lane;
-      for (int c0 = 0; c0 < bn; c0 += 32) {
+      const int row = quarter * 32 + lane;
+      for (int c0 = 32 * (warp >> 2); c0 < bn; c0 += 32 * (NW / 4)) {
         uint32_t r[32];
         XB_TMEM_LD32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(sub * TC_MAX_BN + c0),
                      r);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (o < M) {
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const int b = c0 + c;
-            if (b < B) dst[(size_t)b * ldp + o] = nkb > 0 ? __uint_as_float(r[c]) : 0.f;
-          }
+        for (int c = 0; c < 32; ++c)
+          red[(c0 + c) * TC_BM + row] = nkb > 0 ? __uint_as_float(r[c]) : 0.f;
+      }
+      cluster_sync_all(); // every partial of this sub-tile is in place
+      {
+        // thread: group of 4 rows (grp) x every NW-th column of this CTA's range
+        const int grp = threadIdx.x & 31, cph = threadIdx.x >> 5;
+        const int row0 = m0 + sub * TC_BM; // local output index of row 0 of the sub-tile
+        for (int c = c_lo + cph; c < c_hi; c += NW) {
+          const int b = fo.n0 + c;
+          if (c >= B) break;
+          const SampleState sst = fo.st[b];
+          if (!fo.first_pass && !sst.active) continue;
+          const uint32_t off = red_s + (uint32_t)((c * TC_BM + 4 * grp) * 4);
+          float4 v[8];
+#pragma unroll
+          for (int r = 0; r < 8; ++r) // all remote loads in flight, then the sum
+            if (r < (int)ncta) v[r] = dsmem_ld4(dsmem_map(off, (uint32_t)r));
+          float4 acc4 = v[0];
+#pragma unroll
+          for (int r = 1; r < 8; ++r) // split order == rank order (as the epilogue kernel)
+            if (r < (int)ncta) {
+              acc4.x += v[r].x;
+              acc4.y += v[r].y;
+              acc4.z += v[r].z;
+              acc4.w += v[r].w;
+            }
+          if (row0 + 4 * grp >= M) continue;
+          const float a[4] = {acc4.x, acc4.y, acc4.z, acc4.w};
+          // global output index of this group: o0 + row0 + 4 grp (o0 % 4 == 0
+          // on the fused path, so groups align with the noise groups)
+          const int g = (fo.o0 + row0) / 4 + grp;
+          const bool hit = epilogue_group4(a, g, fo.o0, M, sst, fo.io, fo.key,
+                                           fo.seq0 + (uint64_t)b, fo.Y + (size_t)b * fo.ldy);
+          bm_flag(hit, sst, fo.io, fo.sat, b, fo.B, fo.pass_slot);
         }
       }
+      cluster_sync_all(); // the partials are read before the next sub-tile overwrites them
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -363,27 +474,60 @@ int tc_splits(int M, int K, bool x3) {
   return std::max(1, std::min(s, 16));
 }
 
-template <bool A_MN, bool X3, int NSUB>
+template <bool A_MN, bool X3, int NSUB, bool FUSED>
 static void launch_tc(dim3 grid, cudaStream_t st, const CUtensorMap &ma, const CUtensorMap &mb,
-                      int M, int K, int nb, int bn, int per, float *part, size_t split_stride) {
+                      int M, int K, int nb, int bn, int per, float *part, size_t split_stride,
+                      const FusedOut &fo) {
+  auto kern = tc_gemm_kernel<A_MN, X3, NSUB, FUSED>;
   static bool configured = false;
   if (!configured) {
-    XB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<A_MN, X3, NSUB>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+    XB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  tc_smem<X3, NSUB>()));
+    if (FUSED) XB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
     configured = true;
   }
-  tc_gemm_kernel<A_MN, X3, NSUB><<<grid, tc_threads<X3>(), tc_smem<X3, NSUB>(), st>>>(
-      ma, mb, M, K, nb, bn, per, part, M, split_stride);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(tc_threads<X3, FUSED>());
+  cfg.dynamicSmemBytes = tc_smem<X3, NSUB>();
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  if (FUSED) { // the K-splits of one M-tile form one cluster
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = grid.y;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  XB_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, M, K, nb, bn, per, part, M, split_stride, fo));
   count_launch();
   XB_CUDA(cudaGetLastError());
 }
 
-// contraction on tcgen05: part[s][b][o] (split stride B x M).
+template <bool FUSED>
+static void launch_variant(bool transposed, bool x3, int nsub, dim3 grid, cudaStream_t st,
+                           const CUtensorMap &ma, const CUtensorMap &mb, int M, int K, int nb,
+                           int bn, int per, float *p, size_t ss, const FusedOut &fo) {
+  if (x3) {
+    transposed ? launch_tc<true, true, 1, FUSED>(grid, st, ma, mb, M, K, nb, bn, per, p, ss, fo)
+               : launch_tc<false, true, 1, FUSED>(grid, st, ma, mb, M, K, nb, bn, per, p, ss, fo);
+  } else if (nsub == 2) {
+    transposed ? launch_tc<true, false, 2, FUSED>(grid, st, ma, mb, M, K, nb, bn, per, p, ss, fo)
+               : launch_tc<false, false, 2, FUSED>(grid, st, ma, mb, M, K, nb, bn, per, p, ss, fo);
+  } else {
+    transposed ? launch_tc<true, false, 1, FUSED>(grid, st, ma, mb, M, K, nb, bn, per, p, ss, fo)
+               : launch_tc<false, false, 1, FUSED>(grid, st, ma, mb, M, K, nb, bn, per, p, ss, fo);
+  }
+}
+
+// contraction on tcgen05.
 //   forward : o = row of W, K = columns of W   (A = W, K-major)
 //   backward: o = column of W, K = rows of W   (A = W^T, MN-major)
+// fo == nullptr: partial sums part[s][b][o] (split stride B x M) for the
+// epilogue kernel; otherwise the cluster-fused output stage writes fo->Y.
 void tc_gemm(Tile &t, bool transposed, bool x3, const float *Xt, int ldt, int B, float *part,
-             int splits) {
+             int splits, const FusedOut *fo) {
   const int M = transposed ? t.C : t.R, K = transposed ? t.R : t.C;
   const int nsub = tc_nsub(M, x3);
   const int kbs = (K + TC_BK - 1) / TC_BK;
@@ -399,18 +543,15 @@ void tc_gemm(Tile &t, bool transposed, bool x3, const float *Xt, int ldt, int B,
                    : make_map(t.W, t.R, t.C, t.ld, TC_BM * nsub);
     const CUtensorMap mb = make_map(Xt + (size_t)n0 * ldt, nb, K, ldt, bn);
     const dim3 grid((M + TC_BM * nsub - 1) / (TC_BM * nsub), used);
-    // partial sums of this N slab land at part + n0 rows, split stride B x M
-    float *p = part + (size_t)n0 * M;
-    const size_t ss = (size_t)B * M;
-    if (x3) {
-      transposed ? launch_tc<true, true, 1>(grid, t.stream, ma, mb, M, K, nb, bn, per, p, ss)
-                 : launch_tc<false, true, 1>(grid, t.stream, ma, mb, M, K, nb, bn, per, p, ss);
-    } else if (nsub == 2) {
-      transposed ? launch_tc<true, false, 2>(grid, t.stream, ma, mb, M, K, nb, bn, per, p, ss)
-                 : launch_tc<false, false, 2>(grid, t.stream, ma, mb, M, K, nb, bn, per, p, ss);
+    if (fo) {
+      FusedOut f = *fo;
+      f.n0 = n0;
+      launch_variant<true>(transposed, x3, nsub, grid, t.stream, ma, mb, M, K, nb, bn, per,
+                           nullptr, 0, f);
     } else {
-      transposed ? launch_tc<true, false, 1>(grid, t.stream, ma, mb, M, K, nb, bn, per, p, ss)
-                 : launch_tc<false, false, 1>(grid, t.stream, ma, mb, M, K, nb, bn, per, p, ss);
+      // partial sums of this N slab land at part + n0 rows, split stride B x M
+      launch_variant<false>(transposed, x3, nsub, grid, t.stream, ma, mb, M, K, nb, bn, per,
+                            part + (size_t)n0 * M, (size_t)B * M, FusedOut{});
     }
   }
 }

@@ -330,3 +330,27 @@ def test_tcgen05_forward_odd_widths():
     ref = X.astype(np.float64) @ W.T.astype(np.float64)
     scale = np.linalg.norm(X, axis=1)[:, None] * np.linalg.norm(W, axis=1)[None, :]
     assert (np.abs(Y - ref) / scale).max() < 2e-3
+
+
+@pytest.mark.parametrize("prec", [xb.MVM_TF32, xb.MVM_TF32X3])
+@pytest.mark.parametrize("shape,B,bm", [((4096, 1024), 256, True), ((520, 300), 37, False),
+                                        ((8320, 200), 40, True), ((300, 4096), 300, False)])
+def test_fused_epilogue_matches_unfused(monkeypatch, prec, shape, B, bm):
+    """The cluster-fused output stage (K-splits reduced through distributed
+    shared memory inside the tcgen05 kernel) and the split-K partials +
+    epilogue kernel path produce bit-identical outputs, noise and BM included."""
+    d_out, d_in = shape
+    io = xb.default_io()
+    io.bound_management = xb.BM_ITERATIVE if bm else xb.BM_NONE
+    io.sigma_w = 0.02
+    W = np.random.default_rng(21).uniform(-0.3, 0.3, shape).astype(np.float32)
+    X = np.random.default_rng(22).uniform(-1, 1, (B, d_in)).astype(np.float32)
+    D = np.random.default_rng(23).uniform(-1, 1, (B, d_out)).astype(np.float32)
+    out = []
+    for unfused in ("0", "1"):
+        monkeypatch.setenv("XB_MVM_UNFUSED", unfused)
+        t = xb.AnalogTile(d_out, d_in, cfg_io(io, io, prec), 31)
+        t.set_weights(W)
+        out.append((t.forward(X), t.backward(D), t.forward(X)))
+    for a, b in zip(out[0], out[1]):
+        assert np.array_equal(a, b)
