@@ -173,6 +173,15 @@ def _batch(x, n: int, what: str):
     return a, single
 
 
+def _out(out, shape) -> np.ndarray:
+    if out is None:
+        return np.empty(shape, dtype=np.float32)
+    if (not isinstance(out, np.ndarray) or out.dtype != np.float32 or
+            not out.flags["C_CONTIGUOUS"] or out.size != shape[0] * shape[1]):
+        raise Error(f"out: need a C-contiguous float32 array of {shape[0]}x{shape[1]}")
+    return out
+
+
 def _lr_array(lr, B: int):
     if lr is None:
         return None
@@ -253,11 +262,13 @@ class AnalogTile:
         _check(_lib.xb_tile_set_device(self._h, *[None if a is None else _ptr(a) for a in arrs]))
 
     # -- MVM (tile.hpp:82-85, :95)
-    def forward(self, x) -> np.ndarray:
+    def forward(self, x, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """tile.hpp:80; ``out`` (float32 C-contiguous [B][d_out], e.g. in pinned
+        memory) receives the result instead of a fresh array."""
         X, single = _batch(x, self._d_in, "forward")
-        Y = np.empty((X.shape[0], self.rows), dtype=np.float32)
+        Y = _out(out, (X.shape[0], self.rows))
         _check(_lib.xb_tile_forward(self._h, _ptr(X), X.shape[0], _ptr(Y)))
-        return Y[0] if single else Y
+        return Y[0] if single and out is None else Y
 
     def forward_with_io(self, x, io: IOParams) -> np.ndarray:
         X, single = _batch(x, self._d_in, "forward")

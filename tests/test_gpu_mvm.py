@@ -354,3 +354,19 @@ def test_fused_epilogue_matches_unfused(monkeypatch, prec, shape, B, bm):
         out.append((t.forward(X), t.backward(D), t.forward(X)))
     for a, b in zip(out[0], out[1]):
         assert np.array_equal(a, b)
+
+
+def test_forward_into_caller_buffer():
+    """forward(x, out=Y) writes into the caller's (e.g. pinned) float32 buffer
+    and returns it; shape/dtype mismatches raise."""
+    t = xb.AnalogTile(64, 32, cfg_io(xb.perfect_io(), xb.perfect_io(), xb.MVM_FP32), 3)
+    W = np.random.default_rng(1).uniform(-0.5, 0.5, (64, 32)).astype(np.float32)
+    t.set_weights(W)
+    X = np.random.default_rng(2).uniform(-1, 1, (5, 32)).astype(np.float32)
+    Y = np.empty((5, 64), np.float32)
+    assert t.forward(X, out=Y) is Y
+    assert np.array_equal(Y, t.forward(X))
+    with pytest.raises(xb.Error, match="out:"):
+        t.forward(X, out=np.empty((5, 63), np.float32))
+    with pytest.raises(xb.Error, match="out:"):
+        t.forward(X, out=np.empty((5, 64), np.float64))
