@@ -452,13 +452,11 @@ template <int LAW> struct WCell {
 constexpr int PULSE_QW = 32;             // stream words per lane
 constexpr int PULSE_CAP = PULSE_QW * 32; // pulses per lane per segment
 
-// Launch shape (B200, NS update, round 1): 32 resident warps (64 registers,
-// no spills) either way.  Persistent laws run ONE 1024-thread CTA per SM:
-// 7.48 ms vs 7.65 ms with two 512-thread CTAs and 8.0 ms with four 256-thread
-// CTAs.  ExpStep (per-tile grid, see pulse_persist) keeps two 512-thread CTAs
-// (13.8 ms vs 16.3 ms with 1024-thread CTAs: a CTA waits on its slowest warp).
-template <int LAW> constexpr int pulse_warps();
-template <int LAW> constexpr int pulse_minb() { return 32 / pulse_warps<LAW>(); }
+// Launch shape (B200, round 1): persistent warps, ONE 1024-thread CTA per SM
+// (64 registers, no spills).  NS update: 7.48 ms vs 7.65 ms with two
+// 512-thread CTAs and 8.0 ms with four 256-thread CTAs; ExpStep (cfg3):
+// 13.5 ms vs 13.8 ms for a per-tile grid of 512-thread CTAs.
+constexpr int PULSE_WARPS = 32;
 // samples per vector block of the pre-pass (4: one uint4 of x and of d words;
 // measured 6 % slower than 8)
 #ifndef XB_PULSE_PB
@@ -470,18 +468,13 @@ template <int LAW> constexpr int pulse_minb() { return 32 / pulse_warps<LAW>(); 
 #ifndef XB_PULSE_PERSIST
 #define XB_PULSE_PERSIST 1
 #endif
-// ExpStep (register-heavier, 2 CTAs either way) measured 4 % faster per-tile
-template <int LAW> constexpr bool pulse_persist() {
-  return XB_PULSE_PERSIST && LAW != XB_EXP_STEP;
-}
-template <int LAW> constexpr int pulse_warps() { return pulse_persist<LAW>() ? 32 : 16; }
+template <int LAW> constexpr bool pulse_persist() { return XB_PULSE_PERSIST != 0; }
 
 template <int LAW, bool NOISE>
-__global__ void __launch_bounds__(pulse_warps<LAW>() * 32, pulse_minb<LAW>()) pulse_kernel(
+__global__ void __launch_bounds__(PULSE_WARPS * 32, 1) pulse_kernel(
     float *__restrict__ W, const float4 *__restrict__ P, int ld, int R, int C,
     const uint32_t *__restrict__ xw, const uint32_t *__restrict__ dw, int ldb, int B, int row0,
     LawArgs la, RoundKeys rk, uint32_t call, uint32_t one, uint32_t flip) {
-  constexpr int PULSE_WARPS = pulse_warps<LAW>();
   extern __shared__ uint32_t qsm[]; // [PULSE_WARPS][PULSE_QW][32]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t *q = qsm + warp * (PULSE_QW * 32) + lane;
@@ -633,7 +626,6 @@ __global__ void __launch_bounds__(pulse_warps<LAW>() * 32, pulse_minb<LAW>()) pu
 template <int LAW, bool NOISE>
 static void pulse_dispatch(Tile &t, const uint32_t *xw, const uint32_t *dw, int ldb, int B,
                            LawArgs la, uint32_t call, bool flip) {
-  constexpr int PULSE_WARPS = pulse_warps<LAW>();
   const int smem = PULSE_WARPS * PULSE_QW * 32 * (int)sizeof(uint32_t);
   static bool configured = false;
   if (!configured) {
