@@ -46,10 +46,15 @@ __global__ void __launch_bounds__(PREP_THREADS) prep_kernel(const float *__restr
                                                              IoDev io, Key key, uint64_t seq0,
                                                              int first_pass,
                                                              const float *__restrict__ amax_in,
-                                                             int *__restrict__ sat) {
-  const int b = blockIdx.x;
+                                                             int *__restrict__ sat,
+                                                             const int *__restrict__ map) {
+  // map != nullptr: a compacted bound-management re-issue -- block i prepares
+  // sample map[i] into x~ row i (compact_kernel already re-armed the flags)
+  const int b = map ? map[blockIdx.x] : blockIdx.x;
   SampleState s = st[b];
-  if (!first_pass) { // bound management: re-issue the samples that saturated
+  if (map) {
+    s.m += 1;
+  } else if (!first_pass) { // bound management: re-issue the samples that saturated
     const int again = s.active && sat[b];
     __syncthreads(); // every thread has read the flag before it is re-armed
     if (threadIdx.x == 0) sat[b] = 0;
@@ -63,7 +68,7 @@ __global__ void __launch_bounds__(PREP_THREADS) prep_kernel(const float *__restr
     s.m += 1;
   }
   const float *x = X + (size_t)b * ldx;
-  float *xt = Xt + (size_t)b * ldt;
+  float *xt = Xt + (size_t)blockIdx.x * ldt;
   __shared__ float red[33];
   // the sample stays in registers between the max and the conversion when it fits
   const bool in_regs = n <= PREP_THREADS * PREP_VPT;
@@ -134,6 +139,32 @@ __global__ void __launch_bounds__(PREP_THREADS) prep_kernel(const float *__restr
     s.norm = sqrtf(tot);
     st[b] = s;
   }
+}
+
+// Bound-management bookkeeping between passes: samples that saturated in the
+// last pass (and are still active) are listed in map[0..n) -- in any order:
+// each sample's column of the contraction is independent of its position --
+// the others are retired; all flags are re-armed for the next pass.
+__global__ void __launch_bounds__(256) compact_kernel(int *__restrict__ sat,
+                                                      SampleState *__restrict__ st, int B,
+                                                      int *__restrict__ map,
+                                                      int *__restrict__ count) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  bool again = false;
+  if (b < B) {
+    SampleState s = st[b];
+    again = s.active && sat[b];
+    sat[b] = 0;
+    if (!again && s.active) {
+      s.active = 0;
+      st[b] = s;
+    }
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, again);
+  int base = 0;
+  if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(count, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (again) map[base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = b;
 }
 
 // --------------------------------------------------------------- SIMT GEMM
@@ -217,8 +248,10 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const float *__restrict__
                                                         SampleState *__restrict__ st, IoDev io,
                                                         Key key, uint64_t seq0,
                                                         int *__restrict__ sat, int first_pass,
-                                                        int B, int pass_slot) {
-  const int b = blockIdx.y;
+                                                        int B, int pass_slot,
+                                                        const int *__restrict__ map) {
+  // acc row blockIdx.y holds sample b (compacted re-issue: b = map[row])
+  const int row = blockIdx.y, b = map ? map[row] : row;
   const SampleState s = st[b];
   if (!first_pass && !s.active) return;
   const int g = (o0 >> 2) + blockIdx.x * blockDim.x + threadIdx.x;
@@ -228,8 +261,8 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const float *__restrict__
   for (int k = 0; k < 4; ++k) {
     const int o = 4 * g + k - o0;
     if (o < 0 || o >= M) continue;
-    a[k] = acc[(size_t)b * lda + o];
-    for (int sp = 1; sp < nsplit; ++sp) a[k] += acc[sp * split_stride + (size_t)b * lda + o];
+    a[k] = acc[(size_t)row * lda + o];
+    for (int sp = 1; sp < nsplit; ++sp) a[k] += acc[sp * split_stride + (size_t)row * lda + o];
   }
   const bool hit = epilogue_group4(a, g, o0, M, s, io, key, seq0 + (uint64_t)b,
                                    Y + (size_t)b * ldy);
@@ -303,21 +336,24 @@ struct MvmScratch {
   float *xt;
   float *acc;
   SampleState *st;
-  int *sat;
+  int *sat; // [B] flags, then one saturation counter per BM pass, then the compaction counters
+  int *map; // [B] compacted re-issue list
 };
 
 MvmScratch carve(Tile &t, int B, int K, int M, int nsplit) {
   const size_t xt_b = (size_t)B * K * sizeof(float);
   const size_t acc_b = (size_t)nsplit * B * M * sizeof(float);
   const size_t st_b = (size_t)B * sizeof(SampleState);
-  const size_t sat_b = (size_t)(B + 32) * sizeof(int); // flags + one counter per BM pass
+  const size_t sat_b = (size_t)(B + 64) * sizeof(int); // flags + per-pass counters
+  const size_t map_b = (size_t)B * sizeof(int);
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  char *p = (char *)t.s_io.get(al(xt_b) + al(acc_b) + al(st_b) + al(sat_b));
+  char *p = (char *)t.s_io.get(al(xt_b) + al(acc_b) + al(st_b) + al(sat_b) + al(map_b));
   MvmScratch s;
   s.xt = (float *)p;
   s.acc = (float *)(p + al(xt_b));
   s.st = (SampleState *)(p + al(xt_b) + al(acc_b));
   s.sat = (int *)(p + al(xt_b) + al(acc_b) + al(st_b));
+  s.map = (int *)(p + al(xt_b) + al(acc_b) + al(st_b) + al(sat_b));
   return s;
 }
 
@@ -358,22 +394,24 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io, Key
   const bool fused = tc && !skip_epilogue && (o0 & 3) == 0 && !unfused_requested();
   const int ldt = (K + 3) & ~3; // x~ rows padded to 16 bytes (TMA global stride)
   MvmScratch s = carve(t, B, ldt, M, fused ? 0 : splits);
-  if (io.bm) XB_CUDA(cudaMemsetAsync(s.sat, 0, sizeof(int) * (B + 32), t.stream));
+  if (io.bm) XB_CUDA(cudaMemsetAsync(s.sat, 0, sizeof(int) * (B + 64), t.stream));
   const int passes = io.bm ? 1 + io.bm_max_iter : 1;
+  int nrun = B;             // samples (rows of x~) in this pass
+  const int *map = nullptr; // tensor-core re-issues: the compacted list of saturated samples
   for (int pass = 0; pass < passes; ++pass) {
     const int first = pass == 0;
-    prep_kernel<<<B, PREP_THREADS, 0, t.stream>>>(dIn, K, K, s.xt, ldt, s.st, io, key, seq0,
-                                                   first, amax_in, s.sat);
+    prep_kernel<<<nrun, PREP_THREADS, 0, t.stream>>>(dIn, K, K, s.xt, ldt, s.st, io, key, seq0,
+                                                      first, amax_in, s.sat, map);
     count_launch();
     XB_CUDA(cudaGetLastError());
     int nsplit = 1;
-    if (fused) { // re-issue passes recompute the whole batch on the tensor cores (cheap)
-      FusedOut fo{dOut, M, s.st, io, key, seq0, s.sat, first, B, pass, o0, 0};
-      tc_gemm(t, TRANS, x3, s.xt, ldt, B, nullptr, splits, &fo);
+    if (fused) {
+      FusedOut fo{dOut, M, s.st, io, key, seq0, s.sat, first, B, pass, o0, 0, map};
+      tc_gemm(t, TRANS, x3, s.xt, ldt, nrun, nullptr, splits, &fo);
     } else if (tc) {
-      tc_gemm(t, TRANS, x3, s.xt, ldt, B, s.acc, splits, nullptr);
+      tc_gemm(t, TRANS, x3, s.xt, ldt, nrun, s.acc, splits, nullptr);
       nsplit = splits;
-    } else {
+    } else { // SIMT: re-issues run over the whole batch, skipping inactive tiles
       gemm<TRANS>(t, s, M, K, ldt, B, first);
     }
     if (skip_epilogue) { // row shard: partial sums + this shard's weight-noise fold
@@ -386,21 +424,33 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io, Key
       return;
     }
     if (!fused) {
-      dim3 eg((out_groups(o0, M) + 255) / 256, B);
-      epilogue_kernel<<<eg, 256, 0, t.stream>>>(s.acc, M, nsplit, (size_t)B * M, M, o0, dOut, M,
-                                                s.st, io, key, seq0, s.sat, first, B, pass);
+      dim3 eg((out_groups(o0, M) + 255) / 256, nrun);
+      epilogue_kernel<<<eg, 256, 0, t.stream>>>(s.acc, M, nsplit, (size_t)nrun * M, M, o0, dOut,
+                                                M, s.st, io, key, seq0, s.sat, first, B, pass,
+                                                map);
       count_launch();
       XB_CUDA(cudaGetLastError());
     }
     if (io.bm && pass + 1 < passes) {
       // bound management: re-issue while some sample saturated.  The epilogue
       // counted them; the count crosses to the host (one 4-byte read and a
-      // stream sync per pass with BM on) and the next prep re-arms the flags.
+      // stream sync per pass with BM on).  On the tensor cores only the
+      // saturated samples are recomputed: compact_kernel lists them, retires
+      // the rest and re-arms the flags (the SIMT path's prep does the latter).
       if (!t.bm_count) XB_CUDA(cudaMallocHost(&t.bm_count, sizeof(int)));
       XB_CUDA(cudaMemcpyAsync(t.bm_count, s.sat + B + pass, sizeof(int),
                               cudaMemcpyDeviceToHost, t.stream));
       XB_CUDA(cudaStreamSynchronize(t.stream));
-      if (*t.bm_count == 0) break;
+      const int nsat = *t.bm_count;
+      if (nsat == 0) break;
+      if (tc) {
+        compact_kernel<<<(B + 255) / 256, 256, 0, t.stream>>>(s.sat, s.st, B, s.map,
+                                                              s.sat + B + 32 + pass);
+        count_launch();
+        XB_CUDA(cudaGetLastError());
+        map = s.map;
+        nrun = nsat;
+      }
     }
   }
 }

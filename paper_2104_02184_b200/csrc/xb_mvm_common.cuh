@@ -101,7 +101,8 @@ struct FusedOut {
   int *sat;            // BM flags [B] + per-pass counters
   int first_pass, B, pass_slot;
   int o0;              // global index of output 0 (row shards: row0; backward: 0)
-  int n0;              // first sample of this N slab
+  int n0;              // first x~ row of this N slab
+  const int *map;      // x~ row -> sample (compacted BM re-issue), or nullptr
 };
 
 // tcgen05 contraction (xb_mvm_tc.cu).  fo == nullptr: split-K partial sums
