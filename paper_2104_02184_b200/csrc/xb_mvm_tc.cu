@@ -386,8 +386,8 @@ __global__ void __launch_bounds__(tc_threads<X3, FUSED>(), 1)
         const int grp = threadIdx.x & 31, cph = threadIdx.x >> 5;
         const int row0 = m0 + sub * TC_BM; // local output index of row 0 of the sub-tile
         for (int c = c_lo + cph; c < c_hi; c += NW) {
-          const int b = fo.n0 + c;
           if (c >= B) break;
+          const int b = fo.map ? fo.map[fo.n0 + c] : fo.n0 + c;
           const SampleState sst = fo.st[b];
           if (!fo.first_pass && !sst.active) continue;
           const uint32_t off = red_s + (uint32_t)((c * TC_BM + 4 * grp) * 4);
