@@ -190,6 +190,71 @@ __device__ __forceinline__ void split_tf32(float4 &v, float4 &lo) {
   }
 }
 
+// Cluster-fused output stage.  Every warp of the CTA: drain this CTA's
+// accumulator (NSUB sub-tiles of 128 TMEM lanes x bn columns) into its idle
+// pipeline memory as [bn][128] fp32, cluster barrier, then reduce this CTA's
+// share of the columns (samples) over the S split partials -- split r lives
+// in cluster CTA peer0 + r * pstride -- through distributed shared memory
+// (all S loads in flight, summed in split order like the epilogue kernel) and
+// run the output stage (xb_mvm_common.cuh) straight into Y.
+template <int NW, int NSUB>
+__device__ __forceinline__ void fused_output_stage(const FusedOut &fo, uint32_t tmem,
+                                                   uint8_t *smem, int nkb, int m0, int M, int B,
+                                                   int bn, uint32_t my_split, uint32_t nsplit,
+                                                   uint32_t peer0, uint32_t pstride) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, quarter = warp & 3;
+  float *red = reinterpret_cast<float *>(smem);
+  const uint32_t red_s = smem_u32(red);
+  const int cols = (bn + (int)nsplit - 1) / (int)nsplit;
+  const int c_lo = (int)my_split * cols, c_hi = min(bn, c_lo + cols);
+#pragma unroll 1
+  for (int sub = 0; sub < NSUB; ++sub) {
+    const int row = quarter * 32 + lane;
+    for (int c0 = 32 * (warp >> 2); c0 < bn; c0 += 32 * (NW / 4)) {
+      uint32_t r[32];
+      XB_TMEM_LD32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(sub * TC_MAX_BN + c0), r);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int c = 0; c < 32; ++c) red[(c0 + c) * TC_BM + row] = nkb > 0 ? __uint_as_float(r[c]) : 0.f;
+    }
+    cluster_sync_all(); // every partial of this sub-tile is in place
+    {
+      // thread: group of 4 rows (grp) x every NW-th column of this CTA's range
+      const int grp = threadIdx.x & 31, cph = threadIdx.x >> 5;
+      const int row0 = m0 + sub * TC_BM; // local output index of row 0 of the sub-tile
+      for (int c = c_lo + cph; c < c_hi; c += NW) {
+        if (c >= B) break;
+        const int b = fo.map ? fo.map[fo.n0 + c] : fo.n0 + c;
+        const SampleState sst = fo.st[b];
+        if (!fo.first_pass && !sst.active) continue;
+        const uint32_t off = red_s + (uint32_t)((c * TC_BM + 4 * grp) * 4);
+        float4 v[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) // all remote loads in flight, then the sum
+          if (r < (int)nsplit) v[r] = dsmem_ld4(dsmem_map(off, peer0 + (uint32_t)r * pstride));
+        float4 acc4 = v[0];
+#pragma unroll
+        for (int r = 1; r < 8; ++r) // split order (as the epilogue kernel)
+          if (r < (int)nsplit) {
+            acc4.x += v[r].x;
+            acc4.y += v[r].y;
+            acc4.z += v[r].z;
+            acc4.w += v[r].w;
+          }
+        if (row0 + 4 * grp >= M) continue;
+        const float a[4] = {acc4.x, acc4.y, acc4.z, acc4.w};
+        // global output index of this group: o0 + row0 + 4 grp (o0 % 4 == 0 on
+        // the fused path, so groups align with the noise groups)
+        const int g = (fo.o0 + row0) / 4 + grp;
+        const bool hit = epilogue_group4(a, g, fo.o0, M, sst, fo.io, fo.key,
+                                         fo.seq0 + (uint64_t)b, fo.Y + (size_t)b * fo.ldy);
+        bm_flag(hit, sst, fo.io, fo.sat, b, fo.B, fo.pass_slot);
+      }
+    }
+    cluster_sync_all(); // the partials are read before the next sub-tile overwrites them
+  }
+}
+
 // A_MN = false: A = W tile [NSUB*128 rows][32 K] (forward, K-major; one TMA box)
 // A_MN = true : A = W^T tile, i.e. W[32 K-rows][NSUB*128 columns] (backward,
 //               MN-major): 4*NSUB 32x32 TMA boxes (128B/32B-atom swizzle) per
@@ -355,67 +420,14 @@ __global__ void __launch_bounds__(tc_threads<X3, FUSED>(), 1)
       }
     }
   } else {
-    // partial tile of this CTA in its (now idle) pipeline memory, sample-major
-    // [bn][128 rows], then the cluster reduces and finishes it.  Every warp
-    // of the CTA works here (NW warps; TMEM lane quarter = warp % 4).
-    constexpr int NW = tc_threads<X3, FUSED>() / 32;
     if (!epi_warp && nkb > 0) {
       mbar_wait(done, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
-    float *red = reinterpret_cast<float *>(smem);
-    const uint32_t red_s = smem_u32(red);
-    const uint32_t rank = cluster_rank(), ncta = cluster_size();
-    const int cols = (bn + (int)ncta - 1) / (int)ncta;
-    const int c_lo = (int)rank * cols, c_hi = min(bn, c_lo + cols);
-#pragma unroll 1
-    for (int sub = 0; sub < NSUB; ++sub) {
-      const int row = quarter * 32 + lane;
-      for (int c0 = 32 * (warp >> 2); c0 < bn; c0 += 32 * (NW / 4)) {
-        uint32_t r[32];
-        XB_TMEM_LD32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(sub * TC_MAX_BN + c0),
-                     r);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int c = 0; c < 32; ++c)
-          red[(c0 + c) * TC_BM + row] = nkb > 0 ? __uint_as_float(r[c]) : 0.f;
-      }
-      cluster_sync_all(); // every partial of this sub-tile is in place
-      {
-        // thread: group of 4 rows (grp) x every NW-th column of this CTA's range
-        const int grp = threadIdx.x & 31, cph = threadIdx.x >> 5;
-        const int row0 = m0 + sub * TC_BM; // local output index of row 0 of the sub-tile
-        for (int c = c_lo + cph; c < c_hi; c += NW) {
-          if (c >= B) break;
-          const int b = fo.map ? fo.map[fo.n0 + c] : fo.n0 + c;
-          const SampleState sst = fo.st[b];
-          if (!fo.first_pass && !sst.active) continue;
-          const uint32_t off = red_s + (uint32_t)((c * TC_BM + 4 * grp) * 4);
-          float4 v[8];
-#pragma unroll
-          for (int r = 0; r < 8; ++r) // all remote loads in flight, then the sum
-            if (r < (int)ncta) v[r] = dsmem_ld4(dsmem_map(off, (uint32_t)r));
-          float4 acc4 = v[0];
-#pragma unroll
-          for (int r = 1; r < 8; ++r) // split order == rank order (as the epilogue kernel)
-            if (r < (int)ncta) {
-              acc4.x += v[r].x;
-              acc4.y += v[r].y;
-              acc4.z += v[r].z;
-              acc4.w += v[r].w;
-            }
-          if (row0 + 4 * grp >= M) continue;
-          const float a[4] = {acc4.x, acc4.y, acc4.z, acc4.w};
-          // global output index of this group: o0 + row0 + 4 grp (o0 % 4 == 0
-          // on the fused path, so groups align with the noise groups)
-          const int g = (fo.o0 + row0) / 4 + grp;
-          const bool hit = epilogue_group4(a, g, fo.o0, M, sst, fo.io, fo.key,
-                                           fo.seq0 + (uint64_t)b, fo.Y + (size_t)b * fo.ldy);
-          bm_flag(hit, sst, fo.io, fo.sat, b, fo.B, fo.pass_slot);
-        }
-      }
-      cluster_sync_all(); // the partials are read before the next sub-tile overwrites them
-    }
+    // split peers: cluster (1, S), CTA rank == split index
+    fused_output_stage<tc_threads<X3, FUSED>() / 32, NSUB>(fo, tmem, smem, nkb, m0, M, B, bn,
+                                                            cluster_rank(), cluster_size(), 0u,
+                                                            1u);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
