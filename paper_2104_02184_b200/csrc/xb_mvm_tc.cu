@@ -436,6 +436,190 @@ __global__ void __launch_bounds__(tc_threads<X3, FUSED>(), 1)
                  "r"(TMEM_COLS));
 }
 
+// ============================================================ CTA pairs
+// 2-SM variant (cta_group::2).  A cluster (2, S): the two CTAs of a pair own
+// consecutive 128-row M-tiles of one K-split; each streams its own A tile and
+// HALF of the x~ tile (bn/2 samples) -- signalling the leader's full barrier
+// through the 2-SM TMA form -- and the leader issues M=256 UMMAs that read A
+// and B from both CTAs' shared memory, each CTA accumulating its 128 rows in
+// its own TMEM.  Per stage a CTA holds 16 + 16 KB instead of 16 + 32 KB: six
+// stages in flight instead of four, and half the x~ re-reads from L2.
+constexpr int TP_STAGES = 6;
+constexpr int TP_STAGE = TC_A_BYTES + TC_B_BYTES / 2; // 32 KB
+constexpr int TP_SMEM = TP_STAGES * TP_STAGE + 1024 + 256;
+
+__device__ __forceinline__ uint32_t cluster_ctaid_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctaid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_ctaid_y() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctaid.y;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_nctaid_y() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctaid.y;" : "=r"(r));
+  return r;
+}
+// arrive (+ expected bytes) on an mbarrier of another CTA of the cluster
+__device__ __forceinline__ void mbar_expect_tx_cluster(uint32_t cbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(
+                   cbar),
+               "r"(bytes)
+               : "memory");
+}
+// TMA into this CTA's shared memory, completion counted on the pair leader's
+// mbarrier (cbar: shared::cluster address)
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap *map,
+                                                 uint32_t cbar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(cbar)
+      : "memory");
+}
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t a, uint64_t b,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+// arrive on the same mbarrier offset in both CTAs of the pair (mask: cluster ranks)
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::"
+               "cluster.b64 [%0], %1;" ::"r"(bar),
+               "h"(mask)
+               : "memory");
+}
+
+template <bool A_MN, bool FUSED>
+__global__ void __launch_bounds__(tc_threads<false, FUSED>(), 1)
+    tc_pair_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                   int M, int K, int B, int bn, int kblocks_per_split, float *__restrict__ part,
+                   int ldp, size_t split_stride, const __grid_constant__ FusedOut fo) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t *bars = (uint64_t *)(smem + TP_STAGES * TP_STAGE);
+  uint32_t *tmem_slot = (uint32_t *)(bars + 2 * TP_STAGES + 1);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + TP_STAGES),
+                 done = smem_u32(bars + 2 * TP_STAGES);
+  auto stage_a = [&](int s) { return smem + s * TP_STAGE; };
+  auto stage_b = [&](int s) { return smem + s * TP_STAGE + TC_A_BYTES; };
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t xr = cluster_ctaid_x();      // 0 = pair leader (issues the MMAs), 1 = peer
+  const uint32_t my_rank = cluster_rank();
+  const uint32_t lead_rank = my_rank - xr;    // ranks: x + 2 y
+  const uint16_t pair_mask = (uint16_t)(3u << lead_rank);
+  const int m0 = blockIdx.x * TC_BM;
+  const int split = blockIdx.y;
+  const int kb0 = split * kblocks_per_split;
+  const int nkb = min(kblocks_per_split, (K + TC_BK - 1) / TC_BK - kb0);
+  const int half = bn / 2;
+
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_b)) : "memory");
+    for (int s = 0; s < TP_STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 2); // both producers of the pair arrive on the leader's
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) { // TMEM, allocated by the pair together
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TC_MAX_BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all(); // barriers of both CTAs initialised, TMEM allocated
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t bytes_per_cta = TC_A_BYTES + (uint32_t)half * TC_BK * 4;
+  const uint32_t lead_full0 = dsmem_map(full0, lead_rank);
+
+  if (warp == 0 && lane == 0 && nkb > 0) {
+    // ---------------- TMA producer (both CTAs)
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % TP_STAGES;
+      const uint32_t ph = (uint32_t)(kb / TP_STAGES) & 1u;
+      mbar_wait(empty0 + 8 * s, ph ^ 1u);
+      mbar_expect_tx_cluster(lead_full0 + 8 * s, bytes_per_cta);
+      const int kk = (kb0 + kb) * TC_BK;
+      if (A_MN) {
+#pragma unroll
+        for (int a = 0; a < TC_BM / 32; ++a)
+          tma_load_2d_pair(smem_u32(stage_a(s) + a * 4096), &tm_a, lead_full0 + 8 * s,
+                           m0 + 32 * a, kk);
+      } else {
+        tma_load_2d_pair(smem_u32(stage_a(s)), &tm_a, lead_full0 + 8 * s, kk, m0);
+      }
+      tma_load_2d_pair(smem_u32(stage_b(s)), &tm_b, lead_full0 + 8 * s, kk, (int)xr * half);
+    }
+  } else if (warp == 1 && lane == 0 && xr == 0 && nkb > 0) {
+    // ---------------- MMA issuer: the pair leader, M = 256 across both CTAs
+    const uint32_t idesc =
+        (idesc_tf32(bn, A_MN) & ~(0x1Fu << 24)) | ((uint32_t)(2 * TC_BM >> 4) << 24);
+    const uint32_t a_lbo = A_MN ? 4096u : 16u, a_sbo = A_MN ? 512u : 1024u;
+    const uint32_t a_layout = A_MN ? 1u : 2u;
+    const uint32_t a_step = A_MN ? 64u : 2u;
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % TP_STAGES;
+      const uint32_t ph = (uint32_t)(kb / TP_STAGES) & 1u;
+      mbar_wait(full0 + 8 * s, ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint64_t da = umma_desc(smem_u32(stage_a(s)), a_lbo, a_sbo, a_layout);
+      const uint64_t db = umma_desc(smem_u32(stage_b(s)), 16u, 1024u, 2u);
+#pragma unroll
+      for (int k = 0; k < TC_BK / 8; ++k)
+        mma_tf32_pair(tmem, da + a_step * k, db + 2u * k, idesc, (kb | k) != 0);
+      mma_commit_pair(empty0 + 8 * s, pair_mask); // both CTAs may refill stage s
+    }
+    mma_commit_pair(done, pair_mask);
+  }
+  __syncwarp();
+
+  // ---------------- epilogue: each CTA drains its own 128 accumulator rows
+  if (nkb > 0) {
+    mbar_wait(done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
+  if (!FUSED) {
+    if (warp < 4) {
+      const int o = m0 + warp * 32 + lane;
+      float *dst = part + (size_t)split * split_stride;
+      for (int c0 = 0; c0 < bn; c0 += 32) {
+        uint32_t r[32];
+        XB_TMEM_LD32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, r);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (o < M) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const int b = c0 + c;
+            if (b < B) dst[(size_t)b * ldp + o] = nkb > 0 ? __uint_as_float(r[c]) : 0.f;
+          }
+        }
+      }
+    }
+  } else {
+    // split peers: cluster (2, S), rank = x + 2 y
+    fused_output_stage<tc_threads<false, FUSED>() / 32, 1>(fo, tmem, smem, nkb, m0, M, B, bn,
+                                                            cluster_ctaid_y(), cluster_nctaid_y(),
+                                                            xr, 2u);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all(); // both CTAs are done with the pair's TMEM
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TC_MAX_BN));
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -533,6 +717,42 @@ static void launch_variant(bool transposed, bool x3, int nsub, dim3 grid, cudaSt
   }
 }
 
+template <bool A_MN, bool FUSED>
+static void launch_pair(dim3 grid, cudaStream_t st, const CUtensorMap &ma, const CUtensorMap &mb,
+                        int M, int K, int nb, int bn, int per, float *part, size_t split_stride,
+                        const FusedOut &fo) {
+  auto kern = tc_pair_kernel<A_MN, FUSED>;
+  static bool configured = false;
+  if (!configured) {
+    XB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TP_SMEM));
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(tc_threads<false, FUSED>());
+  cfg.dynamicSmemBytes = TP_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension; // (CTA pair) x (K-splits when fused)
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = FUSED ? grid.y : 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  XB_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, M, K, nb, bn, per, part, M, split_stride, fo));
+  count_launch();
+  XB_CUDA(cudaGetLastError());
+}
+
+// Opt-in (XB_TC_PAIR=1): correct (tests/test_gpu_mvm.py runs it) but measured
+// slower on B200 for the bench shapes -- 4096^2 x 256 forward 109 us fused /
+// 79 us unfused vs 62 / 65 us for the single-CTA kernel; tensor pipe 22 % --
+// so the single-CTA kernel stays the default.
+static bool pair_enabled() {
+  const char *e = getenv("XB_TC_PAIR");
+  return e && e[0] == '1';
+}
+
 // contraction on tcgen05.
 //   forward : o = row of W, K = columns of W   (A = W, K-major)
 //   backward: o = column of W, K = rows of W   (A = W^T, MN-major)
@@ -554,6 +774,27 @@ void tc_gemm(Tile &t, bool transposed, bool x3, const float *Xt, int ldt, int B,
         transposed ? make_map(t.W, t.R, t.C, t.ld, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)
                    : make_map(t.W, t.R, t.C, t.ld, TC_BM * nsub);
     const CUtensorMap mb = make_map(Xt + (size_t)n0 * ldt, nb, K, ldt, bn);
+    const int mtiles = (M + TC_BM - 1) / TC_BM;
+    const bool pair = !x3 && nsub == 1 && mtiles >= 2 && (!fo || used <= 4) && pair_enabled();
+    if (pair) { // 2-SM UMMA: each CTA streams its A tile and half of the x~ tile
+      const CUtensorMap mbh = make_map(Xt + (size_t)n0 * ldt, nb, K, ldt, bn / 2);
+      const dim3 grid2((mtiles + 1) / 2 * 2, used);
+      if (fo) {
+        FusedOut f = *fo;
+        f.n0 = n0;
+        transposed ? launch_pair<true, true>(grid2, t.stream, ma, mbh, M, K, nb, bn, per, nullptr,
+                                             0, f)
+                   : launch_pair<false, true>(grid2, t.stream, ma, mbh, M, K, nb, bn, per,
+                                              nullptr, 0, f);
+      } else {
+        float *p = part + (size_t)n0 * M;
+        transposed ? launch_pair<true, false>(grid2, t.stream, ma, mbh, M, K, nb, bn, per, p,
+                                              (size_t)B * M, FusedOut{})
+                   : launch_pair<false, false>(grid2, t.stream, ma, mbh, M, K, nb, bn, per, p,
+                                               (size_t)B * M, FusedOut{});
+      }
+      continue;
+    }
     const dim3 grid((M + TC_BM * nsub - 1) / (TC_BM * nsub), used);
     if (fo) {
       FusedOut f = *fo;

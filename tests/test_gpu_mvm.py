@@ -370,3 +370,32 @@ def test_forward_into_caller_buffer():
         t.forward(X, out=np.empty((5, 63), np.float32))
     with pytest.raises(xb.Error, match="out:"):
         t.forward(X, out=np.empty((5, 64), np.float64))
+
+
+@pytest.mark.parametrize("shape,B", [((4096, 1024), 256), ((640, 300), 40), ((300, 4096), 64)])
+def test_cta_pair_contraction(monkeypatch, shape, B):
+    """The opt-in 2-SM (cta_group::2) contraction: TF32-accurate against fp64
+    and bit-identical between its fused and unfused output stages."""
+    monkeypatch.setenv("XB_TC_PAIR", "1")
+    d_out, d_in = shape
+    io = xb.default_io()
+    io.bound_management = xb.BM_ITERATIVE
+    W = np.random.default_rng(31).uniform(-0.3, 0.3, shape).astype(np.float32)
+    X = np.random.default_rng(32).uniform(-1, 1, (B, d_in)).astype(np.float32)
+    D = np.random.default_rng(33).uniform(-1, 1, (B, d_out)).astype(np.float32)
+    out = []
+    for unfused in ("0", "1"):
+        monkeypatch.setenv("XB_MVM_UNFUSED", unfused)
+        t = xb.AnalogTile(d_out, d_in, cfg_io(io, io, xb.MVM_TF32), 9)
+        t.set_weights(W)
+        out.append((t.forward(X), t.backward(D)))
+    for a, b in zip(out[0], out[1]):
+        assert np.array_equal(a, b)
+    pio = xb.perfect_io()
+    t = xb.AnalogTile(d_out, d_in, cfg_io(pio, pio, xb.MVM_TF32), 9)
+    t.set_weights(W)
+    for got, ref, scale in ((t.forward(X), X.astype(np.float64) @ W.T.astype(np.float64),
+                             np.linalg.norm(X, axis=1)[:, None] * np.linalg.norm(W, axis=1)[None, :]),
+                            (t.backward(D), D.astype(np.float64) @ W.astype(np.float64),
+                             np.linalg.norm(D, axis=1)[:, None] * np.linalg.norm(W, axis=0)[None, :])):
+        assert (np.abs(got - ref) / scale).max() < 2e-3
