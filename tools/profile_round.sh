@@ -20,7 +20,7 @@ ncu --set full --import-source on --clock-control none -k regex:tc_gemm -s 2 -c 
     -o $OUT/tc_tf32 python tools/profile_pulse.py --precision 1 --iters 2 --backward \
     > $OUT/ncu_tc.log 2>&1
 ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
-    -k "regex:tc_gemm_kernel<1" -s 1 -c 1 -f -o $OUT/tc_tf32_bwd \
+    -k "regex:tc_gemm_kernel<.bool.1" -s 1 -c 1 -f -o $OUT/tc_tf32_bwd \
     python tools/profile_pulse.py --precision 1 --iters 2 --backward > $OUT/ncu_tcb.log 2>&1
 python tools/profile_pulse.py --precision 2 --iters 2 > /dev/null
 ncu --set full --import-source on --clock-control none -k regex:tc_gemm -s 1 -c 1 -f \
