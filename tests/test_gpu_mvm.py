@@ -334,7 +334,8 @@ def test_tcgen05_forward_odd_widths():
 
 @pytest.mark.parametrize("prec", [xb.MVM_TF32, xb.MVM_TF32X3])
 @pytest.mark.parametrize("shape,B,bm", [((4096, 1024), 256, True), ((520, 300), 37, False),
-                                        ((8320, 200), 40, True), ((300, 4096), 300, False)])
+                                        ((8320, 200), 40, True), ((300, 4096), 300, False),
+                                        ((512, 256), 300, True)])
 def test_fused_epilogue_matches_unfused(monkeypatch, prec, shape, B, bm):
     """The cluster-fused output stage (K-splits reduced through distributed
     shared memory inside the tcgen05 kernel) and the split-K partials +
