@@ -191,31 +191,58 @@ def run_ours(args):
 
     # ---------- e2e through the public host-buffer API (pinned host inputs)
     e2e = None
-    if rank == 0:
-        Xh = [x.cpu().pin_memory().numpy() for x in Xs[:max(2, min(args.steps, 4))]]
-        Dh = [d.cpu().pin_memory().numpy() for d in Ds[:len(Xh)]]
-        e2e_tile, _ = make_tile(xb, 0, 1) if world == 1 else (tile, None)
-        if world == 1:
-            e2e_tile.set_weights(w0.cpu().numpy())
-        # warm
+    n_e2e = max(2, min(args.steps, 4))
+    if world == 1:
+        # AnalogTile.forward / update with host arrays: H2D, finiteness check,
+        # kernels and the D2H of y inside each call
+        Xh = [x.cpu().pin_memory().numpy() for x in Xs[:n_e2e]]
+        Dh = [d.cpu().pin_memory().numpy() for d in Ds[:n_e2e]]
+        e2e_tile, _ = make_tile(xb, 0, 1)
+        e2e_tile.set_weights(w0.cpu().numpy())
         # the result lands in pinned host memory (DMA at full PCIe rate)
         yh = torch.empty(BATCH, N_ROWS, dtype=torch.float32).pin_memory().numpy()
-        e2e_tile.forward(Xh[0], out=yh)
-        if world == 1:
-            e2e_tile.update(Xh[0], Dh[0], LR)
+        e2e_tile.forward(Xh[0], out=yh)  # warm
+        e2e_tile.update(Xh[0], Dh[0], LR)
         t0 = time.perf_counter()
-        n_e2e = len(Xh)
         for k in range(n_e2e):
             e2e_tile.forward(Xh[k], out=yh)
-            if world == 1:
-                e2e_tile.update(Xh[k], Dh[k], LR)
+            e2e_tile.update(Xh[k], Dh[k], LR)
         el = time.perf_counter() - t0
         _ = float(yh[0, 0])
-        if world == 1:
-            e2e = {"value": N_ROWS * N_COLS * BATCH * n_e2e / el, "unit": UNIT,
-                   "h2d_bytes_per_step": int(BATCH * N_COLS * 4 * 2 + BATCH * N_ROWS * 4),
-                   "d2h_bytes_per_step": int(BATCH * N_ROWS * 4),
-                   "steps": n_e2e, "api": "AnalogTile.forward(X host) + AnalogTile.update(X, D host)"}
+        e2e = {"value": N_ROWS * N_COLS * BATCH * n_e2e / el, "unit": UNIT,
+               "h2d_bytes_per_step": int(BATCH * N_COLS * 4 * 2 + BATCH * N_ROWS * 4),
+               "d2h_bytes_per_step": int(BATCH * N_ROWS * 4),
+               "steps": n_e2e, "api": "AnalogTile.forward(X host) + AnalogTile.update(X, D host)"}
+    else:
+        # RowShardedTile (the multi-GPU API) fed from pinned host buffers: each
+        # rank copies x and its rows of d in, runs the sharded forward + update
+        # (NCCL max|d| all-reduce) and reads its rows of y back; max over ranks
+        Xh = [x.cpu().pin_memory() for x in Xs[:n_e2e]]
+        Dh = [d.cpu().pin_memory() for d in Ds[:n_e2e]]
+        yh = torch.empty(BATCH, N_ROWS, dtype=torch.float32).pin_memory()
+        Xd = torch.empty(BATCH, N_COLS, device=dev)
+        Dd = torch.empty(BATCH, N_ROWS, device=dev)
+
+        def e2e_step(k):
+            Xd.copy_(Xh[k], non_blocking=True)
+            Dd.copy_(Dh[k], non_blocking=True)
+            sharded.forward(Xd, Y)
+            sharded.update(Xd, Dd, LR)
+            yh.copy_(Y, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        e2e_step(0)  # warm
+        dist.barrier()
+        t0 = time.perf_counter()
+        for k in range(n_e2e):
+            e2e_step(k)
+        el_t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        dist.all_reduce(el_t, op=dist.ReduceOp.MAX)
+        el = float(el_t.item())
+        e2e = {"value": N_ROWS * world * N_COLS * BATCH * n_e2e / el, "unit": UNIT,
+               "h2d_bytes_per_step": int(world * (BATCH * N_COLS * 4 + BATCH * N_ROWS * 4)),
+               "d2h_bytes_per_step": int(world * BATCH * N_ROWS * 4),
+               "steps": n_e2e, "api": "RowShardedTile.forward + update from pinned host buffers "
+                                      "(per-rank H2D of x and local d, D2H of local y)"}
 
     if rank == 0:
         pk, pk_kind = peaks()
