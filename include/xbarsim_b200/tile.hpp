@@ -46,6 +46,7 @@ enum class PulseType { stochastic = XB_PULSE_STOCHASTIC,
                        deterministic_implicit = XB_PULSE_DETERMINISTIC };
 enum class BoundManagement { none = XB_BM_NONE, iterative = XB_BM_ITERATIVE };
 enum class MvmPrecision { fp32 = XB_MVM_FP32, tf32 = XB_MVM_TF32, tf32x3 = XB_MVM_TF32X3 };
+enum class WeightPrecision { automatic = XB_W_AUTO, fp32 = XB_W_FP32, fp32x2 = XB_W_FP32X2 };
 
 // proj/include/xbarsim/device.hpp:24-39
 struct DeviceParams {
@@ -119,6 +120,7 @@ struct TileSettings {
   UpdateParams update;
   TemporalParams temporal;
   MvmPrecision mvm_precision = MvmPrecision::fp32;
+  WeightPrecision weight_precision = WeightPrecision::automatic;
 };
 
 // proj/include/xbarsim/compound.hpp:76-91
@@ -283,6 +285,7 @@ inline xb_tile_config to_c(const TileSettings &s) {
   c.update = to_c(s.update);
   c.temporal = to_c(s.temporal);
   c.mvm_precision = static_cast<int32_t>(s.mvm_precision);
+  c.weight_precision = static_cast<int32_t>(s.weight_precision);
   return c;
 }
 inline xb_inference_model to_c(const InferenceNoiseModel &m) {

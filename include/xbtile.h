@@ -62,6 +62,12 @@ enum { XB_PULSE_STOCHASTIC = 0, XB_PULSE_DETERMINISTIC = 1 };
 /* additive: MVM arithmetic. FP32 = exact fp32 FMA (SIMT); TF32 = one tcgen05
  * kind::tf32 pass; TF32X3 = split-precision 3xTF32 (fp32-level accuracy). */
 enum { XB_MVM_FP32 = 0, XB_MVM_TF32 = 1, XB_MVM_TF32X3 = 2 };
+/* additive: weight storage.  FP32 = one fp32 per cell; FP32X2 = fp32 plus an
+ * fp32 compensation term, pulses added error-free (two-sum), so long runs of
+ * tiny steps do not accumulate fp32 rounding (the reference stores fp64);
+ * AUTO = FP32X2 when dw_min < 2^-12 max(|w_max|, |w_min|), i.e. a pulse is
+ * under ~2048 fp32 ulps of the largest weight (e.g. the "ideal" preset). */
+enum { XB_W_AUTO = 0, XB_W_FP32 = 1, XB_W_FP32X2 = 2 };
 
 /* proj/include/xbarsim/device.hpp:24-39 (same fields and defaults) */
 typedef struct xb_device_params {
@@ -97,6 +103,8 @@ typedef struct xb_tile_config {
   xb_update_params update;
   int32_t mvm_precision; /* XB_MVM_*; default XB_MVM_FP32 */
   xb_temporal_params temporal;
+  int32_t weight_precision; /* XB_W_*; default XB_W_AUTO */
+  int32_t _pad;
 } xb_tile_config;
 
 /* Row shard of a larger logical tile: this handle owns global rows

@@ -8,7 +8,8 @@ is no CPU fallback.
 """
 from ._abi import (BM_ITERATIVE, BM_NONE, CONSTANT_STEP, EXP_STEP, LINEAR_STEP, MVM_FP32,
                    MVM_TF32, MVM_TF32X3, NM_ABS_MAX, NM_NONE, PULSE_DETERMINISTIC,
-                   PULSE_STOCHASTIC, SOFT_BOUNDS, UC_ALL_TOGETHER, UC_ROUND_ROBIN, DeviceParams,
+                   PULSE_STOCHASTIC, SOFT_BOUNDS, UC_ALL_TOGETHER, UC_ROUND_ROBIN, W_AUTO,
+                   W_FP32, W_FP32X2, DeviceParams,
                    InferenceModel, IOParams, TemporalParams, TileConfig, TransferConfig,
                    UnitCellConfig, UpdateParams)
 from .tile import (AnalogTile, Error, InferenceNoiseModel, TileSettings, TransferSettings,
@@ -23,4 +24,5 @@ __all__ = [
     "SOFT_BOUNDS", "EXP_STEP", "NM_NONE", "NM_ABS_MAX", "BM_NONE", "BM_ITERATIVE",
     "PULSE_STOCHASTIC", "PULSE_DETERMINISTIC", "MVM_FP32", "MVM_TF32", "MVM_TF32X3",
     "UnitCellTile", "UnitCellSettings", "UnitCellConfig", "UC_ROUND_ROBIN", "UC_ALL_TOGETHER",
+    "W_AUTO", "W_FP32", "W_FP32X2",
 ]

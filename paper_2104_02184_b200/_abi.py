@@ -18,6 +18,7 @@ NM_NONE, NM_ABS_MAX = 0, 1
 BM_NONE, BM_ITERATIVE = 0, 1
 PULSE_STOCHASTIC, PULSE_DETERMINISTIC = 0, 1
 MVM_FP32, MVM_TF32, MVM_TF32X3 = 0, 1, 2
+W_AUTO, W_FP32, W_FP32X2 = 0, 1, 2
 
 _d = C.c_double
 _i = C.c_int32
@@ -51,9 +52,10 @@ class TemporalParams(C.Structure):
 
 
 class TileConfig(C.Structure):
-    """proj/include/xbarsim/tile.hpp:38-44 (TileSettings) + mvm_precision."""
+    """proj/include/xbarsim/tile.hpp:38-44 (TileSettings) + mvm_precision, weight_precision."""
     _fields_ = [("device", DeviceParams), ("forward_io", IOParams), ("backward_io", IOParams),
-                ("update", UpdateParams), ("mvm_precision", _i), ("temporal", TemporalParams)]
+                ("update", UpdateParams), ("mvm_precision", _i), ("temporal", TemporalParams),
+                ("weight_precision", _i), ("_pad2", _i)]
 
 
 class Shard(C.Structure):

@@ -202,11 +202,33 @@ static void tile_alloc(Tile &t) {
   XB_CUDA(cudaMalloc(&t.P, std::max<size_t>(n, 1) * sizeof(float4)));
   XB_CUDA(cudaMemsetAsync(t.W, 0, n * sizeof(float), t.stream));
   XB_CUDA(cudaMemsetAsync(t.P, 0, n * sizeof(float4), t.stream));
+  if (t.comp) {
+    XB_CUDA(cudaMalloc(&t.Wlo, std::max<size_t>(n, 1) * sizeof(float)));
+    XB_CUDA(cudaMemsetAsync(t.Wlo, 0, n * sizeof(float), t.stream));
+  }
+}
+
+// weight writers other than the pulse kernels (set_weights/clip, temporal
+// steps, program, drift) act on the fp32 weight and drop the compensation
+static void wlo_reset(Tile &t) {
+  if (t.comp && t.Wlo)
+    XB_CUDA(cudaMemsetAsync(t.Wlo, 0, (size_t)t.R * t.ld * sizeof(float), t.stream));
+}
+
+// comp mode: explicit FP32X2, or AUTO when a pulse is under ~2048 fp32 ulps
+// of the largest weight the device can hold
+static bool want_comp(const xb_tile_config &c) {
+  if (c.weight_precision == XB_W_FP32X2) return true;
+  if (c.weight_precision == XB_W_FP32) return false;
+  const double wb = std::max(std::fabs(c.device.w_max), std::fabs(c.device.w_min)) *
+                    (1.0 + 3.0 * std::max(c.device.w_max_dtod, c.device.w_min_dtod));
+  return c.device.dw_min < std::ldexp(wb, -12);
 }
 
 static void tile_free(Tile &t) {
   clear_timing(t);
   cudaFree(t.W);
+  cudaFree(t.Wlo);
   cudaFree(t.P);
   cudaFree(t.xi);
   cudaFree(t.w0);
@@ -535,6 +557,8 @@ int xb_tile_create(const xb_tile_config *cfg, int d_out, int d_in, uint64_t seed
     if (cfg->mvm_precision != XB_MVM_FP32 && cfg->mvm_precision != XB_MVM_TF32 &&
         cfg->mvm_precision != XB_MVM_TF32X3)
       raise("mvm_precision: unknown mode");
+    if (cfg->weight_precision < XB_W_AUTO || cfg->weight_precision > XB_W_FP32X2)
+      raise("weight_precision: unknown mode");
     int r0 = 0, r1 = d_out;
     if (shard) {
       if (shard->d_out_total != d_out) raise("shard.d_out_total: must equal d_out");
@@ -551,6 +575,7 @@ int xb_tile_create(const xb_tile_config *cfg, int d_out, int d_in, uint64_t seed
     t.row0 = r0;
     t.R_total = d_out;
     t.ld = (int)ld_of(d_in);
+    t.comp = want_comp(*cfg);
     XB_CUDA(cudaStreamCreateWithFlags(&t.stream, cudaStreamNonBlocking));
     t.own_stream = true;
     tile_init_keys(t, seed);
@@ -597,12 +622,16 @@ int xb_tile_clone(const xb_tile *src, xb_tile **out) { // tile.hpp:91 (deep copy
     t.temporal_calls = s.temporal_calls;
     t.prog_t0 = s.prog_t0;
     tile_init_keys(t, s.seed);
+    t.comp = s.comp;
     XB_CUDA(cudaStreamCreateWithFlags(&t.stream, cudaStreamNonBlocking));
     t.own_stream = true;
     try {
       tile_alloc(t);
       const size_t n = (size_t)t.R * t.ld;
       XB_CUDA(cudaMemcpyAsync(t.W, s.W, n * sizeof(float), cudaMemcpyDeviceToDevice, t.stream));
+      if (t.comp)
+        XB_CUDA(cudaMemcpyAsync(t.Wlo, s.Wlo, n * sizeof(float), cudaMemcpyDeviceToDevice,
+                                t.stream));
       XB_CUDA(cudaMemcpyAsync(t.P, s.P, n * sizeof(float4), cudaMemcpyDeviceToDevice, t.stream));
       if (s.xi) {
         XB_CUDA(cudaMalloc(&t.xi, 3 * n * sizeof(float)));
@@ -686,6 +715,7 @@ int xb_tile_set_weights(xb_tile *h, const float *w) { // tile.cpp:103-119
     XB_CUDA(cudaMemcpy2DAsync(t.W, t.ld * sizeof(float), w, t.C * sizeof(float),
                               t.C * sizeof(float), t.R, cudaMemcpyHostToDevice, t.stream));
     launch_clip(t);
+    wlo_reset(t);
     sync(t);
   });
 }
@@ -719,6 +749,7 @@ int xb_tile_set_device(xb_tile *h, const float *dw_up, const float *dw_down, con
     }
     XB_CUDA(cudaMemcpy(t.P, p.data(), n * sizeof(float4), cudaMemcpyHostToDevice));
     launch_clip(t);
+    wlo_reset(t);
     sync(t);
   });
 }
@@ -910,6 +941,7 @@ int xb_tile_temporal_step(xb_tile *h, const xb_temporal_params *tp) { // tile.cp
     if (!temporal_any(*tp)) return;
     ensure_xi(t);
     launch_temporal(t, *tp, t.temporal_calls++);
+    wlo_reset(t);
     sync(t);
   });
 }
@@ -948,6 +980,7 @@ int xb_tile_program(xb_tile *h, const float *target, const xb_inference_model *m
     XB_CUDA(cudaMemcpyAsync(dT, target, sizeof(float) * (size_t)t.R * t.C, cudaMemcpyHostToDevice,
                             t.stream));
     launch_program(t, dT, *m, key_of(seed));
+    wlo_reset(t);
     t.prog_t0 = m->t0;
     sync(t);
   });
@@ -959,6 +992,7 @@ int xb_tile_drift_to(xb_tile *h, double time_s) {
     if (!t.w0) raise("drift_to: tile has not been programmed");
     if (time_s < t.prog_t0) raise("drift_to: t < t0");
     launch_drift(t, time_s / t.prog_t0);
+    wlo_reset(t);
     sync(t);
   });
 }

@@ -61,6 +61,8 @@ struct Tile {
   uint32_t upd_calls = 0, temporal_calls = 0;
 
   float *W = nullptr;      // [R][ld] fp32 weights
+  float *Wlo = nullptr;    // [R][ld] compensation terms (comp mode: weight = W + Wlo)
+  bool comp = false;       // compensated weights (xb_tile_config.weight_precision)
   float4 *P = nullptr;     // [R][ld] {dw_up, dw_down, w_max, w_min}
   float *xi = nullptr;     // [3][R][ld] temporal d2d draws (lazy)
   float *w0 = nullptr;     // programmed state (lazy)

@@ -226,65 +226,11 @@ void launch_trains(const Tile &t, const float *X, const float *D, int B, const f
 }
 
 // ============================================================== device laws
-// proj/src/device.cpp:48-77 in fp32.  Everything that depends only on (cell,
-// direction) is folded once per sample into Dir, so one pulse is
-//   t  = law factor (1 for ConstantStep; 1 - w/b; 1 -+ slope w; exp(...))
-//   su = sgn dw (1 + std z)                        (c2c noise, :72-74)
-//   w  = clamp(w + su t, w_min, w_max)             (:75-76)
-// i.e. three FMAs and two min/max per pulse (plus one MUFU.EX2 for ExpStep).
+// proj/src/device.cpp:48-77; see WCell below for the per-pulse arithmetic.
 struct LawArgs {
   float slope, gamma, std;
   float k2; // -2 ln2 std^2: the c2c radius factor of factor8_rk
 };
-
-struct Cell {
-  float dwu, dwd, wmax, wmin;
-  float k_up, k_dn; // SoftBounds: 1/w_max, 1/w_min; ExpStep: gamma log2(e) / range
-};
-
-struct Dir {
-  float sdw;   // sgn * dw_min_{up,down}
-  float sdws;  // sgn * dw * dw_min_std
-  float a, b2; // law factor t = a w + 1 (SB, Linear) or exp2(a w + b2) (Exp)
-};
-
-template <int LAW>
-__device__ __forceinline__ Cell make_cell(float4 p, const LawArgs &la) {
-  Cell c;
-  c.dwu = p.x;
-  c.dwd = p.y;
-  c.wmax = p.z;
-  c.wmin = p.w;
-  c.k_up = 0.f;
-  c.k_dn = 0.f;
-  if (LAW == XB_SOFT_BOUNDS) {
-    c.k_up = 1.0f / p.z;
-    c.k_dn = 1.0f / p.w;
-  } else if (LAW == XB_EXP_STEP) {
-    c.k_up = la.gamma / (p.z - p.w) * 1.4426950408889634f;
-  }
-  return c;
-}
-
-template <int LAW>
-__device__ __forceinline__ Dir make_dir(const Cell &c, bool up, const LawArgs &la) {
-  Dir d;
-  const float dw = up ? c.dwu : c.dwd;
-  d.sdw = up ? dw : -dw;
-  d.sdws = d.sdw * la.std;
-  d.a = 0.f;
-  d.b2 = 0.f;
-  if (LAW == XB_SOFT_BOUNDS) {
-    d.a = up ? -c.k_up : -c.k_dn; // 1 - w / w_max  |  1 - w / w_min
-  } else if (LAW == XB_LINEAR_STEP) {
-    d.a = up ? -la.slope : la.slope; // 1 - slope w  |  1 + slope w
-  } else if (LAW == XB_EXP_STEP) {
-    // up: exp(-g (w - w_min)) ; down: exp(-g (w_max - w)), g = gamma / range (log2 units)
-    d.a = up ? -c.k_up : c.k_up;
-    d.b2 = up ? c.k_up * c.wmin : -c.k_up * c.wmax;
-  }
-  return d;
-}
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -292,18 +238,6 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-template <int LAW, bool NOISE>
-__device__ __forceinline__ float pulse(float w, const Cell &c, const Dir &d, float z) {
-  const float su = NOISE ? fmaf(d.sdws, z, d.sdw) : d.sdw;
-  if (LAW == XB_CONSTANT_STEP) {
-    w += su;
-  } else if (LAW == XB_EXP_STEP) {
-    w = fmaf(su, ex2_approx(fmaf(d.a, w, d.b2)), w);
-  } else {
-    w = fmaf(su, fmaf(d.a, w, 1.0f), w);
-  }
-  return fminf(fmaxf(w, c.wmin), c.wmax);
-}
 
 // ---- c2c noise: Philox4x32-10 with the 10 round keys precomputed on the host
 // (kernel parameters, i.e. constant-bank operands of the LOP3s) and a
@@ -429,7 +363,37 @@ template <int LAW> struct WCell {
     }
     return fminf(fmaxf(fmaf(f, h, w), wmin), wmax);
   }
+  // the same pulse on a compensated weight hi + lo: the law reads hi, the step
+  // d = f h is added with an error-free two-sum, so the per-pulse rounding of
+  // an fp32 add is carried in lo instead of accumulating (the reference keeps
+  // fp64 weights; at dw_min = 1e-6 a step is only ~17 fp32 ulps of w = 0.5)
+  __device__ __forceinline__ void step2(float &hi, float &lo, float f, bool up) const {
+    float h;
+    if (LAW == XB_CONSTANT_STEP) {
+      h = up ? cu : cd;
+    } else if (LAW == XB_EXP_STEP) {
+      const float e = up ? fmaf(-g, hi, bu) : fmaf(g, hi, bd);
+      h = (up ? cu : cd) * ex2_approx(e);
+    } else {
+      const float hu = fmaf(bu, hi, cu), hd = fmaf(bd, hi, cd);
+      h = up ? hu : hd;
+    }
+    const float d = __fmul_rn(f, h);
+    const float s = __fadd_rn(hi, d), bp = __fsub_rn(s, hi);
+    const float e = __fadd_rn(__fsub_rn(hi, __fsub_rn(s, bp)), __fsub_rn(d, bp));
+    const float c = fminf(fmaxf(s, wmin), wmax);
+    lo = (c == s) ? __fadd_rn(lo, e) : 0.f;
+    hi = c;
+  }
 };
+
+// hi + lo -> (fl(hi + lo), exact residual): the stored hi is the best fp32
+// weight (what the MVM and get_weights read), lo keeps the rest
+__device__ __forceinline__ void renorm2(float &hi, float &lo) {
+  const float s = __fadd_rn(hi, lo);
+  lo = __fsub_rn(lo, __fsub_rn(s, hi));
+  hi = s;
+}
 
 // ============================================================== K5: pulse
 // One warp = one row i of the tile and 32 consecutive columns (one cell per
@@ -470,9 +434,10 @@ constexpr int PULSE_WARPS = 32;
 #endif
 template <int LAW> constexpr bool pulse_persist() { return XB_PULSE_PERSIST != 0; }
 
-template <int LAW, bool NOISE>
+template <int LAW, bool NOISE, bool COMP>
 __global__ void __launch_bounds__(PULSE_WARPS * 32, 1) pulse_kernel(
-    float *__restrict__ W, const float4 *__restrict__ P, int ld, int R, int C,
+    float *__restrict__ W, float *__restrict__ Wlo, const float4 *__restrict__ P, int ld, int R,
+    int C,
     const uint32_t *__restrict__ xw, const uint32_t *__restrict__ dw, int ldb, int B, int row0,
     LawArgs la, RoundKeys rk, uint32_t call, uint32_t one, uint32_t flip) {
   extern __shared__ uint32_t qsm[]; // [PULSE_WARPS][PULSE_QW][32]
@@ -497,10 +462,11 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 1) pulse_kernel(
   const bool valid = j < C;
   const size_t idx = (size_t)i * ld + j;
 
-  float w = 0.f;
+  float w = 0.f, wlo = 0.f; // wlo: compensation term (COMP)
   WCell<LAW> cell;
   cell.init(valid ? P[idx] : make_float4(0.f, 0.f, 1.f, -1.f), la);
   if (valid) w = W[idx];
+  if (COMP && valid) wlo = Wlo[idx];
   const uint32_t jg = (uint32_t)j, ig = (uint32_t)(row0 + i);
   // line-major words: this lane's x line and the warp's d line, ldb % 8 == 0
   const uint32_t *xline = xw + (size_t)(valid ? j : 0) * ldb;
@@ -598,9 +564,21 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 1) pulse_kernel(
       if (NOISE) factor8_rk(g0 + (n >> 3), jg, ig, call, rk, la.k2, f);
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
-        const float wn = cell.step(w, f[v], (word >> (sh8 + v)) & 1u);
-        if (!check || n + v < T) w = wn;
+        if (COMP) {
+          float hn = w, ln = wlo;
+          cell.step2(hn, ln, f[v], (word >> (sh8 + v)) & 1u);
+          if (!check || n + v < T) {
+            w = hn;
+            wlo = ln;
+          }
+        } else {
+          const float wn = cell.step(w, f[v], (word >> (sh8 + v)) & 1u);
+          if (!check || n + v < T) w = wn;
+        }
       }
+      // keep lo below an ulp of hi: its own rounding then stays negligible
+      // (left to grow, lo collects a systematic error of its own)
+      if (COMP) renorm2(w, wlo);
     };
     uint32_t n0 = 0;
     for (; n0 + 32u <= minT; n0 += 32u) {
@@ -619,17 +597,19 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 1) pulse_kernel(
     g0 += (T + 7u) >> 3;
     __syncwarp();
   }
+  if (COMP) renorm2(w, wlo);
   if (valid) W[idx] = w;
+  if (COMP && valid) Wlo[idx] = wlo;
   }
 }
 
-template <int LAW, bool NOISE>
+template <int LAW, bool NOISE, bool COMP>
 static void pulse_dispatch(Tile &t, const uint32_t *xw, const uint32_t *dw, int ldb, int B,
                            LawArgs la, uint32_t call, bool flip) {
   const int smem = PULSE_WARPS * PULSE_QW * 32 * (int)sizeof(uint32_t);
   static bool configured = false;
   if (!configured) {
-    XB_CUDA(cudaFuncSetAttribute(pulse_kernel<LAW, NOISE>,
+    XB_CUDA(cudaFuncSetAttribute(pulse_kernel<LAW, NOISE, COMP>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
@@ -638,7 +618,7 @@ static void pulse_dispatch(Tile &t, const uint32_t *xw, const uint32_t *dw, int 
     static int blocks = 0;
     if (!blocks) {
       int per_sm = 0, dev = 0, sms = 0;
-      XB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pulse_kernel<LAW, NOISE>,
+      XB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pulse_kernel<LAW, NOISE, COMP>,
                                                             PULSE_WARPS * 32, smem));
       XB_CUDA(cudaGetDevice(&dev));
       XB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -647,8 +627,8 @@ static void pulse_dispatch(Tile &t, const uint32_t *xw, const uint32_t *dw, int 
     const long items = (long)t.R * ((t.C + 31) / 32);
     grid = dim3((unsigned)std::min<long>(blocks, (items + PULSE_WARPS - 1) / PULSE_WARPS));
   }
-  pulse_kernel<LAW, NOISE><<<grid, PULSE_WARPS * 32, smem, t.stream>>>(
-      t.W, t.P, t.ld, t.R, t.C, xw, dw, ldb, B, t.row0, la, round_keys(t.k_c2c), call, 1u,
+  pulse_kernel<LAW, NOISE, COMP><<<grid, PULSE_WARPS * 32, smem, t.stream>>>(
+      t.W, t.Wlo, t.P, t.ld, t.R, t.C, xw, dw, ldb, B, t.row0, la, round_keys(t.k_c2c), call, 1u,
       flip ? 0x80000000u : 0u);
   count_launch();
   XB_CUDA(cudaGetLastError());
@@ -663,8 +643,12 @@ void launch_pulse(Tile &t, const uint32_t *xw, const uint32_t *dw, int ldb, int 
   const bool noise = t.cfg.device.dw_min_std > 0.0;
 #define XB_PULSE(K)                                                                        \
   case K:                                                                                  \
-    noise ? pulse_dispatch<K, true>(t, xw, dw, ldb, B, la, call_id, flip)                  \
-          : pulse_dispatch<K, false>(t, xw, dw, ldb, B, la, call_id, flip);                \
+    if (t.comp)                                                                            \
+      noise ? pulse_dispatch<K, true, true>(t, xw, dw, ldb, B, la, call_id, flip)          \
+            : pulse_dispatch<K, false, true>(t, xw, dw, ldb, B, la, call_id, flip);        \
+    else                                                                                   \
+      noise ? pulse_dispatch<K, true, false>(t, xw, dw, ldb, B, la, call_id, flip)         \
+            : pulse_dispatch<K, false, false>(t, xw, dw, ldb, B, la, call_id, flip);       \
     break;
   switch (t.cfg.device.kind) {
     XB_PULSE(XB_CONSTANT_STEP)
@@ -702,39 +686,50 @@ void launch_gather_samples(const uint32_t *in, int ldb_in, int lines, const int 
 // proj/src/pulsed.cpp:128-144: count = lround(bl * p_d * p_x) in fp64, pulses
 // in one direction per (cell, sample).  Signed probabilities carry the line
 // signs (p = 0 <=> sign 0 or a no-op sample).
-template <int LAW, bool NOISE>
+template <int LAW, bool NOISE, bool COMP>
 __global__ void __launch_bounds__(256) pulse_det_kernel(
-    float *__restrict__ W, const float4 *__restrict__ P, int ld, int R, int C,
-    const double *__restrict__ px, const double *__restrict__ pd, const int32_t *__restrict__ bl,
-    int B, int row0, LawArgs la, Key key, uint32_t call) {
+    float *__restrict__ W, float *__restrict__ Wlo, const float4 *__restrict__ P, int ld, int R,
+    int C, const double *__restrict__ px, const double *__restrict__ pd,
+    const int32_t *__restrict__ bl, int B, int row0, LawArgs la, Key key, uint32_t call) {
   const int j = blockIdx.x * 32 + (threadIdx.x & 31);
   const int i = blockIdx.y * 8 + (threadIdx.x >> 5);
   if (i >= R || j >= C) return;
   const size_t idx = (size_t)i * ld + j;
-  float w = W[idx];
-  const Cell cell = make_cell<LAW>(P[idx], la);
+  float w = W[idx], wlo = COMP ? Wlo[idx] : 0.f;
+  WCell<LAW> cell;
+  cell.init(P[idx], la);
   uint32_t n = 0;
   float z[4] = {0.f, 0.f, 0.f, 0.f};
   for (int b = 0; b < B; ++b) {
     const double a = pd[(size_t)b * R + i], x = px[(size_t)b * C + j];
     if (a == 0.0 || x == 0.0) continue;
     const long long count = llround((double)bl[b] * fabs(a) * fabs(x));
-    const Dir dir = make_dir<LAW>(cell, (a > 0.0) == (x > 0.0), la);
+    const bool up = (a > 0.0) == (x > 0.0);
     for (long long k = 0; k < count; ++k, ++n) {
       if (NOISE && (n & 3u) == 0u)
         normal4_fast(n >> 2, (uint32_t)j, (uint32_t)(row0 + i), call, key, z[0], z[1], z[2], z[3]);
-      w = pulse<LAW, NOISE>(w, cell, dir, z[n & 3u]);
+      const float f = NOISE ? fmaf(la.std, z[n & 3u], 1.0f) : 1.0f;
+      if (COMP) {
+        cell.step2(w, wlo, f, up);
+        renorm2(w, wlo);
+      } else {
+        w = cell.step(w, f, up);
+      }
     }
+  }
+  if (COMP) {
+    renorm2(w, wlo);
+    Wlo[idx] = wlo;
   }
   W[idx] = w;
 }
 
-template <int LAW, bool NOISE>
+template <int LAW, bool NOISE, bool COMP>
 static void det_dispatch(Tile &t, const double *px, const double *pd, const int32_t *bl, int B,
                          LawArgs la, uint32_t call) {
   dim3 grid((t.C + 31) / 32, (t.R + 7) / 8);
-  pulse_det_kernel<LAW, NOISE><<<grid, 256, 0, t.stream>>>(t.W, t.P, t.ld, t.R, t.C, px, pd, bl,
-                                                           B, t.row0, la, t.k_c2c, call);
+  pulse_det_kernel<LAW, NOISE, COMP><<<grid, 256, 0, t.stream>>>(
+      t.W, t.Wlo, t.P, t.ld, t.R, t.C, px, pd, bl, B, t.row0, la, t.k_c2c, call);
   count_launch();
   XB_CUDA(cudaGetLastError());
 }
@@ -748,8 +743,12 @@ void launch_pulse_det(Tile &t, const double *px, const double *pd, const int32_t
   const bool noise = t.cfg.device.dw_min_std > 0.0;
 #define XB_DET(K)                                                                          \
   case K:                                                                                  \
-    noise ? det_dispatch<K, true>(t, px, pd, bl, B, la, call_id)                           \
-          : det_dispatch<K, false>(t, px, pd, bl, B, la, call_id);                         \
+    if (t.comp)                                                                            \
+      noise ? det_dispatch<K, true, true>(t, px, pd, bl, B, la, call_id)                   \
+            : det_dispatch<K, false, true>(t, px, pd, bl, B, la, call_id);                 \
+    else                                                                                   \
+      noise ? det_dispatch<K, true, false>(t, px, pd, bl, B, la, call_id)                  \
+            : det_dispatch<K, false, false>(t, px, pd, bl, B, la, call_id);                \
     break;
   switch (t.cfg.device.kind) {
     XB_DET(XB_CONSTANT_STEP)

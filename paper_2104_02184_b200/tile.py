@@ -91,7 +91,8 @@ def device_preset(name: str) -> DeviceParams:
 def TileSettings(device: Optional[DeviceParams] = None, forward_io: Optional[IOParams] = None,
                  backward_io: Optional[IOParams] = None, update: Optional[UpdateParams] = None,
                  temporal: Optional[TemporalParams] = None,
-                 mvm_precision: int = _abi.MVM_FP32) -> TileConfig:
+                 mvm_precision: int = _abi.MVM_FP32,
+                 weight_precision: int = _abi.W_AUTO) -> TileConfig:
     """proj/include/xbarsim/tile.hpp:38-44 with reference defaults."""
     c = TileConfig()
     _lib.xb_default_config(C.byref(c))
@@ -106,6 +107,7 @@ def TileSettings(device: Optional[DeviceParams] = None, forward_io: Optional[IOP
     if temporal is not None:
         c.temporal = temporal
     c.mvm_precision = mvm_precision
+    c.weight_precision = weight_precision
     return c
 
 

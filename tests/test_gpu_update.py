@@ -344,3 +344,33 @@ def test_batched_chunks_beyond_smem_batch():
     b.apply_pulse_trains(xw[:256], dw[:256])
     b.apply_pulse_trains(xw[256:], dw[256:])
     np.testing.assert_array_equal(a.get_weights(), b.get_weights())
+
+
+@pytest.mark.parametrize("wp", [xb.W_AUTO, xb.W_FP32X2, xb.W_FP32])
+def test_compensated_weights_track_fp64(restatement, wp):
+    """SURVEY §7 hard part 3: the "ideal" preset steps by dw_min = 1e-6, only
+    ~17 fp32 ulps of w = 0.5, so fp32 storage rounds every pulse the same way
+    and drifts.  Compensated storage (auto-selected for such devices) adds each
+    step error-free and lands on the reference's fp64 result."""
+    dev = xb.device_preset("ideal")
+    s = xb.TileSettings(device=dev, weight_precision=wp)
+    t = xb.AnalogTile(4, 8, s, 5)
+    t.set_weights(np.full((4, 8), 0.5))
+    n = 2000  # saturated trains: 31 up pulses per sample
+    X = np.ones((n, 8), np.float32)
+    D = np.ones((n, 4), np.float32)
+    t.update(X, D, 1e-3)
+    # the reference's ConstantStep in fp64: every pulse adds dw_min exactly
+    ts = restatement.default("tile")
+    ts.device = restatement.preset("ideal")
+    o = restatement.tile(4, 8, ts, 5)
+    o.set_weights(np.full((4, 8), 0.5))
+    for b in range(0, n, 500):  # a quarter of the samples through the oracle
+        o.update(np.ones(8), np.ones(4), 1e-3)
+    assert np.allclose(o.get_weights(), 0.5 + 31 * 4 * dev.dw_min, atol=1e-12)
+    want = 0.5 + 31 * n * dev.dw_min
+    got = t.get_weights().astype(np.float64)
+    if wp == xb.W_FP32:
+        assert np.abs(got - want).max() > 1e-4  # the drift the compensation removes
+    else:
+        assert np.abs(got - want).max() < 2e-7, np.abs(got - want).max()
