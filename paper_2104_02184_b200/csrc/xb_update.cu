@@ -286,25 +286,42 @@ __device__ __forceinline__ void box_muller_fast(uint32_t a, uint32_t b, float &z
 // r = sqrt(-2 std^2 ln u) = sqrt(lg2(u) * k2) with k2 = -2 ln2 std^2, so each
 // factor is one FMA (1 + r cos) instead of a multiply and an FMA
 // (an IMAD-only int->float variant measured 12 % slower: the XU has room for I2F)
-__device__ __forceinline__ void factor_pair16(uint32_t a, float k2, float &f0, float &f1) {
+#ifndef XB_BM_TABLE
+#define XB_BM_TABLE 1
+#endif
+constexpr int BM_ANGLES = 1024; // Box-Muller angles: (cos, sin) table in shared memory
+__device__ __forceinline__ void factor_pair16(uint32_t a, float k2, float &f0, float &f1,
+                                              const float2 *__restrict__ cs) {
   const float u = fmaf((float)(a & 0xffffu), 1.52587890625e-05f, 7.62939453125e-06f);
-  const float th = fmaf((float)(a >> 16), 9.587379924285257e-05f, -3.1415446284412245f);
   float l, r, s, c;
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(u));
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(l * k2));
+#if XB_BM_TABLE
+  // angle (k + 1/2) 2 pi / 1024 from the top 10 bits: one shared-memory load
+  // instead of two MUFU ops.  With a symmetric grid of >= 5 angles the moments
+  // E[cos^2] = 1/2, E[cos^4] = 3/8, E[cos^2 sin^2] = 1/8 are exact, so z0, z1
+  // keep the unit variance, zero cross-correlation and Gaussian kurtosis.
+  const float2 t = cs[a >> 22];
+  c = t.x;
+  s = t.y;
+#else
+  (void)cs;
+  const float th = fmaf((float)(a >> 16), 9.587379924285257e-05f, -3.1415446284412245f);
   asm("sin.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(th));
   asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(th));
+#endif
   f0 = fmaf(r, c, 1.0f);
   f1 = fmaf(r, s, 1.0f);
 }
 
 __device__ __forceinline__ void factor8_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
-                                           const RoundKeys &rk, float k2, float *f) {
+                                           const RoundKeys &rk, float k2, float *f,
+                                           const float2 *__restrict__ cs) {
   philox10_rk(c0, c1, c2, c3, rk);
-  factor_pair16(c0, k2, f[0], f[1]);
-  factor_pair16(c1, k2, f[2], f[3]);
-  factor_pair16(c2, k2, f[4], f[5]);
-  factor_pair16(c3, k2, f[6], f[7]);
+  factor_pair16(c0, k2, f[0], f[1], cs);
+  factor_pair16(c1, k2, f[2], f[3], cs);
+  factor_pair16(c2, k2, f[4], f[5], cs);
+  factor_pair16(c3, k2, f[6], f[7], cs);
 }
 
 
@@ -440,9 +457,18 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 1) pulse_kernel(
     int C,
     const uint32_t *__restrict__ xw, const uint32_t *__restrict__ dw, int ldb, int B, int row0,
     LawArgs la, RoundKeys rk, uint32_t call, uint32_t one, uint32_t flip) {
-  extern __shared__ uint32_t qsm[]; // [PULSE_WARPS][PULSE_QW][32]
+  extern __shared__ uint32_t qsm[]; // [PULSE_WARPS][PULSE_QW][32] streams, then the angle table
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t *q = qsm + warp * (PULSE_QW * 32) + lane;
+  float2 *cs = reinterpret_cast<float2 *>(qsm + PULSE_WARPS * PULSE_QW * 32);
+  if (NOISE && XB_BM_TABLE) {
+    for (int k = threadIdx.x; k < BM_ANGLES; k += blockDim.x) {
+      double sn, cn;
+      sincospi((2.0 * k + 1.0) / BM_ANGLES, &sn, &cn); // (k + 1/2) 2 pi / 1024
+      cs[k] = make_float2((float)cn, (float)sn);
+    }
+    __syncthreads();
+  }
   // persistent warps (pulse_persist): each walks (row, 32-column block) items
   // with a stride of the whole grid; otherwise one item per warp of a 2-D grid
   constexpr bool persist = pulse_persist<LAW>();
@@ -561,7 +587,7 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 1) pulse_kernel(
     // below the shortest stream need no per-pulse activity test.
     auto pulses8 = [&](uint32_t word, uint32_t n, int sh8, bool check) {
       float f[8] = {1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f};
-      if (NOISE) factor8_rk(g0 + (n >> 3), jg, ig, call, rk, la.k2, f);
+      if (NOISE) factor8_rk(g0 + (n >> 3), jg, ig, call, rk, la.k2, f, cs);
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
         if (COMP) {
@@ -606,7 +632,8 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 1) pulse_kernel(
 template <int LAW, bool NOISE, bool COMP>
 static void pulse_dispatch(Tile &t, const uint32_t *xw, const uint32_t *dw, int ldb, int B,
                            LawArgs la, uint32_t call, bool flip) {
-  const int smem = PULSE_WARPS * PULSE_QW * 32 * (int)sizeof(uint32_t);
+  const int smem = PULSE_WARPS * PULSE_QW * 32 * (int)sizeof(uint32_t) +
+                   (NOISE && XB_BM_TABLE ? BM_ANGLES * (int)sizeof(float2) : 0);
   static bool configured = false;
   if (!configured) {
     XB_CUDA(cudaFuncSetAttribute(pulse_kernel<LAW, NOISE, COMP>,

@@ -301,6 +301,30 @@ def test_c2c_noise_moments():
     assert abs(var / expect_var - 1) < 4 * np.sqrt(2 / (n - 1))
 
 
+def test_c2c_single_pulse_distribution():
+    """One pulse per cell on a ConstantStep tile: dW / dw_min - 1 = std z, so
+    the 262 144 cells sample the c2c factor directly.  z must be a standard
+    normal: mean, variance, skewness and kurtosis within 5 standard errors,
+    and a Kolmogorov-Smirnov distance below 5/sqrt(n) (the 16-bit radius and
+    the 1024-angle Box-Muller grid are invisible at this sample size)."""
+    from math import erf, sqrt
+    dev = xb.default_device()
+    dev.dw_min, dev.dw_min_std, dev.w_max, dev.w_min = 2.0 ** -10, 0.25, 10.0, -10.0
+    R, C = 256, 1024
+    g = xb.AnalogTile(R, C, xb.TileSettings(device=dev, weight_precision=xb.W_FP32), 91)
+    g.apply_pulse_trains(np.ones((1, C), np.uint32), np.ones((1, R), np.uint32))  # slot 0 only
+    z = (g.get_weights().ravel().astype(np.float64) / dev.dw_min - 1.0) / dev.dw_min_std
+    n = z.size
+    assert abs(z.mean()) < 5 / np.sqrt(n)
+    assert abs(z.var() - 1) < 5 * np.sqrt(2 / n)
+    assert abs(((z - z.mean()) ** 3).mean() / z.std() ** 3) < 5 * np.sqrt(6 / n)
+    assert abs(((z - z.mean()) ** 4).mean() / z.var() ** 2 - 3) < 5 * np.sqrt(24 / n)
+    zs = np.sort(z)
+    cdf = 0.5 * (1 + np.vectorize(erf)(zs / sqrt(2)))
+    ks = np.max(np.maximum(np.arange(1, n + 1) / n - cdf, cdf - np.arange(n) / n))
+    assert ks < 5 / np.sqrt(n), ks
+
+
 def test_softbounds_closed_form_on_gpu():
     """Acceptance criterion 3 through the tile: 31 up pulses per call on a
     noise-free SoftBounds cell follow w_n = w_max - w_max (1 - dw/w_max)^n."""
