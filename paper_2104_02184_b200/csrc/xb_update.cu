@@ -430,7 +430,10 @@ __device__ __forceinline__ void renorm2(float &hi, float &lo) {
 // c2c normal #(8q + r) of a cell's segment is element r of the 8 normals of
 // Philox(k_c2c, (g0 + q, j, i, call)) with g0 the cell's running group count,
 // independent of launch geometry and of row sharding.
-constexpr int PULSE_QW = 32;             // stream words per lane
+#ifndef XB_PULSE_QW
+#define XB_PULSE_QW 32
+#endif
+constexpr int PULSE_QW = XB_PULSE_QW;    // stream words per lane
 constexpr int PULSE_CAP = PULSE_QW * 32; // pulses per lane per segment
 
 // Launch shape (B200, round 1): persistent warps, ONE 1024-thread CTA per SM
