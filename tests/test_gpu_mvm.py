@@ -11,7 +11,7 @@ import pytest
 
 import oracle
 import paper_2104_02184_b200 as xb
-from gpu_helpers import close, oracle_io, twin
+from gpu_helpers import close, twin
 
 pytestmark = pytest.mark.gpu
 

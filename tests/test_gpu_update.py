@@ -15,7 +15,7 @@ import pytest
 import oracle
 import paper_2104_02184_b200 as xb
 from paper_2104_02184_b200 import trains as T
-from gpu_helpers import apply_words_to_oracle, close, oracle_settings, twin
+from gpu_helpers import apply_words_to_oracle, close, twin
 
 pytestmark = pytest.mark.gpu
 
