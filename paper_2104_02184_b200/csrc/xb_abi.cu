@@ -384,7 +384,7 @@ static void update_device(Tile &t, const float *dX, const float *dD, int B, cons
     XB_CUDA(cudaMemcpyAsync(bl_out, u.bl, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, t.stream));
     sync(t);
     for (int b = 0; b < B; ++b) {
-      for (int j = 0; j < t.C; ++j) xw_out[(size_t)b * t.C + j] = hx[(size_t)j * ldb + b];
+      for (int j = 0; j < t.C; ++j) xw_out[(size_t)b * t.C + j] = hx[xq_index(j, b, t.C)];
       for (int i = 0; i < t.R; ++i) dw_out[(size_t)b * t.R + i] = hd[(size_t)i * ldb + b];
     }
     return;
@@ -916,12 +916,12 @@ int xb_tile_apply_trains(xb_tile *h, const uint32_t *xw, const uint32_t *dw, int
     Tile &t = h->t;
     if (B < 0) raise("apply_trains: batch must be >= 0");
     if (B == 0) return;
-    // reference-facing sample-major words -> internal line-major layout
+    // reference-facing sample-major words -> internal layouts (x quads, d lines)
     const int ldb = train_ld(B);
     const size_t nx = (size_t)ldb * t.C, nd = (size_t)ldb * t.R;
     std::vector<uint32_t> hw(nx + nd, 0u);
     for (int b = 0; b < B; ++b) {
-      for (int j = 0; j < t.C; ++j) hw[(size_t)j * ldb + b] = xw[(size_t)b * t.C + j];
+      for (int j = 0; j < t.C; ++j) hw[xq_index(j, b, t.C)] = xw[(size_t)b * t.C + j];
       for (int i = 0; i < t.R; ++i)
         hw[nx + (size_t)i * ldb + b] = dw[(size_t)b * t.R + i] ^ (flip ? 0x80000000u : 0u);
     }
@@ -1365,7 +1365,7 @@ static void uc_update(xb_unitcell *u, const float *X, const float *D, int B, con
       const int n = (int)idx.size(), ldn = train_ld(n);
       XB_CUDA(cudaMemcpyAsync(dIdx, idx.data(), sizeof(int) * n, cudaMemcpyHostToDevice,
                               e.stream));
-      launch_gather_samples(ub.xw, ldb, e.C, dIdx, n, gx, ldn, e.stream);
+      launch_gather_samples(ub.xw, ldb, e.C, dIdx, n, gx, ldn, e.stream, true);
       launch_gather_samples(ub.dw, ldb, e.R, dIdx, n, gx + (size_t)ldn * e.C, ldn, e.stream);
       Tile &m = u->members[k]->t;
       launch_pulse(m, gx, gx + (size_t)ldn * e.C, ldn, n, m.upd_calls++, u->cfg.gains[k] < 0.0);

@@ -97,15 +97,24 @@ void launch_trains(const Tile &t, const float *X, const float *D, int B, const f
                    float lr_scalar, const float *xm, const float *dm, uint64_t seq0,
                    uint32_t *xw, uint32_t *dw, int ldb, int32_t *bl, double *px, double *pd,
                    bool deterministic, const double *dwmin_b = nullptr);
-// trains are LINE-major: xw[j][b], dw[i][b], row stride ldb (multiple of 8)
+// d trains are LINE-major: dw[i][b], row stride ldb (multiple of 8).  x trains
+// are QUAD-interleaved: the words of samples 4q..4q+3 of column j form one
+// uint4 at quad index q * C + j (xq_index), ldb * C words in all.  A warp of the
+// pulse kernel (32 consecutive columns) then reads 4 samples as one coalesced
+// 512-byte request instead of 32 separate lines (the L1 data pipe was the
+// binding unit with line-major x words).
 inline int train_ld(int B) { return (B + 7) / 8 * 8; }
+__host__ __device__ inline size_t xq_index(int j, int b, int C) {
+  return (((size_t)(b >> 2) * (size_t)C + (size_t)j) << 2) | (size_t)(b & 3);
+}
 // weight-stationary coincidence/pulse kernel over packed words
 // flip inverts every pulse (negative unit-cell gain, tile.cpp:164-167)
 void launch_pulse(Tile &t, const uint32_t *xw, const uint32_t *dw, int ldb, int B,
                   uint32_t call_id, bool flip = false);
-// out[line][k] = in[line][idx[k]] (k < n), zero-padded to ldb_out
+// out[line][k] = in[line][idx[k]] (k < n), zero-padded to ldb_out; quad != 0:
+// both sides in the x quad layout (xq_index with C = lines)
 void launch_gather_samples(const uint32_t *in, int ldb_in, int lines, const int *idx, int n,
-                           uint32_t *out, int ldb_out, cudaStream_t s);
+                           uint32_t *out, int ldb_out, cudaStream_t s, bool quad = false);
 // W_eff = sum_k g_k W_k over [R][ld] (fp64 sum, fp32 store); K <= XB_MAX_CELL_DEVICES
 void launch_effective(float *weff, const float *const *w, const double *g, int K, int R, int C,
                       int ld, cudaStream_t s);

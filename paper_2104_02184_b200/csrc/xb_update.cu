@@ -125,7 +125,8 @@ __device__ __forceinline__ Plan make_plan(double lrb, double x_amax, double d_am
   return pl;
 }
 
-// Packed trains in LINE-major layout out[line][b] (row stride ldb): the pulse
+// Packed trains, d LINE-major dw[line][b] (row stride ldb), x in the quad
+// layout of xq_index (xb_internal.h); zero words for ldb > b >= B.  The pulse
 // kernel then reads 4-8 consecutive samples of one line with a single vector
 // load.  CTA tile: 32 lines x 32 samples; x lines first, then d lines.
 __global__ void __launch_bounds__(256) trains_kernel(
@@ -171,10 +172,16 @@ __global__ void __launch_bounds__(256) trains_kernel(
     tile[lane][s] = word;
   }
   __syncthreads();
-  uint32_t *out = is_x ? xw : dw;
-  for (int r = warp; r < 32; r += 8) {
-    const int ln = l0 + r, b = b0 + lane;
-    if (ln < nl && b < B) out[(size_t)ln * ldb + b] = tile[r][lane];
+  if (is_x) { // quad layout (xq_index): thread = (column r, quad q), one uint4 store
+    const int r = threadIdx.x & 31, q = threadIdx.x >> 5, ln = l0 + r, b = b0 + 4 * q;
+    if (ln < nl && b < ldb)
+      reinterpret_cast<uint4 *>(xw)[(size_t)(b >> 2) * C + ln] =
+          make_uint4(tile[r][4 * q], tile[r][4 * q + 1], tile[r][4 * q + 2], tile[r][4 * q + 3]);
+  } else {
+    for (int r = warp; r < 32; r += 8) {
+      const int ln = l0 + r, b = b0 + lane;
+      if (ln < nl && b < B) dw[(size_t)ln * ldb + b] = tile[r][lane];
+    }
   }
 }
 
@@ -452,6 +459,9 @@ constexpr int PULSE_WARPS = 32;
 #ifndef XB_PULSE_PERSIST
 #define XB_PULSE_PERSIST 1
 #endif
+#ifndef XB_PULSE_COLMAJOR
+#define XB_PULSE_COLMAJOR 1
+#endif
 template <int LAW> constexpr bool pulse_persist() { return XB_PULSE_PERSIST != 0; }
 
 template <int LAW, bool NOISE, bool COMP>
@@ -481,8 +491,17 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 1) pulse_kernel(
        item += gridDim.x * PULSE_WARPS) {
     int i, j;
     if (persist) {
+#if XB_PULSE_COLMAJOR
+      // column-block major: the warps of a CTA take consecutive rows of ONE
+      // 32-column block, so they read the same x train words (L1 hits) and
+      // the L2 sees each x word once per CTA instead of once per row
+      const uint32_t cb = item / (uint32_t)R;
+      i = (int)(item - cb * (uint32_t)R);
+      j = (int)cb * 32 + lane;
+#else
       i = (int)(item / ncb);
       j = (int)(item - (uint32_t)i * ncb) * 32 + lane;
+#endif
     } else {
       j = blockIdx.x * 32 + lane;
       i = blockIdx.y * PULSE_WARPS + warp;
@@ -497,8 +516,9 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 1) pulse_kernel(
   if (valid) w = W[idx];
   if (COMP && valid) wlo = Wlo[idx];
   const uint32_t jg = (uint32_t)j, ig = (uint32_t)(row0 + i);
-  // line-major words: this lane's x line and the warp's d line, ldb % 8 == 0
-  const uint32_t *xline = xw + (size_t)(valid ? j : 0) * ldb;
+  // this lane's x words (quad layout: 4 samples per uint4, stride C uint4s)
+  // and the warp's d line (line-major, ldb % 8 == 0)
+  const uint4 *xq = reinterpret_cast<const uint4 *>(xw) + (valid ? j : 0);
   const uint32_t *dline = dw + (size_t)i * ldb;
   const uint32_t xmask = valid ? 0x7fffffffu : 0u; // idle lanes see no coincidences
   const uint32_t q0 = (uint32_t)__cvta_generic_to_shared(q);
@@ -528,53 +548,42 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 1) pulse_kernel(
       sh = e & 31u;
     };
     auto stream_len = [&]() { return ((qa - q0) >> 2) + sh; };
-    // fast path: aligned blocks of PB samples, vector loads prefetched one
-    // block ahead; a block is taken only if it cannot overflow any lane's stream
+    // fast path: aligned blocks of PB samples held as NV uint4 slots of x
+    // and of d words; each slot is refilled with the next block's words as
+    // soon as it is consumed (rolling prefetch, no register copies).  A block
+    // is taken only if it cannot overflow any lane's stream.
     constexpr int PB = XB_PULSE_PB, NV = PB / 4;
     if ((b % PB) == 0 && b + PB <= B) {
-      const uint4 *xv4 = reinterpret_cast<const uint4 *>(xline);
       const uint4 *dv4 = reinterpret_cast<const uint4 *>(dline);
       uint4 xa[NV], da[NV];
 #pragma unroll
       for (int u = 0; u < NV; ++u) {
-        xa[u] = __ldg(xv4 + (b >> 2) + u);
+        xa[u] = __ldg(xq + (size_t)((b >> 2) + u) * C);
         da[u] = __ldg(dv4 + (b >> 2) + u);
       }
-      while (true) {
-        if (__any_sync(0xffffffffu, stream_len() + PB * 31u > (uint32_t)PULSE_CAP)) break;
+      while (!__any_sync(0xffffffffu, stream_len() + PB * 31u > (uint32_t)PULSE_CAP)) {
         const int bn = b + PB;
-        uint4 nxa[NV], nda[NV];
-#pragma unroll
-        for (int u = 0; u < NV; ++u) {
-          nxa[u] = xa[u];
-          nda[u] = da[u];
-        }
-        if (bn + PB <= B) {
-#pragma unroll
-          for (int u = 0; u < NV; ++u) {
-            nxa[u] = __ldg(xv4 + (bn >> 2) + u);
-            nda[u] = __ldg(dv4 + (bn >> 2) + u);
-          }
-        }
+        const bool more = bn + PB <= B;
 #pragma unroll
         for (int u = 0; u < NV; ++u) {
           append(xa[u].x, da[u].x);
           append(xa[u].y, da[u].y);
           append(xa[u].z, da[u].z);
           append(xa[u].w, da[u].w);
+          if (more) {
+            xa[u] = __ldg(xq + (size_t)((bn >> 2) + u) * C);
+            da[u] = __ldg(dv4 + (bn >> 2) + u);
+          }
         }
         b = bn;
-        if (b + PB > B) break;
-#pragma unroll
-        for (int u = 0; u < NV; ++u) {
-          xa[u] = nxa[u];
-          da[u] = nda[u];
-        }
+        if (!more) break;
       }
     }
     // careful path, one sample at a time: the batch tail, or a stream near CAP
     while (b < B) {
-      const uint32_t xv = __ldg(xline + b), dv = __ldg(dline + b);
+      const uint32_t xv = __ldg(reinterpret_cast<const uint32_t *>(xq + (size_t)(b >> 2) * C) +
+                                (b & 3)),
+                     dv = __ldg(dline + b);
       if (__any_sync(0xffffffffu, stream_len() + __popc(xv & dv & xmask) > (uint32_t)PULSE_CAP))
         break;
       append(xv, dv);
@@ -696,18 +705,22 @@ void launch_pulse(Tile &t, const uint32_t *xw, const uint32_t *dw, int ldb, int 
 // the samples one unit-cell member receives (round-robin policy)
 __global__ void gather_samples_kernel(const uint32_t *__restrict__ in, int ldb_in, int lines,
                                       const int *__restrict__ idx, int n,
-                                      uint32_t *__restrict__ out, int ldb_out) {
+                                      uint32_t *__restrict__ out, int ldb_out, bool quad) {
   const int line = blockIdx.y;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ldb_out; k += gridDim.x * blockDim.x)
-    out[(size_t)line * ldb_out + k] = k < n ? in[(size_t)line * ldb_in + idx[k]] : 0u;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ldb_out; k += gridDim.x * blockDim.x) {
+    if (quad)
+      out[xq_index(line, k, lines)] = k < n ? in[xq_index(line, idx[k], lines)] : 0u;
+    else
+      out[(size_t)line * ldb_out + k] = k < n ? in[(size_t)line * ldb_in + idx[k]] : 0u;
+  }
 }
 
 void launch_gather_samples(const uint32_t *in, int ldb_in, int lines, const int *idx, int n,
-                           uint32_t *out, int ldb_out, cudaStream_t s) {
+                           uint32_t *out, int ldb_out, cudaStream_t s, bool quad) {
   if (lines <= 0 || ldb_out <= 0) return;
   const int threads = std::min(256, (ldb_out + 31) / 32 * 32);
   dim3 grid((ldb_out + threads - 1) / threads, lines);
-  gather_samples_kernel<<<grid, threads, 0, s>>>(in, ldb_in, lines, idx, n, out, ldb_out);
+  gather_samples_kernel<<<grid, threads, 0, s>>>(in, ldb_in, lines, idx, n, out, ldb_out, quad);
   count_launch();
   XB_CUDA(cudaGetLastError());
 }
