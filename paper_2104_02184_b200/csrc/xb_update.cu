@@ -426,7 +426,7 @@ __device__ __forceinline__ void renorm2(float &hi, float &lo) {
 //   pre-pass (branch-free, sample order): per sample b, c = x_b & d_b (slot
 //     bits), k = popc(c), direction = sign(x) * sign(d); the lane appends k
 //     direction bits to its private pulse stream in shared memory
-//     (1 = up, 0 = down).  A segment ends when some lane's stream would pass
+//     (1 = down, 0 = up).  A segment ends when some lane's stream would pass
 //     CAP pulses (a warp vote), so any batch size and pulse density fit.
 //   pulse loop: iteration n applies pulse n of every lane whose stream is
 //     longer than n: the direction bit selects the law constants, the c2c
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 1) pulse_kernel(
     float *__restrict__ W, float *__restrict__ Wlo, const float4 *__restrict__ P, int ld, int R,
     int C,
     const uint32_t *__restrict__ xw, const uint32_t *__restrict__ dw, int ldb, int B, int row0,
-    LawArgs la, RoundKeys rk, uint32_t call, uint32_t one, uint32_t flip) {
+    LawArgs la, RoundKeys rk, uint32_t call, uint32_t two, uint32_t flip) {
   extern __shared__ uint32_t qsm[]; // [PULSE_WARPS][PULSE_QW][32] streams, then the angle table
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t *q = qsm + warp * (PULSE_QW * 32) + lane;
@@ -530,22 +530,26 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 1) pulse_kernel(
     // sh = fill of the open stream word acc, qa = its shared address; the
     // stream length is T = (qa - q0) / 4 + sh (32 pulses per 128-B word step).
     uint32_t sh = 0, acc = 0, qa = q0;
+    // The pulse direction is bit 31 of x ^ d ^ flip (the line signs); it is
+    // moved to bit 0 with a multiply-high on the FMA pipe (dn = 1 iff down)
+    // and the stream bits (1 = down) are added with a multiply-add (the bits
+    // are disjoint), which balances the pre-pass between the ALU and FMA pipes
     auto append = [&](uint32_t xv, uint32_t dv) {
       const uint32_t k = __popc(xv & dv & xmask);
-      uint32_t down; // all ones iff the signs differ: mul.hi by a runtime 1 keeps it on the FMA pipe
-      asm("mul.hi.s32 %0, %1, %2;" : "=r"(down) : "r"(xv ^ dv ^ flip), "r"(one));
-      uint32_t lo; // k ones from bit sh, clipped at bit 31 (BMSK)
-      asm("bmsk.clamp.b32 %0, %1, %2;" : "=r"(lo) : "r"(sh), "r"(k));
-      acc |= lo & ~down;
-      const uint32_t e = sh + k;
+      uint32_t dn, lo;
+      asm("mul.hi.u32 %0, %1, %2;" : "=r"(dn) : "r"(xv ^ dv ^ flip), "r"(two));
+      asm("bmsk.clamp.b32 %0, %1, %2;" : "=r"(lo) : "r"(sh), "r"(k)); // k ones from bit sh
+      asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(acc) : "r"(lo), "r"(dn));
+      uint32_t e = sh + k;
       if (e >= 32u) {
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(qa), "r"(acc));
         qa += 128u;
+        e -= 32u; // e < 63: a predicated add (FMA pipe) instead of an AND (ALU)
         uint32_t hi;
-        asm("bmsk.clamp.b32 %0, %1, %2;" : "=r"(hi) : "r"(0u), "r"(e & 31u));
-        acc = hi & ~down;
+        asm("bmsk.clamp.b32 %0, %1, %2;" : "=r"(hi) : "r"(0u), "r"(e));
+        asm("mul.lo.u32 %0, %1, %2;" : "=r"(acc) : "r"(hi), "r"(dn));
       }
-      sh = e & 31u;
+      sh = e;
     };
     auto stream_len = [&]() { return ((qa - q0) >> 2) + sh; };
     // fast path: aligned blocks of PB samples held as NV uint4 slots of x
@@ -554,16 +558,21 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 1) pulse_kernel(
     // is taken only if it cannot overflow any lane's stream.
     constexpr int PB = XB_PULSE_PB, NV = PB / 4;
     if ((b % PB) == 0 && b + PB <= B) {
-      const uint4 *dv4 = reinterpret_cast<const uint4 *>(dline);
+      // running pointers: one 64-bit step per block instead of index math
+      const uint4 *xn = xq + (size_t)(b >> 2) * C;
+      const uint4 *dn = reinterpret_cast<const uint4 *>(dline) + (b >> 2);
+      const size_t xs = (size_t)C * NV; // uint4s per block of x
       uint4 xa[NV], da[NV];
 #pragma unroll
       for (int u = 0; u < NV; ++u) {
-        xa[u] = __ldg(xq + (size_t)((b >> 2) + u) * C);
-        da[u] = __ldg(dv4 + (b >> 2) + u);
+        xa[u] = __ldg(xn + (size_t)u * C);
+        da[u] = __ldg(dn + u);
       }
       while (!__any_sync(0xffffffffu, stream_len() + PB * 31u > (uint32_t)PULSE_CAP)) {
         const int bn = b + PB;
         const bool more = bn + PB <= B;
+        xn += xs;
+        dn += NV;
 #pragma unroll
         for (int u = 0; u < NV; ++u) {
           append(xa[u].x, da[u].x);
@@ -571,8 +580,8 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 1) pulse_kernel(
           append(xa[u].z, da[u].z);
           append(xa[u].w, da[u].w);
           if (more) {
-            xa[u] = __ldg(xq + (size_t)((bn >> 2) + u) * C);
-            da[u] = __ldg(dv4 + (bn >> 2) + u);
+            xa[u] = __ldg(xn + (size_t)u * C);
+            da[u] = __ldg(dn + u);
           }
         }
         b = bn;
@@ -604,13 +613,13 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, 1) pulse_kernel(
       for (int v = 0; v < 8; ++v) {
         if (COMP) {
           float hn = w, ln = wlo;
-          cell.step2(hn, ln, f[v], (word >> (sh8 + v)) & 1u);
+          cell.step2(hn, ln, f[v], ((word >> (sh8 + v)) & 1u) == 0u);
           if (!check || n + v < T) {
             w = hn;
             wlo = ln;
           }
         } else {
-          const float wn = cell.step(w, f[v], (word >> (sh8 + v)) & 1u);
+          const float wn = cell.step(w, f[v], ((word >> (sh8 + v)) & 1u) == 0u);
           if (!check || n + v < T) w = wn;
         }
       }
@@ -667,7 +676,7 @@ static void pulse_dispatch(Tile &t, const uint32_t *xw, const uint32_t *dw, int 
     grid = dim3((unsigned)std::min<long>(blocks, (items + PULSE_WARPS - 1) / PULSE_WARPS));
   }
   pulse_kernel<LAW, NOISE, COMP><<<grid, PULSE_WARPS * 32, smem, t.stream>>>(
-      t.W, t.Wlo, t.P, t.ld, t.R, t.C, xw, dw, ldb, B, t.row0, la, round_keys(t.k_c2c), call, 1u,
+      t.W, t.Wlo, t.P, t.ld, t.R, t.C, xw, dw, ldb, B, t.row0, la, round_keys(t.k_c2c), call, 2u,
       flip ? 0x80000000u : 0u);
   count_launch();
   XB_CUDA(cudaGetLastError());
