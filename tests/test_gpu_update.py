@@ -58,13 +58,15 @@ def test_identical_trains_parity(kind, shape):
 
 
 @pytest.mark.parametrize("kind", LAWS)
-def test_update_equals_generate_plus_apply(kind):
-    """The fused update path draws exactly the trains generate_trains reports."""
+@pytest.mark.parametrize("B", [40, 13])
+def test_update_equals_generate_plus_apply(kind, B):
+    """The fused update path draws exactly the trains generate_trains reports
+    (B = 13: partial 4-sample quads of the x train layout)."""
     cfg = cfg_law(kind, std=0.3)
     a = xb.AnalogTile(50, 70, cfg, 9)
     a.set_weights(np.random.default_rng(2).uniform(-0.2, 0.2, (50, 70)))
     b = a.clone()
-    X, D = rand_xd(40, 70, 50, 6)
+    X, D = rand_xd(B, 70, 50, 6)
     xw, dw, bl = b.generate_trains(X, D, 0.01)
     a.update(X, D, 0.01)
     b.apply_pulse_trains(xw, dw)
