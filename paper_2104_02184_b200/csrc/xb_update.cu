@@ -447,7 +447,15 @@ constexpr int PULSE_CAP = PULSE_QW * 32; // pulses per lane per segment
 // (64 registers, no spills).  NS update: 7.48 ms vs 7.65 ms with two
 // 512-thread CTAs and 8.0 ms with four 256-thread CTAs; ExpStep (cfg3):
 // 13.5 ms vs 13.8 ms for a per-tile grid of 512-thread CTAs.
-constexpr int PULSE_WARPS = 32;
+// (more warps at fewer registers lose: 2 CTAs x 18 or 20 warps, 56/51 regs,
+// 6.89/6.91 ms vs 6.56 ms for 1 x 32 warps at 64 regs)
+#ifndef XB_PULSE_WARPS
+#define XB_PULSE_WARPS 32
+#endif
+#ifndef XB_PULSE_CTAS
+#define XB_PULSE_CTAS 1
+#endif
+constexpr int PULSE_WARPS = XB_PULSE_WARPS;
 // samples per vector block of the pre-pass (4: one uint4 of x and of d words;
 // measured 6 % slower than 8)
 #ifndef XB_PULSE_PB
@@ -465,7 +473,7 @@ constexpr int PULSE_WARPS = 32;
 template <int LAW> constexpr bool pulse_persist() { return XB_PULSE_PERSIST != 0; }
 
 template <int LAW, bool NOISE, bool COMP>
-__global__ void __launch_bounds__(PULSE_WARPS * 32, 1) pulse_kernel(
+__global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
     float *__restrict__ W, float *__restrict__ Wlo, const float4 *__restrict__ P, int ld, int R,
     int C,
     const uint32_t *__restrict__ xw, const uint32_t *__restrict__ dw, int ldb, int B, int row0,
