@@ -303,19 +303,26 @@ def test_c2c_noise_moments():
     assert abs(var / expect_var - 1) < 4 * np.sqrt(2 / (n - 1))
 
 
-def test_c2c_single_pulse_distribution():
-    """One pulse per cell on a ConstantStep tile: dW / dw_min - 1 = std z, so
-    the 262 144 cells sample the c2c factor directly.  z must be a standard
-    normal: mean, variance, skewness and kurtosis within 5 standard errors,
-    and a Kolmogorov-Smirnov distance below 5/sqrt(n) (the 16-bit radius and
-    the 1024-angle Box-Muller grid are invisible at this sample size)."""
+@pytest.mark.parametrize("kind", [xb.CONSTANT_STEP, xb.EXP_STEP])
+def test_c2c_single_pulse_distribution(kind):
+    """One pulse per cell from w = 0: dW / h - 1 = std z with h the law's
+    step at w = 0 (dw_min for ConstantStep), so the 262 144 cells sample the
+    c2c factor directly.  z must be a standard normal: mean, variance,
+    skewness and kurtosis within 5 standard errors, and a Kolmogorov-Smirnov
+    distance below 5/sqrt(n) (the 16-bit radius and the 1024-angle
+    Box-Muller grid are invisible at this sample size)."""
     from math import erf, sqrt
     dev = xb.default_device()
+    dev.kind = kind
     dev.dw_min, dev.dw_min_std, dev.w_max, dev.w_min = 2.0 ** -10, 0.25, 10.0, -10.0
+    h = dev.dw_min
+    if kind == xb.EXP_STEP:
+        dev.gamma = 2.0
+        h = dev.dw_min * np.exp(-dev.gamma * (0.0 - dev.w_min) / (dev.w_max - dev.w_min))
     R, C = 256, 1024
     g = xb.AnalogTile(R, C, xb.TileSettings(device=dev, weight_precision=xb.W_FP32), 91)
     g.apply_pulse_trains(np.ones((1, C), np.uint32), np.ones((1, R), np.uint32))  # slot 0 only
-    z = (g.get_weights().ravel().astype(np.float64) / dev.dw_min - 1.0) / dev.dw_min_std
+    z = (g.get_weights().ravel().astype(np.float64) / h - 1.0) / dev.dw_min_std
     n = z.size
     assert abs(z.mean()) < 5 / np.sqrt(n)
     assert abs(z.var() - 1) < 5 * np.sqrt(2 / n)
