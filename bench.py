@@ -123,9 +123,13 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # validation-only overrides (never for a reported number): run the N > 1
+    # code path with every rank on one device and gloo host collectives
+    if os.environ.get("XB_BENCH_DEVICE"):
+        local = int(os.environ["XB_BENCH_DEVICE"])
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("XB_BENCH_DIST_BACKEND", "nccl"))
     dev = torch.device("cuda", local)
     # a dedicated (non-default) stream shared by torch and the tile, so CUDA
     # events, NCCL and the tile's kernels are ordered on one queue

@@ -1,0 +1,48 @@
+"""bench.py contract checks on the GPU: the N = 1 line and the N > 1 code
+path (row-sharded tile, max|d| all-reduce, max-over-ranks timing) run as two
+torchrun ranks.  With one GPU both ranks share cuda:0 and all-reduce through
+gloo on the host (XB_BENCH_DEVICE / XB_BENCH_DIST_BACKEND): this validates the
+multi-rank logic only -- its timings are not measurements."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+        "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "roofline",
+        "clocks", "gpu_launches", "e2e"}
+
+
+def _last_json(out: str) -> dict:
+    lines = [ln for ln in out.splitlines() if ln.startswith("{")]
+    assert lines, out[-2000:]
+    return json.loads(lines[-1])
+
+
+@pytest.mark.gpu
+def test_bench_single_gpu_line():
+    r = subprocess.run([sys.executable, "bench.py", "--steps", "2", "--warmup", "3",
+                        "--no-cpu-baseline"], cwd=ROOT, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = _last_json(r.stdout)
+    assert KEYS <= set(d)
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["gpu_launches"] > 0
+    assert d["roofline"]["frac"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
+
+
+@pytest.mark.gpu
+def test_bench_two_rank_code_path():
+    env = dict(os.environ, XB_BENCH_DEVICE="0", XB_BENCH_DIST_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                        "29531", "bench.py", "--gpus", "2", "--steps", "2", "--warmup", "3"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = _last_json(r.stdout)
+    assert KEYS <= set(d)
+    assert d["n_gpus"] == 2 and d["config"]["tile_rows_total"] == 8192
+    assert d["e2e"]["h2d_bytes_per_step"] == 2 * (256 * 4096 * 4 * 2)
