@@ -659,7 +659,12 @@ CUtensorMap make_map(const float *base, int rows, int cols, int ld, int box_rows
 // K-splits to fill the SMs (more partial-sum traffic): measured on B200 they
 // win for 16384^2 (forward 571 vs 607 us, backward 263 vs 278 us) and lose
 // for 4096^2 (70 vs 66 us); one for 3xTF32 (its stage would not fit twice)
-static int tc_nsub(int M, bool x3) { return (!x3 && M >= 8192) ? 2 : 1; }
+// (fused output stage, round 1: NSUB = 2 at 4096^2 doubles the forward,
+// 71 vs 36 us back to back; at 16384^2 the two are equal, 265 us)
+#ifndef XB_TC_NSUB2_MIN
+#define XB_TC_NSUB2_MIN 8192
+#endif
+static int tc_nsub(int M, bool x3) { return (!x3 && M >= XB_TC_NSUB2_MIN) ? 2 : 1; }
 
 int tc_splits(int M, int K, bool x3) {
   const int band = TC_BM * tc_nsub(M, x3);
