@@ -323,7 +323,7 @@ struct UpdBufs {
 static UpdBufs upd_bufs(Tile &t, int B, bool det) {
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   const size_t s_lr = al(B * sizeof(float)), s_bl = al(B * sizeof(int32_t));
-  const size_t nb = det ? (size_t)B : (size_t)train_ld(B); // trains are line-major [line][ldb]
+  const size_t nb = det ? (size_t)B : (size_t)train_ld(B); // ldb words per line (x quads, d lines)
   const size_t s_xw = al(nb * t.C * (det ? sizeof(double) : sizeof(uint32_t)));
   const size_t s_dw = al(nb * std::max(t.R, 1) * (det ? sizeof(double) : sizeof(uint32_t)));
   char *p = (char *)t.s_words.get(3 * s_lr + s_bl + s_xw + s_dw);
