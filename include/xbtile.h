@@ -226,7 +226,11 @@ int xb_tile_update_dev(xb_tile *t, const float *dX, const float *dD, int B, cons
 /* backward of a row shard, split around the reduction over ranks:
  *   partial: dP[B][d_in] = sum over local rows of W^T d~ (+ weight-noise fold);
  *            dAmaxD = GLOBAL max|d| per sample (NULL = local)
- *   finish : dG = alpha * ADC(sum_ranks dP + sigma_out xi) */
+ *   finish : dG = alpha * ADC(sum_ranks dP + sigma_out xi)
+ * Several partials may be in flight before their finishes (a batch split in
+ * sample chunks, each chunk's reduction overlapping the next chunk's
+ * contraction): finishes must then come in the order of their partials, and
+ * the noise draws equal those of one call over the whole batch. */
 int xb_tile_backward_partial_dev(xb_tile *t, const float *dD, int B, const float *dAmaxD,
                                  float *dP);
 int xb_tile_backward_finish_dev(xb_tile *t, const float *dPsum, int B, const float *dAmaxD,

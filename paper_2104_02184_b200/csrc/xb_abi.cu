@@ -617,6 +617,7 @@ int xb_tile_clone(const xb_tile *src, xb_tile **out) { // tile.hpp:91 (deep copy
     t.learning_rate = s.learning_rate;
     t.seq_fwd = s.seq_fwd;
     t.seq_bwd = s.seq_bwd;
+    t.bwd_pending = s.bwd_pending;
     t.seq_upd = s.seq_upd;
     t.upd_calls = s.upd_calls;
     t.temporal_calls = s.temporal_calls;
@@ -852,7 +853,10 @@ int xb_tile_backward_partial_dev(xb_tile *h, const float *dD, int B, const float
     if (io.bound_management != XB_BM_NONE)
       raise("backward_io.bound_management: not supported on row shards");
     IoDev d = make_io(io);
-    mvm_backward(t, dD, B, nullptr, d, t.k_bwd, t.seq_bwd, dAmaxD, true, dP);
+    // partials may run ahead of their finishes (chunked, overlapped
+    // reductions): a partial's samples follow those still pending
+    mvm_backward(t, dD, B, nullptr, d, t.k_bwd, t.seq_bwd + t.bwd_pending, dAmaxD, true, dP);
+    t.bwd_pending += (uint64_t)B;
   });
 }
 
@@ -862,6 +866,7 @@ int xb_tile_backward_finish_dev(xb_tile *h, const float *dPsum, int B, const flo
     Tile &t = h->t;
     mvm_backward_finish(t, dPsum, B, dAmaxD, dG, make_io(t.cfg.backward_io), t.k_bwd, t.seq_bwd);
     t.seq_bwd += (uint64_t)B;
+    t.bwd_pending -= std::min(t.bwd_pending, (uint64_t)B);
   });
 }
 

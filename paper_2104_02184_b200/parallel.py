@@ -7,13 +7,17 @@ unsharded tile.  The only data-path collectives:
 * update  : all-reduce(max) of the per-sample max|d| (translate needs the
             global value, proj/src/pulsed.cpp:34-51); x is replicated;
 * backward: all-reduce(max) of max|d| before the DAC, then all-reduce(sum)
-            of the per-shard column sums; output noise, ADC and alpha are
-            applied after the reduction (proj/src/io.cpp:143-146);
+            of the per-shard column sums, in sample chunks whose reductions
+            overlap the next chunk's contraction; output noise, ADC and alpha
+            are applied after the reduction (proj/src/io.cpp:143-146);
 * forward : none (outputs stay row-sharded).
 
 The local compute object needs five methods (``forward_dev``,
 ``update_dev``, ``backward_partial_dev``, ``backward_finish_dev``,
-``rows_amax``); on a B200 it is :class:`AnalogTile` built with ``shard=``.
+``rows_amax``); on a B200 it is :class:`AnalogTile` built with ``shard=``,
+running on the torch stream current at the calls
+(``local.set_stream(torch.cuda.current_stream().cuda_stream)``): the NCCL
+collectives are ordered after the tile's kernels through that stream.
 """
 from __future__ import annotations
 
@@ -69,13 +73,34 @@ class RowShardedTile:
         """B sequential pulsed updates of the whole tile; D_local = this rank's rows of d."""
         self.local.update_dev(X, D_local, lr, amax_d=self._amax_global(D_local))
 
-    def backward(self, D_local, G):
-        """Full backward G[B][d_in] (replicated on every rank)."""
+    def backward(self, D_local, G, chunks: int | None = None):
+        """Full backward G[B][d_in] (replicated on every rank).
+
+        The batch is cut into ``chunks`` sample ranges (default: 4 when every
+        range keeps >= 64 samples, else 1): all chunk contractions are issued
+        back to back, each followed by its asynchronous all-reduce(sum), so
+        the reduction of chunk c overlaps the contraction of chunk c + 1;
+        the finishes (noise, ADC, alpha) then run in chunk order.  The noise
+        draws are addressed by sample, so every chunking gives the same G."""
         amax = self._amax_global(D_local)
-        P = self.local.backward_partial_dev(D_local, amax)
-        if self.world > 1:
-            self.dist.all_reduce(P, op=self.dist.ReduceOp.SUM, group=self.group)
-        self.local.backward_finish_dev(P, amax, G)
+        B = int(D_local.shape[0])
+        n = chunks if chunks is not None else (4 if B >= 256 else 1)
+        n = max(1, min(n, B))
+        edges = [B * k // n for k in range(n + 1)]
+        inflight = []
+        for b0, b1 in zip(edges[:-1], edges[1:]):
+            if b1 == b0:
+                continue
+            P = self.local.backward_partial_dev(D_local[b0:b1], amax[b0:b1])
+            work = None
+            if self.world > 1:
+                work = self.dist.all_reduce(P, op=self.dist.ReduceOp.SUM, group=self.group,
+                                            async_op=True)
+            inflight.append((b0, b1, P, work))
+        for b0, b1, P, work in inflight:
+            if work is not None:
+                work.wait()
+            self.local.backward_finish_dev(P, amax[b0:b1], G[b0:b1])
         return G
 
 

@@ -89,3 +89,36 @@ def test_sharded_backward_matches_within_one_lsb():
     diff = np.abs(Gf.cpu().numpy() - Gs.cpu().numpy())
     assert np.all(diff <= lsb * 1.001 + 1e-6)
     assert np.mean(diff > 1e-6) < 0.02
+
+
+@pytest.mark.parametrize("prec", [xb.MVM_TF32, xb.MVM_FP32])
+def test_chunked_backward_equals_one_shot(prec):
+    """RowShardedTile.backward in sample chunks (partials issued ahead of
+    their finishes, FIFO) draws the same noise as one call over the batch:
+    G is bit-identical, and the tile's backward counter ends in the same
+    place (a following backward agrees too)."""
+    from paper_2104_02184_b200.parallel import RowShardedTile
+    R, C, B = 192, 160, 256
+    bio = xb.default_io()
+    bio.bound_management = xb.BM_NONE
+    s = xb.TileSettings(device=xb.device_preset("reram_sb"), backward_io=bio, mvm_precision=prec)
+    W = np.random.default_rng(8).uniform(-0.3, 0.3, (R, C)).astype(np.float32)
+    stream = torch.cuda.current_stream()
+    outs = []
+    for chunks in (1, 4, 3):
+        t = xb.AnalogTile(R, C, s, 21)
+        t.set_stream(stream.cuda_stream)
+        t.set_weights(W)
+        sh = RowShardedTile(t, R, C)
+        g = torch.Generator(device="cuda").manual_seed(6)
+        D = torch.rand(B, R, device="cuda", generator=g) * 2 - 1
+        G1 = torch.empty(B, C, device="cuda")
+        G2 = torch.empty(B, C, device="cuda")
+        sh.backward(D, G1, chunks=chunks)
+        sh.backward(D, G2, chunks=1)
+        torch.cuda.synchronize()
+        outs.append((G1.cpu().numpy(), G2.cpu().numpy()))
+    for G1, G2 in outs[1:]:
+        np.testing.assert_array_equal(G1, outs[0][0])
+        np.testing.assert_array_equal(G2, outs[0][1])
+    assert not np.array_equal(outs[0][0], outs[0][1])  # fresh noise per call

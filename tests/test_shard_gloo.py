@@ -65,9 +65,11 @@ def _worker(rank, world, port, W, X, D, out):
     t.update(Xt, Dl, LR)
     G = torch.zeros(B, C, dtype=torch.float64)
     t.backward(Dl, G)
+    G3 = torch.zeros(B, C, dtype=torch.float64)
+    t.backward(Dl, G3, chunks=3)  # three in-flight async all-reduces, finished in order
     Y = torch.zeros(B, r1 - r0, dtype=torch.float64)
     t.forward(Xt, Y)
-    out[rank] = (t.local.W.copy(), G.numpy().copy(), Y.numpy().copy())
+    out[rank] = (t.local.W.copy(), G.numpy().copy(), Y.numpy().copy(), G3.numpy().copy())
     dist.destroy_process_group()
 
 
@@ -104,4 +106,6 @@ def test_two_rank_gloo_matches_unsharded_oracle():
     Wo = o.get_weights()
     np.testing.assert_allclose(out[0][1], D @ Wo, atol=1e-12)  # replicated backward
     np.testing.assert_allclose(out[1][1], D @ Wo, atol=1e-12)
+    np.testing.assert_array_equal(out[0][3], out[0][1])  # chunked = one-shot backward
+    np.testing.assert_array_equal(out[1][3], out[1][1])
     np.testing.assert_allclose(np.hstack([out[0][2], out[1][2]]), X @ Wo.T, atol=1e-12)
