@@ -614,7 +614,9 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
 
     // ---------------- pulse loop: pulse n of every lane with n < T.  Words
     // below the shortest stream need no per-pulse activity test.
-    auto pulses8 = [&](uint32_t word, uint32_t n, int sh8, bool check) {
+    // check: vm holds this lane's valid-pulse bits of the word (a prefix),
+    // tested like the direction bits instead of comparing n + v with T
+    auto pulses8 = [&](uint32_t word, uint32_t n, int sh8, bool check, uint32_t vm) {
       float f[8] = {1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f};
       if (NOISE) factor8_rk(g0 + (n >> 3), jg, ig, call, rk, la.k2, f, cs);
 #pragma unroll
@@ -622,13 +624,13 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
         if (COMP) {
           float hn = w, ln = wlo;
           cell.step2(hn, ln, f[v], ((word >> (sh8 + v)) & 1u) == 0u);
-          if (!check || n + v < T) {
+          if (!check || ((vm >> (sh8 + v)) & 1u)) {
             w = hn;
             wlo = ln;
           }
         } else {
           const float wn = cell.step(w, f[v], ((word >> (sh8 + v)) & 1u) == 0u);
-          if (!check || n + v < T) w = wn;
+          if (!check || ((vm >> (sh8 + v)) & 1u)) w = wn;
         }
       }
       // keep lo below an ulp of hi: its own rounding then stays negligible
@@ -639,14 +641,16 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
     for (; n0 + 32u <= minT; n0 += 32u) {
       const uint32_t word = q[(n0 >> 5) * 32];
 #pragma unroll
-      for (int u4 = 0; u4 < 32; u4 += 8) pulses8(word, n0 + u4, u4, false);
+      for (int u4 = 0; u4 < 32; u4 += 8) pulses8(word, n0 + u4, u4, false, 0u);
     }
     for (; n0 < maxT; n0 += 32u) {
       const uint32_t word = q[(n0 >> 5) * 32];
+      uint32_t vm; // bits [0, T - n0) of this word are pulses of this lane
+      asm("bmsk.clamp.b32 %0, %1, %2;" : "=r"(vm) : "r"(0u), "r"(T > n0 ? T - n0 : 0u));
 #pragma unroll
       for (int u4 = 0; u4 < 32; u4 += 8) {
         if (n0 + u4 >= maxT) break;
-        pulses8(word, n0 + u4, u4, true);
+        pulses8(word, n0 + u4, u4, true, vm);
       }
     }
     g0 += (T + 7u) >> 3;
