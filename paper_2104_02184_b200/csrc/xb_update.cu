@@ -302,16 +302,20 @@ __device__ __forceinline__ void factor_pair16(uint32_t a, float k2, float &f0, f
   const float u = fmaf((float)(a & 0xffffu), 1.52587890625e-05f, 7.62939453125e-06f);
   float l, r, s, c;
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(u));
-  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(l * k2));
 #if XB_BM_TABLE
   // angle (k + 1/2) 2 pi / 1024 from the top 10 bits: one shared-memory load
   // instead of two MUFU ops.  With a symmetric grid of >= 5 angles the moments
   // E[cos^2] = 1/2, E[cos^4] = 3/8, E[cos^2 sin^2] = 1/8 are exact, so z0, z1
   // keep the unit variance, zero cross-correlation and Gaussian kurtosis.
+  // The table holds (cos, sin) * sqrt(2 ln2) std, so the radius is just
+  // sqrt(-lg2 u) (the negation is a MUFU source modifier; no multiply)
+  (void)k2;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(-l));
   const float2 t = cs[a >> 22];
   c = t.x;
   s = t.y;
 #else
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(l * k2));
   (void)cs;
   const float th = fmaf((float)(a >> 16), 9.587379924285257e-05f, -3.1415446284412245f);
   asm("sin.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(th));
@@ -486,7 +490,8 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
     for (int k = threadIdx.x; k < BM_ANGLES; k += blockDim.x) {
       double sn, cn;
       sincospi((2.0 * k + 1.0) / BM_ANGLES, &sn, &cn); // (k + 1/2) 2 pi / 1024
-      cs[k] = make_float2((float)cn, (float)sn);
+      const double r = sqrt(-(double)la.k2);               // sqrt(2 ln2) std
+      cs[k] = make_float2((float)(cn * r), (float)(sn * r));
     }
     __syncthreads();
   }
