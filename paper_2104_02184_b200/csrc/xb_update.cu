@@ -299,11 +299,17 @@ __device__ __forceinline__ void box_muller_fast(uint32_t a, uint32_t b, float &z
 constexpr int BM_ANGLES = 1024; // Box-Muller angles: (cos, sin) table in shared memory
 __device__ __forceinline__ void factor_pair16(uint32_t a, float k2, float &f0, float &f1,
                                               const float2 *__restrict__ cs) {
+#if XB_BM_TABLE
+  // radius from the high half (I2F reads it in place), angle from bits 3..12
+  // (already a byte offset into the 8-byte table entries: one AND)
+  const float u = fmaf((float)(a >> 16), 1.52587890625e-05f, 7.62939453125e-06f);
+#else
   const float u = fmaf((float)(a & 0xffffu), 1.52587890625e-05f, 7.62939453125e-06f);
+#endif
   float l, r, s, c;
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(u));
 #if XB_BM_TABLE
-  // angle (k + 1/2) 2 pi / 1024 from the top 10 bits: one shared-memory load
+  // angle (k + 1/2) 2 pi / 1024 from 10 random bits: one shared-memory load
   // instead of two MUFU ops.  With a symmetric grid of >= 5 angles the moments
   // E[cos^2] = 1/2, E[cos^4] = 3/8, E[cos^2 sin^2] = 1/8 are exact, so z0, z1
   // keep the unit variance, zero cross-correlation and Gaussian kurtosis.
@@ -311,7 +317,8 @@ __device__ __forceinline__ void factor_pair16(uint32_t a, float k2, float &f0, f
   // sqrt(-lg2 u) (the negation is a MUFU source modifier; no multiply)
   (void)k2;
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(-l));
-  const float2 t = cs[a >> 22];
+  const float2 t = *reinterpret_cast<const float2 *>(reinterpret_cast<const char *>(cs) +
+                                                     (a & 0x1ff8u));
   c = t.x;
   s = t.y;
 #else
