@@ -195,7 +195,7 @@ def run_ours(args):
 
     # ---------- e2e through the public host-buffer API (pinned host inputs)
     e2e = None
-    n_e2e = max(2, min(args.steps, 4))
+    n_e2e = max(2, min(args.steps, 10))
     if world == 1:
         # AnalogTile.forward / update with host arrays: H2D, finiteness check,
         # kernels and the D2H of y inside each call
@@ -205,8 +205,9 @@ def run_ours(args):
         e2e_tile.set_weights(w0.cpu().numpy())
         # the result lands in pinned host memory (DMA at full PCIe rate)
         yh = torch.empty(BATCH, N_ROWS, dtype=torch.float32).pin_memory().numpy()
-        e2e_tile.forward(Xh[0], out=yh)  # warm
-        e2e_tile.update(Xh[0], Dh[0], LR)
+        for k in range(2):  # warm
+            e2e_tile.forward(Xh[k], out=yh)
+            e2e_tile.update(Xh[k], Dh[k], LR)
         t0 = time.perf_counter()
         for k in range(n_e2e):
             e2e_tile.forward(Xh[k], out=yh)

@@ -15,7 +15,10 @@ import torch  # noqa: E402
 import paper_2104_02184_b200 as xb  # noqa: E402
 
 N, B, LR = 4096, 256, 0.01
-t = xb.AnalogTile(N, N, xb.TileSettings(device=xb.device_preset("reram_sb")), 3)
+fwd = xb.default_io()
+fwd.bound_management, fwd.bm_max_iter = xb.BM_ITERATIVE, 10
+t = xb.AnalogTile(N, N, xb.TileSettings(device=xb.device_preset("reram_sb"), forward_io=fwd,
+                                        mvm_precision=xb.MVM_TF32), 3)  # the bench's tile
 t.set_weights(np.random.default_rng(7).uniform(-0.1, 0.1, (N, N)).astype(np.float32))
 g = torch.Generator().manual_seed(1)
 X = (torch.rand(B, N, generator=g) * 2 - 1).pin_memory()
@@ -43,3 +46,17 @@ print(f"forward_dev:      {wall(lambda: t.forward_dev(dX, dY)):.3f} ms")
 print(f"forward (host):   {wall(lambda: t.forward(Xn, out=Yn)):.3f} ms")
 print(f"update_dev:       {wall(lambda: t.update_dev(dX, dD, LR)):.3f} ms")
 print(f"update (host):    {wall(lambda: t.update(Xn, Dn, LR)):.3f} ms")
+
+
+def step_host():
+    t.forward(Xn, out=Yn)
+    t.update(Xn, Dn, LR)
+
+
+def step_dev():
+    t.forward_dev(dX, dY)
+    t.update_dev(dX, dD, LR)
+
+
+print(f"step (host API):  {wall(step_host, 20):.3f} ms")
+print(f"step (device):    {wall(step_dev, 20):.3f} ms")
