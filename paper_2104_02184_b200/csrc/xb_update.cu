@@ -71,11 +71,41 @@ void launch_rows_amax(const float *V, int B, int n, int ld, float *out, cudaStre
   XB_CUDA(cudaGetLastError());
 }
 
+// ---- Philox4x32-10 with the 10 round keys precomputed on the host (kernel
+// parameters, i.e. constant-bank operands of the LOP3s): the key schedule
+// costs no instructions.  Used by the trains (Bernoulli slots) and the c2c
+// noise (Box-Muller factors; statistical parity only).
+struct RoundKeys {
+  uint32_t k0[10], k1[10];
+};
+
+static RoundKeys round_keys(Key k) {
+  RoundKeys r;
+  uint32_t a = k.k0, b = k.k1;
+  for (int i = 0; i < 10; ++i) {
+    r.k0[i] = a;
+    r.k1[i] = b;
+    a += 0x9E3779B9u;
+    b += 0xBB67AE85u;
+  }
+  return r;
+}
+
+#ifndef XB_C2C_ROUNDS
+#define XB_C2C_ROUNDS 10
+#endif
+template <int ROUNDS = 10>
+__device__ __forceinline__ void philox10_rk(uint32_t &c0, uint32_t &c1, uint32_t &c2,
+                                            uint32_t &c3, const RoundKeys &rk) {
+#pragma unroll
+  for (int r = 0; r < ROUNDS; ++r) philox_round(c0, c1, c2, c3, rk.k0[r], rk.k1[r]);
+}
+
 // ============================================================== K4: trains
 // Counter of a train draw: (slot group g, global line, seq lo, seq hi ^ side),
 // key = the tile's "update" stream.  Each Philox call gives 4 slots.
-__device__ __forceinline__ uint32_t train_word(float v, double p, int bl, Key key, uint32_t line,
-                                               uint64_t seq, uint32_t side) {
+__device__ __forceinline__ uint32_t train_word(float v, double p, int bl, const RoundKeys &rk,
+                                               uint32_t line, uint64_t seq, uint32_t side) {
   uint32_t bits = 0;
   if (p > 0.0) {
     if (p >= 1.0) {
@@ -85,7 +115,7 @@ __device__ __forceinline__ uint32_t train_word(float v, double p, int bl, Key ke
       const uint32_t c2 = (uint32_t)seq, c3 = (uint32_t)(seq >> 32) ^ side;
       for (int g = 0; g * 4 < bl; ++g) {
         uint32_t a0 = (uint32_t)g, a1 = line, a2 = c2, a3 = c3;
-        philox10(a0, a1, a2, a3, key);
+        philox10_rk(a0, a1, a2, a3, rk);
         const int t = g * 4;
         bits |= (uint32_t)(a0 < thr) << t;
         if (t + 1 < bl) bits |= (uint32_t)(a1 < thr) << (t + 1);
@@ -133,7 +163,7 @@ __global__ void __launch_bounds__(256) trains_kernel(
     const float *__restrict__ X, const float *__restrict__ D, int C, int R, int B,
     const float *__restrict__ lr, float lr_scalar, const float *__restrict__ xm,
     const float *__restrict__ dm, double dw_min, const double *__restrict__ dwmin_b, int BL,
-    int blm, Key key, uint64_t seq0, int row0, uint32_t *__restrict__ xw,
+    int blm, const RoundKeys rk, uint64_t seq0, int row0, uint32_t *__restrict__ xw,
     uint32_t *__restrict__ dw, int ldb, int32_t *__restrict__ bl_out) {
   __shared__ Plan plan[32];
   __shared__ uint32_t tile[32][33];
@@ -155,7 +185,9 @@ __global__ void __launch_bounds__(256) trains_kernel(
   __syncthreads();
   const int line = l0 + lane;
   const float *V = is_x ? X : D;
-  for (int s = warp; s < 32; s += 8) {
+#pragma unroll
+  for (int it = 0; it < 4; ++it) { // 4 independent words per thread: ILP for the Philox chains
+    const int s = warp + 8 * it;
     const int b = b0 + s;
     uint32_t word = 0;
     if (b < B && line < nl) {
@@ -164,8 +196,8 @@ __global__ void __launch_bounds__(256) trains_kernel(
       if (!pl.skip) {
         double p = pl.amp * fabs((double)v) * (is_x ? pl.x_scale : pl.d_scale);
         p = (p < 1.0) ? p : 1.0;
-        word = is_x ? train_word(v, p, pl.bl, key, (uint32_t)line, seq0 + b, 0u)
-                    : train_word(v, p, pl.bl, key, (uint32_t)(row0 + line), seq0 + b,
+        word = is_x ? train_word(v, p, pl.bl, rk, (uint32_t)line, seq0 + b, 0u)
+                    : train_word(v, p, pl.bl, rk, (uint32_t)(row0 + line), seq0 + b,
                                  0x80000000u);
       }
     }
@@ -225,7 +257,7 @@ void launch_trains(const Tile &t, const float *X, const float *D, int B, const f
     dim3 grid((t.C + 31) / 32 + (t.R + 31) / 32, (B + 31) / 32);
     trains_kernel<<<grid, 256, 0, t.stream>>>(X, D, t.C, t.R, B, lr_dev, lr_scalar, xm, dm,
                                               t.cfg.device.dw_min, dwmin_b, t.cfg.update.bl,
-                                              t.cfg.update.bl_management, t.k_upd, seq0, t.row0,
+                                              t.cfg.update.bl_management, round_keys(t.k_upd), seq0, t.row0,
                                               xw, dw, ldb, bl);
   }
   count_launch();
@@ -246,35 +278,6 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 
 
-// ---- c2c noise: Philox4x32-10 with the 10 round keys precomputed on the host
-// (kernel parameters, i.e. constant-bank operands of the LOP3s) and a
-// MUFU-based Box-Muller on 24-bit uniforms.  Statistical parity only; the
-// radius uses u in (0, 1], so the tail extends to sqrt(2 ln 2^24) = 5.8 sigma.
-struct RoundKeys {
-  uint32_t k0[10], k1[10];
-};
-
-static RoundKeys round_keys(Key k) {
-  RoundKeys r;
-  uint32_t a = k.k0, b = k.k1;
-  for (int i = 0; i < 10; ++i) {
-    r.k0[i] = a;
-    r.k1[i] = b;
-    a += 0x9E3779B9u;
-    b += 0xBB67AE85u;
-  }
-  return r;
-}
-
-#ifndef XB_C2C_ROUNDS
-#define XB_C2C_ROUNDS 10
-#endif
-__device__ __forceinline__ void philox10_rk(uint32_t &c0, uint32_t &c1, uint32_t &c2,
-                                            uint32_t &c3, const RoundKeys &rk) {
-#pragma unroll
-  for (int r = 0; r < XB_C2C_ROUNDS; ++r) philox_round(c0, c1, c2, c3, rk.k0[r], rk.k1[r]);
-}
-
 __device__ __forceinline__ void box_muller_fast(uint32_t a, uint32_t b, float &z0, float &z1) {
   // u in (0, 1] and theta in [-pi, pi) straight from the mantissa bits
   const float u = 2.0f - __int_as_float(0x3f800000u | (a >> 9));
@@ -289,9 +292,9 @@ __device__ __forceinline__ void box_muller_fast(uint32_t a, uint32_t b, float &z
   z1 = r * s;
 }
 
-// c2c factors f = 1 + std z directly: std folds into the Box-Muller radius,
-// r = sqrt(-2 std^2 ln u) = sqrt(lg2(u) * k2) with k2 = -2 ln2 std^2, so each
-// factor is one FMA (1 + r cos) instead of a multiply and an FMA
+// c2c factors f = 1 + std z directly: std folds into the Box-Muller radius
+// (table path: into the (cos, sin) table; else r = sqrt(lg2(u) * k2) with
+// k2 = -2 ln2 std^2), so each factor is one FMA (1 + r cos)
 // (an IMAD-only int->float variant measured 12 % slower: the XU has room for I2F)
 #ifndef XB_BM_TABLE
 #define XB_BM_TABLE 1
@@ -335,7 +338,7 @@ __device__ __forceinline__ void factor_pair16(uint32_t a, float k2, float &f0, f
 __device__ __forceinline__ void factor8_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
                                            const RoundKeys &rk, float k2, float *f,
                                            const float2 *__restrict__ cs) {
-  philox10_rk(c0, c1, c2, c3, rk);
+  philox10_rk<XB_C2C_ROUNDS>(c0, c1, c2, c3, rk);
   factor_pair16(c0, k2, f[0], f[1], cs);
   factor_pair16(c1, k2, f[2], f[3], cs);
   factor_pair16(c2, k2, f[4], f[5], cs);
