@@ -207,3 +207,22 @@ def test_errors_match_oracle(restatement):
         with pytest.raises(xb.Error) as eg:
             g()
         assert str(eg.value) == str(eo.value)
+
+
+def test_eight_members_all_together():
+    """The largest cell (XB_MAX_CELL_DEVICES = 8), gains of both signs: every
+    member fires the same trains, negative gains flipped, so on identical
+    noise-free devices W_k = sign(g_k) W_0 and W_eff = sum |g_k| W_0."""
+    dw = 2.0 ** -10
+    gains = [1.0, -0.5, 0.25, -2.0, 0.75, -1.0, 1.5, -0.25]
+    u = cell([const_dev(dw) for _ in gains], gains, xb.UC_ALL_TOGETHER, shape=(40, 36))
+    assert u.n_members() == 8
+    rng = np.random.default_rng(16)
+    X = rng.uniform(-1, 1, (24, 36)).astype(np.float32)
+    D = rng.uniform(-1, 1, (24, 40)).astype(np.float32)
+    u.update(X, D, 0.02)
+    w0 = u.member(0).get_weights()
+    assert np.abs(w0).max() > 0
+    for k, gk in enumerate(gains):
+        np.testing.assert_array_equal(u.member(k).get_weights(), np.sign(gk) * w0)
+    np.testing.assert_allclose(u.get_weights(), sum(abs(g) for g in gains) * w0, rtol=1e-6)
