@@ -255,7 +255,8 @@ struct Finite {
   size_t n;
   const char *what;
 };
-static void check_finite_dev(Tile &t, std::initializer_list<Finite> arrays) {
+// launch half: the flag bits land in t.chk_dev (stream order), nothing waits
+static void launch_finite_dev(Tile &t, std::initializer_list<Finite> arrays) {
   if (!t.chk_dev) {
     XB_CUDA(cudaMalloc(&t.chk_dev, sizeof(int)));
     XB_CUDA(cudaMallocHost(&t.chk_host, sizeof(int)));
@@ -266,13 +267,22 @@ static void check_finite_dev(Tile &t, std::initializer_list<Finite> arrays) {
     launch_nonfinite(a.v, a.n, bit, t.chk_dev, t.stream);
     bit <<= 1;
   }
+}
+
+// read half: one 4-byte read and a stream sync; raises for the first bad array
+static void raise_if_nonfinite(Tile &t, std::initializer_list<Finite> arrays) {
   XB_CUDA(cudaMemcpyAsync(t.chk_host, t.chk_dev, sizeof(int), cudaMemcpyDeviceToHost, t.stream));
   sync(t);
-  bit = 1;
+  int bit = 1;
   for (const Finite &a : arrays) {
     if (*t.chk_host & bit) raise(std::string(a.what) + ": non-finite entry");
     bit <<= 1;
   }
+}
+
+static void check_finite_dev(Tile &t, std::initializer_list<Finite> arrays) {
+  launch_finite_dev(t, arrays);
+  raise_if_nonfinite(t, arrays);
 }
 
 static void ensure_xi(Tile &t) {
@@ -894,10 +904,35 @@ int xb_tile_update(xb_tile *h, const float *X, const float *D, int B, const floa
     float *dD = dX + (size_t)B * t.C;
     XB_CUDA(cudaMemcpyAsync(dX, X, sizeof(float) * B * t.C, cudaMemcpyHostToDevice, t.stream));
     XB_CUDA(cudaMemcpyAsync(dD, D, sizeof(float) * B * t.R, cudaMemcpyHostToDevice, t.stream));
-    check_finite_dev(t, {{dX, (size_t)B * t.C, "update(x)"}, {dD, (size_t)B * t.R, "update(d)"}});
-    check_lr_host(X, D, B, t.C, t.R, lr, t.learning_rate);
-    update_device(t, dX, dD, B, lr, nullptr, false, nullptr, nullptr, nullptr);
-    sync(t);
+    const std::initializer_list<Finite> in = {{dX, (size_t)B * t.C, "update(x)"},
+                                              {dD, (size_t)B * t.R, "update(d)"}};
+    launch_finite_dev(t, in);
+    try {
+      check_lr_host(X, D, B, t.C, t.R, lr, t.learning_rate);
+    } catch (...) { // check_input (tile.cpp:98-99) comes before translate's lr check
+      raise_if_nonfinite(t, in);
+      throw;
+    }
+    // no host round trip before the launch: the pulse kernel reads the
+    // finiteness flag itself and leaves the tile untouched if it is set;
+    // the host counters are rolled back and the error raised after the sync
+    const uint64_t seq_upd = t.seq_upd;
+    const uint32_t calls = t.upd_calls;
+    t.abort_flag = t.chk_dev;
+    try {
+      update_device(t, dX, dD, B, lr, nullptr, false, nullptr, nullptr, nullptr);
+    } catch (...) {
+      t.abort_flag = nullptr;
+      throw;
+    }
+    t.abort_flag = nullptr;
+    try {
+      raise_if_nonfinite(t, in);
+    } catch (...) {
+      t.seq_upd = seq_upd;
+      t.upd_calls = calls;
+      throw;
+    }
   });
 }
 

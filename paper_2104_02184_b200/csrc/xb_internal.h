@@ -59,6 +59,10 @@ struct Tile {
   Key k_fwd{}, k_bwd{}, k_upd{}, k_c2c{}, k_realize{}, k_temporal{}, k_tinit{};
   uint64_t seq_fwd = 0, seq_bwd = 0, seq_upd = 0; // samples drawn so far per stream
   uint64_t bwd_pending = 0; // samples of backward partials not finished yet (FIFO)
+  // device int the pulse kernels read first: nonzero = skip (the host update
+  // path points it at the finiteness flag so the weights stay untouched
+  // without a host round trip before the launch); nullptr = always run
+  const int *abort_flag = nullptr;
   uint32_t upd_calls = 0, temporal_calls = 0;
 
   float *W = nullptr;      // [R][ld] fp32 weights

@@ -491,8 +491,10 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
     float *__restrict__ W, float *__restrict__ Wlo, const float4 *__restrict__ P, int ld, int R,
     int C,
     const uint32_t *__restrict__ xw, const uint32_t *__restrict__ dw, int ldb, int B, int row0,
-    LawArgs la, RoundKeys rk, uint32_t call, uint32_t two, uint32_t flip) {
+    LawArgs la, RoundKeys rk, uint32_t call, uint32_t two, uint32_t flip,
+    const int *__restrict__ abort_flag) {
   extern __shared__ uint32_t qsm[]; // [PULSE_WARPS][PULSE_QW][32] streams, then the angle table
+  if (abort_flag && *abort_flag) return; // rejected input: the tile stays untouched
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t *q = qsm + warp * (PULSE_QW * 32) + lane;
   float2 *cs = reinterpret_cast<float2 *>(qsm + PULSE_WARPS * PULSE_QW * 32);
@@ -704,7 +706,7 @@ static void pulse_dispatch(Tile &t, const uint32_t *xw, const uint32_t *dw, int 
   }
   pulse_kernel<LAW, NOISE, COMP><<<grid, PULSE_WARPS * 32, smem, t.stream>>>(
       t.W, t.Wlo, t.P, t.ld, t.R, t.C, xw, dw, ldb, B, t.row0, la, round_keys(t.k_c2c), call, 2u,
-      flip ? 0x80000000u : 0u);
+      flip ? 0x80000000u : 0u, t.abort_flag);
   count_launch();
   XB_CUDA(cudaGetLastError());
 }
@@ -769,7 +771,9 @@ template <int LAW, bool NOISE, bool COMP>
 __global__ void __launch_bounds__(256) pulse_det_kernel(
     float *__restrict__ W, float *__restrict__ Wlo, const float4 *__restrict__ P, int ld, int R,
     int C, const double *__restrict__ px, const double *__restrict__ pd,
-    const int32_t *__restrict__ bl, int B, int row0, LawArgs la, Key key, uint32_t call) {
+    const int32_t *__restrict__ bl, int B, int row0, LawArgs la, Key key, uint32_t call,
+    const int *__restrict__ abort_flag) {
+  if (abort_flag && *abort_flag) return; // rejected input: the tile stays untouched
   const int j = blockIdx.x * 32 + (threadIdx.x & 31);
   const int i = blockIdx.y * 8 + (threadIdx.x >> 5);
   if (i >= R || j >= C) return;
@@ -808,7 +812,7 @@ static void det_dispatch(Tile &t, const double *px, const double *pd, const int3
                          LawArgs la, uint32_t call) {
   dim3 grid((t.C + 31) / 32, (t.R + 7) / 8);
   pulse_det_kernel<LAW, NOISE, COMP><<<grid, 256, 0, t.stream>>>(
-      t.W, t.Wlo, t.P, t.ld, t.R, t.C, px, pd, bl, B, t.row0, la, t.k_c2c, call);
+      t.W, t.Wlo, t.P, t.ld, t.R, t.C, px, pd, bl, B, t.row0, la, t.k_c2c, call, t.abort_flag);
   count_launch();
   XB_CUDA(cudaGetLastError());
 }
