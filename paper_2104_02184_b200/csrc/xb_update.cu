@@ -299,7 +299,13 @@ __device__ __forceinline__ void box_muller_fast(uint32_t a, uint32_t b, float &z
 #ifndef XB_BM_TABLE
 #define XB_BM_TABLE 1
 #endif
-constexpr int BM_ANGLES = 1024; // Box-Muller angles: (cos, sin) table in shared memory
+// XB_BM_PACK3: four Box-Muller pairs (8 factors) from THREE Philox words --
+// 16-bit radius + 8-bit angle per pair -- so a 32-pulse stream word needs 3
+// Philox calls instead of 4; angles on a 256-point grid (moments still exact)
+#ifndef XB_BM_PACK3
+#define XB_BM_PACK3 1
+#endif
+constexpr int BM_ANGLES = XB_BM_PACK3 ? 256 : 1024; // (cos, sin) table in shared memory
 __device__ __forceinline__ void factor_pair16(uint32_t a, float k2, float &f0, float &f1,
                                               const float2 *__restrict__ cs) {
 #if XB_BM_TABLE
@@ -333,6 +339,31 @@ __device__ __forceinline__ void factor_pair16(uint32_t a, float k2, float &f0, f
 #endif
   f0 = fmaf(r, c, 1.0f);
   f1 = fmaf(r, s, 1.0f);
+}
+
+// one pair from a 16-bit radius (as float) and an angle byte offset into the
+// table (entries (cos, sin) * sqrt(2 ln2) std, see factor_pair16)
+__device__ __forceinline__ void factor_pair_rt(float k16, uint32_t off,
+                                               const float2 *__restrict__ cs, float &f0,
+                                               float &f1) {
+  const float u = fmaf(k16, 1.52587890625e-05f, 7.62939453125e-06f);
+  float l, r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(u));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(-l));
+  const float2 t =
+      *reinterpret_cast<const float2 *>(reinterpret_cast<const char *>(cs) + off);
+  f0 = fmaf(r, t.x, 1.0f);
+  f1 = fmaf(r, t.y, 1.0f);
+}
+
+// 8 factors from 3 words: radii a.hi, b.hi, c.hi, c.lo (I2F reads the halves in
+// place); angles a.byte0, a.byte1, b.byte0, b.byte1 as byte offsets (x 8)
+__device__ __forceinline__ void factor8_3w(uint32_t a, uint32_t b, uint32_t c,
+                                           const float2 *__restrict__ cs, float *f) {
+  factor_pair_rt((float)(a >> 16), (a << 3) & 0x7f8u, cs, f[0], f[1]);
+  factor_pair_rt((float)(b >> 16), (a >> 5) & 0x7f8u, cs, f[2], f[3]);
+  factor_pair_rt((float)(c >> 16), (b << 3) & 0x7f8u, cs, f[4], f[5]);
+  factor_pair_rt((float)(c & 0xffffu), (b >> 5) & 0x7f8u, cs, f[6], f[7]);
 }
 
 __device__ __forceinline__ void factor8_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
@@ -501,7 +532,7 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
   if (NOISE && XB_BM_TABLE) {
     for (int k = threadIdx.x; k < BM_ANGLES; k += blockDim.x) {
       double sn, cn;
-      sincospi((2.0 * k + 1.0) / BM_ANGLES, &sn, &cn); // (k + 1/2) 2 pi / 1024
+      sincospi((2.0 * k + 1.0) / BM_ANGLES, &sn, &cn); // (k + 1/2) 2 pi / BM_ANGLES
       const double r = sqrt(-(double)la.k2);               // sqrt(2 ln2) std
       cs[k] = make_float2((float)(cn * r), (float)(sn * r));
     }
@@ -633,9 +664,7 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
     // below the shortest stream need no per-pulse activity test.
     // check: vm holds this lane's valid-pulse bits of the word (a prefix),
     // tested like the direction bits instead of comparing n + v with T
-    auto pulses8 = [&](uint32_t word, uint32_t n, int sh8, bool check, uint32_t vm) {
-      float f[8] = {1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f};
-      if (NOISE) factor8_rk(g0 + (n >> 3), jg, ig, call, rk, la.k2, f, cs);
+    auto apply8 = [&](uint32_t word, int sh8, bool check, uint32_t vm, const float *f) {
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
         if (COMP) {
@@ -654,6 +683,52 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
       // (left to grow, lo collects a systematic error of its own)
       if (COMP) renorm2(w, wlo);
     };
+#if XB_BM_PACK3
+    // one 32-pulse stream word: Philox calls g0 + 3 m + {0, 1, 2} (m = word
+    // index) give 12 words, three per 8-pulse block; `lim` (warp-uniform)
+    // cuts the ragged last word
+    auto word32 = [&](uint32_t word, uint32_t n0, bool check, uint32_t vm, uint32_t lim) {
+      float f[8] = {1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f};
+      uint32_t p0 = 0, p1 = 0, p2 = 0, p3 = 0, r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+      const uint32_t base = g0 + 3u * (n0 >> 5);
+      if (NOISE) {
+        p0 = base, p1 = jg, p2 = ig, p3 = call;
+        philox10_rk<XB_C2C_ROUNDS>(p0, p1, p2, p3, rk);
+        factor8_3w(p0, p1, p2, cs, f);
+      }
+      apply8(word, 0, check, vm, f);
+      if (lim <= 8u) return;
+      if (NOISE) {
+        r0 = base + 1u, r1 = jg, r2 = ig, r3 = call;
+        philox10_rk<XB_C2C_ROUNDS>(r0, r1, r2, r3, rk);
+        factor8_3w(p3, r0, r1, cs, f);
+      }
+      apply8(word, 8, check, vm, f);
+      if (lim <= 16u) return;
+      if (NOISE) {
+        p0 = base + 2u, p1 = jg, p2 = ig, p3 = call;
+        philox10_rk<XB_C2C_ROUNDS>(p0, p1, p2, p3, rk);
+        factor8_3w(r2, r3, p0, cs, f);
+      }
+      apply8(word, 16, check, vm, f);
+      if (lim <= 24u) return;
+      if (NOISE) factor8_3w(p1, p2, p3, cs, f);
+      apply8(word, 24, check, vm, f);
+    };
+    uint32_t n0 = 0;
+    for (; n0 + 32u <= minT; n0 += 32u) word32(q[(n0 >> 5) * 32], n0, false, 0u, 32u);
+    for (; n0 < maxT; n0 += 32u) {
+      uint32_t vm; // bits [0, T - n0) of this word are pulses of this lane
+      asm("bmsk.clamp.b32 %0, %1, %2;" : "=r"(vm) : "r"(0u), "r"(T > n0 ? T - n0 : 0u));
+      word32(q[(n0 >> 5) * 32], n0, true, vm, maxT - n0);
+    }
+    g0 += 3u * ((T + 31u) >> 5);
+#else
+    auto pulses8 = [&](uint32_t word, uint32_t n, int sh8, bool check, uint32_t vm) {
+      float f[8] = {1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f};
+      if (NOISE) factor8_rk(g0 + (n >> 3), jg, ig, call, rk, la.k2, f, cs);
+      apply8(word, sh8, check, vm, f);
+    };
     uint32_t n0 = 0;
     for (; n0 + 32u <= minT; n0 += 32u) {
       const uint32_t word = q[(n0 >> 5) * 32];
@@ -671,6 +746,7 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
       }
     }
     g0 += (T + 7u) >> 3;
+#endif
     __syncwarp();
   }
   if (COMP) renorm2(w, wlo);
