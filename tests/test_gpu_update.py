@@ -309,7 +309,7 @@ def test_c2c_single_pulse_distribution(kind):
     step at w = 0 (dw_min for ConstantStep), so the 262 144 cells sample the
     c2c factor directly.  z must be a standard normal: mean, variance,
     skewness and kurtosis within 5 standard errors, and a Kolmogorov-Smirnov
-    distance below 5/sqrt(n) (the 16-bit radius and the 1024-angle
+    distance below 5/sqrt(n) (the 16-bit radius and the 256-angle
     Box-Muller grid are invisible at this sample size)."""
     from math import erf, sqrt
     dev = xb.default_device()
