@@ -363,7 +363,7 @@ __device__ __forceinline__ void factor8_3w(uint32_t a, uint32_t b, uint32_t c,
   factor_pair_rt((float)(a >> 16), (a << 3) & 0x7f8u, cs, f[0], f[1]);
   factor_pair_rt((float)(b >> 16), (a >> 5) & 0x7f8u, cs, f[2], f[3]);
   factor_pair_rt((float)(c >> 16), (b << 3) & 0x7f8u, cs, f[4], f[5]);
-  factor_pair_rt((float)(c & 0xffffu), (b >> 5) & 0x7f8u, cs, f[6], f[7]);
+  factor_pair_rt((float)(unsigned short)c, (b >> 5) & 0x7f8u, cs, f[6], f[7]);
 }
 
 __device__ __forceinline__ void factor8_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
