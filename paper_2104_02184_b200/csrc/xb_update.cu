@@ -268,7 +268,7 @@ void launch_trains(const Tile &t, const float *X, const float *D, int B, const f
 // proj/src/device.cpp:48-77; see WCell below for the per-pulse arithmetic.
 struct LawArgs {
   float slope, gamma, std;
-  float k2; // -2 ln2 std^2: the c2c radius factor of factor8_rk
+  float k2; // -2 ln2 std^2 (the angle table holds sqrt(-k2) (cos, sin))
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -292,57 +292,20 @@ __device__ __forceinline__ void box_muller_fast(uint32_t a, uint32_t b, float &z
   z1 = r * s;
 }
 
-// c2c factors f = 1 + std z directly: std folds into the Box-Muller radius
-// (table path: into the (cos, sin) table; else r = sqrt(lg2(u) * k2) with
-// k2 = -2 ln2 std^2), so each factor is one FMA (1 + r cos)
+// c2c factors f = 1 + std z directly.  Box-Muller with the angle from a
+// (cos, sin) table in shared memory (one LDS.64 instead of two MUFU ops) whose
+// entries are pre-scaled by sqrt(2 ln2) std, so the radius is sqrt(-lg2 u)
+// (the negation is a MUFU source modifier) and each factor one FMA, 1 + r cos.
+// On a symmetric grid of >= 5 angles the moments E[cos^2] = 1/2, E[cos^4] =
+// 3/8, E[cos^2 sin^2] = 1/8 are exact, so the factors keep unit variance, zero
+// cross-correlation and Gaussian kurtosis.  Four pairs (8 factors) come from
+// THREE Philox words -- 16-bit radius + 8-bit angle per pair -- so a 32-pulse
+// stream word needs 3 Philox calls instead of 4.
 // (an IMAD-only int->float variant measured 12 % slower: the XU has room for I2F)
-#ifndef XB_BM_TABLE
-#define XB_BM_TABLE 1
-#endif
-// XB_BM_PACK3: four Box-Muller pairs (8 factors) from THREE Philox words --
-// 16-bit radius + 8-bit angle per pair -- so a 32-pulse stream word needs 3
-// Philox calls instead of 4; angles on a 256-point grid (moments still exact)
-#ifndef XB_BM_PACK3
-#define XB_BM_PACK3 1
-#endif
-constexpr int BM_ANGLES = XB_BM_PACK3 ? 256 : 1024; // (cos, sin) table in shared memory
-__device__ __forceinline__ void factor_pair16(uint32_t a, float k2, float &f0, float &f1,
-                                              const float2 *__restrict__ cs) {
-#if XB_BM_TABLE
-  // radius from the high half (I2F reads it in place), angle from bits 3..12
-  // (already a byte offset into the 8-byte table entries: one AND)
-  const float u = fmaf((float)(a >> 16), 1.52587890625e-05f, 7.62939453125e-06f);
-#else
-  const float u = fmaf((float)(a & 0xffffu), 1.52587890625e-05f, 7.62939453125e-06f);
-#endif
-  float l, r, s, c;
-  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(u));
-#if XB_BM_TABLE
-  // angle (k + 1/2) 2 pi / 1024 from 10 random bits: one shared-memory load
-  // instead of two MUFU ops.  With a symmetric grid of >= 5 angles the moments
-  // E[cos^2] = 1/2, E[cos^4] = 3/8, E[cos^2 sin^2] = 1/8 are exact, so z0, z1
-  // keep the unit variance, zero cross-correlation and Gaussian kurtosis.
-  // The table holds (cos, sin) * sqrt(2 ln2) std, so the radius is just
-  // sqrt(-lg2 u) (the negation is a MUFU source modifier; no multiply)
-  (void)k2;
-  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(-l));
-  const float2 t = *reinterpret_cast<const float2 *>(reinterpret_cast<const char *>(cs) +
-                                                     (a & 0x1ff8u));
-  c = t.x;
-  s = t.y;
-#else
-  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(l * k2));
-  (void)cs;
-  const float th = fmaf((float)(a >> 16), 9.587379924285257e-05f, -3.1415446284412245f);
-  asm("sin.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(th));
-  asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(th));
-#endif
-  f0 = fmaf(r, c, 1.0f);
-  f1 = fmaf(r, s, 1.0f);
-}
+constexpr int BM_ANGLES = 256; // (cos, sin) table entries in shared memory
 
 // one pair from a 16-bit radius (as float) and an angle byte offset into the
-// table (entries (cos, sin) * sqrt(2 ln2) std, see factor_pair16)
+// table (entries (cos, sin) * sqrt(2 ln2) std)
 __device__ __forceinline__ void factor_pair_rt(float k16, uint32_t off,
                                                const float2 *__restrict__ cs, float &f0,
                                                float &f1) {
@@ -366,15 +329,6 @@ __device__ __forceinline__ void factor8_3w(uint32_t a, uint32_t b, uint32_t c,
   factor_pair_rt((float)(unsigned short)c, (b >> 5) & 0x7f8u, cs, f[6], f[7]);
 }
 
-__device__ __forceinline__ void factor8_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
-                                           const RoundKeys &rk, float k2, float *f,
-                                           const float2 *__restrict__ cs) {
-  philox10_rk<XB_C2C_ROUNDS>(c0, c1, c2, c3, rk);
-  factor_pair16(c0, k2, f[0], f[1], cs);
-  factor_pair16(c1, k2, f[2], f[3], cs);
-  factor_pair16(c2, k2, f[4], f[5], cs);
-  factor_pair16(c3, k2, f[6], f[7], cs);
-}
 
 
 __device__ __forceinline__ void normal4_fast(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
@@ -506,16 +460,6 @@ constexpr int PULSE_WARPS = XB_PULSE_WARPS;
 #ifndef XB_PULSE_PB
 #define XB_PULSE_PB 8
 #endif
-// persistent warps walk the (row, column block) items: warps drift out of
-// phase, so the ALU-bound pre-pass of some overlaps the FMA/MUFU-bound pulse
-// loop of others (warps of a per-tile CTA grid run the two phases in lockstep)
-#ifndef XB_PULSE_PERSIST
-#define XB_PULSE_PERSIST 1
-#endif
-#ifndef XB_PULSE_COLMAJOR
-#define XB_PULSE_COLMAJOR 1
-#endif
-template <int LAW> constexpr bool pulse_persist() { return XB_PULSE_PERSIST != 0; }
 
 template <int LAW, bool NOISE, bool COMP>
 __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
@@ -529,7 +473,7 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t *q = qsm + warp * (PULSE_QW * 32) + lane;
   float2 *cs = reinterpret_cast<float2 *>(qsm + PULSE_WARPS * PULSE_QW * 32);
-  if (NOISE && XB_BM_TABLE) {
+  if (NOISE) {
     for (int k = threadIdx.x; k < BM_ANGLES; k += blockDim.x) {
       double sn, cn;
       sincospi((2.0 * k + 1.0) / BM_ANGLES, &sn, &cn); // (k + 1/2) 2 pi / BM_ANGLES
@@ -538,31 +482,19 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
     }
     __syncthreads();
   }
-  // persistent warps (pulse_persist): each walks (row, 32-column block) items
-  // with a stride of the whole grid; otherwise one item per warp of a 2-D grid
-  constexpr bool persist = pulse_persist<LAW>();
+  // persistent warps: each walks (row, 32-column block) items with a stride
+  // of the whole grid, column-block major -- the warps of a CTA take
+  // consecutive rows of ONE 32-column block, so they read the same x train
+  // words (L1 hits) and the L2 sees each x word once per CTA, not per row.
+  // Warps drift out of phase, so the ALU/FMA-bound pre-pass of some overlaps
+  // the pulse loop of others.
   const uint32_t ncb = (uint32_t)(C + 31) / 32u;
-  const uint32_t n_items = persist ? (uint32_t)R * ncb : 1u; // < 2^31 for any tile that fits
-  for (uint32_t item = persist ? blockIdx.x * PULSE_WARPS + warp : 0u; item < n_items;
+  const uint32_t n_items = (uint32_t)R * ncb; // < 2^31 for any tile that fits
+  for (uint32_t item = blockIdx.x * PULSE_WARPS + warp; item < n_items;
        item += gridDim.x * PULSE_WARPS) {
-    int i, j;
-    if (persist) {
-#if XB_PULSE_COLMAJOR
-      // column-block major: the warps of a CTA take consecutive rows of ONE
-      // 32-column block, so they read the same x train words (L1 hits) and
-      // the L2 sees each x word once per CTA instead of once per row
-      const uint32_t cb = item / (uint32_t)R;
-      i = (int)(item - cb * (uint32_t)R);
-      j = (int)cb * 32 + lane;
-#else
-      i = (int)(item / ncb);
-      j = (int)(item - (uint32_t)i * ncb) * 32 + lane;
-#endif
-    } else {
-      j = blockIdx.x * 32 + lane;
-      i = blockIdx.y * PULSE_WARPS + warp;
-      if (i >= R) return; // warp-uniform: no block-level barriers below
-    }
+  const uint32_t cb = item / (uint32_t)R;
+  const int i = (int)(item - cb * (uint32_t)R);
+  const int j = (int)cb * 32 + lane;
   const bool valid = j < C;
   const size_t idx = (size_t)i * ld + j;
 
@@ -683,7 +615,6 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
       // (left to grow, lo collects a systematic error of its own)
       if (COMP) renorm2(w, wlo);
     };
-#if XB_BM_PACK3
     // one 32-pulse stream word: Philox calls g0 + 3 m + {0, 1, 2} (m = word
     // index) give 12 words, three per 8-pulse block; `lim` (warp-uniform)
     // cuts the ragged last word
@@ -723,30 +654,6 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
       word32(q[(n0 >> 5) * 32], n0, true, vm, maxT - n0);
     }
     g0 += 3u * ((T + 31u) >> 5);
-#else
-    auto pulses8 = [&](uint32_t word, uint32_t n, int sh8, bool check, uint32_t vm) {
-      float f[8] = {1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f};
-      if (NOISE) factor8_rk(g0 + (n >> 3), jg, ig, call, rk, la.k2, f, cs);
-      apply8(word, sh8, check, vm, f);
-    };
-    uint32_t n0 = 0;
-    for (; n0 + 32u <= minT; n0 += 32u) {
-      const uint32_t word = q[(n0 >> 5) * 32];
-#pragma unroll
-      for (int u4 = 0; u4 < 32; u4 += 8) pulses8(word, n0 + u4, u4, false, 0u);
-    }
-    for (; n0 < maxT; n0 += 32u) {
-      const uint32_t word = q[(n0 >> 5) * 32];
-      uint32_t vm; // bits [0, T - n0) of this word are pulses of this lane
-      asm("bmsk.clamp.b32 %0, %1, %2;" : "=r"(vm) : "r"(0u), "r"(T > n0 ? T - n0 : 0u));
-#pragma unroll
-      for (int u4 = 0; u4 < 32; u4 += 8) {
-        if (n0 + u4 >= maxT) break;
-        pulses8(word, n0 + u4, u4, true, vm);
-      }
-    }
-    g0 += (T + 7u) >> 3;
-#endif
     __syncwarp();
   }
   if (COMP) renorm2(w, wlo);
@@ -759,27 +666,25 @@ template <int LAW, bool NOISE, bool COMP>
 static void pulse_dispatch(Tile &t, const uint32_t *xw, const uint32_t *dw, int ldb, int B,
                            LawArgs la, uint32_t call, bool flip) {
   const int smem = PULSE_WARPS * PULSE_QW * 32 * (int)sizeof(uint32_t) +
-                   (NOISE && XB_BM_TABLE ? BM_ANGLES * (int)sizeof(float2) : 0);
+                   (NOISE ? BM_ANGLES * (int)sizeof(float2) : 0);
   static bool configured = false;
   if (!configured) {
     XB_CUDA(cudaFuncSetAttribute(pulse_kernel<LAW, NOISE, COMP>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
-  dim3 grid((t.C + 31) / 32, (t.R + PULSE_WARPS - 1) / PULSE_WARPS);
-  if (pulse_persist<LAW>()) {
-    static int blocks = 0;
-    if (!blocks) {
-      int per_sm = 0, dev = 0, sms = 0;
-      XB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pulse_kernel<LAW, NOISE, COMP>,
-                                                            PULSE_WARPS * 32, smem));
-      XB_CUDA(cudaGetDevice(&dev));
-      XB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      blocks = std::max(1, per_sm) * sms;
-    }
-    const long items = (long)t.R * ((t.C + 31) / 32);
-    grid = dim3((unsigned)std::min<long>(blocks, (items + PULSE_WARPS - 1) / PULSE_WARPS));
+  // persistent grid: every resident CTA slot of the device, capped by the work
+  static int blocks = 0;
+  if (!blocks) {
+    int per_sm = 0, dev = 0, sms = 0;
+    XB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pulse_kernel<LAW, NOISE, COMP>,
+                                                          PULSE_WARPS * 32, smem));
+    XB_CUDA(cudaGetDevice(&dev));
+    XB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    blocks = std::max(1, per_sm) * sms;
   }
+  const long items = (long)t.R * ((t.C + 31) / 32);
+  const dim3 grid((unsigned)std::min<long>(blocks, (items + PULSE_WARPS - 1) / PULSE_WARPS));
   pulse_kernel<LAW, NOISE, COMP><<<grid, PULSE_WARPS * 32, smem, t.stream>>>(
       t.W, t.Wlo, t.P, t.ld, t.R, t.C, xw, dw, ldb, B, t.row0, la, round_keys(t.k_c2c), call, 2u,
       flip ? 0x80000000u : 0u, t.abort_flag);
