@@ -285,6 +285,24 @@ static void check_finite_dev(Tile &t, std::initializer_list<Finite> arrays) {
   raise_if_nonfinite(t, arrays);
 }
 
+// Small host inputs (cfg1/cfg2-sized calls) are scanned on the host before
+// the copy: cheaper than a kernel, a 4-byte read and a stream sync.  Same
+// test (exponent all ones = Inf/NaN), same order, same messages.
+constexpr size_t kHostCheckMax = size_t(1) << 16; // floats over all arrays of a call
+
+static bool host_check_small(std::initializer_list<Finite> host_arrays) {
+  size_t n = 0;
+  for (const Finite &a : host_arrays) n += a.n;
+  if (n > kHostCheckMax) return false;
+  for (const Finite &a : host_arrays) {
+    const uint32_t *u = reinterpret_cast<const uint32_t *>(a.v);
+    uint32_t bad = 0;
+    for (size_t i = 0; i < a.n; ++i) bad |= ((u[i] & 0x7f800000u) == 0x7f800000u);
+    if (bad) raise(std::string(a.what) + ": non-finite entry");
+  }
+  return true;
+}
+
 static void ensure_xi(Tile &t) {
   if (t.xi) return;
   XB_CUDA(cudaMalloc(&t.xi, std::max<size_t>(3 * (size_t)t.R * t.ld, 1) * sizeof(float)));
@@ -804,8 +822,9 @@ static void forward_host(xb_tile *h, const float *X, int B, float *Y, const xb_i
   if (B == 0) return;
   float *dX = scratch_as<float>(t.s_y, (size_t)B * (t.C + t.R));
   float *dY = dX + (size_t)B * t.C;
+  const bool checked = !check || host_check_small({{X, (size_t)B * t.C, "forward"}});
   XB_CUDA(cudaMemcpyAsync(dX, X, sizeof(float) * B * t.C, cudaMemcpyHostToDevice, t.stream));
-  if (check) check_finite_dev(t, {{dX, (size_t)B * t.C, "forward"}});
+  if (!checked) check_finite_dev(t, {{dX, (size_t)B * t.C, "forward"}});
   forward_device(t, dX, B, dY, io);
   XB_CUDA(cudaMemcpyAsync(Y, dY, sizeof(float) * B * t.R, cudaMemcpyDeviceToHost, t.stream));
   sync(t);
@@ -841,8 +860,9 @@ static void backward_host(xb_tile *h, const float *D, int B, float *G, bool chec
   if (t.R != t.R_total) raise("backward: row-sharded tile; use xb_tile_backward_partial_dev");
   float *dD = scratch_as<float>(t.s_y, (size_t)B * (t.C + t.R));
   float *dG = dD + (size_t)B * t.R;
+  const bool checked = !check || host_check_small({{D, (size_t)B * t.R, "backward"}});
   XB_CUDA(cudaMemcpyAsync(dD, D, sizeof(float) * B * t.R, cudaMemcpyHostToDevice, t.stream));
-  if (check) check_finite_dev(t, {{dD, (size_t)B * t.R, "backward"}});
+  if (!checked) check_finite_dev(t, {{dD, (size_t)B * t.R, "backward"}});
   mvm_backward(t, dD, B, dG, make_io(t.cfg.backward_io), t.k_bwd, t.seq_bwd, nullptr, false,
                nullptr);
   t.seq_bwd += (uint64_t)B;
@@ -902,8 +922,17 @@ int xb_tile_update(xb_tile *h, const float *X, const float *D, int B, const floa
     if (B == 0) return;
     float *dX = scratch_as<float>(t.s_y, (size_t)B * (t.C + t.R));
     float *dD = dX + (size_t)B * t.C;
+    // small inputs: checked on the host before anything is enqueued
+    const bool small =
+        host_check_small({{X, (size_t)B * t.C, "update(x)"}, {D, (size_t)B * t.R, "update(d)"}});
+    if (small) check_lr_host(X, D, B, t.C, t.R, lr, t.learning_rate);
     XB_CUDA(cudaMemcpyAsync(dX, X, sizeof(float) * B * t.C, cudaMemcpyHostToDevice, t.stream));
     XB_CUDA(cudaMemcpyAsync(dD, D, sizeof(float) * B * t.R, cudaMemcpyHostToDevice, t.stream));
+    if (small) {
+      update_device(t, dX, dD, B, lr, nullptr, false, nullptr, nullptr, nullptr);
+      sync(t);
+      return;
+    }
     const std::initializer_list<Finite> in = {{dX, (size_t)B * t.C, "update(x)"},
                                               {dD, (size_t)B * t.R, "update(d)"}};
     launch_finite_dev(t, in);

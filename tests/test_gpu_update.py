@@ -224,11 +224,13 @@ def test_errors_match_reference():
         xb.AnalogTile(0, 2, xb.TileSettings(), 1)
 
 
-@pytest.mark.parametrize("shape", [(64, 1024, 8), (37, 101, 5)])
+@pytest.mark.parametrize("shape", [(64, 1024, 8), (37, 101, 5), (600, 96, 120), (96, 600, 120)])
 def test_nonfinite_inputs_leave_tile_untouched(shape):
-    """check_input (tile.cpp:65-75) runs on the device after the H2D copy; an
-    Inf/NaN anywhere (16-B vector body or scalar tail, x or d) raises before
-    the weights or the noise streams move."""
+    """check_input (tile.cpp:65-75): an Inf/NaN anywhere (16-B vector body or
+    scalar tail, x or d) raises before the weights or the noise streams move.
+    Calls up to 2^16 input floats are scanned on the host before the copy;
+    larger ones on the device after it (the last two shapes: the update, and
+    the backward or the forward, take the device path)."""
     R, C, B = shape
     rng = np.random.default_rng(3)
     X = rng.uniform(-1, 1, (B, C)).astype(np.float32)
