@@ -556,7 +556,16 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
         xa[u] = __ldg(xn + (size_t)u * C);
         da[u] = __ldg(dn + u);
       }
-      while (!__any_sync(0xffffffffu, stream_len() + PB * 31u > (uint32_t)PULSE_CAP)) {
+      // a block adds at most PB * 31 pulses to a lane's stream: `room` is a
+      // warp-uniform lower bound on the space left, refreshed by a max
+      // reduction only when it could not take another block
+      uint32_t room = 0;
+      while (true) {
+        if (room < PB * 31u) {
+          room = (uint32_t)PULSE_CAP - __reduce_max_sync(0xffffffffu, stream_len());
+          if (room < PB * 31u) break;
+        }
+        room -= PB * 31u;
         const int bn = b + PB;
         const bool more = bn + PB <= B;
         xn += xs;
