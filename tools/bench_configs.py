@@ -48,6 +48,35 @@ def rand(shape, seed):
     return torch.rand(*shape, device="cuda", generator=g) * 2 - 1
 
 
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}
+
+
+def kbar(t, X, D, lr, samples=16):
+    """Measured pulses per cell-update on `samples` samples (sum over slots of
+    #x lines firing x #d lines firing, from the trains the update would draw)."""
+    c = t.clone()
+    xw, dw, _ = c.generate_trains(X[:samples].cpu().numpy(), D[:samples].cpu().numpy(), lr)
+    del c
+    pulses = 0
+    for b in range(xw.shape[0]):
+        cx = ((xw[b][:, None] >> np.arange(31, dtype=np.uint32)) & 1).sum(axis=0)
+        cd = ((dw[b][:, None] >> np.arange(31, dtype=np.uint32)) & 1).sum(axis=0)
+        pulses += int((cx.astype(np.int64) * cd.astype(np.int64)).sum())
+    return pulses / (xw.shape[0] * xw.shape[1] * dw.shape[1])
+
+
+def int_roofline(cells_per_s, kb):
+    """(2 + 15 kbar) INT ops per cell-update against the ALU pipe."""
+    peak = 148 * 64 * peaks().get("sm_max_mhz", 1965.0) * 1e6
+    return {"bound": "int-pipe", "kbar": round(kb, 4),
+            "frac": (2.0 + 15.0 * kb) * cells_per_s / peak}
+
+
 def ref_oracle():
     import oracle
     impl = "reference" if oracle.available("reference") else "restatement"
@@ -159,6 +188,7 @@ def update_cfg(name, preset, n, B, blm, args, stream, ref_samples=1):
     X, D = rand((B, n), 1), rand((B, n), 2)
     ms = ev_time(lambda: t.update_dev(X, D, 0.01), 5, stream)
     out = {"config": name, "ms_per_batch": ms, "cell_updates_per_s": n * n * B / (ms * 1e-3)}
+    out["roofline"] = int_roofline(out["cell_updates_per_s"], kbar(t, X, D, 0.01))
     if not args.no_ref:
         O, impl = ref_oracle()
         s = O.default("tile")
@@ -226,9 +256,14 @@ def cfg5(args, stream):
     t0 = time.perf_counter()
     t.drift_to(1e4)
     d_s = time.perf_counter() - t0
+    mvm_bytes = 4.0 * n * n + 4.0 * B * 2 * n  # W once + x and y
+    hbm = peaks().get("hbm_gbs", 6650.0)
     return {"config": "cfg5 16384^2 reram_sb 1 GPU", "forward_ms": f_ms,
             "forward_samples_per_s": B / (f_ms * 1e-3), "backward_ms": b_ms, "update_ms": u_ms,
             "update_cell_updates_per_s": n * n * B / (u_ms * 1e-3),
+            "roofline_update": int_roofline(n * n * B / (u_ms * 1e-3), kbar(t, X, D, 0.01)),
+            "roofline_mvm_hbm_frac": {"forward": mvm_bytes / (f_ms * 1e-3) / 1e9 / hbm,
+                                      "backward": mvm_bytes / (b_ms * 1e-3) / 1e9 / hbm},
             "program_s_incl_h2d_of_target": p_s, "drift_to_s": d_s,
             "ref_1core": "SURVEY §6: program 29.5 s, drift_to 10.9 s, update 33.5 s/sample, "
                          "forward 1.10 s/sample"}
