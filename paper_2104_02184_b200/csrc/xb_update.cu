@@ -429,13 +429,13 @@ __device__ __forceinline__ void renorm2(float &hi, float &lo) {
 //     CAP pulses (a warp vote), so any batch size and pulse density fit.
 //   pulse loop: iteration n applies pulse n of every lane whose stream is
 //     longer than n: the direction bit selects the law constants, the c2c
-//     normal comes from a warp-uniform Philox refill every 4 iterations.
+//     factors come from warp-uniform Philox refills (3 calls per 32 pulses).
 // Lanes therefore wait only on the longest stream of the segment, and the
 // per-cell pulse order is exactly the reference's (sample order; one
 // direction per sample; pulses of a sample are interchangeable).
-// c2c normal #(8q + r) of a cell's segment is element r of the 8 normals of
-// Philox(k_c2c, (g0 + q, j, i, call)) with g0 the cell's running group count,
-// independent of launch geometry and of row sharding.
+// The c2c normals of stream word m of a cell's segment come from
+// Philox(k_c2c, (g0 + 3m + {0,1,2}, j, i, call)) with g0 the cell's running
+// call count: independent of launch geometry and of row sharding.
 #ifndef XB_PULSE_QW
 #define XB_PULSE_QW 32
 #endif
@@ -443,7 +443,7 @@ constexpr int PULSE_QW = XB_PULSE_QW;    // stream words per lane
 constexpr int PULSE_CAP = PULSE_QW * 32; // pulses per lane per segment
 
 // Launch shape (B200, round 1): persistent warps, ONE 1024-thread CTA per SM
-// (64 registers, no spills).  NS update: 7.48 ms vs 7.65 ms with two
+// (64 registers; a few bytes spill outside the loops).  NS update: 7.48 ms vs 7.65 ms with two
 // 512-thread CTAs and 8.0 ms with four 256-thread CTAs; ExpStep (cfg3):
 // 13.5 ms vs 13.8 ms for a per-tile grid of 512-thread CTAs.
 // (more warps at fewer registers lose: 2 CTAs x 18 or 20 warps, 56/51 regs,
