@@ -305,7 +305,7 @@ def test_c2c_noise_moments():
     assert abs(var / expect_var - 1) < 4 * np.sqrt(2 / (n - 1))
 
 
-@pytest.mark.parametrize("kind", [xb.CONSTANT_STEP, xb.EXP_STEP])
+@pytest.mark.parametrize("kind", [xb.CONSTANT_STEP, xb.LINEAR_STEP, xb.SOFT_BOUNDS, xb.EXP_STEP])
 def test_c2c_single_pulse_distribution(kind):
     """One pulse per cell from w = 0: dW / h - 1 = std z with h the law's
     step at w = 0 (dw_min for ConstantStep), so the 262 144 cells sample the
@@ -317,7 +317,9 @@ def test_c2c_single_pulse_distribution(kind):
     dev = xb.default_device()
     dev.kind = kind
     dev.dw_min, dev.dw_min_std, dev.w_max, dev.w_min = 2.0 ** -10, 0.25, 10.0, -10.0
-    h = dev.dw_min
+    h = dev.dw_min  # ConstantStep, and LinearStep / SoftBounds at w = 0
+    if kind == xb.LINEAR_STEP:
+        dev.slope = 0.5
     if kind == xb.EXP_STEP:
         dev.gamma = 2.0
         h = dev.dw_min * np.exp(-dev.gamma * (0.0 - dev.w_min) / (dev.w_max - dev.w_min))
