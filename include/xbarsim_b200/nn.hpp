@@ -288,7 +288,7 @@ public:
       } else {
         std::vector<float> d(q_gz_.size());
         for (size_t k = 0; k < d.size(); ++k) d[k] = static_cast<float>(-q_gz_[k] * inv_b);
-        std::vector<float> l(static_cast<size_t>(n), static_cast<float>(lr));
+        std::vector<double> l(static_cast<size_t>(n), lr);
         tile_->update_batch(q_in_.data(), d.data(), n, l.data());
       }
       if (bias_mode_ == BiasMode::digital)
@@ -483,7 +483,7 @@ public:
       } else {
         std::vector<float> d(q_gcol_.size());
         for (size_t k = 0; k < d.size(); ++k) d[k] = static_cast<float>(-q_gcol_[k] * inv_b);
-        std::vector<float> l(static_cast<size_t>(n), static_cast<float>(lr));
+        std::vector<double> l(static_cast<size_t>(n), lr);
         tile_->update_batch(q_patch_.data(), d.data(), n, l.data());
       }
       if (bias_mode_ == BiasMode::digital)

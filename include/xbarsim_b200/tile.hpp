@@ -18,6 +18,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <limits>
 #include <memory>
 #include <span>
 #include <stdexcept>
@@ -119,7 +120,7 @@ struct TileSettings {
   IOParams backward_io;
   UpdateParams update;
   TemporalParams temporal;
-  MvmPrecision mvm_precision = MvmPrecision::fp32;
+  MvmPrecision mvm_precision = MvmPrecision::tf32x3;
   WeightPrecision weight_precision = WeightPrecision::automatic;
 };
 
@@ -138,7 +139,7 @@ struct TransferSettings {
   double gamma = 0.0;
   bool has_transfer_io = false;
   IOParams transfer_io;
-  MvmPrecision mvm_precision = MvmPrecision::fp32;
+  MvmPrecision mvm_precision = MvmPrecision::tf32x3;
 };
 
 // proj/include/xbarsim/inference.hpp:21-36
@@ -318,6 +319,13 @@ inline void check_input(std::span<const double> v, int expected, const char *wha
   for (double x : v)
     if (!std::isfinite(x)) throw Error(std::string(what) + ": non-finite entry");
 }
+// the GPU computes on fp32 inputs: a finite double outside the fp32 range
+// would turn into Inf on the device (check_input already passed it)
+inline void check_f32_range(std::span<const double> v, const char *what) {
+  for (double x : v)
+    if (std::fabs(x) > static_cast<double>(std::numeric_limits<float>::max()))
+      throw Error(std::string(what) + ": entry exceeds the fp32 range of the B200 tile");
+}
 } // namespace detail
 
 // proj/src/device.cpp:100-132
@@ -360,7 +368,7 @@ public:
   virtual void forward_batch(const float *X, int B, float *Y) = 0;
   virtual void forward_noisy_batch(const float *X, int B, float *Y, double extra_sigma) = 0;
   virtual void backward_batch(const float *D, int B, float *G) = 0;
-  virtual void update_batch(const float *X, const float *D, int B, const float *lr) = 0;
+  virtual void update_batch(const float *X, const float *D, int B, const double *lr) = 0;
 };
 
 // proj/include/xbarsim/tile.hpp:75-131, on the GPU
@@ -414,9 +422,14 @@ public:
     for (double v : d) dz = dz && v == 0.0;
     if (lr == 0.0 || xz || dz) return; // proj/src/pulsed.cpp:122-124, no draw
     if (!(lr > 0.0)) throw Error("translate: learning rate must be > 0");
+    // the queue stores fp32 x/d (the device arithmetic); a finite double
+    // beyond the fp32 range would become Inf there, so it is rejected here,
+    // at the call, like check_input's non-finite entries
+    detail::check_f32_range(x, "update(x)");
+    detail::check_f32_range(d, "update(d)");
     qx_.insert(qx_.end(), x.begin(), x.end());
     qd_.insert(qd_.end(), d.begin(), d.end());
-    qlr_.push_back(static_cast<float>(lr));
+    qlr_.push_back(lr); // double, as the reference's update(..., double lr)
   }
   std::vector<double> forward_noisy(std::span<const double> x, double extra) override {
     detail::check_input(x, d_in_, "forward");
@@ -533,18 +546,22 @@ public:
     flush();
     check(xb_tile_backward(h_, D, B, G));
   }
-  void update_batch(const float *X, const float *D, int B, const float *lr) override {
+  void update_batch(const float *X, const float *D, int B, const double *lr) override {
     flush();
     check(xb_tile_update(h_, X, D, B, lr));
   }
   // applies the queued updates now (also done implicitly, see the file comment)
+  // The queue is taken out BEFORE the call: if the batched update fails (a
+  // CUDA error), the batch is dropped and reported once, instead of staying
+  // queued and re-raising from every later call on this tile.
   void flush() const {
     if (qlr_.empty()) return;
-    const int B = static_cast<int>(qlr_.size());
-    check(xb_tile_update(h_, qx_.data(), qd_.data(), B, qlr_.data()));
-    qx_.clear();
-    qd_.clear();
-    qlr_.clear();
+    std::vector<float> x, d;
+    std::vector<double> lr;
+    x.swap(qx_);
+    d.swap(qd_);
+    lr.swap(qlr_);
+    check(xb_tile_update(h_, x.data(), d.data(), static_cast<int>(lr.size()), lr.data()));
   }
   size_t queued_updates() const { return qlr_.size(); }
   xb_tile *handle() const { return h_; }
@@ -554,7 +571,8 @@ private:
   xb_tile *h_ = nullptr;
   int d_out_ = 0, d_in_ = 0;
   bool owned_ = true;
-  mutable std::vector<float> qx_, qd_, qlr_;
+  mutable std::vector<float> qx_, qd_;
+  mutable std::vector<double> qlr_;
   mutable DeviceMatrix device_;
   mutable Matrix weights_;
 };
@@ -613,8 +631,7 @@ public:
     detail::check_input(d, d_out_, "update(d)");
     auto xf = detail::to_f(x);
     auto df = detail::to_f(d);
-    const float l = static_cast<float>(lr);
-    check(xb_transfer_update(h_, xf.data(), df.data(), 1, &l));
+    check(xb_transfer_update(h_, xf.data(), df.data(), 1, &lr));
   }
   // proj/src/compound.cpp:228-238
   std::vector<double> forward_noisy(std::span<const double> x, double extra) override {
@@ -648,7 +665,7 @@ public:
   void backward_batch(const float *D, int B, float *G) override {
     check(xb_transfer_backward(h_, D, B, G));
   }
-  void update_batch(const float *X, const float *D, int B, const float *lr) override {
+  void update_batch(const float *X, const float *D, int B, const double *lr) override {
     check(xb_transfer_update(h_, X, D, B, lr));
   }
   void transfer_step() { check(xb_transfer_step(h_)); }
@@ -670,7 +687,7 @@ struct UnitCellSettings {
   IOParams backward_io;
   UpdateParams update;
   TemporalParams temporal;
-  MvmPrecision mvm_precision = MvmPrecision::fp32;
+  MvmPrecision mvm_precision = MvmPrecision::tf32x3;
 };
 
 // proj/include/xbarsim/compound.hpp:30-71, on the GPU: members are B200 tiles,
@@ -740,8 +757,7 @@ public:
       throw Error("update: x/d lengths do not match tile shape");
     auto xf = detail::to_f(x);
     auto df = detail::to_f(d);
-    const float l = static_cast<float>(lr);
-    check(xb_unitcell_update(h_, xf.data(), df.data(), 1, &l));
+    check(xb_unitcell_update(h_, xf.data(), df.data(), 1, &lr));
   }
   Matrix get_weights() const override {
     std::vector<float> w(static_cast<size_t>(d_out_) * d_in_);
@@ -767,7 +783,7 @@ public:
   void backward_batch(const float *D, int B, float *G) override {
     check(xb_unitcell_backward(h_, D, B, G));
   }
-  void update_batch(const float *X, const float *D, int B, const float *lr) override {
+  void update_batch(const float *X, const float *D, int B, const double *lr) override {
     check(xb_unitcell_update(h_, X, D, B, lr));
   }
   int n_members() const { return static_cast<int>(members_.size()); }

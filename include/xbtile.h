@@ -101,7 +101,7 @@ typedef struct xb_tile_config {
   xb_device_params device;
   xb_io_params forward_io, backward_io;
   xb_update_params update;
-  int32_t mvm_precision; /* XB_MVM_*; default XB_MVM_FP32 */
+  int32_t mvm_precision; /* XB_MVM_*; default XB_MVM_TF32X3 (tcgen05 for B >= 16) */
   xb_temporal_params temporal;
   int32_t weight_precision; /* XB_W_*; default XB_W_AUTO */
   int32_t _pad;
@@ -200,13 +200,13 @@ int xb_tile_forward_noisy(xb_tile *t, const float *X, int B, float *Y, double ex
 /* D [B][d_out] -> G [B][d_in] (unsharded tiles; see *_partial for shards) */
 int xb_tile_backward(xb_tile *t, const float *D, int B, float *G);
 /* B sequential pulsed updates; lr[B] per sample (NULL = learning_rate) */
-int xb_tile_update(xb_tile *t, const float *X, const float *D, int B, const float *lr);
+int xb_tile_update(xb_tile *t, const float *X, const float *D, int B, const double *lr);
 /* packed pulse trains: xw [B][d_in], dw [B][d_out_local]; bits 0..bl-1 are
  * the slots, bit 31 the sign (1 = negative); flip inverts every pulse */
 int xb_tile_apply_trains(xb_tile *t, const uint32_t *xw, const uint32_t *dw, int B, int flip);
 /* the trains the NEXT xb_tile_update on these inputs would draw (does not
  * change the tile); bl[B] receives the per-sample train length */
-int xb_tile_generate_trains(xb_tile *t, const float *X, const float *D, int B, const float *lr,
+int xb_tile_generate_trains(xb_tile *t, const float *X, const float *D, int B, const double *lr,
                             uint32_t *xw, uint32_t *dw, int32_t *bl);
 int xb_tile_temporal_step(xb_tile *t, const xb_temporal_params *tp);
 int xb_tile_end_minibatch(xb_tile *t);
@@ -221,7 +221,7 @@ int xb_tile_backward_dev(xb_tile *t, const float *dD, int B, float *dG);
 /* lr: host array of B learning rates (NULL -> learning_rate for all).
  * dAmaxD: optional device array [B] of the GLOBAL max|d| per sample (row
  * shards: the allreduce-max of xb_rows_amax_dev over ranks); NULL = local. */
-int xb_tile_update_dev(xb_tile *t, const float *dX, const float *dD, int B, const float *lr,
+int xb_tile_update_dev(xb_tile *t, const float *dX, const float *dD, int B, const double *lr,
                        const float *dAmaxD);
 /* backward of a row shard, split around the reduction over ranks:
  *   partial: dP[B][d_in] = sum over local rows of W^T d~ (+ weight-noise fold);
@@ -271,7 +271,7 @@ int xb_transfer_forward_noisy(xb_transfer *t, const float *X, int B, float *Y,
    (compound.hpp:109-111) */
 int xb_transfer_clone(const xb_transfer *t, xb_transfer **out);
 int xb_transfer_backward(xb_transfer *t, const float *D, int B, float *G);
-int xb_transfer_update(xb_transfer *t, const float *X, const float *D, int B, const float *lr);
+int xb_transfer_update(xb_transfer *t, const float *X, const float *D, int B, const double *lr);
 int xb_transfer_end_minibatch(xb_transfer *t);
 int xb_transfer_step(xb_transfer *t);
 int xb_transfer_get_weights(const xb_transfer *t, float *w);
@@ -298,7 +298,7 @@ int xb_unitcell_forward_noisy(xb_unitcell *u, const float *X, int B, float *Y,
                               double extra_sigma);
 int xb_unitcell_backward(xb_unitcell *u, const float *D, int B, float *G);
 /* B sequential UnitCellTile::update calls; lr may be NULL (0.01 each) */
-int xb_unitcell_update(xb_unitcell *u, const float *X, const float *D, int B, const float *lr);
+int xb_unitcell_update(xb_unitcell *u, const float *X, const float *D, int B, const double *lr);
 int xb_unitcell_get_weights(xb_unitcell *u, float *w);
 int xb_unitcell_set_weights(xb_unitcell *u, const float *w);
 int xb_unitcell_end_minibatch(xb_unitcell *u);

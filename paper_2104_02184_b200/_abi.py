@@ -92,6 +92,7 @@ class UnitCellConfig(C.Structure):
 
 _P = C.c_void_p
 _fp = C.POINTER(C.c_float)
+_dp = C.POINTER(C.c_double)
 _u32p = C.POINTER(C.c_uint32)
 _i32p = C.POINTER(C.c_int32)
 _dp = C.POINTER(C.c_double)
@@ -124,16 +125,16 @@ SIGNATURES = {
     "xb_tile_forward_io": (C.c_int, [_P, _fp, C.c_int, _fp, C.POINTER(IOParams)]),
     "xb_tile_forward_noisy": (C.c_int, [_P, _fp, C.c_int, _fp, C.c_double]),
     "xb_tile_backward": (C.c_int, [_P, _fp, C.c_int, _fp]),
-    "xb_tile_update": (C.c_int, [_P, _fp, _fp, C.c_int, _fp]),
+    "xb_tile_update": (C.c_int, [_P, _fp, _fp, C.c_int, _dp]),
     "xb_tile_apply_trains": (C.c_int, [_P, _u32p, _u32p, C.c_int, C.c_int]),
-    "xb_tile_generate_trains": (C.c_int, [_P, _fp, _fp, C.c_int, _fp, _u32p, _u32p, _i32p]),
+    "xb_tile_generate_trains": (C.c_int, [_P, _fp, _fp, C.c_int, _dp, _u32p, _u32p, _i32p]),
     "xb_tile_temporal_step": (C.c_int, [_P, C.POINTER(TemporalParams)]),
     "xb_tile_end_minibatch": (C.c_int, [_P]),
     "xb_tile_set_learning_rate": (C.c_int, [_P, C.c_double]),
     "xb_tile_learning_rate": (C.c_double, [_P]),
     "xb_tile_forward_dev": (C.c_int, [_P, _P, C.c_int, _P, C.POINTER(IOParams), C.c_double]),
     "xb_tile_backward_dev": (C.c_int, [_P, _P, C.c_int, _P]),
-    "xb_tile_update_dev": (C.c_int, [_P, _P, _P, C.c_int, _fp, _P]),
+    "xb_tile_update_dev": (C.c_int, [_P, _P, _P, C.c_int, _dp, _P]),
     "xb_tile_backward_partial_dev": (C.c_int, [_P, _P, C.c_int, _P, _P]),
     "xb_tile_backward_finish_dev": (C.c_int, [_P, _P, C.c_int, _P, _P]),
     "xb_rows_amax_dev": (C.c_int, [_P, C.c_int, C.c_int, _P, _P]),
@@ -152,7 +153,7 @@ SIGNATURES = {
     "xb_transfer_backward": (C.c_int, [_P, _fp, C.c_int, _fp]),
     "xb_transfer_forward_noisy": (C.c_int, [_P, _fp, C.c_int, _fp, C.c_double]),
     "xb_transfer_clone": (C.c_int, [_P, C.POINTER(_P)]),
-    "xb_transfer_update": (C.c_int, [_P, _fp, _fp, C.c_int, _fp]),
+    "xb_transfer_update": (C.c_int, [_P, _fp, _fp, C.c_int, _dp]),
     "xb_transfer_end_minibatch": (C.c_int, [_P]),
     "xb_transfer_step": (C.c_int, [_P]),
     "xb_transfer_get_weights": (C.c_int, [_P, _fp]),
@@ -166,7 +167,7 @@ SIGNATURES = {
     "xb_unitcell_forward": (C.c_int, [_P, _fp, C.c_int, _fp]),
     "xb_unitcell_forward_noisy": (C.c_int, [_P, _fp, C.c_int, _fp, C.c_double]),
     "xb_unitcell_backward": (C.c_int, [_P, _fp, C.c_int, _fp]),
-    "xb_unitcell_update": (C.c_int, [_P, _fp, _fp, C.c_int, _fp]),
+    "xb_unitcell_update": (C.c_int, [_P, _fp, _fp, C.c_int, _dp]),
     "xb_unitcell_get_weights": (C.c_int, [_P, _fp]),
     "xb_unitcell_set_weights": (C.c_int, [_P, _fp]),
     "xb_unitcell_end_minibatch": (C.c_int, [_P]),

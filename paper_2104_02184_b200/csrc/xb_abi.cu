@@ -241,6 +241,8 @@ static void tile_free(Tile &t) {
   if (t.own_stream && t.stream) cudaStreamDestroy(t.stream);
   if (t.bm_count) cudaFreeHost(t.bm_count);
   if (t.chk_host) cudaFreeHost(t.chk_host);
+  if (t.lr_pin) cudaFreeHost(t.lr_pin);
+  if (t.lr_ev) cudaEventDestroy(t.lr_ev);
   cudaFree(t.chk_dev);
 }
 
@@ -320,10 +322,10 @@ template <class T> static T *scratch_as(Scratch &s, size_t count) {
 
 // validate a host lr array the way the reference does per sample: lr == 0 or
 // a zero vector is a no-op; otherwise lr must be > 0 (pulsed.cpp:27-29,122-124)
-static void check_lr_host(const float *X, const float *D, int B, int C, int R, const float *lr,
+static void check_lr_host(const float *X, const float *D, int B, int C, int R, const double *lr,
                           double def_lr) {
   for (int b = 0; b < B; ++b) {
-    const double l = lr ? (double)lr[b] : def_lr;
+    const double l = lr ? lr[b] : def_lr;
     if (l == 0.0) continue;
     bool xz = true, dz = true;
     for (int j = 0; j < C && xz; ++j) xz = X[(size_t)b * C + j] == 0.f;
@@ -333,16 +335,17 @@ static void check_lr_host(const float *X, const float *D, int B, int C, int R, c
   }
 }
 
-static void check_lr_dev(const float *lr, int B, double def_lr) {
+static void check_lr_dev(const double *lr, int B, double def_lr) {
   for (int b = 0; b < B; ++b) {
-    const double l = lr ? (double)lr[b] : def_lr;
+    const double l = lr ? lr[b] : def_lr;
     if (!(l >= 0.0)) raise("translate: learning rate must be > 0");
   }
 }
 
 // update scratch layout
 struct UpdBufs {
-  float *lr, *xm, *dm;
+  double *lr;
+  float *xm, *dm;
   int32_t *bl;
   uint32_t *xw, *dw;
   double *px, *pd;
@@ -350,13 +353,13 @@ struct UpdBufs {
 
 static UpdBufs upd_bufs(Tile &t, int B, bool det) {
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  const size_t s_lr = al(B * sizeof(float)), s_bl = al(B * sizeof(int32_t));
+  const size_t s_lr = al(B * sizeof(double)), s_bl = al(B * sizeof(int32_t));
   const size_t nb = det ? (size_t)B : (size_t)train_ld(B); // ldb words per line (x quads, d lines)
   const size_t s_xw = al(nb * t.C * (det ? sizeof(double) : sizeof(uint32_t)));
   const size_t s_dw = al(nb * std::max(t.R, 1) * (det ? sizeof(double) : sizeof(uint32_t)));
   char *p = (char *)t.s_words.get(3 * s_lr + s_bl + s_xw + s_dw);
   UpdBufs u{};
-  u.lr = (float *)p;
+  u.lr = (double *)p;
   u.xm = (float *)(p + s_lr);
   u.dm = (float *)(p + 2 * s_lr);
   u.bl = (int32_t *)(p + 3 * s_lr);
@@ -372,25 +375,38 @@ static UpdBufs upd_bufs(Tile &t, int B, bool det) {
 }
 
 // a uniform learning rate travels as a kernel argument (no copy, no sync);
-// per-sample rates are uploaded (synchronously: the host array is borrowed)
-static const float *upload_lr(Tile &t, float *dst, const float *lr, int B, float *scalar) {
-  *scalar = lr ? lr[0] : (float)t.learning_rate;
+// per-sample rates are staged in the tile's pinned buffer (the host array is
+// only borrowed for the call) and copied in stream order.  The staging buffer
+// is reused only after its previous copy has executed (an event, not a
+// stream sync).
+static const double *upload_lr(Tile &t, double *dst, const double *lr, int B, double *scalar) {
+  *scalar = lr ? lr[0] : t.learning_rate;
   bool uniform = true;
   for (int b = 1; lr && b < B && uniform; ++b) uniform = lr[b] == lr[0];
   if (uniform) return nullptr;
-  XB_CUDA(cudaMemcpyAsync(dst, lr, B * sizeof(float), cudaMemcpyHostToDevice, t.stream));
-  XB_CUDA(cudaStreamSynchronize(t.stream));
+  if (t.lr_ev) XB_CUDA(cudaEventSynchronize(t.lr_ev));
+  if (t.lr_pin_n < (size_t)B) {
+    if (t.lr_pin) XB_CUDA(cudaFreeHost(t.lr_pin));
+    t.lr_pin = nullptr;
+    t.lr_pin_n = 0;
+    XB_CUDA(cudaMallocHost(&t.lr_pin, (size_t)B * sizeof(double)));
+    t.lr_pin_n = (size_t)B;
+  }
+  if (!t.lr_ev) XB_CUDA(cudaEventCreateWithFlags(&t.lr_ev, cudaEventDisableTiming));
+  std::memcpy(t.lr_pin, lr, (size_t)B * sizeof(double));
+  XB_CUDA(cudaMemcpyAsync(dst, t.lr_pin, B * sizeof(double), cudaMemcpyHostToDevice, t.stream));
+  XB_CUDA(cudaEventRecord(t.lr_ev, t.stream));
   return dst;
 }
 
 // the whole pulsed update of B samples from device inputs
-static void update_device(Tile &t, const float *dX, const float *dD, int B, const float *lr,
+static void update_device(Tile &t, const float *dX, const float *dD, int B, const double *lr,
                           const float *dAmaxD, bool peek, uint32_t *xw_out, uint32_t *dw_out,
                           int32_t *bl_out) {
   const bool det = t.cfg.update.pulse_type == XB_PULSE_DETERMINISTIC && !peek;
   UpdBufs u = upd_bufs(t, B, det);
-  float lr_s = 0.f;
-  const float *lr_d = upload_lr(t, u.lr, lr, B, &lr_s);
+  double lr_s = 0.0;
+  const double *lr_d = upload_lr(t, u.lr, lr, B, &lr_s);
   {
     PhaseTimer pt(t, XB_TIMER_TRAINS);
     launch_rows_amax(dX, B, t.C, t.C, u.xm, t.stream);
@@ -503,7 +519,7 @@ void xb_default_config(xb_tile_config *c) {
   c->update.bl = 31;
   c->update.bl_management = 0;
   c->update.pulse_type = XB_PULSE_STOCHASTIC;
-  c->mvm_precision = XB_MVM_FP32;
+  c->mvm_precision = XB_MVM_TF32X3;
 }
 
 void xb_default_transfer_config(xb_transfer_config *c) { // compound.hpp:76-91
@@ -513,7 +529,7 @@ void xb_default_transfer_config(xb_transfer_config *c) { // compound.hpp:76-91
   xb_default_io(&c->forward_io);
   xb_default_io(&c->backward_io);
   c->update.bl = 31;
-  c->mvm_precision = XB_MVM_FP32;
+  c->mvm_precision = XB_MVM_TF32X3;
   c->transfer_every = 1;
   c->units_in_mbatch = 0;
   c->transfer_lr = 0.1;
@@ -597,6 +613,7 @@ int xb_tile_create(const xb_tile_config *cfg, int d_out, int d_in, uint64_t seed
     ensure_device();
     auto h = std::make_unique<xb_tile>();
     Tile &t = h->t;
+    DevScope ds_(t.device);
     t.cfg = *cfg;
     t.R = r1 - r0;
     t.C = d_in;
@@ -604,6 +621,7 @@ int xb_tile_create(const xb_tile_config *cfg, int d_out, int d_in, uint64_t seed
     t.R_total = d_out;
     t.ld = (int)ld_of(d_in);
     t.comp = want_comp(*cfg);
+    t.device = current_device();
     XB_CUDA(cudaStreamCreateWithFlags(&t.stream, cudaStreamNonBlocking));
     t.own_stream = true;
     tile_init_keys(t, seed);
@@ -633,9 +651,11 @@ int xb_tile_clone(const xb_tile *src, xb_tile **out) { // tile.hpp:91 (deep copy
   return guard([&] {
     *out = nullptr;
     const Tile &s = src->t;
+    DevScope ds(s.device);
     XB_CUDA(cudaStreamSynchronize(s.stream));
     auto h = std::make_unique<xb_tile>();
     Tile &t = h->t;
+    DevScope ds_(t.device);
     t.cfg = s.cfg;
     t.R = s.R;
     t.C = s.C;
@@ -652,6 +672,7 @@ int xb_tile_clone(const xb_tile *src, xb_tile **out) { // tile.hpp:91 (deep copy
     t.prog_t0 = s.prog_t0;
     tile_init_keys(t, s.seed);
     t.comp = s.comp;
+    t.device = s.device;
     XB_CUDA(cudaStreamCreateWithFlags(&t.stream, cudaStreamNonBlocking));
     t.own_stream = true;
     try {
@@ -694,6 +715,7 @@ int xb_tile_shape(const xb_tile *t, int *d_out_local, int *d_in, int *row_begin,
 int xb_tile_set_stream(xb_tile *h, void *stream) {
   return guard([&] {
     Tile &t = h->t;
+    DevScope ds_(t.device);
     XB_CUDA(cudaStreamSynchronize(t.stream));
     if (t.own_stream) XB_CUDA(cudaStreamDestroy(t.stream));
     if (stream) {
@@ -723,6 +745,7 @@ int xb_tile_set_timing(xb_tile *h, int enable) {
 int xb_tile_read_timing(xb_tile *h, double *ms, int *counts) {
   return guard([&] {
     Tile &t = h->t;
+    DevScope ds_(t.device);
     sync(t);
     for (int k = 0; k < XB_TIMER_COUNT; ++k) {
       double tot = 0.0;
@@ -741,6 +764,7 @@ int xb_tile_read_timing(xb_tile *h, double *ms, int *counts) {
 int xb_tile_set_weights(xb_tile *h, const float *w) { // tile.cpp:103-119
   return guard([&] {
     Tile &t = h->t;
+    DevScope ds_(t.device);
     XB_CUDA(cudaMemcpy2DAsync(t.W, t.ld * sizeof(float), w, t.C * sizeof(float),
                               t.C * sizeof(float), t.R, cudaMemcpyHostToDevice, t.stream));
     launch_clip(t);
@@ -752,6 +776,7 @@ int xb_tile_set_weights(xb_tile *h, const float *w) { // tile.cpp:103-119
 int xb_tile_get_weights(const xb_tile *h, float *w) {
   return guard([&] {
     const Tile &t = h->t;
+    DevScope ds_(t.device);
     XB_CUDA(cudaMemcpy2DAsync(w, t.C * sizeof(float), t.W, t.ld * sizeof(float),
                               t.C * sizeof(float), t.R, cudaMemcpyDeviceToHost, t.stream));
     XB_CUDA(cudaStreamSynchronize(t.stream));
@@ -762,6 +787,7 @@ int xb_tile_set_device(xb_tile *h, const float *dw_up, const float *dw_down, con
                        const float *w_min) {
   return guard([&] {
     Tile &t = h->t;
+    DevScope ds_(t.device);
     const size_t n = (size_t)t.R * t.ld;
     std::vector<float4> p(n);
     XB_CUDA(cudaMemcpy(p.data(), t.P, n * sizeof(float4), cudaMemcpyDeviceToHost));
@@ -787,6 +813,7 @@ int xb_tile_get_device(const xb_tile *h, float *dw_up, float *dw_down, float *w_
                        float *w_min) {
   return guard([&] {
     const Tile &t = h->t;
+    DevScope ds_(t.device);
     const size_t n = (size_t)t.R * t.ld;
     std::vector<float4> p(n);
     XB_CUDA(cudaStreamSynchronize(t.stream));
@@ -808,6 +835,7 @@ int xb_tile_forward_dev(xb_tile *h, const float *dX, int B, float *dY, const xb_
                         double extra_sigma) {
   return guard([&] {
     Tile &t = h->t;
+    DevScope ds_(t.device);
     if (B < 0) raise("forward: batch must be >= 0");
     const xb_io_params base = io ? *io : t.cfg.forward_io;
     forward_device(t, dX, B, dY, noisy_io(base, extra_sigma));
@@ -818,6 +846,7 @@ int xb_tile_forward_dev(xb_tile *h, const float *dX, int B, float *dY, const xb_
 static void forward_host(xb_tile *h, const float *X, int B, float *Y, const xb_io_params &io,
                          bool check = true) {
   Tile &t = h->t;
+  DevScope ds_(t.device);
   if (B < 0) raise("forward: batch must be >= 0");
   if (B == 0) return;
   float *dX = scratch_as<float>(t.s_y, (size_t)B * (t.C + t.R));
@@ -845,6 +874,7 @@ int xb_tile_forward_noisy(xb_tile *h, const float *X, int B, float *Y, double ex
 int xb_tile_backward_dev(xb_tile *h, const float *dD, int B, float *dG) {
   return guard([&] {
     Tile &t = h->t;
+    DevScope ds_(t.device);
     if (t.R != t.R_total) raise("backward: row-sharded tile; use xb_tile_backward_partial_dev");
     io_validate(t.cfg.backward_io, "backward_io");
     mvm_backward(t, dD, B, dG, make_io(t.cfg.backward_io), t.k_bwd, t.seq_bwd, nullptr, false,
@@ -855,6 +885,7 @@ int xb_tile_backward_dev(xb_tile *h, const float *dD, int B, float *dG) {
 
 static void backward_host(xb_tile *h, const float *D, int B, float *G, bool check = true) {
   Tile &t = h->t;
+  DevScope ds_(t.device);
   if (B < 0) raise("backward: batch must be >= 0");
   if (B == 0) return;
   if (t.R != t.R_total) raise("backward: row-sharded tile; use xb_tile_backward_partial_dev");
@@ -878,6 +909,7 @@ int xb_tile_backward_partial_dev(xb_tile *h, const float *dD, int B, const float
                                  float *dP) {
   return guard([&] {
     Tile &t = h->t;
+    DevScope ds_(t.device);
     if (B < 0) raise("backward: batch must be >= 0");
     const xb_io_params &io = t.cfg.backward_io;
     if (io.bound_management != XB_BM_NONE)
@@ -894,6 +926,7 @@ int xb_tile_backward_finish_dev(xb_tile *h, const float *dPsum, int B, const flo
                                 float *dG) {
   return guard([&] {
     Tile &t = h->t;
+    DevScope ds_(t.device);
     mvm_backward_finish(t, dPsum, B, dAmaxD, dG, make_io(t.cfg.backward_io), t.k_bwd, t.seq_bwd);
     t.seq_bwd += (uint64_t)B;
     t.bwd_pending -= std::min(t.bwd_pending, (uint64_t)B);
@@ -904,10 +937,11 @@ int xb_rows_amax_dev(const float *dV, int B, int n, float *dOut, void *stream) {
   return guard([&] { launch_rows_amax(dV, B, n, n, dOut, (cudaStream_t)stream); });
 }
 
-int xb_tile_update_dev(xb_tile *h, const float *dX, const float *dD, int B, const float *lr,
+int xb_tile_update_dev(xb_tile *h, const float *dX, const float *dD, int B, const double *lr,
                        const float *dAmaxD) {
   return guard([&] {
     Tile &t = h->t;
+    DevScope ds_(t.device);
     if (B < 0) raise("update: batch must be >= 0");
     if (B == 0) return;
     check_lr_dev(lr, B, t.learning_rate);
@@ -915,9 +949,10 @@ int xb_tile_update_dev(xb_tile *h, const float *dX, const float *dD, int B, cons
   });
 }
 
-int xb_tile_update(xb_tile *h, const float *X, const float *D, int B, const float *lr) {
+int xb_tile_update(xb_tile *h, const float *X, const float *D, int B, const double *lr) {
   return guard([&] {
     Tile &t = h->t;
+    DevScope ds_(t.device);
     if (B < 0) raise("update: batch must be >= 0");
     if (B == 0) return;
     float *dX = scratch_as<float>(t.s_y, (size_t)B * (t.C + t.R));
@@ -965,10 +1000,11 @@ int xb_tile_update(xb_tile *h, const float *X, const float *D, int B, const floa
   });
 }
 
-int xb_tile_generate_trains(xb_tile *h, const float *X, const float *D, int B, const float *lr,
+int xb_tile_generate_trains(xb_tile *h, const float *X, const float *D, int B, const double *lr,
                             uint32_t *xw, uint32_t *dw, int32_t *bl) {
   return guard([&] {
     Tile &t = h->t;
+    DevScope ds_(t.device);
     if (B <= 0) raise("generate_trains: batch must be >= 1");
     float *dX = scratch_as<float>(t.s_y, (size_t)B * (t.C + t.R));
     float *dD = dX + (size_t)B * t.C;
@@ -983,6 +1019,7 @@ int xb_tile_generate_trains(xb_tile *h, const float *X, const float *D, int B, c
 int xb_tile_apply_trains(xb_tile *h, const uint32_t *xw, const uint32_t *dw, int B, int flip) {
   return guard([&] { // tile.cpp:158-169
     Tile &t = h->t;
+    DevScope ds_(t.device);
     if (B < 0) raise("apply_trains: batch must be >= 0");
     if (B == 0) return;
     // reference-facing sample-major words -> internal layouts (x quads, d lines)
@@ -1006,6 +1043,7 @@ int xb_tile_apply_trains(xb_tile *h, const uint32_t *xw, const uint32_t *dw, int
 int xb_tile_temporal_step(xb_tile *h, const xb_temporal_params *tp) { // tile.cpp:128-156
   return guard([&] {
     Tile &t = h->t;
+    DevScope ds_(t.device);
     temporal_validate(*tp);
     if (!temporal_any(*tp)) return;
     ensure_xi(t);
@@ -1039,6 +1077,7 @@ static void model_validate(const xb_inference_model &m) { // inference.cpp:19-32
 int xb_tile_program(xb_tile *h, const float *target, const xb_inference_model *m, uint64_t seed) {
   return guard([&] { // inference.cpp:34-61
     Tile &t = h->t;
+    DevScope ds_(t.device);
     model_validate(*m);
     const size_t n = (size_t)t.R * t.ld;
     if (!t.w0) {
@@ -1058,6 +1097,7 @@ int xb_tile_program(xb_tile *h, const float *target, const xb_inference_model *m
 int xb_tile_drift_to(xb_tile *h, double time_s) {
   return guard([&] { // inference.cpp:63-76
     Tile &t = h->t;
+    DevScope ds_(t.device);
     if (!t.w0) raise("drift_to: tile has not been programmed");
     if (time_s < t.prog_t0) raise("drift_to: t < t0");
     launch_drift(t, time_s / t.prog_t0);
@@ -1069,6 +1109,7 @@ int xb_tile_drift_to(xb_tile *h, double time_s) {
 int xb_tile_probe_readout(xb_tile *h, const xb_inference_model *m, double *out) {
   return guard([&] { // inference.cpp:85-95
     Tile &t = h->t;
+    DevScope ds_(t.device);
     model_validate(*m);
     const int P = m->compensation_probes;
     std::vector<float> X((size_t)P * t.C, 1.0f), Y((size_t)P * t.R);
@@ -1221,7 +1262,7 @@ static void transfer_step_impl(xb_transfer *tr) {
   forward_device(a, oh, 1, ro, io);
   sync(a);
   Tile &c = tr->slow->t;
-  const float lr = (float)tr->cfg.transfer_lr;
+  const double lr = tr->cfg.transfer_lr;
   update_device(c, oh, ro, 1, &lr, nullptr, false, nullptr, nullptr, nullptr);
   sync(c);
   tr->next_column = (tr->next_column + 1) % a.C;
@@ -1239,7 +1280,7 @@ int xb_transfer_step(xb_transfer *t) {
   return guard([&] { transfer_step_impl(t); });
 }
 
-int xb_transfer_update(xb_transfer *t, const float *X, const float *D, int B, const float *lr) {
+int xb_transfer_update(xb_transfer *t, const float *X, const float *D, int B, const double *lr) {
   return guard([&] { // compound.cpp:240-245
     Tile &a = t->fast->t;
     if (t->cfg.units_in_mbatch || t->cfg.transfer_every == 0) {
@@ -1324,6 +1365,7 @@ static void unitcell_validate(const xb_unitcell_config &c) { // compound.cpp:12-
 static xb_tile *view_tile_create(const xb_tile_config &cfg, int R, int C, uint64_t seed) {
   auto h = std::make_unique<xb_tile>();
   Tile &t = h->t;
+  DevScope ds_(t.device);
   t.cfg = cfg;
   t.R = R;
   t.C = C;
@@ -1367,19 +1409,19 @@ static void uc_free(xb_unitcell *u) {
 // compound.cpp:109-147 for B samples in order: one translate + trains per
 // sample on the compound's update stream (grain per sample), then each member
 // fires the trains of its samples in one weight-stationary pulse launch
-static void uc_update(xb_unitcell *u, const float *X, const float *D, int B, const float *lr) {
+static void uc_update(xb_unitcell *u, const float *X, const float *D, int B, const double *lr) {
   Tile &e = u->eff->t;
   const int K = (int)u->members.size();
   const bool rr = u->cfg.policy == XB_UC_ROUND_ROBIN;
   double grain_all = 0.0;
   for (int k = 0; k < K; ++k) grain_all += std::fabs(u->cfg.gains[k]) * u->cfg.devices[k].dw_min;
-  std::vector<float> lre(B, 0.f);
+  std::vector<double> lre(B, 0.0);
   std::vector<double> grain(B, 0.0);
   std::vector<int> member(B, -1);
   int cursor = u->next_member;
   bool any = false;
   for (int b = 0; b < B; ++b) {
-    const double l = lr ? (double)lr[b] : e.learning_rate;
+    const double l = lr ? lr[b] : e.learning_rate;
     bool xz = true, dz = true;
     for (int j = 0; j < e.C && xz; ++j) xz = X[(size_t)b * e.C + j] == 0.f;
     for (int i = 0; i < e.R && dz; ++i) dz = D[(size_t)b * e.R + i] == 0.f;
@@ -1392,7 +1434,7 @@ static void uc_update(xb_unitcell *u, const float *X, const float *D, int B, con
     }
     if (g == 0.0) continue; // zero-gain member (or all gains zero): a no-op event
     if (!(l > 0.0)) raise("translate: learning rate must be > 0"); // pulsed.cpp:27-29
-    lre[b] = (float)l;
+    lre[b] = l;
     grain[b] = g;
     any = true;
   }
@@ -1408,12 +1450,12 @@ static void uc_update(xb_unitcell *u, const float *X, const float *D, int B, con
   int *dIdx = (int *)(aux + (size_t)B * sizeof(double));
   XB_CUDA(cudaMemcpyAsync(dX, X, sizeof(float) * B * e.C, cudaMemcpyHostToDevice, e.stream));
   XB_CUDA(cudaMemcpyAsync(dD, D, sizeof(float) * B * e.R, cudaMemcpyHostToDevice, e.stream));
-  XB_CUDA(cudaMemcpyAsync(ub.lr, lre.data(), sizeof(float) * B, cudaMemcpyHostToDevice, e.stream));
+  XB_CUDA(cudaMemcpyAsync(ub.lr, lre.data(), sizeof(double) * B, cudaMemcpyHostToDevice, e.stream));
   XB_CUDA(cudaMemcpyAsync(dG, grain.data(), sizeof(double) * B, cudaMemcpyHostToDevice,
                           e.stream));
   launch_rows_amax(dX, B, e.C, e.C, ub.xm, e.stream);
   launch_rows_amax(dD, B, e.R, e.R, ub.dm, e.stream);
-  launch_trains(e, dX, dD, B, ub.lr, 0.f, ub.xm, ub.dm, e.seq_upd, ub.xw, ub.dw, ldb, ub.bl,
+  launch_trains(e, dX, dD, B, ub.lr, 0.0, ub.xm, ub.dm, e.seq_upd, ub.xw, ub.dw, ldb, ub.bl,
                 nullptr, nullptr, false, dG);
   e.seq_upd += (uint64_t)B;
   if (!rr) {
@@ -1457,7 +1499,7 @@ void xb_default_unitcell_config(xb_unitcell_config *c) { // compound.hpp:15-28
   xb_default_io(&c->forward_io);
   xb_default_io(&c->backward_io);
   c->update = xb_update_params{31, 0, XB_PULSE_STOCHASTIC};
-  c->mvm_precision = XB_MVM_FP32;
+  c->mvm_precision = XB_MVM_TF32X3;
 }
 
 int xb_unitcell_create(const xb_unitcell_config *cfg, int d_out, int d_in, uint64_t seed,
@@ -1549,7 +1591,7 @@ int xb_unitcell_backward(xb_unitcell *u, const float *D, int B, float *G) {
   });
 }
 
-int xb_unitcell_update(xb_unitcell *u, const float *X, const float *D, int B, const float *lr) {
+int xb_unitcell_update(xb_unitcell *u, const float *X, const float *D, int B, const double *lr) {
   return guard([&] {
     if (B < 0) raise("update: batch must be >= 0");
     if (B > 0) uc_update(u, X, D, B, lr);

@@ -113,6 +113,8 @@ __device__ __forceinline__ void box_muller16(uint32_t a, float &z0, float &z1) {
 struct Quant {
   double bound, step, inv_step, levels_m1;
   int bits;
+  // fp32 copies for the tensor-core output stage (quantize_f)
+  float fbound, fstep, finv_step, flevels_m1;
 };
 
 __host__ __device__ __forceinline__ Quant make_quant(double bound, int bits) {
@@ -129,6 +131,10 @@ __host__ __device__ __forceinline__ Quant make_quant(double bound, int bits) {
     q.inv_step = 0.0;
     q.levels_m1 = 0.0;
   }
+  q.fbound = (float)q.bound;
+  q.fstep = (float)q.step;
+  q.finv_step = (float)q.inv_step;
+  q.flevels_m1 = (float)q.levels_m1;
   return q;
 }
 
@@ -141,6 +147,22 @@ __device__ __forceinline__ double quantize(double v, const Quant &q) {
   double k = round((v + q.bound - 0.5 * q.step) * q.inv_step);
   k = fmin(fmax(k, 0.0), q.levels_m1);
   return -q.bound + (k + 0.5) * q.step;
+}
+
+// The same quantizer in fp32, for the output stage of the tensor-core MVM
+// (TF32 / 3xTF32): its accumulators are fp32 already, so fp64 converter
+// arithmetic there buys nothing but FP64-pipe time (the B200 runs fp64 at
+// half the fp32 rate; the fused epilogue was bound by it).  The grid step is
+// a power of two, so -b + (k + 1/2) step is exact in fp32; only inputs within
+// ~1 fp32 ulp of a grid threshold can land one level away from the fp64
+// quantizer, far below the TF32 contraction error.
+__device__ __forceinline__ float quantize_f(float v, const Quant &q) {
+  if (v == 0.f) return 0.f;
+  v = fminf(fmaxf(v, -q.fbound), q.fbound);
+  if (q.bits <= 0) return v;
+  float k = roundf((v + q.fbound - 0.5f * q.fstep) * q.finv_step);
+  k = fminf(fmaxf(k, 0.f), q.flevels_m1);
+  return fmaf(k + 0.5f, q.fstep, -q.fbound);
 }
 
 // ------------------------------------------------------------ reductions

@@ -1,6 +1,7 @@
 // xb_internal.h -- host-side internals shared by the libxbtile translation units.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <string>
@@ -33,6 +34,22 @@ inline uint64_t derive_seed_idx(uint64_t base, const char *name, uint64_t idx) {
 }
 inline Key key_of(uint64_t seed) { return Key{(uint32_t)seed, (uint32_t)(seed >> 32)}; }
 
+// One-time per-device setup (cudaFuncSetAttribute is per device context): bit
+// d of `mask` records that device d is configured.  Concurrent first calls may
+// both run f -- harmless, the attributes are idempotent.
+inline int current_device() {
+  int d = 0;
+  XB_CUDA(cudaGetDevice(&d));
+  return d;
+}
+template <class F> inline void once_per_device(std::atomic<uint64_t> &mask, F &&f) {
+  const int d = current_device();
+  const uint64_t bit = 1ull << (d & 63);
+  if (mask.load(std::memory_order_acquire) & bit) return;
+  f();
+  mask.fetch_or(bit, std::memory_order_acq_rel);
+}
+
 // device scratch that grows on demand
 struct Scratch {
   void *p = nullptr;
@@ -46,11 +63,31 @@ struct IoDev {
   Quant dac, adc;
   double sigma_inp, sigma_out, sigma_w;
   int nm_absmax, perfect, bm, bm_max_iter;
+  // output stage arithmetic: 1 = fp64 like the reference (exact FP32 mode),
+  // 0 = fp32 (tensor-core modes, whose accumulators are fp32/TF32 anyway)
+  int exact;
 };
 IoDev make_io(const xb_io_params &io);
 
+// makes `dev` current for the scope of one ABI call on a tile (a handle keeps
+// the device it was created on; the caller's current device is restored)
+struct DevScope {
+  int prev = -1;
+  explicit DevScope(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) XB_CUDA(cudaSetDevice(dev));
+  }
+  ~DevScope() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+  DevScope(const DevScope &) = delete;
+  DevScope &operator=(const DevScope &) = delete;
+};
+
 struct Tile {
   xb_tile_config cfg;
+  int device = 0;            // CUDA device ordinal of every buffer and the stream
   int R = 0, C = 0;          // local rows, columns
   int row0 = 0, R_total = 0; // first global row, global rows
   int ld = 0;                // leading dimension of W / params (floats)
@@ -78,6 +115,9 @@ struct Tile {
   int *bm_count = nullptr; // pinned host word for the bound-management loop
   int *chk_dev = nullptr;  // input-check flag word (device) and its pinned host copy
   int *chk_host = nullptr;
+  double *lr_pin = nullptr; // pinned staging of per-sample learning rates
+  size_t lr_pin_n = 0;
+  cudaEvent_t lr_ev = nullptr; // last lr copy out of lr_pin
 
   Scratch s_words, s_params, s_io, s_y, s_lr;
 
@@ -98,8 +138,8 @@ struct PhaseTimer {
 // ---- kernel launchers (xb_update.cu) ----
 void launch_rows_amax(const float *V, int B, int n, int ld, float *out, cudaStream_t s);
 // per-sample translate + Bernoulli trains; writes packed words and bl[B]
-void launch_trains(const Tile &t, const float *X, const float *D, int B, const float *lr_dev,
-                   float lr_scalar, const float *xm, const float *dm, uint64_t seq0,
+void launch_trains(const Tile &t, const float *X, const float *D, int B, const double *lr_dev,
+                   double lr_scalar, const float *xm, const float *dm, uint64_t seq0,
                    uint32_t *xw, uint32_t *dw, int ldb, int32_t *bl, double *px, double *pd,
                    bool deterministic, const double *dwmin_b = nullptr);
 // d trains are LINE-major: dw[i][b], row stride ldb (multiple of 8).  x trains

@@ -47,7 +47,10 @@ __global__ void __launch_bounds__(PREP_THREADS) prep_kernel(const float *__restr
                                                              int first_pass,
                                                              const float *__restrict__ amax_in,
                                                              int *__restrict__ sat,
-                                                             const int *__restrict__ map) {
+                                                             const int *__restrict__ map,
+                                                             int in0) {
+  // in0: global index of input 0 (row-shard backward: the shard's first row),
+  // so the input-noise counters match the unsharded tile's
   // map != nullptr: a compacted bound-management re-issue -- block i prepares
   // sample map[i] into x~ row i (compact_kernel already re-armed the flags)
   const int b = map ? map[blockIdx.x] : blockIdx.x;
@@ -104,7 +107,7 @@ __global__ void __launch_bounds__(PREP_THREADS) prep_kernel(const float *__restr
     if (s.alpha == 0.f) return 0.f;
     double q = quantize((double)xv * inv, io.dac); // x / alpha, then the DAC (io.cpp:122-130)
     if (io.sigma_inp > 0.0) {
-      const float z = normal1((uint32_t)j, (uint32_t)seq, (uint32_t)(seq >> 32) | (s.m << 24),
+      const float z = normal1((uint32_t)(j + in0), (uint32_t)seq, (uint32_t)(seq >> 32) | (s.m << 24),
                               TAG_IN_NOISE << 24, key);
       q += io.sigma_inp * (double)z;
     }
@@ -304,32 +307,20 @@ __global__ void __launch_bounds__(256) finish_kernel(const float *__restrict__ P
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (4 * g >= M) return;
   const float m = amax[b];
-  const double alpha = (m == 0.f) ? 0.0 : (io.nm_absmax ? (double)m : 1.0);
-  const uint64_t seq = seq0 + (uint64_t)b;
-  uint32_t w[4] = {0u, 0u, 0u, 0u};
-  const bool noisy = !io.perfect && (io.sigma_w > 0.0 || io.sigma_out > 0.0);
-  if (noisy) out_noise_words((uint32_t)g, seq, 0, key, w);
+  SampleState s;
+  s.alpha = (m == 0.f) ? 0.f : (io.nm_absmax ? m : 1.f);
+  s.norm = 0.f;
+  s.m = 0;
+  s.active = 1;
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int o = 4 * g + k;
-    if (o >= M) continue;
-    const float a = Psum[(size_t)b * M + o];
-    if (io.perfect) {
-      Y[(size_t)b * M + o] = a;
-      continue;
-    }
-    float z0 = 0.f, z1 = 0.f;
-    if (noisy) box_muller16(w[k], z0, z1);
-    double v, scale;
-    if (alpha == 0.0) {
-      v = io.sigma_out > 0.0 ? io.sigma_out * (double)z1 : 0.0;
-      scale = 1.0;
-    } else {
-      v = (double)a + (io.sigma_out > 0.0 ? io.sigma_out * (double)z1 : 0.0);
-      scale = alpha;
-    }
-    Y[(size_t)b * M + o] = (float)(scale * quantize(v, io.adc));
-  }
+  for (int k = 0; k < 4; ++k)
+    if (4 * g + k < M) a[k] = Psum[(size_t)b * M + 4 * g + k];
+  // the weight-noise fold is already in the partial sums (partial_kernel):
+  // only the output noise, the ADC and alpha act here, with the same noise
+  // words and arithmetic as the whole-tile output stage
+  io.sigma_w = 0.0;
+  epilogue_group4(a, g, 0, M, s, io, key, seq0 + (uint64_t)b, Y + (size_t)b * M);
 }
 
 struct MvmScratch {
@@ -374,16 +365,22 @@ static bool unfused_requested() {
 }
 
 // one full noisy MVM in direction TRANS (forward: false)
+// tensor-core contraction at TF32 / 3xTF32 (B >= 16); the fp32 SIMT kernel
+// otherwise (exact-fp32 parity mode, tiny batches)
+static bool use_tc(const Tile &t, int B) {
+  return (t.cfg.mvm_precision == XB_MVM_TF32 || t.cfg.mvm_precision == XB_MVM_TF32X3) && B >= 16;
+}
+
 template <bool TRANS>
-void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io, Key key,
+void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io_in, Key key,
              uint64_t seq0, const float *amax_in, bool skip_epilogue, float *dPartial) {
   const int K = TRANS ? t.R : t.C; // contraction length
   const int M = TRANS ? t.C : t.R; // outputs
   if (B <= 0) return;
-  // tensor-core contraction at TF32 / 3xTF32 (B >= 16); the fp32 SIMT kernel
-  // otherwise (exact-fp32 parity mode, tiny batches)
   const bool x3 = t.cfg.mvm_precision == XB_MVM_TF32X3;
-  const bool tc = (t.cfg.mvm_precision == XB_MVM_TF32 || x3) && B >= 16;
+  const bool tc = use_tc(t, B);
+  IoDev io = io_in;
+  io.exact = !tc; // fp64 output stage only behind the exact fp32 contraction
   const int o0 = TRANS ? 0 : t.row0; // global index of output 0 (noise counters)
   // the output stage runs inside the tcgen05 kernel (K-splits reduced over a
   // thread-block cluster) unless the caller wants raw partial sums, the noise
@@ -401,7 +398,8 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io, Key
   for (int pass = 0; pass < passes; ++pass) {
     const int first = pass == 0;
     prep_kernel<<<nrun, PREP_THREADS, 0, t.stream>>>(dIn, K, K, s.xt, ldt, s.st, io, key, seq0,
-                                                      first, amax_in, s.sat, map);
+                                                      first, amax_in, s.sat, map,
+                                                      TRANS ? t.row0 : 0);
     count_launch();
     XB_CUDA(cudaGetLastError());
     int nsplit = 1;
@@ -468,6 +466,7 @@ IoDev make_io(const xb_io_params &io) {
   d.perfect = io.is_perfect;
   d.bm = io.bound_management == XB_BM_ITERATIVE && !io.is_perfect;
   d.bm_max_iter = io.bm_max_iter;
+  d.exact = 1;
   return d;
 }
 
@@ -485,8 +484,10 @@ void mvm_backward_finish(Tile &t, const float *dPsum, int B, const float *amax_g
                          const IoDev &io, Key key, uint64_t seq0) {
   if (B <= 0) return;
   if (!amax_global) raise("backward_finish: the global max|d| per sample is required");
+  IoDev io2 = io;
+  io2.exact = !use_tc(t, B);
   dim3 eg((out_groups(0, t.C) + 255) / 256, B);
-  finish_kernel<<<eg, 256, 0, t.stream>>>(dPsum, t.C, amax_global, dG, io, key, seq0);
+  finish_kernel<<<eg, 256, 0, t.stream>>>(dPsum, t.C, amax_global, dG, io2, key, seq0);
   count_launch();
   XB_CUDA(cudaGetLastError());
 }

@@ -53,8 +53,32 @@ __device__ __forceinline__ bool epilogue_group4(const float a[4], int g, int o0,
   uint32_t w[4] = {0u, 0u, 0u, 0u};
   const bool noisy = !io.perfect && (io.sigma_w > 0.0 || io.sigma_out > 0.0);
   if (noisy) out_noise_words((uint32_t)g, seq, s.m, key, w);
-  const double scale = s.alpha == 0.f ? 1.0 : (double)s.alpha * pow2i(s.m);
   bool hit = false;
+  if (!io.exact && !io.perfect) {
+    // fp32 output stage (tensor-core modes): alpha 2^m y rounds once in fp32,
+    // exactly like the fp64 product cast to fp32 (2^m is exact)
+    const float scale = s.alpha == 0.f ? 1.f : s.alpha * (float)pow2i(s.m);
+    const float sw = (float)io.sigma_w * s.norm, so = (float)io.sigma_out;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int o = 4 * g + k - o0;
+      if (o < 0 || o >= M) continue;
+      float z0 = 0.f, z1 = 0.f;
+      if (noisy) box_muller16(w[k], z0, z1);
+      float v;
+      if (s.alpha == 0.f) {
+        v = so * z1;
+      } else {
+        v = a[k];
+        if (io.sigma_w > 0.0) v = fmaf(sw, z0, v);
+        v = fmaf(so, z1, v);
+        hit |= fabsf(v) >= io.adc.fbound;
+      }
+      yrow[o] = scale * quantize_f(v, io.adc);
+    }
+    return hit;
+  }
+  const double scale = s.alpha == 0.f ? 1.0 : (double)s.alpha * pow2i(s.m);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int o = 4 * g + k - o0;

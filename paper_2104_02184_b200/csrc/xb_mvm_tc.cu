@@ -32,6 +32,29 @@
 
 #include "xb_mvm_common.cuh"
 
+#ifdef XB_TC_TRACE
+// experiment builds only: per-CTA globaltimer stamps of the contraction
+// (start, first stage landed, accumulator complete, end)
+__device__ unsigned long long g_tc_trace[4096][4];
+__device__ __forceinline__ unsigned long long xb_gtime() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  return v;
+}
+#define XB_TRACE(k)                                                                             \
+  do {                                                                                          \
+    const unsigned slot_ = blockIdx.x + gridDim.x * blockIdx.y;                                 \
+    if (slot_ < 4096) g_tc_trace[slot_][k] = xb_gtime();                                        \
+  } while (0)
+extern "C" __attribute__((visibility("default"))) int xb_debug_tc_trace(unsigned long long *out,
+                                                                          int n) {
+  return (int)cudaMemcpyFromSymbol(out, g_tc_trace, sizeof(unsigned long long) * 4 *
+                                                        (size_t)(n < 4096 ? n : 4096));
+}
+#else
+#define XB_TRACE(k) ((void)0)
+#endif
+
 namespace xb {
 
 namespace {
@@ -285,6 +308,7 @@ __global__ void __launch_bounds__(tc_threads<X3, FUSED>(), 1)
   auto stage_b = [&](int s) { return smem + s * SB + AB; };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) XB_TRACE(0);
   const int m0 = blockIdx.x * TC_BM * NSUB;
   const int split = blockIdx.y;
   const int kb0 = split * kblocks_per_split;
@@ -345,6 +369,7 @@ __global__ void __launch_bounds__(tc_threads<X3, FUSED>(), 1)
       const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
       mbar_wait((X3 ? conv0 : full0) + 8 * s, ph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (kb == 0) XB_TRACE(1);
       const uint64_t db = umma_desc(smem_u32(stage_b(s)), 16u, 1024u, 2u);
       const uint64_t dbl = umma_desc(smem_u32(stage_b(s) + LO), 16u, 1024u, 2u);
 #pragma unroll
@@ -395,6 +420,7 @@ __global__ void __launch_bounds__(tc_threads<X3, FUSED>(), 1)
   if (epi_warp && nkb > 0) {
     mbar_wait(done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (threadIdx.x == 32 * EPI_W0) XB_TRACE(2);
   }
   const int quarter = warp & 3;
   if (!FUSED) {
@@ -431,6 +457,7 @@ __global__ void __launch_bounds__(tc_threads<X3, FUSED>(), 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (threadIdx.x == 0) XB_TRACE(3);
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(TMEM_COLS));
@@ -680,13 +707,12 @@ static void launch_tc(dim3 grid, cudaStream_t st, const CUtensorMap &ma, const C
                       int M, int K, int nb, int bn, int per, float *part, size_t split_stride,
                       const FusedOut &fo) {
   auto kern = tc_gemm_kernel<A_MN, X3, NSUB, FUSED>;
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<uint64_t> configured{0};
+  once_per_device(configured, [&] {
     XB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  tc_smem<X3, NSUB>()));
     if (FUSED) XB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
-    configured = true;
-  }
+  });
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(tc_threads<X3, FUSED>());
@@ -727,11 +753,10 @@ static void launch_pair(dim3 grid, cudaStream_t st, const CUtensorMap &ma, const
                         int M, int K, int nb, int bn, int per, float *part, size_t split_stride,
                         const FusedOut &fo) {
   auto kern = tc_pair_kernel<A_MN, FUSED>;
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<uint64_t> configured{0};
+  once_per_device(configured, [&] {
     XB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TP_SMEM));
-    configured = true;
-  }
+  });
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(tc_threads<false, FUSED>());

@@ -161,7 +161,7 @@ __device__ __forceinline__ Plan make_plan(double lrb, double x_amax, double d_am
 // load.  CTA tile: 32 lines x 32 samples; x lines first, then d lines.
 __global__ void __launch_bounds__(256) trains_kernel(
     const float *__restrict__ X, const float *__restrict__ D, int C, int R, int B,
-    const float *__restrict__ lr, float lr_scalar, const float *__restrict__ xm,
+    const double *__restrict__ lr, double lr_scalar, const float *__restrict__ xm,
     const float *__restrict__ dm, double dw_min, const double *__restrict__ dwmin_b, int BL,
     int blm, const RoundKeys rk, uint64_t seq0, int row0, uint32_t *__restrict__ xw,
     uint32_t *__restrict__ dw, int ldb, int32_t *__restrict__ bl_out) {
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(256) trains_kernel(
   if (threadIdx.x < 32) {
     const int b = b0 + threadIdx.x;
     if (b < B) {
-      const double lrb = (double)(lr ? lr[b] : lr_scalar);
+      const double lrb = lr ? lr[b] : lr_scalar;
       plan[threadIdx.x] =
           make_plan(lrb, (double)xm[b], (double)dm[b], dwmin_b ? dwmin_b[b] : dw_min, BL, blm);
       if (blockIdx.x == 0 && bl_out) bl_out[b] = plan[threadIdx.x].skip ? 0 : plan[threadIdx.x].bl;
@@ -221,11 +221,11 @@ __global__ void __launch_bounds__(256) trains_kernel(
 // (sign of the line, 0 for a no-op sample), sample-major [b][line]
 __global__ void __launch_bounds__(256) probs_kernel(
     const float *__restrict__ X, const float *__restrict__ D, int C, int R,
-    const float *__restrict__ lr, float lr_scalar, const float *__restrict__ xm,
+    const double *__restrict__ lr, double lr_scalar, const float *__restrict__ xm,
     const float *__restrict__ dm, double dw_min, int BL, int blm, int32_t *__restrict__ bl_out,
     double *__restrict__ px, double *__restrict__ pd) {
   const int b = blockIdx.x;
-  const Plan pl = make_plan((double)(lr ? lr[b] : lr_scalar), (double)xm[b], (double)dm[b],
+  const Plan pl = make_plan(lr ? lr[b] : lr_scalar, (double)xm[b], (double)dm[b],
                             dw_min, BL, blm);
   if (threadIdx.x == 0 && bl_out) bl_out[b] = pl.skip ? 0 : pl.bl;
   for (int j = threadIdx.x; j < C; j += blockDim.x) {
@@ -244,8 +244,8 @@ __global__ void __launch_bounds__(256) probs_kernel(
   }
 }
 
-void launch_trains(const Tile &t, const float *X, const float *D, int B, const float *lr_dev,
-                   float lr_scalar, const float *xm, const float *dm, uint64_t seq0,
+void launch_trains(const Tile &t, const float *X, const float *D, int B, const double *lr_dev,
+                   double lr_scalar, const float *xm, const float *dm, uint64_t seq0,
                    uint32_t *xw, uint32_t *dw, int ldb, int32_t *bl, double *px, double *pd,
                    bool deterministic, const double *dwmin_b) {
   if (B <= 0) return;
@@ -676,22 +676,19 @@ static void pulse_dispatch(Tile &t, const uint32_t *xw, const uint32_t *dw, int 
                            LawArgs la, uint32_t call, bool flip) {
   const int smem = PULSE_WARPS * PULSE_QW * 32 * (int)sizeof(uint32_t) +
                    (NOISE ? BM_ANGLES * (int)sizeof(float2) : 0);
-  static bool configured = false;
-  if (!configured) {
+  // persistent grid: every resident CTA slot of the device, capped by the work
+  static std::atomic<uint64_t> configured{0};
+  static std::atomic<int> blocks_of[64];
+  once_per_device(configured, [&] {
     XB_CUDA(cudaFuncSetAttribute(pulse_kernel<LAW, NOISE, COMP>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
-  }
-  // persistent grid: every resident CTA slot of the device, capped by the work
-  static int blocks = 0;
-  if (!blocks) {
-    int per_sm = 0, dev = 0, sms = 0;
+    int per_sm = 0, sms = 0;
     XB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pulse_kernel<LAW, NOISE, COMP>,
                                                           PULSE_WARPS * 32, smem));
-    XB_CUDA(cudaGetDevice(&dev));
-    XB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    blocks = std::max(1, per_sm) * sms;
-  }
+    XB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, current_device()));
+    blocks_of[current_device() & 63].store(std::max(1, per_sm) * sms);
+  });
+  const int blocks = blocks_of[current_device() & 63].load();
   const long items = (long)t.R * ((t.C + 31) / 32);
   const dim3 grid((unsigned)std::min<long>(blocks, (items + PULSE_WARPS - 1) / PULSE_WARPS));
   pulse_kernel<LAW, NOISE, COMP><<<grid, PULSE_WARPS * 32, smem, t.stream>>>(

@@ -45,6 +45,14 @@ class RowShardedTile:
         self.rows = partition_rows(d_out, self.world, self.rank)
         self.local = local
         self.d_out, self.d_in = d_out, d_in
+        # the NCCL collectives are issued on torch's current stream: the tile
+        # must run on that same stream, or a reduction could read a buffer
+        # before the tile's kernel has written it (and vice versa)
+        bind = getattr(local, "set_stream", None)
+        if bind is not None:
+            import torch
+            if torch.cuda.is_available():
+                bind(torch.cuda.current_stream().cuda_stream)
 
     @classmethod
     def create(cls, d_out: int, d_in: int, settings, seed: int, group=None):

@@ -24,6 +24,7 @@ from ._abi import (DeviceParams, InferenceModel, IOParams, Shard, TemporalParams
 _lib = _abi.load()
 
 _fp = C.POINTER(C.c_float)
+_dp = C.POINTER(C.c_double)
 _u32p = C.POINTER(C.c_uint32)
 _i32p = C.POINTER(C.c_int32)
 
@@ -91,7 +92,7 @@ def device_preset(name: str) -> DeviceParams:
 def TileSettings(device: Optional[DeviceParams] = None, forward_io: Optional[IOParams] = None,
                  backward_io: Optional[IOParams] = None, update: Optional[UpdateParams] = None,
                  temporal: Optional[TemporalParams] = None,
-                 mvm_precision: int = _abi.MVM_FP32,
+                 mvm_precision: int = _abi.MVM_TF32X3,
                  weight_precision: int = _abi.W_AUTO) -> TileConfig:
     """proj/include/xbarsim/tile.hpp:38-44 with reference defaults."""
     c = TileConfig()
@@ -121,7 +122,7 @@ def UnitCellSettings(devices=None, gains=None, policy: int = _abi.UC_ALL_TOGETHE
                      forward_io: Optional[IOParams] = None, backward_io: Optional[IOParams] = None,
                      update: Optional[UpdateParams] = None,
                      temporal: Optional[TemporalParams] = None,
-                     mvm_precision: int = _abi.MVM_FP32) -> UnitCellConfig:
+                     mvm_precision: int = _abi.MVM_TF32X3) -> UnitCellConfig:
     """proj/include/xbarsim/compound.hpp:15-28 with reference defaults
     (one default device of gain 1, all_together)."""
     c = UnitCellConfig()
@@ -187,8 +188,9 @@ def _out(out, shape) -> np.ndarray:
 def _lr_array(lr, B: int):
     if lr is None:
         return None
-    arr = np.ascontiguousarray(np.broadcast_to(np.asarray(lr, dtype=np.float32), (B,)))
-    return arr
+    # the reference takes double lr (proj/include/xbarsim/tile.hpp:84); no narrowing
+    arr = np.ascontiguousarray(np.broadcast_to(np.asarray(lr, dtype=np.float64), (B,)))
+    return arr.ctypes.data_as(_dp), arr
 
 
 def _tptr(t) -> int:
@@ -299,7 +301,7 @@ class AnalogTile:
             raise Error("update: x and d batch sizes differ")
         lra = _lr_array(lr, X.shape[0])
         _check(_lib.xb_tile_update(self._h, _ptr(X), _ptr(D), X.shape[0],
-                                   None if lra is None else _ptr(lra)))
+                                   None if lra is None else lra[0]))
 
     def generate_trains(self, x, d, lr):
         """Packed trains the next update(x, d, lr) would draw: (xw, dw, bl)."""
@@ -311,7 +313,7 @@ class AnalogTile:
         dw = np.empty((B, self.rows), dtype=np.uint32)
         bl = np.empty(B, dtype=np.int32)
         _check(_lib.xb_tile_generate_trains(self._h, _ptr(X), _ptr(D), B,
-                                            None if lra is None else _ptr(lra),
+                                            None if lra is None else lra[0],
                                             xw.ctypes.data_as(_u32p), dw.ctypes.data_as(_u32p),
                                             bl.ctypes.data_as(_i32p)))
         return xw, dw, bl
@@ -394,7 +396,7 @@ class AnalogTile:
         B = int(X.shape[0])
         lra = _lr_array(lr, B)
         _check(_lib.xb_tile_update_dev(self._h, _tptr(X), _tptr(D), B,
-                                       None if lra is None else _ptr(lra),
+                                       None if lra is None else lra[0],
                                        None if amax_d is None else _tptr(amax_d)))
 
     # -- PCM inference (inference.hpp:49-70)
@@ -493,7 +495,7 @@ class TransferTile:
         D, _ = _batch(d, self._d_out, "update(d)")
         lra = _lr_array(lr, X.shape[0])
         _check(_lib.xb_transfer_update(self._h, _ptr(X), _ptr(D), X.shape[0],
-                                       None if lra is None else _ptr(lra)))
+                                       None if lra is None else lra[0]))
 
     def end_minibatch(self) -> None:
         _check(_lib.xb_transfer_end_minibatch(self._h))
@@ -585,8 +587,8 @@ class UnitCellTile:
             raise Error("update: x/d lengths do not match tile shape")
         lra = _lr_array(lr, X.shape[0])
         if lra is None:
-            lra = np.full(X.shape[0], 0.01, dtype=np.float32)
-        _check(_lib.xb_unitcell_update(self._h, _ptr(X), _ptr(D), X.shape[0], _ptr(lra)))
+            lra = _lr_array(0.01, X.shape[0])
+        _check(_lib.xb_unitcell_update(self._h, _ptr(X), _ptr(D), X.shape[0], lra[0]))
 
     def get_weights(self) -> np.ndarray:
         w = np.empty((self._d_out, self._d_in), dtype=np.float32)

@@ -149,14 +149,15 @@ int main() {
     s.update.pulse_type = PulseType::deterministic_implicit;
     AnalogTile a(3, 5, s, 3);
     AnalogTile b(3, 5, s, 3);
-    std::vector<float> X, D, L;
+    std::vector<float> X, D;
+    std::vector<double> L;
     for (int t = 0; t < 7; ++t) {
       auto x = random_matrix(1, 5, 1.0, 100 + t), d = random_matrix(1, 3, 1.0, 200 + t);
       std::vector<double> xs(x.data(), x.data() + 5), ds(d.data(), d.data() + 3);
       a.update(xs, ds, 0.02);
       X.insert(X.end(), xs.begin(), xs.end());
       D.insert(D.end(), ds.begin(), ds.end());
-      L.push_back(0.02f);
+      L.push_back(0.02);
     }
     b.update_batch(X.data(), D.data(), 7, L.data());
     CHECK(a.get_weights() == b.get_weights());

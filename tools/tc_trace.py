@@ -1,0 +1,66 @@
+"""Per-CTA timeline of the tcgen05 contraction (experiment build with -DXB_TC_TRACE):
+
+    python paper_2104_02184_b200/build.py -DXB_TC_TRACE --out=$PWD/paper_2104_02184_b200/variants/trace.so
+    XBTILE_LIB=$PWD/paper_2104_02184_b200/variants/trace.so python tools/tc_trace.py [--n 4096]
+
+Runs one noisy forward (default IO, BM off) and one perfect-IO forward at
+batch 256 and prints, over the CTAs of the LAST contraction launch: pipeline
+fill (start -> first stage landed), mainloop (-> accumulator complete),
+output stage (-> end), and the launch span.  Never a bench number."""
+import argparse
+import ctypes as C
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2104_02184_b200 as xb  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, default=4096)
+ap.add_argument("--batch", type=int, default=256)
+ap.add_argument("--precision", type=int, default=xb.MVM_TF32)
+ap.add_argument("--backward", action="store_true")
+a = ap.parse_args()
+from paper_2104_02184_b200 import tile as _tile  # noqa: E402
+lib = _tile.lib()
+fn = lib.xb_debug_tc_trace
+fn.argtypes = [C.POINTER(C.c_uint64), C.c_int]
+s = torch.cuda.Stream()
+torch.cuda.set_stream(s)
+for name, io in (("default", xb.default_io()), ("perfect", xb.perfect_io())):
+    cfg = xb.TileSettings(device=xb.device_preset("reram_sb"), forward_io=io, backward_io=io,
+                          mvm_precision=a.precision)
+    t = xb.AnalogTile(a.n, a.n, cfg, 5)
+    t.set_stream(s.cuda_stream)
+    t.set_weights(np.random.default_rng(7).uniform(-0.1, 0.1, (a.n, a.n)).astype(np.float32))
+    g = torch.Generator(device="cuda")
+    g.manual_seed(3)
+    X = torch.rand(a.batch, a.n, device="cuda", generator=g) * 2 - 1
+    Y = torch.empty(a.batch, a.n, device="cuda")
+    run = (lambda: t.backward_dev(X, Y)) if a.backward else (lambda: t.forward_dev(X, Y))
+    for _ in range(3):
+        run()
+    torch.cuda.synchronize()
+    buf = (C.c_uint64 * (4096 * 4))()
+    fn(buf, 4096)
+    tr = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 4).astype(np.int64)
+    tr = tr[tr[:, 0] > 0]
+    # keep the CTAs of the last launch (start within 1 ms of the latest start)
+    tr = tr[tr[:, 0] > tr[:, 0].max() - 1_000_000]
+    t0 = tr[:, 0].min()
+    fill = (tr[:, 1] - tr[:, 0]) / 1e3
+    main = (tr[:, 2] - tr[:, 1]) / 1e3
+    epi = (tr[:, 3] - tr[:, 2]) / 1e3
+    span = (tr[:, 3].max() - t0) / 1e3
+    late = (tr[:, 0] - t0) / 1e3
+
+    def q(v):
+        return f"min {v.min():6.2f} med {np.median(v):6.2f} max {v.max():6.2f}"
+    print(f"{name:8s} ctas {len(tr)}  span {span:6.2f} us")
+    print(f"   start offset {q(late)}")
+    print(f"   fill         {q(fill)}")
+    print(f"   mainloop     {q(main)}")
+    print(f"   output stage {q(epi)}")
