@@ -8,6 +8,7 @@
 // of launch geometry, batching into kernels and row sharding.
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -115,6 +116,7 @@ struct Quant {
   int bits;
   // fp32 copies for the tensor-core output stage (quantize_f)
   float fbound, fstep, finv_step, flevels_m1;
+  int pow2; // bound is a power of two: every grid point is exact in fp32
 };
 
 __host__ __device__ __forceinline__ Quant make_quant(double bound, int bits) {
@@ -135,6 +137,8 @@ __host__ __device__ __forceinline__ Quant make_quant(double bound, int bits) {
   q.fstep = (float)q.step;
   q.finv_step = (float)q.inv_step;
   q.flevels_m1 = (float)q.levels_m1;
+  int e = 0;
+  q.pow2 = bound > 0.0 && bound < 1e30 && frexp(bound, &e) == 0.5;
   return q;
 }
 

@@ -69,6 +69,18 @@ struct IoDev {
 };
 IoDev make_io(const xb_io_params &io);
 
+// In-stream collectives of a row-sharded tile (xb_comm, xb_comm.cu): NCCL
+// over NVLink between processes, or a loopback group of shard handles in one
+// process.  Every call is enqueued on `s` and returns without waiting.
+struct Collective {
+  virtual ~Collective() = default;
+  virtual int size() const = 0;
+  virtual int rank() const = 0;
+  virtual void allreduce_max_i32(int *buf, size_t n, cudaStream_t s) = 0;
+  virtual void allreduce_max_f32(float *buf, size_t n, cudaStream_t s) = 0;
+  virtual void allreduce_sum_f32(float *buf, size_t n, cudaStream_t s) = 0;
+};
+
 // makes `dev` current for the scope of one ABI call on a tile (a handle keeps
 // the device it was created on; the caller's current device is restored)
 struct DevScope {
@@ -88,6 +100,7 @@ struct DevScope {
 struct Tile {
   xb_tile_config cfg;
   int device = 0;            // CUDA device ordinal of every buffer and the stream
+  Collective *comm = nullptr; // row shards: the group of the other shards (borrowed)
   int R = 0, C = 0;          // local rows, columns
   int row0 = 0, R_total = 0; // first global row, global rows
   int ld = 0;                // leading dimension of W / params (floats)

@@ -22,9 +22,6 @@ namespace xb {
 
 namespace {
 
-constexpr int PREP_THREADS = 512;
-constexpr int PREP_VPT = 8; // values per thread kept in registers (n <= 4096)
-
 __device__ __forceinline__ float block_max(float m, float *red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   m = warp_max(m);
@@ -39,160 +36,85 @@ __device__ __forceinline__ float block_max(float m, float *red) {
   return red[32];
 }
 
-__global__ void __launch_bounds__(PREP_THREADS) prep_kernel(const float *__restrict__ X, int n,
-                                                             int ldx, float *__restrict__ Xt,
-                                                             int ldt,
-                                                             SampleState *__restrict__ st,
-                                                             IoDev io, Key key, uint64_t seq0,
-                                                             int first_pass,
-                                                             const float *__restrict__ amax_in,
-                                                             int *__restrict__ sat,
-                                                             const int *__restrict__ map,
-                                                             int in0) {
-  // in0: global index of input 0 (row-shard backward: the shard's first row),
-  // so the input-noise counters match the unsharded tile's
-  // map != nullptr: a compacted bound-management re-issue -- block i prepares
-  // sample map[i] into x~ row i (compact_kernel already re-armed the flags)
-  const int b = map ? map[blockIdx.x] : blockIdx.x;
-  SampleState s = st[b];
-  if (map) {
-    s.m += 1;
-  } else if (!first_pass) { // bound management: re-issue the samples that saturated
-    const int again = s.active && sat[b];
-    __syncthreads(); // every thread has read the flag before it is re-armed
-    if (threadIdx.x == 0) sat[b] = 0;
-    if (!again) {
-      if (threadIdx.x == 0 && s.active) {
-        s.active = 0;
-        st[b] = s;
-      }
-      return;
-    }
-    s.m += 1;
-  }
-  const float *x = X + (size_t)b * ldx;
-  float *xt = Xt + (size_t)blockIdx.x * ldt;
+constexpr int PREP_THREADS = 512;
+
+// Pass 0: alpha = max|x| per sample (abs-max; or the all-reduced global value
+// of a row shard), x~ at m = 0, ||x~||.  Block 0 also clears the
+// bound-management buffers of the call (flags, counters, grid barriers), so
+// no memset precedes the contraction.
+__global__ void __launch_bounds__(PREP_THREADS) prep_kernel(
+    const float *__restrict__ X, int n, float *__restrict__ Xt, int ldt,
+    SampleState *__restrict__ st, IoDev io, Key key, uint64_t seq0,
+    const float *__restrict__ amax_in, int in0, int *__restrict__ bm_clear, int bm_words) {
+  // the contraction (a programmatic dependent) may start its prologue and
+  // W loads now; it waits for this grid before touching x~ / st / flags
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int b = blockIdx.x;
   __shared__ float red[33];
-  // the sample stays in registers between the max and the conversion when it fits
-  const bool in_regs = n <= PREP_THREADS * PREP_VPT;
-  float v[PREP_VPT];
-  if (in_regs) {
-#pragma unroll
-    for (int u = 0; u < PREP_VPT; ++u) {
-      const int j = threadIdx.x + u * PREP_THREADS;
-      v[u] = j < n ? x[j] : 0.f;
-    }
-  }
-  if (first_pass) {
-    float m = 0.f;
-    if (amax_in) {
-      m = amax_in[b];
-    } else {
-      if (in_regs) {
-#pragma unroll
-        for (int u = 0; u < PREP_VPT; ++u) m = fmaxf(m, fabsf(v[u]));
-      } else {
-        for (int j = threadIdx.x; j < n; j += blockDim.x) m = fmaxf(m, fabsf(x[j]));
-      }
-      m = block_max(m, red);
-    }
-    s.alpha = (m == 0.f) ? 0.f : (io.nm_absmax ? m : 1.f);
-    s.m = 0;
-    s.active = 1;
-  }
-  const uint64_t seq = seq0 + (uint64_t)b;
-  const double inv = (s.alpha == 0.f) ? 0.0 : 1.0 / ((double)s.alpha * pow2i(s.m));
-  auto convert = [&](float xv, int j) -> float {
-    if (io.perfect) return xv;
-    if (s.alpha == 0.f) return 0.f;
-    double q = quantize((double)xv * inv, io.dac); // x / alpha, then the DAC (io.cpp:122-130)
-    if (io.sigma_inp > 0.0) {
-      const float z = normal1((uint32_t)(j + in0), (uint32_t)seq, (uint32_t)(seq >> 32) | (s.m << 24),
-                              TAG_IN_NOISE << 24, key);
-      q += io.sigma_inp * (double)z;
-    }
-    return (float)q;
-  };
-  float nrm = 0.f;
-  if (in_regs) {
-#pragma unroll
-    for (int u = 0; u < PREP_VPT; ++u) {
-      const int j = threadIdx.x + u * PREP_THREADS;
-      if (j < n) {
-        const float f = convert(v[u], j);
-        xt[j] = f;
-        nrm = fmaf(f, f, nrm);
-      }
-    }
+  if (bm_clear && b == 0)
+    for (int i = threadIdx.x; i < bm_words; i += blockDim.x) bm_clear[i] = 0;
+  const float *x = X + (size_t)b * n;
+  float m = 0.f;
+  if (amax_in) {
+    m = amax_in[b];
   } else {
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
-      const float f = convert(x[j], j);
-      xt[j] = f;
-      nrm = fmaf(f, f, nrm);
-    }
+    for (int j = threadIdx.x; j < n; j += blockDim.x) m = fmaxf(m, fabsf(x[j]));
+    m = block_max(m, red);
   }
-  nrm = warp_sum(nrm);
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) red[warp] = nrm;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float tot = 0.f;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
-    s.norm = sqrtf(tot);
-    st[b] = s;
-  }
+  SampleState s;
+  s.alpha = (m == 0.f) ? 0.f : (io.nm_absmax ? m : 1.f);
+  s.m = 0;
+  s.active = 1;
+  s.norm = prep_row(x, n, Xt + (size_t)b * ldt, s, io, key, seq0 + (uint64_t)b, in0, red);
+  if (threadIdx.x == 0) st[b] = s;
 }
 
-// Bound-management bookkeeping between passes: samples that saturated in the
-// last pass (and are still active) are listed in map[0..n) -- in any order:
-// each sample's column of the contraction is independent of its position --
-// the others are retired; all flags are re-armed for the next pass.
-__global__ void __launch_bounds__(256) compact_kernel(int *__restrict__ sat,
-                                                      SampleState *__restrict__ st, int B,
-                                                      int *__restrict__ map,
+// Re-issue prep (host-driven passes): block c < *count prepares the x~ row c
+// of sample map[c] at m + 1.
+__global__ void __launch_bounds__(PREP_THREADS) reprep_kernel(
+    const float *__restrict__ X, int n, float *__restrict__ Xt, int ldt,
+    SampleState *__restrict__ st, IoDev io, Key key, uint64_t seq0, int in0,
+    const int *__restrict__ map, const int *__restrict__ count) {
+  const int c = blockIdx.x;
+  if (c >= *count) return;
+  __shared__ float red[33];
+  const int b = map[c];
+  SampleState s = st[b];
+  s.m += 1;
+  s.norm = prep_row(X + (size_t)b * n, n, Xt + (size_t)c * ldt, s, io, key, seq0 + (uint64_t)b,
+                    in0, red);
+  if (threadIdx.x == 0) st[b] = s;
+}
+
+// Host-driven re-issue bookkeeping (one block per N slab): the samples whose
+// pass-(p-1) flag is set, ascending, into map; their number into *count; the
+// flags pass p will write are cleared.
+__global__ void __launch_bounds__(256) compact_kernel(int *__restrict__ flags, int nb, int n0,
+                                                      int prev_pass, int *__restrict__ map,
                                                       int *__restrict__ count) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  bool again = false;
-  if (b < B) {
-    SampleState s = st[b];
-    again = s.active && sat[b];
-    sat[b] = 0;
-    if (!again && s.active) {
-      s.active = 0;
-      st[b] = s;
-    }
-  }
-  const unsigned m = __ballot_sync(0xffffffffu, again);
-  int base = 0;
-  if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(count, __popc(m));
-  base = __shfl_sync(0xffffffffu, base, 0);
-  if (again) map[base + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = b;
+  __shared__ int cnt[40];
+  const int n = block_compact(flags + (prev_pass & 1) * nb, nb, n0, map, cnt);
+  int *nf = flags + ((prev_pass + 1) & 1) * nb;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) nf[i] = 0;
+  if (threadIdx.x == 0) *count = n;
 }
 
 // --------------------------------------------------------------- SIMT GEMM
 // acc[b][o] = sum_k A(o, k) x~[b][k];  forward: A(o,k) = W[o][k] (K-major),
 // backward: A(o,k) = W[k][o] (M-major).  Tile 64 (o) x 64 (b) x 16 (k),
-// 256 threads x (4 x 4) outputs.  Samples of inactive BM passes are skipped
-// per tile.
+// 256 threads x (4 x 4) outputs.  n_rows != nullptr: a compacted BM
+// re-issue, only the first *n_rows rows of x~ are valid.
 template <bool TRANS>
 __global__ void __launch_bounds__(256) mvm_simt_kernel(const float *__restrict__ W, int ldw,
                                                         int M, int K, const float *__restrict__ Xt,
                                                         int ldt, int B, float *__restrict__ acc,
-                                                        int lda, const SampleState *__restrict__ st,
-                                                        int first_pass) {
+                                                        int lda, const int *__restrict__ n_rows) {
   __shared__ float As[16][64 + 4];
   __shared__ float Bs[16][64 + 4];
-  __shared__ int any_active;
   const int m0 = blockIdx.x * 64, b0 = blockIdx.y * 64;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  if (!first_pass) {
-    if (threadIdx.x == 0) any_active = 0;
-    __syncthreads();
-    if (threadIdx.x < 64 && b0 + threadIdx.x < B && st[b0 + threadIdx.x].active) any_active = 1;
-    __syncthreads();
-    if (!any_active) return;
-  }
+  if (n_rows) B = min(B, *n_rows);
+  if (b0 >= B) return;
   float c[4][4] = {};
   for (int k0 = 0; k0 < K; k0 += 16) {
     // A tile
@@ -244,19 +166,21 @@ __global__ void __launch_bounds__(256) mvm_simt_kernel(const float *__restrict__
 }
 
 // --------------------------------------------------------------- epilogue
-// one thread = one group of 4 outputs of one sample (xb_mvm_common.cuh)
+// one thread = one group of 4 outputs of one sample (xb_mvm_common.cuh).
+// acc row r (r < n; n = *n_rows for a compacted re-issue) holds sample
+// map[r] (re-issue) or n0 + r (pass 0); rows of one N slab per launch.
 __global__ void __launch_bounds__(256) epilogue_kernel(const float *__restrict__ acc, int lda,
                                                         int nsplit, size_t split_stride, int M,
                                                         int o0, float *__restrict__ Y, int ldy,
-                                                        SampleState *__restrict__ st, IoDev io,
-                                                        Key key, uint64_t seq0,
-                                                        int *__restrict__ sat, int first_pass,
-                                                        int B, int pass_slot,
-                                                        const int *__restrict__ map) {
-  // acc row blockIdx.y holds sample b (compacted re-issue: b = map[row])
-  const int row = blockIdx.y, b = map ? map[row] : row;
+                                                        const SampleState *__restrict__ st,
+                                                        IoDev io, Key key, uint64_t seq0,
+                                                        BmBufs bm, int nb, int n0, int pass,
+                                                        const int *__restrict__ map,
+                                                        const int *__restrict__ n_rows) {
+  const int row = blockIdx.y;
+  if (n_rows && row >= *n_rows) return;
+  const int b = map ? map[row] : n0 + row;
   const SampleState s = st[b];
-  if (!first_pass && !s.active) return;
   const int g = (o0 >> 2) + blockIdx.x * blockDim.x + threadIdx.x;
   if (4 * g >= o0 + M) return;
   float a[4] = {0.f, 0.f, 0.f, 0.f};
@@ -269,7 +193,7 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const float *__restrict__
   }
   const bool hit = epilogue_group4(a, g, o0, M, s, io, key, seq0 + (uint64_t)b,
                                    Y + (size_t)b * ldy);
-  bm_flag(hit, s, io, sat, b, B, pass_slot);
+  bm_flag(hit, s, io, bm.flags + (pass & 1) * nb + (b - n0), bm.counts + pass);
 }
 
 // Row-shard backward, phase 1: the shard's column sums plus its share of the
@@ -325,34 +249,57 @@ __global__ void __launch_bounds__(256) finish_kernel(const float *__restrict__ P
 
 struct MvmScratch {
   float *xt;
-  float *acc;
+  float *acc;   // pass 0 partial sums [nsplit][B][M] (unfused)
+  float *acc_r; // re-issue partial sums [nsplit][256][M] (unfused)
   SampleState *st;
-  int *sat; // [B] flags, then one saturation counter per BM pass, then the compaction counters
-  int *map; // [B] compacted re-issue list
+  int *bm;      // per slab: flags [2][256], counts [64]; then grid barriers [nslab]
+  int *map;     // [B]
+  int bm_words;
 };
 
+constexpr int SLAB = 256;
+
 MvmScratch carve(Tile &t, int B, int K, int M, int nsplit) {
+  const int nslab = (B + SLAB - 1) / SLAB;
   const size_t xt_b = (size_t)B * K * sizeof(float);
   const size_t acc_b = (size_t)nsplit * B * M * sizeof(float);
+  const size_t accr_b = nsplit ? (size_t)nsplit * std::min(B, SLAB) * M * sizeof(float) : 0;
   const size_t st_b = (size_t)B * sizeof(SampleState);
-  const size_t sat_b = (size_t)(B + 64) * sizeof(int); // flags + per-pass counters
+  const int bm_words = nslab * (BM_SLAB_WORDS + 1);
+  const size_t bm_b = (size_t)bm_words * sizeof(int);
   const size_t map_b = (size_t)B * sizeof(int);
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  char *p = (char *)t.s_io.get(al(xt_b) + al(acc_b) + al(st_b) + al(sat_b) + al(map_b));
+  char *p = (char *)t.s_io.get(al(xt_b) + al(acc_b) + al(accr_b) + al(st_b) + al(bm_b) +
+                               al(map_b));
   MvmScratch s;
   s.xt = (float *)p;
-  s.acc = (float *)(p + al(xt_b));
-  s.st = (SampleState *)(p + al(xt_b) + al(acc_b));
-  s.sat = (int *)(p + al(xt_b) + al(acc_b) + al(st_b));
-  s.map = (int *)(p + al(xt_b) + al(acc_b) + al(st_b) + al(sat_b));
+  p += al(xt_b);
+  s.acc = (float *)p;
+  p += al(acc_b);
+  s.acc_r = (float *)p;
+  p += al(accr_b);
+  s.st = (SampleState *)p;
+  p += al(st_b);
+  s.bm = (int *)p;
+  p += al(bm_b);
+  s.map = (int *)p;
+  s.bm_words = bm_words;
   return s;
 }
 
+BmBufs slab_bufs(const MvmScratch &s, int slab) {
+  BmBufs b;
+  b.flags = s.bm + (size_t)slab * BM_SLAB_WORDS;
+  b.counts = b.flags + 2 * SLAB;
+  b.map = s.map + (size_t)slab * SLAB;
+  return b;
+}
+
 template <bool TRANS>
-void gemm(Tile &t, const MvmScratch &s, int M, int K, int ldt, int B, int first) {
+void gemm(Tile &t, const float *xt, int ldt, int M, int K, int B, float *acc,
+          const int *n_rows) {
   dim3 grid((M + 63) / 64, (B + 63) / 64);
-  mvm_simt_kernel<TRANS><<<grid, 256, 0, t.stream>>>(t.W, t.ld, M, K, s.xt, ldt, B, s.acc, M,
-                                                     s.st, first);
+  mvm_simt_kernel<TRANS><<<grid, 256, 0, t.stream>>>(t.W, t.ld, M, K, xt, ldt, B, acc, M, n_rows);
   count_launch();
   XB_CUDA(cudaGetLastError());
 }
@@ -363,14 +310,31 @@ static bool unfused_requested() {
   const char *e = getenv("XB_MVM_UNFUSED");
   return e && e[0] == '1';
 }
+// XB_BM_HOST_PASSES=1 forces host-driven re-issue passes on the fused path
+// (the sharded mode; tests compare it with the in-kernel loop)
+static bool host_passes_requested() {
+  const char *e = getenv("XB_BM_HOST_PASSES");
+  return e && e[0] == '1';
+}
 
-// one full noisy MVM in direction TRANS (forward: false)
 // tensor-core contraction at TF32 / 3xTF32 (B >= 16); the fp32 SIMT kernel
 // otherwise (exact-fp32 parity mode, tiny batches)
 static bool use_tc(const Tile &t, int B) {
   return (t.cfg.mvm_precision == XB_MVM_TF32 || t.cfg.mvm_precision == XB_MVM_TF32X3) && B >= 16;
 }
 
+// One full noisy MVM in direction TRANS (forward: false).  Nothing here waits
+// on the device:
+//  * pass 0: prep (alpha, x~, norms; clears the BM buffers) + contraction with
+//    the output stage;
+//  * bound management, tensor cores, unsharded: the re-issue passes run inside
+//    the contraction launch (grid barriers between passes);
+//  * otherwise (SIMT, unfused, row shards, or a grid that cannot be
+//    co-resident): bm_max_iter re-issue passes are enqueued per N slab --
+//    compaction, prep, contraction, output stage -- each of which leaves at
+//    once when the previous pass flagged nothing.  Row shards all-reduce the
+//    flags (max) before every compaction, so every shard re-issues exactly
+//    the samples the unsharded tile would.
 template <bool TRANS>
 void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io_in, Key key,
              uint64_t seq0, const float *amax_in, bool skip_epilogue, float *dPartial) {
@@ -382,72 +346,113 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io_in, 
   IoDev io = io_in;
   io.exact = !tc; // fp64 output stage only behind the exact fp32 contraction
   const int o0 = TRANS ? 0 : t.row0; // global index of output 0 (noise counters)
+  const int in0 = TRANS ? t.row0 : 0; // global index of input 0 (input-noise counters)
   // the output stage runs inside the tcgen05 kernel (K-splits reduced over a
   // thread-block cluster) unless the caller wants raw partial sums, the noise
   // groups of 4 outputs do not align with the tile, or a cluster would exceed
-  // the portable 8 CTAs
-  // (both paths use the same K-splits, so they agree bit for bit)
+  // the portable 8 CTAs (both paths use the same K-splits: bit-identical)
   const int splits = tc ? tc_used_splits(K, std::min(8, tc_splits(M, K, x3))) : 1;
   const bool fused = tc && !skip_epilogue && (o0 & 3) == 0 && !unfused_requested();
   const int ldt = (K + 3) & ~3; // x~ rows padded to 16 bytes (TMA global stride)
   MvmScratch s = carve(t, B, ldt, M, fused ? 0 : splits);
-  if (io.bm) XB_CUDA(cudaMemsetAsync(s.sat, 0, sizeof(int) * (B + 64), t.stream));
-  const int passes = io.bm ? 1 + io.bm_max_iter : 1;
-  int nrun = B;             // samples (rows of x~) in this pass
-  const int *map = nullptr; // tensor-core re-issues: the compacted list of saturated samples
-  for (int pass = 0; pass < passes; ++pass) {
-    const int first = pass == 0;
-    prep_kernel<<<nrun, PREP_THREADS, 0, t.stream>>>(dIn, K, K, s.xt, ldt, s.st, io, key, seq0,
-                                                      first, amax_in, s.sat, map,
-                                                      TRANS ? t.row0 : 0);
+  const bool bm = io.bm && !skip_epilogue;
+  const bool sharded_bm = bm && t.comm && !TRANS;
+  const int nslab = (B + SLAB - 1) / SLAB;
+  int *bars = s.bm + (size_t)nslab * BM_SLAB_WORDS;
+
+  const bool want_loop = fused && bm && !sharded_bm && !host_passes_requested();
+  prep_kernel<<<B, PREP_THREADS, 0, t.stream>>>(dIn, K, s.xt, ldt, s.st, io, key, seq0, amax_in,
+                                                 in0, bm ? s.bm : nullptr, s.bm_words);
+  count_launch();
+  XB_CUDA(cudaGetLastError());
+
+  FusedOut fo{};
+  fo.Y = dOut;
+  fo.ldy = M;
+  fo.st = s.st;
+  fo.io = io;
+  fo.key = key;
+  fo.seq0 = seq0;
+  fo.bm = slab_bufs(s, 0);
+  fo.pass = 0;
+  fo.o0 = o0;
+  fo.X = dIn;
+  fo.K = K;
+  fo.in0 = in0;
+  fo.xt = s.xt;
+  fo.ldt = ldt;
+  fo.bar = reinterpret_cast<unsigned *>(bars);
+
+  // ---- pass 0
+  bool looped = false;
+  int nsplit = 1;
+  if (fused) {
+    looped = tc_gemm(t, TRANS, x3, s.xt, ldt, B, nullptr, splits, &fo, nullptr, want_loop);
+  } else if (tc) {
+    tc_gemm(t, TRANS, x3, s.xt, ldt, B, s.acc, splits, nullptr);
+    nsplit = splits;
+  } else {
+    gemm<TRANS>(t, s.xt, ldt, M, K, B, s.acc, nullptr);
+  }
+  if (skip_epilogue) { // row shard: partial sums + this shard's weight-noise fold
+    dim3 eg((M + 255) / 256, B);
+    partial_kernel<<<eg, 256, 0, t.stream>>>(s.acc, M, nsplit, (size_t)B * M, dPartial, s.st,
+                                             io, key, seq0,
+                                             (TAG_W_NOISE << 24) | (uint32_t)t.row0);
     count_launch();
     XB_CUDA(cudaGetLastError());
-    int nsplit = 1;
-    if (fused) {
-      FusedOut fo{dOut, M, s.st, io, key, seq0, s.sat, first, B, pass, o0, 0, map};
-      tc_gemm(t, TRANS, x3, s.xt, ldt, nrun, nullptr, splits, &fo);
-    } else if (tc) {
-      tc_gemm(t, TRANS, x3, s.xt, ldt, nrun, s.acc, splits, nullptr);
-      nsplit = splits;
-    } else { // SIMT: re-issues run over the whole batch, skipping inactive tiles
-      gemm<TRANS>(t, s, M, K, ldt, B, first);
-    }
-    if (skip_epilogue) { // row shard: partial sums + this shard's weight-noise fold
-      dim3 eg((M + 255) / 256, B);
-      partial_kernel<<<eg, 256, 0, t.stream>>>(s.acc, M, nsplit, (size_t)B * M, dPartial, s.st,
-                                               io, key, seq0,
-                                               (TAG_W_NOISE << 24) | (uint32_t)t.row0);
-      count_launch();
-      XB_CUDA(cudaGetLastError());
-      return;
-    }
-    if (!fused) {
-      dim3 eg((out_groups(o0, M) + 255) / 256, nrun);
-      epilogue_kernel<<<eg, 256, 0, t.stream>>>(s.acc, M, nsplit, (size_t)nrun * M, M, o0, dOut,
-                                                M, s.st, io, key, seq0, s.sat, first, B, pass,
-                                                map);
+    return;
+  }
+  if (!fused) {
+    for (int sl = 0; sl < nslab; ++sl) {
+      const int n0 = sl * SLAB, nb = std::min(SLAB, B - n0);
+      dim3 eg((out_groups(o0, M) + 255) / 256, nb);
+      epilogue_kernel<<<eg, 256, 0, t.stream>>>(s.acc + (size_t)n0 * M, M, nsplit,
+                                                (size_t)B * M, M, o0, dOut, M, s.st, io, key,
+                                                seq0, slab_bufs(s, sl), nb, n0, 0, nullptr,
+                                                nullptr);
       count_launch();
       XB_CUDA(cudaGetLastError());
     }
-    if (io.bm && pass + 1 < passes) {
-      // bound management: re-issue while some sample saturated.  The epilogue
-      // counted them; the count crosses to the host (one 4-byte read and a
-      // stream sync per pass with BM on).  On the tensor cores only the
-      // saturated samples are recomputed: compact_kernel lists them, retires
-      // the rest and re-arms the flags (the SIMT path's prep does the latter).
-      if (!t.bm_count) XB_CUDA(cudaMallocHost(&t.bm_count, sizeof(int)));
-      XB_CUDA(cudaMemcpyAsync(t.bm_count, s.sat + B + pass, sizeof(int),
-                              cudaMemcpyDeviceToHost, t.stream));
-      XB_CUDA(cudaStreamSynchronize(t.stream));
-      const int nsat = *t.bm_count;
-      if (nsat == 0) break;
-      if (tc) {
-        compact_kernel<<<(B + 255) / 256, 256, 0, t.stream>>>(s.sat, s.st, B, s.map,
-                                                              s.sat + B + 32 + pass);
+  }
+  if (!bm || looped) return;
+
+  // ---- host-driven re-issue passes (enqueued; each leaves early when idle)
+  for (int pass = 1; pass <= io.bm_max_iter; ++pass) {
+    for (int sl = 0; sl < nslab; ++sl) {
+      const int n0 = sl * SLAB, nb = std::min(SLAB, B - n0);
+      BmBufs bb = slab_bufs(s, sl);
+      if (sharded_bm) // every shard re-issues the samples saturated on ANY shard
+        t.comm->allreduce_max_i32(bb.flags + ((pass - 1) & 1) * nb, nb, t.stream);
+      int *cnt = bb.counts + 32 + pass;
+      compact_kernel<<<1, 256, 0, t.stream>>>(bb.flags, nb, n0, pass - 1, bb.map, cnt);
+      count_launch();
+      float *xt = s.xt + (size_t)n0 * ldt; // the slab's x~ rows, compacted from row 0
+      reprep_kernel<<<nb, PREP_THREADS, 0, t.stream>>>(dIn, K, xt, ldt, s.st, io, key, seq0, in0,
+                                                       bb.map, cnt);
+      count_launch();
+      XB_CUDA(cudaGetLastError());
+      if (fused) { // one slab: its x~ rows, BM buffers and first sample
+        FusedOut f = fo;
+        f.bm = bb;
+        f.pass = pass;
+        f.n_dev = cnt;
+        f.n0 = n0;
+        f.xt = xt;
+        f.loop = 0;
+        tc_gemm(t, TRANS, x3, xt, ldt, nb, nullptr, splits, &f);
+      } else {
+        float *acc = tc ? s.acc_r : s.acc;
+        if (tc)
+          tc_gemm(t, TRANS, x3, xt, ldt, nb, acc, splits, nullptr, cnt);
+        else
+          gemm<TRANS>(t, xt, ldt, M, K, nb, acc, cnt);
+        dim3 eg((out_groups(o0, M) + 255) / 256, nb);
+        epilogue_kernel<<<eg, 256, 0, t.stream>>>(acc, M, tc ? splits : 1, (size_t)nb * M, M, o0,
+                                                  dOut, M, s.st, io, key, seq0, bb, nb, n0, pass,
+                                                  bb.map, cnt);
         count_launch();
         XB_CUDA(cudaGetLastError());
-        map = s.map;
-        nrun = nsat;
       }
     }
   }

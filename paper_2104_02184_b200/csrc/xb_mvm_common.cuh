@@ -44,25 +44,44 @@ __host__ __device__ __forceinline__ int out_groups(int o0, int M) {
   return ((o0 + M - 1) >> 2) - (o0 >> 2) + 1;
 }
 
+// stores the outputs 4g..4g+3 that fall in [o0, o0 + M): one 16-byte store
+// when the group is whole and aligned, else per element
+__device__ __forceinline__ void store_group4(const float y[4], int g, int o0, int M,
+                                             float *__restrict__ yrow) {
+  const int o = 4 * g - o0;
+  if (o >= 0 && o + 3 < M && ((reinterpret_cast<uintptr_t>(yrow + o) & 15u) == 0)) {
+    *reinterpret_cast<float4 *>(yrow + o) = make_float4(y[0], y[1], y[2], y[3]);
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (o + k >= 0 && o + k < M) yrow[o + k] = y[k];
+}
+
 // Outputs 4g..4g+3 (global index) of one sample: a[k] = their contraction
 // sums; the ones inside [o0, o0 + M) are written to yrow[o - o0].  Returns
 // whether any of them reached the ADC bound (bound management).
 __device__ __forceinline__ bool epilogue_group4(const float a[4], int g, int o0, int M,
                                                 const SampleState &s, const IoDev &io, Key key,
                                                 uint64_t seq, float *__restrict__ yrow) {
-  uint32_t w[4] = {0u, 0u, 0u, 0u};
-  const bool noisy = !io.perfect && (io.sigma_w > 0.0 || io.sigma_out > 0.0);
-  if (noisy) out_noise_words((uint32_t)g, seq, s.m, key, w);
+  float y[4];
   bool hit = false;
-  if (!io.exact && !io.perfect) {
+  if (io.perfect) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) y[k] = a[k];
+    store_group4(y, g, o0, M, yrow);
+    return false;
+  }
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
+  const bool noisy = io.sigma_w > 0.0 || io.sigma_out > 0.0;
+  if (noisy) out_noise_words((uint32_t)g, seq, s.m, key, w);
+  if (!io.exact) {
     // fp32 output stage (tensor-core modes): alpha 2^m y rounds once in fp32,
     // exactly like the fp64 product cast to fp32 (2^m is exact)
     const float scale = s.alpha == 0.f ? 1.f : s.alpha * (float)pow2i(s.m);
     const float sw = (float)io.sigma_w * s.norm, so = (float)io.sigma_out;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const int o = 4 * g + k - o0;
-      if (o < 0 || o >= M) continue;
       float z0 = 0.f, z1 = 0.f;
       if (noisy) box_muller16(w[k], z0, z1);
       float v;
@@ -72,21 +91,18 @@ __device__ __forceinline__ bool epilogue_group4(const float a[4], int g, int o0,
         v = a[k];
         if (io.sigma_w > 0.0) v = fmaf(sw, z0, v);
         v = fmaf(so, z1, v);
-        hit |= fabsf(v) >= io.adc.fbound;
+        // only outputs of this tile/shard count (a group may straddle its edge)
+        const int o = 4 * g + k - o0;
+        hit |= (o >= 0 && o < M) && fabsf(v) >= io.adc.fbound;
       }
-      yrow[o] = scale * quantize_f(v, io.adc);
+      y[k] = scale * quantize_f(v, io.adc);
     }
+    store_group4(y, g, o0, M, yrow);
     return hit;
   }
   const double scale = s.alpha == 0.f ? 1.0 : (double)s.alpha * pow2i(s.m);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const int o = 4 * g + k - o0;
-    if (o < 0 || o >= M) continue;
-    if (io.perfect) {
-      yrow[o] = a[k];
-      continue;
-    }
     float z0 = 0.f, z1 = 0.f;
     if (noisy) box_muller16(w[k], z0, z1);
     double v;
@@ -96,43 +112,192 @@ __device__ __forceinline__ bool epilogue_group4(const float a[4], int g, int o0,
       v = (double)a[k];
       if (io.sigma_w > 0.0) v += io.sigma_w * (double)s.norm * (double)z0;
       if (io.sigma_out > 0.0) v += io.sigma_out * (double)z1;
-      hit |= fabs(v) >= io.adc.bound;
+      const int o = 4 * g + k - o0;
+      hit |= (o >= 0 && o < M) && fabs(v) >= io.adc.bound;
     }
-    yrow[o] = (float)(scale * quantize(v, io.adc));
+    y[k] = (float)(scale * quantize(v, io.adc));
   }
+  store_group4(y, g, o0, M, yrow);
   return hit;
 }
 
 // BM bookkeeping: one flag write per warp (a saturating sample saturates many
-// outputs; per-thread atomics on the same word would serialise)
+// outputs; per-thread atomics on the same word would serialise).  flag = this
+// sample's word in the pass's flag array, count = the pass's counter.
 __device__ __forceinline__ void bm_flag(bool hit, const SampleState &s, const IoDev &io,
-                                        int *sat, int b, int B, int pass_slot) {
+                                        int *flag, int *count) {
   if (io.bm && s.alpha != 0.f && s.m < io.bm_max_iter) {
     const unsigned any = __ballot_sync(__activemask(), hit);
-    if (hit && (threadIdx.x & 31) == __ffs(any) - 1 && atomicExch(sat + b, 1) == 0)
-      atomicAdd(sat + B + pass_slot, 1);
+    if (hit && (threadIdx.x & 31) == __ffs(any) - 1 && atomicExch(flag, 1) == 0)
+      atomicAdd(count, 1);
   }
 }
 
-// arguments of the fused output stage
+// Bound-management bookkeeping, per N slab of nb samples (slab-local sample
+// index b - n0):  pass p writes its saturation flags to flags[(p & 1) nb ..]
+// and counts them in counts[p]; the re-issue of pass p + 1 takes the flagged
+// samples of pass p (ascending order), and clears the other parity's flags
+// for pass p + 1 to write.
+// words per N slab (<= 256 samples): flags [2][256], counts [64]
+constexpr int BM_SLAB_WORDS = 2 * 256 + 64;
+struct BmBufs {
+  int *flags;  // [2][nb]
+  int *counts; // [64] per pass; [32 + p]: compacted count for pass p (host-driven rounds)
+  int *map;    // [nb] compacted sample list (global sample index)
+};
+
+// (x~ prep, one sample) proj/src/io.cpp:117-131: x~_j = Q_dac(x_j / (alpha 2^m))
+// + sigma_inp xi_j in fp64 converter arithmetic, ||x~|| returned in every
+// thread.  All threads of the block take part; red: >= 33 floats of shared.
+__device__ __forceinline__ float prep_row(const float *__restrict__ x, int n,
+                                          float *__restrict__ xt, const SampleState &s,
+                                          const IoDev &io, Key key, uint64_t seq, int in0,
+                                          float *red) {
+  const double inv = (s.alpha == 0.f) ? 0.0 : 1.0 / ((double)s.alpha * pow2i(s.m));
+  // fp32 fast path of the DAC, bit-identical to the fp64 quantizer: the grid
+  // index is k = round_half_away(t), t = x inv L / (2 b) + (L - 1) / 2
+  // (L = 2^bits).  In fp32, t carries at most L 2^-23 of error; outside a
+  // window of L 2^-20 around a half-integer both evaluations round the same
+  // way, and inside it (rare) the element takes the fp64 path.  Without it
+  // the DAC was fp64-conversion bound (~4 us per 4096-wide sample on B200).
+  const bool fast = !io.perfect && s.alpha != 0.f && io.dac.bits > 0 && io.dac.bits <= 16 &&
+                    io.dac.pow2 && io.sigma_inp == 0.0;
+  const float a32 = fast ? (float)(inv * exp2((double)io.dac.bits) / (2.0 * io.dac.bound)) : 0.f;
+  const float c032 = 0.5f * (io.dac.flevels_m1);   // (L - 1) / 2, exact
+  const float tie_eps = fast ? ldexpf(1.f, io.dac.bits - 20) : 0.f;
+  auto convert = [&](float xv, int j) -> float {
+    if (io.perfect) return xv;
+    if (s.alpha == 0.f) return 0.f;
+    if (fast) {
+      if (xv == 0.f) return 0.f; // exact zero passes (io.cpp:44)
+      const float t = fmaf(xv, a32, c032);
+      const float fr = t - floorf(t);
+      if (fabsf(fr - 0.5f) > tie_eps) {
+        float k = floorf(t + 0.5f); // not a tie: round-half-away == round-half-up here
+        k = fminf(fmaxf(k, 0.f), io.dac.flevels_m1);
+        return fmaf(k + 0.5f, io.dac.fstep, -io.dac.fbound);
+      }
+    }
+    double q = quantize((double)xv * inv, io.dac);
+    if (io.sigma_inp > 0.0) {
+      const float z = normal1((uint32_t)(j + in0), (uint32_t)seq,
+                              (uint32_t)(seq >> 32) | ((uint32_t)s.m << 24), TAG_IN_NOISE << 24,
+                              key);
+      q += io.sigma_inp * (double)z;
+    }
+    return (float)q;
+  };
+  float nrm = 0.f;
+  constexpr int VPT = 8; // all loads of a thread in flight before any conversion
+  if (n <= (int)blockDim.x * VPT) {
+    float v[VPT];
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) {
+      const int j = threadIdx.x + u * (int)blockDim.x;
+      v[u] = j < n ? x[j] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < VPT; ++u) {
+      const int j = threadIdx.x + u * (int)blockDim.x;
+      if (j < n) {
+        const float f = convert(v[u], j);
+        xt[j] = f;
+        nrm = fmaf(f, f, nrm);
+      }
+    }
+  } else {
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      const float f = convert(x[j], j);
+      xt[j] = f;
+      nrm = fmaf(f, f, nrm);
+    }
+  }
+  nrm = warp_sum(nrm);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
+  __syncthreads();
+  float tot = 0.f;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+  __syncthreads();
+  return sqrtf(tot);
+}
+
+// Block-wide compaction: map[0..n) = the indices i < nb with flags[i] != 0,
+// ascending, written as base + i; returns n in every thread.  cnt: >= 33 ints
+// of shared memory.
+__device__ __forceinline__ int block_compact(const int *__restrict__ flags, int nb, int base,
+                                             int *__restrict__ map, int *cnt) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int total = 0;
+  for (int i0 = 0; i0 < nb; i0 += blockDim.x) {
+    const int i = i0 + threadIdx.x;
+    const bool f = i < nb && flags[i] != 0;
+    const unsigned m = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) cnt[warp] = __popc(m);
+    __syncthreads();
+    int before = 0, all = 0;
+    for (int w = 0; w < nw; ++w) {
+      before += (w < warp) ? cnt[w] : 0;
+      all += cnt[w];
+    }
+    if (f) map[total + before + __popc(m & ((1u << lane) - 1u))] = base + i;
+    total += all;
+    __syncthreads();
+  }
+  return total;
+}
+
+// Grid-wide barrier of a launch whose CTAs are all co-resident (checked on
+// the host with cudaOccupancyMaxActiveClusters): `target` = arrivals expected
+// so far (k-th barrier: k * gridDim).  Release/acquire at gpu scope; a spin
+// past ~2 s traps (a kernel error, never a hung GPU).
+__device__ __forceinline__ void grid_sync(unsigned *ctr, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    const long long t0 = clock64();
+    unsigned v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      if (v >= target) break;
+      if (clock64() - t0 > (1ll << 32)) __trap();
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
+}
+
+// arguments of the fused output stage (and of the in-kernel re-issue rounds)
 struct FusedOut {
   float *Y;            // [B][ldy]
   int ldy;
-  const SampleState *st;
+  SampleState *st;     // per sample (global index)
   IoDev io;
   Key key;
   uint64_t seq0;       // sequence number of sample 0 of the call
-  int *sat;            // BM flags [B] + per-pass counters
-  int first_pass, B, pass_slot;
+  BmBufs bm;           // flags/counts/map of this N slab
+  int pass;            // pass index of the launch's first pass (0, or a host-driven re-issue)
   int o0;              // global index of output 0 (row shards: row0; backward: 0)
-  int n0;              // first x~ row of this N slab
-  const int *map;      // x~ row -> sample (compacted BM re-issue), or nullptr
+  int n0;              // first sample (= x~ row of pass 0) of this N slab
+  int nb;              // samples in this N slab
+  const int *n_dev;    // host-driven re-issue: number of compacted samples (device), else null
+  // in-kernel bound management (loop != 0): re-issue rounds inside this launch
+  int loop;
+  const float *X;      // raw inputs [B][K] (re-issue prep)
+  int K, in0;          // input length; global index of input 0
+  float *xt;           // x~ rows of this slab; re-issue rows are compacted from row 0
+  int ldt;
+  unsigned *bar;       // grid-barrier counter, zero at launch
 };
 
 // tcgen05 contraction (xb_mvm_tc.cu).  fo == nullptr: split-K partial sums
-// part[s][b][o] (split stride B x M); otherwise the cluster-fused output stage
-// writes fo->Y (requires fo->o0 % 4 == 0 and splits <= 8).
-void tc_gemm(Tile &t, bool transposed, bool x3, const float *Xt, int ldt, int B, float *part,
-             int splits, const FusedOut *fo);
+// part[s][b][o] (split stride B x M; rows are x~ rows, n_dev = the number of
+// valid rows when non-null); otherwise the cluster-fused output stage writes
+// fo->Y (requires fo->o0 % 4 == 0 and splits <= 8).  bm_loop: run every BM
+// re-issue inside the launch (returns false, and runs one pass, when the grid
+// cannot be co-resident).
+bool tc_gemm(Tile &t, bool transposed, bool x3, const float *Xt, int ldt, int B, float *part,
+             int splits, const FusedOut *fo, const int *n_dev = nullptr, bool bm_loop = false);
 
 } // namespace xb

@@ -35,7 +35,7 @@
 #ifdef XB_TC_TRACE
 // experiment builds only: per-CTA globaltimer stamps of the contraction
 // (start, first stage landed, accumulator complete, end)
-__device__ unsigned long long g_tc_trace[4096][4];
+__device__ unsigned long long g_tc_trace[4096][16];
 __device__ __forceinline__ unsigned long long xb_gtime() {
   unsigned long long v;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
@@ -48,7 +48,7 @@ __device__ __forceinline__ unsigned long long xb_gtime() {
   } while (0)
 extern "C" __attribute__((visibility("default"))) int xb_debug_tc_trace(unsigned long long *out,
                                                                           int n) {
-  return (int)cudaMemcpyFromSymbol(out, g_tc_trace, sizeof(unsigned long long) * 4 *
+  return (int)cudaMemcpyFromSymbol(out, g_tc_trace, sizeof(unsigned long long) * 16 *
                                                         (size_t)(n < 4096 ? n : 4096));
 }
 #else
@@ -191,13 +191,6 @@ __device__ __forceinline__ uint32_t dsmem_map(uint32_t saddr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
   return r;
 }
-__device__ __forceinline__ float4 dsmem_ld4(uint32_t addr) {
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(addr));
-  return v;
-}
 
 
 // split x into hi = x with the low 13 mantissa bits cleared (exactly a TF32
@@ -213,67 +206,119 @@ __device__ __forceinline__ void split_tf32(float4 &v, float4 &lo) {
   }
 }
 
-// Cluster-fused output stage.  Every warp of the CTA: drain this CTA's
-// accumulator (NSUB sub-tiles of 128 TMEM lanes x bn columns) into its idle
-// pipeline memory as [bn][128] fp32, cluster barrier, then reduce this CTA's
-// share of the columns (samples) over the S split partials -- split r lives
-// in cluster CTA peer0 + r * pstride -- through distributed shared memory
-// (all S loads in flight, summed in split order like the epilogue kernel) and
-// run the output stage (xb_mvm_common.cuh) straight into Y.
+__device__ __forceinline__ float4 dsmem_ld4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
+
+// Cluster-fused output stage (split-K reduction over distributed shared
+// memory).  Every warp of the CTA drains this CTA's accumulator (NSUB
+// sub-tiles of 128 TMEM lanes x bnr columns) into its idle pipeline memory
+// as [bnr][128] fp32 (tcgen05.ld, lane = row: conflict-free stores); after a
+// cluster barrier CTA r reduces columns (samples) [r c, (r + 1) c) over the
+// S split partials -- split q lives in cluster CTA q -- through distributed
+// shared memory (mapa + ld.shared::cluster.v4, all S loads in flight, summed
+// in split order like the epilogue kernel, so fused and unfused agree bit
+// for bit) and runs the output stage (xb_mvm_common.cuh) straight into Y.
+// (Measured on B200, 4096^2 x 256: pushing the partials to their owners with
+// st.shared::cluster instead -- scalar or 16-byte scattered -- was slower:
+// DSMEM moves whole-warp contiguous lines best, which the pull form keeps.)
+// (Measured alternative, round 2: staging the partials in L2 and reading them
+// back with ld.global.cg was slower still -- the drain to global memory alone
+// took 4 us vs 1.5 us into shared memory.)
+// Column loop of the fused output stage: thread = group of 4 rows (grp) x
+// every NW-th column of this CTA's range.  Software-pipelined: the S partial
+// loads of the next column (all in flight) are issued before the output
+// stage of the current one, so the ~20 B/clk DSMEM stream overlaps the math.
+template <int NW, int NS>
+__device__ __forceinline__ void reduce_columns(const FusedOut &fo, const float *red,
+                                               uint32_t red_s, int row0, int M, int c_lo,
+                                               int c_hi, uint32_t my_split, uint32_t nsplit,
+                                               const int *map, int *flags, int *count) {
+  const int grp = threadIdx.x & 31, cph = threadIdx.x >> 5;
+  auto load = [&](int c, float4 (&v)[NS]) {
+    const uint32_t off = red_s + (uint32_t)((c * TC_BM + 4 * grp) * 4);
+#pragma unroll
+    for (int r = 0; r < NS; ++r)
+      if (r < (int)nsplit)
+        v[r] = r == (int)my_split ? *reinterpret_cast<const float4 *>(red + (off - red_s) / 4)
+                                  : dsmem_ld4(dsmem_map(off, (uint32_t)r));
+  };
+  int c = c_lo + cph;
+  if (c >= c_hi) return;
+  float4 v[NS];
+  load(c, v);
+  const bool rows_ok = row0 + 4 * grp < M;
+  for (;;) {
+    const int cn = c + NW;
+    float4 vn[NS];
+    if (NS <= 4 && cn < c_hi) load(cn, vn); // (8 splits: no registers to spare)
+    float4 acc4 = v[0];
+#pragma unroll
+    for (int r = 1; r < NS; ++r) // split order (as the epilogue kernel)
+      if (r < (int)nsplit) {
+        acc4.x += v[r].x;
+        acc4.y += v[r].y;
+        acc4.z += v[r].z;
+        acc4.w += v[r].w;
+      }
+    if (rows_ok) {
+      const int b = map ? map[c] : fo.n0 + c;
+      const SampleState sst = fo.st[b];
+      const float a[4] = {acc4.x, acc4.y, acc4.z, acc4.w};
+      // global output index of this group: o0 + row0 + 4 grp (o0 % 4 == 0 on
+      // the fused path, so groups align with the noise groups)
+      const int g = (fo.o0 + row0) / 4 + grp;
+      const bool hit = epilogue_group4(a, g, fo.o0, M, sst, fo.io, fo.key,
+                                       fo.seq0 + (uint64_t)b, fo.Y + (size_t)b * fo.ldy);
+      bm_flag(hit, sst, fo.io, flags + (b - fo.n0), count);
+    }
+    if (cn >= c_hi) break;
+    if (NS <= 4) {
+#pragma unroll
+      for (int r = 0; r < NS; ++r) v[r] = vn[r];
+    } else {
+      load(cn, v);
+    }
+    c = cn;
+  }
+}
+
 template <int NW, int NSUB>
 __device__ __forceinline__ void fused_output_stage(const FusedOut &fo, uint32_t tmem,
-                                                   uint8_t *smem, int nkb, int m0, int M, int B,
-                                                   int bn, uint32_t my_split, uint32_t nsplit,
-                                                   uint32_t peer0, uint32_t pstride) {
+                                                   uint8_t *smem, int nkb, int m0, int M, int n,
+                                                   int bnr, uint32_t my_split, uint32_t nsplit,
+                                                   const int *map, int pass) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, quarter = warp & 3;
   float *red = reinterpret_cast<float *>(smem);
   const uint32_t red_s = smem_u32(red);
-  const int cols = (bn + (int)nsplit - 1) / (int)nsplit;
-  const int c_lo = (int)my_split * cols, c_hi = min(bn, c_lo + cols);
+  const int cols = (bnr + (int)nsplit - 1) / (int)nsplit;
+  const int c_lo = (int)my_split * cols, c_hi = min(n, c_lo + cols);
+  int *flags = fo.bm.flags + (pass & 1) * fo.nb;
+  int *count = fo.bm.counts + pass;
 #pragma unroll 1
   for (int sub = 0; sub < NSUB; ++sub) {
     const int row = quarter * 32 + lane;
-    for (int c0 = 32 * (warp >> 2); c0 < bn; c0 += 32 * (NW / 4)) {
+    for (int c0 = 32 * (warp >> 2); c0 < bnr; c0 += 32 * (NW / 4)) {
       uint32_t r[32];
       XB_TMEM_LD32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(sub * TC_MAX_BN + c0), r);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
       for (int c = 0; c < 32; ++c) red[(c0 + c) * TC_BM + row] = nkb > 0 ? __uint_as_float(r[c]) : 0.f;
     }
+    if (threadIdx.x == 0 && sub == 0) XB_TRACE(4);
     cluster_sync_all(); // every partial of this sub-tile is in place
-    {
-      // thread: group of 4 rows (grp) x every NW-th column of this CTA's range
-      const int grp = threadIdx.x & 31, cph = threadIdx.x >> 5;
-      const int row0 = m0 + sub * TC_BM; // local output index of row 0 of the sub-tile
-      for (int c = c_lo + cph; c < c_hi; c += NW) {
-        if (c >= B) break;
-        const int b = fo.map ? fo.map[fo.n0 + c] : fo.n0 + c;
-        const SampleState sst = fo.st[b];
-        if (!fo.first_pass && !sst.active) continue;
-        const uint32_t off = red_s + (uint32_t)((c * TC_BM + 4 * grp) * 4);
-        float4 v[8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) // all remote loads in flight, then the sum
-          if (r < (int)nsplit) v[r] = dsmem_ld4(dsmem_map(off, peer0 + (uint32_t)r * pstride));
-        float4 acc4 = v[0];
-#pragma unroll
-        for (int r = 1; r < 8; ++r) // split order (as the epilogue kernel)
-          if (r < (int)nsplit) {
-            acc4.x += v[r].x;
-            acc4.y += v[r].y;
-            acc4.z += v[r].z;
-            acc4.w += v[r].w;
-          }
-        if (row0 + 4 * grp >= M) continue;
-        const float a[4] = {acc4.x, acc4.y, acc4.z, acc4.w};
-        // global output index of this group: o0 + row0 + 4 grp (o0 % 4 == 0 on
-        // the fused path, so groups align with the noise groups)
-        const int g = (fo.o0 + row0) / 4 + grp;
-        const bool hit = epilogue_group4(a, g, fo.o0, M, sst, fo.io, fo.key,
-                                         fo.seq0 + (uint64_t)b, fo.Y + (size_t)b * fo.ldy);
-        bm_flag(hit, sst, fo.io, fo.sat, b, fo.B, fo.pass_slot);
-      }
-    }
+    if (threadIdx.x == 0 && sub == 0) XB_TRACE(5);
+    const int row0 = m0 + sub * TC_BM; // local output index of row 0 of the sub-tile
+    if (nsplit <= 4)
+      reduce_columns<NW, 4>(fo, red, red_s, row0, M, c_lo, c_hi, my_split, nsplit, map, flags,
+                            count);
+    else
+      reduce_columns<NW, 8>(fo, red, red_s, row0, M, c_lo, c_hi, my_split, nsplit, map, flags,
+                            count);
     cluster_sync_all(); // the partials are read before the next sub-tile overwrites them
   }
 }
@@ -287,16 +332,28 @@ __device__ __forceinline__ void fused_output_stage(const FusedOut &fo, uint32_t 
 //               the MMA thread issues hi*hi + hi*lo + lo*hi per K-step, which
 //               recovers ~fp32 accuracy of the products at 3x the tensor work.
 //               Warps 4-7 run the epilogue (TMEM lane quarter = warp % 4).
+// B operand   : pass 0 streams the slab's x~ rows with one bn-row box (tm_b);
+//               a re-issue pass streams ceil(n/32) 32-row boxes of the
+//               compacted rows (tm_r), the MMA N is round_up(n, 16).
+// FUSED + fo.loop: bound management runs inside the launch.  After a pass,
+//               a grid barrier; every CTA compacts the pass's saturation
+//               flags (same ascending order everywhere), prepares its share of
+//               the re-issued x~ rows (DAC at m + 1, fp64), a second grid
+//               barrier, and the next pass streams W again (L2-resident when
+//               it fits).  The host never waits on the device.
 template <bool A_MN, bool X3, int NSUB, bool FUSED>
 __global__ void __launch_bounds__(tc_threads<X3, FUSED>(), 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
-                   int M, int K, int B, int bn, int kblocks_per_split, float *__restrict__ part,
-                   int ldp, size_t split_stride, const __grid_constant__ FusedOut fo) {
+                   const __grid_constant__ CUtensorMap tm_r, int M, int K, int B, int bn,
+                   int kblocks_per_split, float *__restrict__ part, int ldp, size_t split_stride,
+                   const int *__restrict__ n_rows, const __grid_constant__ FusedOut fo) {
   constexpr int STAGES = tc_stages<X3, NSUB>();
   constexpr int SB = tc_stage_bytes<X3, NSUB>();
   constexpr int AB = NSUB * TC_A_BYTES;          // A bytes per stage
   constexpr int LO = NSUB * TC_A_BYTES + TC_B_BYTES; // offset of the lo copies (X3)
+  constexpr int NT = tc_threads<X3, FUSED>();
   extern __shared__ uint8_t smem_raw[];
+  __shared__ float red[40];
   // 1024-byte alignment for the 128-byte swizzle atoms; stage s holds
   // [A | B | A_lo | B_lo]
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -313,8 +370,14 @@ __global__ void __launch_bounds__(tc_threads<X3, FUSED>(), 1)
   const int split = blockIdx.y;
   const int kb0 = split * kblocks_per_split;
   const int nkb = min(kblocks_per_split, (K + TC_BK - 1) / TC_BK - kb0);
-  constexpr int CONV_THREADS = tc_threads<X3, FUSED>() - 64;
+  constexpr int CONV_THREADS = NT - 64;
   constexpr uint32_t TMEM_COLS = NSUB * TC_MAX_BN; // 256 or all 512 columns
+
+  // rows (samples) of the first pass: pass 0 = the whole slab; a host-driven
+  // re-issue (FUSED with fo.n_dev, or unfused with n_rows) = the compacted count
+  const int *ndev = FUSED ? fo.n_dev : n_rows;
+  int n = ndev ? *ndev : B;
+  if (n <= 0) return; // nothing saturated: the whole grid leaves before any setup
 
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_a)) : "memory");
@@ -337,314 +400,214 @@ __global__ void __launch_bounds__(tc_threads<X3, FUSED>(), 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  const uint32_t b_bytes = (uint32_t)bn * TC_BK * 4;
 
-  if (warp == 0 && lane == 0 && nkb > 0) {
-    // ---------------- TMA producer
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
-      mbar_wait(empty0 + 8 * s, ph ^ 1u);
-      mbar_expect_tx(full0 + 8 * s, AB + b_bytes);
-      const int kk = (kb0 + kb) * TC_BK;
-      if (A_MN) {
+  const int *map = FUSED ? fo.bm.map : nullptr; // compacted list (re-issue passes)
+  bool reissue = ndev != nullptr;               // B operand = compacted rows (tm_r)
+  int pass = FUSED ? fo.pass : 0;
+  uint32_t gk = 0;     // k-blocks streamed by this CTA in this launch (ring position)
+  uint32_t iter = 0;   // passes run in this launch (parity of `done`)
+  unsigned bar_target = 0;
+  const unsigned nctas = gridDim.x * gridDim.y;
+
+  for (;;) {
+    const int bnr = reissue ? max(16, (n + 15) / 16 * 16) : bn; // MMA N of this pass
+    // a re-issue of a few samples streams just their x~ rows (32-row boxes);
+    // of many, the slab's whole box (rows >= n are stale and never read out)
+    const bool boxes = reissue && n <= 64;
+    const int nbox = (n + 31) / 32;
+    const uint32_t b_bytes = boxes ? (uint32_t)nbox * 32u * TC_BK * 4u : (uint32_t)bn * TC_BK * 4;
+    if (warp == 0 && lane == 0 && nkb > 0) {
+      // ---------------- TMA producer
+      // Pass 0 is launched as a programmatic dependent of the prep kernel: the
+      // W tiles of the first stages stream while prep finishes; the x~ tiles
+      // wait for it (griddepcontrol.wait).  Every later stage waits for a
+      // free slot, i.e. after the first ones were consumed.
+      const int pre = iter == 0 ? min(nkb, STAGES) : 0;
+      auto load_a = [&](int kb, int s) {
+        const int kk = (kb0 + kb) * TC_BK;
+        if (A_MN) {
 #pragma unroll
-        for (int a = 0; a < NSUB * TC_BM / 32; ++a)
-          tma_load_2d(smem_u32(stage_a(s) + a * 4096), &tm_a, full0 + 8 * s, m0 + 32 * a, kk);
-      } else {
-        tma_load_2d(smem_u32(stage_a(s)), &tm_a, full0 + 8 * s, kk, m0);
+          for (int a = 0; a < NSUB * TC_BM / 32; ++a)
+            tma_load_2d(smem_u32(stage_a(s) + a * 4096), &tm_a, full0 + 8 * s, m0 + 32 * a, kk);
+        } else {
+          tma_load_2d(smem_u32(stage_a(s)), &tm_a, full0 + 8 * s, kk, m0);
+        }
+      };
+      for (int kb = 0; kb < pre; ++kb) { // fresh ring: slots kb are free
+        mbar_expect_tx(full0 + 8 * kb, AB + b_bytes);
+        load_a(kb, kb);
       }
-      tma_load_2d(smem_u32(stage_b(s)), &tm_b, full0 + 8 * s, kk, 0);
-    }
-  } else if (warp == 1 && lane == 0 && nkb > 0) {
-    // ---------------- MMA issuer (one thread)
-    const uint32_t idesc = idesc_tf32(bn, A_MN);
-    const uint32_t a_lbo = A_MN ? 4096u : 16u, a_sbo = A_MN ? 512u : 1024u;
-    const uint32_t a_layout = A_MN ? 1u : 2u;
-    // one MMA = 8 tf32 of K: K-major advances 32 bytes (+2 in 16-byte units),
-    // MN-major advances 8 K-rows = two 4-row groups (+1024 bytes = +64)
-    const uint32_t a_step = A_MN ? 64u : 2u;
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
-      mbar_wait((X3 ? conv0 : full0) + 8 * s, ph);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (kb == 0) XB_TRACE(1);
-      const uint64_t db = umma_desc(smem_u32(stage_b(s)), 16u, 1024u, 2u);
-      const uint64_t dbl = umma_desc(smem_u32(stage_b(s) + LO), 16u, 1024u, 2u);
-#pragma unroll
-      for (int sub = 0; sub < NSUB; ++sub) {
-        // sub-tile: K-major rows 128*sub.. (16 KB further); MN-major atoms 4*sub..
-        const uint64_t da =
-            umma_desc(smem_u32(stage_a(s) + sub * TC_A_BYTES), a_lbo, a_sbo, a_layout);
-        const uint64_t dal =
-            umma_desc(smem_u32(stage_a(s) + LO + sub * TC_A_BYTES), a_lbo, a_sbo, a_layout);
-        const uint32_t acc = tmem + (uint32_t)(sub * TC_MAX_BN);
-#pragma unroll
-        for (int k = 0; k < TC_BK / 8; ++k) {
-          mma_tf32(acc, da + a_step * k, db + 2u * k, idesc, (kb | k) != 0);
-          if (X3) {
-            mma_tf32(acc, da + a_step * k, dbl + 2u * k, idesc, 1u);
-            mma_tf32(acc, dal + a_step * k, db + 2u * k, idesc, 1u);
-          }
+      if (iter == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
+      for (int kb = 0; kb < nkb; ++kb) {
+        const uint32_t g = gk + (uint32_t)kb;
+        const int s = (int)(g % STAGES);
+        const uint32_t ph = (g / STAGES) & 1u;
+        const int kk = (kb0 + kb) * TC_BK;
+        if (kb >= pre) {
+          mbar_wait(empty0 + 8 * s, ph ^ 1u);
+          mbar_expect_tx(full0 + 8 * s, AB + b_bytes);
+          load_a(kb, s);
+        }
+        if (boxes) {
+          for (int j = 0; j < nbox; ++j)
+            tma_load_2d(smem_u32(stage_b(s) + j * 4096), &tm_r, full0 + 8 * s, kk, 32 * j);
+        } else {
+          tma_load_2d(smem_u32(stage_b(s)), &tm_b, full0 + 8 * s, kk, 0);
         }
       }
-      mma_commit(empty0 + 8 * s); // smem stage free once these MMAs retire
-    }
-    mma_commit(done);
-  } else if (X3 && warp >= 2 && nkb > 0) {
-    // ---------------- hi/lo split of each landed stage (3xTF32)
-    const int ct = threadIdx.x - 64;
-    const int n4 = (AB + (int)b_bytes) / 16; // B follows A directly in both halves
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
-      mbar_wait(full0 + 8 * s, ph);
-      float4 *a4 = reinterpret_cast<float4 *>(stage_a(s));
-      float4 *al4 = reinterpret_cast<float4 *>(stage_a(s) + LO);
-      for (int e = ct; e < n4; e += CONV_THREADS) {
-        float4 v = a4[e], lo;
-        split_tf32(v, lo);
-        a4[e] = v;
-        al4[e] = lo;
+    } else if (warp == 1 && lane == 0 && nkb > 0) {
+      // ---------------- MMA issuer (one thread)
+      const uint32_t idesc = idesc_tf32(bnr, A_MN);
+      const uint32_t a_lbo = A_MN ? 4096u : 16u, a_sbo = A_MN ? 512u : 1024u;
+      const uint32_t a_layout = A_MN ? 1u : 2u;
+      // one MMA = 8 tf32 of K: K-major advances 32 bytes (+2 in 16-byte units),
+      // MN-major advances 8 K-rows = two 4-row groups (+1024 bytes = +64)
+      const uint32_t a_step = A_MN ? 64u : 2u;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int kb = 0; kb < nkb; ++kb) {
+        const uint32_t g = gk + (uint32_t)kb;
+        const int s = (int)(g % STAGES);
+        const uint32_t ph = (g / STAGES) & 1u;
+        mbar_wait((X3 ? conv0 : full0) + 8 * s, ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (kb == 0 && iter == 0) XB_TRACE(1);
+        if (kb == 0 && iter == 1) XB_TRACE(11);
+        const uint64_t db = umma_desc(smem_u32(stage_b(s)), 16u, 1024u, 2u);
+        const uint64_t dbl = umma_desc(smem_u32(stage_b(s) + LO), 16u, 1024u, 2u);
+#pragma unroll
+        for (int sub = 0; sub < NSUB; ++sub) {
+          // sub-tile: K-major rows 128*sub.. (16 KB further); MN-major atoms 4*sub..
+          const uint64_t da =
+              umma_desc(smem_u32(stage_a(s) + sub * TC_A_BYTES), a_lbo, a_sbo, a_layout);
+          const uint64_t dal =
+              umma_desc(smem_u32(stage_a(s) + LO + sub * TC_A_BYTES), a_lbo, a_sbo, a_layout);
+          const uint32_t acc = tmem + (uint32_t)(sub * TC_MAX_BN);
+#pragma unroll
+          for (int k = 0; k < TC_BK / 8; ++k) {
+            mma_tf32(acc, da + a_step * k, db + 2u * k, idesc, (kb | k) != 0);
+            if (X3) {
+              mma_tf32(acc, da + a_step * k, dbl + 2u * k, idesc, 1u);
+              mma_tf32(acc, dal + a_step * k, db + 2u * k, idesc, 1u);
+            }
+          }
+        }
+        mma_commit(empty0 + 8 * s); // smem stage free once these MMAs retire
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(conv0 + 8 * s) : "memory");
+      mma_commit(done);
+    } else if (X3 && warp >= 2 && nkb > 0) {
+      // ---------------- hi/lo split of each landed stage (3xTF32)
+      const int ct = threadIdx.x - 64;
+      const int n4 = (AB + (int)b_bytes) / 16; // B follows A directly in both halves
+      for (int kb = 0; kb < nkb; ++kb) {
+        const uint32_t g = gk + (uint32_t)kb;
+        const int s = (int)(g % STAGES);
+        const uint32_t ph = (g / STAGES) & 1u;
+        mbar_wait(full0 + 8 * s, ph);
+        float4 *a4 = reinterpret_cast<float4 *>(stage_a(s));
+        float4 *al4 = reinterpret_cast<float4 *>(stage_a(s) + LO);
+        for (int e = ct; e < n4; e += CONV_THREADS) {
+          float4 v = a4[e], lo;
+          split_tf32(v, lo);
+          a4[e] = v;
+          al4[e] = lo;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(conv0 + 8 * s) : "memory");
+      }
     }
-  }
-  __syncwarp();
+    __syncwarp();
+    if (iter == 0) asm volatile("griddepcontrol.wait;" ::: "memory"); // prep's st[] / flags
 
-  // ---------------- epilogue: TMEM -> registers -> partial sums
-  constexpr int EPI_W0 = X3 ? 4 : 0;
-  const bool epi_warp = warp >= EPI_W0 && warp < EPI_W0 + 4;
-  if (epi_warp && nkb > 0) {
-    mbar_wait(done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (threadIdx.x == 32 * EPI_W0) XB_TRACE(2);
-  }
-  const int quarter = warp & 3;
-  if (!FUSED) {
-    if (epi_warp) {
-      float *dst = part + (size_t)split * split_stride;
+    // ---------------- epilogue: TMEM -> registers -> partial sums / output stage
+    if (nkb > 0) {
+      mbar_wait(done, iter & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (threadIdx.x == 0 && iter == 0) XB_TRACE(2);
+      if (threadIdx.x == 0 && iter == 1) XB_TRACE(12);
+    }
+    const int quarter = warp & 3;
+    if (!FUSED) {
+      constexpr int EPI_W0 = X3 ? 4 : 0;
+      if (warp >= EPI_W0 && warp < EPI_W0 + 4) {
+        float *dst = part + (size_t)split * split_stride;
 #pragma unroll
-      for (int sub = 0; sub < NSUB; ++sub) {
-        const int o = m0 + sub * TC_BM + quarter * 32 + lane;
-        for (int c0 = 0; c0 < bn; c0 += 32) {
-          uint32_t r[32];
-          XB_TMEM_LD32(tmem + ((uint32_t)(quarter * 32) << 16) +
-                           (uint32_t)(sub * TC_MAX_BN + c0),
-                       r);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (o < M) {
+        for (int sub = 0; sub < NSUB; ++sub) {
+          const int o = m0 + sub * TC_BM + quarter * 32 + lane;
+          for (int c0 = 0; c0 < bnr; c0 += 32) {
+            uint32_t r[32];
+            XB_TMEM_LD32(tmem + ((uint32_t)(quarter * 32) << 16) +
+                             (uint32_t)(sub * TC_MAX_BN + c0),
+                         r);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (o < M) {
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              const int b = c0 + c;
-              if (b < B) dst[(size_t)b * ldp + o] = nkb > 0 ? __uint_as_float(r[c]) : 0.f;
+              for (int c = 0; c < 32; ++c) {
+                const int b = c0 + c;
+                if (b < n) dst[(size_t)b * ldp + o] = nkb > 0 ? __uint_as_float(r[c]) : 0.f;
+              }
             }
           }
         }
       }
-    }
-  } else {
-    if (!epi_warp && nkb > 0) {
-      mbar_wait(done, 0);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      break;
     }
     // split peers: cluster (1, S), CTA rank == split index
-    fused_output_stage<tc_threads<X3, FUSED>() / 32, NSUB>(fo, tmem, smem, nkb, m0, M, B, bn,
-                                                            cluster_rank(), cluster_size(), 0u,
-                                                            1u);
+    fused_output_stage<NT / 32, NSUB>(fo, tmem, smem, nkb, m0, M, n, bnr, cluster_rank(),
+                                      cluster_size(), reissue ? map : nullptr, pass);
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    gk += (uint32_t)max(nkb, 0);
+    ++iter;
+    if (!fo.loop) break;
+    // ---------------- in-kernel bound management: next re-issue pass
+    bar_target += nctas;
+    grid_sync(fo.bar, bar_target); // every flag of this pass is final
+    if (threadIdx.x == 0 && iter == 1) XB_TRACE(8);
+    const int nb = fo.nb;
+    n = block_compact(fo.bm.flags + (pass & 1) * nb, nb, fo.n0, fo.bm.map,
+                      reinterpret_cast<int *>(red));
+#ifdef XB_TC_TRACE
+    if (threadIdx.x == 0 && iter == 1 && blockIdx.x + gridDim.x * blockIdx.y < 4096)
+      g_tc_trace[blockIdx.x + gridDim.x * blockIdx.y][15] = (unsigned long long)n;
+#endif
+    if (n == 0) break; // uniform: every CTA read the same flags
+    {
+      // clear the flags the next pass will write (read by nobody now)
+      int *nf = fo.bm.flags + ((pass + 1) & 1) * nb;
+      const unsigned cta = blockIdx.x + gridDim.x * blockIdx.y;
+      for (int i = (int)(cta * NT) + threadIdx.x; i < nb; i += (int)(nctas * NT)) nf[i] = 0;
+      // this CTA's share of the re-issued rows: x~ at m + 1 (io.cpp:117-131)
+      for (int c = (int)cta; c < n; c += (int)nctas) {
+        const int b = fo.bm.map[c];
+        SampleState s = fo.st[b];
+        s.m += 1;
+        s.norm = prep_row(fo.X + (size_t)b * fo.K, fo.K, fo.xt + (size_t)c * fo.ldt, s, fo.io,
+                          fo.key, fo.seq0 + (uint64_t)b, fo.in0, red);
+        if (threadIdx.x == 0) fo.st[b] = s;
+      }
+      if (threadIdx.x == 0 && iter == 1) XB_TRACE(14);
+      // the x~ rows are read by other CTAs' TMA (async proxy)
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    if (threadIdx.x == 0 && iter == 1) XB_TRACE(9);
+    bar_target += nctas;
+    grid_sync(fo.bar, bar_target);
+    if (threadIdx.x == 0 && iter == 1) XB_TRACE(10);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    reissue = true;
+    ++pass;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (threadIdx.x == 0) XB_TRACE(3);
+#ifdef XB_TC_TRACE
+  if (threadIdx.x == 0 && blockIdx.x + gridDim.x * blockIdx.y < 4096)
+    g_tc_trace[blockIdx.x + gridDim.x * blockIdx.y][7] = iter;
+  if (threadIdx.x == 0 && blockIdx.x + gridDim.x * blockIdx.y < 4096)
+    g_tc_trace[blockIdx.x + gridDim.x * blockIdx.y][13] = (unsigned long long)n;
+#endif
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(TMEM_COLS));
-}
-
-// ============================================================ CTA pairs
-// 2-SM variant (cta_group::2).  A cluster (2, S): the two CTAs of a pair own
-// consecutive 128-row M-tiles of one K-split; each streams its own A tile and
-// HALF of the x~ tile (bn/2 samples) -- signalling the leader's full barrier
-// through the 2-SM TMA form -- and the leader issues M=256 UMMAs that read A
-// and B from both CTAs' shared memory, each CTA accumulating its 128 rows in
-// its own TMEM.  Per stage a CTA holds 16 + 16 KB instead of 16 + 32 KB: six
-// stages in flight instead of four, and half the x~ re-reads from L2.
-constexpr int TP_STAGES = 6;
-constexpr int TP_STAGE = TC_A_BYTES + TC_B_BYTES / 2; // 32 KB
-constexpr int TP_SMEM = TP_STAGES * TP_STAGE + 1024 + 256;
-
-__device__ __forceinline__ uint32_t cluster_ctaid_x() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctaid.x;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t cluster_ctaid_y() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctaid.y;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t cluster_nctaid_y() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_nctaid.y;" : "=r"(r));
-  return r;
-}
-// arrive (+ expected bytes) on an mbarrier of another CTA of the cluster
-__device__ __forceinline__ void mbar_expect_tx_cluster(uint32_t cbar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(
-                   cbar),
-               "r"(bytes)
-               : "memory");
-}
-// TMA into this CTA's shared memory, completion counted on the pair leader's
-// mbarrier (cbar: shared::cluster address)
-__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap *map,
-                                                 uint32_t cbar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(cbar)
-      : "memory");
-}
-__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t a, uint64_t b,
-                                              uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
-}
-// arrive on the same mbarrier offset in both CTAs of the pair (mask: cluster ranks)
-__device__ __forceinline__ void mma_commit_pair(uint32_t bar, uint16_t mask) {
-  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::"
-               "cluster.b64 [%0], %1;" ::"r"(bar),
-               "h"(mask)
-               : "memory");
-}
-
-template <bool A_MN, bool FUSED>
-__global__ void __launch_bounds__(tc_threads<false, FUSED>(), 1)
-    tc_pair_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
-                   int M, int K, int B, int bn, int kblocks_per_split, float *__restrict__ part,
-                   int ldp, size_t split_stride, const __grid_constant__ FusedOut fo) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t *bars = (uint64_t *)(smem + TP_STAGES * TP_STAGE);
-  uint32_t *tmem_slot = (uint32_t *)(bars + 2 * TP_STAGES + 1);
-  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + TP_STAGES),
-                 done = smem_u32(bars + 2 * TP_STAGES);
-  auto stage_a = [&](int s) { return smem + s * TP_STAGE; };
-  auto stage_b = [&](int s) { return smem + s * TP_STAGE + TC_A_BYTES; };
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t xr = cluster_ctaid_x();      // 0 = pair leader (issues the MMAs), 1 = peer
-  const uint32_t my_rank = cluster_rank();
-  const uint32_t lead_rank = my_rank - xr;    // ranks: x + 2 y
-  const uint16_t pair_mask = (uint16_t)(3u << lead_rank);
-  const int m0 = blockIdx.x * TC_BM;
-  const int split = blockIdx.y;
-  const int kb0 = split * kblocks_per_split;
-  const int nkb = min(kblocks_per_split, (K + TC_BK - 1) / TC_BK - kb0);
-  const int half = bn / 2;
-
-  if (threadIdx.x == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_a)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_b)) : "memory");
-    for (int s = 0; s < TP_STAGES; ++s) {
-      mbar_init(full0 + 8 * s, 2); // both producers of the pair arrive on the leader's
-      mbar_init(empty0 + 8 * s, 1);
-    }
-    mbar_init(done, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 1) { // TMEM, allocated by the pair together
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(TC_MAX_BN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  cluster_sync_all(); // barriers of both CTAs initialised, TMEM allocated
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t bytes_per_cta = TC_A_BYTES + (uint32_t)half * TC_BK * 4;
-  const uint32_t lead_full0 = dsmem_map(full0, lead_rank);
-
-  if (warp == 0 && lane == 0 && nkb > 0) {
-    // ---------------- TMA producer (both CTAs)
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % TP_STAGES;
-      const uint32_t ph = (uint32_t)(kb / TP_STAGES) & 1u;
-      mbar_wait(empty0 + 8 * s, ph ^ 1u);
-      mbar_expect_tx_cluster(lead_full0 + 8 * s, bytes_per_cta);
-      const int kk = (kb0 + kb) * TC_BK;
-      if (A_MN) {
-#pragma unroll
-        for (int a = 0; a < TC_BM / 32; ++a)
-          tma_load_2d_pair(smem_u32(stage_a(s) + a * 4096), &tm_a, lead_full0 + 8 * s,
-                           m0 + 32 * a, kk);
-      } else {
-        tma_load_2d_pair(smem_u32(stage_a(s)), &tm_a, lead_full0 + 8 * s, kk, m0);
-      }
-      tma_load_2d_pair(smem_u32(stage_b(s)), &tm_b, lead_full0 + 8 * s, kk, (int)xr * half);
-    }
-  } else if (warp == 1 && lane == 0 && xr == 0 && nkb > 0) {
-    // ---------------- MMA issuer: the pair leader, M = 256 across both CTAs
-    const uint32_t idesc =
-        (idesc_tf32(bn, A_MN) & ~(0x1Fu << 24)) | ((uint32_t)(2 * TC_BM >> 4) << 24);
-    const uint32_t a_lbo = A_MN ? 4096u : 16u, a_sbo = A_MN ? 512u : 1024u;
-    const uint32_t a_layout = A_MN ? 1u : 2u;
-    const uint32_t a_step = A_MN ? 64u : 2u;
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % TP_STAGES;
-      const uint32_t ph = (uint32_t)(kb / TP_STAGES) & 1u;
-      mbar_wait(full0 + 8 * s, ph);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint64_t da = umma_desc(smem_u32(stage_a(s)), a_lbo, a_sbo, a_layout);
-      const uint64_t db = umma_desc(smem_u32(stage_b(s)), 16u, 1024u, 2u);
-#pragma unroll
-      for (int k = 0; k < TC_BK / 8; ++k)
-        mma_tf32_pair(tmem, da + a_step * k, db + 2u * k, idesc, (kb | k) != 0);
-      mma_commit_pair(empty0 + 8 * s, pair_mask); // both CTAs may refill stage s
-    }
-    mma_commit_pair(done, pair_mask);
-  }
-  __syncwarp();
-
-  // ---------------- epilogue: each CTA drains its own 128 accumulator rows
-  if (nkb > 0) {
-    mbar_wait(done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  }
-  if (!FUSED) {
-    if (warp < 4) {
-      const int o = m0 + warp * 32 + lane;
-      float *dst = part + (size_t)split * split_stride;
-      for (int c0 = 0; c0 < bn; c0 += 32) {
-        uint32_t r[32];
-        XB_TMEM_LD32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, r);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (o < M) {
-#pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const int b = c0 + c;
-            if (b < B) dst[(size_t)b * ldp + o] = nkb > 0 ? __uint_as_float(r[c]) : 0.f;
-          }
-        }
-      }
-    }
-  } else {
-    // split peers: cluster (2, S), rank = x + 2 y
-    fused_output_stage<tc_threads<false, FUSED>() / 32, 1>(fo, tmem, smem, nkb, m0, M, B, bn,
-                                                            cluster_ctaid_y(), cluster_nctaid_y(),
-                                                            xr, 2u);
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  cluster_sync_all(); // both CTAs are done with the pair's TMEM
-  if (warp == 1)
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(TC_MAX_BN));
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -702,10 +665,22 @@ int tc_splits(int M, int K, bool x3) {
   return std::max(1, std::min(s, 16));
 }
 
+struct TcArgs {
+  dim3 grid;
+  cudaStream_t st;
+  CUtensorMap ma, mb, mr;
+  int M, K, nb, bn, per;
+  float *part;
+  size_t split_stride;
+  const int *n_rows;
+  FusedOut fo;
+  bool pdl; // programmatic dependent of the preceding kernel
+};
+
+// launch one contraction; check_loop: only report whether every cluster of
+// the grid can be resident at once (the in-kernel BM loop needs it)
 template <bool A_MN, bool X3, int NSUB, bool FUSED>
-static void launch_tc(dim3 grid, cudaStream_t st, const CUtensorMap &ma, const CUtensorMap &mb,
-                      int M, int K, int nb, int bn, int per, float *part, size_t split_stride,
-                      const FusedOut &fo) {
+static bool launch_tc(const TcArgs &a, bool check_loop) {
   auto kern = tc_gemm_kernel<A_MN, X3, NSUB, FUSED>;
   static std::atomic<uint64_t> configured{0};
   once_per_device(configured, [&] {
@@ -714,72 +689,56 @@ static void launch_tc(dim3 grid, cudaStream_t st, const CUtensorMap &ma, const C
     if (FUSED) XB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
   });
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
+  cfg.gridDim = a.grid;
   cfg.blockDim = dim3(tc_threads<X3, FUSED>());
   cfg.dynamicSmemBytes = tc_smem<X3, NSUB>();
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cfg.stream = a.st;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
   if (FUSED) { // the K-splits of one M-tile form one cluster
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 1;
-    attr[0].val.clusterDim.y = grid.y;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 1;
+    attr[na].val.clusterDim.y = a.grid.y;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
   }
-  XB_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, M, K, nb, bn, per, part, M, split_stride, fo));
+  if (a.pdl) { // pass 0: may start while the prep kernel finishes (griddepcontrol)
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  if (check_loop) {
+    int clusters = 0;
+    if (!FUSED || cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return clusters >= (int)a.grid.x;
+  }
+  XB_CUDA(cudaLaunchKernelEx(&cfg, kern, a.ma, a.mb, a.mr, a.M, a.K, a.nb, a.bn, a.per, a.part,
+                             a.M, a.split_stride, a.n_rows, a.fo));
   count_launch();
   XB_CUDA(cudaGetLastError());
+  return true;
 }
 
 template <bool FUSED>
-static void launch_variant(bool transposed, bool x3, int nsub, dim3 grid, cudaStream_t st,
-                           const CUtensorMap &ma, const CUtensorMap &mb, int M, int K, int nb,
-                           int bn, int per, float *p, size_t ss, const FusedOut &fo) {
-  if (x3) {
-    transposed ? launch_tc<true, true, 1, FUSED>(grid, st, ma, mb, M, K, nb, bn, per, p, ss, fo)
-               : launch_tc<false, true, 1, FUSED>(grid, st, ma, mb, M, K, nb, bn, per, p, ss, fo);
-  } else if (nsub == 2) {
-    transposed ? launch_tc<true, false, 2, FUSED>(grid, st, ma, mb, M, K, nb, bn, per, p, ss, fo)
-               : launch_tc<false, false, 2, FUSED>(grid, st, ma, mb, M, K, nb, bn, per, p, ss, fo);
-  } else {
-    transposed ? launch_tc<true, false, 1, FUSED>(grid, st, ma, mb, M, K, nb, bn, per, p, ss, fo)
-               : launch_tc<false, false, 1, FUSED>(grid, st, ma, mb, M, K, nb, bn, per, p, ss, fo);
-  }
+static bool launch_variant(bool transposed, bool x3, int nsub, const TcArgs &a, bool check) {
+  if (x3)
+    return transposed ? launch_tc<true, true, 1, FUSED>(a, check)
+                      : launch_tc<false, true, 1, FUSED>(a, check);
+  if (nsub == 2)
+    return transposed ? launch_tc<true, false, 2, FUSED>(a, check)
+                      : launch_tc<false, false, 2, FUSED>(a, check);
+  return transposed ? launch_tc<true, false, 1, FUSED>(a, check)
+                    : launch_tc<false, false, 1, FUSED>(a, check);
 }
 
-template <bool A_MN, bool FUSED>
-static void launch_pair(dim3 grid, cudaStream_t st, const CUtensorMap &ma, const CUtensorMap &mb,
-                        int M, int K, int nb, int bn, int per, float *part, size_t split_stride,
-                        const FusedOut &fo) {
-  auto kern = tc_pair_kernel<A_MN, FUSED>;
-  static std::atomic<uint64_t> configured{0};
-  once_per_device(configured, [&] {
-    XB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TP_SMEM));
-  });
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = dim3(tc_threads<false, FUSED>());
-  cfg.dynamicSmemBytes = TP_SMEM;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension; // (CTA pair) x (K-splits when fused)
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = FUSED ? grid.y : 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  XB_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, M, K, nb, bn, per, part, M, split_stride, fo));
-  count_launch();
-  XB_CUDA(cudaGetLastError());
-}
-
-// Opt-in (XB_TC_PAIR=1): correct (tests/test_gpu_mvm.py runs it) but measured
-// slower on B200 for the bench shapes -- 4096^2 x 256 forward 109 us fused /
-// 79 us unfused vs 62 / 65 us for the single-CTA kernel; tensor pipe 22 % --
-// so the single-CTA kernel stays the default.
-static bool pair_enabled() {
-  const char *e = getenv("XB_TC_PAIR");
+// XB_NO_PDL=1: launch pass 0 in plain stream order (A/B measurements)
+static bool pdl_disabled() {
+  const char *e = getenv("XB_NO_PDL");
   return e && e[0] == '1';
 }
 
@@ -787,56 +746,63 @@ static bool pair_enabled() {
 //   forward : o = row of W, K = columns of W   (A = W, K-major)
 //   backward: o = column of W, K = rows of W   (A = W^T, MN-major)
 // fo == nullptr: partial sums part[s][b][o] (split stride B x M) for the
-// epilogue kernel; otherwise the cluster-fused output stage writes fo->Y.
-void tc_gemm(Tile &t, bool transposed, bool x3, const float *Xt, int ldt, int B, float *part,
-             int splits, const FusedOut *fo) {
+// epilogue kernel; n_dev != nullptr: a compacted re-issue whose row count is
+// on the device.  Otherwise the cluster-fused output stage writes fo->Y, per
+// N slab of <= 256 samples (fo->bm points at slab 0's buffers; slab k uses
+// flags + 512 k, counts + 64 k, map + 256 k, bar + k).  bm_loop: every BM
+// re-issue runs inside the launch; false when the grid could not be
+// co-resident (the caller then drives the re-issue passes).
+bool tc_gemm(Tile &t, bool transposed, bool x3, const float *Xt, int ldt, int B, float *part,
+             int splits, const FusedOut *fo, const int *n_dev, bool bm_loop) {
   const int M = transposed ? t.C : t.R, K = transposed ? t.R : t.C;
   const int nsub = tc_nsub(M, x3);
   const int kbs = (K + TC_BK - 1) / TC_BK;
   const int per = (kbs + splits - 1) / splits;
   const int used = (kbs + per - 1) / per;
+  bool looped = bm_loop;
   for (int n0 = 0; n0 < B; n0 += TC_MAX_BN) {
     const int nb = std::min(TC_MAX_BN, B - n0);
     const int bn = std::max(16, (nb + 15) / 16 * 16);
+    TcArgs a;
     // W as [R][C] with row stride ld: the forward box is 128*nsub rows x 32
     // columns, the backward box 32 rows (K) x 32 columns (one MN atom)
-    const CUtensorMap ma =
-        transposed ? make_map(t.W, t.R, t.C, t.ld, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)
-                   : make_map(t.W, t.R, t.C, t.ld, TC_BM * nsub);
-    const CUtensorMap mb = make_map(Xt + (size_t)n0 * ldt, nb, K, ldt, bn);
-    const int mtiles = (M + TC_BM - 1) / TC_BM;
-    const bool pair = !x3 && nsub == 1 && mtiles >= 2 && (!fo || used <= 4) && pair_enabled();
-    if (pair) { // 2-SM UMMA: each CTA streams its A tile and half of the x~ tile
-      const CUtensorMap mbh = make_map(Xt + (size_t)n0 * ldt, nb, K, ldt, bn / 2);
-      const dim3 grid2((mtiles + 1) / 2 * 2, used);
-      if (fo) {
-        FusedOut f = *fo;
-        f.n0 = n0;
-        transposed ? launch_pair<true, true>(grid2, t.stream, ma, mbh, M, K, nb, bn, per, nullptr,
-                                             0, f)
-                   : launch_pair<false, true>(grid2, t.stream, ma, mbh, M, K, nb, bn, per,
-                                              nullptr, 0, f);
-      } else {
-        float *p = part + (size_t)n0 * M;
-        transposed ? launch_pair<true, false>(grid2, t.stream, ma, mbh, M, K, nb, bn, per, p,
-                                              (size_t)B * M, FusedOut{})
-                   : launch_pair<false, false>(grid2, t.stream, ma, mbh, M, K, nb, bn, per, p,
-                                               (size_t)B * M, FusedOut{});
-      }
-      continue;
-    }
-    const dim3 grid((M + TC_BM * nsub - 1) / (TC_BM * nsub), used);
+    a.ma = transposed ? make_map(t.W, t.R, t.C, t.ld, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)
+                      : make_map(t.W, t.R, t.C, t.ld, TC_BM * nsub);
+    a.mb = make_map(Xt + (size_t)n0 * ldt, nb, K, ldt, bn);
+    a.mr = make_map(Xt + (size_t)n0 * ldt, nb, K, ldt, 32);
+    a.grid = dim3((M + TC_BM * nsub - 1) / (TC_BM * nsub), used);
+    a.st = t.stream;
+    a.M = M;
+    a.K = K;
+    a.nb = nb;
+    a.bn = bn;
+    a.per = per;
+    a.n_rows = n_dev;
+    a.pdl = !n_dev && !(fo && fo->n_dev) && !pdl_disabled();
     if (fo) {
-      FusedOut f = *fo;
-      f.n0 = n0;
-      launch_variant<true>(transposed, x3, nsub, grid, t.stream, ma, mb, M, K, nb, bn, per,
-                           nullptr, 0, f);
+      a.fo = *fo;
+      const int slab = n0 / TC_MAX_BN;
+      a.fo.n0 = fo->n0 + n0; // global index of the slab's first sample
+      a.fo.nb = nb;
+      a.fo.bm.flags = fo->bm.flags + (size_t)BM_SLAB_WORDS * slab;
+      a.fo.bm.counts = fo->bm.counts + (size_t)BM_SLAB_WORDS * slab;
+      a.fo.bm.map = fo->bm.map + n0;
+      a.fo.bar = fo->bar ? fo->bar + slab : nullptr;
+      a.fo.xt = fo->xt ? fo->xt + (size_t)n0 * ldt : nullptr;
+      a.part = nullptr;
+      a.split_stride = 0;
+      if (bm_loop && n0 == 0) looped = launch_variant<true>(transposed, x3, nsub, a, true);
+      a.fo.loop = looped ? 1 : 0;
+      launch_variant<true>(transposed, x3, nsub, a, false);
     } else {
       // partial sums of this N slab land at part + n0 rows, split stride B x M
-      launch_variant<false>(transposed, x3, nsub, grid, t.stream, ma, mb, M, K, nb, bn, per,
-                            part + (size_t)n0 * M, (size_t)B * M, FusedOut{});
+      a.part = part + (size_t)n0 * M;
+      a.split_stride = (size_t)B * M;
+      a.fo = FusedOut{};
+      launch_variant<false>(transposed, x3, nsub, a, false);
     }
   }
+  return looped;
 }
 
 int tc_used_splits(int K, int splits) {

@@ -23,6 +23,8 @@ ap.add_argument("--n", type=int, default=4096)
 ap.add_argument("--batch", type=int, default=256)
 ap.add_argument("--precision", type=int, default=xb.MVM_TF32)
 ap.add_argument("--backward", action="store_true")
+ap.add_argument("--bench", action="store_true",
+                help="the bench's forward: reram_sb, BM on, weights after 23 update steps")
 a = ap.parse_args()
 from paper_2104_02184_b200 import tile as _tile  # noqa: E402
 lib = _tile.lib()
@@ -30,7 +32,11 @@ fn = lib.xb_debug_tc_trace
 fn.argtypes = [C.POINTER(C.c_uint64), C.c_int]
 s = torch.cuda.Stream()
 torch.cuda.set_stream(s)
-for name, io in (("default", xb.default_io()), ("perfect", xb.perfect_io())):
+bm_io = xb.default_io()
+bm_io.bound_management = xb.BM_ITERATIVE
+cases = (("bench-bm", bm_io),) if a.bench else (("default", xb.default_io()),
+                                                ("perfect", xb.perfect_io()))
+for name, io in cases:
     cfg = xb.TileSettings(device=xb.device_preset("reram_sb"), forward_io=io, backward_io=io,
                           mvm_precision=a.precision)
     t = xb.AnalogTile(a.n, a.n, cfg, 5)
@@ -40,27 +46,47 @@ for name, io in (("default", xb.default_io()), ("perfect", xb.perfect_io())):
     g.manual_seed(3)
     X = torch.rand(a.batch, a.n, device="cuda", generator=g) * 2 - 1
     Y = torch.empty(a.batch, a.n, device="cuda")
+    if a.bench:
+        for _ in range(23):
+            Dr = torch.rand(a.batch, a.n, device="cuda", generator=g) * 2 - 1
+            t.update_dev(X, Dr, 0.01)
     run = (lambda: t.backward_dev(X, Y)) if a.backward else (lambda: t.forward_dev(X, Y))
     for _ in range(3):
         run()
     torch.cuda.synchronize()
-    buf = (C.c_uint64 * (4096 * 4))()
+    buf = (C.c_uint64 * (4096 * 16))()
     fn(buf, 4096)
-    tr = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 4).astype(np.int64)
+    tr = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 16).astype(np.int64)
     tr = tr[tr[:, 0] > 0]
     # keep the CTAs of the last launch (start within 1 ms of the latest start)
     tr = tr[tr[:, 0] > tr[:, 0].max() - 1_000_000]
+    tr[:, 7] = tr[:, 7]  # pass count (not a time)
     t0 = tr[:, 0].min()
     fill = (tr[:, 1] - tr[:, 0]) / 1e3
     main = (tr[:, 2] - tr[:, 1]) / 1e3
     epi = (tr[:, 3] - tr[:, 2]) / 1e3
+    wait_a = (tr[:, 4] - tr[:, 2]) / 1e3
+    drain = (tr[:, 5] - tr[:, 4]) / 1e3
+    reduce_ = (tr[:, 3] - tr[:, 5]) / 1e3
     span = (tr[:, 3].max() - t0) / 1e3
     late = (tr[:, 0] - t0) / 1e3
 
     def q(v):
         return f"min {v.min():6.2f} med {np.median(v):6.2f} max {v.max():6.2f}"
-    print(f"{name:8s} ctas {len(tr)}  span {span:6.2f} us")
+    print(f"{name:8s} ctas {len(tr)}  span {span:6.2f} us  passes {tr[:, 7].max()}")
+    if tr[:, 7].max() > 1:
+        print(f"   pass 0 done -> barrier 1 {q((tr[:, 8] - tr[:, 2]) / 1e3)}")
+        print(f"   re-issued samples (pass 1) {tr[:, 15].max()}")
+        print(f"   barrier 1 -> prep        {q((tr[:, 14] - tr[:, 8]) / 1e3)}")
+        print(f"   fence.proxy.async        {q((tr[:, 9] - tr[:, 14]) / 1e3)}")
+        print(f"   prep -> barrier 2        {q((tr[:, 10] - tr[:, 9]) / 1e3)}")
+        print(f"   barrier 2 -> 1st stage   {q((tr[:, 11] - tr[:, 10]) / 1e3)}")
+        print(f"   1st stage -> pass-1 done {q((tr[:, 12] - tr[:, 11]) / 1e3)}")
+        print(f"   samples in the last pass {tr[:, 13].max()}")
     print(f"   start offset {q(late)}")
     print(f"   fill         {q(fill)}")
     print(f"   mainloop     {q(main)}")
     print(f"   output stage {q(epi)}")
+    print(f"     drain (TMEM) {q(wait_a)}")
+    print(f"     cluster bar  {q(drain)}")
+    print(f"     reduce+epi   {q(reduce_)}")
