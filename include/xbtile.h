@@ -153,6 +153,7 @@ typedef struct xb_unitcell_config {
 typedef struct xb_tile xb_tile;
 typedef struct xb_transfer xb_transfer;
 typedef struct xb_unitcell xb_unitcell;
+typedef struct xb_comm xb_comm;
 
 /* ---- library ---- */
 int xb_abi_version(void);
@@ -248,6 +249,39 @@ enum { XB_TIMER_PULSE = 0, XB_TIMER_TRAINS = 1, XB_TIMER_FORWARD = 2, XB_TIMER_B
        XB_TIMER_COUNT = 4 };
 int xb_tile_set_timing(xb_tile *t, int enable);
 int xb_tile_read_timing(xb_tile *t, double *ms, int *counts);
+
+/* ---- row sharding over several GPUs (no reference symbol:
+ *      the reference tile is single-device) ----
+ * A logical d_out x d_in tile is split by rows over P ranks; rank r creates
+ * its handle with an xb_shard and attaches the group's communicator.  The
+ * sharded handle then runs the whole-tile semantics of every entry above on
+ * its own rows, with the cross-rank reductions enqueued on its stream:
+ *   update   -- all-reduce(max) of max|d| before translate (pulsed.cpp:34-51);
+ *   forward  -- all-reduce(max) of the bound-management saturation flags
+ *               before each re-issue (outputs stay row-sharded: Y[B][local]);
+ *   backward -- D is the rank's rows [B][local], G is the full [B][d_in] on
+ *               every rank: all-reduce(max) of max|d|, all-reduce(sum) of the
+ *               column sums in sample chunks (the reduction of a chunk
+ *               overlaps the next chunk's contraction), then noise/ADC/alpha
+ *               on the reduced sums (io.cpp:143-146).
+ * Random draws are keyed on global rows, so update and forward are bit for
+ * bit those of the unsharded tile; the backward differs only by the fp32
+ * order of the cross-rank sum.
+ * NCCL (over NVLink / NVSwitch) is loaded at run time (XB_NCCL_LIB, else
+ * libnccl.so.2). */
+#define XB_COMM_ID_BYTES 128
+/* ncclGetUniqueId: rank 0 creates it and sends it to the others out of band */
+int xb_comm_unique_id(uint8_t *id /* [XB_COMM_ID_BYTES] */);
+/* ncclCommInitRank on the current CUDA device (collective over the ranks) */
+int xb_comm_create(const uint8_t *id, int nranks, int rank, xb_comm **out);
+/* an in-process group of nranks handles out[0..nranks), each to be driven by
+ * its own host thread (loopback: several shards may share one device) */
+int xb_comm_create_local(int nranks, xb_comm **out);
+int xb_comm_destroy(xb_comm *c);
+int xb_comm_size(const xb_comm *c);
+int xb_comm_rank(const xb_comm *c);
+/* route the tile's cross-shard reductions through c (borrowed; NULL detaches) */
+int xb_tile_attach_comm(xb_tile *t, xb_comm *c);
 
 /* ---- PCM inference (proj/src/inference.cpp:34-110) ---- */
 /* program target (host, local rows x d_in); stores w0 and nu on the device */

@@ -12,7 +12,7 @@ from ._abi import (BM_ITERATIVE, BM_NONE, CONSTANT_STEP, EXP_STEP, LINEAR_STEP, 
                    W_FP32, W_FP32X2, DeviceParams,
                    InferenceModel, IOParams, TemporalParams, TileConfig, TransferConfig,
                    UnitCellConfig, UpdateParams)
-from .tile import (AnalogTile, Error, InferenceNoiseModel, TileSettings, TransferSettings,
+from .tile import (AnalogTile, Comm, Error, InferenceNoiseModel, TileSettings, TransferSettings,
                    TransferTile, UnitCellSettings, UnitCellTile, default_device, default_io,
                    device_check, device_preset, io_off, launch_count, perfect_io, rows_amax_dev)
 
@@ -24,5 +24,5 @@ __all__ = [
     "SOFT_BOUNDS", "EXP_STEP", "NM_NONE", "NM_ABS_MAX", "BM_NONE", "BM_ITERATIVE",
     "PULSE_STOCHASTIC", "PULSE_DETERMINISTIC", "MVM_FP32", "MVM_TF32", "MVM_TF32X3",
     "UnitCellTile", "UnitCellSettings", "UnitCellConfig", "UC_ROUND_ROBIN", "UC_ALL_TOGETHER",
-    "W_AUTO", "W_FP32", "W_FP32X2",
+    "W_AUTO", "W_FP32", "W_FP32X2", "Comm",
 ]

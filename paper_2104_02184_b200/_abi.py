@@ -175,7 +175,15 @@ SIGNATURES = {
     "xb_unitcell_member": (_P, [_P, C.c_int]),
     "xb_transfer_fast": (_P, [_P]),
     "xb_transfer_slow": (_P, [_P]),
+    "xb_comm_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "xb_comm_create": (C.c_int, [C.POINTER(C.c_uint8), C.c_int, C.c_int, C.POINTER(_P)]),
+    "xb_comm_create_local": (C.c_int, [C.c_int, C.POINTER(_P)]),
+    "xb_comm_destroy": (C.c_int, [_P]),
+    "xb_comm_size": (C.c_int, [_P]),
+    "xb_comm_rank": (C.c_int, [_P]),
+    "xb_tile_attach_comm": (C.c_int, [_P, _P]),
 }
+COMM_ID_BYTES = 128
 
 
 def load(path: str = LIB_PATH) -> C.CDLL:

@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libxbtile.so")
-SOURCES = ["xb_abi.cu", "xb_update.cu", "xb_mvm.cu", "xb_mvm_tc.cu", "xb_elem.cu"]
+SOURCES = ["xb_abi.cu", "xb_update.cu", "xb_mvm.cu", "xb_mvm_tc.cu", "xb_elem.cu", "xb_comm.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -61,7 +61,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = LIB
         objs.append(o)
     tmp = out + ".tmp"
     subprocess.run([nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-lcuda"
-                    if _have_libcuda() else "-lrt"], check=True)
+                    if _have_libcuda() else "-lrt", "-ldl"], check=True)
     os.replace(tmp, out)
     return out
 

@@ -85,18 +85,9 @@ void Scratch::release() {
   bytes = 0;
 }
 
-template <class F> static int guard(F &&f) {
-  try {
-    f();
-    return 0;
-  } catch (const Err &e) {
-    g_err = e.msg;
-    return 1;
-  } catch (const std::exception &e) {
-    g_err = e.what();
-    return 1;
-  }
-}
+void set_last_error(const std::string &msg) { g_err = msg; }
+
+template <class F> static int guard(F &&f) { return xb_guard(static_cast<F &&>(f)); }
 
 // ------------------------------------------------------------------ validation
 static void io_validate(const xb_io_params &io, const char *ctx) { // io.cpp:14-30
@@ -243,6 +234,8 @@ static void tile_free(Tile &t) {
   if (t.chk_host) cudaFreeHost(t.chk_host);
   if (t.lr_pin) cudaFreeHost(t.lr_pin);
   if (t.lr_ev) cudaEventDestroy(t.lr_ev);
+  for (cudaEvent_t e : t.side_ev) cudaEventDestroy(e);
+  if (t.side) cudaStreamDestroy(t.side);
   cudaFree(t.chk_dev);
 }
 
@@ -413,6 +406,8 @@ static void update_device(Tile &t, const float *dX, const float *dD, int B, cons
     const float *dm = dAmaxD;
     if (!dm) {
       launch_rows_amax(dD, B, t.R, t.R, u.dm, t.stream);
+      // row shard: translate needs max|d| over the whole tile (pulsed.cpp:34-51)
+      if (t.comm) t.comm->allreduce_max_f32(u.dm, (size_t)B, t.stream);
       dm = u.dm;
     }
     launch_trains(t, dX, dD, B, lr_d, lr_s, u.xm, dm, t.seq_upd, u.xw, u.dw, train_ld(B), u.bl,
@@ -871,10 +866,60 @@ int xb_tile_forward_noisy(xb_tile *h, const float *X, int B, float *Y, double ex
   return guard([&] { forward_host(h, X, B, Y, noisy_io(h->t.cfg.forward_io, extra_sigma)); });
 }
 
+// Backward of a row shard with an attached communicator: the global max|d|
+// (all-reduce max), then per sample chunk the shard's column sums (partial),
+// their all-reduce(sum) on the side stream -- overlapping the next chunk's
+// contraction on the tile stream -- and the output stage on the reduced sums
+// (finish), in chunk order.  Noise draws are addressed by sample: the result
+// does not depend on the chunking.
+static void backward_sharded(Tile &t, const float *dD, int B, float *dG) {
+  if (B <= 0) return;
+  const xb_io_params &io = t.cfg.backward_io;
+  if (io.bound_management != XB_BM_NONE)
+    raise("backward_io.bound_management: not supported on row shards");
+  io_validate(io, "backward_io");
+  const int nch = B >= 256 ? 4 : 1;
+  const size_t amax_b = ((size_t)B * sizeof(float) + 255) & ~(size_t)255;
+  char *p = (char *)t.s_y.get(amax_b + (size_t)B * t.C * sizeof(float) + 256);
+  float *amax = (float *)p;
+  float *P = (float *)(p + amax_b);
+  launch_rows_amax(dD, B, t.R, t.R, amax, t.stream);
+  t.comm->allreduce_max_f32(amax, (size_t)B, t.stream);
+  if (!t.side) XB_CUDA(cudaStreamCreateWithFlags(&t.side, cudaStreamNonBlocking));
+  while ((int)t.side_ev.size() < 2 * nch) {
+    cudaEvent_t e;
+    XB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    t.side_ev.push_back(e);
+  }
+  const IoDev d = make_io(io);
+  std::vector<int> edge(nch + 1);
+  for (int k = 0; k <= nch; ++k) edge[k] = (int)((long)B * k / nch);
+  for (int k = 0; k < nch; ++k) {
+    const int b0 = edge[k], nb = edge[k + 1] - b0;
+    float *Pk = P + (size_t)b0 * t.C;
+    mvm_backward(t, dD + (size_t)b0 * t.R, nb, nullptr, d, t.k_bwd, t.seq_bwd + t.bwd_pending,
+                 amax + b0, true, Pk);
+    t.bwd_pending += (uint64_t)nb;
+    XB_CUDA(cudaEventRecord(t.side_ev[2 * k], t.stream));
+    XB_CUDA(cudaStreamWaitEvent(t.side, t.side_ev[2 * k], 0));
+    t.comm->allreduce_sum_f32(Pk, (size_t)nb * t.C, t.side);
+    XB_CUDA(cudaEventRecord(t.side_ev[2 * k + 1], t.side));
+  }
+  for (int k = 0; k < nch; ++k) {
+    const int b0 = edge[k], nb = edge[k + 1] - b0;
+    XB_CUDA(cudaStreamWaitEvent(t.stream, t.side_ev[2 * k + 1], 0));
+    mvm_backward_finish(t, P + (size_t)b0 * t.C, nb, amax + b0, dG + (size_t)b0 * t.C, d, t.k_bwd,
+                        t.seq_bwd);
+    t.seq_bwd += (uint64_t)nb;
+    t.bwd_pending -= std::min(t.bwd_pending, (uint64_t)nb);
+  }
+}
+
 int xb_tile_backward_dev(xb_tile *h, const float *dD, int B, float *dG) {
   return guard([&] {
     Tile &t = h->t;
     DevScope ds_(t.device);
+    if (t.R != t.R_total && t.comm) return backward_sharded(t, dD, B, dG);
     if (t.R != t.R_total) raise("backward: row-sharded tile; use xb_tile_backward_partial_dev");
     io_validate(t.cfg.backward_io, "backward_io");
     mvm_backward(t, dD, B, dG, make_io(t.cfg.backward_io), t.k_bwd, t.seq_bwd, nullptr, false,
@@ -888,12 +933,23 @@ static void backward_host(xb_tile *h, const float *D, int B, float *G, bool chec
   DevScope ds_(t.device);
   if (B < 0) raise("backward: batch must be >= 0");
   if (B == 0) return;
-  if (t.R != t.R_total) raise("backward: row-sharded tile; use xb_tile_backward_partial_dev");
-  float *dD = scratch_as<float>(t.s_y, (size_t)B * (t.C + t.R));
+  const bool sharded = t.R != t.R_total;
+  if (sharded && !t.comm)
+    raise("backward: row-sharded tile; attach a communicator (xb_tile_attach_comm) or use "
+          "xb_tile_backward_partial_dev");
+  // sharded: D and G live in s_params (backward_sharded uses s_y for its scratch)
+  float *dD = sharded ? scratch_as<float>(t.s_params, (size_t)B * (t.C + t.R))
+                      : scratch_as<float>(t.s_y, (size_t)B * (t.C + t.R));
   float *dG = dD + (size_t)B * t.R;
   const bool checked = !check || host_check_small({{D, (size_t)B * t.R, "backward"}});
   XB_CUDA(cudaMemcpyAsync(dD, D, sizeof(float) * B * t.R, cudaMemcpyHostToDevice, t.stream));
   if (!checked) check_finite_dev(t, {{dD, (size_t)B * t.R, "backward"}});
+  if (sharded) {
+    backward_sharded(t, dD, B, dG);
+    XB_CUDA(cudaMemcpyAsync(G, dG, sizeof(float) * B * t.C, cudaMemcpyDeviceToHost, t.stream));
+    sync(t);
+    return;
+  }
   mvm_backward(t, dD, B, dG, make_io(t.cfg.backward_io), t.k_bwd, t.seq_bwd, nullptr, false,
                nullptr);
   t.seq_bwd += (uint64_t)B;
@@ -1054,6 +1110,16 @@ int xb_tile_temporal_step(xb_tile *h, const xb_temporal_params *tp) { // tile.cp
 }
 
 int xb_tile_end_minibatch(xb_tile *h) { return xb_tile_temporal_step(h, &h->t.cfg.temporal); }
+
+int xb_tile_attach_comm(xb_tile *h, xb_comm *c) {
+  return guard([&] {
+    Tile &t = h->t;
+    Collective *col = comm_of(c);
+    if (col && t.R == t.R_total && col->size() > 1)
+      raise("attach_comm: the tile is not row-sharded (create it with an xb_shard)");
+    t.comm = col;
+  });
+}
 
 int xb_tile_set_learning_rate(xb_tile *h, double lr) { // tile.cpp:121-126
   return guard([&] {

@@ -4,6 +4,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <stdexcept>
 #include <string>
 #include <utility>
 #include <vector>
@@ -20,6 +21,20 @@ struct Err {
   std::string msg;
 };
 [[noreturn]] void raise(const std::string &msg);
+void set_last_error(const std::string &msg);
+// every ABI entry: run f, map exceptions to a non-zero status + xb_last_error()
+template <class F> inline int xb_guard(F &&f) {
+  try {
+    f();
+    return 0;
+  } catch (const Err &e) {
+    set_last_error(e.msg);
+    return 1;
+  } catch (const std::exception &e) {
+    set_last_error(e.what());
+    return 1;
+  }
+}
 void cuda_check(cudaError_t e, const char *what);
 #define XB_CUDA(call) ::xb::cuda_check((call), #call)
 void count_launch(int n = 1);
@@ -101,6 +116,8 @@ struct Tile {
   xb_tile_config cfg;
   int device = 0;            // CUDA device ordinal of every buffer and the stream
   Collective *comm = nullptr; // row shards: the group of the other shards (borrowed)
+  cudaStream_t side = nullptr; // backward reductions overlap the next chunk here (lazy)
+  std::vector<cudaEvent_t> side_ev; // [2 per backward chunk]
   int R = 0, C = 0;          // local rows, columns
   int row0 = 0, R_total = 0; // first global row, global rows
   int ld = 0;                // leading dimension of W / params (floats)
@@ -147,6 +164,10 @@ struct PhaseTimer {
   PhaseTimer(Tile &t_, int ph);
   ~PhaseTimer();
 };
+
+// ---- communicators (xb_comm.cu) ----
+struct Collective;
+Collective *comm_of(xb_comm *c);
 
 // ---- kernel launchers (xb_update.cu) ----
 void launch_rows_amax(const float *V, int B, int n, int ld, float *out, cudaStream_t s);

@@ -1,23 +1,26 @@
-"""Row sharding of one logical analog tile over the ranks of a process group.
+"""Row sharding of one logical analog tile over several GPUs.
 
-SURVEY.md §8e: rank r owns rows [r0, r1) of W and of every per-cell array.
-Random draws are keyed on global indices, so P shards reproduce the
-unsharded tile.  The only data-path collectives:
+Rank r owns rows [r0, r1) of W and of every per-cell array
+(:func:`partition_rows`).  The compute AND the collectives live in the C
+library: each rank's :class:`~paper_2104_02184_b200.AnalogTile` is created
+with ``shard=(r0, r1)`` and an attached :class:`~paper_2104_02184_b200.Comm`
+(NCCL over NVLink/NVSwitch, ``xb_comm_create``), and then runs the whole-tile
+semantics on its rows with every cross-rank reduction enqueued on its own
+stream (include/xbtile.h, "row sharding"):
 
 * update  : all-reduce(max) of the per-sample max|d| (translate needs the
             global value, proj/src/pulsed.cpp:34-51); x is replicated;
-* backward: all-reduce(max) of max|d| before the DAC, then all-reduce(sum)
-            of the per-shard column sums, in sample chunks whose reductions
-            overlap the next chunk's contraction; output noise, ADC and alpha
-            are applied after the reduction (proj/src/io.cpp:143-146);
-* forward : none (outputs stay row-sharded).
+* forward : all-reduce(max) of the bound-management saturation flags before
+            every re-issue; outputs stay row-sharded;
+* backward: all-reduce(max) of max|d|, all-reduce(sum) of the column sums in
+            sample chunks overlapping the next chunk's contraction; output
+            noise, ADC and alpha after the sum (proj/src/io.cpp:143-146).
 
-The local compute object needs five methods (``forward_dev``,
-``update_dev``, ``backward_partial_dev``, ``backward_finish_dev``,
-``rows_amax``); on a B200 it is :class:`AnalogTile` built with ``shard=``,
-running on the torch stream current at the calls
-(``local.set_stream(torch.cuda.current_stream().cuda_stream)``): the NCCL
-collectives are ordered after the tile's kernels through that stream.
+Random draws are keyed on global rows, so P shards reproduce the unsharded
+tile (update and forward bit for bit).  Python only bootstraps: the NCCL
+unique id travels from rank 0 to the others over an existing
+``torch.distributed`` group (any backend, CPU objects), after which no
+PyTorch collective is involved.
 """
 from __future__ import annotations
 
@@ -33,84 +36,60 @@ def partition_rows(d_out: int, world: int, rank: int) -> tuple[int, int]:
     return r0, r0 + base + (1 if rank < extra else 0)
 
 
-class RowShardedTile:
-    """One logical d_out x d_in tile, row-sharded over ``group``."""
+def share_unique_id(make_id, group=None) -> bytes:
+    """Rank 0 calls ``make_id()`` (``Comm.unique_id``); every rank returns it.
+    Bootstrap only: one 128-byte object over the torch.distributed group."""
+    import torch.distributed as dist
+    obj = [make_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return obj[0]
 
-    def __init__(self, local, d_out: int, d_in: int, group=None):
-        import torch.distributed as dist
-        self.dist = dist
-        self.group = group
-        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
-        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
-        self.rows = partition_rows(d_out, self.world, self.rank)
+
+def nccl_comm(group=None):
+    """The NCCL communicator of this rank over ``group`` (current CUDA device)."""
+    import torch.distributed as dist
+
+    from .tile import Comm
+    uid = share_unique_id(Comm.unique_id, group)
+    return Comm(uid, dist.get_world_size(group), dist.get_rank(group))
+
+
+class RowShardedTile:
+    """One logical d_out x d_in tile, row-sharded over the ranks of ``comm``.
+
+    ``local`` is this rank's shard handle (``AnalogTile(..., shard=rows)``);
+    the communicator is attached to it here.  All calls take CUDA tensors
+    (device pointers) and are asynchronous on the shard's stream."""
+
+    def __init__(self, local, d_out: int, d_in: int, comm):
         self.local = local
+        self.comm = comm
+        self.world, self.rank = comm.size, comm.rank
+        self.rows = partition_rows(d_out, self.world, self.rank)
         self.d_out, self.d_in = d_out, d_in
-        # the NCCL collectives are issued on torch's current stream: the tile
-        # must run on that same stream, or a reduction could read a buffer
-        # before the tile's kernel has written it (and vice versa)
-        bind = getattr(local, "set_stream", None)
-        if bind is not None:
-            import torch
-            if torch.cuda.is_available():
-                bind(torch.cuda.current_stream().cuda_stream)
+        if self.world > 1:
+            local.attach_comm(comm)
 
     @classmethod
-    def create(cls, d_out: int, d_in: int, settings, seed: int, group=None):
-        """Build the local B200 shard (``AnalogTile(shard=...)``) of this rank."""
-        import torch.distributed as dist
-
+    def create(cls, d_out: int, d_in: int, settings, seed: int, comm):
         from .tile import AnalogTile
-        world = dist.get_world_size(group) if dist.is_initialized() else 1
-        rank = dist.get_rank(group) if dist.is_initialized() else 0
-        r0, r1 = partition_rows(d_out, world, rank)
-        local = AnalogTile(d_out, d_in, settings, seed, shard=(r0, r1) if world > 1 else None)
-        return cls(local, d_out, d_in, group)
-
-    def _amax_global(self, D):
-        amax = self.local.rows_amax(D)
-        if self.world > 1:
-            self.dist.all_reduce(amax, op=self.dist.ReduceOp.MAX, group=self.group)
-        return amax
+        r0, r1 = partition_rows(d_out, comm.size, comm.rank)
+        shard = (r0, r1) if comm.size > 1 else None
+        return cls(AnalogTile(d_out, d_in, settings, seed, shard=shard), d_out, d_in, comm)
 
     def forward(self, X, Y, io=None):
-        """Y[:, local rows] of the noisy forward; no collective."""
+        """Y[:, local rows] of the noisy forward (x replicated on every rank)."""
         self.local.forward_dev(X, Y, io)
         return Y
 
     def update(self, X, D_local, lr=None):
         """B sequential pulsed updates of the whole tile; D_local = this rank's rows of d."""
-        self.local.update_dev(X, D_local, lr, amax_d=self._amax_global(D_local))
+        self.local.update_dev(X, D_local, lr)
 
-    def backward(self, D_local, G, chunks: int | None = None):
-        """Full backward G[B][d_in] (replicated on every rank).
-
-        The batch is cut into ``chunks`` sample ranges (default: 4 when every
-        range keeps >= 64 samples, else 1): all chunk contractions are issued
-        back to back, each followed by its asynchronous all-reduce(sum), so
-        the reduction of chunk c overlaps the contraction of chunk c + 1;
-        the finishes (noise, ADC, alpha) then run in chunk order.  The noise
-        draws are addressed by sample, so every chunking gives the same G."""
-        amax = self._amax_global(D_local)
-        B = int(D_local.shape[0])
-        n = chunks if chunks is not None else (4 if B >= 256 else 1)
-        n = max(1, min(n, B))
-        edges = [B * k // n for k in range(n + 1)]
-        inflight = []
-        for b0, b1 in zip(edges[:-1], edges[1:]):
-            if b1 == b0:
-                continue
-            P = self.local.backward_partial_dev(D_local[b0:b1], amax[b0:b1])
-            work = None
-            if self.world > 1:
-                work = self.dist.all_reduce(P, op=self.dist.ReduceOp.SUM, group=self.group,
-                                            async_op=True)
-            inflight.append((b0, b1, P, work))
-        for b0, b1, P, work in inflight:
-            if work is not None:
-                work.wait()
-            self.local.backward_finish_dev(P, amax[b0:b1], G[b0:b1])
+    def backward(self, D_local, G):
+        """Full backward G[B][d_in] (the same on every rank) from this rank's rows of d."""
+        self.local.backward_dev(D_local, G)
         return G
 
 
-__all__ = ["partition_rows", "RowShardedTile"]
-
+__all__ = ["partition_rows", "share_unique_id", "nccl_comm", "RowShardedTile"]

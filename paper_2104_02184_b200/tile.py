@@ -197,6 +197,57 @@ def _tptr(t) -> int:
     return C.c_void_p(t.data_ptr())
 
 
+class Comm:
+    """Communicator of a row-sharded tile (include/xbtile.h: xb_comm_*).
+
+    ``Comm.unique_id()`` on rank 0, sent to the other ranks out of band, then
+    ``Comm(uid, nranks, rank)`` on every rank (NCCL, current CUDA device);
+    ``Comm.local(n)`` is an in-process group of n handles, one per host thread
+    driving one shard (loopback, for tests on one device)."""
+
+    def __init__(self, uid: Optional[bytes] = None, nranks: int = 1, rank: int = 0, _h=None):
+        if _h is not None:
+            self._h = _h
+            return
+        if uid is None or len(uid) != _abi.COMM_ID_BYTES:
+            raise Error(f"comm: unique id of {_abi.COMM_ID_BYTES} bytes required")
+        buf = (C.c_uint8 * _abi.COMM_ID_BYTES).from_buffer_copy(uid)
+        h = C.c_void_p()
+        _check(_lib.xb_comm_create(buf, nranks, rank, C.byref(h)))
+        self._h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * _abi.COMM_ID_BYTES)()
+        _check(_lib.xb_comm_unique_id(buf))
+        return bytes(buf)
+
+    @staticmethod
+    def local(n: int) -> list:
+        hs = (C.c_void_p * n)()
+        _check(_lib.xb_comm_create_local(n, hs))
+        return [Comm(_h=C.c_void_p(hs[r])) for r in range(n)]
+
+    @property
+    def size(self) -> int:
+        return int(_lib.xb_comm_size(self._h))
+
+    @property
+    def rank(self) -> int:
+        return int(_lib.xb_comm_rank(self._h))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _lib.xb_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class AnalogTile:
     """GPU AnalogTile (proj/include/xbarsim/tile.hpp:75-131)."""
 
@@ -343,6 +394,13 @@ class AnalogTile:
     # -- device-resident entries (torch CUDA tensors or anything with data_ptr())
     def stream(self) -> int:
         return _lib.xb_tile_stream(self._h) or 0
+
+    def attach_comm(self, comm: Optional["Comm"]) -> None:
+        """Route this row shard's cross-shard reductions through ``comm``
+        (update: max|d|; forward: BM flags; backward: max|d| and the column
+        sums).  The communicator must outlive the attachment."""
+        _check(_lib.xb_tile_attach_comm(self._h, comm._h if comm is not None else None))
+        self._comm = comm
 
     def set_stream(self, stream_handle: int) -> None:
         _check(_lib.xb_tile_set_stream(self._h, C.c_void_p(stream_handle)))

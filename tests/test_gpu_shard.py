@@ -1,7 +1,8 @@
 """Row sharding on one GPU: two shard handles of one logical tile reproduce
-the unsharded tile (Philox draws are keyed on global rows).  The collective
-(max over shards of max|d|, sum of backward partials) is done here on the
-host side with torch ops, exactly what RowShardedTile does with NCCL."""
+the unsharded tile (Philox draws are keyed on global rows).  Here the
+collective (max over shards of max|d|, sum of backward partials) is done by
+hand between the split-phase entries; tests/test_gpu_comm.py runs the same
+through the library's communicators (xb_comm)."""
 import numpy as np
 import pytest
 import torch
@@ -93,29 +94,37 @@ def test_sharded_backward_matches_within_one_lsb():
 
 @pytest.mark.parametrize("prec", [xb.MVM_TF32, xb.MVM_FP32])
 def test_chunked_backward_equals_one_shot(prec):
-    """RowShardedTile.backward in sample chunks (partials issued ahead of
-    their finishes, FIFO) draws the same noise as one call over the batch:
-    G is bit-identical, and the tile's backward counter ends in the same
-    place (a following backward agrees too)."""
-    from paper_2104_02184_b200.parallel import RowShardedTile
+    """The split-phase backward entries in sample chunks -- partials issued
+    ahead of their finishes (FIFO), as the sharded backward does to overlap
+    each chunk's reduction with the next contraction -- draw the same noise as
+    one call over the batch: G is bit-identical, and the tile's backward
+    counter ends in the same place (a following backward agrees too)."""
     R, C, B = 192, 160, 256
     bio = xb.default_io()
     bio.bound_management = xb.BM_NONE
     s = xb.TileSettings(device=xb.device_preset("reram_sb"), backward_io=bio, mvm_precision=prec)
     W = np.random.default_rng(8).uniform(-0.3, 0.3, (R, C)).astype(np.float32)
     stream = torch.cuda.current_stream()
+
+    def run(t, D, G, chunks):
+        amax = t.rows_amax(D)
+        edges = [B * k // chunks for k in range(chunks + 1)]
+        parts = [(b0, b1, t.backward_partial_dev(D[b0:b1], amax[b0:b1]))
+                 for b0, b1 in zip(edges[:-1], edges[1:])]
+        for b0, b1, P in parts:
+            t.backward_finish_dev(P, amax[b0:b1], G[b0:b1])
+
     outs = []
     for chunks in (1, 4, 3):
         t = xb.AnalogTile(R, C, s, 21)
         t.set_stream(stream.cuda_stream)
         t.set_weights(W)
-        sh = RowShardedTile(t, R, C)
         g = torch.Generator(device="cuda").manual_seed(6)
         D = torch.rand(B, R, device="cuda", generator=g) * 2 - 1
         G1 = torch.empty(B, C, device="cuda")
         G2 = torch.empty(B, C, device="cuda")
-        sh.backward(D, G1, chunks=chunks)
-        sh.backward(D, G2, chunks=1)
+        run(t, D, G1, chunks)
+        run(t, D, G2, 1)
         torch.cuda.synchronize()
         outs.append((G1.cpu().numpy(), G2.cpu().numpy()))
     for G1, G2 in outs[1:]:

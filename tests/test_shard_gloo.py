@@ -1,11 +1,16 @@
-"""World-size-2 gloo test of the row-sharding orchestration (CPU).
+"""World-size-2 gloo tests of the row-sharding orchestration (CPU).
 
-RowShardedTile's collectives (all-reduce max of max|d|, all-reduce sum of the
-backward partials) run over gloo between two processes.  The local compute
-object is a test double restating the deterministic, noise-free tile in
-numpy (ConstantStep, deterministic_implicit pulses, perfect IO) -- it is
-test infrastructure, not a product fallback -- and the sharded result must
-equal the unsharded oracle tile."""
+* the NCCL bootstrap (parallel.share_unique_id): rank 0's 128-byte unique id
+  reaches every rank over a torch.distributed group;
+* the sharding algebra the C library implements (include/xbtile.h, "row
+  sharding"; csrc/xb_comm.cu): all-reduce(max) of max|d| before translate,
+  all-reduce(sum) of the per-shard column sums (in in-flight sample chunks,
+  finished in order), row-local forward.  The collectives run over gloo
+  between two processes; the per-shard compute is a test double restating
+  the deterministic, noise-free tile in numpy (ConstantStep,
+  deterministic_implicit pulses, perfect IO) -- test infrastructure, not a
+  product fallback -- and the sharded result must equal the unsharded oracle
+  tile.  The same orchestration on the device is tests/test_gpu_comm.py."""
 import os
 
 import numpy as np
@@ -15,7 +20,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle
-from paper_2104_02184_b200.parallel import RowShardedTile, partition_rows
+from paper_2104_02184_b200.parallel import partition_rows, share_unique_id
 
 R, C, B, LR, DW = 13, 9, 6, 0.05, 0.01
 
@@ -53,13 +58,46 @@ class NumpyShard:
         G[:] = P
 
 
+class ShardedOrchestration:
+    """The C library's sharded-tile control flow (csrc/xb_abi.cu:
+    update_device / backward_sharded; csrc/xb_mvm.cu: row-local forward),
+    restated over torch.distributed for this CPU test."""
+
+    def __init__(self, local):
+        self.local = local
+
+    def _amax(self, D):
+        a = self.local.rows_amax(D)
+        dist.all_reduce(a, op=dist.ReduceOp.MAX)
+        return a
+
+    def update(self, X, D_local, lr):
+        self.local.update_dev(X, D_local, lr, amax_d=self._amax(D_local))
+
+    def backward(self, D_local, G, chunks=1):
+        amax = self._amax(D_local)
+        B_ = D_local.shape[0]
+        edges = [B_ * k // chunks for k in range(chunks + 1)]
+        inflight = []
+        for b0, b1 in zip(edges[:-1], edges[1:]):
+            P = self.local.backward_partial_dev(D_local[b0:b1], amax[b0:b1])
+            inflight.append((b0, b1, P, dist.all_reduce(P, async_op=True)))
+        for b0, b1, P, work in inflight:
+            work.wait()
+            self.local.backward_finish_dev(P, amax[b0:b1], G[b0:b1])
+
+    def forward(self, X, Y):
+        self.local.forward_dev(X, Y)
+
+
 def _worker(rank, world, port, W, X, D, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    uid = share_unique_id(lambda: bytes(range(128)))
+    assert uid == bytes(range(128))
     r0, r1 = partition_rows(R, world, rank)
-    t = RowShardedTile(NumpyShard(W, r0, r1), R, C)
-    assert t.rows == (r0, r1)
+    t = ShardedOrchestration(NumpyShard(W, r0, r1))
     Dl = torch.from_numpy(D[:, r0:r1].copy())
     Xt = torch.from_numpy(X)
     t.update(Xt, Dl, LR)
