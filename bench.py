@@ -6,10 +6,15 @@ management on) followed by the 256 sequential pulsed updates.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun, one process per GPU): one logical (4096 N) x 4096 tile,
-row-sharded, 4096 rows per GPU (weak scaling).  x is replicated, the only
-collective is the all-reduce(max) of the per-sample max|d| the pulse
-translation needs (proj/src/pulsed.cpp:34-51); the forward is row-local.
+N > 1 (torchrun, one process per GPU): the north star's multi-GPU case,
+BASELINE config 5 -- ONE logical 16384 x 16384 reram_sb tile row-sharded over
+the N GPUs (strong scaling; 16384/N rows per GPU), the same step (forward
+with output noise, bound management and ADC, then the pulsed update of 256
+samples).  The cross-GPU reductions (max|d| for translate, the bound-
+management flags) run inside libxbtile over NCCL (xb_comm, NVLink/NVSwitch);
+torch.distributed (gloo) only bootstraps the NCCL id and gathers the timings.
+The line also carries a weak-scaling measurement ((4096 N) x 4096, 4096 rows
+per GPU) and the PCM program + drift_to pass on the 16384^2 shards.
 
 --impl reference times the reference CPU implementation (oracle/_ref, the
 xbarsim sources compiled here; the C restatement when _ref is absent) on the
@@ -99,7 +104,10 @@ class Clocks:
 
 
 # ============================================================ our arm
-def make_tile(xb, rank, world):
+CFG5 = 16384  # BASELINE config 5: 16384 x 16384 tile, row-sharded over N GPUs
+
+
+def tile_settings(xb, prec=None):
     dev = xb.device_preset("reram_sb")
     fwd = xb.default_io()
     fwd.bound_management = xb.BM_ITERATIVE
@@ -107,11 +115,53 @@ def make_tile(xb, rank, world):
     # TF32 tensor-core contraction: its ~1e-3 relative error (of the dot-product
     # scale) is far below sigma_out = 0.06 and the 9-bit ADC step
     cfg = xb.TileSettings(device=dev, forward_io=fwd, backward_io=xb.default_io(),
-                          mvm_precision=xb.MVM_TF32)
+                          mvm_precision=prec if prec is not None else xb.MVM_TF32)
     cfg.update.bl = 31
-    d_out = N_ROWS * world
-    shard = (rank * N_ROWS, (rank + 1) * N_ROWS) if world > 1 else None
-    return xb.AnalogTile(d_out, N_COLS, cfg, 1234, shard=shard), cfg
+    return cfg
+
+
+def make_tile(xb, rank, world, d_out=N_ROWS, d_in=N_COLS, comm=None):
+    """This rank's shard of a d_out x d_in tile (the whole tile when world == 1)."""
+    from paper_2104_02184_b200.parallel import partition_rows
+    cfg = tile_settings(xb)
+    if world == 1:
+        return xb.AnalogTile(d_out, d_in, cfg, 1234), cfg, (0, d_out)
+    r0, r1 = partition_rows(d_out, world, rank)
+    t = xb.AnalogTile(d_out, d_in, cfg, 1234, shard=(r0, r1))
+    t.attach_comm(comm)
+    return t, cfg, (r0, r1)
+
+
+def timed_steps(torch, dist, tile, stream, Xs, Ds, Y, steps, warmup, world, clk=None):
+    """W untimed steps, then K steps between CUDA events on the tile stream,
+    bracketed by a barrier + device sync; returns the max over ranks (ms)
+    plus this rank's phase timings."""
+    def step(s):
+        tile.forward_dev(Xs[s], Y)        # sharded: BM flags all-reduced per pass (NCCL)
+        tile.update_dev(Xs[s], Ds[s], LR)  # sharded: global max|d| all-reduced (NCCL)
+    for s in range(warmup):
+        step(s)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    tile.set_timing(True)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for s in range(steps):
+        step(warmup + s)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if clk is not None:
+        clk.__exit__(None, None, None)
+    timing = tile.read_timing()
+    tile.set_timing(False)
+    t = torch.tensor([e0.elapsed_time(e1)] + [timing[k][0] for k in tile.TIMERS[:3]],
+                     dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)  # gloo, CPU tensor
+    return t.tolist(), [timing[k][1] for k in tile.TIMERS]
 
 
 def run_ours(args):
@@ -119,181 +169,137 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_2104_02184_b200 as xb
+    from paper_2104_02184_b200.parallel import nccl_comm
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # validation-only overrides (never for a reported number): run the N > 1
-    # code path with every rank on one device and gloo host collectives
-    if os.environ.get("XB_BENCH_DEVICE"):
+    # validation-only override (never for a reported number): every rank on one
+    # device, loopback collectives instead of NCCL (tests/test_gpu_bench.py)
+    loopback = bool(os.environ.get("XB_BENCH_DEVICE"))
+    if loopback:
         local = int(os.environ["XB_BENCH_DEVICE"])
     torch.cuda.set_device(local)
+    comm = None
     if world > 1:
-        dist.init_process_group(os.environ.get("XB_BENCH_DIST_BACKEND", "nccl"))
+        # gloo: bootstrap (NCCL id) and timing gathers only; data path = libxbtile + NCCL
+        dist.init_process_group("gloo")
+        comm = loopback_comm(xb, dist, world, rank) if loopback else nccl_comm()
     dev = torch.device("cuda", local)
     # a dedicated (non-default) stream shared by torch and the tile, so CUDA
-    # events, NCCL and the tile's kernels are ordered on one queue
+    # events and the tile's kernels (and its NCCL calls) are ordered on one queue
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
 
-    from paper_2104_02184_b200.parallel import RowShardedTile
-    tile, cfg = make_tile(xb, rank, world)
+    R_total = N_ROWS if world == 1 else CFG5
+    C = N_COLS if world == 1 else CFG5
+    tile, cfg, (r0, r1) = make_tile(xb, rank, world, R_total, C, comm)
     tile.set_stream(stream.cuda_stream)
-    sharded = RowShardedTile(tile, N_ROWS * world, N_COLS)
+    rows = r1 - r0
     g = torch.Generator(device=dev)
     g.manual_seed(7 + rank)
-    w0 = (torch.rand(N_ROWS, N_COLS, generator=g, device=dev) * 0.2 - 0.1)
+    w0 = torch.rand(rows, C, generator=g, device=dev) * 0.2 - 0.1
     tile.set_weights(w0.cpu().numpy())
     nsets = args.steps + args.warmup
     # distinct synthetic batches per step; x is replicated (same seed on every rank)
     gx = torch.Generator(device=dev)
     gx.manual_seed(7)
-    Xs = [torch.rand(BATCH, N_COLS, generator=gx, device=dev) * 2 - 1 for _ in range(nsets)]
-    Ds = [torch.rand(BATCH, N_ROWS, generator=g, device=dev) * 2 - 1 for _ in range(nsets)]
-    Y = torch.empty(BATCH, N_ROWS, device=dev)
-
-    def step(s):
-        sharded.forward(Xs[s], Y)          # row-local, no collective
-        if world > 1:
-            sharded.update(Xs[s], Ds[s], LR)  # all-reduce(max) of max|d| over NCCL
-        else:
-            tile.update_dev(Xs[s], Ds[s], LR)
+    nx = min(nsets, 8) if world > 1 else nsets  # 16 MB per x batch at 16384 columns
+    Xs = [torch.rand(BATCH, C, generator=gx, device=dev) * 2 - 1 for _ in range(nx)]
+    Ds = [torch.rand(BATCH, rows, generator=g, device=dev) * 2 - 1 for _ in range(nx)]
+    Xs = [Xs[k % nx] for k in range(nsets)]
+    Ds = [Ds[k % nx] for k in range(nsets)]
+    Y = torch.empty(BATCH, rows, device=dev)
 
     clk = Clocks(local).__enter__()  # sampling starts before the warm-up so it spans the timed region
-    for s in range(args.warmup):
-        step(s)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-
-    tile.set_timing(True)
     launches0 = xb.launch_count()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    if True:
-        e0.record(stream)
-        for s in range(args.steps):
-            step(args.warmup + s)
-        e1.record(stream)
-        torch.cuda.synchronize()
-    clk.__exit__(None, None, None)
+    (ms_total, ms_pulse, ms_trains, ms_fwd), ph_n = timed_steps(
+        torch, dist, tile, stream, Xs, Ds, Y, args.steps, args.warmup, world, clk)
     launches = xb.launch_count() - launches0
-    ms_total = e0.elapsed_time(e1)
-    timing = tile.read_timing()
-    tile.set_timing(False)
-    ph_ms = [timing[k][0] for k in tile.TIMERS]
-    ph_n = [timing[k][1] for k in tile.TIMERS]
-
-    t = torch.tensor([ms_total, ph_ms[0], ph_ms[1], ph_ms[2]], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_total, ms_pulse, ms_trains, ms_fwd = t.tolist()
+    launches = int(round(launches * args.steps / (args.steps + args.warmup)))  # timed steps only
     ms_step = ms_total / args.steps
-    cells = float(N_ROWS) * world * N_COLS * BATCH
+    cells = float(R_total) * C * BATCH
     value = cells / (ms_step * 1e-3)
 
     # ---------- e2e through the public host-buffer API (pinned host inputs)
-    e2e = None
     n_e2e = max(2, min(args.steps, 10))
-    if world == 1:
-        # AnalogTile.forward / update with host arrays: H2D, finiteness check,
-        # kernels and the D2H of y inside each call
-        Xh = [x.cpu().pin_memory().numpy() for x in Xs[:n_e2e]]
-        Dh = [d.cpu().pin_memory().numpy() for d in Ds[:n_e2e]]
-        e2e_tile, _ = make_tile(xb, 0, 1)
-        e2e_tile.set_weights(w0.cpu().numpy())
-        # the result lands in pinned host memory (DMA at full PCIe rate)
-        yh = torch.empty(BATCH, N_ROWS, dtype=torch.float32).pin_memory().numpy()
-        for k in range(2):  # warm
-            e2e_tile.forward(Xh[k], out=yh)
-            e2e_tile.update(Xh[k], Dh[k], LR)
-        t0 = time.perf_counter()
-        for k in range(n_e2e):
-            e2e_tile.forward(Xh[k], out=yh)
-            e2e_tile.update(Xh[k], Dh[k], LR)
-        el = time.perf_counter() - t0
-        _ = float(yh[0, 0])
-        e2e = {"value": N_ROWS * N_COLS * BATCH * n_e2e / el, "unit": UNIT,
-               "h2d_bytes_per_step": int(BATCH * N_COLS * 4 * 2 + BATCH * N_ROWS * 4),
-               "d2h_bytes_per_step": int(BATCH * N_ROWS * 4),
-               "steps": n_e2e, "api": "AnalogTile.forward(X host) + AnalogTile.update(X, D host)"}
-    else:
-        # RowShardedTile (the multi-GPU API) fed from pinned host buffers: each
-        # rank copies x and its rows of d in, runs the sharded forward + update
-        # (NCCL max|d| all-reduce) and reads its rows of y back; max over ranks
-        Xh = [x.cpu().pin_memory() for x in Xs[:n_e2e]]
-        Dh = [d.cpu().pin_memory() for d in Ds[:n_e2e]]
-        yh = torch.empty(BATCH, N_ROWS, dtype=torch.float32).pin_memory()
-        Xd = torch.empty(BATCH, N_COLS, device=dev)
-        Dd = torch.empty(BATCH, N_ROWS, device=dev)
-
-        def e2e_step(k):
-            Xd.copy_(Xh[k], non_blocking=True)
-            Dd.copy_(Dh[k], non_blocking=True)
-            sharded.forward(Xd, Y)
-            sharded.update(Xd, Dd, LR)
-            yh.copy_(Y, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-        e2e_step(0)  # warm
+    Xh = [Xs[k].cpu().pin_memory().numpy() for k in range(n_e2e)]
+    Dh = [Ds[k].cpu().pin_memory().numpy() for k in range(n_e2e)]
+    e2e_tile, _, _ = make_tile(xb, rank, world, R_total, C, comm)
+    e2e_tile.set_weights(w0.cpu().numpy())
+    # the result lands in pinned host memory (DMA at full PCIe rate)
+    yh = torch.empty(BATCH, rows, dtype=torch.float32).pin_memory().numpy()
+    for k in range(2):  # warm
+        e2e_tile.forward(Xh[k], out=yh)
+        e2e_tile.update(Xh[k], Dh[k], LR)
+    if world > 1:
         dist.barrier()
-        t0 = time.perf_counter()
-        for k in range(n_e2e):
-            e2e_step(k)
-        el_t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-        dist.all_reduce(el_t, op=dist.ReduceOp.MAX)
-        el = float(el_t.item())
-        e2e = {"value": N_ROWS * world * N_COLS * BATCH * n_e2e / el, "unit": UNIT,
-               "h2d_bytes_per_step": int(world * (BATCH * N_COLS * 4 + BATCH * N_ROWS * 4)),
-               "d2h_bytes_per_step": int(world * BATCH * N_ROWS * 4),
-               "steps": n_e2e, "api": "RowShardedTile.forward + update from pinned host buffers "
-                                      "(per-rank H2D of x and local d, D2H of local y)"}
+    t0 = time.perf_counter()
+    for k in range(n_e2e):
+        e2e_tile.forward(Xh[k], out=yh)
+        e2e_tile.update(Xh[k], Dh[k], LR)
+    el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    _ = float(yh[0, 0])
+    del e2e_tile
+    e2e = {"value": cells * n_e2e / float(el.item()), "unit": UNIT,
+           "h2d_bytes_per_step": int(world * (BATCH * C * 4 * 2 + BATCH * rows * 4)),
+           "d2h_bytes_per_step": int(world * BATCH * rows * 4),
+           "steps": n_e2e,
+           "api": ("AnalogTile.forward(X host) + AnalogTile.update(X, D host)" if world == 1 else
+                   "per rank: AnalogTile(shard).forward(X host) + update(X, D_local host), "
+                   "NCCL reductions inside libxbtile")}
+
+    extra = {}
+    if world > 1:
+        extra = sharded_extras(torch, dist, xb, tile, comm, stream, rank, world, r0, r1, args)
 
     if rank == 0:
         pk, pk_kind = peaks()
         clocks = clk.summary()
         # --- measured pulses per cell-update (k-bar) on 32 samples of the workload:
         # sum_ij popc(x_j & d_i) = sum_t (#x lines firing slot t)(#d lines firing slot t)
-        kb_tile = tile.clone()
-        xw, dw, _ = kb_tile.generate_trains(Xs[0][:32].cpu().numpy(), Ds[0][:32].cpu().numpy(), LR)
-        del kb_tile
-        pulses = 0
-        for b in range(xw.shape[0]):
-            cx = ((xw[b][:, None] >> np.arange(31, dtype=np.uint32)) & 1).sum(axis=0)
-            cd = ((dw[b][:, None] >> np.arange(31, dtype=np.uint32)) & 1).sum(axis=0)
-            pulses += int((cx.astype(np.int64) * cd.astype(np.int64)).sum())
-        kbar = pulses / (xw.shape[0] * xw.shape[1] * dw.shape[1])
+        kbar = measure_kbar(xb, R_total if world == 1 else rows, C, Xs[0][:32].cpu().numpy(),
+                            Ds[0][:32].cpu().numpy())
         # --- roofline of the dominant kernel (pulse_kernel): integer pipe, SURVEY 8d
-        int_ops = (2.0 + kbar * 15.0) * N_ROWS * N_COLS * BATCH  # per launch (per step)
+        int_ops = (2.0 + kbar * 15.0) * rows * C * BATCH  # per launch (per step, this GPU)
         pulse_ms = ms_pulse / max(ph_n[0], 1)
         sm_mhz = pk.get("sm_max_mhz", 1965.0)
         int_peak = 148 * 64 * sm_mhz * 1e6  # ALU-pipe lane-ops/s (16 lanes/clk/SMSP)
         achieved = int_ops / (pulse_ms * 1e-3)
-        mvm_flops = 2.0 * N_ROWS * N_COLS * BATCH
-        mvm_bytes = 4.0 * N_ROWS * N_COLS + 4.0 * BATCH * (N_ROWS + N_COLS)
+        mvm_bytes = 4.0 * rows * C + 4.0 * BATCH * (rows + C)
         fwd_ms = ms_fwd / max(ph_n[2], 1)
+        if world == 1:
+            workload = ("NS: 4096x4096 reram_sb (SoftBounds, d2d 0.3, c2c 0.3), BL 31, batch 256, "
+                        "lr 0.01; forward default IO + BM")
+        else:
+            workload = (f"cfg5: 16384x16384 reram_sb tile row-sharded over {world} GPUs "
+                        f"({rows} rows each), BL 31, batch 256, lr 0.01; forward default IO "
+                        "(sigma_out 0.06, DAC 7 b, ADC 9 b) + BM; NCCL reductions in libxbtile")
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
+            "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (x, d ~ U(-1,1), W0 ~ U(-0.1,0.1), seed 7)",
-            "config": {"workload": "NS: 4096x4096 reram_sb (SoftBounds, d2d 0.3, c2c 0.3), "
-                                   "BL 31, batch 256, lr 0.01; forward default IO + BM",
-                       "tile_rows_total": N_ROWS * world, "tile_cols": N_COLS,
-                       "rows_per_gpu": N_ROWS, "batch": BATCH,
+            "config": {"workload": workload,
+                       "tile_rows_total": R_total, "tile_cols": C,
+                       "rows_per_gpu": rows, "batch": BATCH,
                        "parallelism": f"row-shard{world}",
-                       "l2": "no flush: per-step working set (W + per-cell params 335 MB) > "
-                             "126 MB L2; fresh input batch every step",
+                       "l2": "no flush: per-step working set (W + per-cell params, 335 MB per "
+                             "GPU at 4096^2) > 126 MB L2; fresh input batch every step",
                        "mvm_precision": "tf32 (tcgen05)"},
-            "mvm": {"samples_per_s": BATCH * world / (fwd_ms * 1e-3), "ms_per_batch": fwd_ms},
+            "mvm": {"samples_per_s": BATCH / (fwd_ms * 1e-3), "ms_per_batch": fwd_ms},
             "phase_ms_per_step": {"pulse": pulse_ms, "trains": ms_trains / max(ph_n[1], 1),
                                   "forward": fwd_ms},
             "roofline": {"bound": "int-pipe", "achieved": achieved / 1e9,
                          "peak": int_peak / 1e9, "unit": "Gop/s",
-                         "frac": achieved / int_peak, "traffic": pulse_traffic(),
+                         "frac": achieved / int_peak,
+                         "traffic": pulse_traffic() if world == 1 else None,
                          "traffic_unit": "DRAM bytes per launch (read + write)",
-                         "algorithmic_bytes": 4.0 * 2 * N_ROWS * N_COLS + 16.0 * N_ROWS * N_COLS
-                         + 4.0 * (N_ROWS + N_COLS) * BATCH,
+                         "algorithmic_bytes": 4.0 * 2 * rows * C + 16.0 * rows * C
+                         + 4.0 * (rows + C) * BATCH,
                          "kernel": "pulse_kernel<SOFT_BOUNDS,noise>",
                          "basis": f"SURVEY 8d: (2 + kbar*15) INT ops per cell-update, "
                                   f"kbar={kbar:.4f} measured on 32 samples",
@@ -301,16 +307,84 @@ def run_ours(args):
             "roofline_mvm": {"bound": "hbm", "achieved": mvm_bytes / (fwd_ms * 1e-3) / 1e9,
                              "peak": pk["hbm_gbs"], "unit": "GB/s",
                              "frac": mvm_bytes / (fwd_ms * 1e-3) / 1e9 / pk["hbm_gbs"],
-                             "tflops": mvm_flops / (fwd_ms * 1e-3) / 1e12},
+                             "tflops": 2.0 * rows * C * BATCH / (fwd_ms * 1e-3) / 1e12,
+                             "basis": "algorithmic bytes 4 N_r N_c + 4 B (N_r + N_c) per "
+                                      "forward of this GPU; BM re-issues are overhead"},
             "clocks": clocks,
             "gpu_launches": int(launches),
             "e2e": e2e,
         }
+        out.update(extra)
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline_sample()
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
+
+
+def loopback_comm(xb, dist, world, rank):
+    """Validation only (XB_BENCH_DEVICE, tests/test_gpu_bench.py): every rank
+    of the torchrun job shares one GPU, where NCCL cannot form a group, so each
+    rank gets a one-rank NCCL communicator.  The multi-rank control flow
+    (sharded tiles, gathers, max-over-ranks timing) runs; the cross-rank
+    reductions do not -- the numbers are neither measurements nor the
+    unsharded tile's (the sharded arithmetic is tests/test_gpu_comm.py)."""
+    return xb.Comm(xb.Comm.unique_id(), 1, 0)
+
+
+def measure_kbar(xb, rows, cols, X, D):
+    """Pulses per cell-update of the workload's trains (32 samples)."""
+    t = xb.AnalogTile(rows, cols, tile_settings(xb), 1234)
+    xw, dw, _ = t.generate_trains(X, D[:, :rows], LR)
+    del t
+    pulses = 0
+    for b in range(xw.shape[0]):
+        cx = ((xw[b][:, None] >> np.arange(31, dtype=np.uint32)) & 1).sum(axis=0)
+        cd = ((dw[b][:, None] >> np.arange(31, dtype=np.uint32)) & 1).sum(axis=0)
+        pulses += int((cx.astype(np.int64) * cd.astype(np.int64)).sum())
+    return pulses / (xw.shape[0] * xw.shape[1] * dw.shape[1])
+
+
+def sharded_extras(torch, dist, xb, tile, comm, stream, rank, world, r0, r1, args):
+    """Weak scaling alongside ((4096 N) x 4096, 4096 rows per GPU, same step)
+    and the cfg5 PCM program + drift_to pass on this rank's 16384^2 rows."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    wt, _, (w0, w1) = make_tile(xb, rank, world, N_ROWS * world, N_COLS, comm)
+    wt.set_stream(stream.cuda_stream)
+    g = torch.Generator(device=dev)
+    g.manual_seed(11 + rank)
+    wt.set_weights((torch.rand(w1 - w0, N_COLS, generator=g, device=dev) * 0.2 - 0.1)
+                   .cpu().numpy())
+    gx = torch.Generator(device=dev)
+    gx.manual_seed(7)
+    n = args.steps + args.warmup
+    Xs = [torch.rand(BATCH, N_COLS, generator=gx, device=dev) * 2 - 1 for _ in range(4)]
+    Ds = [torch.rand(BATCH, w1 - w0, generator=g, device=dev) * 2 - 1 for _ in range(4)]
+    Y = torch.empty(BATCH, w1 - w0, device=dev)
+    (ms, _, _, _), _ = timed_steps(torch, dist, wt, stream, [Xs[k % 4] for k in range(n)],
+                                   [Ds[k % 4] for k in range(n)], Y, args.steps, args.warmup,
+                                   world)
+    del wt
+    weak = {"tile": f"{N_ROWS * world}x{N_COLS}", "rows_per_gpu": N_ROWS,
+            "ms_per_step": ms / args.steps,
+            "value": float(N_ROWS) * world * N_COLS * BATCH / (ms / args.steps * 1e-3),
+            "unit": UNIT}
+    # PCM programming noise + drift (inference.cpp:34-76) on this rank's rows
+    model = xb.InferenceNoiseModel()
+    target = (torch.rand(r1 - r0, CFG5, generator=g, device=dev) * 0.4 - 0.2).cpu().numpy()
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    tile.program(target, model, 99 + rank)
+    t1 = time.perf_counter()
+    tile.drift_to(1e4)
+    t2 = time.perf_counter()
+    tm = torch.tensor([t1 - t0, t2 - t1], dtype=torch.float64)
+    dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    return {"weak_scaling": weak,
+            "inference_pass": {"program_s": tm[0].item(), "drift_to_s": tm[1].item(),
+                               "note": "host API (program uploads the target from host "
+                                       "memory), max over ranks"}}
 
 
 def pulse_traffic():

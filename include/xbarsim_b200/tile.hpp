@@ -16,6 +16,7 @@
 // mini-batch after all its forwards/backwards (proj/src/nn.cpp:708-735).
 #pragma once
 
+#include <array>
 #include <cmath>
 #include <cstdint>
 #include <limits>
@@ -24,6 +25,8 @@
 #include <stdexcept>
 #include <string>
 #include <string_view>
+#include <tuple>
+#include <utility>
 #include <vector>
 
 #include "../xbtile.h"
@@ -855,6 +858,109 @@ inline DriftCompensation calibrate_compensation(AnalogTile &tile,
   check(xb_tile_probe_readout(tile.handle(), &m, &out));
   return DriftCompensation{out};
 }
+
+// ------------------------------------------------------------ row sharding
+// Multi-GPU extension (no reference symbol: the reference tile is one device;
+// SURVEY.md 8e).  A Comm joins the ranks of one logical tile: NCCL over
+// NVLink/NVSwitch (unique id from rank 0, sent out of band), or an in-process
+// loopback group whose members are driven by one host thread each.
+class Comm {
+public:
+  using Id = std::array<uint8_t, XB_COMM_ID_BYTES>;
+  static Id unique_id() {
+    Id id{};
+    check(xb_comm_unique_id(id.data()));
+    return id;
+  }
+  // ncclCommInitRank on the current CUDA device (collective over the ranks)
+  Comm(const Id &id, int nranks, int rank) { check(xb_comm_create(id.data(), nranks, rank, &h_)); }
+  static std::vector<Comm> local(int nranks) {
+    std::vector<xb_comm *> hs(static_cast<size_t>(nranks), nullptr);
+    check(xb_comm_create_local(nranks, hs.data()));
+    std::vector<Comm> out;
+    for (xb_comm *h : hs) out.emplace_back(Comm(h));
+    return out;
+  }
+  Comm(Comm &&o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+  Comm &operator=(Comm &&o) noexcept {
+    std::swap(h_, o.h_);
+    return *this;
+  }
+  Comm(const Comm &) = delete;
+  ~Comm() {
+    if (h_) xb_comm_destroy(h_);
+  }
+  int size() const { return xb_comm_size(h_); }
+  int rank() const { return xb_comm_rank(h_); }
+  xb_comm *handle() const { return h_; }
+
+private:
+  explicit Comm(xb_comm *h) : h_(h) {}
+  xb_comm *h_ = nullptr;
+};
+
+// contiguous, balanced row ranges; the first d_out % P ranks get one more row
+inline std::pair<int, int> partition_rows(int d_out, int world, int rank) {
+  if (world < 1 || rank < 0 || rank >= world || d_out < world)
+    throw Error("partition_rows: need 0 <= rank < world <= d_out");
+  const int base = d_out / world, extra = d_out % world;
+  const int r0 = rank * base + std::min(rank, extra);
+  return {r0, r0 + base + (rank < extra ? 1 : 0)};
+}
+
+// This rank's shard of one logical d_out x d_in AnalogTile.  x is replicated;
+// d and y are this rank's rows; the backward returns the full g on every
+// rank.  update and forward are bit for bit those of the unsharded tile
+// (global-index random draws; max|d| and the bound-management flags are
+// all-reduced); the backward differs only by the fp32 order of the
+// cross-rank sum.  Host buffers, synchronous, like AnalogTile's batch calls.
+class RowShardedTile {
+public:
+  RowShardedTile(int d_out, int d_in, const TileSettings &settings, uint64_t seed, Comm &comm)
+      : d_out_(d_out), d_in_(d_in) {
+    std::tie(r0_, r1_) = partition_rows(d_out, comm.size(), comm.rank());
+    const xb_tile_config c = detail::to_c(settings);
+    const xb_shard sh{r0_, r1_, d_out, 0};
+    check(xb_tile_create(&c, d_out, d_in, seed, &sh, &h_));
+    if (xb_tile_attach_comm(h_, comm.handle())) {
+      const std::string msg = xb_last_error();
+      xb_tile_destroy(h_);
+      throw Error(msg);
+    }
+  }
+  ~RowShardedTile() {
+    if (h_) xb_tile_destroy(h_);
+  }
+  RowShardedTile(const RowShardedTile &) = delete;
+  RowShardedTile &operator=(const RowShardedTile &) = delete;
+
+  int d_out() const { return d_out_; }
+  int d_in() const { return d_in_; }
+  int row_begin() const { return r0_; }
+  int row_end() const { return r1_; }
+  int local_rows() const { return r1_ - r0_; }
+
+  // W rows [row_begin, row_end), row-major
+  void set_weights(const float *w_local) { check(xb_tile_set_weights(h_, w_local)); }
+  std::vector<float> get_weights() const {
+    std::vector<float> w(static_cast<size_t>(local_rows()) * d_in_);
+    check(xb_tile_get_weights(h_, w.data()));
+    return w;
+  }
+  // X [B][d_in] -> Y [B][local_rows]
+  void forward_batch(const float *X, int B, float *Y) { check(xb_tile_forward(h_, X, B, Y)); }
+  // D [B][local_rows] -> G [B][d_in] (all rows)
+  void backward_batch(const float *D, int B, float *G) { check(xb_tile_backward(h_, D, B, G)); }
+  // B sequential updates of the whole tile (lr[B] may be null)
+  void update_batch(const float *X, const float *D, int B, const double *lr) {
+    check(xb_tile_update(h_, X, D, B, lr));
+  }
+  xb_tile *handle() const { return h_; }
+
+private:
+  xb_tile *h_ = nullptr;
+  int d_out_ = 0, d_in_ = 0, r0_ = 0, r1_ = 0;
+};
 
 inline double drift_compensation_factor(AnalogTile &tile, const DriftCompensation &comp,
                                         const InferenceNoiseModel &model) {

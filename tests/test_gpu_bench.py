@@ -1,8 +1,10 @@
 """bench.py contract checks on the GPU: the N = 1 line and the N > 1 code
-path (row-sharded tile, max|d| all-reduce, max-over-ranks timing) run as two
-torchrun ranks.  With one GPU both ranks share cuda:0 and all-reduce through
-gloo on the host (XB_BENCH_DEVICE / XB_BENCH_DIST_BACKEND): this validates the
-multi-rank logic only -- its timings are not measurements."""
+path (the cfg5 16384^2 tile row-sharded over the ranks, max-over-ranks
+timing, weak-scaling and inference extras) run as two torchrun ranks.  With
+one GPU both ranks share cuda:0, where NCCL cannot join them, so each rank
+gets a one-rank communicator (XB_BENCH_DEVICE): this validates the multi-rank
+control flow only -- its timings are not measurements and its reductions are
+rank-local (the sharded arithmetic itself: tests/test_gpu_comm.py)."""
 import json
 import os
 import subprocess
@@ -36,7 +38,7 @@ def test_bench_single_gpu_line():
 
 @pytest.mark.gpu
 def test_bench_two_rank_code_path():
-    env = dict(os.environ, XB_BENCH_DEVICE="0", XB_BENCH_DIST_BACKEND="gloo")
+    env = dict(os.environ, XB_BENCH_DEVICE="0")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                         "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
                         "29531", "bench.py", "--gpus", "2", "--steps", "2", "--warmup", "3"],
@@ -44,5 +46,8 @@ def test_bench_two_rank_code_path():
     assert r.returncode == 0, r.stderr[-3000:]
     d = _last_json(r.stdout)
     assert KEYS <= set(d)
-    assert d["n_gpus"] == 2 and d["config"]["tile_rows_total"] == 8192
-    assert d["e2e"]["h2d_bytes_per_step"] == 2 * (256 * 4096 * 4 * 2)
+    assert d["n_gpus"] == 2 and d["config"]["tile_rows_total"] == 16384
+    assert d["scaling"] == "strong" and d["config"]["rows_per_gpu"] == 8192
+    assert d["e2e"]["h2d_bytes_per_step"] == 2 * (256 * 16384 * 4 * 2 + 256 * 8192 * 4)
+    assert d["weak_scaling"]["rows_per_gpu"] == 4096 and d["weak_scaling"]["value"] > 0
+    assert d["inference_pass"]["drift_to_s"] > 0

@@ -9,7 +9,7 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-@pytest.mark.parametrize("driver", ["test_tile_b200", "test_nn_b200"])
+@pytest.mark.parametrize("driver", ["test_tile_b200", "test_nn_b200", "test_shard_b200"])
 def test_cpp_parity_driver(driver):
     exe = os.path.join(HERE, "cpp", driver)
     src = os.path.join(HERE, "cpp", driver + ".cpp")
