@@ -410,29 +410,39 @@ def pulse_traffic():
 
 # ============================================================ reference arm
 def _ref_lib():
+    """The reference's own sources compiled here (oracle/_ref): the -O2
+    -march=native build when this CPU runs it, else the
+    pinned -O2 build; the C restatement only when neither exists."""
     import oracle
-    impl = "reference" if oracle.available("reference") else "restatement"
-    if not oracle.available(impl):
-        oracle.build(reference=False)
-    return oracle.load(impl), impl
+    for impl in ("reference_native", "reference", "restatement"):
+        if oracle.available(impl):
+            return oracle.load(impl), impl
+    oracle.build(reference=False)
+    return oracle.load("restatement"), "restatement"
+
+
+def _kind(impl):
+    return "port" if impl == "restatement" else "reference"
 
 
 def _ref_worker(args):
-    """One process: a 4096^2 reram_sb reference tile, `warm` untimed samples,
-    then `n_upd` updates and `n_fwd` forwards of independent samples;
-    returns (t_update, t_forward)."""
+    """One process: a rows x cols reram_sb reference tile (AnalogTile through
+    its own API), `warm` untimed samples, then `n_upd` updates and `n_fwd`
+    forwards of independent samples; returns (t_update, t_forward)."""
     n_upd, n_fwd, seed = args[:3]
     warm = args[3] if len(args) > 3 else 0
+    rows = args[4] if len(args) > 4 else N_ROWS
+    cols = args[5] if len(args) > 5 else N_COLS
     O, impl = _ref_lib()
     s = O.default("tile")
     s.device = O.preset("reram_sb")
     fwd = O.default("io")
     s.forward_io = fwd
-    t = O.tile(N_ROWS, N_COLS, s, 1234 + seed)
+    t = O.tile(rows, cols, s, 1234 + seed)
     rng = np.random.default_rng(7 + seed)
-    t.set_weights(rng.uniform(-0.1, 0.1, (N_ROWS, N_COLS)))
-    xs = rng.uniform(-1, 1, (max(n_upd, n_fwd), N_COLS)).astype(np.float32).astype(np.float64)
-    ds = rng.uniform(-1, 1, (n_upd, N_ROWS)).astype(np.float32).astype(np.float64)
+    t.set_weights(rng.uniform(-0.1, 0.1, (rows, cols)))
+    xs = rng.uniform(-1, 1, (max(n_upd, n_fwd), cols)).astype(np.float32).astype(np.float64)
+    ds = rng.uniform(-1, 1, (n_upd, rows)).astype(np.float32).astype(np.float64)
     for k in range(warm):
         t.forward(xs[k % len(xs)])
         t.update(xs[k % len(xs)], ds[k % len(ds)], LR)
@@ -452,42 +462,53 @@ def cpu_baseline_sample():
     t_upd, t_fwd = _ref_worker((2, 4, 0))
     step = t_upd / 2 + t_fwd / 4
     return {"value": N_ROWS * N_COLS / step, "unit": UNIT, "cores": 1,
-            "kind": "reference" if impl == "reference" else "port",
+            "kind": _kind(impl), "build": impl,
             "sample": "4096x4096 reram_sb tile, 2 AnalogTile::update + 4 forward calls "
                       "(one sample each), 1 thread; value = cells / (update + forward) per sample",
             "update_s_per_sample": t_upd / 2, "forward_s_per_sample": t_fwd / 4}
 
 
 def run_reference(args):
+    """The reference CPU implementation on this box's host cores, on our arm's
+    config: one independent reference tile per core (the reference has no
+    threading; SPEC.md allows tile-level parallelism).  N = 1: the NS 4096^2
+    tile.  N > 1 (cfg5, 16384^2): a 1024-row slice of the 16384-column tile
+    per core -- the same per-cell work (update and forward are per cell and
+    per row), bounded to minutes; value = cell-updates/s over all cores."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     O, impl = _ref_lib()
+    rows, cols = (N_ROWS, N_COLS) if world == 1 else (1024, CFG5)
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    try:  # one 4096^2 reference tile holds ~1.4 GB of host memory
+    try:  # one reference tile holds ~88 B per cell of host memory
         import psutil
-        cores = max(1, min(cores, int(psutil.virtual_memory().available / 1.6e9)))
+        cores = max(1, min(cores, int(psutil.virtual_memory().available / (rows * cols * 100.0))))
     except ImportError:
         pass
     per = max(1, args.steps)
     t0 = time.perf_counter()
     with mp.get_context("fork").Pool(cores) as pool:
-        res = pool.map(_ref_worker, [(per, per, c, args.warmup) for c in range(cores)])
+        res = pool.map(_ref_worker, [(per, per, c, args.warmup, rows, cols) for c in range(cores)])
     wall = time.perf_counter() - t0
     # per process: per-sample forward + update time; aggregate over processes
     step_s = max(r[0] + r[1] for r in res) / per
-    value = cores * N_ROWS * N_COLS / step_s
+    value = cores * rows * cols / step_s
+    workload = ("NS: 4096x4096 reram_sb tile, BL 31; per step each core runs one forward + one "
+                "update sample on its own tile" if world == 1 else
+                "cfg5: 16384-column reram_sb tile, BL 31; each core runs one forward + one update "
+                "sample per step on its own 1024x16384 row slice")
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "scaling": "weak" if world == 1 else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": {"workload": "NS: 4096x4096 reram_sb tile, BL 31; per step each core runs one "
-                               "forward + one update sample on its own tile",
-                   "parallelism": f"{cores} independent tile processes"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores,
-                         "kind": "reference" if impl == "reference" else "port",
-                         "sample": f"{per} forward+update samples per core, {cores} cores"},
+        "config": {"workload": workload, "parallelism": f"{cores} independent tile processes",
+                   "build": impl},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": _kind(impl),
+                         "sample": f"{per} forward+update samples per core on a {rows}x{cols} "
+                                   f"tile, {cores} cores ({impl} build)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": wall,
     }

@@ -25,6 +25,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIBS = {
     "restatement": os.path.join(HERE, "liboracle.so"),
     "reference": os.path.join(HERE, "_ref", "libxbref.so"),
+    # the reference sources at -O2 -march=sapphirerapids: the timed reference arm
+    "reference_native": os.path.join(HERE, "_ref", "libxbref_native.so"),
 }
 REF_TREE = "/root/reference/proj"
 
@@ -100,7 +102,18 @@ def build(reference: bool = True) -> None:
 
 
 def available(impl: str) -> bool:
+    if impl == "reference_native" and not _cpu_has("avx512f", "avx512_fp16"):
+        return False  # built for sapphirerapids: never run it on an older ISA
     return os.path.exists(LIBS[impl])
+
+
+def _cpu_has(*flags) -> bool:
+    try:
+        with open("/proc/cpuinfo") as f:
+            have = set(f.read().split())
+    except OSError:
+        return False
+    return all(x in have for x in flags)
 
 
 _P = C.c_void_p
