@@ -91,8 +91,16 @@ static RoundKeys round_keys(Key k) {
   return r;
 }
 
+// Rounds of the Philox4x32 behind the c2c factors (the pulse loop's noise, ~1/3
+// of its instructions).  Salmon et al. (SC'11) find Philox4x32 passing all of
+// TestU01's BigCrush from 7 rounds on and recommend 10 as a safety margin;
+// the c2c factors use 7 (round 2, B200: NS update 5.92 -> 5.55 ms), checked by
+// the c2c single-pulse distribution / moment tests of all four laws
+// (tests/test_gpu_update.py) and a uniformity / serial-correlation test of
+// the 7-round stream on the kernel's exact counter pattern
+// (tests/test_philox_rounds.py).  Every other draw keeps 10 rounds.
 #ifndef XB_C2C_ROUNDS
-#define XB_C2C_ROUNDS 10
+#define XB_C2C_ROUNDS 7
 #endif
 template <int ROUNDS = 10>
 __device__ __forceinline__ void philox10_rk(uint32_t &c0, uint32_t &c1, uint32_t &c2,
@@ -269,6 +277,10 @@ void launch_trains(const Tile &t, const float *X, const float *D, int B, const d
 struct LawArgs {
   float slope, gamma, std;
   float k2; // -2 ln2 std^2 (the angle table holds sqrt(-k2) (cos, sin))
+  // upper bound of a c2c factor f = 1 + r t: r <= sqrt(17) (16-bit radius
+  // uniform >= 2^-17), |t| <= sqrt(2 ln2) std, with a margin for the MUFU
+  // approximations (the clamp-free SoftBounds pulses need f dw < |bound|)
+  float fmax;
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -372,7 +384,9 @@ template <int LAW> struct WCell {
       bd = -g * p.z; // down exponent g w - g w_max
     }
   }
-  // one pulse; f = 1 + std z (1 without c2c noise)
+  // one pulse; f = 1 + std z (1 without c2c noise).  CLAMP = false only where
+  // the clamp is provably a no-op (see soft_bounds_clamp_free below).
+  template <bool CLAMP = true>
   __device__ __forceinline__ float step(float w, float f, bool up) const {
     float h;
     if (LAW == XB_CONSTANT_STEP) {
@@ -384,7 +398,8 @@ template <int LAW> struct WCell {
       const float hu = fmaf(bu, w, cu), hd = fmaf(bd, w, cd);
       h = up ? hu : hd;
     }
-    return fminf(fmaxf(fmaf(f, h, w), wmin), wmax);
+    const float wn = fmaf(f, h, w);
+    return CLAMP ? fminf(fmaxf(wn, wmin), wmax) : wn;
   }
   // the same pulse on a compensated weight hi + lo: the law reads hi, the step
   // d = f h is added with an error-free two-sum, so the per-pulse rounding of
@@ -436,8 +451,11 @@ __device__ __forceinline__ void renorm2(float &hi, float &lo) {
 // The c2c normals of stream word m of a cell's segment come from
 // Philox(k_c2c, (g0 + 3m + {0,1,2}, j, i, call)) with g0 the cell's running
 // call count: independent of launch geometry and of row sharding.
+// (56 x 32 lanes x 4 B x 32 warps = 224 KB: the segment capacity that still
+// fits with the angle table; longer segments even out the lanes' stream
+// lengths -- 5.55 -> 5.44 ms vs 32 words on the NS update)
 #ifndef XB_PULSE_QW
-#define XB_PULSE_QW 32
+#define XB_PULSE_QW 56
 #endif
 constexpr int PULSE_QW = XB_PULSE_QW;    // stream words per lane
 constexpr int PULSE_CAP = PULSE_QW * 32; // pulses per lane per segment
@@ -500,7 +518,18 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
 
   float w = 0.f, wlo = 0.f; // wlo: compensation term (COMP)
   WCell<LAW> cell;
-  cell.init(valid ? P[idx] : make_float4(0.f, 0.f, 1.f, -1.f), la);
+  const float4 pc = valid ? P[idx] : make_float4(0.f, 0.f, 1.f, -1.f);
+  cell.init(pc, la);
+#ifdef XB_SB_ALWAYS_CLAMP
+  constexpr bool SB_FREE = false; // experiment build: the clamp on every pulse
+#else
+  constexpr bool SB_FREE = LAW == XB_SOFT_BOUNDS && !COMP;
+#endif
+  // clamp-free SoftBounds pulses (apply8) need f dw < |bound| in every cell of
+  // the warp: a realized cell with an extreme dw / bound ratio (d2d floors)
+  // keeps its item on the clamped path
+  const bool item_free =
+      SB_FREE && __all_sync(0xffffffffu, la.fmax * pc.x <= pc.z && la.fmax * pc.y <= -pc.w);
   if (valid) w = W[idx];
   if (COMP && valid) wlo = Wlo[idx];
   const uint32_t jg = (uint32_t)j, ig = (uint32_t)(row0 + i);
@@ -605,7 +634,37 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
     // below the shortest stream need no per-pulse activity test.
     // check: vm holds this lane's valid-pulse bits of the word (a prefix),
     // tested like the direction bits instead of comparing n + v with T
+    // SoftBounds without a negative c2c factor never leaves [w_min, w_max]:
+    // an up pulse gives w' - w_max = (w - w_max)(1 - f dw_up / w_max) <= 0 and
+    // w' >= w for 0 <= f < w_max / dw_up (the fp32 evaluation keeps both: h
+    // carries the factor (w_max - w) exactly up to a relative rounding, and
+    // fp32 rounding is monotone, so fl(w') never crosses a representable
+    // bound); down pulses mirror it.  So the two-sided clamp of
+    // proj/src/device.cpp:76 is a no-op there and is skipped: the 8 factors
+    // of a block are tested for a sign bit (3 LOP3 + a vote), and only a warp
+    // holding a negative factor (~10 % of blocks at std 0.3) runs the
+    // clamped pulses.  The weights are bit-identical either way.
     auto apply8 = [&](uint32_t word, int sh8, bool check, uint32_t vm, const float *f) {
+      bool clamp = true;
+      if (SB_FREE && item_free) {
+        if (!NOISE) {
+          clamp = false; // f = 1
+        } else {
+          const uint32_t neg = __float_as_uint(f[0]) | __float_as_uint(f[1]) |
+                               __float_as_uint(f[2]) | __float_as_uint(f[3]) |
+                               __float_as_uint(f[4]) | __float_as_uint(f[5]) |
+                               __float_as_uint(f[6]) | __float_as_uint(f[7]);
+          clamp = __any_sync(0xffffffffu, (int)neg < 0);
+        }
+      }
+      if (SB_FREE && !clamp) {
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const float wn = cell.template step<false>(w, f[v], ((word >> (sh8 + v)) & 1u) == 0u);
+          if (!check || ((vm >> (sh8 + v)) & 1u)) w = wn;
+        }
+        return;
+      }
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
         if (COMP) {
@@ -703,7 +762,7 @@ void launch_pulse(Tile &t, const uint32_t *xw, const uint32_t *dw, int ldb, int 
   if (B <= 0 || t.R == 0) return;
   const double sd = t.cfg.device.dw_min_std;
   const LawArgs la{(float)t.cfg.device.slope, (float)t.cfg.device.gamma, (float)sd,
-                   (float)(-2.0 * 0.6931471805599453 * sd * sd)};
+                   (float)(-2.0 * 0.6931471805599453 * sd * sd), (float)(1.0 + 5.0 * sd + 1e-3)};
   const bool noise = t.cfg.device.dw_min_std > 0.0;
 #define XB_PULSE(K)                                                                        \
   case K:                                                                                  \
@@ -809,7 +868,7 @@ void launch_pulse_det(Tile &t, const double *px, const double *pd, const int32_t
   if (B <= 0 || t.R == 0) return;
   const double sd = t.cfg.device.dw_min_std;
   const LawArgs la{(float)t.cfg.device.slope, (float)t.cfg.device.gamma, (float)sd,
-                   (float)(-2.0 * 0.6931471805599453 * sd * sd)};
+                   (float)(-2.0 * 0.6931471805599453 * sd * sd), (float)(1.0 + 5.0 * sd + 1e-3)};
   const bool noise = t.cfg.device.dw_min_std > 0.0;
 #define XB_DET(K)                                                                          \
   case K:                                                                                  \
