@@ -14,6 +14,7 @@
 // Weight noise: sum_j (w_ij + sigma_w xi_ij) x~_j = sum_j w_ij x~_j + sigma_w
 // ||x~|| zeta_i exactly in distribution (independent xi_ij), so the per-use
 // d_out x d_in Gaussian draws of the reference become one normal per output.
+#include <algorithm>
 #include <cstdlib>
 
 #include "xb_mvm_common.cuh"
@@ -165,6 +166,161 @@ __global__ void __launch_bounds__(256) mvm_simt_kernel(const float *__restrict__
   }
 }
 
+// --------------------------------------------------------------- GEMV
+// Small batches (B <= 15: every per-sample call of the reference API) stream
+// W once at HBM rate with every sample's accumulator in registers (the 64 x
+// 64 SIMT tile kernel would run 64 CTAs for a 4096-row tile).  fp32 FMA,
+// like the SIMT path; one instantiation per batch size (no runtime trip
+// counts inside the unrolled loops).
+//
+// forward: acc[b][o] = sum_k W[o][k] x~[b][k].  A warp owns R rows: per
+// 16-byte chunk position each lane loads the chunk of all R rows (U chunk
+// positions in flight), then every x~ chunk once for all R rows -- the x~
+// re-reads through L1 cost (R + B) / R times the W bytes -- and a warp
+// reduction at the end.  8 warps per CTA.
+constexpr int GV_MAXB = 15;
+template <int NB> constexpr int gv_rows() { return NB <= 8 ? 4 : 2; }
+
+template <int NB>
+__global__ void __launch_bounds__(256) gemv_fwd_kernel(const float *__restrict__ W, int ldw, int M,
+                                                        int K, const float *__restrict__ Xt,
+                                                        int ldt, float *__restrict__ acc, int lda,
+                                                        const int *__restrict__ n_rows) {
+  constexpr int R = gv_rows<NB>();
+  if (n_rows && *n_rows != NB) return; // compacted re-issue: one instantiation per count
+  const int lane = threadIdx.x & 31;
+  const int o0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * R;
+  if (o0 >= M) return;
+  float a[R][NB];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) a[r][b] = 0.f;
+  const float4 *w[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    w[r] = reinterpret_cast<const float4 *>(W + (size_t)min(o0 + r, M - 1) * ldw);
+  const int K4 = K >> 2; // 16-byte chunks (W rows: ld % 32 == 0; x~ rows: ldt % 4 == 0)
+  constexpr int U = NB <= 4 ? 4 : 2;
+  int c = lane;
+  auto step = [&](const float4 (&wv)[R], int cc) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const float4 xv = __ldg(reinterpret_cast<const float4 *>(Xt + (size_t)b * ldt) + cc);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        a[r][b] = fmaf(wv[r].x, xv.x, a[r][b]);
+        a[r][b] = fmaf(wv[r].y, xv.y, a[r][b]);
+        a[r][b] = fmaf(wv[r].z, xv.z, a[r][b]);
+        a[r][b] = fmaf(wv[r].w, xv.w, a[r][b]);
+      }
+    }
+  };
+  for (; c + 32 * (U - 1) < K4; c += 32 * U) {
+    float4 wv[U][R];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int r = 0; r < R; ++r) wv[u][r] = __ldcs(w[r] + c + 32 * u);
+#pragma unroll
+    for (int u = 0; u < U; ++u) step(wv[u], c + 32 * u);
+  }
+  for (; c < K4; c += 32) {
+    float4 wv[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) wv[r] = __ldcs(w[r] + c);
+    step(wv, c);
+  }
+  for (int k = 4 * K4 + lane; k < K; k += 32) // K % 4 tail
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const float xv = Xt[(size_t)b * ldt + k];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        a[r][b] = fmaf(reinterpret_cast<const float *>(w[r])[k], xv, a[r][b]);
+    }
+#pragma unroll
+  for (int b = 0; b < NB; ++b)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const float v = warp_sum(a[r][b]);
+      if (lane == 0 && o0 + r < M) acc[(size_t)b * lda + o0 + r] = v;
+    }
+}
+
+// backward: part[s][b][j] = sum over rows i of split s of W[i][j] d~[b][i].
+// A thread owns 4 consecutive columns (one 16-byte chunk of a W row: a warp
+// reads 512 contiguous bytes per row) and 16 rows in flight; the rows are
+// split over blockIdx.y; d~ values are warp-uniform broadcasts.
+constexpr int GVB_SPLITS = 64;
+template <int NB>
+__global__ void __launch_bounds__(128) gemv_bwd_kernel(const float *__restrict__ W, int ldw, int M,
+                                                        int K, const float *__restrict__ Dt,
+                                                        int ldt, float *__restrict__ part,
+                                                        int lda, size_t split_stride,
+                                                        int rows_per_split,
+                                                        const int *__restrict__ n_rows) {
+  if (n_rows && *n_rows != NB) return;
+  const int j0 = (blockIdx.x * 128 + threadIdx.x) * 4; // first of this thread's 4 columns
+  if (j0 >= M) return;
+  const int i0 = blockIdx.y * rows_per_split, i1 = min(K, i0 + rows_per_split);
+  float4 a[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) a[b] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const bool full = j0 + 3 < M;
+  auto ldw4 = [&](int i) {
+    const float *row = W + (size_t)i * ldw + j0;
+    return full ? __ldcs(reinterpret_cast<const float4 *>(row))
+                : make_float4(row[0], j0 + 1 < M ? row[1] : 0.f, j0 + 2 < M ? row[2] : 0.f, 0.f);
+  };
+  auto fma4 = [&](const float4 &wv, int i) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const float dv = __ldg(Dt + (size_t)b * ldt + i);
+      a[b].x = fmaf(wv.x, dv, a[b].x);
+      a[b].y = fmaf(wv.y, dv, a[b].y);
+      a[b].z = fmaf(wv.z, dv, a[b].z);
+      a[b].w = fmaf(wv.w, dv, a[b].w);
+    }
+  };
+  int i = i0;
+  constexpr int U = NB <= 4 ? 16 : 8;
+  for (; i + U <= i1; i += U) {
+    float4 wv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) wv[u] = ldw4(i + u);
+#pragma unroll
+    for (int u = 0; u < U; ++u) fma4(wv[u], i + u);
+  }
+  for (; i < i1; ++i) fma4(ldw4(i), i);
+  float *dst = part + (size_t)blockIdx.y * split_stride;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    float *o = dst + (size_t)b * lda + j0;
+    if (full && ((lda & 3) == 0)) {
+      *reinterpret_cast<float4 *>(o) = a[b];
+    } else {
+      o[0] = a[b].x;
+      if (j0 + 1 < M) o[1] = a[b].y;
+      if (j0 + 2 < M) o[2] = a[b].z;
+      if (j0 + 3 < M) o[3] = a[b].w;
+    }
+  }
+}
+
+// out[e] = sum_{s < S} part[s][e] in split order (e < n): the backward
+// GEMV's row splits, reduced with one thread per element
+__global__ void __launch_bounds__(256) split_reduce_kernel(const float *__restrict__ part, int S,
+                                                            size_t stride, size_t n,
+                                                            float *__restrict__ out) {
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n;
+       e += (size_t)gridDim.x * blockDim.x) {
+    float v = part[e];
+    for (int s = 1; s < S; ++s) v += part[(size_t)s * stride + e];
+    out[e] = v;
+  }
+}
+
 // --------------------------------------------------------------- epilogue
 // one thread = one group of 4 outputs of one sample (xb_mvm_common.cuh).
 // acc row r (r < n; n = *n_rows for a compacted re-issue) holds sample
@@ -304,6 +460,28 @@ void gemm(Tile &t, const float *xt, int ldt, int M, int K, int B, float *acc,
   XB_CUDA(cudaGetLastError());
 }
 
+// The small-batch contraction (B <= GV_MAXB) into acc [B][M] (lda = M).
+// The backward stages its row-split partials in `work` ([S][B][M], S =
+// GVB_SPLITS) and reduces them in order; a compacted re-issue (n_rows on
+// the device) runs the instantiation of every batch size up to B, each of
+// which leaves unless it matches the count.
+template <bool TRANS>
+void gemv(Tile &t, const float *xt, int ldt, int M, int K, int B, float *acc, float *work,
+          const int *n_rows) {
+  const int lo = n_rows ? 1 : B;
+  for (int nb = lo; nb <= B; ++nb) {
+#define XB_GV(NB)                                                                            case NB:                                                                                     if (TRANS) {                                                                                 const int rps = (K + GVB_SPLITS - 1) / GVB_SPLITS;                                         dim3 g((M + 511) / 512, (K + rps - 1) / rps);                                              gemv_bwd_kernel<NB><<<g, 128, 0, t.stream>>>(t.W, t.ld, M, K, xt, ldt, work, M,                                                         (size_t)NB * M, rps, n_rows);                  count_launch();                                                                            split_reduce_kernel<<<std::min<size_t>(((size_t)NB * M + 255) / 256, 2048), 256, 0,                              t.stream>>>(work, (int)g.y, (size_t)NB * M, (size_t)NB * M, acc);     } else {                                                                                     dim3 g((M + 8 * gv_rows<NB>() - 1) / (8 * gv_rows<NB>()));                                 gemv_fwd_kernel<NB><<<g, 256, 0, t.stream>>>(t.W, t.ld, M, K, xt, ldt, acc, M, n_rows);     }                                                                                          break;
+    switch (nb) {
+      XB_GV(1) XB_GV(2) XB_GV(3) XB_GV(4) XB_GV(5) XB_GV(6) XB_GV(7) XB_GV(8)
+      XB_GV(9) XB_GV(10) XB_GV(11) XB_GV(12) XB_GV(13) XB_GV(14) XB_GV(15)
+    }
+#undef XB_GV
+    count_launch();
+    XB_CUDA(cudaGetLastError());
+  }
+}
+
+
 // XB_MVM_UNFUSED=1 forces the split-K partials + epilogue kernel path: the
 // parity tests run both and require bit-identical outputs
 static bool unfused_requested() {
@@ -354,7 +532,11 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io_in, 
   const int splits = tc ? tc_used_splits(K, std::min(8, tc_splits(M, K, x3))) : 1;
   const bool fused = tc && !skip_epilogue && (o0 & 3) == 0 && !unfused_requested();
   const int ldt = (K + 3) & ~3; // x~ rows padded to 16 bytes (TMA global stride)
-  MvmScratch s = carve(t, B, ldt, M, fused ? 0 : splits);
+  // small batches on the exact fp32 path stream W once (GEMV); the backward
+  // GEMV splits the rows (partials summed in order by the epilogue kernel)
+  const bool gv = !tc && B <= GV_MAXB;
+  // (GEMV backward: acc_r holds the row-split partials; GVB_SPLITS sets of B x M)
+  MvmScratch s = carve(t, B, ldt, M, fused ? 0 : (tc ? splits : (gv && TRANS ? GVB_SPLITS : 1)));
   const bool bm = io.bm && !skip_epilogue;
   const bool sharded_bm = bm && t.comm && !TRANS;
   const int nslab = (B + SLAB - 1) / SLAB;
@@ -391,6 +573,8 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io_in, 
   } else if (tc) {
     tc_gemm(t, TRANS, x3, s.xt, ldt, B, s.acc, splits, nullptr);
     nsplit = splits;
+  } else if (gv) {
+    gemv<TRANS>(t, s.xt, ldt, M, K, B, s.acc, s.acc_r, nullptr);
   } else {
     gemm<TRANS>(t, s.xt, ldt, M, K, B, s.acc, nullptr);
   }
@@ -443,12 +627,18 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io_in, 
         tc_gemm(t, TRANS, x3, xt, ldt, nb, nullptr, splits, &f);
       } else {
         float *acc = tc ? s.acc_r : s.acc;
-        if (tc)
+        int ns = 1;
+        if (tc) {
           tc_gemm(t, TRANS, x3, xt, ldt, nb, acc, splits, nullptr, cnt);
-        else
+          ns = splits;
+        } else if (gv) {
+          gemv<TRANS>(t, xt, ldt, M, K, nb, s.acc, s.acc_r, cnt);
+          acc = s.acc;
+        } else {
           gemm<TRANS>(t, xt, ldt, M, K, nb, acc, cnt);
+        }
         dim3 eg((out_groups(o0, M) + 255) / 256, nb);
-        epilogue_kernel<<<eg, 256, 0, t.stream>>>(acc, M, tc ? splits : 1, (size_t)nb * M, M, o0,
+        epilogue_kernel<<<eg, 256, 0, t.stream>>>(acc, M, ns, (size_t)nb * M, M, o0,
                                                   dOut, M, s.st, io, key, seq0, bb, nb, n0, pass,
                                                   bb.map, cnt);
         count_launch();

@@ -418,3 +418,23 @@ def test_dac_exact_including_ties(prec):
         assert np.array_equal(Y.astype(np.float32), ref)
     else:
         assert np.array_equal(Y.astype(np.float32), ref)
+
+
+@pytest.mark.parametrize("B", [1, 3, 8, 15])
+@pytest.mark.parametrize("shape", [(4096, 4096), (77, 45), (300, 130), (1, 513), (513, 1)])
+def test_small_batch_gemv_matches_fp64(B, shape):
+    """Batches of <= 15 samples (every per-sample reference call) take the
+    streaming GEMV kernels (forward: warp per 2 rows; backward: row splits
+    summed in order): fp32-exact to 1e-5 of max(1, |y|) against fp64, every
+    precision mode (the tensor cores serve B >= 16 only), odd widths."""
+    d_out, d_in = shape
+    W = np.random.default_rng(41).uniform(-0.5, 0.5, shape).astype(np.float32)
+    X = np.random.default_rng(42).uniform(-1, 1, (B, d_in)).astype(np.float32)
+    D = np.random.default_rng(43).uniform(-1, 1, (B, d_out)).astype(np.float32)
+    for prec in PRECISIONS:
+        t = xb.AnalogTile(d_out, d_in, cfg_io(xb.perfect_io(), xb.perfect_io(), prec), 5)
+        t.set_weights(W)
+        Y = t.forward(X)
+        G = t.backward(D)
+        assert close(Y, X.astype(np.float64) @ W.T.astype(np.float64), 1e-5, 1.0).all()
+        assert close(G, D.astype(np.float64) @ W.astype(np.float64), 1e-5, 1.0).all()

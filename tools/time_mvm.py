@@ -40,5 +40,9 @@ for name, io in (("default", xb.default_io()), ("perfect", xb.perfect_io())):
             fn()
         e1.record(s)
         torch.cuda.synchronize()
-        res[f"{name}_{key}_us"] = round(e0.elapsed_time(e1) / a.iters * 1e3, 1)
+        us = e0.elapsed_time(e1) / a.iters * 1e3
+        res[f"{name}_{key}_us"] = round(us, 1)
+        # algorithmic HBM bytes of one call: W once + inputs + outputs
+        res[f"{name}_{key}_hbm_frac"] = round((4.0 * a.n * a.n + 8.0 * a.batch * a.n) /
+                                              (us * 1e-6) / 6.5259e12, 3)
 print(os.environ.get("XBTILE_LIB", "default").split("/")[-1], a.n, res)
