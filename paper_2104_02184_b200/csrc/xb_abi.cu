@@ -395,7 +395,7 @@ static const double *upload_lr(Tile &t, double *dst, const double *lr, int B, do
 // the whole pulsed update of B samples from device inputs
 static void update_device(Tile &t, const float *dX, const float *dD, int B, const double *lr,
                           const float *dAmaxD, bool peek, uint32_t *xw_out, uint32_t *dw_out,
-                          int32_t *bl_out) {
+                          int32_t *bl_out, int col = -1) {
   const bool det = t.cfg.update.pulse_type == XB_PULSE_DETERMINISTIC && !peek;
   UpdBufs u = upd_bufs(t, B, det);
   double lr_s = 0.0;
@@ -433,7 +433,7 @@ static void update_device(Tile &t, const float *dX, const float *dD, int B, cons
     if (det)
       launch_pulse_det(t, u.px, u.pd, u.bl, B, t.upd_calls);
     else
-      launch_pulse(t, u.xw, u.dw, train_ld(B), B, t.upd_calls);
+      launch_pulse(t, u.xw, u.dw, train_ld(B), B, t.upd_calls, false, col);
   }
   t.upd_calls += 1;
   t.seq_upd += (uint64_t)B;
@@ -1237,6 +1237,14 @@ int xb_transfer_create(const xb_transfer_config *cfg, int d_out, int d_in, uint6
     xb_tile_destroy(slow);
     return rc;
   }
+  // both members on the fast tile's stream: the transfer's read (A) and
+  // update (C) are ordered without events or host waits
+  rc = xb_tile_set_stream(slow, fast->t.stream);
+  if (rc) {
+    xb_tile_destroy(fast);
+    xb_tile_destroy(slow);
+    return rc;
+  }
   auto *t = new xb_transfer;
   t->cfg = *cfg;
   t->fast = fast;
@@ -1247,8 +1255,8 @@ int xb_transfer_create(const xb_transfer_config *cfg, int d_out, int d_in, uint6
 
 int xb_transfer_destroy(xb_transfer *t) {
   if (!t) return 0;
+  xb_tile_destroy(t->slow); // borrows the fast tile's stream: first
   xb_tile_destroy(t->fast);
-  xb_tile_destroy(t->slow);
   t->onehot.release();
   t->readout.release();
   t->tmp.release();
@@ -1293,6 +1301,12 @@ int xb_transfer_clone(const xb_transfer *t, xb_transfer **out) {
     xb_tile_destroy(fast);
     return rc;
   }
+  rc = xb_tile_set_stream(slow, fast->t.stream);
+  if (rc) {
+    xb_tile_destroy(slow);
+    xb_tile_destroy(fast);
+    return rc;
+  }
   auto *c = new xb_transfer;
   c->cfg = t->cfg;
   c->fast = fast;
@@ -1314,24 +1328,36 @@ int xb_transfer_backward(xb_transfer *t, const float *D, int B, float *G) {
   return 0;
 }
 
-// compound.cpp:257-267: one-hot read of A's column through the forward path,
-// then a pulsed update of C with x = e_j, d = readout.  The readout never
-// leaves the device; a zero readout is a no-op inside the update itself.
+// compound.cpp:257-267: a noisy read of A's column j (the forward of the
+// one-hot e_j through the transfer io), then the pulsed update of C with x =
+// e_j, d = readout.  All on the compound's one stream, nothing waits on the
+// host: the read is a column gather plus the shared output stage
+// (launch_column_read, bit-identical to the full forward), the update fires
+// only the 32-column block holding j (x trains are zero elsewhere), and a
+// zero readout is a no-op inside the update itself.  (Input noise or bound
+// management on the transfer io take the full forward instead.)
 static void transfer_step_impl(xb_transfer *tr) {
   Tile &a = tr->fast->t;
+  Tile &c = tr->slow->t;
+  const int j = tr->next_column;
   float *oh = scratch_as<float>(tr->onehot, a.C);
   float *ro = scratch_as<float>(tr->readout, a.R);
-  std::vector<float> e(a.C, 0.f);
-  e[tr->next_column] = 1.0f;
-  XB_CUDA(cudaMemcpyAsync(oh, e.data(), sizeof(float) * a.C, cudaMemcpyHostToDevice, a.stream));
-  const xb_io_params &io = tr->cfg.has_transfer_io ? tr->cfg.transfer_io : tr->cfg.forward_io;
-  forward_device(a, oh, 1, ro, io);
-  sync(a);
-  Tile &c = tr->slow->t;
+  const xb_io_params &iop = tr->cfg.has_transfer_io ? tr->cfg.transfer_io : tr->cfg.forward_io;
+  io_validate(iop, "transfer_io");
+  const IoDev io = make_io(iop);
+  if (io.sigma_inp > 0.0 || io.bm) {
+    std::vector<float> e(a.C, 0.f);
+    e[j] = 1.0f;
+    XB_CUDA(cudaMemcpyAsync(oh, e.data(), sizeof(float) * a.C, cudaMemcpyHostToDevice, a.stream));
+    XB_CUDA(cudaStreamSynchronize(a.stream)); // e is a host temporary
+    forward_device(a, oh, 1, ro, iop);
+  } else {
+    launch_column_read(a, j, io, a.k_fwd, a.seq_fwd, ro, oh);
+    a.seq_fwd += 1;
+  }
   const double lr = tr->cfg.transfer_lr;
-  update_device(c, oh, ro, 1, &lr, nullptr, false, nullptr, nullptr, nullptr);
-  sync(c);
-  tr->next_column = (tr->next_column + 1) % a.C;
+  update_device(c, oh, ro, 1, &lr, nullptr, false, nullptr, nullptr, nullptr, j);
+  tr->next_column = (j + 1) % a.C;
 }
 
 static void tick(xb_transfer *t) { // compound.cpp:247-255

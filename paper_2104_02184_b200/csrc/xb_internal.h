@@ -188,8 +188,15 @@ __host__ __device__ inline size_t xq_index(int j, int b, int C) {
 }
 // weight-stationary coincidence/pulse kernel over packed words
 // flip inverts every pulse (negative unit-cell gain, tile.cpp:164-167)
+// col >= 0: only the 32-column block holding column `col` (x trains zero elsewhere)
 void launch_pulse(Tile &t, const uint32_t *xw, const uint32_t *dw, int ldb, int B,
-                  uint32_t call_id, bool flip = false);
+                  uint32_t call_id, bool flip = false, int col = -1);
+// Tiki-Taka transfer read (compound.cpp:257-267): out = the forward of the
+// one-hot e_col through the output stage of `io` (B = 1, exact fp32 path),
+// without a contraction: acc_i = W[i][col] Q_dac(1); also writes e_col [C]
+// to onehot.  Only for io without input noise or bound management.
+void launch_column_read(Tile &t, int col, const IoDev &io, Key key, uint64_t seq, float *out,
+                        float *onehot);
 // out[line][k] = in[line][idx[k]] (k < n), zero-padded to ldb_out; quad != 0:
 // both sides in the x quad layout (xq_index with C = lines)
 void launch_gather_samples(const uint32_t *in, int ldb_in, int lines, const int *idx, int n,

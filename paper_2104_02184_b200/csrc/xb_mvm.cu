@@ -650,6 +650,48 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io_in, 
 
 } // namespace
 
+// ---- Tiki-Taka transfer read (compound.cpp:257-267) -----------------------
+// The forward of the one-hot e_col (B = 1, the exact fp32 path): prep gives
+// alpha = max|e_col| = 1, x~ = Q_dac(e_col) -- zero except Q_dac(1) at col,
+// exact zeros pass the quantizer -- and ||x~|| = |Q_dac(1)|; every fp32 sum of
+// the contraction then reduces to the one product W[i][col] Q_dac(1).  So the
+// read is a strided gather of one column and the shared output stage (same
+// noise counters, fp64 converters): bit-identical to the full forward, at R
+// loads instead of a pass over the whole tile.
+__global__ void __launch_bounds__(256) column_read_kernel(const float *__restrict__ W, int ld, int R,
+                                                           int C, int col, IoDev io, Key key,
+                                                           uint64_t seq, float *__restrict__ out,
+                                                           float *__restrict__ onehot) {
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int k = tid; k < C; k += gridDim.x * blockDim.x) onehot[k] = k == col ? 1.f : 0.f;
+  const int g = tid;
+  if (4 * g >= R) return;
+  const float xq = io.perfect ? 1.f : (float)quantize(1.0, io.dac);
+  SampleState s;
+  s.alpha = 1.f;
+  s.m = 0;
+  s.active = 1;
+  s.norm = sqrtf(fmaf(xq, xq, 0.f));
+  float a[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int row = 4 * g + k;
+    a[k] = row < R ? W[(size_t)row * ld + col] * xq : 0.f;
+  }
+  epilogue_group4(a, g, 0, R, s, io, key, seq, out);
+}
+
+void launch_column_read(Tile &t, int col, const IoDev &io_in, Key key, uint64_t seq, float *out,
+                        float *onehot) {
+  IoDev io = io_in;
+  io.exact = 1; // a single sample takes the exact fp32 path (fp64 converters)
+  const int n = std::max((t.R + 3) / 4, (t.C + 3) / 4);
+  column_read_kernel<<<(n + 255) / 256, 256, 0, t.stream>>>(t.W, t.ld, t.R, t.C, col, io, key,
+                                                            seq, out, onehot);
+  count_launch();
+  XB_CUDA(cudaGetLastError());
+}
+
 IoDev make_io(const xb_io_params &io) {
   IoDev d;
   d.dac = make_quant(io.input_bound, io.dac_bits);

@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
     int C,
     const uint32_t *__restrict__ xw, const uint32_t *__restrict__ dw, int ldb, int B, int row0,
     LawArgs la, RoundKeys rk, uint32_t call, uint32_t two, uint32_t flip,
-    const int *__restrict__ abort_flag) {
+    const int *__restrict__ abort_flag, uint32_t cb0, uint32_t ncb_run) {
   extern __shared__ uint32_t qsm[]; // [PULSE_WARPS][PULSE_QW][32] streams, then the angle table
   if (abort_flag && *abort_flag) return; // rejected input: the tile stays untouched
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -506,12 +506,13 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
   // words (L1 hits) and the L2 sees each x word once per CTA, not per row.
   // Warps drift out of phase, so the ALU/FMA-bound pre-pass of some overlaps
   // the pulse loop of others.
-  const uint32_t ncb = (uint32_t)(C + 31) / 32u;
-  const uint32_t n_items = (uint32_t)R * ncb; // < 2^31 for any tile that fits
+  // items of the column blocks [cb0, cb0 + ncb_run) only (a one-hot x, e.g.
+  // a Tiki-Taka transfer, has no coincidences anywhere else)
+  const uint32_t n_items = (uint32_t)R * ncb_run; // < 2^31 for any tile that fits
   for (uint32_t item = blockIdx.x * PULSE_WARPS + warp; item < n_items;
        item += gridDim.x * PULSE_WARPS) {
-  const uint32_t cb = item / (uint32_t)R;
-  const int i = (int)(item - cb * (uint32_t)R);
+  const uint32_t cb = cb0 + item / (uint32_t)R;
+  const int i = (int)(item - (cb - cb0) * (uint32_t)R);
   const int j = (int)cb * 32 + lane;
   const bool valid = j < C;
   const size_t idx = (size_t)i * ld + j;
@@ -732,7 +733,7 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
 
 template <int LAW, bool NOISE, bool COMP>
 static void pulse_dispatch(Tile &t, const uint32_t *xw, const uint32_t *dw, int ldb, int B,
-                           LawArgs la, uint32_t call, bool flip) {
+                           LawArgs la, uint32_t call, bool flip, int col) {
   const int smem = PULSE_WARPS * PULSE_QW * 32 * (int)sizeof(uint32_t) +
                    (NOISE ? BM_ANGLES * (int)sizeof(float2) : 0);
   // persistent grid: every resident CTA slot of the device, capped by the work
@@ -748,17 +749,19 @@ static void pulse_dispatch(Tile &t, const uint32_t *xw, const uint32_t *dw, int 
     blocks_of[current_device() & 63].store(std::max(1, per_sm) * sms);
   });
   const int blocks = blocks_of[current_device() & 63].load();
-  const long items = (long)t.R * ((t.C + 31) / 32);
+  const uint32_t cb0 = col >= 0 ? (uint32_t)(col / 32) : 0u;
+  const uint32_t ncb_run = col >= 0 ? 1u : (uint32_t)((t.C + 31) / 32);
+  const long items = (long)t.R * ncb_run;
   const dim3 grid((unsigned)std::min<long>(blocks, (items + PULSE_WARPS - 1) / PULSE_WARPS));
   pulse_kernel<LAW, NOISE, COMP><<<grid, PULSE_WARPS * 32, smem, t.stream>>>(
       t.W, t.Wlo, t.P, t.ld, t.R, t.C, xw, dw, ldb, B, t.row0, la, round_keys(t.k_c2c), call, 2u,
-      flip ? 0x80000000u : 0u, t.abort_flag);
+      flip ? 0x80000000u : 0u, t.abort_flag, cb0, ncb_run);
   count_launch();
   XB_CUDA(cudaGetLastError());
 }
 
 void launch_pulse(Tile &t, const uint32_t *xw, const uint32_t *dw, int ldb, int B,
-                  uint32_t call_id, bool flip) {
+                  uint32_t call_id, bool flip, int col) {
   if (B <= 0 || t.R == 0) return;
   const double sd = t.cfg.device.dw_min_std;
   const LawArgs la{(float)t.cfg.device.slope, (float)t.cfg.device.gamma, (float)sd,
@@ -767,11 +770,11 @@ void launch_pulse(Tile &t, const uint32_t *xw, const uint32_t *dw, int ldb, int 
 #define XB_PULSE(K)                                                                        \
   case K:                                                                                  \
     if (t.comp)                                                                            \
-      noise ? pulse_dispatch<K, true, true>(t, xw, dw, ldb, B, la, call_id, flip)          \
-            : pulse_dispatch<K, false, true>(t, xw, dw, ldb, B, la, call_id, flip);        \
+      noise ? pulse_dispatch<K, true, true>(t, xw, dw, ldb, B, la, call_id, flip, col)          \
+            : pulse_dispatch<K, false, true>(t, xw, dw, ldb, B, la, call_id, flip, col);        \
     else                                                                                   \
-      noise ? pulse_dispatch<K, true, false>(t, xw, dw, ldb, B, la, call_id, flip)         \
-            : pulse_dispatch<K, false, false>(t, xw, dw, ldb, B, la, call_id, flip);       \
+      noise ? pulse_dispatch<K, true, false>(t, xw, dw, ldb, B, la, call_id, flip, col)         \
+            : pulse_dispatch<K, false, false>(t, xw, dw, ldb, B, la, call_id, flip, col);       \
     break;
   switch (t.cfg.device.kind) {
     XB_PULSE(XB_CONSTANT_STEP)

@@ -266,3 +266,37 @@ def test_compensation_factor():
     z = wide_tile(2, 2, 36)
     with pytest.raises(xb.Error, match="degenerate readout"):
         z.drift_compensation_factor(1.0, m)
+
+
+@pytest.mark.parametrize("exact_io", [False, True])
+def test_transfer_step_equals_explicit_read_and_update(exact_io):
+    """The device-side transfer (column gather + the shared output stage,
+    then a pulsed update restricted to column j's block, no host round trip)
+    is bit for bit the reference's definition run through the public API on
+    a clone: A.forward_with_io(e_j, transfer io) then C.update(e_j, readout,
+    transfer_lr) (proj/src/compound.cpp:257-267), noise on."""
+    s = xb.TransferSettings()
+    s.fast_device = xb.device_preset("reram_sb")
+    s.slow_device = xb.device_preset("reram_sb")
+    s.transfer_lr = 0.3
+    if exact_io:  # perfect transfer io (no converters)
+        s.has_transfer_io = 1
+        s.transfer_io = xb.perfect_io()
+    d_out, d_in = 300, 70
+    t = xb.TransferTile(d_out, d_in, s, 12)
+    r = np.random.default_rng(3)
+    t.fast_tile().set_weights(r.uniform(-0.3, 0.3, (d_out, d_in)).astype(np.float32))
+    t.slow_tile().set_weights(r.uniform(-0.3, 0.3, (d_out, d_in)).astype(np.float32))
+    c = t.clone()
+    io = s.transfer_io if exact_io else s.forward_io
+    for j in range(3):
+        t.transfer_step()
+        e = np.zeros(d_in, np.float32)
+        e[j] = 1.0
+        ro = c.fast_tile().forward_with_io(e, io)
+        c.slow_tile().update(e, ro, s.transfer_lr)
+    np.testing.assert_array_equal(t.slow_tile().get_weights(), c.slow_tile().get_weights())
+    np.testing.assert_array_equal(t.fast_tile().get_weights(), c.fast_tile().get_weights())
+    # the next forward of A draws the same noise on both (read counters in step)
+    X = r.uniform(-1, 1, (4, d_in)).astype(np.float32)
+    np.testing.assert_array_equal(t.fast_tile().forward(X), c.fast_tile().forward(X))
