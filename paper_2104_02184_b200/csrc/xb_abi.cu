@@ -784,20 +784,21 @@ int xb_tile_set_device(xb_tile *h, const float *dw_up, const float *dw_down, con
     Tile &t = h->t;
     DevScope ds_(t.device);
     const size_t n = (size_t)t.R * t.ld;
-    std::vector<float4> p(n);
-    XB_CUDA(cudaMemcpy(p.data(), t.P, n * sizeof(float4), cudaMemcpyDeviceToHost));
+    std::vector<float2> p(2 * n); // planes: steps [n], bounds [n] (Tile::P)
+    XB_CUDA(cudaStreamSynchronize(t.stream));
+    XB_CUDA(cudaMemcpy(p.data(), t.P, 2 * n * sizeof(float2), cudaMemcpyDeviceToHost));
     for (int i = 0; i < t.R; ++i) {
       for (int j = 0; j < t.C; ++j) {
-        const size_t s = (size_t)i * t.C + j;
-        float4 &q = p[(size_t)i * t.ld + j];
-        if (dw_up) q.x = dw_up[s];
-        if (dw_down) q.y = dw_down[s];
-        if (w_max) q.z = w_max[s];
-        if (w_min) q.w = w_min[s];
-        if (!(q.w < 0.f && 0.f < q.z)) raise("set_device: requires w_min < 0 < w_max per cell");
+        const size_t s = (size_t)i * t.C + j, k = (size_t)i * t.ld + j;
+        float2 &st = p[k], &bd = p[n + k];
+        if (dw_up) st.x = dw_up[s];
+        if (dw_down) st.y = dw_down[s];
+        if (w_max) bd.x = w_max[s];
+        if (w_min) bd.y = w_min[s];
+        if (!(bd.y < 0.f && 0.f < bd.x)) raise("set_device: requires w_min < 0 < w_max per cell");
       }
     }
-    XB_CUDA(cudaMemcpy(t.P, p.data(), n * sizeof(float4), cudaMemcpyHostToDevice));
+    XB_CUDA(cudaMemcpy(t.P, p.data(), 2 * n * sizeof(float2), cudaMemcpyHostToDevice));
     launch_clip(t);
     wlo_reset(t);
     sync(t);
@@ -810,17 +811,16 @@ int xb_tile_get_device(const xb_tile *h, float *dw_up, float *dw_down, float *w_
     const Tile &t = h->t;
     DevScope ds_(t.device);
     const size_t n = (size_t)t.R * t.ld;
-    std::vector<float4> p(n);
+    std::vector<float2> p(2 * n); // planes: steps [n], bounds [n] (Tile::P)
     XB_CUDA(cudaStreamSynchronize(t.stream));
-    XB_CUDA(cudaMemcpy(p.data(), t.P, n * sizeof(float4), cudaMemcpyDeviceToHost));
+    XB_CUDA(cudaMemcpy(p.data(), t.P, 2 * n * sizeof(float2), cudaMemcpyDeviceToHost));
     for (int i = 0; i < t.R; ++i) {
       for (int j = 0; j < t.C; ++j) {
-        const size_t s = (size_t)i * t.C + j;
-        const float4 q = p[(size_t)i * t.ld + j];
-        if (dw_up) dw_up[s] = q.x;
-        if (dw_down) dw_down[s] = q.y;
-        if (w_max) w_max[s] = q.z;
-        if (w_min) w_min[s] = q.w;
+        const size_t s = (size_t)i * t.C + j, k = (size_t)i * t.ld + j;
+        if (dw_up) dw_up[s] = p[k].x;
+        if (dw_down) dw_down[s] = p[k].y;
+        if (w_max) w_max[s] = p[n + k].x;
+        if (w_min) w_min[s] = p[n + k].y;
       }
     }
   });

@@ -33,7 +33,8 @@ struct DevArgs {
 };
 
 // proj/src/device.cpp:26-46: four Gaussians per cell (xi_dw, xi_ud, xi_max, xi_min)
-__global__ void __launch_bounds__(EW_THREADS) realize_kernel(float4 *__restrict__ P, int ld,
+__global__ void __launch_bounds__(EW_THREADS) realize_kernel(float2 *__restrict__ S,
+                                                              float2 *__restrict__ Bd, int ld,
                                                               int R, int C, int row0,
                                                               DevArgs a, Key key) {
   int i, j;
@@ -43,22 +44,20 @@ __global__ void __launch_bounds__(EW_THREADS) realize_kernel(float4 *__restrict_
   const double fl = 0.01 * a.dw_min;
   const double dw = fmax(a.dw_min * (1.0 + a.dw_min_dtod * z0), fl);
   const double bias = a.up_down + a.up_down_dtod * z1;
-  float4 p;
-  p.x = (float)fmax(dw * (1.0 + bias), fl);
-  p.y = (float)fmax(dw * (1.0 - bias), fl);
-  p.z = (float)fmax(a.w_max * (1.0 + a.w_max_dtod * z2), 0.01 * a.w_max);
-  p.w = (float)fmin(a.w_min * (1.0 + a.w_min_dtod * z3), 0.01 * a.w_min);
-  P[(size_t)i * ld + j] = p;
+  const size_t k = (size_t)i * ld + j;
+  S[k] = make_float2((float)fmax(dw * (1.0 + bias), fl), (float)fmax(dw * (1.0 - bias), fl));
+  Bd[k] = make_float2((float)fmax(a.w_max * (1.0 + a.w_max_dtod * z2), 0.01 * a.w_max),
+                      (float)fmin(a.w_min * (1.0 + a.w_min_dtod * z3), 0.01 * a.w_min));
 }
 
 __global__ void __launch_bounds__(EW_THREADS) clip_kernel(float *__restrict__ W,
-                                                           const float4 *__restrict__ P, int ld,
+                                                           const float2 *__restrict__ Bd, int ld,
                                                            int R, int C) {
   int i, j;
   if (!ew_index(R, C, i, j)) return;
   const size_t k = (size_t)i * ld + j;
-  const float4 p = P[k];
-  W[k] = fminf(fmaxf(W[k], p.w), p.z);
+  const float2 p = Bd[k];
+  W[k] = fminf(fmaxf(W[k], p.y), p.x);
 }
 
 __global__ void __launch_bounds__(EW_THREADS) temporal_xi_kernel(float *__restrict__ xi, int ld,
@@ -80,7 +79,7 @@ struct TempArgs {
 
 // proj/src/tile.cpp:128-156
 __global__ void __launch_bounds__(EW_THREADS) temporal_kernel(float *__restrict__ W,
-                                                               const float4 *__restrict__ P,
+                                                               const float2 *__restrict__ Bd,
                                                                const float *__restrict__ xi,
                                                                int ld, int R, int C, int row0,
                                                                TempArgs a, Key key,
@@ -106,8 +105,8 @@ __global__ void __launch_bounds__(EW_THREADS) temporal_kernel(float *__restrict_
     const bool hit = (p >= 1.0) || (p > 0.0 && (double)c2 * 2.3283064365386963e-10 < p);
     if (hit) w = 0.0;
   }
-  const float4 pp = P[k];
-  W[k] = fminf(fmaxf((float)w, pp.w), pp.z);
+  const float2 pp = Bd[k];
+  W[k] = fminf(fmaxf((float)w, pp.y), pp.x);
 }
 
 struct ProgArgs {
@@ -118,7 +117,7 @@ struct ProgArgs {
 // nu = clip(nu_mean (1 + nu_std xi'), nu_min, nu_max)
 __global__ void __launch_bounds__(EW_THREADS) program_kernel(
     float *__restrict__ W, float *__restrict__ w0, float *__restrict__ nu,
-    const float4 *__restrict__ P, const float *__restrict__ target, int ld, int R, int C,
+    const float2 *__restrict__ Bd, const float *__restrict__ target, int ld, int R, int C,
     int row0, ProgArgs a, Key key) {
   int i, j;
   if (!ew_index(R, C, i, j)) return;
@@ -128,8 +127,8 @@ __global__ void __launch_bounds__(EW_THREADS) program_kernel(
   const double t = target[(size_t)i * C + j];
   const double at = fabs(t);
   const double sig = a.scale * (a.c0 + a.c1 * at + a.c2 * at * at);
-  const float4 p = P[k];
-  const float w = fminf(fmaxf((float)(t + sig * (double)z0), p.w), p.z);
+  const float2 p = Bd[k];
+  const float w = fminf(fmaxf((float)(t + sig * (double)z0), p.y), p.x);
   W[k] = w;
   w0[k] = w;
   const double v = a.nu_mean * (1.0 + a.nu_std * (double)z1);
@@ -140,14 +139,14 @@ __global__ void __launch_bounds__(EW_THREADS) program_kernel(
 __global__ void __launch_bounds__(EW_THREADS) drift_kernel(float *__restrict__ W,
                                                             const float *__restrict__ w0,
                                                             const float *__restrict__ nu,
-                                                            const float4 *__restrict__ P, int ld,
+                                                            const float2 *__restrict__ Bd, int ld,
                                                             int R, int C, double log2_ratio) {
   int i, j;
   if (!ew_index(R, C, i, j)) return;
   const size_t k = (size_t)i * ld + j;
   const double f = exp2(-(double)nu[k] * log2_ratio);
-  const float4 p = P[k];
-  W[k] = fminf(fmaxf((float)((double)w0[k] * f), p.w), p.z);
+  const float2 p = Bd[k];
+  W[k] = fminf(fmaxf((float)((double)w0[k] * f), p.y), p.x);
 }
 
 // ORs `bit` into *flag if any of v[0..n) is Inf or NaN (exponent all ones):
@@ -219,7 +218,7 @@ void launch_realize(Tile &t) {
   const xb_device_params &d = t.cfg.device;
   DevArgs a{d.dw_min, d.dw_min_dtod, d.up_down, d.up_down_dtod, d.w_max, d.w_min, d.w_max_dtod,
             d.w_min_dtod};
-  realize_kernel<<<ew_grid(t.R, t.C), EW_THREADS, 0, t.stream>>>(t.P, t.ld, t.R, t.C, t.row0, a,
+  realize_kernel<<<ew_grid(t.R, t.C), EW_THREADS, 0, t.stream>>>(t.steps(), t.bounds(), t.ld, t.R, t.C, t.row0, a,
                                                                   t.k_realize);
   count_launch();
   XB_CUDA(cudaGetLastError());
@@ -227,7 +226,7 @@ void launch_realize(Tile &t) {
 
 void launch_clip(Tile &t) {
   if (t.R == 0) return;
-  clip_kernel<<<ew_grid(t.R, t.C), EW_THREADS, 0, t.stream>>>(t.W, t.P, t.ld, t.R, t.C);
+  clip_kernel<<<ew_grid(t.R, t.C), EW_THREADS, 0, t.stream>>>(t.W, t.bounds(), t.ld, t.R, t.C);
   count_launch();
   XB_CUDA(cudaGetLastError());
 }
@@ -245,7 +244,7 @@ void launch_temporal(Tile &t, const xb_temporal_params &tp, uint32_t call) {
   TempArgs a{tp.decay_rate, tp.decay_dtod, tp.diffusion_sigma, tp.diffusion_dtod, tp.reset_prob,
              tp.reset_dtod};
   temporal_kernel<<<ew_grid(t.R, t.C), EW_THREADS, 0, t.stream>>>(
-      t.W, t.P, t.xi, t.ld, t.R, t.C, t.row0, a, t.k_temporal, call);
+      t.W, t.bounds(), t.xi, t.ld, t.R, t.C, t.row0, a, t.k_temporal, call);
   count_launch();
   XB_CUDA(cudaGetLastError());
 }
@@ -255,14 +254,14 @@ void launch_program(Tile &t, const float *target_dev, const xb_inference_model &
   ProgArgs a{m.prog_noise_scale, m.prog_c0, m.prog_c1, m.prog_c2,
              m.nu_mean,          m.nu_std,  m.nu_min,  m.nu_max};
   program_kernel<<<ew_grid(t.R, t.C), EW_THREADS, 0, t.stream>>>(
-      t.W, t.w0, t.nu, t.P, target_dev, t.ld, t.R, t.C, t.row0, a, key);
+      t.W, t.w0, t.nu, t.bounds(), target_dev, t.ld, t.R, t.C, t.row0, a, key);
   count_launch();
   XB_CUDA(cudaGetLastError());
 }
 
 void launch_drift(Tile &t, double ratio) {
   if (t.R == 0) return;
-  drift_kernel<<<ew_grid(t.R, t.C), EW_THREADS, 0, t.stream>>>(t.W, t.w0, t.nu, t.P, t.ld, t.R,
+  drift_kernel<<<ew_grid(t.R, t.C), EW_THREADS, 0, t.stream>>>(t.W, t.w0, t.nu, t.bounds(), t.ld, t.R,
                                                                 t.C, log2(ratio));
   count_launch();
   XB_CUDA(cudaGetLastError());

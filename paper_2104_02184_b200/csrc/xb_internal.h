@@ -135,7 +135,13 @@ struct Tile {
   float *W = nullptr;      // [R][ld] fp32 weights
   float *Wlo = nullptr;    // [R][ld] compensation terms (comp mode: weight = W + Wlo)
   bool comp = false;       // compensated weights (xb_tile_config.weight_precision)
-  float4 *P = nullptr;     // [R][ld] {dw_up, dw_down, w_max, w_min}
+  // per-cell realization, two planes of [R][ld] float2 in one allocation:
+  // steps {dw_up, dw_down} (the pulse kernels), then bounds {w_max, w_min}
+  // (every pass that clips: set_weights, temporal, program, drift read 8
+  // bytes per cell, not 16)
+  float4 *P = nullptr;
+  float2 *steps() const { return reinterpret_cast<float2 *>(P); }
+  float2 *bounds() const { return reinterpret_cast<float2 *>(P) + (size_t)R * ld; }
   float *xi = nullptr;     // [3][R][ld] temporal d2d draws (lazy)
   float *w0 = nullptr;     // programmed state (lazy)
   float *nu = nullptr;

@@ -481,7 +481,8 @@ constexpr int PULSE_WARPS = XB_PULSE_WARPS;
 
 template <int LAW, bool NOISE, bool COMP>
 __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
-    float *__restrict__ W, float *__restrict__ Wlo, const float4 *__restrict__ P, int ld, int R,
+    float *__restrict__ W, float *__restrict__ Wlo, const float2 *__restrict__ S,
+    const float2 *__restrict__ Bd, int ld, int R,
     int C,
     const uint32_t *__restrict__ xw, const uint32_t *__restrict__ dw, int ldb, int B, int row0,
     LawArgs la, RoundKeys rk, uint32_t call, uint32_t two, uint32_t flip,
@@ -519,7 +520,11 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
 
   float w = 0.f, wlo = 0.f; // wlo: compensation term (COMP)
   WCell<LAW> cell;
-  const float4 pc = valid ? P[idx] : make_float4(0.f, 0.f, 1.f, -1.f);
+  float4 pc = make_float4(0.f, 0.f, 1.f, -1.f);
+  if (valid) {
+    const float2 st = S[idx], bd = Bd[idx];
+    pc = make_float4(st.x, st.y, bd.x, bd.y);
+  }
   cell.init(pc, la);
 #ifdef XB_SB_ALWAYS_CLAMP
   constexpr bool SB_FREE = false; // experiment build: the clamp on every pulse
@@ -754,7 +759,8 @@ static void pulse_dispatch(Tile &t, const uint32_t *xw, const uint32_t *dw, int 
   const long items = (long)t.R * ncb_run;
   const dim3 grid((unsigned)std::min<long>(blocks, (items + PULSE_WARPS - 1) / PULSE_WARPS));
   pulse_kernel<LAW, NOISE, COMP><<<grid, PULSE_WARPS * 32, smem, t.stream>>>(
-      t.W, t.Wlo, t.P, t.ld, t.R, t.C, xw, dw, ldb, B, t.row0, la, round_keys(t.k_c2c), call, 2u,
+      t.W, t.Wlo, t.steps(), t.bounds(), t.ld, t.R, t.C, xw, dw, ldb, B, t.row0, la,
+      round_keys(t.k_c2c), call, 2u,
       flip ? 0x80000000u : 0u, t.abort_flag, cb0, ncb_run);
   count_launch();
   XB_CUDA(cudaGetLastError());
@@ -818,7 +824,8 @@ void launch_gather_samples(const uint32_t *in, int ldb_in, int lines, const int 
 // signs (p = 0 <=> sign 0 or a no-op sample).
 template <int LAW, bool NOISE, bool COMP>
 __global__ void __launch_bounds__(256) pulse_det_kernel(
-    float *__restrict__ W, float *__restrict__ Wlo, const float4 *__restrict__ P, int ld, int R,
+    float *__restrict__ W, float *__restrict__ Wlo, const float2 *__restrict__ S,
+    const float2 *__restrict__ Bd, int ld, int R,
     int C, const double *__restrict__ px, const double *__restrict__ pd,
     const int32_t *__restrict__ bl, int B, int row0, LawArgs la, Key key, uint32_t call,
     const int *__restrict__ abort_flag) {
@@ -829,7 +836,7 @@ __global__ void __launch_bounds__(256) pulse_det_kernel(
   const size_t idx = (size_t)i * ld + j;
   float w = W[idx], wlo = COMP ? Wlo[idx] : 0.f;
   WCell<LAW> cell;
-  cell.init(P[idx], la);
+  cell.init(make_float4(S[idx].x, S[idx].y, Bd[idx].x, Bd[idx].y), la);
   uint32_t n = 0;
   float z[4] = {0.f, 0.f, 0.f, 0.f};
   for (int b = 0; b < B; ++b) {
@@ -861,7 +868,8 @@ static void det_dispatch(Tile &t, const double *px, const double *pd, const int3
                          LawArgs la, uint32_t call) {
   dim3 grid((t.C + 31) / 32, (t.R + 7) / 8);
   pulse_det_kernel<LAW, NOISE, COMP><<<grid, 256, 0, t.stream>>>(
-      t.W, t.Wlo, t.P, t.ld, t.R, t.C, px, pd, bl, B, t.row0, la, t.k_c2c, call, t.abort_flag);
+      t.W, t.Wlo, t.steps(), t.bounds(), t.ld, t.R, t.C, px, pd, bl, B, t.row0, la, t.k_c2c, call,
+      t.abort_flag);
   count_launch();
   XB_CUDA(cudaGetLastError());
 }
