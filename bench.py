@@ -317,9 +317,42 @@ def run_ours(args):
         out.update(extra)
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline_sample()
+        if world == 1 and not args.no_configs:
+            # every BASELINE config, each with roofline, cpu_baseline and e2e
+            # (tools/bench_configs.py; `--config cfgN` prints one as the line)
+            bc = _bench_configs()
+            cargs = argparse.Namespace(no_ref=args.no_cpu_baseline)
+            out["configs"] = {}
+            for name, fn in bc.CONFIGS.items():
+                try:
+                    out["configs"][name] = bc.summary(fn(cargs, stream))
+                except Exception as e:  # a failed config is reported, not hidden
+                    out["configs"][name] = {"error": f"{type(e).__name__}: {e}"}
+                torch.cuda.synchronize()
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
+
+
+def _bench_configs():
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import bench_configs
+    return bench_configs
+
+
+def run_config(args):
+    """`--config cfgN`: that BASELINE config as the contract line (1 GPU)."""
+    import torch
+    bc = _bench_configs()
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    clk = Clocks(0).__enter__()
+    d = bc.CONFIGS[args.config](argparse.Namespace(no_ref=args.no_cpu_baseline), stream)
+    clk.__exit__(None, None, None)
+    d.update({"n_gpus": 1, "steps": None, "warmup": None, "scaling": "weak", "vs_baseline": None,
+              "dtype": "f32", "data": "synthetic", "clocks": clk.summary()})
+    d.setdefault("gpu_launches", d.get("gpu_launches_per_2_batches"))
+    print(json.dumps(d))
 
 
 def loopback_comm(xb, dist, world, rank):
@@ -522,9 +555,15 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the per-config summary of the default NS line")
+    ap.add_argument("--config", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
+                    help="print this BASELINE config's line instead of the NS line")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config:
+        run_config(args)
     else:
         run_ours(args)
 

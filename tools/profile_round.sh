@@ -1,21 +1,22 @@
 #!/bin/sh
 # One GPU call that refreshes the round's evidence (run under gpurun):
-#   the bench line, the bench's launch list, ncu --set full captures of the
-#   pulse kernel (NS update) and the fused tcgen05 forward (BM on, the bench's
-#   step), and the per-config lines.  Every ncu pass runs only after the same
-#   command exited 0 without ncu.  Output: gpurun_out/prof/
+#   the bench line (with the five configs), the bench's launch list, ncu
+#   --set full captures of the pulse kernel (NS update) and of the fused
+#   tcgen05 forward (default IO, one pass) and one with bound management.
+#   Every ncu pass runs only after the same command exited 0 without ncu.
+#   Output: gpurun_out/prof/
 set -e
 cd "$(dirname "$0")/.."
 OUT=gpurun_out/prof
 mkdir -p $OUT
 python bench.py > $OUT/bench.json 2> $OUT/bench.err
-python bench.py --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
+python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-configs > /dev/null 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file $OUT/launches_bench_steps2.csv python bench.py --steps 2 --warmup 1 \
-    --no-cpu-baseline > $OUT/ncu_launches.log 2>&1
+    --no-cpu-baseline --no-configs > $OUT/ncu_launches.log 2>&1
 python tools/profile_pulse.py --precision 1 --iters 2 > /dev/null
 ncu --set full --import-source on --clock-control none -k regex:pulse_kernel -s 1 -c 1 -f \
     -o $OUT/pulse python tools/profile_pulse.py --precision 1 --iters 2 > $OUT/ncu_pulse.log 2>&1
+python tools/time_mvm.py --iters 3 > /dev/null
 ncu --set full --import-source on --clock-control none -k regex:tc_gemm -s 2 -c 1 -f \
-    -o $OUT/tc_fwd python tools/profile_pulse.py --precision 1 --iters 3 > $OUT/ncu_tc.log 2>&1
-if [ -f tools/bench_configs.py ]; then python tools/bench_configs.py > $OUT/configs.jsonl 2>&1 || true; fi
+    -o $OUT/tc_fwd python tools/time_mvm.py --iters 3 > $OUT/ncu_tc.log 2>&1
