@@ -432,6 +432,12 @@ def cfg5(args, stream):
                             "backward": hbm_roofline(mvm_bytes, b_ms, "4 N^2 + 8 B N bytes")},
            # drift_to: w0, nu read (8 B) + bounds (8 B) + W written (4 B) per cell
            "roofline_drift": hbm_roofline(20.0 * n * n, d_ms, "20 B per cell")}
+    Xh, Dh = X.cpu().numpy(), D.cpu().numpy()
+    yh = torch.empty(B, n, dtype=torch.float32).pin_memory().numpy()
+    e_ms = wall_time(lambda: (t.forward(Xh, out=yh), t.update(Xh, Dh, 0.01)), 2)
+    out["e2e"] = {"value": n * n * B / (e_ms * 1e-3), "unit": UNIT_CU,
+                  "h2d_bytes_per_step": 4 * B * 3 * n, "d2h_bytes_per_step": 4 * B * n,
+                  "api": "AnalogTile.forward(X host) + update(X, D host)"}
     if not args.no_ref:
         # a 256-row slice of the 16384-column tile: the same per-cell work
         O, impl = ref_oracle()
