@@ -248,6 +248,181 @@ __global__ void __launch_bounds__(256) gemv_fwd_kernel(const float *__restrict__
     }
 }
 
+// Fused small-batch forward (B <= 4, no bound management, no input noise):
+// the whole noisy MVM in ONE launch.  A CTA of 8 warps owns 32 rows: it
+// computes each sample's abs-max alpha (block reduction; the inputs are
+// L2-resident), converts K-chunks of the inputs with the DAC into shared
+// memory (prep_row's arithmetic; each thread keeps the partial norms of the
+// two 512-thread prep threads it stands for and the warp sums are added in
+// prep_row's order, so x~ and ||x~|| are bit-identical to the prep kernel's),
+// and every warp streams its 4 rows of W against them (16 rows' chunks in
+// flight per lane) with every sample's accumulator in registers;
+// after a warp reduction lane b runs the output stage (noise, ADC, alpha) of
+// sample b.  prep + contraction + epilogue become one W stream.
+constexpr int GF_THREADS = 256, GF_ROWS = 4, GF_KC = 4096;
+constexpr int GF_MAXB = 2; // larger batches: the staged GEMV path measured faster
+
+template <int NB>
+__global__ void __launch_bounds__(GF_THREADS) gemv_fused_fwd_kernel(
+    const float *__restrict__ W, int ldw, int M, int K, const float *__restrict__ X, int ldx,
+    float *__restrict__ Y, int ldy, IoDev io, Key key, uint64_t seq0, int o0) {
+  extern __shared__ float4 xs4[]; // [NB][GF_KC / 4] converted inputs of the chunk
+  float *xs = reinterpret_cast<float *>(xs4);
+  __shared__ float red[NB][17];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r0 = (blockIdx.x * (GF_THREADS / 32) + warp) * GF_ROWS; // this warp's first row
+  {
+    // the CTA's rows of W start streaming into L2 now (one bulk prefetch per
+    // row), under the abs-max and the DAC below
+    const int row = blockIdx.x * (GF_THREADS / 32) * GF_ROWS + threadIdx.x;
+    if (threadIdx.x < (GF_THREADS / 32) * GF_ROWS && row < M) {
+      const uint32_t bytes = (uint32_t)((K + 3) & ~3) * 4u;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(W + (size_t)row * ldw),
+                   "r"(bytes)
+                   : "memory");
+    }
+  }
+  // ---- alpha per sample (prep_kernel: block max)
+  SampleState st[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    float m = 0.f;
+    for (int k = threadIdx.x; k < K; k += GF_THREADS) m = fmaxf(m, fabsf(X[(size_t)b * ldx + k]));
+    m = warp_max(m);
+    if (lane == 0) red[b][warp] = m;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    float m = 0.f;
+    for (int w2 = 0; w2 < GF_THREADS / 32; ++w2) m = fmaxf(m, red[b][w2]);
+    st[b].alpha = (m == 0.f) ? 0.f : (io.nm_absmax ? m : 1.f);
+    st[b].m = 0;
+    st[b].active = 1;
+  }
+  __syncthreads();
+  // nrm[b][h]: the partial of prep_row's thread threadIdx.x + 256 h
+  float nrm[NB][2], a[GF_ROWS][NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    nrm[b][0] = nrm[b][1] = 0.f;
+#pragma unroll
+    for (int r = 0; r < GF_ROWS; ++r) a[r][b] = 0.f;
+  }
+  const bool rows_ok = r0 < M;
+  const float *w[GF_ROWS];
+#pragma unroll
+  for (int r = 0; r < GF_ROWS; ++r) w[r] = W + (size_t)min(r0 + r, M - 1) * ldw;
+  for (int kc = 0; kc < K; kc += GF_KC) {
+    const int n = min(GF_KC, K - kc);
+    // ---- DAC of the chunk (prep_row's convert, same thread per element)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const double inv = st[b].alpha == 0.f ? 0.0 : 1.0 / (double)st[b].alpha;
+      const bool fast = !io.perfect && st[b].alpha != 0.f;
+      const float a32 = fast ? (float)(inv * exp2((double)io.dac.bits) / (2.0 * io.dac.bound)) : 0.f;
+      const float c032 = 0.5f * io.dac.flevels_m1;
+      const float tie_eps = fast ? ldexpf(1.f, io.dac.bits - 20) : 0.f;
+      for (int k = threadIdx.x; k < n; k += GF_THREADS) {
+        const float xv = X[(size_t)b * ldx + kc + k];
+        float f;
+        if (io.perfect) {
+          f = xv;
+        } else if (st[b].alpha == 0.f || xv == 0.f) {
+          f = 0.f;
+        } else {
+          const float t = fmaf(xv, a32, c032);
+          const float fr = t - floorf(t);
+          if (fabsf(fr - 0.5f) > tie_eps) {
+            float kk = floorf(t + 0.5f);
+            kk = fminf(fmaxf(kk, 0.f), io.dac.flevels_m1);
+            f = fmaf(kk + 0.5f, io.dac.fstep, -io.dac.fbound);
+          } else {
+            f = (float)quantize((double)xv * inv, io.dac);
+          }
+        }
+        xs[b * GF_KC + k] = f;
+        const int h = ((kc + k) >> 8) & 1; // (kc + k) % 512 >= 256
+        nrm[b][h] = fmaf(f, f, nrm[b][h]);
+      }
+    }
+    __syncthreads();
+    // ---- stream this warp's rows over the chunk
+    if (rows_ok) {
+      const int n4 = ((n & 3) == 0 && (kc & 3) == 0) ? n >> 2 : 0;
+      constexpr int U = NB <= 2 ? 4 : 2;
+      for (int c = lane; c < n4; c += 32 * U) {
+        float4 wv[U][GF_ROWS];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int r = 0; r < GF_ROWS; ++r)
+            wv[u][r] = c + 32 * u < n4 ? __ldcs(reinterpret_cast<const float4 *>(w[r] + kc) + c + 32 * u)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (c + 32 * u >= n4) break;
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            const float4 xv = xs4[b * (GF_KC / 4) + c + 32 * u];
+#pragma unroll
+            for (int r = 0; r < GF_ROWS; ++r) {
+              a[r][b] = fmaf(wv[u][r].x, xv.x, a[r][b]);
+              a[r][b] = fmaf(wv[u][r].y, xv.y, a[r][b]);
+              a[r][b] = fmaf(wv[u][r].z, xv.z, a[r][b]);
+              a[r][b] = fmaf(wv[u][r].w, xv.w, a[r][b]);
+            }
+          }
+        }
+      }
+      for (int k = 4 * n4 + lane; k < n; k += 32)
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          const float xv = xs[b * GF_KC + k];
+#pragma unroll
+          for (int r = 0; r < GF_ROWS; ++r) a[r][b] = fmaf(w[r][kc + k], xv, a[r][b]);
+        }
+    }
+    __syncthreads(); // the chunk is read before the next one overwrites it
+  }
+  // ---- ||x~|| per sample, in prep_row's order: 16 virtual warps of 32
+  // (warp w, half h) -> virtual warp 8 h + w
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const float v0 = warp_sum(nrm[b][0]), v1 = warp_sum(nrm[b][1]);
+    if (lane == 0) {
+      red[b][warp] = v0;
+      red[b][8 + warp] = v1;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    float tot = 0.f;
+    for (int w2 = 0; w2 < 16; ++w2) tot += red[b][w2];
+    st[b].norm = sqrtf(tot);
+  }
+  if (!rows_ok) return;
+  // ---- every lane gets every sum (butterfly), then lane b finishes sample b
+  float mine[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int b = 0; b < NB; ++b)
+#pragma unroll
+    for (int r = 0; r < GF_ROWS; ++r) {
+      const float v = warp_sum(a[r][b]);
+      if (lane == b) mine[r] = v;
+    }
+  if (lane >= NB) return;
+  SampleState s = st[0];  // (rows r0 .. r0 + 3: one whole noise group)
+#pragma unroll
+  for (int b = 1; b < NB; ++b)
+    if (lane == b) s = st[b];
+  // the warp holds rows r0, r0 + 1 of the 4-row noise group g (o0 % 4 == 0);
+  // epilogue_group4 writes only the rows inside [r0, r0 + 2) of this warp
+  const int g = (o0 + r0) >> 2;
+  epilogue_group4(mine, g, o0, M, s, io, key, seq0 + (uint64_t)lane, Y + (size_t)lane * ldy);
+}
+
 // backward: part[s][b][j] = sum over rows i of split s of W[i][j] d~[b][i].
 // A thread owns 4 consecutive columns (one 16-byte chunk of a W row: a warp
 // reads 512 contiguous bytes per row) and 16 rows in flight; the rows are
@@ -460,6 +635,32 @@ void gemm(Tile &t, const float *xt, int ldt, int M, int K, int B, float *acc,
   XB_CUDA(cudaGetLastError());
 }
 
+// the fused small-batch forward (one launch: DAC, contraction, output stage)
+static void gemv_fused_fwd(Tile &t, const float *X, int K, int M, int B, float *Y, IoDev io,
+                           Key key, uint64_t seq0, int o0) {
+  io.exact = 1; // the exact fp32 path's output stage (fp64 converters)
+  constexpr int rows_per_cta = (GF_THREADS / 32) * GF_ROWS;
+  dim3 g((M + rows_per_cta - 1) / rows_per_cta);
+#define XB_GF(NB)                                                                          \
+  case NB: {                                                                               \
+    const int smem = NB * GF_KC * (int)sizeof(float);                                      \
+    static std::atomic<uint64_t> cfg_##NB{0};                                              \
+    once_per_device(cfg_##NB, [&] {                                                        \
+      XB_CUDA(cudaFuncSetAttribute(gemv_fused_fwd_kernel<NB>,                              \
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));    \
+    });                                                                                    \
+    gemv_fused_fwd_kernel<NB><<<g, GF_THREADS, smem, t.stream>>>(t.W, t.ld, M, K, X, K, Y, M, \
+                                                                 io, key, seq0, o0);       \
+    break;                                                                                 \
+  }
+  switch (B) {
+    XB_GF(1) XB_GF(2)
+  }
+#undef XB_GF
+  count_launch();
+  XB_CUDA(cudaGetLastError());
+}
+
 // The small-batch contraction (B <= GV_MAXB) into acc [B][M] (lda = M).
 // The backward stages its row-split partials in `work` ([S][B][M], S =
 // GVB_SPLITS) and reduces them in order; a compacted re-issue (n_rows on
@@ -542,6 +743,14 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io_in, 
   const int nslab = (B + SLAB - 1) / SLAB;
   int *bars = s.bm + (size_t)nslab * BM_SLAB_WORDS;
 
+  // small batches without bound management or input noise: the whole MVM in
+  // one launch (DAC on the fly, output stage fused; gemv_fused_fwd_kernel)
+  const bool dac_fast = io.perfect || (io.dac.bits > 0 && io.dac.bits <= 16 && io.dac.pow2);
+  if (gv && B <= GF_MAXB && !TRANS && !bm && !skip_epilogue && io.sigma_inp == 0.0 && dac_fast &&
+      (o0 & 3) == 0 && !amax_in && !unfused_requested()) {
+    gemv_fused_fwd(t, dIn, K, M, B, dOut, io, key, seq0, o0);
+    return;
+  }
   const bool want_loop = fused && bm && !sharded_bm && !host_passes_requested();
   prep_kernel<<<B, PREP_THREADS, 0, t.stream>>>(dIn, K, s.xt, ldt, s.st, io, key, seq0, amax_in,
                                                  in0, bm ? s.bm : nullptr, s.bm_words);

@@ -61,15 +61,14 @@ __device__ __forceinline__ void store_group4(const float y[4], int g, int o0, in
 // Outputs 4g..4g+3 (global index) of one sample: a[k] = their contraction
 // sums; the ones inside [o0, o0 + M) are written to yrow[o - o0].  Returns
 // whether any of them reached the ADC bound (bound management).
-__device__ __forceinline__ bool epilogue_group4(const float a[4], int g, int o0, int M,
-                                                const SampleState &s, const IoDev &io, Key key,
-                                                uint64_t seq, float *__restrict__ yrow) {
-  float y[4];
+// the output values y[k] of outputs 4g + k (the store is the caller's)
+__device__ __forceinline__ bool epilogue_values4(const float a[4], int g, int o0, int M,
+                                                 const SampleState &s, const IoDev &io, Key key,
+                                                 uint64_t seq, float y[4]) {
   bool hit = false;
   if (io.perfect) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) y[k] = a[k];
-    store_group4(y, g, o0, M, yrow);
     return false;
   }
   uint32_t w[4] = {0u, 0u, 0u, 0u};
@@ -97,7 +96,6 @@ __device__ __forceinline__ bool epilogue_group4(const float a[4], int g, int o0,
       }
       y[k] = scale * quantize_f(v, io.adc);
     }
-    store_group4(y, g, o0, M, yrow);
     return hit;
   }
   const double scale = s.alpha == 0.f ? 1.0 : (double)s.alpha * pow2i(s.m);
@@ -117,6 +115,14 @@ __device__ __forceinline__ bool epilogue_group4(const float a[4], int g, int o0,
     }
     y[k] = (float)(scale * quantize(v, io.adc));
   }
+  return hit;
+}
+
+__device__ __forceinline__ bool epilogue_group4(const float a[4], int g, int o0, int M,
+                                                const SampleState &s, const IoDev &io, Key key,
+                                                uint64_t seq, float *__restrict__ yrow) {
+  float y[4];
+  const bool hit = epilogue_values4(a, g, o0, M, s, io, key, seq, y);
   store_group4(y, g, o0, M, yrow);
   return hit;
 }

@@ -438,3 +438,45 @@ def test_small_batch_gemv_matches_fp64(B, shape):
         G = t.backward(D)
         assert close(Y, X.astype(np.float64) @ W.T.astype(np.float64), 1e-5, 1.0).all()
         assert close(G, D.astype(np.float64) @ W.astype(np.float64), 1e-5, 1.0).all()
+
+
+@pytest.mark.parametrize("B", [1, 5, 15])
+@pytest.mark.parametrize("shape", [(4096, 4096), (260, 77)])
+def test_fused_small_batch_forward_equals_staged_path(monkeypatch, B, shape):
+    """Small batches run prep + contraction + output stage as ONE kernel (the
+    DAC on the fly, gemv_fused_fwd_kernel); with the default converters and
+    output noise it equals the staged path (prep kernel, GEMV, epilogue
+    kernel; forced by XB_MVM_UNFUSED) bit for bit -- same DAC grid, same
+    contraction order, same noise words -- including an all-zero sample."""
+    d_out, d_in = shape
+    io = xb.default_io()  # DAC 7 b, ADC 9 b, sigma_out 0.06, abs-max
+    W = np.random.default_rng(51).uniform(-0.4, 0.4, shape).astype(np.float32)
+    X = np.random.default_rng(52).uniform(-1, 1, (B, d_in)).astype(np.float32)
+    X[0, : d_in // 3] = np.linspace(-1, 1, d_in // 3) * 0.5  # exact DAC thresholds
+    if B > 1:
+        X[1] = 0.0
+    out = []
+    for unfused in ("0", "1"):
+        monkeypatch.setenv("XB_MVM_UNFUSED", unfused)
+        t = xb.AnalogTile(d_out, d_in, cfg_io(io, io, xb.MVM_FP32), 77)
+        t.set_weights(W)
+        out.append((t.forward(X), t.forward(X)))
+    for a, b in zip(out[0], out[1]):
+        np.testing.assert_array_equal(a, b)
+    assert not np.array_equal(out[0][0], out[0][1])  # fresh noise per call
+
+
+def test_fused_small_batch_forward_weight_noise_equals_staged(monkeypatch):
+    """With weight noise (sigma_w ||x~|| zeta) the fused kernel's ||x~|| is the
+    prep kernel's to the bit (same per-thread partials, same reduction order)."""
+    io = xb.default_io()
+    io.sigma_w = 0.05
+    W = np.random.default_rng(61).uniform(-0.4, 0.4, (512, 5000)).astype(np.float32)
+    X = np.random.default_rng(62).uniform(-1, 1, (3, 5000)).astype(np.float32)
+    out = []
+    for unfused in ("0", "1"):
+        monkeypatch.setenv("XB_MVM_UNFUSED", unfused)
+        t = xb.AnalogTile(512, 5000, cfg_io(io, io, xb.MVM_FP32), 78)
+        t.set_weights(W)
+        out.append(t.forward(X))
+    np.testing.assert_array_equal(out[0], out[1])
