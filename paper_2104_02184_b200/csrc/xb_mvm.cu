@@ -485,13 +485,23 @@ __global__ void __launch_bounds__(128) gemv_bwd_kernel(const float *__restrict__
 
 // out[e] = sum_{s < S} part[s][e] in split order (e < n): the backward
 // GEMV's row splits, reduced with one thread per element
-__global__ void __launch_bounds__(256) split_reduce_kernel(const float *__restrict__ part, int S,
-                                                            size_t stride, size_t n,
-                                                            float *__restrict__ out) {
+// (16 loads in flight per thread, summed in split order; small CTAs spread
+// the few thousand elements of a per-sample call over many SMs)
+__global__ void __launch_bounds__(64) split_reduce_kernel(const float *__restrict__ part, int S,
+                                                           size_t stride, size_t n,
+                                                           float *__restrict__ out) {
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n;
        e += (size_t)gridDim.x * blockDim.x) {
-    float v = part[e];
-    for (int s = 1; s < S; ++s) v += part[(size_t)s * stride + e];
+    float v = 0.f;
+    int s = 0;
+    for (; s + 16 <= S; s += 16) {
+      float t[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) t[u] = __ldcg(part + (size_t)(s + u) * stride + e);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v = (s + u == 0) ? t[u] : v + t[u];
+    }
+    for (; s < S; ++s) v = (s == 0) ? part[e] : v + part[(size_t)s * stride + e];
     out[e] = v;
   }
 }
@@ -671,7 +681,7 @@ void gemv(Tile &t, const float *xt, int ldt, int M, int K, int B, float *acc, fl
           const int *n_rows) {
   const int lo = n_rows ? 1 : B;
   for (int nb = lo; nb <= B; ++nb) {
-#define XB_GV(NB)                                                                            case NB:                                                                                     if (TRANS) {                                                                                 const int rps = (K + GVB_SPLITS - 1) / GVB_SPLITS;                                         dim3 g((M + 511) / 512, (K + rps - 1) / rps);                                              gemv_bwd_kernel<NB><<<g, 128, 0, t.stream>>>(t.W, t.ld, M, K, xt, ldt, work, M,                                                         (size_t)NB * M, rps, n_rows);                  count_launch();                                                                            split_reduce_kernel<<<std::min<size_t>(((size_t)NB * M + 255) / 256, 2048), 256, 0,                              t.stream>>>(work, (int)g.y, (size_t)NB * M, (size_t)NB * M, acc);     } else {                                                                                     dim3 g((M + 8 * gv_rows<NB>() - 1) / (8 * gv_rows<NB>()));                                 gemv_fwd_kernel<NB><<<g, 256, 0, t.stream>>>(t.W, t.ld, M, K, xt, ldt, acc, M, n_rows);     }                                                                                          break;
+#define XB_GV(NB)                                                                            case NB:                                                                                     if (TRANS) {                                                                                 const int rps = (K + GVB_SPLITS - 1) / GVB_SPLITS;                                         dim3 g((M + 511) / 512, (K + rps - 1) / rps);                                              gemv_bwd_kernel<NB><<<g, 128, 0, t.stream>>>(t.W, t.ld, M, K, xt, ldt, work, M,                                                         (size_t)NB * M, rps, n_rows);                  count_launch();                                                                            split_reduce_kernel<<<std::min<size_t>(((size_t)NB * M + 63) / 64, 8192), 64, 0,                              t.stream>>>(work, (int)g.y, (size_t)NB * M, (size_t)NB * M, acc);     } else {                                                                                     dim3 g((M + 8 * gv_rows<NB>() - 1) / (8 * gv_rows<NB>()));                                 gemv_fwd_kernel<NB><<<g, 256, 0, t.stream>>>(t.W, t.ld, M, K, xt, ldt, acc, M, n_rows);     }                                                                                          break;
     switch (nb) {
       XB_GV(1) XB_GV(2) XB_GV(3) XB_GV(4) XB_GV(5) XB_GV(6) XB_GV(7) XB_GV(8)
       XB_GV(9) XB_GV(10) XB_GV(11) XB_GV(12) XB_GV(13) XB_GV(14) XB_GV(15)
