@@ -317,6 +317,8 @@ def run_ours(args):
         out.update(extra)
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline_sample()
+        if world == 1:
+            out["per_sample"] = per_sample(xb, torch, stream)
         if world == 1 and not args.no_configs:
             # every BASELINE config, each with roofline, cpu_baseline and e2e
             # (tools/bench_configs.py; `--config cfgN` prints one as the line)
@@ -332,6 +334,47 @@ def run_ours(args):
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
+
+
+def per_sample(xb, torch, stream):
+    """The reference API's per-sample path (TileBase::forward / update, one
+    sample per call) at 4096^2: the device time of one B = 1 forward (the
+    fused GEMV launch) against the HBM roofline, and the C++ mirror end to end
+    (tools/per_sample_bench: host vectors per call)."""
+    t, _, _ = make_tile(xb, 0, 1)
+    t.set_stream(stream.cuda_stream)
+    t.set_weights(np.random.default_rng(7).uniform(-0.1, 0.1, (N_ROWS, N_COLS))
+                  .astype(np.float32))
+    io = xb.default_io()  # the reference's default IO (no bound management)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    X = torch.rand(64, N_COLS, device="cuda", generator=g) * 2 - 1
+    Y = torch.empty(1, N_ROWS, device="cuda")
+    for k in range(4):
+        t.forward_dev(X[k:k + 1], Y, io)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(64):
+        t.forward_dev(X[k:k + 1], Y, io)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) / 64 * 1e3
+    pk, kind = peaks()
+    byts = 4.0 * N_ROWS * N_COLS + 4.0 * (N_ROWS + N_COLS)
+    out = {"forward_b1_device_us": us,
+           "roofline": {"bound": "hbm", "achieved": byts / (us * 1e-6) / 1e9,
+                        "peak": pk["hbm_gbs"], "unit": "GB/s",
+                        "frac": byts / (us * 1e-6) / 1e9 / pk["hbm_gbs"],
+                        "kernel": "gemv_fused_fwd_kernel<1> (abs-max, DAC, W stream, output "
+                                  "stage in one launch)"}}
+    exe = os.path.join(ROOT, "tools", "per_sample_bench")
+    if os.path.exists(exe):
+        try:
+            r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+            out["cpp_api"] = json.loads(r.stdout.strip().splitlines()[-1])
+        except Exception as e:  # reported, not hidden
+            out["cpp_api"] = {"error": f"{type(e).__name__}: {e}"}
+    return out
 
 
 def _bench_configs():

@@ -7,3 +7,7 @@ for t in test_tile_b200 test_nn_b200 test_shard_b200; do
       -L"$ROOT/paper_2104_02184_b200" -lxbtile \
       -Wl,-rpath,'$ORIGIN/../../paper_2104_02184_b200' -o "$ROOT/tests/cpp/$t"
 done
+# the per-sample C++ bench (bench.py reports it as "per_sample")
+g++ -std=c++20 -O2 -Wall -Wextra -I"$ROOT/include" "$ROOT/tools/per_sample_bench.cpp" \
+    -L"$ROOT/paper_2104_02184_b200" -lxbtile \
+    -Wl,-rpath,'$ORIGIN/../paper_2104_02184_b200' -o "$ROOT/tools/per_sample_bench"
