@@ -113,40 +113,101 @@ struct ProgArgs {
   double scale, c0, c1, c2, nu_mean, nu_std, nu_min, nu_max;
 };
 
+// The inference kernels stream 20-28 B per cell and are HBM-bound: each thread
+// owns a quad of 4 consecutive cells of one row (16-B loads/stores; rows are
+// 128-B aligned, ld a multiple of 32), a warp 128 columns.  Cells at j >= C
+// (the row padding) are never touched.
+inline unsigned ew4_blocks(int R, int ld) {
+  const size_t quads = (size_t)R * (ld / 4);
+  return (unsigned)((quads + EW_THREADS - 1) / EW_THREADS);
+}
+
+__device__ __forceinline__ bool ew4_index(int R, int C, int ld, int &i, int &j) {
+  const size_t q = (size_t)blockIdx.x * EW_THREADS + threadIdx.x;
+  const int qpr = ld >> 2;
+  i = (int)(q / qpr);
+  j = (int)(q - (size_t)i * qpr) * 4;
+  return i < R && j < C;
+}
+
 // proj/src/inference.cpp:34-61: w = target + sigma(|target|) xi, clip -> w0;
 // nu = clip(nu_mean (1 + nu_std xi'), nu_min, nu_max)
+__device__ __forceinline__ void program_cell(float t32, float2 p, int j, int gi, const ProgArgs &a,
+                                             Key key, float &w, float &nu) {
+  float z0, z1, z2, z3;
+  normal4((uint32_t)j, (uint32_t)gi, 0u, TAG_PROGRAM << 24, key, z0, z1, z2, z3);
+  const double t = t32;
+  const double at = fabs(t);
+  const double sig = a.scale * (a.c0 + a.c1 * at + a.c2 * at * at);
+  w = fminf(fmaxf((float)(t + sig * (double)z0), p.y), p.x);
+  const double v = a.nu_mean * (1.0 + a.nu_std * (double)z1);
+  nu = (float)fmin(fmax(v, a.nu_min), a.nu_max);
+}
+
 __global__ void __launch_bounds__(EW_THREADS) program_kernel(
     float *__restrict__ W, float *__restrict__ w0, float *__restrict__ nu,
     const float2 *__restrict__ Bd, const float *__restrict__ target, int ld, int R, int C,
     int row0, ProgArgs a, Key key) {
   int i, j;
-  if (!ew_index(R, C, i, j)) return;
+  if (!ew4_index(R, C, ld, i, j)) return;
   const size_t k = (size_t)i * ld + j;
-  float z0, z1, z2, z3;
-  normal4((uint32_t)j, (uint32_t)(row0 + i), 0u, TAG_PROGRAM << 24, key, z0, z1, z2, z3);
-  const double t = target[(size_t)i * C + j];
-  const double at = fabs(t);
-  const double sig = a.scale * (a.c0 + a.c1 * at + a.c2 * at * at);
-  const float2 p = Bd[k];
-  const float w = fminf(fmaxf((float)(t + sig * (double)z0), p.y), p.x);
-  W[k] = w;
-  w0[k] = w;
-  const double v = a.nu_mean * (1.0 + a.nu_std * (double)z1);
-  nu[k] = (float)fmin(fmax(v, a.nu_min), a.nu_max);
+  const float *tr = target + (size_t)i * C + j;
+  if (j + 4 <= C) {
+    float tv[4];
+    if ((C & 3) == 0) {
+      const float4 t4 = __ldcs(reinterpret_cast<const float4 *>(tr));
+      tv[0] = t4.x, tv[1] = t4.y, tv[2] = t4.z, tv[3] = t4.w;
+    } else {
+      for (int e = 0; e < 4; ++e) tv[e] = __ldcs(tr + e);
+    }
+    const float4 b01 = __ldcs(reinterpret_cast<const float4 *>(Bd + k));
+    const float4 b23 = __ldcs(reinterpret_cast<const float4 *>(Bd + k + 2));
+    const float2 pb[4] = {{b01.x, b01.y}, {b01.z, b01.w}, {b23.x, b23.y}, {b23.z, b23.w}};
+    float w[4], n[4];
+    for (int e = 0; e < 4; ++e) program_cell(tv[e], pb[e], j + e, row0 + i, a, key, w[e], n[e]);
+    const float4 w4 = make_float4(w[0], w[1], w[2], w[3]);
+    __stcs(reinterpret_cast<float4 *>(W + k), w4);
+    __stcs(reinterpret_cast<float4 *>(w0 + k), w4);
+    __stcs(reinterpret_cast<float4 *>(nu + k), make_float4(n[0], n[1], n[2], n[3]));
+  } else {
+    for (int e = 0; j + e < C; ++e) {
+      float w, n;
+      program_cell(tr[e], Bd[k + e], j + e, row0 + i, a, key, w, n);
+      W[k + e] = w;
+      w0[k + e] = w;
+      nu[k + e] = n;
+    }
+  }
 }
 
 // proj/src/inference.cpp:63-76 with log2(t/t0) precomputed in fp64 on the host
+__device__ __forceinline__ float drift_cell(float w0, float nu, float2 p, double log2_ratio) {
+  const double f = exp2(-(double)nu * log2_ratio);
+  return fminf(fmaxf((float)((double)w0 * f), p.y), p.x);
+}
+
 __global__ void __launch_bounds__(EW_THREADS) drift_kernel(float *__restrict__ W,
                                                             const float *__restrict__ w0,
                                                             const float *__restrict__ nu,
                                                             const float2 *__restrict__ Bd, int ld,
                                                             int R, int C, double log2_ratio) {
   int i, j;
-  if (!ew_index(R, C, i, j)) return;
+  if (!ew4_index(R, C, ld, i, j)) return;
   const size_t k = (size_t)i * ld + j;
-  const double f = exp2(-(double)nu[k] * log2_ratio);
-  const float2 p = Bd[k];
-  W[k] = fminf(fmaxf((float)((double)w0[k] * f), p.y), p.x);
+  if (j + 4 <= C) {
+    const float4 a = __ldcs(reinterpret_cast<const float4 *>(w0 + k));
+    const float4 n = __ldcs(reinterpret_cast<const float4 *>(nu + k));
+    const float4 b01 = __ldcs(reinterpret_cast<const float4 *>(Bd + k));
+    const float4 b23 = __ldcs(reinterpret_cast<const float4 *>(Bd + k + 2));
+    float4 o;
+    o.x = drift_cell(a.x, n.x, make_float2(b01.x, b01.y), log2_ratio);
+    o.y = drift_cell(a.y, n.y, make_float2(b01.z, b01.w), log2_ratio);
+    o.z = drift_cell(a.z, n.z, make_float2(b23.x, b23.y), log2_ratio);
+    o.w = drift_cell(a.w, n.w, make_float2(b23.z, b23.w), log2_ratio);
+    __stcs(reinterpret_cast<float4 *>(W + k), o);
+  } else {
+    for (int e = 0; j + e < C; ++e) W[k + e] = drift_cell(w0[k + e], nu[k + e], Bd[k + e], log2_ratio);
+  }
 }
 
 // ORs `bit` into *flag if any of v[0..n) is Inf or NaN (exponent all ones):
@@ -253,7 +314,7 @@ void launch_program(Tile &t, const float *target_dev, const xb_inference_model &
   if (t.R == 0) return;
   ProgArgs a{m.prog_noise_scale, m.prog_c0, m.prog_c1, m.prog_c2,
              m.nu_mean,          m.nu_std,  m.nu_min,  m.nu_max};
-  program_kernel<<<ew_grid(t.R, t.C), EW_THREADS, 0, t.stream>>>(
+  program_kernel<<<ew4_blocks(t.R, t.ld), EW_THREADS, 0, t.stream>>>(
       t.W, t.w0, t.nu, t.bounds(), target_dev, t.ld, t.R, t.C, t.row0, a, key);
   count_launch();
   XB_CUDA(cudaGetLastError());
@@ -261,7 +322,7 @@ void launch_program(Tile &t, const float *target_dev, const xb_inference_model &
 
 void launch_drift(Tile &t, double ratio) {
   if (t.R == 0) return;
-  drift_kernel<<<ew_grid(t.R, t.C), EW_THREADS, 0, t.stream>>>(t.W, t.w0, t.nu, t.bounds(), t.ld, t.R,
+  drift_kernel<<<ew4_blocks(t.R, t.ld), EW_THREADS, 0, t.stream>>>(t.W, t.w0, t.nu, t.bounds(), t.ld, t.R,
                                                                 t.C, log2(ratio));
   count_launch();
   XB_CUDA(cudaGetLastError());
