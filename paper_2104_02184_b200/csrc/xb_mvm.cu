@@ -37,7 +37,7 @@ __device__ __forceinline__ float block_max(float m, float *red) {
   return red[32];
 }
 
-constexpr int PREP_THREADS = 512;
+constexpr int PREP_THREADS = XB_PREP_THREADS;
 
 // Pass 0: alpha = max|x| per sample (abs-max; or the all-reduced global value
 // of a row shard), x~ at m = 0, ||x~||.  Block 0 also clears the
@@ -55,18 +55,32 @@ __global__ void __launch_bounds__(PREP_THREADS) prep_kernel(
   if (bm_clear && b == 0)
     for (int i = threadIdx.x; i < bm_words; i += blockDim.x) bm_clear[i] = 0;
   const float *x = X + (size_t)b * n;
+  // short rows (the usual case): one read of x into registers serves the
+  // abs-max and the DAC
+  const bool regs = n <= (int)blockDim.x * PREP_VPT;
+  float v[PREP_VPT];
   float m = 0.f;
-  if (amax_in) {
-    m = amax_in[b];
-  } else {
+  if (regs) {
+#pragma unroll
+    for (int u = 0; u < PREP_VPT; ++u) {
+      const int j = threadIdx.x + u * (int)blockDim.x;
+      v[u] = j < n ? __ldcs(x + j) : 0.f;
+      m = fmaxf(m, fabsf(v[u]));
+    }
+  } else if (!amax_in) {
     for (int j = threadIdx.x; j < n; j += blockDim.x) m = fmaxf(m, fabsf(x[j]));
-    m = block_max(m, red);
   }
+  if (amax_in)
+    m = amax_in[b];
+  else
+    m = block_max(m, red);
   SampleState s;
   s.alpha = (m == 0.f) ? 0.f : (io.nm_absmax ? m : 1.f);
   s.m = 0;
   s.active = 1;
-  s.norm = prep_row(x, n, Xt + (size_t)b * ldt, s, io, key, seq0 + (uint64_t)b, in0, red);
+  const uint64_t seq = seq0 + (uint64_t)b;
+  s.norm = regs ? prep_row_vals(v, n, Xt + (size_t)b * ldt, s, io, key, seq, in0, red)
+                : prep_row(x, n, Xt + (size_t)b * ldt, s, io, key, seq, in0, red);
   if (threadIdx.x == 0) st[b] = s;
 }
 
@@ -534,7 +548,7 @@ __global__ void __launch_bounds__(256) epilogue_kernel(const float *__restrict__
   }
   const bool hit = epilogue_group4(a, g, o0, M, s, io, key, seq0 + (uint64_t)b,
                                    Y + (size_t)b * ldy);
-  bm_flag(hit, s, io, bm.flags + (pass & 1) * nb + (b - n0), bm.counts + pass);
+  bm_flag(hit, s, io, bm.flags + (pass & 1) * nb + (b - n0));
 }
 
 // Row-shard backward, phase 1: the shard's column sums plus its share of the
@@ -590,6 +604,8 @@ __global__ void __launch_bounds__(256) finish_kernel(const float *__restrict__ P
 
 struct MvmScratch {
   float *xt;
+  float *xt1;   // x~ at m = 1 [B][ldt] (in-kernel bound management), else null
+  SampleState *st1;
   float *acc;   // pass 0 partial sums [nsplit][B][M] (unfused)
   float *acc_r; // re-issue partial sums [nsplit][256][M] (unfused)
   SampleState *st;
@@ -600,9 +616,10 @@ struct MvmScratch {
 
 constexpr int SLAB = 256;
 
-MvmScratch carve(Tile &t, int B, int K, int M, int nsplit) {
+MvmScratch carve(Tile &t, int B, int K, int M, int nsplit, bool level1) {
   const int nslab = (B + SLAB - 1) / SLAB;
   const size_t xt_b = (size_t)B * K * sizeof(float);
+  const size_t xt1_b = level1 ? xt_b : 0, st1_b = level1 ? (size_t)B * sizeof(SampleState) : 0;
   const size_t acc_b = (size_t)nsplit * B * M * sizeof(float);
   const size_t accr_b = nsplit ? (size_t)nsplit * std::min(B, SLAB) * M * sizeof(float) : 0;
   const size_t st_b = (size_t)B * sizeof(SampleState);
@@ -611,10 +628,14 @@ MvmScratch carve(Tile &t, int B, int K, int M, int nsplit) {
   const size_t map_b = (size_t)B * sizeof(int);
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   char *p = (char *)t.s_io.get(al(xt_b) + al(acc_b) + al(accr_b) + al(st_b) + al(bm_b) +
-                               al(map_b));
+                               al(map_b) + al(xt1_b) + al(st1_b));
   MvmScratch s;
   s.xt = (float *)p;
   p += al(xt_b);
+  s.xt1 = level1 ? (float *)p : nullptr;
+  p += al(xt1_b);
+  s.st1 = level1 ? (SampleState *)p : nullptr;
+  p += al(st1_b);
   s.acc = (float *)p;
   p += al(acc_b);
   s.acc_r = (float *)p;
@@ -706,6 +727,13 @@ static bool host_passes_requested() {
   return e && e[0] == '1';
 }
 
+// XB_BM_NO_LEVEL1=1: every in-kernel re-issue is compacted and prepared after
+// its barrier (A/B measurements of the prestaged m = 1 slab)
+static bool level1_disabled() {
+  const char *e = getenv("XB_BM_NO_LEVEL1");
+  return e && e[0] == '1';
+}
+
 // tensor-core contraction at TF32 / 3xTF32 (B >= 16); the fp32 SIMT kernel
 // otherwise (exact-fp32 parity mode, tiny batches)
 static bool use_tc(const Tile &t, int B) {
@@ -747,9 +775,14 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io_in, 
   // GEMV splits the rows (partials summed in order by the epilogue kernel)
   const bool gv = !tc && B <= GV_MAXB;
   // (GEMV backward: acc_r holds the row-split partials; GVB_SPLITS sets of B x M)
-  MvmScratch s = carve(t, B, ldt, M, fused ? 0 : (tc ? splits : (gv && TRANS ? GVB_SPLITS : 1)));
   const bool bm = io.bm && !skip_epilogue;
   const bool sharded_bm = bm && t.comm && !TRANS;
+  const bool want_loop = fused && bm && !sharded_bm && !host_passes_requested();
+  // the loop's first re-issue streams an m = 1 slab the contraction's idle
+  // warps prepare during pass 0 (FusedOut::xt1; TF32: 3xTF32 has no idle warps)
+  const bool level1 = want_loop && !x3 && io.bm_max_iter >= 1 && !level1_disabled();
+  MvmScratch s = carve(t, B, ldt, M, fused ? 0 : (tc ? splits : (gv && TRANS ? GVB_SPLITS : 1)),
+                       level1);
   const int nslab = (B + SLAB - 1) / SLAB;
   int *bars = s.bm + (size_t)nslab * BM_SLAB_WORDS;
 
@@ -761,7 +794,6 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io_in, 
     gemv_fused_fwd(t, dIn, K, M, B, dOut, io, key, seq0, o0);
     return;
   }
-  const bool want_loop = fused && bm && !sharded_bm && !host_passes_requested();
   prep_kernel<<<B, PREP_THREADS, 0, t.stream>>>(dIn, K, s.xt, ldt, s.st, io, key, seq0, amax_in,
                                                  in0, bm ? s.bm : nullptr, s.bm_words);
   count_launch();
@@ -783,6 +815,8 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io_in, 
   fo.xt = s.xt;
   fo.ldt = ldt;
   fo.bar = reinterpret_cast<unsigned *>(bars);
+  fo.xt1 = s.xt1;
+  fo.st1 = s.st1;
 
   // ---- pass 0
   bool looped = false;

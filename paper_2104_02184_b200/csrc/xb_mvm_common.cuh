@@ -127,15 +127,16 @@ __device__ __forceinline__ bool epilogue_group4(const float a[4], int g, int o0,
   return hit;
 }
 
-// BM bookkeeping: one flag write per warp (a saturating sample saturates many
-// outputs; per-thread atomics on the same word would serialise).  flag = this
-// sample's word in the pass's flag array, count = the pass's counter.
+// BM bookkeeping: one flag store per warp (a saturating sample saturates many
+// outputs).  A plain store of 1, never read back here: every writer stores the
+// same value, and the readers run after a kernel boundary or a grid barrier
+// (a returning atomic here would hold the warp for an L2 round trip per
+// output column).  flag = this sample's word in the pass's flag array.
 __device__ __forceinline__ void bm_flag(bool hit, const SampleState &s, const IoDev &io,
-                                        int *flag, int *count) {
+                                        int *flag) {
   if (io.bm && s.alpha != 0.f && s.m < io.bm_max_iter) {
     const unsigned any = __ballot_sync(__activemask(), hit);
-    if (hit && (threadIdx.x & 31) == __ffs(any) - 1 && atomicExch(flag, 1) == 0)
-      atomicAdd(count, 1);
+    if (hit && (threadIdx.x & 31) == __ffs(any) - 1) *reinterpret_cast<volatile int *>(flag) = 1;
   }
 }
 
@@ -148,30 +149,33 @@ __device__ __forceinline__ void bm_flag(bool hit, const SampleState &s, const Io
 constexpr int BM_SLAB_WORDS = 2 * 256 + 64;
 struct BmBufs {
   int *flags;  // [2][nb]
-  int *counts; // [64] per pass; [32 + p]: compacted count for pass p (host-driven rounds)
+  int *counts; // [64]; [32 + p]: compacted count for pass p (host-driven rounds)
   int *map;    // [nb] compacted sample list (global sample index)
 };
 
 // (x~ prep, one sample) proj/src/io.cpp:117-131: x~_j = Q_dac(x_j / (alpha 2^m))
-// + sigma_inp xi_j in fp64 converter arithmetic, ||x~|| returned in every
-// thread.  All threads of the block take part; red: >= 33 floats of shared.
-__device__ __forceinline__ float prep_row(const float *__restrict__ x, int n,
-                                          float *__restrict__ xt, const SampleState &s,
-                                          const IoDev &io, Key key, uint64_t seq, int in0,
-                                          float *red) {
-  const double inv = (s.alpha == 0.f) ? 0.0 : 1.0 / ((double)s.alpha * pow2i(s.m));
-  // fp32 fast path of the DAC, bit-identical to the fp64 quantizer: the grid
-  // index is k = round_half_away(t), t = x inv L / (2 b) + (L - 1) / 2
-  // (L = 2^bits).  In fp32, t carries at most L 2^-23 of error; outside a
-  // window of L 2^-20 around a half-integer both evaluations round the same
-  // way, and inside it (rare) the element takes the fp64 path.  Without it
-  // the DAC was fp64-conversion bound (~4 us per 4096-wide sample on B200).
-  const bool fast = !io.perfect && s.alpha != 0.f && io.dac.bits > 0 && io.dac.bits <= 16 &&
-                    io.dac.pow2 && io.sigma_inp == 0.0;
-  const float a32 = fast ? (float)(inv * exp2((double)io.dac.bits) / (2.0 * io.dac.bound)) : 0.f;
-  const float c032 = 0.5f * (io.dac.flevels_m1);   // (L - 1) / 2, exact
-  const float tie_eps = fast ? ldexpf(1.f, io.dac.bits - 20) : 0.f;
-  auto convert = [&](float xv, int j) -> float {
+// + sigma_inp xi_j in fp64 converter arithmetic.
+struct RowDac {
+  double inv;
+  float a32, c032, tie_eps;
+  bool fast;
+  __device__ __forceinline__ RowDac(const SampleState &s, const IoDev &io) {
+    inv = (s.alpha == 0.f) ? 0.0 : 1.0 / ((double)s.alpha * pow2i(s.m));
+    // fp32 fast path of the DAC, bit-identical to the fp64 quantizer: the grid
+    // index is k = round_half_away(t), t = x inv L / (2 b) + (L - 1) / 2
+    // (L = 2^bits).  In fp32, t carries at most L 2^-23 of error; outside a
+    // window of L 2^-20 around a half-integer both evaluations round the same
+    // way, and inside it (rare) the element takes the fp64 path.  Without it
+    // the DAC was fp64-conversion bound (~4 us per 4096-wide sample on B200).
+    fast = !io.perfect && s.alpha != 0.f && io.dac.bits > 0 && io.dac.bits <= 16 && io.dac.pow2 &&
+           io.sigma_inp == 0.0;
+    a32 = fast ? (float)(inv * exp2((double)io.dac.bits) / (2.0 * io.dac.bound)) : 0.f;
+    c032 = 0.5f * (io.dac.flevels_m1); // (L - 1) / 2, exact
+    tie_eps = fast ? ldexpf(1.f, io.dac.bits - 20) : 0.f;
+  }
+  __device__ __forceinline__ float operator()(float xv, int j, const SampleState &s,
+                                              const IoDev &io, Key key, uint64_t seq,
+                                              int in0) const {
     if (io.perfect) return xv;
     if (s.alpha == 0.f) return 0.f;
     if (fast) {
@@ -192,32 +196,12 @@ __device__ __forceinline__ float prep_row(const float *__restrict__ x, int n,
       q += io.sigma_inp * (double)z;
     }
     return (float)q;
-  };
-  float nrm = 0.f;
-  constexpr int VPT = 8; // all loads of a thread in flight before any conversion
-  if (n <= (int)blockDim.x * VPT) {
-    float v[VPT];
-#pragma unroll
-    for (int u = 0; u < VPT; ++u) {
-      const int j = threadIdx.x + u * (int)blockDim.x;
-      v[u] = j < n ? x[j] : 0.f;
-    }
-#pragma unroll
-    for (int u = 0; u < VPT; ++u) {
-      const int j = threadIdx.x + u * (int)blockDim.x;
-      if (j < n) {
-        const float f = convert(v[u], j);
-        xt[j] = f;
-        nrm = fmaf(f, f, nrm);
-      }
-    }
-  } else {
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
-      const float f = convert(x[j], j);
-      xt[j] = f;
-      nrm = fmaf(f, f, nrm);
-    }
   }
+};
+
+// ||x~|| from every thread's partial sum of squares: warp sums, then the
+// warps in order (the order every x~ prep of the library shares)
+__device__ __forceinline__ float row_norm(float nrm, float *red) {
   nrm = warp_sum(nrm);
   __syncthreads();
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
@@ -226,6 +210,56 @@ __device__ __forceinline__ float prep_row(const float *__restrict__ x, int n,
   for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
   __syncthreads();
   return sqrtf(tot);
+}
+
+// block size of every x~ prep (prep / re-issue kernels, the in-kernel loop):
+// ||x~|| sums per-thread partials in this layout, so it fixes the bits
+#define XB_PREP_THREADS 512
+
+// the register path of the prep: element j = threadIdx.x + u blockDim.x is
+// v[u] (n <= blockDim.x PREP_VPT); ||x~|| returned in every thread
+constexpr int PREP_VPT = 8;
+__device__ __forceinline__ float prep_row_vals(const float (&v)[PREP_VPT], int n,
+                                               float *__restrict__ xt, const SampleState &s,
+                                               const IoDev &io, Key key, uint64_t seq, int in0,
+                                               float *red) {
+  const RowDac dac(s, io);
+  float nrm = 0.f;
+#pragma unroll
+  for (int u = 0; u < PREP_VPT; ++u) {
+    const int j = threadIdx.x + u * (int)blockDim.x;
+    if (j < n) {
+      const float f = dac(v[u], j, s, io, key, seq, in0);
+      xt[j] = f;
+      nrm = fmaf(f, f, nrm);
+    }
+  }
+  return row_norm(nrm, red);
+}
+
+// x~ row of one sample at level s.m, ||x~|| returned in every thread.  All
+// threads of the block take part; red: >= 33 floats of shared.
+__device__ __forceinline__ float prep_row(const float *__restrict__ x, int n,
+                                          float *__restrict__ xt, const SampleState &s,
+                                          const IoDev &io, Key key, uint64_t seq, int in0,
+                                          float *red) {
+  if (n <= (int)blockDim.x * PREP_VPT) { // all loads of a thread in flight first
+    float v[PREP_VPT];
+#pragma unroll
+    for (int u = 0; u < PREP_VPT; ++u) {
+      const int j = threadIdx.x + u * (int)blockDim.x;
+      v[u] = j < n ? x[j] : 0.f;
+    }
+    return prep_row_vals(v, n, xt, s, io, key, seq, in0, red);
+  }
+  const RowDac dac(s, io);
+  float nrm = 0.f;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const float f = dac(x[j], j, s, io, key, seq, in0);
+    xt[j] = f;
+    nrm = fmaf(f, f, nrm);
+  }
+  return row_norm(nrm, red);
 }
 
 // Block-wide compaction: map[0..n) = the indices i < nb with flags[i] != 0,
@@ -295,6 +329,12 @@ struct FusedOut {
   float *xt;           // x~ rows of this slab; re-issue rows are compacted from row 0
   int ldt;
   unsigned *bar;       // grid-barrier counter, zero at launch
+  // x~ of every sample of the slab at m = 1, prepared during pass 0 by the
+  // contraction's idle warps, and its states (global index): the first re-issue
+  // streams this slab whole -- no compaction, prep or second barrier -- and
+  // writes only the samples pass 0 flagged.  Null: every re-issue is compacted.
+  float *xt1;
+  SampleState *st1;
 };
 
 // tcgen05 contraction (xb_mvm_tc.cu).  fo == nullptr: split-K partial sums

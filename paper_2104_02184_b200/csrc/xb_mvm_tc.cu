@@ -237,7 +237,8 @@ template <int NW, int NS>
 __device__ __forceinline__ void reduce_columns(const FusedOut &fo, const float *red,
                                                uint32_t red_s, int row0, int M, int c_lo,
                                                int c_hi, uint32_t my_split, uint32_t nsplit,
-                                               const int *map, int *flags, int *count) {
+                                               const int *map, const SampleState *st,
+                                               const int *live, int *flags) {
   const int grp = threadIdx.x & 31, cph = threadIdx.x >> 5;
   auto load = [&](int c, float4 (&v)[NS]) {
     const uint32_t off = red_s + (uint32_t)((c * TC_BM + 4 * grp) * 4);
@@ -247,15 +248,32 @@ __device__ __forceinline__ void reduce_columns(const FusedOut &fo, const float *
         v[r] = r == (int)my_split ? *reinterpret_cast<const float4 *>(red + (off - red_s) / 4)
                                   : dsmem_ld4(dsmem_map(off, (uint32_t)r));
   };
+  // the column's sample, its state and (first prestaged re-issue) whether
+  // the previous pass flagged it: loaded one column ahead with the partials
+  auto meta = [&](int c, int &b, SampleState &sst, bool &on) {
+    b = map ? map[c] : fo.n0 + c;
+    on = !live || live[c] != 0;
+    sst = st[b];
+  };
   int c = c_lo + cph;
   if (c >= c_hi) return;
   float4 v[NS];
   load(c, v);
+  int b;
+  SampleState sst;
+  bool on;
+  meta(c, b, sst, on);
   const bool rows_ok = row0 + 4 * grp < M;
   for (;;) {
     const int cn = c + NW;
     float4 vn[NS];
-    if (NS <= 4 && cn < c_hi) load(cn, vn); // (8 splits: no registers to spare)
+    int bn_ = 0;
+    SampleState sn{};
+    bool onn = false;
+    if (cn < c_hi) {
+      if (NS <= 4) load(cn, vn); // (8 splits: no registers to spare)
+      meta(cn, bn_, sn, onn);
+    }
     float4 acc4 = v[0];
 #pragma unroll
     for (int r = 1; r < NS; ++r) // split order (as the epilogue kernel)
@@ -265,16 +283,14 @@ __device__ __forceinline__ void reduce_columns(const FusedOut &fo, const float *
         acc4.z += v[r].z;
         acc4.w += v[r].w;
       }
-    if (rows_ok) {
-      const int b = map ? map[c] : fo.n0 + c;
-      const SampleState sst = fo.st[b];
+    if (rows_ok && on) {
       const float a[4] = {acc4.x, acc4.y, acc4.z, acc4.w};
       // global output index of this group: o0 + row0 + 4 grp (o0 % 4 == 0 on
       // the fused path, so groups align with the noise groups)
       const int g = (fo.o0 + row0) / 4 + grp;
       const bool hit = epilogue_group4(a, g, fo.o0, M, sst, fo.io, fo.key,
                                        fo.seq0 + (uint64_t)b, fo.Y + (size_t)b * fo.ldy);
-      bm_flag(hit, sst, fo.io, flags + (b - fo.n0), count);
+      bm_flag(hit, sst, fo.io, flags + (b - fo.n0));
     }
     if (cn >= c_hi) break;
     if (NS <= 4) {
@@ -284,21 +300,82 @@ __device__ __forceinline__ void reduce_columns(const FusedOut &fo, const float *
       load(cn, v);
     }
     c = cn;
+    b = bn_;
+    sst = sn;
+    on = onn;
   }
+}
+
+// The m = 1 x~ rows of the slab (FusedOut::xt1/st1), prepared by the warps
+// idle during pass 0's mainloop (warps 2.., TF32), sample c on CTA c mod grid.
+// Bit-identical to prep_row run by XB_PREP_THREADS threads: each helper warp
+// plays whole virtual warps of that block -- virtual thread t converts
+// j = t + XB_PREP_THREADS u in ascending u and sums the squares in that
+// order -- and the 16 warp sums are added in virtual-warp order.
+__device__ __forceinline__ void stage_level1(const FusedOut &fo, float *red) {
+  constexpr int VW = XB_PREP_THREADS / 32;
+  const int hw = (int)(threadIdx.x >> 5) - 2, nh = (int)(blockDim.x >> 5) - 2;
+  const int lane = threadIdx.x & 31;
+  const unsigned cta = blockIdx.x + gridDim.x * blockIdx.y, nctas = gridDim.x * gridDim.y;
+  const int K = fo.K;
+  for (int c = (int)cta; c < fo.nb; c += (int)nctas) {
+    const int b = fo.n0 + c;
+    SampleState s = fo.st[b];
+    s.m = 1;
+    const RowDac dac(s, fo.io);
+    const uint64_t seq = fo.seq0 + (uint64_t)b;
+    const float *x = fo.X + (size_t)b * K;
+    float *xt = fo.xt1 + (size_t)c * fo.ldt;
+    for (int vw = hw; vw < VW; vw += nh) {
+      const int t = vw * 32 + lane;
+      float nrm = 0.f;
+      for (int j0 = 0; j0 < K; j0 += XB_PREP_THREADS * PREP_VPT) {
+        float v[PREP_VPT];
+#pragma unroll
+        for (int u = 0; u < PREP_VPT; ++u) {
+          const int j = j0 + t + u * XB_PREP_THREADS;
+          v[u] = j < K ? x[j] : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < PREP_VPT; ++u) {
+          const int j = j0 + t + u * XB_PREP_THREADS;
+          if (j < K) {
+            const float f = dac(v[u], j, s, fo.io, fo.key, seq, fo.in0);
+            xt[j] = f;
+            nrm = fmaf(f, f, nrm);
+          }
+        }
+      }
+      nrm = warp_sum(nrm);
+      if (lane == 0) red[vw] = nrm;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(nh * 32) : "memory");
+    if (hw == 0 && lane == 0) {
+      float tot = 0.f;
+      for (int w = 0; w < VW; ++w) tot += red[w];
+      s.norm = sqrtf(tot);
+      fo.st1[b] = s;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(nh * 32) : "memory");
+  }
+  // pass 1 streams these rows with TMA (async proxy), after the grid barrier
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 template <int NW, int NSUB>
 __device__ __forceinline__ void fused_output_stage(const FusedOut &fo, uint32_t tmem,
                                                    uint8_t *smem, int nkb, int m0, int M, int n,
                                                    int bnr, uint32_t my_split, uint32_t nsplit,
-                                                   const int *map, int pass) {
+                                                   const int *map, int pass, bool level1) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, quarter = warp & 3;
   float *red = reinterpret_cast<float *>(smem);
   const uint32_t red_s = smem_u32(red);
   const int cols = (bnr + (int)nsplit - 1) / (int)nsplit;
   const int c_lo = (int)my_split * cols, c_hi = min(n, c_lo + cols);
   int *flags = fo.bm.flags + (pass & 1) * fo.nb;
-  int *count = fo.bm.counts + pass;
+  // prestaged m = 1 pass: every column of the slab, written where pass 0 flagged
+  const SampleState *st = level1 ? fo.st1 : fo.st;
+  const int *live = level1 ? fo.bm.flags + ((pass - 1) & 1) * fo.nb : nullptr;
 #pragma unroll 1
   for (int sub = 0; sub < NSUB; ++sub) {
     const int row = quarter * 32 + lane;
@@ -314,11 +391,11 @@ __device__ __forceinline__ void fused_output_stage(const FusedOut &fo, uint32_t 
     if (threadIdx.x == 0 && sub == 0) XB_TRACE(5);
     const int row0 = m0 + sub * TC_BM; // local output index of row 0 of the sub-tile
     if (nsplit <= 4)
-      reduce_columns<NW, 4>(fo, red, red_s, row0, M, c_lo, c_hi, my_split, nsplit, map, flags,
-                            count);
+      reduce_columns<NW, 4>(fo, red, red_s, row0, M, c_lo, c_hi, my_split, nsplit, map, st,
+                            live, flags);
     else
-      reduce_columns<NW, 8>(fo, red, red_s, row0, M, c_lo, c_hi, my_split, nsplit, map, flags,
-                            count);
+      reduce_columns<NW, 8>(fo, red, red_s, row0, M, c_lo, c_hi, my_split, nsplit, map, st,
+                            live, flags);
     cluster_sync_all(); // the partials are read before the next sub-tile overwrites them
   }
 }
@@ -344,7 +421,8 @@ __device__ __forceinline__ void fused_output_stage(const FusedOut &fo, uint32_t 
 template <bool A_MN, bool X3, int NSUB, bool FUSED>
 __global__ void __launch_bounds__(tc_threads<X3, FUSED>(), 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
-                   const __grid_constant__ CUtensorMap tm_r, int M, int K, int B, int bn,
+                   const __grid_constant__ CUtensorMap tm_r,
+                   const __grid_constant__ CUtensorMap tm_1, int M, int K, int B, int bn,
                    int kblocks_per_split, float *__restrict__ part, int ldp, size_t split_stride,
                    const int *__restrict__ n_rows, const __grid_constant__ FusedOut fo) {
   constexpr int STAGES = tc_stages<X3, NSUB>();
@@ -352,6 +430,7 @@ __global__ void __launch_bounds__(tc_threads<X3, FUSED>(), 1)
   constexpr int AB = NSUB * TC_A_BYTES;          // A bytes per stage
   constexpr int LO = NSUB * TC_A_BYTES + TC_B_BYTES; // offset of the lo copies (X3)
   constexpr int NT = tc_threads<X3, FUSED>();
+  static_assert(!FUSED || NT == XB_PREP_THREADS, "the in-kernel x~ prep shares prep_row's layout");
   extern __shared__ uint8_t smem_raw[];
   __shared__ float red[40];
   // 1024-byte alignment for the 128-byte swizzle atoms; stage s holds
@@ -403,6 +482,7 @@ __global__ void __launch_bounds__(tc_threads<X3, FUSED>(), 1)
 
   const int *map = FUSED ? fo.bm.map : nullptr; // compacted list (re-issue passes)
   bool reissue = ndev != nullptr;               // B operand = compacted rows (tm_r)
+  bool level1 = false; // B operand = the prestaged m = 1 slab (tm_1), all columns
   int pass = FUSED ? fo.pass : 0;
   uint32_t gk = 0;     // k-blocks streamed by this CTA in this launch (ring position)
   uint32_t iter = 0;   // passes run in this launch (parity of `done`)
@@ -414,6 +494,7 @@ __global__ void __launch_bounds__(tc_threads<X3, FUSED>(), 1)
     // a re-issue of a few samples streams just their x~ rows (32-row boxes);
     // of many, the slab's whole box (rows >= n are stale and never read out)
     const bool boxes = reissue && n <= 64;
+    const int ncols = level1 ? fo.nb : n; // output columns of this pass
     const int nbox = (n + 31) / 32;
     const uint32_t b_bytes = boxes ? (uint32_t)nbox * 32u * TC_BK * 4u : (uint32_t)bn * TC_BK * 4;
     if (warp == 0 && lane == 0 && nkb > 0) {
@@ -451,6 +532,8 @@ __global__ void __launch_bounds__(tc_threads<X3, FUSED>(), 1)
         if (boxes) {
           for (int j = 0; j < nbox; ++j)
             tma_load_2d(smem_u32(stage_b(s) + j * 4096), &tm_r, full0 + 8 * s, kk, 32 * j);
+        } else if (level1) {
+          tma_load_2d(smem_u32(stage_b(s)), &tm_1, full0 + 8 * s, kk, 0);
         } else {
           tma_load_2d(smem_u32(stage_b(s)), &tm_b, full0 + 8 * s, kk, 0);
         }
@@ -517,6 +600,7 @@ __global__ void __launch_bounds__(tc_threads<X3, FUSED>(), 1)
     }
     __syncwarp();
     if (iter == 0) asm volatile("griddepcontrol.wait;" ::: "memory"); // prep's st[] / flags
+    if (FUSED && !X3 && iter == 0 && fo.loop && fo.xt1 && warp >= 2) stage_level1(fo, red);
 
     // ---------------- epilogue: TMEM -> registers -> partial sums / output stage
     if (nkb > 0) {
@@ -552,8 +636,8 @@ __global__ void __launch_bounds__(tc_threads<X3, FUSED>(), 1)
       break;
     }
     // split peers: cluster (1, S), CTA rank == split index
-    fused_output_stage<NT / 32, NSUB>(fo, tmem, smem, nkb, m0, M, n, bnr, cluster_rank(),
-                                      cluster_size(), reissue ? map : nullptr, pass);
+    fused_output_stage<NT / 32, NSUB>(fo, tmem, smem, nkb, m0, M, ncols, bnr, cluster_rank(),
+                                      cluster_size(), reissue ? map : nullptr, pass, level1);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     gk += (uint32_t)max(nkb, 0);
     ++iter;
@@ -570,6 +654,15 @@ __global__ void __launch_bounds__(tc_threads<X3, FUSED>(), 1)
       g_tc_trace[blockIdx.x + gridDim.x * blockIdx.y][15] = (unsigned long long)n;
 #endif
     if (n == 0) break; // uniform: every CTA read the same flags
+    if (pass == 0 && fo.xt1) {
+      // first re-issue from the prestaged m = 1 slab: nothing to prepare, and
+      // the flags pass 1 writes are still clear from the prep kernel -- so no
+      // second barrier either
+      level1 = true;
+      ++pass;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      continue;
+    }
     {
       // clear the flags the next pass will write (read by nobody now)
       int *nf = fo.bm.flags + ((pass + 1) & 1) * nb;
@@ -578,7 +671,7 @@ __global__ void __launch_bounds__(tc_threads<X3, FUSED>(), 1)
       // this CTA's share of the re-issued rows: x~ at m + 1 (io.cpp:117-131)
       for (int c = (int)cta; c < n; c += (int)nctas) {
         const int b = fo.bm.map[c];
-        SampleState s = fo.st[b];
+        SampleState s = level1 ? fo.st1[b] : fo.st[b]; // its state in the pass just run
         s.m += 1;
         s.norm = prep_row(fo.X + (size_t)b * fo.K, fo.K, fo.xt + (size_t)c * fo.ldt, s, fo.io,
                           fo.key, fo.seq0 + (uint64_t)b, fo.in0, red);
@@ -594,6 +687,7 @@ __global__ void __launch_bounds__(tc_threads<X3, FUSED>(), 1)
     if (threadIdx.x == 0 && iter == 1) XB_TRACE(10);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     reissue = true;
+    level1 = false;
     ++pass;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -668,7 +762,7 @@ int tc_splits(int M, int K, bool x3) {
 struct TcArgs {
   dim3 grid;
   cudaStream_t st;
-  CUtensorMap ma, mb, mr;
+  CUtensorMap ma, mb, mr, m1;
   int M, K, nb, bn, per;
   float *part;
   size_t split_stride;
@@ -717,7 +811,7 @@ static bool launch_tc(const TcArgs &a, bool check_loop) {
     }
     return clusters >= (int)a.grid.x;
   }
-  XB_CUDA(cudaLaunchKernelEx(&cfg, kern, a.ma, a.mb, a.mr, a.M, a.K, a.nb, a.bn, a.per, a.part,
+  XB_CUDA(cudaLaunchKernelEx(&cfg, kern, a.ma, a.mb, a.mr, a.m1, a.M, a.K, a.nb, a.bn, a.per, a.part,
                              a.M, a.split_stride, a.n_rows, a.fo));
   count_launch();
   XB_CUDA(cudaGetLastError());
@@ -770,6 +864,7 @@ bool tc_gemm(Tile &t, bool transposed, bool x3, const float *Xt, int ldt, int B,
                       : make_map(t.W, t.R, t.C, t.ld, TC_BM * nsub);
     a.mb = make_map(Xt + (size_t)n0 * ldt, nb, K, ldt, bn);
     a.mr = make_map(Xt + (size_t)n0 * ldt, nb, K, ldt, 32);
+    a.m1 = (fo && fo->xt1) ? make_map(fo->xt1 + (size_t)n0 * ldt, nb, K, ldt, bn) : a.mb;
     a.grid = dim3((M + TC_BM * nsub - 1) / (TC_BM * nsub), used);
     a.st = t.stream;
     a.M = M;
@@ -789,6 +884,7 @@ bool tc_gemm(Tile &t, bool transposed, bool x3, const float *Xt, int ldt, int B,
       a.fo.bm.map = fo->bm.map + n0;
       a.fo.bar = fo->bar ? fo->bar + slab : nullptr;
       a.fo.xt = fo->xt ? fo->xt + (size_t)n0 * ldt : nullptr;
+      a.fo.xt1 = fo->xt1 ? fo->xt1 + (size_t)n0 * ldt : nullptr;
       a.part = nullptr;
       a.split_stride = 0;
       if (bm_loop && n0 == 0) looped = launch_variant<true>(transposed, x3, nsub, a, true);
