@@ -3,6 +3,8 @@ reference's own unit-test cases re-run through the C++ API."""
 import os
 import subprocess
 
+import numpy as np
+
 import pytest
 
 pytestmark = pytest.mark.gpu
@@ -104,3 +106,40 @@ def test_reference_nn_tests_on_the_b200_tile():
         else:
             assert ok, (name, msgs)
     assert sum(ok for ok, _ in cases.values()) >= 19 - len(FP64_EXACT)
+
+
+def _history(text):
+    rows = [ln.split(",") for ln in text.strip().splitlines()[1:]]
+    return [(int(e), float(l), float(a)) for e, l, a in rows]
+
+
+@pytest.mark.parametrize("name", ["train_reram", "tiki_taka", "conv_digits", "inference_pcm"])
+def test_config_driven_training_on_b200(name):
+    """The reference's config-driven training (parse_config, build_network,
+    train: proj/src/config.cpp, nn.cpp, compiled where they lie) with the
+    B200 backend of build_tile (integration/b200_backend.hpp): every tile of
+    the network -- AnalogTile, TransferTile (Tiki-Taka), conv layers' tiles --
+    is a GPU tile.  The reference's own run of the same config on its CPU
+    tiles is tests/golden/train/<name>.csv (make_train_golden.py).  The two
+    draw different random streams (Philox vs mt19937), so they are compared
+    as training outcomes: the same epochs, the loss falling as far, and the
+    final accuracy as high."""
+    root = os.path.dirname(HERE)
+    exe = os.path.join(root, "integration", "_ref", "train_config_b200")
+    if not os.path.exists(exe):
+        pytest.skip("integration/_ref not built (needs /root/reference at build time)")
+    cfg = os.path.join(HERE, "golden", "train", name + ".json")
+    r = subprocess.run([exe, cfg], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = _history(r.stdout)
+    with open(os.path.join(HERE, "golden", "train", name + ".csv")) as f:
+        ref = _history(f.read())
+    print(name, "b200", got[-1], "reference", ref[-1])
+    assert [e for e, _, _ in got] == [e for e, _, _ in ref]
+    loss0, lossN = got[0][1], np.mean([l for _, l, _ in got[-5:]])
+    ref0, refN = ref[0][1], np.mean([l for _, l, _ in ref[-5:]])
+    assert abs(loss0 - ref0) <= 0.25 * ref0
+    assert lossN <= max(2.0 * refN, refN + 0.02), (lossN, refN)
+    if ref[-1][2] == ref[-1][2]:  # classification (NaN for regression)
+        acc = np.mean([a for _, _, a in got[-5:]])
+        assert acc >= np.mean([a for _, _, a in ref[-5:]]) - 0.05, acc
