@@ -559,10 +559,10 @@ __global__ void __launch_bounds__(256) partial_kernel(const float *__restrict__ 
                                                        float *__restrict__ P,
                                                        const SampleState *__restrict__ st,
                                                        IoDev io, Key key, uint64_t seq0,
-                                                       uint32_t shard_tag) {
-  const int b = blockIdx.y;
+                                                       uint32_t shard_tag, int B) {
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= M) return;
+  for (int b = blockIdx.y; b < B; b += gridDim.y) { // (gridDim.y <= 65535)
   const SampleState s = st[b];
   float v = acc[(size_t)b * M + o];
   for (int sp = 1; sp < nsplit; ++sp) v += acc[sp * split_stride + (size_t)b * M + o];
@@ -572,6 +572,7 @@ __global__ void __launch_bounds__(256) partial_kernel(const float *__restrict__ 
     v += (float)(io.sigma_w * (double)s.norm * (double)z);
   }
   P[(size_t)b * M + o] = v;
+  }
 }
 
 // Row-shard backward, phase 2 (after the sum over shards): output noise, ADC
@@ -581,10 +582,11 @@ __global__ void __launch_bounds__(256) partial_kernel(const float *__restrict__ 
 __global__ void __launch_bounds__(256) finish_kernel(const float *__restrict__ Psum, int M,
                                                       const float *__restrict__ amax,
                                                       float *__restrict__ Y, IoDev io, Key key,
-                                                      uint64_t seq0) {
-  const int b = blockIdx.y;
+                                                      uint64_t seq0, int B) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (4 * g >= M) return;
+  io.sigma_w = 0.0;
+  for (int b = blockIdx.y; b < B; b += gridDim.y) { // (gridDim.y <= 65535)
   const float m = amax[b];
   SampleState s;
   s.alpha = (m == 0.f) ? 0.f : (io.nm_absmax ? m : 1.f);
@@ -597,9 +599,9 @@ __global__ void __launch_bounds__(256) finish_kernel(const float *__restrict__ P
     if (4 * g + k < M) a[k] = Psum[(size_t)b * M + 4 * g + k];
   // the weight-noise fold is already in the partial sums (partial_kernel):
   // only the output noise, the ADC and alpha act here, with the same noise
-  // words and arithmetic as the whole-tile output stage
-  io.sigma_w = 0.0;
+  // words and arithmetic as the whole-tile output stage (sigma_w = 0 above)
   epilogue_group4(a, g, 0, M, s, io, key, seq0 + (uint64_t)b, Y + (size_t)b * M);
+  }
 }
 
 struct MvmScratch {
@@ -832,10 +834,10 @@ void run_mvm(Tile &t, const float *dIn, int B, float *dOut, const IoDev &io_in, 
     gemm<TRANS>(t, s.xt, ldt, M, K, B, s.acc, nullptr);
   }
   if (skip_epilogue) { // row shard: partial sums + this shard's weight-noise fold
-    dim3 eg((M + 255) / 256, B);
+    dim3 eg((M + 255) / 256, std::min(B, 65535));
     partial_kernel<<<eg, 256, 0, t.stream>>>(s.acc, M, nsplit, (size_t)B * M, dPartial, s.st,
                                              io, key, seq0,
-                                             (TAG_W_NOISE << 24) | (uint32_t)t.row0);
+                                             (TAG_W_NOISE << 24) | (uint32_t)t.row0, B);
     count_launch();
     XB_CUDA(cudaGetLastError());
     return;
@@ -976,8 +978,8 @@ void mvm_backward_finish(Tile &t, const float *dPsum, int B, const float *amax_g
   if (!amax_global) raise("backward_finish: the global max|d| per sample is required");
   IoDev io2 = io;
   io2.exact = !use_tc(t, B);
-  dim3 eg((out_groups(0, t.C) + 255) / 256, B);
-  finish_kernel<<<eg, 256, 0, t.stream>>>(dPsum, t.C, amax_global, dG, io2, key, seq0);
+  dim3 eg((out_groups(0, t.C) + 255) / 256, std::min(B, 65535));
+  finish_kernel<<<eg, 256, 0, t.stream>>>(dPsum, t.C, amax_global, dG, io2, key, seq0, B);
   count_launch();
   XB_CUDA(cudaGetLastError());
 }

@@ -799,20 +799,20 @@ void launch_pulse(Tile &t, const uint32_t *xw, const uint32_t *dw, int ldb, int 
 __global__ void gather_samples_kernel(const uint32_t *__restrict__ in, int ldb_in, int lines,
                                       const int *__restrict__ idx, int n,
                                       uint32_t *__restrict__ out, int ldb_out, bool quad) {
-  const int line = blockIdx.y;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ldb_out; k += gridDim.x * blockDim.x) {
-    if (quad)
-      out[xq_index(line, k, lines)] = k < n ? in[xq_index(line, idx[k], lines)] : 0u;
-    else
-      out[(size_t)line * ldb_out + k] = k < n ? in[(size_t)line * ldb_in + idx[k]] : 0u;
-  }
+  for (int line = blockIdx.y; line < lines; line += gridDim.y) // (gridDim.y <= 65535)
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ldb_out; k += gridDim.x * blockDim.x) {
+      if (quad)
+        out[xq_index(line, k, lines)] = k < n ? in[xq_index(line, idx[k], lines)] : 0u;
+      else
+        out[(size_t)line * ldb_out + k] = k < n ? in[(size_t)line * ldb_in + idx[k]] : 0u;
+    }
 }
 
 void launch_gather_samples(const uint32_t *in, int ldb_in, int lines, const int *idx, int n,
                            uint32_t *out, int ldb_out, cudaStream_t s, bool quad) {
   if (lines <= 0 || ldb_out <= 0) return;
   const int threads = std::min(256, (ldb_out + 31) / 32 * 32);
-  dim3 grid((ldb_out + threads - 1) / threads, lines);
+  dim3 grid((ldb_out + threads - 1) / threads, std::min(lines, 65535));
   gather_samples_kernel<<<grid, threads, 0, s>>>(in, ldb_in, lines, idx, n, out, ldb_out, quad);
   count_launch();
   XB_CUDA(cudaGetLastError());

@@ -131,3 +131,29 @@ def test_chunked_backward_equals_one_shot(prec):
         np.testing.assert_array_equal(G1, outs[0][0])
         np.testing.assert_array_equal(G2, outs[0][1])
     assert not np.array_equal(outs[0][0], outs[0][1])  # fresh noise per call
+
+
+def test_split_phase_backward_beyond_grid_y_limit():
+    """More samples than a grid's y dimension holds (65535): the split-phase
+    backward in one call equals the same entries in two chunks below the
+    limit, bit for bit (the partial/finish kernels stride over samples)."""
+    R, C, B = 24, 16, 70000
+    bio = xb.default_io()
+    s = xb.TileSettings(device=xb.device_preset("reram_sb"), backward_io=bio)
+    W = np.random.default_rng(8).uniform(-0.3, 0.3, (R, C)).astype(np.float32)
+    g = torch.Generator(device="cuda").manual_seed(6)
+    D = torch.rand(B, R, device="cuda", generator=g) * 2 - 1
+    out = []
+    for edges in ((0, B), (0, 40000, B)):
+        t = xb.AnalogTile(R, C, s, 21)
+        t.set_stream(torch.cuda.current_stream().cuda_stream)
+        t.set_weights(W)
+        amax = t.rows_amax(D)
+        G = torch.empty(B, C, device="cuda")
+        for b0, b1 in zip(edges[:-1], edges[1:]):
+            P = t.backward_partial_dev(D[b0:b1], amax[b0:b1])
+            t.backward_finish_dev(P, amax[b0:b1], G[b0:b1])
+        torch.cuda.synchronize()
+        out.append(G.cpu().numpy())
+    np.testing.assert_array_equal(out[0], out[1])
+    assert np.abs(out[0]).max() > 0
