@@ -17,6 +17,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=4096)
 ap.add_argument("--batch", type=int, default=256)
 ap.add_argument("--iters", type=int, default=50)
+ap.add_argument("--only", default=None, help="run one variant (perfect, default, noise-off, "
+                "bm-iter0, bm); e.g. under ncu")
 a = ap.parse_args()
 s = torch.cuda.Stream()
 torch.cuda.set_stream(s)
@@ -46,6 +48,8 @@ for _ in range(23):
 W = base.get_weights()
 for name, env in (("perfect", {}), ("default", {}), ("noise-off", {}), ("bm-iter0", {}),
                   ("bm", {}), ("bm", {"XB_BM_NO_LEVEL1": "1"}), ("bm", {"XB_BM_HOST_PASSES": "1"})):
+    if a.only and (name != a.only or env):
+        continue
     for k in ("XB_BM_NO_LEVEL1", "XB_BM_HOST_PASSES"):
         os.environ.pop(k, None)
     os.environ.update(env)
