@@ -17,14 +17,15 @@ ap.add_argument("--iters", type=int, default=5)
 a = ap.parse_args()
 t = xb.AnalogTile(a.n, a.n, xb.TileSettings(device=xb.device_preset("reram_sb")), 5)
 target = np.random.default_rng(1).uniform(-0.5, 0.5, (a.n, a.n)).astype(np.float32)
-t.program(target, xb.InferenceNoiseModel(), 11)
+m = xb.InferenceNoiseModel()
+t.program(target, m, 11)
 s = torch.cuda.ExternalStream(t.stream())
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-t.drift_to(10.0)
+t.drift_to(10.0 * m.t0)
 torch.cuda.synchronize()
 e0.record(s)
 for k in range(a.iters):
-    t.drift_to(100.0 * (k + 1))
+    t.drift_to(100.0 * (k + 1) * m.t0)
 e1.record(s)
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / a.iters
