@@ -19,6 +19,23 @@
 
 #include "xb_mvm_common.cuh"
 
+#ifdef XB_TC_TRACE
+// experiment builds only: globaltimer at the start and end of every prep block
+__device__ unsigned long long g_prep_trace[4096][2];
+extern "C" __attribute__((visibility("default"))) int xb_debug_prep_trace(unsigned long long *out,
+                                                                            int n) {
+  return (int)cudaMemcpyFromSymbol(out, g_prep_trace,
+                                   sizeof(unsigned long long) * 2 * (size_t)(n < 4096 ? n : 4096));
+}
+__device__ __forceinline__ void prep_stamp(int k) {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  if (threadIdx.x == 0 && blockIdx.x < 4096) g_prep_trace[blockIdx.x][k] = v;
+}
+#else
+__device__ __forceinline__ void prep_stamp(int) {}
+#endif
+
 namespace xb {
 
 namespace {
@@ -50,6 +67,7 @@ __global__ void __launch_bounds__(PREP_THREADS) prep_kernel(
   // the contraction (a programmatic dependent) may start its prologue and
   // W loads now; it waits for this grid before touching x~ / st / flags
   asm volatile("griddepcontrol.launch_dependents;");
+  prep_stamp(0);
   const int b = blockIdx.x;
   __shared__ float red[33];
   if (bm_clear && b == 0)
@@ -82,6 +100,7 @@ __global__ void __launch_bounds__(PREP_THREADS) prep_kernel(
   s.norm = regs ? prep_row_vals(v, n, Xt + (size_t)b * ldt, s, io, key, seq, in0, red)
                 : prep_row(x, n, Xt + (size_t)b * ldt, s, io, key, seq, in0, red);
   if (threadIdx.x == 0) st[b] = s;
+  prep_stamp(1);
 }
 
 // Re-issue prep (host-driven passes): block c < *count prepares the x~ row c

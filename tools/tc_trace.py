@@ -60,6 +60,11 @@ for name, io in cases:
     buf = (C.c_uint64 * (4096 * 16))()
     fn(buf, 4096)
     tr = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 16).astype(np.int64)
+    pfn = lib.xb_debug_prep_trace
+    pfn.argtypes = [C.POINTER(C.c_uint64), C.c_int]
+    pbuf = (C.c_uint64 * (4096 * 2))()
+    pfn(pbuf, a.batch)
+    pt = np.frombuffer(pbuf, dtype=np.uint64).reshape(4096, 2)[:a.batch].astype(np.int64)
     tr = tr[tr[:, 0] > 0]
     # keep the CTAs of the last launch (start within 1 ms of the latest start)
     tr = tr[tr[:, 0] > tr[:, 0].max() - 1_000_000]
@@ -77,6 +82,11 @@ for name, io in cases:
     def q(v):
         return f"min {v.min():6.2f} med {np.median(v):6.2f} max {v.max():6.2f}"
     print(f"{name:8s} ctas {len(tr)}  span {span:6.2f} us  passes {tr[:, 7].max()}")
+    p0 = pt[:, 0].min()
+    print(f"   prep: blocks {len(pt)}  span {(pt[:, 1].max() - p0) / 1e3:6.2f} us  block "
+          f"{np.median((pt[:, 1] - pt[:, 0]) / 1e3):5.2f} us med; contraction CTAs start "
+          f"{(t0 - p0) / 1e3:+6.2f} us after prep, first stage "
+          f"{(tr[:, 1].min() - pt[:, 1].max()) / 1e3:+6.2f} us after prep's end")
     if tr[:, 7].max() > 1:
         print(f"   pass 0 done -> barrier 1 {q((tr[:, 8] - tr[:, 2]) / 1e3)}")
         print(f"   re-issued samples (pass 1) {tr[:, 15].max()}")
