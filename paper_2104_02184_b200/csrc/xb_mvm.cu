@@ -21,11 +21,11 @@
 
 #ifdef XB_TC_TRACE
 // experiment builds only: globaltimer at the start and end of every prep block
-__device__ unsigned long long g_prep_trace[4096][2];
+__device__ unsigned long long g_prep_trace[4096][4];
 extern "C" __attribute__((visibility("default"))) int xb_debug_prep_trace(unsigned long long *out,
                                                                             int n) {
   return (int)cudaMemcpyFromSymbol(out, g_prep_trace,
-                                   sizeof(unsigned long long) * 2 * (size_t)(n < 4096 ? n : 4096));
+                                   sizeof(unsigned long long) * 4 * (size_t)(n < 4096 ? n : 4096));
 }
 __device__ __forceinline__ void prep_stamp(int k) {
   unsigned long long v;
@@ -88,10 +88,12 @@ __global__ void __launch_bounds__(PREP_THREADS) prep_kernel(
   } else if (!amax_in) {
     for (int j = threadIdx.x; j < n; j += blockDim.x) m = fmaxf(m, fabsf(x[j]));
   }
+  prep_stamp(2);
   if (amax_in)
     m = amax_in[b];
   else
     m = block_max(m, red);
+  prep_stamp(3);
   SampleState s;
   s.alpha = (m == 0.f) ? 0.f : (io.nm_absmax ? m : 1.f);
   s.m = 0;
@@ -353,9 +355,9 @@ __global__ void __launch_bounds__(GF_THREADS) gemv_fused_fwd_kernel(
     for (int b = 0; b < NB; ++b) {
       const double inv = st[b].alpha == 0.f ? 0.0 : 1.0 / (double)st[b].alpha;
       const bool fast = !io.perfect && st[b].alpha != 0.f;
-      const float a32 = fast ? (float)(inv * exp2((double)io.dac.bits) / (2.0 * io.dac.bound)) : 0.f;
+      const float a32 = fast ? (float)(inv * pow2i(io.dac.bits) / (2.0 * io.dac.bound)) : 0.f;
       const float c032 = 0.5f * io.dac.flevels_m1;
-      const float tie_eps = fast ? ldexpf(1.f, io.dac.bits - 20) : 0.f;
+      const float tie_eps = fast ? __int_as_float((127 + io.dac.bits - 20) << 23) /* 2^(bits-20) */ : 0.f;
       for (int k = threadIdx.x; k < n; k += GF_THREADS) {
         const float xv = X[(size_t)b * ldx + kc + k];
         float f;

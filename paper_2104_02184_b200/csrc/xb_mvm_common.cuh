@@ -169,9 +169,9 @@ struct RowDac {
     // the DAC was fp64-conversion bound (~4 us per 4096-wide sample on B200).
     fast = !io.perfect && s.alpha != 0.f && io.dac.bits > 0 && io.dac.bits <= 16 && io.dac.pow2 &&
            io.sigma_inp == 0.0;
-    a32 = fast ? (float)(inv * exp2((double)io.dac.bits) / (2.0 * io.dac.bound)) : 0.f;
+    a32 = fast ? (float)(inv * pow2i(io.dac.bits) / (2.0 * io.dac.bound)) : 0.f;
     c032 = 0.5f * (io.dac.flevels_m1); // (L - 1) / 2, exact
-    tie_eps = fast ? ldexpf(1.f, io.dac.bits - 20) : 0.f;
+    tie_eps = fast ? __int_as_float((127 + io.dac.bits - 20) << 23) /* 2^(bits-20) */ : 0.f;
   }
   __device__ __forceinline__ float operator()(float xv, int j, const SampleState &s,
                                               const IoDev &io, Key key, uint64_t seq,

@@ -62,9 +62,9 @@ for name, io in cases:
     tr = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 16).astype(np.int64)
     pfn = lib.xb_debug_prep_trace
     pfn.argtypes = [C.POINTER(C.c_uint64), C.c_int]
-    pbuf = (C.c_uint64 * (4096 * 2))()
+    pbuf = (C.c_uint64 * (4096 * 4))()
     pfn(pbuf, a.batch)
-    pt = np.frombuffer(pbuf, dtype=np.uint64).reshape(4096, 2)[:a.batch].astype(np.int64)
+    pt = np.frombuffer(pbuf, dtype=np.uint64).reshape(4096, 4)[:a.batch].astype(np.int64)
     tr = tr[tr[:, 0] > 0]
     # keep the CTAs of the last launch (start within 1 ms of the latest start)
     tr = tr[tr[:, 0] > tr[:, 0].max() - 1_000_000]
@@ -87,6 +87,10 @@ for name, io in cases:
           f"{np.median((pt[:, 1] - pt[:, 0]) / 1e3):5.2f} us med; contraction CTAs start "
           f"{(t0 - p0) / 1e3:+6.2f} us after prep, first stage "
           f"{(tr[:, 1].min() - pt[:, 1].max()) / 1e3:+6.2f} us after prep's end")
+    print(f"   prep block phases (med): loads {np.median(pt[:, 2] - pt[:, 0]) / 1e3:5.2f}  "
+          f"block max {np.median(pt[:, 3] - pt[:, 2]) / 1e3:5.2f}  DAC + norm "
+          f"{np.median(pt[:, 1] - pt[:, 3]) / 1e3:5.2f} us; block starts spread "
+          f"{(pt[:, 0].max() - p0) / 1e3:5.2f} us")
     if tr[:, 7].max() > 1:
         print(f"   pass 0 done -> barrier 1 {q((tr[:, 8] - tr[:, 2]) / 1e3)}")
         print(f"   re-issued samples (pass 1) {tr[:, 15].max()}")
