@@ -40,12 +40,45 @@ det = xb.TileSettings(device=xb.device_preset("reram_sb"))
 det.update.pulse_type = xb.PULSE_DETERMINISTIC
 td = xb.AnalogTile(R, C, det, 1)
 td.update(X, D, 0.05)
-for mode in ("0", "1"):
-    os.environ["XB_TC_PAIR"] = mode
-    t = xb.AnalogTile(300, 260, xb.TileSettings(mvm_precision=xb.MVM_TF32), 2)
-    t.forward(rng.uniform(-1, 1, (48, 260)).astype(np.float32))
-    t.backward(rng.uniform(-1, 1, (48, 300)).astype(np.float32))
-os.environ["XB_TC_PAIR"] = "0"
+# tcgen05 at odd sizes; the in-kernel bound-management loop (prestaged m = 1
+# slab) and the host-driven re-issue passes on a workload that saturates
+t = xb.AnalogTile(300, 260, xb.TileSettings(mvm_precision=xb.MVM_TF32), 2)
+t.forward(rng.uniform(-1, 1, (48, 260)).astype(np.float32))
+t.backward(rng.uniform(-1, 1, (48, 300)).astype(np.float32))
+bio = xb.default_io()
+bio.bound_management = xb.BM_ITERATIVE
+dev = xb.default_device()
+dev.w_max, dev.w_min = 1.0, -1.0
+Wb = rng.uniform(-0.9, 0.9, (256, 512)).astype(np.float32)
+Xb = rng.uniform(-1, 1, (300, 512)).astype(np.float32)
+for host in ("0", "1"):
+    os.environ["XB_BM_HOST_PASSES"] = host
+    for prec in (xb.MVM_TF32, xb.MVM_TF32X3):
+        t = xb.AnalogTile(256, 512, xb.TileSettings(device=dev, forward_io=bio, backward_io=bio,
+                                                    mvm_precision=prec), 4)
+        t.set_weights(Wb)
+        t.forward(Xb)
+os.environ["XB_BM_HOST_PASSES"] = "0"
+# per-sample paths: fused B <= 2, GEMV B <= 15 (forward and backward)
+for prec in (xb.MVM_FP32, xb.MVM_TF32X3):
+    t = xb.AnalogTile(R, C, xb.TileSettings(device=xb.device_preset("reram_sb"),
+                                            mvm_precision=prec), 8)
+    t.set_weights(W)
+    for b in (1, 2, 5):
+        t.forward(X[:b])
+        t.backward(D[:b])
+        t.update(X[:b], D[:b], 0.05)
+# row shards: split-phase backward
+import torch  # noqa: E402
+sh = [xb.AnalogTile(R, C, xb.TileSettings(), 9, shard=(0, 96)),
+      xb.AnalogTile(R, C, xb.TileSettings(), 9, shard=(96, R))]
+Dt = torch.from_numpy(D).cuda()
+amax = torch.maximum(sh[0].rows_amax(Dt[:, :96].contiguous()), sh[1].rows_amax(Dt[:, 96:].contiguous()))
+P = [s_.backward_partial_dev(Dt[:, a:b].contiguous(), amax) for s_, (a, b) in zip(sh, ((0, 96), (96, R)))]
+torch.cuda.synchronize()
+G = torch.empty(B, C, device="cuda")
+sh[0].backward_finish_dev(P[0] + P[1], amax, G)
+torch.cuda.synchronize()
 tr = xb.TransferSettings()
 tr.fast_device = xb.device_preset("reram_sb")
 tr.slow_device = xb.device_preset("reram_sb")
