@@ -141,10 +141,10 @@ __device__ __forceinline__ void bm_flag(bool hit, const SampleState &s, const Io
 }
 
 // Bound-management bookkeeping, per N slab of nb samples (slab-local sample
-// index b - n0):  pass p writes its saturation flags to flags[(p & 1) nb ..]
-// and counts them in counts[p]; the re-issue of pass p + 1 takes the flagged
-// samples of pass p (ascending order), and clears the other parity's flags
-// for pass p + 1 to write.
+// index b - n0):  pass p writes its saturation flags to flags[(p & 1) nb ..];
+// the re-issue of pass p + 1 takes the flagged samples of pass p (ascending
+// order, compacted -- their number lands in counts[32 + p] on the
+// host-driven route), and clears the other parity's flags for pass p + 1.
 // words per N slab (<= 256 samples): flags [2][256], counts [64]
 constexpr int BM_SLAB_WORDS = 2 * 256 + 64;
 struct BmBufs {
