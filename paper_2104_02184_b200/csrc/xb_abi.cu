@@ -1117,6 +1117,7 @@ int xb_tile_attach_comm(xb_tile *h, xb_comm *c) {
     Collective *col = comm_of(c);
     if (col && t.R == t.R_total && col->size() > 1)
       raise("attach_comm: the tile is not row-sharded (create it with an xb_shard)");
+    if (col) col->bind(t.device);
     t.comm = col;
   });
 }

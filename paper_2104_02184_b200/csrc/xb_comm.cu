@@ -34,6 +34,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <utility>
 #include <vector>
 
 #include <nccl.h>
@@ -126,6 +127,7 @@ struct LocalGroup {
   int arrived = 0;
   uint64_t gen = 0;
   std::vector<void *> bufs;
+  std::vector<int> devs; // each member's device once bound (-1 before)
   std::vector<cudaEvent_t> ready, done;
   ~LocalGroup() {
     for (cudaEvent_t e : ready)
@@ -153,6 +155,31 @@ struct LocalCollective : Collective {
   std::shared_ptr<LocalGroup> g;
   int r = 0;
   Scratch tmp, ptrs;
+  // members on other devices: each rank's reduction kernel reads every
+  // member's buffer directly, so peer access is enabled both ways when a
+  // member binds (before any collective: a failure here cannot strand peers
+  // at a rendezvous)
+  void bind(int device) override {
+    std::lock_guard<std::mutex> lk(g->m);
+    for (int q = 0; q < g->P; ++q) {
+      const int other = g->devs[q];
+      if (q == r || other < 0 || other == device) continue;
+      for (const auto &[from, to] : {std::pair<int, int>{device, other}, {other, device}}) {
+        int can = 0;
+        XB_CUDA(cudaDeviceCanAccessPeer(&can, from, to));
+        if (!can)
+          raise("comm: loopback group members on devices " + std::to_string(from) + " and " +
+                std::to_string(to) + " without peer access; use an NCCL communicator");
+        DevScope ds(from);
+        const cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled)
+          cudaGetLastError();
+        else
+          XB_CUDA(e);
+      }
+    }
+    g->devs[r] = device;
+  }
   int size() const override { return g->P; }
   int rank() const override { return r; }
 
@@ -241,6 +268,7 @@ int xb_comm_create_local(int nranks, xb_comm **out) {
     auto g = std::make_shared<LocalGroup>();
     g->P = nranks;
     g->bufs.assign(nranks, nullptr);
+    g->devs.assign(nranks, -1);
     g->ready.assign(nranks, nullptr);
     g->done.assign(nranks, nullptr);
     for (int r = 0; r < nranks; ++r) {

@@ -94,6 +94,9 @@ struct Collective {
   virtual void allreduce_max_i32(int *buf, size_t n, cudaStream_t s) = 0;
   virtual void allreduce_max_f32(float *buf, size_t n, cudaStream_t s) = 0;
   virtual void allreduce_sum_f32(float *buf, size_t n, cudaStream_t s) = 0;
+  // the device of this rank's tile, told once when the tile attaches (not a
+  // collective, so it may raise: every cross-member check happens here)
+  virtual void bind(int device) { (void)device; }
 };
 
 // makes `dev` current for the scope of one ABI call on a tile (a handle keeps
