@@ -271,7 +271,7 @@ class AnalogTile:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _lib is not None:  # (module globals are gone at interpreter exit)
             _lib.xb_tile_destroy(h)
             self._h = None
 
@@ -507,7 +507,8 @@ class TransferTile:
             for m in (getattr(self, "_fast", None), getattr(self, "_slow", None)):
                 if m is not None:
                     m._h = None
-            _lib.xb_transfer_destroy(h)
+            if _lib is not None:
+                _lib.xb_transfer_destroy(h)
             self._h = None
 
     def d_out(self) -> int:
@@ -598,7 +599,8 @@ class UnitCellTile:
         if h:
             for m in getattr(self, "_members", []):
                 m._h = None  # owned by the compound
-            _lib.xb_unitcell_destroy(h)
+            if _lib is not None:
+                _lib.xb_unitcell_destroy(h)
             self._h = None
 
     def d_out(self) -> int:
