@@ -233,6 +233,7 @@ static void tile_free(Tile &t) {
   if (t.bm_count) cudaFreeHost(t.bm_count);
   if (t.chk_host) cudaFreeHost(t.chk_host);
   if (t.lr_pin) cudaFreeHost(t.lr_pin);
+  if (t.io_pin) cudaFreeHost(t.io_pin);
   if (t.lr_ev) cudaEventDestroy(t.lr_ev);
   for (cudaEvent_t e : t.side_ev) cudaEventDestroy(e);
   if (t.side) cudaStreamDestroy(t.side);
@@ -240,6 +241,43 @@ static void tile_free(Tile &t) {
 }
 
 static void sync(Tile &t) { XB_CUDA(cudaStreamSynchronize(t.stream)); }
+
+// Small host-buffer calls -- the per-sample reference API -- stage their
+// inputs and outputs through one pinned buffer per tile: a pageable copy
+// costs the driver a staging pass and several microseconds more latency each
+// way, a pinned one is a plain DMA.  Every host-buffer entry synchronises
+// the tile's stream before it returns, so the buffer is free at the next call.
+constexpr size_t kPinStageMax = size_t(1) << 18; // floats per call (1 MB)
+
+static float *io_stage(Tile &t, size_t n) {
+  if (n == 0 || n > kPinStageMax) return nullptr;
+  if (t.io_pin_n < n) {
+    if (t.io_pin) XB_CUDA(cudaFreeHost(t.io_pin));
+    t.io_pin = nullptr;
+    t.io_pin_n = 0;
+    const size_t want = std::max<size_t>(n, 8192);
+    XB_CUDA(cudaMallocHost(&t.io_pin, want * sizeof(float)));
+    t.io_pin_n = want;
+  }
+  return t.io_pin;
+}
+
+// host -> device of n floats, through `pin` (a slot of io_stage) when given
+static void h2d(Tile &t, float *dst, const float *src, size_t n, float *pin) {
+  if (pin) {
+    std::memcpy(pin, src, n * sizeof(float));
+    src = pin;
+  }
+  XB_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(float), cudaMemcpyHostToDevice, t.stream));
+}
+
+// device -> host of n floats and the stream sync that ends a host-buffer call
+static void d2h_sync(Tile &t, float *dst, const float *src, size_t n, float *pin) {
+  XB_CUDA(cudaMemcpyAsync(pin ? pin : dst, src, n * sizeof(float), cudaMemcpyDeviceToHost,
+                          t.stream));
+  sync(t);
+  if (pin) std::memcpy(dst, pin, n * sizeof(float));
+}
 
 // check_input's finiteness test (tile.cpp:65-75) on the inputs after their
 // H2D copy: one streaming kernel per array on the tile's stream, then one
@@ -847,11 +885,12 @@ static void forward_host(xb_tile *h, const float *X, int B, float *Y, const xb_i
   float *dX = scratch_as<float>(t.s_y, (size_t)B * (t.C + t.R));
   float *dY = dX + (size_t)B * t.C;
   const bool checked = !check || host_check_small({{X, (size_t)B * t.C, "forward"}});
-  XB_CUDA(cudaMemcpyAsync(dX, X, sizeof(float) * B * t.C, cudaMemcpyHostToDevice, t.stream));
-  if (!checked) check_finite_dev(t, {{dX, (size_t)B * t.C, "forward"}});
+  const size_t nx = (size_t)B * t.C, ny = (size_t)B * t.R;
+  float *pin = io_stage(t, nx + ny);
+  h2d(t, dX, X, nx, pin);
+  if (!checked) check_finite_dev(t, {{dX, nx, "forward"}});
   forward_device(t, dX, B, dY, io);
-  XB_CUDA(cudaMemcpyAsync(Y, dY, sizeof(float) * B * t.R, cudaMemcpyDeviceToHost, t.stream));
-  sync(t);
+  d2h_sync(t, Y, dY, ny, pin ? pin + nx : nullptr);
 }
 
 int xb_tile_forward(xb_tile *h, const float *X, int B, float *Y) {
@@ -942,19 +981,19 @@ static void backward_host(xb_tile *h, const float *D, int B, float *G, bool chec
                       : scratch_as<float>(t.s_y, (size_t)B * (t.C + t.R));
   float *dG = dD + (size_t)B * t.R;
   const bool checked = !check || host_check_small({{D, (size_t)B * t.R, "backward"}});
-  XB_CUDA(cudaMemcpyAsync(dD, D, sizeof(float) * B * t.R, cudaMemcpyHostToDevice, t.stream));
-  if (!checked) check_finite_dev(t, {{dD, (size_t)B * t.R, "backward"}});
+  const size_t nd = (size_t)B * t.R, ng = (size_t)B * t.C;
+  float *pin = io_stage(t, nd + ng);
+  h2d(t, dD, D, nd, pin);
+  if (!checked) check_finite_dev(t, {{dD, nd, "backward"}});
   if (sharded) {
     backward_sharded(t, dD, B, dG);
-    XB_CUDA(cudaMemcpyAsync(G, dG, sizeof(float) * B * t.C, cudaMemcpyDeviceToHost, t.stream));
-    sync(t);
+    d2h_sync(t, G, dG, ng, pin ? pin + nd : nullptr);
     return;
   }
   mvm_backward(t, dD, B, dG, make_io(t.cfg.backward_io), t.k_bwd, t.seq_bwd, nullptr, false,
                nullptr);
   t.seq_bwd += (uint64_t)B;
-  XB_CUDA(cudaMemcpyAsync(G, dG, sizeof(float) * B * t.C, cudaMemcpyDeviceToHost, t.stream));
-  sync(t);
+  d2h_sync(t, G, dG, ng, pin ? pin + nd : nullptr);
 }
 
 int xb_tile_backward(xb_tile *h, const float *D, int B, float *G) {
@@ -1017,8 +1056,10 @@ int xb_tile_update(xb_tile *h, const float *X, const float *D, int B, const doub
     const bool small =
         host_check_small({{X, (size_t)B * t.C, "update(x)"}, {D, (size_t)B * t.R, "update(d)"}});
     if (small) check_lr_host(X, D, B, t.C, t.R, lr, t.learning_rate);
-    XB_CUDA(cudaMemcpyAsync(dX, X, sizeof(float) * B * t.C, cudaMemcpyHostToDevice, t.stream));
-    XB_CUDA(cudaMemcpyAsync(dD, D, sizeof(float) * B * t.R, cudaMemcpyHostToDevice, t.stream));
+    const size_t nx = (size_t)B * t.C, nd = (size_t)B * t.R;
+    float *pin = io_stage(t, nx + nd);
+    h2d(t, dX, X, nx, pin);
+    h2d(t, dD, D, nd, pin ? pin + nx : nullptr);
     if (small) {
       update_device(t, dX, dD, B, lr, nullptr, false, nullptr, nullptr, nullptr);
       sync(t);

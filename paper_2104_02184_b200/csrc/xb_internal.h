@@ -154,6 +154,8 @@ struct Tile {
   int *bm_count = nullptr; // pinned host word for the bound-management loop
   int *chk_dev = nullptr;  // input-check flag word (device) and its pinned host copy
   int *chk_host = nullptr;
+  float *io_pin = nullptr;  // pinned staging of small host-buffer calls (inputs, then outputs)
+  size_t io_pin_n = 0;      // floats
   double *lr_pin = nullptr; // pinned staging of per-sample learning rates
   size_t lr_pin_n = 0;
   cudaEvent_t lr_ev = nullptr; // last lr copy out of lr_pin
