@@ -722,8 +722,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // 2-D fp32 tensor map over a row-major [rows][cols] array with row stride ld
 // floats; box = [box_rows][32 floats], 128-byte swizzle (16- or 32-byte
 // granule), OOB zero fill
-CUtensorMap make_map(const float *base, int rows, int cols, int ld, int box_rows,
-                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+CUtensorMap encode_map(const float *base, int rows, int cols, int ld, int box_rows,
+                       CUtensorMapSwizzle swz) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
@@ -735,6 +735,39 @@ CUtensorMap make_map(const float *base, int rows, int cols, int ld, int box_rows
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) raise("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return m;
+}
+
+// A launch needs up to four maps and a call re-uses the same tile and
+// scratch buffers, so the encodings (a driver call each) are kept in a small
+// per-thread cache keyed by every argument: a hit is the same 128-byte map.
+CUtensorMap make_map(const float *base, int rows, int cols, int ld, int box_rows,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+  struct Entry {
+    const float *base;
+    int rows, cols, ld, box;
+    CUtensorMapSwizzle swz;
+    CUtensorMap map;
+  };
+  constexpr int N = 16;
+  thread_local Entry cache[N];
+  thread_local int used = 0, next = 0;
+  for (int i = 0; i < used; ++i) {
+    const Entry &e = cache[i];
+    if (e.base == base && e.rows == rows && e.cols == cols && e.ld == ld && e.box == box_rows &&
+        e.swz == swz)
+      return e.map;
+  }
+  Entry &e = cache[next];
+  e.map = encode_map(base, rows, cols, ld, box_rows, swz);
+  e.base = base;
+  e.rows = rows;
+  e.cols = cols;
+  e.ld = ld;
+  e.box = box_rows;
+  e.swz = swz;
+  next = (next + 1) % N;
+  used = used < N ? used + 1 : N;
+  return e.map;
 }
 
 } // namespace

@@ -185,10 +185,23 @@ def _out(out, shape) -> np.ndarray:
     return out
 
 
+_LR_CACHE = {}
+
+
 def _lr_array(lr, B: int):
     if lr is None:
         return None
     # the reference takes double lr (proj/include/xbarsim/tile.hpp:84); no narrowing
+    if np.ndim(lr) == 0:  # a scalar: the same B-vector every call (kept, read-only)
+        key = (float(lr), B)
+        hit = _LR_CACHE.get(key)
+        if hit is None:
+            if len(_LR_CACHE) > 64:
+                _LR_CACHE.clear()
+            arr = np.full(B, float(lr), dtype=np.float64)
+            arr.setflags(write=False)
+            hit = _LR_CACHE[key] = (arr.ctypes.data_as(_dp), arr)
+        return hit
     arr = np.ascontiguousarray(np.broadcast_to(np.asarray(lr, dtype=np.float64), (B,)))
     return arr.ctypes.data_as(_dp), arr
 

@@ -210,24 +210,28 @@ def cfg2(args, stream):
     X = torch.rand(B, 784, device="cuda", generator=g)
     labels = torch.randint(0, 10, (B,), device="cuda", generator=g)
     acts = [X] + [torch.empty(B, n, device="cuda") for n in sizes[1:]]
+    # the step's glue (activations, loss gradient, scaling) as few torch ops
+    # on preallocated buffers: the step is enqueue-bound, not GPU-bound
+    onehot = torch.zeros(B, 10, device="cuda")
+    onehot[torch.arange(B, device="cuda"), labels] = 1.0
+    gins = [None] + [torch.empty(B, sizes[k], device="cuda") for k in (1, 2)]
+    deltas = [torch.empty(B, sizes[k + 1], device="cuda") for k in range(3)]
+    slope = [None] + [torch.empty(B, sizes[k], device="cuda") for k in (1, 2)]
+    upd = [torch.empty(B, sizes[k + 1], device="cuda") for k in range(3)]
 
     def step():
         for k, t in enumerate(tiles):           # forward (sigmoid hidden, logits out)
             t.forward_dev(acts[k], acts[k + 1])
             if k < 2:
-                acts[k + 1].sigmoid_()
-        p = torch.softmax(acts[3], dim=1)
-        delta = p
-        delta[torch.arange(B, device="cuda"), labels] -= 1.0
-        deltas = [None, None, None]
-        deltas[2] = delta.contiguous()
+                torch.sigmoid(acts[k + 1], out=acts[k + 1])
+        torch.sub(torch.softmax(acts[3], dim=1), onehot, out=deltas[2])  # softmax CE grad
         for k in (2, 1):                         # backward through the tiles
-            gin = torch.empty(B, sizes[k], device="cuda")
-            tiles[k].backward_dev(deltas[k], gin)
-            a = acts[k]
-            deltas[k - 1] = (gin * a * (1 - a)).contiguous()
+            tiles[k].backward_dev(deltas[k], gins[k])
+            torch.addcmul(acts[k], acts[k], acts[k], value=-1.0, out=slope[k])  # a (1 - a)
+            torch.mul(gins[k], slope[k], out=deltas[k - 1])
         for k in range(3):                       # pulsed updates, d = -grad / B
-            tiles[k].update_dev(acts[k], (-deltas[k] / B).contiguous(), lr)
+            torch.mul(deltas[k], -1.0 / B, out=upd[k])
+            tiles[k].update_dev(acts[k], upd[k], lr)
     ms = ev_time(step, 50, stream)
     nl = launches_in(step)
     cells = sum(sizes[k] * sizes[k + 1] for k in range(3)) * B
