@@ -440,13 +440,14 @@ static void update_device(Tile &t, const float *dX, const float *dD, int B, cons
   const double *lr_d = upload_lr(t, u.lr, lr, B, &lr_s);
   {
     PhaseTimer pt(t, XB_TIMER_TRAINS);
-    launch_rows_amax(dX, B, t.C, t.C, u.xm, t.stream);
     const float *dm = dAmaxD;
     if (!dm) {
-      launch_rows_amax(dD, B, t.R, t.R, u.dm, t.stream);
+      launch_rows_amax2(dX, t.C, u.xm, dD, t.R, u.dm, B, t.stream);
       // row shard: translate needs max|d| over the whole tile (pulsed.cpp:34-51)
       if (t.comm) t.comm->allreduce_max_f32(u.dm, (size_t)B, t.stream);
       dm = u.dm;
+    } else {
+      launch_rows_amax(dX, B, t.C, t.C, u.xm, t.stream);
     }
     launch_trains(t, dX, dD, B, lr_d, lr_s, u.xm, dm, t.seq_upd, u.xw, u.dw, train_ld(B), u.bl,
                   u.px, u.pd, det);
@@ -1587,8 +1588,7 @@ static void uc_update(xb_unitcell *u, const float *X, const float *D, int B, con
   XB_CUDA(cudaMemcpyAsync(ub.lr, lre.data(), sizeof(double) * B, cudaMemcpyHostToDevice, e.stream));
   XB_CUDA(cudaMemcpyAsync(dG, grain.data(), sizeof(double) * B, cudaMemcpyHostToDevice,
                           e.stream));
-  launch_rows_amax(dX, B, e.C, e.C, ub.xm, e.stream);
-  launch_rows_amax(dD, B, e.R, e.R, ub.dm, e.stream);
+  launch_rows_amax2(dX, e.C, ub.xm, dD, e.R, ub.dm, B, e.stream);
   launch_trains(e, dX, dD, B, ub.lr, 0.0, ub.xm, ub.dm, e.seq_upd, ub.xw, ub.dw, ldb, ub.bl,
                 nullptr, nullptr, false, dG);
   e.seq_upd += (uint64_t)B;

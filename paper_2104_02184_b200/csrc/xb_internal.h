@@ -182,6 +182,9 @@ Collective *comm_of(xb_comm *c);
 
 // ---- kernel launchers (xb_update.cu) ----
 void launch_rows_amax(const float *V, int B, int n, int ld, float *out, cudaStream_t s);
+// the x and d maxima of an update (rows of length nx and nd) in one launch
+void launch_rows_amax2(const float *X, int nx, float *xm, const float *D, int nd, float *dm, int B,
+                       cudaStream_t s);
 // per-sample translate + Bernoulli trains; writes packed words and bl[B]
 void launch_trains(const Tile &t, const float *X, const float *D, int B, const double *lr_dev,
                    double lr_scalar, const float *xm, const float *dm, uint64_t seq0,

@@ -28,9 +28,21 @@ namespace xb {
 // one CTA per sample row; 16-byte loads (when the row allows them), four in
 // flight per thread, so the pass streams at HBM rate instead of waiting on
 // one dependent load per iteration
+// blocks [0, nb1) take rows of V (length n, stride ld) into out; blocks
+// [nb1, gridDim.x) rows of V2 (n2, ld2) into out2 -- the x and d maxima of an
+// update in one launch
 __global__ void __launch_bounds__(256) rows_amax_kernel(const float *__restrict__ V, int n, int ld,
-                                                        float *__restrict__ out) {
-  const int b = blockIdx.x;
+                                                        float *__restrict__ out, int nb1,
+                                                        const float *__restrict__ V2, int n2,
+                                                        int ld2, float *__restrict__ out2) {
+  int b = blockIdx.x;
+  if (b >= nb1) {
+    b -= nb1;
+    V = V2;
+    n = n2;
+    ld = ld2;
+    out = out2;
+  }
   const float *row = V + (size_t)b * ld;
   float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
   int head = 0;
@@ -66,7 +78,15 @@ __global__ void __launch_bounds__(256) rows_amax_kernel(const float *__restrict_
 
 void launch_rows_amax(const float *V, int B, int n, int ld, float *out, cudaStream_t s) {
   if (B <= 0) return;
-  rows_amax_kernel<<<B, 256, 0, s>>>(V, n, ld, out);
+  rows_amax_kernel<<<B, 256, 0, s>>>(V, n, ld, out, B, nullptr, 0, 0, nullptr);
+  count_launch();
+  XB_CUDA(cudaGetLastError());
+}
+
+void launch_rows_amax2(const float *X, int nx, float *xm, const float *D, int nd, float *dm, int B,
+                       cudaStream_t s) {
+  if (B <= 0) return;
+  rows_amax_kernel<<<2 * B, 256, 0, s>>>(X, nx, nx, xm, B, D, nd, nd, dm);
   count_launch();
   XB_CUDA(cudaGetLastError());
 }
