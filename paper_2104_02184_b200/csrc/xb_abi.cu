@@ -238,6 +238,7 @@ static void tile_free(Tile &t) {
   for (cudaEvent_t e : t.side_ev) cudaEventDestroy(e);
   if (t.side) cudaStreamDestroy(t.side);
   cudaFree(t.chk_dev);
+  cudaFree(t.pulse_ctr);
 }
 
 static void sync(Tile &t) { XB_CUDA(cudaStreamSynchronize(t.stream)); }

@@ -152,6 +152,7 @@ struct Tile {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int *bm_count = nullptr; // pinned host word for the bound-management loop
+  unsigned *pulse_ctr = nullptr; // pulse kernel's tail work queue {next ticket, warps done}; zero between launches
   int *chk_dev = nullptr;  // input-check flag word (device) and its pinned host copy
   int *chk_host = nullptr;
   float *io_pin = nullptr;  // pinned staging of small host-buffer calls (inputs, then outputs)

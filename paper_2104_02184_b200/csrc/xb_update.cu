@@ -506,7 +506,8 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
     int C,
     const uint32_t *__restrict__ xw, const uint32_t *__restrict__ dw, int ldb, int B, int row0,
     LawArgs la, RoundKeys rk, uint32_t call, uint32_t two, uint32_t flip,
-    const int *__restrict__ abort_flag, uint32_t cb0, uint32_t ncb_run) {
+    const int *__restrict__ abort_flag, uint32_t cb0, uint32_t ncb_run,
+    unsigned *__restrict__ ctr) {
   extern __shared__ uint32_t qsm[]; // [PULSE_WARPS][PULSE_QW][32] streams, then the angle table
   if (abort_flag && *abort_flag) return; // rejected input: the tile stays untouched
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -529,9 +530,35 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
   // the pulse loop of others.
   // items of the column blocks [cb0, cb0 + ncb_run) only (a one-hot x, e.g.
   // a Tiki-Taka transfer, has no coincidences anywhere else)
+  // The last XB_PULSE_DYN_ROUNDS rounds are handed out from a work queue
+  // instead (ctr[0]: next ticket): items differ in cost (the longest stream
+  // of a row decides) and warps drift, so a static stride ends on its slowest
+  // warps.  Measured on the NS update: 5.40 ms static, 5.32 with one queued
+  // round, 5.27 with 4-16, 5.28 fully queued (the static part keeps the
+  // CTA's warps on one column block).  The warp that retires last resets the
+  // queue for the next launch on the stream.
   const uint32_t n_items = (uint32_t)R * ncb_run; // < 2^31 for any tile that fits
-  for (uint32_t item = blockIdx.x * PULSE_WARPS + warp; item < n_items;
-       item += gridDim.x * PULSE_WARPS) {
+  const uint32_t nwarps = gridDim.x * PULSE_WARPS;
+  const uint32_t rounds = n_items / nwarps;
+#ifndef XB_PULSE_DYN_ROUNDS
+#define XB_PULSE_DYN_ROUNDS 8
+#endif
+  const uint32_t dyn0 = (rounds > XB_PULSE_DYN_ROUNDS ? rounds - XB_PULSE_DYN_ROUNDS : 0) * nwarps;
+  uint32_t item = blockIdx.x * PULSE_WARPS + warp;
+  for (;;) {
+    if (item >= dyn0) { // queued part: one ticket per warp per item
+      uint32_t tk = 0;
+      if (lane == 0) tk = atomicAdd(ctr, 1u);
+      item = dyn0 + __shfl_sync(0xffffffffu, tk, 0);
+    }
+    if (item >= n_items) {
+      if (lane == 0 && atomicAdd(ctr + 1, 1u) == nwarps - 1) {
+        ctr[0] = 0u; // every warp has drawn its last ticket: reset for the next launch
+        ctr[1] = 0u;
+      }
+      break;
+    }
+    {
   const uint32_t cb = cb0 + item / (uint32_t)R;
   const int i = (int)(item - (cb - cb0) * (uint32_t)R);
   const int j = (int)cb * 32 + lane;
@@ -753,6 +780,8 @@ __global__ void __launch_bounds__(PULSE_WARPS * 32, XB_PULSE_CTAS) pulse_kernel(
   if (COMP) renorm2(w, wlo);
   if (valid) W[idx] = w;
   if (COMP && valid) Wlo[idx] = wlo;
+    }
+    item += nwarps; // static part: stride of the whole grid
   }
 }
 
@@ -778,10 +807,14 @@ static void pulse_dispatch(Tile &t, const uint32_t *xw, const uint32_t *dw, int 
   const uint32_t ncb_run = col >= 0 ? 1u : (uint32_t)((t.C + 31) / 32);
   const long items = (long)t.R * ncb_run;
   const dim3 grid((unsigned)std::min<long>(blocks, (items + PULSE_WARPS - 1) / PULSE_WARPS));
+  if (!t.pulse_ctr) {
+    XB_CUDA(cudaMalloc(&t.pulse_ctr, 2 * sizeof(unsigned)));
+    XB_CUDA(cudaMemsetAsync(t.pulse_ctr, 0, 2 * sizeof(unsigned), t.stream));
+  }
   pulse_kernel<LAW, NOISE, COMP><<<grid, PULSE_WARPS * 32, smem, t.stream>>>(
       t.W, t.Wlo, t.steps(), t.bounds(), t.ld, t.R, t.C, xw, dw, ldb, B, t.row0, la,
       round_keys(t.k_c2c), call, 2u,
-      flip ? 0x80000000u : 0u, t.abort_flag, cb0, ncb_run);
+      flip ? 0x80000000u : 0u, t.abort_flag, cb0, ncb_run, t.pulse_ctr);
   count_launch();
   XB_CUDA(cudaGetLastError());
 }
