@@ -162,6 +162,10 @@ const char *xb_last_error(void);
 int xb_device_check(void);
 /* kernel launches issued by this library since load (process-wide) */
 uint64_t xb_launch_count(void);
+/* measurement helper: device time per launch of n empty kernels issued back
+ * to back from C on a fresh stream (best of `reps`), in microseconds -- the
+ * launch-latency floor of a step whose work is too small to fill the GPU */
+int xb_launch_floor_us(int n, int reps, double *us_per_launch);
 
 /* defaults: the reference's struct initialisers */
 void xb_default_device(xb_device_params *p);

@@ -14,13 +14,14 @@ from ._abi import (BM_ITERATIVE, BM_NONE, CONSTANT_STEP, EXP_STEP, LINEAR_STEP, 
                    UnitCellConfig, UpdateParams)
 from .tile import (AnalogTile, Comm, Error, InferenceNoiseModel, TileSettings, TransferSettings,
                    TransferTile, UnitCellSettings, UnitCellTile, default_device, default_io,
-                   device_check, device_preset, io_off, launch_count, perfect_io, rows_amax_dev)
+                   device_check, device_preset, io_off, launch_count, launch_floor_us, perfect_io,
+                   rows_amax_dev)
 
 __all__ = [
     "AnalogTile", "TransferTile", "TileSettings", "TransferSettings", "InferenceNoiseModel",
     "DeviceParams", "IOParams", "UpdateParams", "TemporalParams", "TileConfig", "TransferConfig",
     "InferenceModel", "Error", "device_preset", "default_device", "default_io", "perfect_io",
-    "io_off", "device_check", "launch_count", "rows_amax_dev", "CONSTANT_STEP", "LINEAR_STEP",
+    "io_off", "device_check", "launch_count", "launch_floor_us", "rows_amax_dev", "CONSTANT_STEP", "LINEAR_STEP",
     "SOFT_BOUNDS", "EXP_STEP", "NM_NONE", "NM_ABS_MAX", "BM_NONE", "BM_ITERATIVE",
     "PULSE_STOCHASTIC", "PULSE_DETERMINISTIC", "MVM_FP32", "MVM_TF32", "MVM_TF32X3",
     "UnitCellTile", "UnitCellSettings", "UnitCellConfig", "UC_ROUND_ROBIN", "UC_ALL_TOGETHER",

@@ -103,6 +103,7 @@ SIGNATURES = {
     "xb_last_error": (C.c_char_p, []),
     "xb_device_check": (C.c_int, []),
     "xb_launch_count": (C.c_uint64, []),
+    "xb_launch_floor_us": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "xb_default_device": (None, [C.POINTER(DeviceParams)]),
     "xb_default_io": (None, [C.POINTER(IOParams)]),
     "xb_perfect_io": (None, [C.POINTER(IOParams)]),

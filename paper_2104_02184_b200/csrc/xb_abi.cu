@@ -511,6 +511,32 @@ int xb_abi_version(void) { return XB_ABI_VERSION; }
 const char *xb_last_error(void) { return g_err.c_str(); }
 uint64_t xb_launch_count(void) { return g_launches.load(); }
 
+int xb_launch_floor_us(int n, int reps, double *us_per_launch) {
+  return guard([&] {
+    if (n < 1 || reps < 1) raise("launch_floor: need n >= 1 and reps >= 1");
+    ensure_device();
+    cudaStream_t s;
+    cudaEvent_t e0, e1;
+    XB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    XB_CUDA(cudaEventCreate(&e0));
+    XB_CUDA(cudaEventCreate(&e1));
+    float best = 0.f;
+    for (int r = 0; r <= reps; ++r) { // round 0 warms up
+      XB_CUDA(cudaEventRecord(e0, s));
+      for (int k = 0; k < n; ++k) launch_empty(s);
+      XB_CUDA(cudaEventRecord(e1, s));
+      XB_CUDA(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      XB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      if (r > 0 && (r == 1 || ms < best)) best = ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(s);
+    *us_per_launch = 1e3 * (double)best / n;
+  });
+}
+
 int xb_device_check(void) {
   return guard([] { ensure_device(); });
 }

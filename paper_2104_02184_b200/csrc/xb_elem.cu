@@ -266,6 +266,13 @@ void launch_effective(float *weff, const float *const *w, const double *g, int K
   XB_CUDA(cudaGetLastError());
 }
 
+__global__ void empty_kernel() {}
+
+void launch_empty(cudaStream_t s) {
+  empty_kernel<<<1, 32, 0, s>>>();
+  XB_CUDA(cudaGetLastError());
+}
+
 void launch_nonfinite(const float *v, size_t n, int bit, int *flag, cudaStream_t s) {
   if (n == 0) return;
   const size_t blocks = std::min<size_t>((n / 4 + EW_THREADS - 1) / EW_THREADS + 1, 148 * 8);

@@ -183,6 +183,8 @@ Collective *comm_of(xb_comm *c);
 
 // ---- kernel launchers (xb_update.cu) ----
 void launch_rows_amax(const float *V, int B, int n, int ld, float *out, cudaStream_t s);
+// one empty kernel (xb_launch_floor_us; not counted as a library launch)
+void launch_empty(cudaStream_t s);
 // the x and d maxima of an update (rows of length nx and nd) in one launch
 void launch_rows_amax2(const float *X, int nx, float *xm, const float *D, int nd, float *dm, int B,
                        cudaStream_t s);

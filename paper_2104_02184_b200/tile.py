@@ -46,6 +46,14 @@ def launch_count() -> int:
     return int(_lib.xb_launch_count())
 
 
+def launch_floor_us(n: int = 64, reps: int = 5) -> float:
+    """Device microseconds per launch of n empty kernels issued back to back
+    from C (include/xbtile.h: xb_launch_floor_us)."""
+    out = C.c_double()
+    _check(_lib.xb_launch_floor_us(int(n), int(reps), C.byref(out)))
+    return out.value
+
+
 def device_check() -> None:
     _check(_lib.xb_device_check())
 

@@ -107,11 +107,10 @@ def hbm_roofline(bytes_, ms, what):
 
 
 def launch_floor_us(stream, iters=200):
-    """Device time of the smallest kernel this library launches (a 1-element
-    row max): the per-launch floor a latency-bound step cannot go under."""
-    v = torch.zeros(1, 1, device="cuda")
-    out = torch.zeros(1, device="cuda")
-    return ev_time(lambda: xb.rows_amax_dev(v, out, stream.cuda_stream), iters, stream) * 1e3
+    """Device time per launch of empty kernels issued back to back from C
+    (xb_launch_floor_us): the per-launch floor a latency-bound step cannot go
+    under (a floor measured through Python would include the interpreter)."""
+    return xb.launch_floor_us(64, 5)
 
 
 def latency_roofline(ms, launches, floor_us):
@@ -119,8 +118,8 @@ def latency_roofline(ms, launches, floor_us):
     floor = launches * floor_us * 1e-3
     return {"bound": "launch-latency", "achieved": ms, "peak": floor, "unit": "ms/step",
             "frac": floor / ms, "launches_per_step": launches,
-            "basis": f"{launches} dependent launches x {floor_us:.2f} us (measured minimal "
-                     "kernel of this library, back to back)"}
+            "basis": f"{launches} dependent launches x {floor_us:.2f} us (measured: empty "
+                     "kernels issued back to back from C)"}
 
 
 def ref_oracle():
