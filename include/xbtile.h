@@ -29,8 +29,10 @@
  *
  * Errors: every function returns 0 on success, non-zero on error; the
  * thread-local message (naming the field, like xbarsim::Error) is returned by
- * xb_last_error().  CUDA errors are reported the same way.  There is no CPU
- * fallback: without a usable sm_100 device every compute entry fails.
+ * xb_last_error().  CUDA errors are reported the same way.  A failed call
+ * leaves the tile's state (weights, noise counters) as it was; the contents
+ * of its output buffers are unspecified.  There is no CPU fallback: without a
+ * usable sm_100 device every compute entry fails.
  *
  * Host-buffer entries (no suffix) are synchronous: inputs are borrowed for
  * the duration of the call, outputs are written before return.  *_dev

@@ -916,9 +916,20 @@ static void forward_host(xb_tile *h, const float *X, int B, float *Y, const xb_i
   const size_t nx = (size_t)B * t.C, ny = (size_t)B * t.R;
   float *pin = io_stage(t, nx + ny);
   h2d(t, dX, X, nx, pin);
-  if (!checked) check_finite_dev(t, {{dX, nx, "forward"}});
+  // large inputs: the finiteness scan is enqueued ahead of the forward and its
+  // flag read back with the outputs -- one host round trip per call, not two;
+  // a non-finite input rolls the noise counter back and raises (the output
+  // buffer is then unspecified, as for every failed call)
+  if (!checked) launch_finite_dev(t, {{dX, nx, "forward"}});
+  const uint64_t seq = t.seq_fwd;
   forward_device(t, dX, B, dY, io);
+  if (!checked)
+    XB_CUDA(cudaMemcpyAsync(t.chk_host, t.chk_dev, sizeof(int), cudaMemcpyDeviceToHost, t.stream));
   d2h_sync(t, Y, dY, ny, pin ? pin + nx : nullptr);
+  if (!checked && (*t.chk_host & 1)) {
+    t.seq_fwd = seq;
+    raise("forward: non-finite entry");
+  }
 }
 
 int xb_tile_forward(xb_tile *h, const float *X, int B, float *Y) {
