@@ -51,3 +51,14 @@ def test_bench_two_rank_code_path():
     assert d["e2e"]["h2d_bytes_per_step"] == 2 * (256 * 16384 * 4 * 2 + 256 * 8192 * 4)
     assert d["weak_scaling"]["rows_per_gpu"] == 4096 and d["weak_scaling"]["value"] > 0
     assert d["inference_pass"]["drift_to_s"] > 0
+
+
+@pytest.mark.gpu
+def test_launch_floor_measurement():
+    """xb_launch_floor_us (the latency floor of cfg1/cfg2's rooflines): empty
+    kernels back to back from C cost a few microseconds each on the device."""
+    import paper_2104_02184_b200 as xb
+    us = xb.launch_floor_us(32, 3)
+    assert 0.3 < us < 50.0, us
+    with pytest.raises(xb.Error, match="launch_floor"):
+        xb.launch_floor_us(0, 1)
