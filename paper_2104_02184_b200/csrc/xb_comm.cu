@@ -24,9 +24,11 @@
 //                      one device: the test harness of the sharded path).  A
 //                      reduction is a host rendezvous plus stream-ordered
 //                      device work: every rank waits (cudaStreamWaitEvent) for
-//                      all ranks' inputs, reduces them in rank order into its
-//                      own scratch, and copies back after every rank has read.
-//                      No kernel ever spins on another.
+//                      all ranks' inputs, reduces ITS slice of the elements
+//                      over every member's buffer in rank order and writes the
+//                      result into every member's buffer over peer memory
+//                      (reduce-scatter + all-gather in one kernel), then waits
+//                      for every rank's slice.  No kernel ever spins on another.
 #include <dlfcn.h>
 
 #include <condition_variable>
@@ -109,14 +111,21 @@ struct NcclCollective : Collective {
 // ------------------------------------------------------------------ loopback
 enum class Op { max_i32, max_f32, sum_f32 };
 
-// out[i] = reduce over ranks r = 0..P-1 (rank order) of in[r][i]
+// Elements [lo, hi) -- this rank's slice -- reduced over every member's
+// buffer in rank order and written back into every member's buffer: a
+// reduce-scatter and an all-gather in one pass over peer memory.  Each rank
+// touches only its own slice of every buffer, so the P kernels never
+// conflict; every element is read and written once per member.
 template <class T, bool MAX>
-__global__ void reduce_ranks_kernel(const T *const *in, int P, size_t n, T *out) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+__global__ void reduce_slice_kernel(T *const *bufs, int P, size_t lo, size_t hi) {
+  for (size_t i = lo + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < hi;
        i += (size_t)gridDim.x * blockDim.x) {
-    T v = in[0][i];
-    for (int r = 1; r < P; ++r) v = MAX ? (in[r][i] > v ? in[r][i] : v) : v + in[r][i];
-    out[i] = v;
+    T v = bufs[0][i];
+    for (int q = 1; q < P; ++q) {
+      const T x = bufs[q][i];
+      v = MAX ? (x > v ? x : v) : v + x;
+    }
+    for (int q = 0; q < P; ++q) bufs[q][i] = v;
   }
 }
 
@@ -154,7 +163,7 @@ struct LocalGroup {
 struct LocalCollective : Collective {
   std::shared_ptr<LocalGroup> g;
   int r = 0;
-  Scratch tmp, ptrs;
+  Scratch ptrs;
   // members on other devices: each rank's reduction kernel reads every
   // member's buffer directly, so peer access is enabled both ways when a
   // member binds (before any collective: a failure here cannot strand peers
@@ -188,42 +197,43 @@ struct LocalCollective : Collective {
     LocalGroup &G = *g;
     XB_CUDA(cudaEventRecord(G.ready[r], s));
     G.barrier([&] { G.bufs[r] = buf; });
-    // every rank's input is enqueued: wait for them in stream order and reduce
+    // every rank's input is enqueued: wait for them in stream order, then
+    // reduce this rank's slice into every buffer
     for (int q = 0; q < G.P; ++q)
       if (q != r) XB_CUDA(cudaStreamWaitEvent(s, G.ready[q], 0));
-    void **dptr = (void **)ptrs.get(sizeof(void *) * G.P);
-    XB_CUDA(cudaMemcpyAsync(dptr, G.bufs.data(), sizeof(void *) * G.P, cudaMemcpyHostToDevice, s));
-    void *out = tmp.get(n * elem);
-    const int blocks = (int)std::min<size_t>((n + 255) / 256, 1024);
-    switch (op) {
-    case Op::max_i32:
-      reduce_ranks_kernel<int, true><<<blocks, 256, 0, s>>>((const int *const *)dptr, G.P, n, (int *)out);
-      break;
-    case Op::max_f32:
-      reduce_ranks_kernel<float, true><<<blocks, 256, 0, s>>>((const float *const *)dptr, G.P, n, (float *)out);
-      break;
-    case Op::sum_f32:
-      reduce_ranks_kernel<float, false><<<blocks, 256, 0, s>>>((const float *const *)dptr, G.P, n, (float *)out);
-      break;
+    const size_t lo = n * (size_t)r / (size_t)G.P, hi = n * (size_t)(r + 1) / (size_t)G.P;
+    if (hi > lo) {
+      void **dptr = (void **)ptrs.get(sizeof(void *) * G.P);
+      XB_CUDA(cudaMemcpyAsync(dptr, G.bufs.data(), sizeof(void *) * G.P, cudaMemcpyHostToDevice,
+                              s));
+      const int blocks = (int)std::min<size_t>((hi - lo + 255) / 256, 1024);
+      switch (op) {
+      case Op::max_i32:
+        reduce_slice_kernel<int, true><<<blocks, 256, 0, s>>>((int *const *)dptr, G.P, lo, hi);
+        break;
+      case Op::max_f32:
+        reduce_slice_kernel<float, true><<<blocks, 256, 0, s>>>((float *const *)dptr, G.P, lo, hi);
+        break;
+      case Op::sum_f32:
+        reduce_slice_kernel<float, false><<<blocks, 256, 0, s>>>((float *const *)dptr, G.P, lo, hi);
+        break;
+      }
+      count_launch();
+      XB_CUDA(cudaGetLastError());
     }
-    count_launch();
-    XB_CUDA(cudaGetLastError());
+    (void)elem;
     XB_CUDA(cudaEventRecord(G.done[r], s));
-    G.barrier([] {}); // every rank has enqueued its reads of every input
+    G.barrier([] {}); // every rank has enqueued its slice
     for (int q = 0; q < G.P; ++q)
       if (q != r) XB_CUDA(cudaStreamWaitEvent(s, G.done[q], 0));
-    XB_CUDA(cudaMemcpyAsync(buf, out, n * elem, cudaMemcpyDeviceToDevice, s));
-    // the pointer table of the next call must not be overwritten before the
+    // (the pointer table of the next call must not be overwritten before the
     // kernel above has read it: the stream order covers this rank; the
-    // barrier at the next call's start covers the others
+    // barrier at the next call's start covers the others)
   }
   void allreduce_max_i32(int *b, size_t n, cudaStream_t s) override { reduce(b, n, 4, Op::max_i32, s); }
   void allreduce_max_f32(float *b, size_t n, cudaStream_t s) override { reduce(b, n, 4, Op::max_f32, s); }
   void allreduce_sum_f32(float *b, size_t n, cudaStream_t s) override { reduce(b, n, 4, Op::sum_f32, s); }
-  ~LocalCollective() override {
-    tmp.release();
-    ptrs.release();
-  }
+  ~LocalCollective() override { ptrs.release(); }
 };
 
 } // namespace
