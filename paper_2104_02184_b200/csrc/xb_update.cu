@@ -131,29 +131,8 @@ __device__ __forceinline__ void philox10_rk(uint32_t &c0, uint32_t &c1, uint32_t
 
 // ============================================================== K4: trains
 // Counter of a train draw: (slot group g, global line, seq lo, seq hi ^ side),
-// key = the tile's "update" stream.  Each Philox call gives 4 slots.
-__device__ __forceinline__ uint32_t train_word(float v, double p, int bl, const RoundKeys &rk,
-                                               uint32_t line, uint64_t seq, uint32_t side) {
-  uint32_t bits = 0;
-  if (p > 0.0) {
-    if (p >= 1.0) {
-      bits = (bl >= 32) ? 0x7fffffffu : ((1u << bl) - 1u); // bernoulli(p>=1) == 1, no draw
-    } else {
-      const uint32_t thr = (uint32_t)(p * 4294967296.0); // P(u < thr) = thr / 2^32
-      const uint32_t c2 = (uint32_t)seq, c3 = (uint32_t)(seq >> 32) ^ side;
-      for (int g = 0; g * 4 < bl; ++g) {
-        uint32_t a0 = (uint32_t)g, a1 = line, a2 = c2, a3 = c3;
-        philox10_rk(a0, a1, a2, a3, rk);
-        const int t = g * 4;
-        bits |= (uint32_t)(a0 < thr) << t;
-        if (t + 1 < bl) bits |= (uint32_t)(a1 < thr) << (t + 1);
-        if (t + 2 < bl) bits |= (uint32_t)(a2 < thr) << (t + 2);
-        if (t + 3 < bl) bits |= (uint32_t)(a3 < thr) << (t + 3);
-      }
-    }
-  }
-  return bits | (v < 0.f ? 0x80000000u : 0u);
-}
+// key = the tile's "update" stream.  Each Philox call gives 4 slots
+// (trains_kernel).
 
 // translate, proj/src/pulsed.cpp:25-66, in fp64 on the fp32 inputs: the
 // per-sample part (BL management, amplitude, x/d rebalancing)
@@ -213,24 +192,56 @@ __global__ void __launch_bounds__(256) trains_kernel(
   __syncthreads();
   const int line = l0 + lane;
   const float *V = is_x ? X : D;
+  // 4 words per thread (samples warp + 8 it), their Philox chains interleaved
+  // call by call -- train_word's draws, in one loop, so the four dependent
+  // chains overlap instead of running one word after the other
+  const uint32_t lid = is_x ? (uint32_t)line : (uint32_t)(row0 + line);
+  const uint32_t side = is_x ? 0u : 0x80000000u;
+  uint32_t word[4], thr[4], c2[4], c3[4];
+  int bl4[4], ng[4], gmax = 0;
 #pragma unroll
-  for (int it = 0; it < 4; ++it) { // 4 independent words per thread: ILP for the Philox chains
+  for (int it = 0; it < 4; ++it) {
     const int s = warp + 8 * it;
     const int b = b0 + s;
-    uint32_t word = 0;
+    word[it] = thr[it] = c2[it] = c3[it] = 0u;
+    bl4[it] = ng[it] = 0;
     if (b < B && line < nl) {
       const Plan pl = plan[s];
       const float v = V[(size_t)b * nl + line];
       if (!pl.skip) {
         double p = pl.amp * fabs((double)v) * (is_x ? pl.x_scale : pl.d_scale);
         p = (p < 1.0) ? p : 1.0;
-        word = is_x ? train_word(v, p, pl.bl, rk, (uint32_t)line, seq0 + b, 0u)
-                    : train_word(v, p, pl.bl, rk, (uint32_t)(row0 + line), seq0 + b,
-                                 0x80000000u);
+        word[it] = v < 0.f ? 0x80000000u : 0u; // sign
+        if (p >= 1.0) { // bernoulli(p >= 1) == 1, no draw
+          word[it] |= (pl.bl >= 32) ? 0x7fffffffu : ((1u << pl.bl) - 1u);
+        } else if (p > 0.0) {
+          thr[it] = (uint32_t)(p * 4294967296.0); // P(u < thr) = thr / 2^32
+          const uint64_t seq = seq0 + (uint64_t)b;
+          c2[it] = (uint32_t)seq;
+          c3[it] = (uint32_t)(seq >> 32) ^ side;
+          bl4[it] = pl.bl;
+          ng[it] = (pl.bl + 3) >> 2;
+          gmax = max(gmax, ng[it]);
+        }
       }
     }
-    tile[lane][s] = word;
   }
+  for (int g = 0; g < gmax; ++g) {
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      if (g < ng[it]) {
+        uint32_t a0 = (uint32_t)g, a1 = lid, a2 = c2[it], a3 = c3[it];
+        philox10_rk(a0, a1, a2, a3, rk);
+        uint32_t m = (uint32_t)(a0 < thr[it]) | ((uint32_t)(a1 < thr[it]) << 1) |
+                     ((uint32_t)(a2 < thr[it]) << 2) | ((uint32_t)(a3 < thr[it]) << 3);
+        const int rem = bl4[it] - 4 * g; // slots 4g .. 4g + 3 that exist
+        if (rem < 4) m &= (1u << rem) - 1u;
+        word[it] |= m << (4 * g);
+      }
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < 4; ++it) tile[lane][warp + 8 * it] = word[it];
   __syncthreads();
   if (is_x) { // quad layout (xq_index): thread = (column r, quad q), one uint4 store
     const int r = threadIdx.x & 31, q = threadIdx.x >> 5, ln = l0 + r, b = b0 + 4 * q;
