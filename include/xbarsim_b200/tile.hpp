@@ -322,12 +322,26 @@ inline void check_input(std::span<const double> v, int expected, const char *wha
   for (double x : v)
     if (!std::isfinite(x)) throw Error(std::string(what) + ": non-finite entry");
 }
-// the GPU computes on fp32 inputs: a finite double outside the fp32 range
-// would turn into Inf on the device (check_input already passed it)
-inline void check_f32_range(std::span<const double> v, const char *what) {
-  for (double x : v)
-    if (std::fabs(x) > static_cast<double>(std::numeric_limits<float>::max()))
-      throw Error(std::string(what) + ": entry exceeds the fp32 range of the B200 tile");
+// One pass over an update vector: check_input's length and finiteness (raised
+// at once, in the reference's order), and whether it is all zero or leaves
+// the fp32 range (raised by the caller after the reference's earlier checks).
+struct UpdateScan {
+  bool zero = true, beyond_f32 = false;
+};
+inline UpdateScan scan_update_input(std::span<const double> v, int expected, const char *what) {
+  if (static_cast<int>(v.size()) != expected)
+    throw Error(std::string(what) + ": length " + std::to_string(v.size()) + ", expected " +
+                std::to_string(expected));
+  constexpr double fmax = static_cast<double>(std::numeric_limits<float>::max());
+  bool bad = false, zero = true, big = false;
+  for (double x : v) {
+    const double a = std::fabs(x);
+    bad |= !(a <= std::numeric_limits<double>::max()); // Inf or NaN
+    zero &= x == 0.0;
+    big |= a > fmax;
+  }
+  if (bad) throw Error(std::string(what) + ": non-finite entry");
+  return {zero, big};
 }
 } // namespace detail
 
@@ -418,18 +432,19 @@ public:
   }
   // proj/src/tile.cpp:97-101 via the batching bridge
   void update(std::span<const double> x, std::span<const double> d, double lr) override {
-    detail::check_input(x, d_in_, "update(x)");
-    detail::check_input(d, d_out_, "update(d)");
-    bool xz = true, dz = true;
-    for (double v : x) xz = xz && v == 0.0;
-    for (double v : d) dz = dz && v == 0.0;
-    if (lr == 0.0 || xz || dz) return; // proj/src/pulsed.cpp:122-124, no draw
+    // (one scan per vector for every check below, then the fp32 append: the
+    // per-sample update is host-bound)
+    const detail::UpdateScan sx = detail::scan_update_input(x, d_in_, "update(x)");
+    const detail::UpdateScan sd = detail::scan_update_input(d, d_out_, "update(d)");
+    if (lr == 0.0 || sx.zero || sd.zero) return; // proj/src/pulsed.cpp:122-124, no draw
     if (!(lr > 0.0)) throw Error("translate: learning rate must be > 0");
     // the queue stores fp32 x/d (the device arithmetic); a finite double
     // beyond the fp32 range would become Inf there, so it is rejected here,
     // at the call, like check_input's non-finite entries
-    detail::check_f32_range(x, "update(x)");
-    detail::check_f32_range(d, "update(d)");
+    if (sx.beyond_f32)
+      throw Error("update(x): entry exceeds the fp32 range of the B200 tile");
+    if (sd.beyond_f32)
+      throw Error("update(d): entry exceeds the fp32 range of the B200 tile");
     qx_.insert(qx_.end(), x.begin(), x.end());
     qd_.insert(qd_.end(), d.begin(), d.end());
     qlr_.push_back(lr); // double, as the reference's update(..., double lr)
