@@ -289,13 +289,18 @@ struct Finite {
   size_t n;
   const char *what;
 };
-// launch half: the flag bits land in t.chk_dev (stream order), nothing waits
-static void launch_finite_dev(Tile &t, std::initializer_list<Finite> arrays) {
+// the input-check flag word, cleared in stream order
+static void clear_chk(Tile &t) {
   if (!t.chk_dev) {
     XB_CUDA(cudaMalloc(&t.chk_dev, sizeof(int)));
     XB_CUDA(cudaMallocHost(&t.chk_host, sizeof(int)));
   }
   XB_CUDA(cudaMemsetAsync(t.chk_dev, 0, sizeof(int), t.stream));
+}
+
+// launch half: the flag bits land in t.chk_dev (stream order), nothing waits
+static void launch_finite_dev(Tile &t, std::initializer_list<Finite> arrays) {
+  clear_chk(t);
   int bit = 1;
   for (const Finite &a : arrays) {
     launch_nonfinite(a.v, a.n, bit, t.chk_dev, t.stream);
@@ -443,7 +448,9 @@ static void update_device(Tile &t, const float *dX, const float *dD, int B, cons
     PhaseTimer pt(t, XB_TIMER_TRAINS);
     const float *dm = dAmaxD;
     if (!dm) {
-      launch_rows_amax2(dX, t.C, u.xm, dD, t.R, u.dm, B, t.stream);
+      // (abort_flag set: the host-buffer update's finiteness test rides along)
+      launch_rows_amax2(dX, t.C, u.xm, dD, t.R, u.dm, B, t.stream,
+                        t.abort_flag ? t.chk_dev : nullptr);
       // row shard: translate needs max|d| over the whole tile (pulsed.cpp:34-51)
       if (t.comm) t.comm->allreduce_max_f32(u.dm, (size_t)B, t.stream);
       dm = u.dm;
@@ -1106,16 +1113,18 @@ int xb_tile_update(xb_tile *h, const float *X, const float *D, int B, const doub
     }
     const std::initializer_list<Finite> in = {{dX, (size_t)B * t.C, "update(x)"},
                                               {dD, (size_t)B * t.R, "update(d)"}};
-    launch_finite_dev(t, in);
     try {
       check_lr_host(X, D, B, t.C, t.R, lr, t.learning_rate);
     } catch (...) { // check_input (tile.cpp:98-99) comes before translate's lr check
-      raise_if_nonfinite(t, in);
+      check_finite_dev(t, in);
       throw;
     }
-    // no host round trip before the launch: the pulse kernel reads the
-    // finiteness flag itself and leaves the tile untouched if it is set;
-    // the host counters are rolled back and the error raised after the sync
+    // no host round trip before the launch: the update's x/d maxima kernel
+    // also runs the finiteness test (bits 1, 2 of chk_dev, the order of
+    // `in`), the pulse kernel reads the flag itself and leaves the tile
+    // untouched if it is set; the host counters are rolled back and the
+    // error raised after the sync
+    clear_chk(t);
     const uint64_t seq_upd = t.seq_upd;
     const uint32_t calls = t.upd_calls;
     t.abort_flag = t.chk_dev;

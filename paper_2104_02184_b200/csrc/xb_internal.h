@@ -185,9 +185,10 @@ Collective *comm_of(xb_comm *c);
 void launch_rows_amax(const float *V, int B, int n, int ld, float *out, cudaStream_t s);
 // one empty kernel (xb_launch_floor_us; not counted as a library launch)
 void launch_empty(cudaStream_t s);
-// the x and d maxima of an update (rows of length nx and nd) in one launch
+// the x and d maxima of an update (rows of length nx and nd) in one launch;
+// flag != null: also check_input's finiteness test (bits 1 = x, 2 = d)
 void launch_rows_amax2(const float *X, int nx, float *xm, const float *D, int nd, float *dm, int B,
-                       cudaStream_t s);
+                       cudaStream_t s, int *flag = nullptr);
 // per-sample translate + Bernoulli trains; writes packed words and bl[B]
 void launch_trains(const Tile &t, const float *X, const float *D, int B, const double *lr_dev,
                    double lr_scalar, const float *xm, const float *dm, uint64_t seq0,

@@ -30,19 +30,26 @@ namespace xb {
 // one dependent load per iteration
 // blocks [0, nb1) take rows of V (length n, stride ld) into out; blocks
 // [nb1, gridDim.x) rows of V2 (n2, ld2) into out2 -- the x and d maxima of an
-// update in one launch
+// update in one launch.  flag != null: check_input's finiteness test in the
+// same pass (OR-ing bit1 / bit2 into *flag for a non-finite entry of V / V2):
+// z sums v * 0, which stays 0 for finite entries and turns NaN otherwise.
 __global__ void __launch_bounds__(256) rows_amax_kernel(const float *__restrict__ V, int n, int ld,
                                                         float *__restrict__ out, int nb1,
                                                         const float *__restrict__ V2, int n2,
-                                                        int ld2, float *__restrict__ out2) {
+                                                        int ld2, float *__restrict__ out2,
+                                                        int *__restrict__ flag, int bit1,
+                                                        int bit2) {
   int b = blockIdx.x;
+  int bit = bit1;
   if (b >= nb1) {
     b -= nb1;
     V = V2;
     n = n2;
     ld = ld2;
     out = out2;
+    bit = bit2;
   }
+  float z = 0.f;
   const float *row = V + (size_t)b * ld;
   float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
   int head = 0;
@@ -57,14 +64,25 @@ __global__ void __launch_bounds__(256) rows_amax_kernel(const float *__restrict_
       m1 = fmaxf(m1, fmaxf(fmaxf(fabsf(c.x), fabsf(c.y)), fmaxf(fabsf(c.z), fabsf(c.w))));
       m2 = fmaxf(m2, fmaxf(fmaxf(fabsf(e.x), fabsf(e.y)), fmaxf(fabsf(e.z), fabsf(e.w))));
       m3 = fmaxf(m3, fmaxf(fmaxf(fabsf(g.x), fabsf(g.y)), fmaxf(fabsf(g.z), fabsf(g.w))));
+      if (flag) {
+        z = fmaf(a.x, 0.f, fmaf(a.y, 0.f, fmaf(a.z, 0.f, fmaf(a.w, 0.f, z))));
+        z = fmaf(c.x, 0.f, fmaf(c.y, 0.f, fmaf(c.z, 0.f, fmaf(c.w, 0.f, z))));
+        z = fmaf(e.x, 0.f, fmaf(e.y, 0.f, fmaf(e.z, 0.f, fmaf(e.w, 0.f, z))));
+        z = fmaf(g.x, 0.f, fmaf(g.y, 0.f, fmaf(g.z, 0.f, fmaf(g.w, 0.f, z))));
+      }
     }
     for (; j < n4; j += 256) {
       const float4 a = __ldg(r4 + j);
       m0 = fmaxf(m0, fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(a.z), fabsf(a.w))));
+      if (flag) z = fmaf(a.x, 0.f, fmaf(a.y, 0.f, fmaf(a.z, 0.f, fmaf(a.w, 0.f, z))));
     }
     head = n4 << 2;
   }
-  for (int j = head + threadIdx.x; j < n; j += 256) m1 = fmaxf(m1, fabsf(row[j]));
+  for (int j = head + threadIdx.x; j < n; j += 256) {
+    m1 = fmaxf(m1, fabsf(row[j]));
+    if (flag) z = fmaf(row[j], 0.f, z);
+  }
+  if (flag && __syncthreads_or(!(z == 0.f)) && threadIdx.x == 0) atomicOr(flag, bit);
   float m = warp_max(fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)));
   __shared__ float red[8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -78,15 +96,15 @@ __global__ void __launch_bounds__(256) rows_amax_kernel(const float *__restrict_
 
 void launch_rows_amax(const float *V, int B, int n, int ld, float *out, cudaStream_t s) {
   if (B <= 0) return;
-  rows_amax_kernel<<<B, 256, 0, s>>>(V, n, ld, out, B, nullptr, 0, 0, nullptr);
+  rows_amax_kernel<<<B, 256, 0, s>>>(V, n, ld, out, B, nullptr, 0, 0, nullptr, nullptr, 0, 0);
   count_launch();
   XB_CUDA(cudaGetLastError());
 }
 
 void launch_rows_amax2(const float *X, int nx, float *xm, const float *D, int nd, float *dm, int B,
-                       cudaStream_t s) {
+                       cudaStream_t s, int *flag) {
   if (B <= 0) return;
-  rows_amax_kernel<<<2 * B, 256, 0, s>>>(X, nx, nx, xm, B, D, nd, nd, dm);
+  rows_amax_kernel<<<2 * B, 256, 0, s>>>(X, nx, nx, xm, B, D, nd, nd, dm, flag, 1, 2);
   count_launch();
   XB_CUDA(cudaGetLastError());
 }
