@@ -208,3 +208,32 @@ def test_softbounds_update_ns_shape_row_slice():
     wg, wo = t.get_weights()[:rows], o.get_weights()
     assert close(wg, wo, 1e-5, 0.1).all(), f"max |dw| {np.abs(wg - wo).max():.3e}"
     assert np.abs(wg - W0[:rows]).max() > 0
+
+
+@pytest.mark.parametrize("prec", [xb.MVM_TF32, xb.MVM_TF32X3])
+def test_bm_loop_two_subtile_ctas(monkeypatch, prec):
+    """Tiles of >= 8192 rows run the contraction with two 128-row sub-tiles
+    per CTA (the cfg5 shape class): the in-kernel re-issue loop there equals
+    the host-driven passes bit for bit too (8192 x 1024, B = 256, noise on,
+    weights that saturate the ADC bound)."""
+    R, C, Bn = 8192, 1024, 256
+    r = np.random.default_rng(31)
+    W = r.uniform(-0.6, 0.6, (R, C)).astype(np.float32)
+    X = r.uniform(-1, 1, (Bn, C)).astype(np.float32)
+    io = xb.default_io()
+    io.sigma_w = 0.01
+    io.bound_management = xb.BM_ITERATIVE
+    dev = xb.default_device()
+    dev.w_max, dev.w_min = 1.0, -1.0
+    cfg = xb.TileSettings(device=dev, forward_io=io, backward_io=io, mvm_precision=prec)
+    out = []
+    for host in ("0", "1"):
+        monkeypatch.setenv("XB_BM_HOST_PASSES", host)
+        t = xb.AnalogTile(R, C, cfg, 23)
+        t.set_weights(W)
+        out.append(t.forward(X))
+    np.testing.assert_array_equal(out[0], out[1])
+    # the workload re-issues: some sample has outputs beyond alpha * bound,
+    # which only a level m >= 1 (scale alpha 2^m) can produce
+    alpha = np.abs(X).max(axis=1).astype(np.float64)
+    assert (np.abs(out[0]) > io.output_bound * alpha[:, None] * (1 + 1e-6)).any()
