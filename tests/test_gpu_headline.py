@@ -237,3 +237,26 @@ def test_bm_loop_two_subtile_ctas(monkeypatch, prec):
     # which only a level m >= 1 (scale alpha 2^m) can produce
     alpha = np.abs(X).max(axis=1).astype(np.float64)
     assert (np.abs(out[0]) > io.output_bound * alpha[:, None] * (1 + 1e-6)).any()
+
+
+@pytest.mark.parametrize("prec", [xb.MVM_TF32, xb.MVM_TF32X3])
+def test_bm_loop_backward_equals_host_passes(monkeypatch, headline_inputs, prec):
+    """Bound management on the backward (W^T as the MN-major operand): the
+    in-kernel re-issue loop equals the host-driven passes bit for bit, noise
+    on, at the headline shape."""
+    W, X = headline_inputs
+    io = xb.default_io()
+    io.sigma_w = 0.01
+    io.bound_management = xb.BM_ITERATIVE
+    dev = xb.default_device()
+    cfg = xb.TileSettings(device=dev, forward_io=io, backward_io=io, mvm_precision=prec)
+    D = np.random.default_rng(77).uniform(-1, 1, (B, N)).astype(np.float32)
+    out = []
+    for host in ("0", "1"):
+        monkeypatch.setenv("XB_BM_HOST_PASSES", host)
+        t = xb.AnalogTile(N, N, cfg, 29)
+        t.set_weights(W)
+        out.append(t.backward(D))
+    np.testing.assert_array_equal(out[0], out[1])
+    alpha = np.abs(D).max(axis=1).astype(np.float64)
+    assert (np.abs(out[0]) > io.output_bound * alpha[:, None] * (1 + 1e-6)).any()
