@@ -122,8 +122,8 @@ def test_forward_converters_headline_shape(headline_inputs, prec, lsb_frac, deci
     assert (off[ok] > 0.5).mean() <= lsb_frac, f"{(off[ok] > 0.5).mean():.4f} off-grid"
 
 
-@pytest.mark.parametrize("batch,prec", [(256, xb.MVM_TF32), (300, xb.MVM_TF32),
-                                        (300, xb.MVM_TF32X3)])
+@pytest.mark.parametrize("batch,prec", [(256, xb.MVM_TF32), (100, xb.MVM_TF32),
+                                        (300, xb.MVM_TF32), (300, xb.MVM_TF32X3)])
 def test_bm_inkernel_loop_equals_host_passes(monkeypatch, headline_inputs, batch, prec):
     """The in-kernel re-issue loop (one launch, grid barriers; at TF32 its
     first re-issue streams the m = 1 slab the idle warps prepared during pass
@@ -131,7 +131,7 @@ def test_bm_inkernel_loop_equals_host_passes(monkeypatch, headline_inputs, batch
     re-issue prep kernel) are bit-identical, with output and weight noise on,
     for one and two N slabs."""
     W, X = headline_inputs
-    Xb = np.concatenate([X, X[: batch - B] * 0.5]) if batch > B else X
+    Xb = np.concatenate([X, X[: batch - B] * 0.5]) if batch > B else X[:batch]
     io = xb.default_io()
     io.sigma_w = 0.01
     io.bound_management = xb.BM_ITERATIVE
